@@ -1,0 +1,120 @@
+"""ctypes binding of libpsk.so — the C ABI declared in include/psk.h.
+
+The product path has no fallback: if the library is missing or fails to
+load, every entry point raises. Errors from the library are raised as
+PskError carrying psk_last_error().
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libpsk.so"
+
+PSK_OK = 0
+PSK_EINVAL = -1
+PSK_ECUDA = -2
+PSK_ECAPACITY = -3
+PSK_ECAPACITY_NEED = -4
+PSK_EUNDERFLOW = -5
+PSK_ENOMEM = -6
+
+
+class PskError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"psk error {code}: {msg}")
+        self.code = code
+
+
+class PoolResult(C.Structure):
+    _fields_ = [
+        ("status", C.c_int64),
+        ("count", C.c_int64),
+        ("first_block_id", C.c_int64),
+        ("evicted", C.c_int64),
+        ("used_blocks", C.c_int64),
+        ("matched_tokens", C.c_int64),
+        ("lookup_tokens", C.c_int64),
+        ("eviction_count", C.c_int64),
+        ("next_block_id", C.c_int64),
+        ("err_index", C.c_int64),
+        ("err_block_id", C.c_int64),
+        ("reserved", C.c_int64 * 5),
+    ]
+
+
+_P = C.c_void_p
+_I32 = C.c_int32
+_I64 = C.c_int64
+_U64 = C.c_uint64
+_F = C.c_float
+
+# name -> argtypes (restype is int unless listed in _RESTYPE)
+_SIGS: dict[str, list] = {
+    "psk_abi_version": [],
+    "psk_last_error": [],
+    "psk_sm_count": [C.c_int, C.POINTER(_I32)],
+    "psk_init_normal_bf16": [_P, _I64, _U64, _F, _P],
+    "psk_fill_bf16": [_P, _I64, _F, _P],
+    # K7 pool
+    "psk_pool_create": [C.POINTER(_P), _I64, _I32, _I64, _I64, C.c_int],
+    "psk_pool_destroy": [_P],
+    "psk_pool_reserve": [_P, _I64],
+    "psk_pool_records": [_P],
+    "psk_pool_host_buffers": [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
+                              C.POINTER(_P), C.POINTER(_P)],
+    "psk_pool_device_out_slots": [_P, C.POINTER(_P)],
+    "psk_pool_lookup": [_P, _I32, _P, _I64, _I64, _I32, _P],
+    "psk_pool_insert": [_P, _I32, _P, _I64, _I64, _P],
+    "psk_pool_evict_until": [_P, _I64, _P],
+    "psk_pool_pin": [_P, _I64, _I64, _P],
+    "psk_pool_release": [_P, _I64, _P],
+    "psk_pool_footprint": [_P, _I32, C.POINTER(_I64), C.POINTER(_I64)],
+    "psk_pool_snapshot": [_P, _P, _P, _P, _P, _P, _P, _P],
+    "psk_pool_read_record": [_P, _I32, _P, _P],
+}
+_RESTYPE = {
+    "psk_last_error": C.c_char_p,
+    "psk_pool_records": _I64,
+}
+
+_lib: C.CDLL | None = None
+
+
+def load() -> C.CDLL:
+    """Load libpsk.so (built in-tree by paper_2602_12029_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise PskError(PSK_EINVAL, f"{LIB_PATH} missing: run `python -m paper_2602_12029_b200.build` "
+                                   "(the CUDA extension is required; there is no CPU fallback)")
+    lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_LOCAL | os.RTLD_NOW)
+    for name, args in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPE.get(name, C.c_int)
+    _lib = lib
+    return lib
+
+
+def declared_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def last_error() -> str:
+    msg = load().psk_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(code: int) -> int:
+    if code != PSK_OK:
+        raise PskError(code, last_error())
+    return code
+
+
+def call(name: str, *args) -> int:
+    """Call an int-returning entry point and raise on failure."""
+    return check(getattr(load(), name)(*args))

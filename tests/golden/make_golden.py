@@ -1,0 +1,265 @@
+"""Generate golden fixtures by running the REFERENCE implementation.
+
+Run in the build container only (it imports the read-only reference from
+/root/reference/pkg/src); the fixtures it writes are committed and are all
+the GPU box ever sees.
+
+    python tests/golden/make_golden.py
+
+pool_streams.json.gz — seeded op streams (lookup / insert / pin / release /
+  evict_until, incl. capacity failures and release underflow) replayed
+  through prefillsim.kvstore.BlockPool, with the observable outcome of every
+  op and a digest of the full block state after every op.
+router_traces.json — prefillsim.router.Router decisions over seeded request
+  streams in both serving modes.
+workload.json — splitmix64 vectors, mix_seed, synth_tokens and a generated
+  session list (prefillsim.workload).
+"""
+
+from __future__ import annotations
+
+import gzip
+import hashlib
+import json
+import random
+import sys
+from pathlib import Path
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent
+
+
+def state_digest(blocks) -> str:
+    """Canonical digest of a pool's block records (shared with the tests)."""
+    rows = sorted(
+        (b.block_id, b.namespace, list(b.token_span), b.parent_id, b.ref_count,
+         b.last_access, b.child_count)
+        for b in blocks
+    )
+    return hashlib.sha1(json.dumps(rows, separators=(",", ":")).encode()).hexdigest()
+
+
+def run_stream(BlockPool, CapacityExhausted, capacity, block_size, ops):
+    pool = BlockPool(capacity_blocks=capacity, block_size=block_size)
+    results = {}  # op index -> blocks returned (reference objects)
+    expect = []
+    for i, op in enumerate(ops):
+        kind = op["op"]
+        rec: dict = {}
+        results[i] = []  # a failed insert returns nothing to pin/release
+        try:
+            if kind == "lookup":
+                matched, blocks = pool.longest_prefix_match(op["ns"], tuple(expand_tokens(op)), op["now"])
+                results[i] = blocks
+                rec["matched"] = matched
+                rec["ids"] = [b.block_id for b in blocks]
+            elif kind == "insert":
+                new = pool.insert(op["ns"], tuple(expand_tokens(op)), op["now"])
+                results[i] = new
+                rec["ids"] = [b.block_id for b in new]
+            elif kind == "pin":
+                pool.pin(results[op["ref"]], op["now"])
+            elif kind == "release":
+                pool.release(results[op["ref"]])
+            elif kind == "evict":
+                rec["evicted"] = pool.evict_until(op["need"])
+            rec["error"] = None
+        except CapacityExhausted:
+            rec["error"] = "capacity"
+        except RuntimeError:
+            rec["error"] = "underflow"
+        rec["used"] = pool.used_blocks
+        rec["evictions"] = pool.eviction_count
+        rec["matched_tokens"] = pool.matched_tokens
+        rec["lookup_tokens"] = pool.lookup_tokens
+        rec["digest"] = state_digest(pool._blocks.values())
+        expect.append(rec)
+    final = sorted(
+        (b.block_id, b.namespace, list(b.token_span), b.parent_id, b.ref_count,
+         b.last_access, b.child_count)
+        for b in pool._blocks.values()
+    )
+    return expect, final, pool.footprint_tokens(), pool.peak_footprint_tokens(), pool.dump_tree()
+
+
+def small_random_stream(rng: random.Random):
+    """Shape of test_kvstore.py:160-217 (hypothesis op streams)."""
+    ops = []
+    held = []
+    now = 0
+    for _ in range(rng.randint(1, 60)):
+        now += 1
+        ns = rng.choice(["shared", "model:m0", "model:m1"])
+        toks = [rng.randint(0, 7) for _ in range(rng.randint(0, 24))]
+        if rng.random() < 0.5:
+            ops.append({"op": "lookup", "ns": ns, "tokens": toks, "now": now})
+            held.append(len(ops) - 1)
+            if len(held) > 3:
+                ops.append({"op": "release", "ref": held.pop(0)})
+        else:
+            ops.append({"op": "insert", "ns": ns, "tokens": toks, "now": now})
+            if rng.random() < 0.3:
+                ops.append({"op": "pin", "ref": len(ops) - 1, "now": now})
+                held.append(len(ops) - 2)
+    return ops
+
+
+def a2_stream(rng: random.Random, block_size: int, n_ops: int):
+    """Shape of test_acceptance.py:283-324 (A2 randomized equivalence)."""
+    ops = []
+    held = []
+    for now in range(n_ops):
+        ns = rng.choice(["shared", "model:a", "model:b"])
+        base = rng.randrange(6)
+        length = rng.randrange(0, 4 * block_size + 3)
+        toks = [base * 1000 + t for t in range(length)]
+        if rng.random() < 0.5:
+            ops.append({"op": "lookup", "ns": ns, "tokens": toks, "now": now})
+            held.append(len(ops) - 1)
+        else:
+            ops.append({"op": "insert", "ns": ns, "tokens": toks, "now": now})
+        while len(held) > rng.randrange(1, 5):
+            ops.append({"op": "release", "ref": held.pop(0)})
+    return ops
+
+
+def expand_tokens(op) -> list:
+    """Token list of an op; DES ops store synth_tokens segments
+    (workload.py:375-387 packing) instead of the expanded ids."""
+    if "segs" not in op:
+        return op["tokens"]
+    out = []
+    for sid, purpose, n in op["segs"]:
+        base = ((sid + 1) << 32) | (purpose << 16)
+        out.extend(base | i for i in range(n))
+    return out
+
+
+def des_like_stream(rng: random.Random, wl, n_sessions: int, turns: int):
+    """Multi-turn agent contexts of synth_tokens ids (cluster.py:271-366
+    order: lookup at prefill start, insert + pin at prefill complete, release
+    at handoff) with interleaved sessions and eviction pressure."""
+    ops = []
+    segs = {s: [[s, 0, 512]] for s in range(n_sessions)}
+    step = {s: 0 for s in range(n_sessions)}
+    now = 0
+    pending = []
+    for _ in range(n_sessions * turns):
+        s = rng.randrange(n_sessions)
+        segs[s].append([s, 2 * step[s] + 1, 64])
+        now += rng.randint(1, 1000)
+        ops.append({"op": "lookup", "ns": "shared", "segs": [list(x) for x in segs[s]], "now": now})
+        lk = len(ops) - 1
+        now += rng.randint(1, 1000)
+        ops.append({"op": "insert", "ns": "shared", "segs": [list(x) for x in segs[s]], "now": now})
+        ins = len(ops) - 1
+        ops.append({"op": "pin", "ref": ins, "now": now})
+        pending.append((lk, ins))
+        segs[s].append([s, 2 * step[s] + 2, 128])
+        step[s] += 1
+        while len(pending) > rng.randint(0, 3):
+            a, b = pending.pop(0)
+            ops.append({"op": "release", "ref": a})
+            ops.append({"op": "release", "ref": b})
+    for a, b in pending:
+        ops.append({"op": "release", "ref": a})
+        ops.append({"op": "release", "ref": b})
+    ops.append({"op": "evict", "need": 10})
+    return ops
+
+
+def underflow_stream():
+    return [
+        {"op": "insert", "ns": "ns", "tokens": [1, 2, 3, 4, 5, 6, 7, 8], "now": 1},
+        {"op": "pin", "ref": 0, "now": 2},
+        {"op": "lookup", "ns": "ns", "tokens": [1, 2, 3, 4], "now": 3},
+        {"op": "release", "ref": 0},
+        {"op": "release", "ref": 0},          # underflow at the first block
+        {"op": "release", "ref": 2},
+        {"op": "release", "ref": 2},          # underflow
+        {"op": "evict", "need": 3},           # need > capacity
+        {"op": "evict", "need": 2},
+    ]
+
+
+def pool_fixtures(wl, BlockPool, CapacityExhausted):
+    rng = random.Random(20260212)
+    streams = []
+    for i in range(60):
+        bs = rng.choice([1, 2, 4])
+        cap = rng.randint(1, 12)
+        ops = small_random_stream(rng)
+        streams.append({"name": f"small_{i}", "capacity": cap, "block_size": bs, "ops": ops})
+    for bs in (1, 4, 16):
+        ops = a2_stream(random.Random(1000 + bs), bs, 1200)
+        streams.append({"name": f"a2_bs{bs}", "capacity": 48, "block_size": bs, "ops": ops})
+    streams.append({"name": "des_pressure", "capacity": 300, "block_size": 16,
+                    "ops": des_like_stream(random.Random(7), wl, 12, 30)})
+    streams.append({"name": "des_unbounded", "capacity": 1 << 62, "block_size": 16,
+                    "ops": des_like_stream(random.Random(8), wl, 8, 12)})
+    streams.append({"name": "underflow", "capacity": 2, "block_size": 4, "ops": underflow_stream()})
+    for st in streams:
+        expect, final, fp, peak, dump = run_stream(BlockPool, CapacityExhausted, st["capacity"],
+                                                   st["block_size"], st["ops"])
+        st["expect"] = expect
+        st["final"] = final
+        st["footprint"] = fp
+        st["peak"] = peak
+        st["dump_tree"] = dump
+    return streams
+
+
+def router_fixtures(core, router):
+    rng = random.Random(99)
+    models = ["model_a", "model_b", "model_c", "model_d"]
+    traces = []
+    for mode in (router.ServingMode.BASELINE, router.ServingMode.PREFILLSHARE):
+        r = router.Router(mode, models)
+        steps = []
+        for i in range(400):
+            sid = rng.randrange(60)
+            m = rng.choice(models + (["model_x"] if rng.random() < 0.02 else []))
+            depths = [rng.randrange(6) for _ in range(4)]
+            req = core.Request(request_id=i, session_id=sid, model_id=m, context_snapshot=(),
+                               output_len=1, issue_time=0)
+            try:
+                w = r.route_prefill(req, depths)
+                d = r.decode_worker(req)
+                steps.append({"session": sid, "model": m, "depths": depths, "prefill": w,
+                              "decode": d, "ns": r.prefill_namespace(m)})
+            except router.ConfigurationError:
+                steps.append({"session": sid, "model": m, "depths": depths, "error": "config"})
+        traces.append({"mode": mode.value, "models": models, "steps": steps})
+    return traces
+
+
+def workload_fixtures(wl):
+    s = wl.splitmix64(0)
+    vec = [next(s) for _ in range(8)]
+    cfg = wl.WorkloadConfig(pattern="react", arrival_rate_per_s=4.0, duration_s=20.0, seed=3)
+    sessions = json.loads(wl.export_sessions(wl.generate(cfg)))
+    return {
+        "splitmix64_seed0": [str(v) for v in vec],
+        "mix_seed": {"1,2": str(wl.mix_seed(1, 2)), "0": str(wl.mix_seed(0)),
+                     "0,0": str(wl.mix_seed(0, 0))},
+        "synth_tokens_3_5_4": [str(t) for t in wl.synth_tokens(3, 5, 4)],
+        "generate_react_seed3_20s": sessions,
+    }
+
+
+def main() -> None:
+    sys.path.insert(0, str(REF))
+    from prefillsim import core, kvstore, router, workload as wl  # noqa: E402
+
+    pools = pool_fixtures(wl, kvstore.BlockPool, kvstore.CapacityExhausted)
+    blob = json.dumps({"generator": "prefillsim.kvstore.BlockPool", "streams": pools},
+                      separators=(",", ":")).encode()
+    (OUT / "pool_streams.json.gz").write_bytes(gzip.compress(blob, 9, mtime=0))
+    (OUT / "router_traces.json").write_text(json.dumps(router_fixtures(core, router)))
+    (OUT / "workload.json").write_text(json.dumps(workload_fixtures(wl), indent=0))
+    n_ops = sum(len(s["ops"]) for s in pools)
+    print(f"pool streams: {len(pools)} ({n_ops} ops); router traces; workload vectors")
+
+
+if __name__ == "__main__":
+    main()
