@@ -119,6 +119,98 @@ int psk_pool_snapshot(psk_pool* pool, int64_t* block_id, int64_t* parent_id,
  * last_access, parent_slot}; tokens = its span (block_size ids). */
 int psk_pool_read_record(psk_pool* pool, int32_t slot, int64_t* fields, int64_t* tokens);
 
+/* ------------------------------------------------------------------------ *
+ * Paged KV layout (shared by prefill, decode and transfer kernels).
+ * One page holds `page_tokens` (=16 = kvstore block_size) consecutive
+ * positions for ALL layers: page[layer][K|V][kv_head][token][head_dim] bf16,
+ * so one page is one contiguous NVLink copy unit (2 MiB at the 8B shape) and
+ * each (layer, K|V, head) tile is a contiguous 4 KiB run.
+ * ------------------------------------------------------------------------ */
+typedef struct psk_kv_layout {
+  void* base;            /* bf16 [n_pages][page_elems]                      */
+  int64_t page_elems;    /* n_layers * 2 * n_kv_heads * page_tokens * head_dim */
+  int32_t n_layers;
+  int32_t n_kv_heads;
+  int32_t head_dim;      /* 128 */
+  int32_t page_tokens;   /* 16  */
+} psk_kv_layout;
+
+/* A batch of decode rows. Row r = (decode module row_mod[r], session
+ * row_sess[r]); rows are grouped by module: module i owns rows
+ * [mod_row_start[i], mod_row_start[i+1]). Session s shares its base-prefill
+ * KV for positions [0, sess_len[s]) through sess_pages; row r's own KV
+ * (positions sess_len + [0, priv_len[r])) lives in row_pages. All arrays are
+ * device memory; the step kernels read lengths on the device so a whole
+ * step can be captured in a CUDA graph. Mirrors the decode-module contract
+ * of frontend/src/model.ts:363-399 (generate with an injected strict-prefix
+ * cache; the module itself processes the last prompt token, :372-374 and
+ * evaluate.ts:16-19). */
+typedef struct psk_decode_batch {
+  int32_t n_rows;
+  int32_t n_sess;
+  int32_t n_mod;
+  int32_t max_rows_per_sess;   /* <= 16 (64 query heads per KV head tile)  */
+  const int32_t* row_mod;      /* [n_rows] module index (0..n_mod)         */
+  const int32_t* row_sess;     /* [n_rows]                                 */
+  const int32_t* row_in_sess;  /* [n_rows] index of the row in its session */
+  const int32_t* mod_row_start;/* [n_mod+1]                                */
+  const int32_t* sess_rows;    /* [n_sess][max_rows_per_sess] row ids      */
+  const int32_t* sess_nrows;   /* [n_sess]                                 */
+  const int32_t* sess_len;     /* [n_sess] shared prefix tokens            */
+  const int32_t* sess_pages;   /* [n_sess][max_sess_pages]                 */
+  int32_t max_sess_pages;
+  const int32_t* row_pages;    /* [n_rows][max_row_pages]                  */
+  int32_t max_row_pages;
+  int32_t* priv_len;           /* [n_rows] private tokens already written  */
+  int32_t* tokens;             /* [n_rows] current input token             */
+} psk_decode_batch;
+
+/* h[r,:] = embed[row_mod[r]][tokens[r],:] (fp32 residual stream).
+ * embed: device array of n_mod bf16 table pointers [vocab][d]. */
+int psk_embed_rows(const psk_decode_batch* b, const void* const* embed, int32_t d,
+                   float* h, void* stream);
+/* out[r,:] = bf16(h[r,:] * rsqrt(mean(h^2)+eps) * gamma[mod(r)]) where
+ * mod(r) = row_mod ? row_mod[r] : 0; gamma: device array of pointers. */
+int psk_rmsnorm_rows(const float* h, int32_t n_rows, int32_t d, const void* const* gamma,
+                     const int32_t* row_mod, float eps, void* out, void* stream);
+
+/* Grouped weight-streaming GEMV (K5): for each module i and each of its
+ * rows r, y[r, n] = sum_k x[r, k] * W_i[n, k]  (x bf16 [n_rows][K], W_i bf16
+ * [N][K] row-major). Epilogues: */
+#define PSK_EPI_STORE_BF16 0   /* out bf16 [n_rows][N]                          */
+#define PSK_EPI_STORE_F32 1    /* out fp32 [n_rows][N]                          */
+#define PSK_EPI_RESID_ADD 2    /* out fp32 [n_rows][N] += y (residual stream)   */
+#define PSK_EPI_SILU_MUL 3     /* W rows interleaved [gate16|up16]...; out bf16 [n_rows][N/2] = silu(g)*u */
+int psk_gemv(const void* x, int32_t n_rows, int32_t K, const void* const* W,
+             const int32_t* mod_row_start, int32_t n_mod, int32_t N, int32_t epilogue,
+             void* out, void* stream);
+
+/* RoPE (rotate-half, Llama) on q and k of the fused qkv rows (fp32
+ * [n_rows][(nq+2*nkv)*hd]) at position sess_len[sess]+priv_len[r]; writes
+ * q_rot bf16 [n_rows][nq][hd] and appends k,v (bf16) to the row's private
+ * page at index priv_len[r]. rope: fp32 [max_pos][hd/2][2] (cos, sin). */
+int psk_rope_append(const psk_decode_batch* b, const float* qkv, int32_t n_q_heads,
+                    const float* rope, int32_t layer, psk_kv_layout kv, void* q_rot,
+                    void* stream);
+
+/* K6: shared-prefix paged decode attention for one layer. Every KV page of
+ * a session's shared prefix is streamed from HBM once per step for ALL of
+ * the session's decode rows (modules) and their GQA query heads; each row's
+ * private suffix (incl. the token appended this step) is a second pass; the
+ * partials merge by log-sum-exp. out bf16 [n_rows][nq][hd]. workspace: see
+ * psk_decode_attn_workspace. */
+int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int32_t head_dim,
+                              int32_t shared_splits, int32_t priv_splits, int64_t* bytes);
+int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_heads,
+                    int32_t layer, psk_kv_layout kv, int32_t shared_splits,
+                    int32_t priv_splits, void* workspace, void* out, void* stream);
+
+/* Greedy step end: tokens[r] = argmax(logits[r]) (first max, as tf.argMax /
+ * torch.argmax), out_tokens[r*max_new + priv_len[r]] = it (if in range),
+ * then priv_len[r] += 1 (the row's KV for this step was appended). */
+int psk_argmax_advance(const psk_decode_batch* b, const float* logits, int32_t vocab,
+                       int32_t* out_tokens, int32_t max_new, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -45,6 +45,23 @@ class PoolResult(C.Structure):
     ]
 
 
+class KVLayout(C.Structure):
+    _fields_ = [("base", C.c_void_p), ("page_elems", C.c_int64), ("n_layers", C.c_int32),
+                ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("page_tokens", C.c_int32)]
+
+
+class DecodeBatchC(C.Structure):
+    _fields_ = [
+        ("n_rows", C.c_int32), ("n_sess", C.c_int32), ("n_mod", C.c_int32),
+        ("max_rows_per_sess", C.c_int32),
+        ("row_mod", C.c_void_p), ("row_sess", C.c_void_p), ("row_in_sess", C.c_void_p),
+        ("mod_row_start", C.c_void_p), ("sess_rows", C.c_void_p), ("sess_nrows", C.c_void_p),
+        ("sess_len", C.c_void_p), ("sess_pages", C.c_void_p), ("max_sess_pages", C.c_int32),
+        ("row_pages", C.c_void_p), ("max_row_pages", C.c_int32),
+        ("priv_len", C.c_void_p), ("tokens", C.c_void_p),
+    ]
+
+
 _P = C.c_void_p
 _I32 = C.c_int32
 _I64 = C.c_int64
@@ -74,6 +91,14 @@ _SIGS: dict[str, list] = {
     "psk_pool_footprint": [_P, _I32, C.POINTER(_I64), C.POINTER(_I64)],
     "psk_pool_snapshot": [_P, _P, _P, _P, _P, _P, _P, _P],
     "psk_pool_read_record": [_P, _I32, _P, _P],
+    # decode step (K5 / K6)
+    "psk_embed_rows": [C.POINTER(DecodeBatchC), _P, _I32, _P, _P],
+    "psk_rmsnorm_rows": [_P, _I32, _I32, _P, _P, _F, _P, _P],
+    "psk_gemv": [_P, _I32, _I32, _P, _P, _I32, _I32, _I32, _P, _P],
+    "psk_rope_append": [C.POINTER(DecodeBatchC), _P, _I32, _P, _I32, KVLayout, _P, _P],
+    "psk_decode_attn_workspace": [C.POINTER(DecodeBatchC), _I32, _I32, _I32, _I32, C.POINTER(_I64)],
+    "psk_decode_attn": [C.POINTER(DecodeBatchC), _P, _I32, _I32, KVLayout, _I32, _I32, _P, _P, _P],
+    "psk_argmax_advance": [C.POINTER(DecodeBatchC), _P, _I32, _P, _I32, _P],
 }
 _RESTYPE = {
     "psk_last_error": C.c_char_p,

@@ -1,0 +1,403 @@
+"""Prefill / decode module factorisation on B200 (host side).
+
+Mirrors the reference's module split (frontend/src/model.ts): a frozen base
+("prefill module") builds the prompt KV cache once (buildBaseCache,
+model.ts:340-352) and task-specific decode modules with the same architecture
+but their own weights (train.ts:234, base.clone()) generate from it
+(generate with an injected strict-prefix cache, model.ts:363-412). The
+architecture is Llama-style (RMSNorm, RoPE rotate-half, GQA, SwiGLU) at the
+shapes BASELINE.json names; weights are random-init and generated on the GPU.
+
+All tensor work is done by libpsk.so kernels; torch only owns device memory
+and streams.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+
+PAGE_TOKENS = 16  # == kvstore block_size
+HEAD_DIM = 128
+
+
+@dataclass(frozen=True)
+class LlamaConfig:
+    n_layers: int
+    d_model: int
+    n_heads: int
+    n_kv_heads: int
+    ffn: int
+    vocab: int
+    rope_theta: float
+    norm_eps: float = 1e-5
+    max_pos: int = 8192
+    head_dim: int = HEAD_DIM
+
+    @property
+    def qkv_dim(self) -> int:
+        return (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
+
+    @property
+    def page_elems(self) -> int:
+        return self.n_layers * 2 * self.n_kv_heads * PAGE_TOKENS * self.head_dim
+
+    @property
+    def kv_bytes_per_token(self) -> int:
+        return 2 * self.n_layers * self.n_kv_heads * self.head_dim * 2
+
+    def param_count(self, with_head: bool = True) -> int:
+        d, L = self.d_model, self.n_layers
+        per_layer = 2 * d + self.qkv_dim * d + d * self.n_heads * self.head_dim + 3 * self.ffn * d
+        return self.vocab * d * (2 if with_head else 1) + L * per_layer + d
+
+    @staticmethod
+    def tiny(max_pos: int = 2048) -> "LlamaConfig":
+        """BASELINE config 1: 2 layers, d=256 (2 q heads x 128, 1 kv head)."""
+        return LlamaConfig(n_layers=2, d_model=256, n_heads=2, n_kv_heads=1, ffn=768, vocab=4096,
+                           rope_theta=1e4, max_pos=max_pos)
+
+    @staticmethod
+    def llama8b(n_layers: int = 32, max_pos: int = 8192) -> "LlamaConfig":
+        """Llama-3.1-8B shape (BASELINE configs 2-5); n_layers < 32 gives the
+        full-width truncations used by parity tests."""
+        return LlamaConfig(n_layers=n_layers, d_model=4096, n_heads=32, n_kv_heads=8, ffn=14336,
+                           vocab=128256, rope_theta=5e5, max_pos=max_pos)
+
+
+def rope_table(cfg: LlamaConfig) -> np.ndarray:
+    """[max_pos][head_dim/2][cos, sin] fp32, computed in float64 (rotate-half
+    convention: dims i and i+64 form a pair)."""
+    half = cfg.head_dim // 2
+    inv = 1.0 / (cfg.rope_theta ** (np.arange(half, dtype=np.float64) * 2.0 / cfg.head_dim))
+    ang = np.arange(cfg.max_pos, dtype=np.float64)[:, None] * inv[None, :]
+    return np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+def _mix(*parts: int) -> int:
+    x = 0x243F6A8885A308D3
+    for p in parts:
+        x = (x ^ (p & 0xFFFFFFFFFFFFFFFF)) & 0xFFFFFFFFFFFFFFFF
+        x = (x + 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+        z = x
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+        x = z ^ (z >> 31)
+    return x
+
+
+class ModuleWeights:
+    """One module's bf16 weights in the kernels' fused layouts:
+    wqkv [q|k|v rows][d]; wgu rows interleaved in 16-row groups
+    [gate 16 | up 16] so the gate/up GEMV epilogue fuses SiLU*mul."""
+
+    def __init__(self, cfg: LlamaConfig, seed: int, device: int = 0, with_head: bool = True,
+                 std: float = 0.02):
+        self.cfg = cfg
+        self.seed = seed
+        dev = torch.device("cuda", device)
+        bf = torch.bfloat16
+        d = cfg.d_model
+        self.embed = torch.empty(cfg.vocab, d, dtype=bf, device=dev)
+        self.attn_norm, self.wqkv, self.wo, self.mlp_norm, self.wgu, self.wdown = [], [], [], [], [], []
+        for _ in range(cfg.n_layers):
+            self.attn_norm.append(torch.empty(d, dtype=bf, device=dev))
+            self.wqkv.append(torch.empty(cfg.qkv_dim, d, dtype=bf, device=dev))
+            self.wo.append(torch.empty(d, cfg.n_heads * cfg.head_dim, dtype=bf, device=dev))
+            self.mlp_norm.append(torch.empty(d, dtype=bf, device=dev))
+            self.wgu.append(torch.empty(2 * cfg.ffn, d, dtype=bf, device=dev))
+            self.wdown.append(torch.empty(d, cfg.ffn, dtype=bf, device=dev))
+        self.final_norm = torch.empty(d, dtype=bf, device=dev)
+        self.head = torch.empty(cfg.vocab, d, dtype=bf, device=dev) if with_head else None
+        s = _stream()
+        lib = _lib.load()
+        for i, (t, kind) in enumerate(self._tensors()):
+            tseed = _mix(seed, i)
+            if kind == "norm":
+                # gammas ~ 1 + N(0, 0.1): exercises the per-module gamma path
+                _lib.check(lib.psk_init_normal_bf16(_ptr(t), t.numel(), tseed, 0.1, s))
+                t.add_(1.0)
+            else:
+                _lib.check(lib.psk_init_normal_bf16(_ptr(t), t.numel(), tseed, std, s))
+
+    def _tensors(self):
+        out = [(self.embed, "w")]
+        for l in range(self.cfg.n_layers):
+            out += [(self.attn_norm[l], "norm"), (self.wqkv[l], "w"), (self.wo[l], "w"),
+                    (self.mlp_norm[l], "norm"), (self.wgu[l], "w"), (self.wdown[l], "w")]
+        out.append((self.final_norm, "norm"))
+        if self.head is not None:
+            out.append((self.head, "w"))
+        return out
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * 2 for t, _ in self._tensors())
+
+    def layer_bytes(self) -> int:
+        """Weight bytes one decode step streams per module (all layers + head)."""
+        c = self.cfg
+        per_layer = (c.qkv_dim * c.d_model + c.d_model * c.n_heads * c.head_dim +
+                     3 * c.ffn * c.d_model + 2 * c.d_model) * 2
+        return c.n_layers * per_layer + (c.vocab * c.d_model * 2 if self.head is not None else 0)
+
+    def reference_layout(self) -> dict:
+        """fp32 CPU copies in the standard (un-fused) layout, for the oracle."""
+        c = self.cfg
+        f = lambda t: t.float().cpu()  # noqa: E731
+        out = {"embed": f(self.embed), "final_norm": f(self.final_norm), "layers": []}
+        if self.head is not None:
+            out["head"] = f(self.head)
+        qd, kd = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
+        for l in range(c.n_layers):
+            qkv = f(self.wqkv[l])
+            gu = f(self.wgu[l]).view(-1, 2, 16, c.d_model)
+            out["layers"].append({
+                "attn_norm": f(self.attn_norm[l]), "wq": qkv[:qd], "wk": qkv[qd:qd + kd],
+                "wv": qkv[qd + kd:], "wo": f(self.wo[l]), "mlp_norm": f(self.mlp_norm[l]),
+                "w_gate": gu[:, 0].reshape(c.ffn, c.d_model),
+                "w_up": gu[:, 1].reshape(c.ffn, c.d_model),
+                "w_down": f(self.wdown[l]),
+            })
+        return out
+
+
+class KVCache:
+    """Paged KV memory: bf16 [n_pages][layer][K|V][kv_head][16][128]."""
+
+    def __init__(self, cfg: LlamaConfig, n_pages: int, device: int = 0):
+        self.cfg = cfg
+        self.n_pages = n_pages
+        self.data = torch.zeros(n_pages, cfg.page_elems, dtype=torch.bfloat16,
+                                device=torch.device("cuda", device))
+
+    def layout(self) -> "KVLayout":
+        c = self.cfg
+        return KVLayout(self.data.data_ptr(), c.page_elems, c.n_layers, c.n_kv_heads, c.head_dim,
+                        PAGE_TOKENS)
+
+    def page_view(self) -> torch.Tensor:
+        c = self.cfg
+        return self.data.view(self.n_pages, c.n_layers, 2, c.n_kv_heads, PAGE_TOKENS, c.head_dim)
+
+    def write_positions(self, pages: list[int], layer: int, k: torch.Tensor, v: torch.Tensor,
+                        start: int = 0) -> None:
+        """Test / transfer plumbing: write K,V [n_kv, T, hd] for positions
+        start..start+T-1 of a page table (not on any hot path)."""
+        pv = self.page_view()
+        T = k.shape[1]
+        for t in range(T):
+            p = start + t
+            pg = pages[p // PAGE_TOKENS]
+            pv[pg, layer, 0, :, p % PAGE_TOKENS] = k[:, t].to(pv.dtype)
+            pv[pg, layer, 1, :, p % PAGE_TOKENS] = v[:, t].to(pv.dtype)
+
+    def read_positions(self, pages: list[int], layer: int, n: int, start: int = 0):
+        pv = self.page_view()
+        ks, vs = [], []
+        for t in range(n):
+            p = start + t
+            pg = pages[p // PAGE_TOKENS]
+            ks.append(pv[pg, layer, 0, :, p % PAGE_TOKENS])
+            vs.append(pv[pg, layer, 1, :, p % PAGE_TOKENS])
+        return torch.stack(ks, 1), torch.stack(vs, 1)
+
+
+KVLayout = _lib.KVLayout
+DecodeBatchC = _lib.DecodeBatchC
+
+
+@dataclass
+class DecodeRow:
+    module: int          # index into the runner's module list
+    session: int         # index into the batch's sessions
+    first_token: int     # last prompt token (the module processes it itself)
+    pages: list[int]     # private KV pages (capacity for max_new tokens)
+
+
+@dataclass
+class SessionSpec:
+    shared_len: int      # base-prefill positions the rows attend to: n - 1
+    pages: list[int]     # shared KV page table (covers shared_len positions)
+
+
+class DecodeBatch:
+    """Device arrays describing a set of decode rows (psk_decode_batch)."""
+
+    def __init__(self, sessions: list[SessionSpec], rows: list[DecodeRow], n_modules: int,
+                 device: int = 0):
+        dev = torch.device("cuda", device)
+        order = sorted(range(len(rows)), key=lambda i: (rows[i].module, i))
+        self.rows = [rows[i] for i in order]
+        self.order = order  # batch row j is caller row order[j]
+        self.mod_ids = sorted({r.module for r in self.rows})
+        mod_index = {m: i for i, m in enumerate(self.mod_ids)}
+        R, S = len(self.rows), len(sessions)
+        mrs = [0] * (len(self.mod_ids) + 1)
+        for r in self.rows:
+            mrs[mod_index[r.module] + 1] += 1
+        for i in range(len(self.mod_ids)):
+            mrs[i + 1] += mrs[i]
+        sess_rows: list[list[int]] = [[] for _ in range(S)]
+        row_in_sess = []
+        for j, r in enumerate(self.rows):
+            row_in_sess.append(len(sess_rows[r.session]))
+            sess_rows[r.session].append(j)
+        self.max_rps = max(1, max(len(x) for x in sess_rows))
+        msp = max(1, max(len(s.pages) for s in sessions))
+        mrp = max(1, max(len(r.pages) for r in self.rows))
+        i32 = lambda x: torch.tensor(x, dtype=torch.int32, device=dev)  # noqa: E731
+        self.t_row_mod = i32([mod_index[r.module] for r in self.rows])
+        self.t_row_sess = i32([r.session for r in self.rows])
+        self.t_row_in_sess = i32(row_in_sess)
+        self.t_mrs = i32(mrs)
+        self.t_sess_rows = i32([x + [0] * (self.max_rps - len(x)) for x in sess_rows])
+        self.t_sess_nrows = i32([len(x) for x in sess_rows])
+        self.t_sess_len = i32([s.shared_len for s in sessions])
+        self.t_sess_pages = i32([s.pages + [0] * (msp - len(s.pages)) for s in sessions])
+        self.t_row_pages = i32([r.pages + [0] * (mrp - len(r.pages)) for r in self.rows])
+        self.t_priv_len = i32([0] * R)
+        self.t_tokens = i32([r.first_token for r in self.rows])
+        self.n_rows, self.n_sess, self.n_mod = R, S, len(self.mod_ids)
+        self.c = DecodeBatchC(
+            R, S, len(self.mod_ids), self.max_rps,
+            _ptr(self.t_row_mod), _ptr(self.t_row_sess), _ptr(self.t_row_in_sess), _ptr(self.t_mrs),
+            _ptr(self.t_sess_rows), _ptr(self.t_sess_nrows), _ptr(self.t_sess_len),
+            _ptr(self.t_sess_pages), msp, _ptr(self.t_row_pages), mrp,
+            _ptr(self.t_priv_len), _ptr(self.t_tokens))
+
+    def reset(self) -> None:
+        self.t_priv_len.zero_()
+        self.t_tokens.copy_(torch.tensor([r.first_token for r in self.rows], dtype=torch.int32))
+
+
+class DecodeRunner:
+    """Runs greedy decode steps for a DecodeBatch of heterogeneous modules.
+
+    One step = embed -> L x [RMSNorm, grouped QKV GEMV, RoPE + KV append,
+    shared-prefix attention (K6), O GEMV (+residual), RMSNorm, gate/up GEMV
+    (+SiLU*mul), down GEMV (+residual)] -> RMSNorm -> LM head GEMV -> argmax.
+    The step is captured once into a CUDA graph and replayed.
+    """
+
+    def __init__(self, cfg: LlamaConfig, modules: list[ModuleWeights], kv: KVCache,
+                 batch: DecodeBatch, max_new: int, shared_splits: int | None = None,
+                 priv_splits: int = 1, device: int = 0):
+        self.cfg, self.kv, self.b, self.max_new = cfg, kv, batch, max_new
+        self.lib = _lib.load()
+        dev = torch.device("cuda", device)
+        mods = [modules[m] for m in batch.mod_ids]
+        ptrs = lambda ts: torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64, device=dev)  # noqa: E731
+        L = cfg.n_layers
+        self.p_embed = ptrs([m.embed for m in mods])
+        self.p_attn_norm = [ptrs([m.attn_norm[l] for m in mods]) for l in range(L)]
+        self.p_wqkv = [ptrs([m.wqkv[l] for m in mods]) for l in range(L)]
+        self.p_wo = [ptrs([m.wo[l] for m in mods]) for l in range(L)]
+        self.p_mlp_norm = [ptrs([m.mlp_norm[l] for m in mods]) for l in range(L)]
+        self.p_wgu = [ptrs([m.wgu[l] for m in mods]) for l in range(L)]
+        self.p_wdown = [ptrs([m.wdown[l] for m in mods]) for l in range(L)]
+        self.p_final_norm = ptrs([m.final_norm for m in mods])
+        self.p_head = ptrs([m.head for m in mods])
+        self.weight_bytes_per_step = sum(m.layer_bytes() for m in mods)
+        R, d = batch.n_rows, cfg.d_model
+        f32, bf = torch.float32, torch.bfloat16
+        self.h = torch.empty(R, d, dtype=f32, device=dev)
+        self.xn = torch.empty(R, d, dtype=bf, device=dev)
+        self.qkv = torch.empty(R, cfg.qkv_dim, dtype=f32, device=dev)
+        self.q_rot = torch.empty(R, cfg.n_heads, cfg.head_dim, dtype=bf, device=dev)
+        self.attn = torch.empty(R, cfg.n_heads * cfg.head_dim, dtype=bf, device=dev)
+        self.act = torch.empty(R, cfg.ffn, dtype=bf, device=dev)
+        self.logits = torch.empty(R, cfg.vocab, dtype=f32, device=dev)
+        self.out_tokens = torch.full((R, max_new), -1, dtype=torch.int32, device=dev)
+        self.rope = torch.from_numpy(rope_table(cfg)).to(dev)
+        if shared_splits is None:
+            # fill ~2 CTAs per SM with the shared pass
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            shared_splits = max(1, (2 * sms) // max(1, batch.n_sess * cfg.n_kv_heads))
+        self.ns_shared, self.ns_priv = shared_splits, priv_splits
+        ws = C.c_int64()
+        _lib.check(self.lib.psk_decode_attn_workspace(C.byref(batch.c), cfg.n_kv_heads, cfg.head_dim,
+                                                      shared_splits, priv_splits, C.byref(ws)))
+        self.ws = torch.empty(ws.value // 4 + 1, dtype=f32, device=dev)
+        self.graph: torch.cuda.CUDAGraph | None = None
+        self.launches_per_step = 2 + L * 9 + 3
+
+    # -- one step, eager ----------------------------------------------------
+    def _step(self, s: int) -> None:
+        lib, cfg, b = self.lib, self.cfg, self.b
+        bc = C.byref(b.c)
+        R, d = b.n_rows, cfg.d_model
+        kvl = self.kv.layout()
+        mrs = _ptr(b.t_mrs)
+        chk = _lib.check
+        chk(lib.psk_embed_rows(bc, _ptr(self.p_embed), d, _ptr(self.h), s))
+        for l in range(cfg.n_layers):
+            chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_attn_norm[l]), _ptr(b.t_row_mod),
+                                     C.c_float(cfg.norm_eps), _ptr(self.xn), s))
+            chk(lib.psk_gemv(_ptr(self.xn), R, d, _ptr(self.p_wqkv[l]), mrs, b.n_mod, cfg.qkv_dim,
+                             1, _ptr(self.qkv), s))
+            chk(lib.psk_rope_append(bc, _ptr(self.qkv), cfg.n_heads, _ptr(self.rope), l, kvl,
+                                    _ptr(self.q_rot), s))
+            chk(lib.psk_decode_attn(bc, _ptr(self.q_rot), cfg.n_heads, l, kvl, self.ns_shared,
+                                    self.ns_priv, _ptr(self.ws), _ptr(self.attn), s))
+            chk(lib.psk_gemv(_ptr(self.attn), R, cfg.n_heads * cfg.head_dim, _ptr(self.p_wo[l]), mrs,
+                             b.n_mod, d, 2, _ptr(self.h), s))
+            chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_mlp_norm[l]), _ptr(b.t_row_mod),
+                                     C.c_float(cfg.norm_eps), _ptr(self.xn), s))
+            chk(lib.psk_gemv(_ptr(self.xn), R, d, _ptr(self.p_wgu[l]), mrs, b.n_mod, 2 * cfg.ffn, 3,
+                             _ptr(self.act), s))
+            chk(lib.psk_gemv(_ptr(self.act), R, cfg.ffn, _ptr(self.p_wdown[l]), mrs, b.n_mod, d, 2,
+                             _ptr(self.h), s))
+        chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_final_norm), _ptr(b.t_row_mod),
+                                 C.c_float(cfg.norm_eps), _ptr(self.xn), s))
+        chk(lib.psk_gemv(_ptr(self.xn), R, d, _ptr(self.p_head), mrs, b.n_mod, cfg.vocab, 1,
+                         _ptr(self.logits), s))
+        chk(lib.psk_argmax_advance(bc, _ptr(self.logits), cfg.vocab, _ptr(self.out_tokens),
+                                   self.max_new, s))
+
+    def capture(self) -> None:
+        """Capture one step into a CUDA graph (lengths live on the device)."""
+        self.b.reset()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            self._step(st.cuda_stream)  # warm-up (sets kernel attributes)
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._step(torch.cuda.current_stream().cuda_stream)
+        self.graph = g
+        torch.cuda.synchronize()
+
+    def run(self, n_steps: int, use_graph: bool = True) -> torch.Tensor:
+        """Reset and generate n_steps tokens per row; returns out_tokens in the
+        caller's row order."""
+        self.b.reset()
+        self.out_tokens.fill_(-1)
+        if use_graph and self.graph is None:
+            self.capture()
+            self.b.reset()
+            self.out_tokens.fill_(-1)
+        for _ in range(n_steps):
+            if use_graph:
+                self.graph.replay()
+            else:
+                self._step(_stream())
+        inv = torch.empty_like(self.out_tokens)
+        inv[torch.tensor(self.b.order, device=self.out_tokens.device)] = self.out_tokens
+        return inv
