@@ -211,6 +211,24 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
 int psk_argmax_advance(const psk_decode_batch* b, const float* logits, int32_t vocab,
                        int32_t* out_tokens, int32_t max_new, void* stream);
 
+/* ------------------------------------------------------------------------ *
+ * K1/K2 — prefill GEMMs on tcgen05 (TMA -> smem -> UMMA -> TMEM).
+ * out = A[M,K] . B[N,K]^T with bf16 A/B (K-major), fp32 accumulation and a
+ * fused epilogue (PSK_EPI_* above; ldo = output row stride in elements).
+ * Replaces the q/k/v, o and MLP matmuls of frontend/src/model.ts:298-323.
+ * N % 256 == 0, K % 64 == 0; any M (tail rows masked).
+ * ------------------------------------------------------------------------ */
+#define PSK_EPI_QKV_ROPE_KV 4  /* internal: see psk_gemm_qkv_rope_kv          */
+int psk_gemm(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epilogue,
+             void* out, int64_t ldo, void* stream);
+/* Fused QKV projection of T prompt tokens at positions pos0.. : RoPE on q
+ * and k (rotate-half), q_rot bf16 [T][nq][128] out, k/v written straight into
+ * the paged cache (page_table[pos/16]) — the base module's KV write
+ * (buildBaseCache, model.ts:340-352; cache push model.ts:307-311). */
+int psk_gemm_qkv_rope_kv(const void* A, const void* Wqkv, int32_t T, int32_t K, int32_t n_q_heads,
+                         const float* rope, int32_t pos0, psk_kv_layout kv, int32_t layer,
+                         const int32_t* page_table, void* q_out, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -1,0 +1,461 @@
+// K1 + K2 — prefill GEMMs on the 5th-gen tensor cores.
+//
+// C[M,N] = A[M,K] . B[N,K]^T, bf16 operands (both K-major), fp32 accumulate
+// in TMEM. Replaces the dense contractions of the reference forward
+// (frontend/src/model.ts:298-306 q/k/v, :318 o-proj, :322-323 MLP) which the
+// simulator only models as time (src/prefillsim/costs.py:46-54).
+//
+// Kernel anatomy (persistent, one CTA per SM, 8 warps):
+//   warp 0     TMA producer: 128x64 A and 256x64 B boxes, 128B-swizzled,
+//              into a 4-stage shared-memory ring (48 KiB / stage)
+//   warp 1     MMA issuer: one elected lane issues tcgen05.mma (M=128,
+//              N=256, K=16) x4 per stage; tcgen05.commit frees the stage
+//   warp 2     TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//   warps 4-7  epilogue: tcgen05.ld 32x32b.x32 (thread = tile row), fused
+//              epilogue, stores; accumulator stage released via mbarrier so
+//              the MMA of tile i+1 overlaps the epilogue of tile i.
+// Tiles are walked m-fastest so one wave shares its B (weight) tiles in L2.
+//
+// Fused epilogues: bf16 store, fp32 residual add, SiLU(gate)*up over the
+// [gate16|up16]-interleaved weight layout, and QKV -> RoPE (rotate-half) ->
+// q_rot + paged K/V write (K2, model.ts:307-311 cache push, done in place).
+#include "common.cuh"
+
+#include <cuda.h>
+
+namespace psk {
+namespace gemm {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int THREADS = 256;
+constexpr int TMEM_COLS = 512;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+struct Epi {
+  int mode;
+  void* out;
+  int64_t ldo;
+  // QKV_ROPE_KV
+  const float* rope;
+  int pos0;
+  int nq, nkv;
+  psk_kv_layout kv;
+  int layer;
+  const int32_t* page_table;
+  __nv_bfloat16* q_out;
+};
+
+// ----------------------------------------------------------- PTX helpers --
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x,
+                                            int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(smem_addr(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
+  // K-major, 128B swizzle: LBO = 16 B (unused), SBO = 1024 B (8 rows x 128 B),
+  // version 1 (sm100), layout SWIZZLE_128B (2) in bits 61-63.
+  uint64_t d = (uint64_t)((smem_addr(p) >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_addr(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ------------------------------------------------------------- epilogues --
+
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) reinterpret_cast<uint4*>(dst)[i] = f32_to_bf16x8(v + 8 * i);
+}
+
+__device__ __forceinline__ __nv_bfloat16* kv_dst(const psk_kv_layout& kv, int page, int layer,
+                                                 int kvsel, int head, int tok) {
+  return reinterpret_cast<__nv_bfloat16*>(kv.base) + (int64_t)page * kv.page_elems +
+         ((((int64_t)layer * 2 + kvsel) * kv.n_kv_heads + head) * kv.page_tokens + tok) * kv.head_dim;
+}
+
+// Epilogue for one 128x256 tile; thread owns tile row `r` (TMEM lane).
+__device__ void epilogue_tile(const Epi& e, uint32_t tacc, int row, bool row_ok, int n0) {
+  float v[32], w[32];
+  if (e.mode == PSK_EPI_QKV_ROPE_KV) {
+    const int pos = e.pos0 + row;
+    const float* cs = e.rope + (int64_t)pos * 128;
+#pragma unroll 1
+    for (int hh = 0; hh < 2; ++hh) {
+      const int head = (n0 >> 7) + hh;
+      const uint32_t hb = tacc + hh * 128;
+      if (head >= e.nq + e.nkv) {  // V head: plain copy into the page
+        const int vh = head - e.nq - e.nkv;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          tmem_ld32(hb + c * 32, v);
+          if (row_ok) {
+            const int page = e.page_table[pos / 16];
+            store_bf16x32(kv_dst(e.kv, page, e.layer, 1, vh, pos % 16) + c * 32, v);
+          }
+        }
+        continue;
+      }
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        tmem_ld32(hb + half * 32, v);       // dims [32h, 32h+32)
+        tmem_ld32(hb + half * 32 + 64, w);  // dims [64+32h, ...)
+        if (!row_ok) continue;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float c = cs[2 * (half * 32 + j)], s = cs[2 * (half * 32 + j) + 1];
+          const float x1 = v[j], x2 = w[j];
+          v[j] = x1 * c - x2 * s;
+          w[j] = x2 * c + x1 * s;
+        }
+        __nv_bfloat16* dst;
+        if (head < e.nq) {
+          dst = e.q_out + ((int64_t)row * e.nq + head) * 128;
+        } else {
+          const int page = e.page_table[pos / 16];
+          dst = kv_dst(e.kv, page, e.layer, 0, head - e.nq, pos % 16);
+        }
+        store_bf16x32(dst + half * 32, v);
+        store_bf16x32(dst + half * 32 + 64, w);
+      }
+    }
+    return;
+  }
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    tmem_ld32(tacc + c * 32, v);
+    if (!row_ok) continue;
+    const int col = n0 + c * 32;
+    if (e.mode == PSK_EPI_STORE_BF16) {
+      store_bf16x32(reinterpret_cast<__nv_bfloat16*>(e.out) + (int64_t)row * e.ldo + col, v);
+    } else if (e.mode == PSK_EPI_STORE_F32) {
+      float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (int64_t)row * e.ldo + col);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    } else if (e.mode == PSK_EPI_RESID_ADD) {
+      float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (int64_t)row * e.ldo + col);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 o = d[i];
+        o.x += v[4 * i];
+        o.y += v[4 * i + 1];
+        o.z += v[4 * i + 2];
+        o.w += v[4 * i + 3];
+        d[i] = o;
+      }
+    } else if (e.mode == PSK_EPI_SILU_MUL) {
+      float o[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float g = v[i], u = v[16 + i];
+        o[i] = g / (1.f + __expf(-g)) * u;
+      }
+      __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(e.out) + (int64_t)row * e.ldo + col / 2;
+      reinterpret_cast<uint4*>(d)[0] = f32_to_bf16x8(o);
+      reinterpret_cast<uint4*>(d)[1] = f32_to_bf16x8(o + 8);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- kernel --
+
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                        const __grid_constant__ CUtensorMap tmap_b, int M, int N, int K, Epi e) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m_tiles = (M + BM - 1) / BM, n_tiles = N / BN;
+  const int n_tiles_total = m_tiles * n_tiles;
+  const int kb_n = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmap_a);
+    tma_prefetch(&tmap_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_addr(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+        const int mb = t % m_tiles, nb = t / m_tiles;
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(&tmap_a, &full[stage], sA + stage * A_BYTES, kb * BK, mb * BM);
+          tma_load_2d(&tmap_b, &full[stage], sB + stage * B_BYTES, kb * BK, nb * BN);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tacc = tmem_base + acc * BN;
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t da = smem_desc_sw128(sA + stage * A_BYTES);
+          const uint64_t db = smem_desc_sw128(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // +32 bytes along K inside the 128B swizzle atom = +2 in the
+            // descriptor's 16-byte address units
+            umma_bf16(tacc, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int r_in_tile = q * 32 + lane;
+    int it = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++it) {
+      const int mb = t % m_tiles, nb = t / m_tiles;
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int row = mb * BM + r_in_tile;
+      const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      epilogue_tile(e, tacc, row, row < M, nb * BN);
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------ host side --
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return PSK_ECUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return PSK_ECUDA;
+  }
+  return PSK_OK;
+}
+
+static int launch(const void* A, const void* B, int M, int N, int K, const Epi& e, cudaStream_t s) {
+  if (M <= 0) return PSK_OK;
+  if (N % BN != 0 || K % BK != 0) {
+    set_error("psk_gemm: N %% 256 and K %% 64 must be 0 (N=%d K=%d)", N, K);
+    return PSK_EINVAL;
+  }
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, A, M, K, BM);
+  if (rc) return rc;
+  rc = make_map(&mb, B, N, K, BN);
+  if (rc) return rc;
+  static int sms = 0;
+  if (!sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    PSK_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_BYTES));
+  }
+  const int tiles = ((M + BM - 1) / BM) * (N / BN);
+  const int grid = tiles < sms ? tiles : sms;
+  gemm_bf16_tn_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ma, mb, M, N, K, e);
+  PSK_LAUNCH_CHECK();
+  return PSK_OK;
+}
+
+}  // namespace gemm
+}  // namespace psk
+
+extern "C" {
+
+int psk_gemm(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epilogue,
+             void* out, int64_t ldo, void* stream) {
+  PSK_CHECK_ARG(A && B && out && epilogue >= 0 && epilogue <= PSK_EPI_SILU_MUL,
+                "psk_gemm: bad args");
+  psk::gemm::Epi e{};
+  e.mode = epilogue;
+  e.out = out;
+  e.ldo = ldo;
+  return psk::gemm::launch(A, B, M, N, K, e, psk::as_stream(stream));
+}
+
+int psk_gemm_qkv_rope_kv(const void* A, const void* Wqkv, int32_t T, int32_t K, int32_t n_q_heads,
+                         const float* rope, int32_t pos0, psk_kv_layout kv, int32_t layer,
+                         const int32_t* page_table, void* q_out, void* stream) {
+  PSK_CHECK_ARG(A && Wqkv && rope && page_table && q_out && kv.head_dim == 128 && kv.page_tokens == 16,
+                "psk_gemm_qkv_rope_kv: bad args");
+  psk::gemm::Epi e{};
+  e.mode = PSK_EPI_QKV_ROPE_KV;
+  e.rope = rope;
+  e.pos0 = pos0;
+  e.nq = n_q_heads;
+  e.nkv = kv.n_kv_heads;
+  e.kv = kv;
+  e.layer = layer;
+  e.page_table = page_table;
+  e.q_out = reinterpret_cast<__nv_bfloat16*>(q_out);
+  const int N = (n_q_heads + 2 * kv.n_kv_heads) * 128;
+  return psk::gemm::launch(A, Wqkv, T, N, K, e, psk::as_stream(stream));
+}
+
+}  // extern "C"
