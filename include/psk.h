@@ -229,6 +229,16 @@ int psk_gemm_qkv_rope_kv(const void* A, const void* Wqkv, int32_t T, int32_t K, 
                          const float* rope, int32_t pos0, psk_kv_layout kv, int32_t layer,
                          const int32_t* page_table, void* q_out, void* stream);
 
+/* K3 — causal prefill attention of T new positions [pos0, pos0+T) over the
+ * paged cache (keys [0, pos0+T) through page_table; the new keys were
+ * written by psk_gemm_qkv_rope_kv). q_rot bf16 [T][nq][128] -> out bf16
+ * [T][nq*128]. frontend/src/model.ts:288-293, :312-315. */
+int psk_prefill_attn(const void* q_rot, int32_t T, int32_t pos0, int32_t n_q_heads, psk_kv_layout kv,
+                     int32_t layer, const int32_t* page_table, void* out, void* stream);
+/* h[t,:] = table[tokens[t],:] (fp32). model.ts:276-284 (token embedding). */
+int psk_embed_tokens(const int32_t* tokens, int32_t T, const void* table, int32_t d, float* h,
+                     void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

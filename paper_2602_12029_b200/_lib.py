@@ -102,6 +102,8 @@ _SIGS: dict[str, list] = {
     # prefill (K1-K3)
     "psk_gemm": [_P, _P, _I32, _I32, _I32, _I32, _P, _I64, _P],
     "psk_gemm_qkv_rope_kv": [_P, _P, _I32, _I32, _I32, _P, _I32, KVLayout, _I32, _P, _P, _P],
+    "psk_prefill_attn": [_P, _I32, _I32, _I32, KVLayout, _I32, _P, _P, _P],
+    "psk_embed_tokens": [_P, _I32, _P, _I32, _P, _P],
 }
 _RESTYPE = {
     "psk_last_error": C.c_char_p,

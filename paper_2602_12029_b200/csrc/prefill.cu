@@ -1,0 +1,266 @@
+// K3 — causal prefill attention over the paged KV cache, plus the token
+// embedding gather of the prefill module.
+//
+// Reference: softmax(QK^T/sqrt(hd) + causal mask) V per layer
+// (frontend/src/model.ts:288-293 mask, :312-315 attention), where new
+// positions [pos0, pos0+T) attend to every cached position and causally to
+// themselves (a partial prefill after a prefix hit starts at the matched,
+// block-aligned pos0: kvstore.py:123-138, cluster.py:322-337).
+//
+// One CTA = (kv head, block of query positions); its 8 warps are
+// (q head of the GQA group) x (16-position sub-block), so each 4 KiB K / V
+// page tile is loaded once into XOR-swizzled shared memory (cp.async ring)
+// and consumed by every q head of the group. Heavy (late) query blocks are
+// scheduled first. Tensor math is mma.sync m16n8k16 (bf16 -> fp32).
+#include "common.cuh"
+#include "mma.cuh"
+
+#include <math.h>
+
+namespace psk {
+namespace pre {
+
+constexpr int HD = 128, PT = 16;
+constexpr int WARPS = 8, THREADS = WARPS * 32;
+constexpr int RP = 4, NST = 3;
+constexpr int TILE = PT * HD * 2;
+constexpr int STAGE = RP * 2 * TILE;
+constexpr int SMEM = NST * STAGE;  // 96 KiB
+
+__global__ void embed_tokens_kernel(const int32_t* __restrict__ tokens,
+                                    const __nv_bfloat16* __restrict__ table, int d,
+                                    float* __restrict__ h) {
+  const int t = blockIdx.x;
+  const __nv_bfloat16* row = table + (int64_t)tokens[t] * d;
+  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+    float f[8];
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(row + i), f);
+    float4* o = reinterpret_cast<float4*>(h + (int64_t)t * d + i);
+    o[0] = make_float4(f[0], f[1], f[2], f[3]);
+    o[1] = make_float4(f[4], f[5], f[6], f[7]);
+  }
+}
+
+struct Params {
+  const __nv_bfloat16* q;  // [T][nq][HD]
+  __nv_bfloat16* out;      // [T][nq*HD]
+  psk_kv_layout kv;
+  const int32_t* pages;
+  int T, pos0, nq, grp, layer;
+  int qb;        // query positions per CTA
+  int n_qblocks;
+  float scale_log2;
+};
+
+__device__ __forceinline__ const __nv_bfloat16* tile_ptr(const psk_kv_layout& kv, int page, int layer,
+                                                         int kvsel, int head) {
+  return reinterpret_cast<const __nv_bfloat16*>(kv.base) + (int64_t)page * kv.page_elems +
+         (((int64_t)layer * 2 + kvsel) * kv.n_kv_heads + head) * kv.page_tokens * kv.head_dim;
+}
+
+__global__ void __launch_bounds__(THREADS, 2) prefill_attn_kernel(Params p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkv = p.kv.n_kv_heads;
+  const int h = blockIdx.x % nkv;
+  const int qblk = p.n_qblocks - 1 - (int)(blockIdx.x / nkv);  // heavy blocks first
+  const int t0 = qblk * p.qb;                                  // first query (token index)
+  const int qh = h * p.grp + warp % p.grp;
+  const int sub = warp / p.grp;
+  const int wt0 = t0 + sub * 16;                               // this warp's 16 queries
+  const bool active = wt0 < p.T;
+  const int kv_end = p.pos0 + min(t0 + p.qb, p.T);             // keys [0, kv_end)
+  const int n_pages = (kv_end + PT - 1) / PT;
+  const int w_last_pos = p.pos0 + min(wt0 + 15, p.T - 1);      // last query position of the warp
+
+  uint32_t qa[8][4];
+  {
+    const int ta = wt0 + (lane >> 2), tb = ta + 8;
+    const int t2 = (lane & 3) * 2;
+    const __nv_bfloat16* qA = (active && ta < p.T) ? p.q + ((int64_t)ta * p.nq + qh) * HD : nullptr;
+    const __nv_bfloat16* qB = (active && tb < p.T) ? p.q + ((int64_t)tb * p.nq + qh) * HD : nullptr;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int c0 = ks * 16 + t2, c1 = c0 + 8;
+      qa[ks][0] = qA ? *reinterpret_cast<const uint32_t*>(qA + c0) : 0u;
+      qa[ks][1] = qB ? *reinterpret_cast<const uint32_t*>(qB + c0) : 0u;
+      qa[ks][2] = qA ? *reinterpret_cast<const uint32_t*>(qA + c1) : 0u;
+      qa[ks][3] = qB ? *reinterpret_cast<const uint32_t*>(qB + c1) : 0u;
+    }
+  }
+  const int posA = p.pos0 + wt0 + (lane >> 2), posB = posA + 8;
+
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  const int rounds = (n_pages + RP - 1) / RP;
+  const uint32_t sbase = smem_u32(smem);
+  auto issue = [&](int rd) {
+    if (rd < rounds) {
+      const uint32_t st = sbase + (rd % NST) * STAGE;
+      for (int e = threadIdx.x; e < RP * 2 * 256; e += THREADS) {
+        const int ps = e >> 9, kvsel = (e >> 8) & 1, ce = e & 255;
+        const int pg = rd * RP + ps;
+        if (pg < n_pages) {
+          const __nv_bfloat16* src = tile_ptr(p.kv, p.pages[pg], p.layer, kvsel, h);
+          const int tr = ce >> 4, c = ce & 15;
+          cp_async16(st + (ps * 2 + kvsel) * TILE + swz256(tr, c), src + tr * HD + c * 8);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < NST - 1; ++s) issue(s);
+
+  for (int rd = 0; rd < rounds; ++rd) {
+    cp_async_wait<NST - 2>();
+    __syncthreads();
+    issue(rd + NST - 1);
+    if (!active) continue;
+    const uint32_t st = sbase + (rd % NST) * STAGE;
+#pragma unroll 1
+    for (int ps = 0; ps < RP; ++ps) {
+      const int pg = rd * RP + ps;
+      if (pg >= n_pages) break;
+      const int key0 = pg * PT;
+      if (key0 > w_last_pos) break;  // fully in the causal future of this warp
+      const uint32_t kt = st + (ps * 2) * TILE, vt = kt + TILE;
+      float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      {
+        const int mi = lane >> 3, ri = lane & 7;
+        const int tok = (mi >> 1) * 8 + ri;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          uint32_t b0, b1, b2, b3;
+          ldmatrix_x4(kt + swz256(tok, 2 * ks + (mi & 1)), b0, b1, b2, b3);
+          mma_bf16_16816(s[0], qa[ks], b0, b1);
+          mma_bf16_16816(s[1], qa[ks], b2, b3);
+        }
+      }
+      const int cb = (lane & 3) * 2;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int key = key0 + nt * 8 + cb + (e & 1);
+          const int qpos = (e < 2) ? posA : posB;
+          s[nt][e] = (key <= qpos && key < kv_end) ? s[nt][e] * p.scale_log2 : -INFINITY;
+        }
+      float mx0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
+      float mx1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
+      const float r0 = n0 == -INFINITY ? 0.f : n0, r1 = n1 == -INFINITY ? 0.f : n1;
+      const float c0 = exp2f(m0 - r0), c1 = exp2f(m1 - r1);
+      m0 = n0;
+      m1 = n1;
+      float pr[2][4];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        pr[nt][0] = exp2f(s[nt][0] - r0);
+        pr[nt][1] = exp2f(s[nt][1] - r0);
+        pr[nt][2] = exp2f(s[nt][2] - r1);
+        pr[nt][3] = exp2f(s[nt][3] - r1);
+      }
+      l0 = l0 * c0 + pr[0][0] + pr[0][1] + pr[1][0] + pr[1][1];
+      l1 = l1 * c1 + pr[0][2] + pr[0][3] + pr[1][2] + pr[1][3];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        o[i][0] *= c0;
+        o[i][1] *= c0;
+        o[i][2] *= c1;
+        o[i][3] *= c1;
+      }
+      uint32_t pa[4];
+      pa[0] = pack_bf16(pr[0][0], pr[0][1]);
+      pa[1] = pack_bf16(pr[0][2], pr[0][3]);
+      pa[2] = pack_bf16(pr[1][0], pr[1][1]);
+      pa[3] = pack_bf16(pr[1][2], pr[1][3]);
+      {
+        const int mi = lane >> 3, ri = lane & 7;
+        const int tok = (mi & 1) * 8 + ri;
+#pragma unroll
+        for (int np = 0; np < 8; ++np) {
+          uint32_t b0, b1, b2, b3;
+          ldmatrix_x4_trans(vt + swz256(tok, 2 * np + (mi >> 1)), b0, b1, b2, b3);
+          mma_bf16_16816(o[2 * np], pa, b0, b1);
+          mma_bf16_16816(o[2 * np + 1], pa, b2, b3);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (!active) return;
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
+  const int ta = wt0 + (lane >> 2), tb = ta + 8;
+  const int cb = (lane & 3) * 2;
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    if (ta < p.T)
+      *reinterpret_cast<__nv_bfloat162*>(p.out + ((int64_t)ta * p.nq + qh) * HD + nt * 8 + cb) =
+          __floats2bfloat162_rn(o[nt][0] * i0, o[nt][1] * i0);
+    if (tb < p.T)
+      *reinterpret_cast<__nv_bfloat162*>(p.out + ((int64_t)tb * p.nq + qh) * HD + nt * 8 + cb) =
+          __floats2bfloat162_rn(o[nt][2] * i1, o[nt][3] * i1);
+  }
+}
+
+}  // namespace pre
+}  // namespace psk
+
+extern "C" {
+
+int psk_embed_tokens(const int32_t* tokens, int32_t T, const void* table, int32_t d, float* h,
+                     void* stream) {
+  PSK_CHECK_ARG(tokens && table && h && d % 8 == 0 && T >= 0, "psk_embed_tokens: bad args");
+  if (T == 0) return PSK_OK;
+  psk::pre::embed_tokens_kernel<<<T, 128, 0, psk::as_stream(stream)>>>(
+      tokens, reinterpret_cast<const __nv_bfloat16*>(table), d, h);
+  PSK_LAUNCH_CHECK();
+  return PSK_OK;
+}
+
+int psk_prefill_attn(const void* q_rot, int32_t T, int32_t pos0, int32_t n_q_heads, psk_kv_layout kv,
+                     int32_t layer, const int32_t* page_table, void* out, void* stream) {
+  using namespace psk::pre;
+  PSK_CHECK_ARG(q_rot && page_table && out && kv.head_dim == HD && kv.page_tokens == PT &&
+                    n_q_heads % kv.n_kv_heads == 0,
+                "psk_prefill_attn: bad args");
+  const int grp = n_q_heads / kv.n_kv_heads;
+  PSK_CHECK_ARG(grp >= 1 && grp <= WARPS && WARPS % grp == 0, "psk_prefill_attn: GQA group %d", grp);
+  if (T == 0) return PSK_OK;
+  Params p;
+  p.q = reinterpret_cast<const __nv_bfloat16*>(q_rot);
+  p.out = reinterpret_cast<__nv_bfloat16*>(out);
+  p.kv = kv;
+  p.pages = page_table;
+  p.T = T;
+  p.pos0 = pos0;
+  p.nq = n_q_heads;
+  p.grp = grp;
+  p.layer = layer;
+  p.qb = 16 * (WARPS / grp);
+  p.n_qblocks = (T + p.qb - 1) / p.qb;
+  p.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
+  static bool attr = false;
+  if (!attr) {
+    PSK_CUDA_TRY(cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM));
+    attr = true;
+  }
+  prefill_attn_kernel<<<p.n_qblocks * kv.n_kv_heads, THREADS, SMEM, psk::as_stream(stream)>>>(p);
+  PSK_LAUNCH_CHECK();
+  return PSK_OK;
+}
+
+}  // extern "C"

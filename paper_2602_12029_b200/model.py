@@ -401,3 +401,75 @@ class DecodeRunner:
         inv = torch.empty_like(self.out_tokens)
         inv[torch.tensor(self.b.order, device=self.out_tokens.device)] = self.out_tokens
         return inv
+
+
+class PrefillRunner:
+    """The frozen prefill module: buildBaseCache (model.ts:340-352) on B200.
+
+    Forwards the new prompt tokens [pos0, pos0+T) through all layers and
+    leaves their K/V in the paged cache (fused into the QKV GEMM epilogue).
+    No final norm / LM head: the prefill module's own next token is never
+    used ((., C_base) = F(X, 0), PAPER.md:152-155).
+    Per layer: RMSNorm -> QKV GEMM (+RoPE, paged KV write) -> causal paged
+    attention -> O GEMM (+residual) -> RMSNorm -> gate/up GEMM (+SiLU*mul)
+    -> down GEMM (+residual).
+    """
+
+    def __init__(self, cfg: LlamaConfig, weights: ModuleWeights, kv: KVCache, max_tokens: int,
+                 device: int = 0):
+        self.cfg, self.w, self.kv = cfg, weights, kv
+        self.lib = _lib.load()
+        dev = torch.device("cuda", device)
+        d = cfg.d_model
+        self.max_tokens = max_tokens
+        f32, bf = torch.float32, torch.bfloat16
+        self.h = torch.empty(max_tokens, d, dtype=f32, device=dev)
+        self.xn = torch.empty(max_tokens, d, dtype=bf, device=dev)
+        self.q = torch.empty(max_tokens, cfg.n_heads, cfg.head_dim, dtype=bf, device=dev)
+        self.attn = torch.empty(max_tokens, cfg.n_heads * cfg.head_dim, dtype=bf, device=dev)
+        self.act = torch.empty(max_tokens, cfg.ffn, dtype=bf, device=dev)
+        self.rope = torch.from_numpy(rope_table(cfg)).to(dev)
+        self.gamma_ptrs = [
+            (torch.tensor([weights.attn_norm[l].data_ptr()], dtype=torch.int64, device=dev),
+             torch.tensor([weights.mlp_norm[l].data_ptr()], dtype=torch.int64, device=dev))
+            for l in range(cfg.n_layers)]
+        self.launches_per_call = 1 + 7 * cfg.n_layers
+
+    def flops(self, T: int, pos0: int = 0) -> float:
+        """Algorithmic FLOPs of one call (GEMMs + causal attention)."""
+        c = self.cfg
+        gemm = 2.0 * T * c.n_layers * (c.qkv_dim * c.d_model + c.d_model * c.n_heads * c.head_dim +
+                                       3 * c.ffn * c.d_model)
+        # causal: query i (absolute pos0+i) sees pos0+i+1 keys
+        keys = T * pos0 + T * (T + 1) / 2.0
+        attn = 4.0 * c.n_layers * c.n_heads * c.head_dim * keys
+        return gemm + attn
+
+    def run(self, tokens: torch.Tensor, pos0: int, page_table: torch.Tensor, stream: int | None = None) -> None:
+        """tokens: int32 device [T]; page_table: int32 device covering
+        positions [0, pos0+T)."""
+        cfg, lib, w = self.cfg, self.lib, self.w
+        T = int(tokens.shape[0])
+        if T > self.max_tokens:
+            raise ValueError(f"prefill of {T} tokens exceeds max_tokens {self.max_tokens}")
+        if pos0 + T > cfg.max_pos:
+            raise ValueError(f"sequence length {pos0 + T} exceeds max_pos {cfg.max_pos}")
+        s = stream if stream is not None else _stream()
+        chk = _lib.check
+        d = cfg.d_model
+        kvl = self.kv.layout()
+        pt = _ptr(page_table)
+        eps = C.c_float(cfg.norm_eps)
+        chk(lib.psk_embed_tokens(_ptr(tokens), T, _ptr(w.embed), d, _ptr(self.h), s))
+        for l in range(cfg.n_layers):
+            g1, g2 = self.gamma_ptrs[l]
+            chk(lib.psk_rmsnorm_rows(_ptr(self.h), T, d, _ptr(g1), None, eps, _ptr(self.xn), s))
+            chk(lib.psk_gemm_qkv_rope_kv(_ptr(self.xn), _ptr(w.wqkv[l]), T, d, cfg.n_heads,
+                                         _ptr(self.rope), pos0, kvl, l, pt, _ptr(self.q), s))
+            chk(lib.psk_prefill_attn(_ptr(self.q), T, pos0, cfg.n_heads, kvl, l, pt, _ptr(self.attn), s))
+            chk(lib.psk_gemm(_ptr(self.attn), _ptr(w.wo[l]), T, d, cfg.n_heads * cfg.head_dim, 2,
+                             _ptr(self.h), d, s))
+            chk(lib.psk_rmsnorm_rows(_ptr(self.h), T, d, _ptr(g2), None, eps, _ptr(self.xn), s))
+            chk(lib.psk_gemm(_ptr(self.xn), _ptr(w.wgu[l]), T, 2 * cfg.ffn, d, 3, _ptr(self.act),
+                             cfg.ffn, s))
+            chk(lib.psk_gemm(_ptr(self.act), _ptr(w.wdown[l]), T, d, cfg.ffn, 2, _ptr(self.h), d, s))
