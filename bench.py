@@ -1,0 +1,419 @@
+"""PrefillShare hot-path benchmark (BASELINE.json configs[1]).
+
+Workload (N=1): Llama-3.1-8B-shape frozen prefill module + 4 decode modules
+(random init, bf16) on one B200. One step = one serve() of a batch of
+--sessions sessions, each a fresh synthetic 4096-token prompt: GPU block-pool
+lookup/insert (K7), shared prefill of the prompt (K1-K3), then every decode
+module generates 256 tokens greedily from the shared KV (K5/K6). A request =
+one decode module's 256-token generation on one session.
+
+  value : req/s with prompts resident in HBM (device tokens), CUDA events.
+  e2e   : req/s through PrefillShareEngine.serve() with HOST prompts
+          (pinned H2D of the token ids and D2H of the generated ids inside
+          the timed region).
+  roofline : the dominant kernel (decode GEMV, weight streaming) timed live
+          with CUDA events on its launch stream; plus decode attention (K6)
+          at the config-2 and config-4 (32k x 16 modules) shapes and the
+          prefill (tcgen05) TFLOP/s.
+  cpu_baseline : the fp32 CPU oracle on a bounded sample of the same
+          workload (1 of 32 layers, 3 decode steps), scaled to req/s.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Under torchrun each rank serves its own batch (weak scaling, no data-path
+collective); timing is max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PROMPT = 4096
+MAX_NEW = 256
+N_MOD = 4
+METRIC = "multi-model agent req/s (8B-shape shared prefill + 4 decode modules, 4k prompt, 256 out)"
+
+
+def _peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm": d["hbm_gbs"], "bf16": d["bf16_tflops"], "bf16_sus": d["bf16_tflops_sustained"],
+                "src": "measured"}
+    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
+
+
+# --------------------------------------------------------------- clocks ----
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ CPU oracle ---
+
+def cpu_reference_sample(n_sessions: int = 1) -> dict:
+    """Time the fp32 CPU oracle (oracle/model.py, the reference path restated)
+    on a bounded sample of the same workload and scale it to req/s:
+    1 full-width layer of the 4096-token prefill + 3 single-token decode
+    steps of 1 layer with the 4095-token shared KV (per module) + a 16384-row
+    slice of the LM head; the per-request time is
+    32*prefill_layer/4 + 256*(32*decode_layer + head)."""
+    import torch
+    from oracle.model import LlamaOracle
+    from paper_2602_12029_b200.model import LlamaConfig
+
+    torch.manual_seed(0)
+    full = LlamaConfig.llama8b()
+    cfg = LlamaConfig(n_layers=1, d_model=full.d_model, n_heads=full.n_heads,
+                      n_kv_heads=full.n_kv_heads, ffn=full.ffn, vocab=4096,
+                      rope_theta=full.rope_theta, max_pos=PROMPT + MAX_NEW)
+    d, f, hd = cfg.d_model, cfg.ffn, cfg.head_dim
+    r = lambda *s: torch.randn(*s) * 0.02  # noqa: E731
+    lw = {"attn_norm": torch.ones(d), "wq": r(cfg.n_heads * hd, d), "wk": r(cfg.n_kv_heads * hd, d),
+          "wv": r(cfg.n_kv_heads * hd, d), "wo": r(d, cfg.n_heads * hd), "mlp_norm": torch.ones(d),
+          "w_gate": r(f, d), "w_up": r(f, d), "w_down": r(d, f)}
+    w = {"embed": r(4096, d), "final_norm": torch.ones(d), "head": r(4096, d), "layers": [lw]}
+    o = LlamaOracle(cfg, w)
+    prompt = torch.randint(0, 4096, (PROMPT,)).tolist()
+    with torch.no_grad():
+        t0 = time.perf_counter()
+        kv = o.forward(prompt[:-1], None, with_logits=False)[1]
+        t_pre = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        cache = kv
+        for i in range(3):
+            _, cache = o.forward([prompt[-1] if i == 0 else 7], cache, with_logits=False)
+        t_dec = (time.perf_counter() - t0) / 3
+        head = r(16384, d)
+        x = torch.randn(1, d)
+        t0 = time.perf_counter()
+        for _ in range(3):
+            _ = x @ head.T
+        t_head = (time.perf_counter() - t0) / 3 * (full.vocab / 16384)
+    per_session = full.n_layers * t_pre + MAX_NEW * N_MOD * (full.n_layers * t_dec + t_head)
+    reqs = n_sessions * N_MOD
+    value = reqs / (n_sessions * per_session)
+    return {"value": value, "unit": "req/s", "cores": torch.get_num_threads(), "kind": "port",
+            "sample": (f"fp32 CPU oracle: 1 of 32 layers at full 8B width (4096-token prefill "
+                       f"{t_pre:.2f}s, decode layer-step {t_dec * 1e3:.1f}ms x {N_MOD} modules, LM head "
+                       f"{t_head * 1e3:.1f}ms/step), scaled to 32 layers x 256 tokens"),
+            "sample_seconds": t_pre + 3 * t_dec + 3 * t_head / (full.vocab / 16384)}
+
+
+# --------------------------------------------------------- kernel timing ---
+
+def _time_launches(fn, n: int) -> float:
+    import torch
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        fn()
+    st.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(n):
+        fn()
+    b.record(st)
+    b.synchronize()
+    return a.elapsed_time(b) / 1e3 / n
+
+
+def gemv_roofline(eng, peaks) -> dict:
+    """Dominant kernel: the grouped gate/up GEMV (4 modules x 235 MB weights
+    per launch), timed back-to-back over the 32 layers' weights (working set
+    7.5 GB >> L2)."""
+    import torch
+    from paper_2602_12029_b200 import _lib
+    r = eng.runner
+    lib, cfg, b = r.lib, eng.cfg, eng.batch
+    s = torch.cuda.current_stream().cuda_stream
+    it = [0]
+
+    def launch():
+        l = it[0] % cfg.n_layers
+        it[0] += 1
+        _lib.check(lib.psk_gemv(r.xn.data_ptr(), b.n_rows, cfg.d_model, r.p_wgu[l].data_ptr(),
+                                b.t_mrs.data_ptr(), b.n_mod, 2 * cfg.ffn, 3, r.act.data_ptr(), s))
+    dt = _time_launches(launch, 4 * cfg.n_layers)
+    nbytes = b.n_mod * 2 * cfg.ffn * cfg.d_model * 2 + b.n_rows * (cfg.d_model + cfg.ffn) * 2
+    gbs = nbytes / dt / 1e9
+    return {"bound": "hbm", "kernel": "psk_gemv (gate/up, SiLU*mul epilogue)", "achieved": round(gbs, 1),
+            "peak": peaks["hbm"], "unit": "GB/s", "frac": round(gbs / peaks["hbm"], 4),
+            "traffic": None, "bytes_per_launch": nbytes, "us_per_launch": round(dt * 1e6, 2),
+            "peak_source": peaks["src"]}
+
+
+def decode_attn_roofline(eng, peaks) -> dict:
+    """K6 on the engine's live batch (shared 4095-token prefix, 4 modules),
+    cycling the 32 layers (512 MiB of KV, > L2)."""
+    import torch
+    from paper_2602_12029_b200 import _lib
+    r = eng.runner
+    cfg, b = eng.cfg, eng.batch
+    kvl = eng.kv.layout()
+    s = torch.cuda.current_stream().cuda_stream
+    b.t_priv_len.fill_(MAX_NEW - 1)  # state of the last decode step
+    it = [0]
+
+    def launch():
+        l = it[0] % cfg.n_layers
+        it[0] += 1
+        _lib.check(r.lib.psk_decode_attn(b.c_ref(), r.q_rot.data_ptr(), cfg.n_heads, l, kvl,
+                                         r.ns_shared, r.ns_priv, r.ws.data_ptr(), r.attn.data_ptr(), s))
+    dt = _time_launches(launch, 4 * cfg.n_layers)
+    shared = int(b.t_sess_len.sum().item())
+    priv = int((b.t_priv_len + 1).sum().item())
+    per_tok = 2 * cfg.n_kv_heads * cfg.head_dim * 2
+    nbytes = (shared + priv) * per_tok + 2 * b.n_rows * cfg.n_heads * cfg.head_dim * 2
+    gbs = nbytes / dt / 1e9
+    return {"shape": f"{b.n_sess} session(s) x {shared // max(1, b.n_sess)} shared tokens, {b.n_rows} rows",
+            "achieved": round(gbs, 1), "unit": "GB/s", "frac": round(gbs / peaks["hbm"], 4),
+            "bytes_per_launch": nbytes, "us_per_launch": round(dt * 1e6, 2)}
+
+
+def decode_attn_fanout(peaks, shared_tokens=32767, modules=16) -> dict:
+    """K6 at the config-4 fan-out shape: one 32k-token shared context read by
+    16 decode modules (64 query heads per KV head), random KV / queries,
+    32 layers cycled (4 GiB working set)."""
+    import torch
+    from paper_2602_12029_b200 import _lib
+    from paper_2602_12029_b200.model import (DecodeBatch, DecodeRow, KVCache, LlamaConfig,
+                                             SessionSpec)
+    cfg = LlamaConfig.llama8b(max_pos=shared_tokens + 64)
+    n_sh = (shared_tokens + 15) // 16
+    kv = KVCache(cfg, n_sh + modules)
+    lib = _lib.load()
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.psk_init_normal_bf16(kv.data.data_ptr(), kv.data.numel(), 99, 1.0, s))
+    rows = [DecodeRow(module=m, session=0, first_token=0, pages=[n_sh + m]) for m in range(modules)]
+    b = DecodeBatch([SessionSpec(shared_len=shared_tokens, pages=list(range(n_sh)))], rows, modules)
+    q = torch.randn(modules, cfg.n_heads, cfg.head_dim, device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(q)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    nss = max(1, 2 * sms // cfg.n_kv_heads)
+    ws = torch.empty(1, dtype=torch.int64)
+    wsb = __import__("ctypes").c_int64()
+    _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), cfg.n_kv_heads, 128, nss, 1,
+                                             __import__("ctypes").byref(wsb)))
+    ws = torch.empty(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
+    it = [0]
+    kvl = kv.layout()
+
+    def launch():
+        l = it[0] % cfg.n_layers
+        it[0] += 1
+        _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), cfg.n_heads, l, kvl, nss, 1,
+                                       ws.data_ptr(), out.data_ptr(), s))
+    dt = _time_launches(launch, 2 * cfg.n_layers)
+    per_tok = 2 * cfg.n_kv_heads * cfg.head_dim * 2
+    nbytes = (shared_tokens + modules) * per_tok + 2 * modules * cfg.n_heads * cfg.head_dim * 2
+    gbs = nbytes / dt / 1e9
+    del kv
+    torch.cuda.empty_cache()
+    return {"shape": f"1 session x {shared_tokens} shared tokens, {modules} modules",
+            "achieved": round(gbs, 1), "unit": "GB/s", "frac": round(gbs / peaks["hbm"], 4),
+            "bytes_per_launch": nbytes, "us_per_launch": round(dt * 1e6, 2),
+            "per_model_reread_bytes": modules * shared_tokens * per_tok}
+
+
+def prefill_roofline(eng, peaks) -> dict:
+    import torch
+    T = PROMPT
+    toks = torch.randint(0, eng.cfg.vocab, (T,), device="cuda", dtype=torch.int64)
+    pt = torch.arange(eng.pool_pages - (T + 15) // 16, eng.pool_pages, dtype=torch.int32, device="cuda")
+    dt = _time_launches(lambda: eng.prefill.run(toks, 0, pt), 3)
+    fl = eng.prefill.flops(T)
+    tf = fl / dt / 1e12
+    return {"bound": "tensor", "tokens": T, "achieved": round(tf, 1), "unit": "TFLOP/s",
+            "peak": peaks["bf16_sus"], "frac": round(tf / peaks["bf16_sus"], 4),
+            "ms_per_prefill": round(dt * 1e3, 2)}
+
+
+# ----------------------------------------------------------------- main ----
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sessions", type=int, default=1, help="sessions per serve() batch")
+    ap.add_argument("--no-extras", action="store_true", help="skip kernel rooflines / cpu baseline")
+    a = ap.parse_args()
+    a.warmup = max(3, a.warmup)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": "configs[1]: Llama-3.1-8B-shape shared prefill + 4 decode modules, "
+                          "4k-token shared prompt, 256 output tokens",
+              "model": "llama-3.1-8b-shape (random init)", "sessions_per_step": a.sessions,
+              "prompt_tokens": PROMPT, "output_tokens": MAX_NEW, "decode_modules": N_MOD,
+              "l2": "inputs larger than L2 (60 GB of decode weights streamed per token step)"}
+
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        samples = [cpu_reference_sample(a.sessions) for _ in range(a.warmup + a.steps)][a.warmup:]
+        v = statistics.median(s["value"] for s in samples)
+        cb = dict(samples[-1])
+        cb["value"] = v
+        cb.pop("sample_seconds", None)
+        print(json.dumps({"metric": METRIC, "value": v, "unit": "req/s", "impl": "reference",
+                          "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                          "dtype": "f32", "data": "synthetic", "config": config, "cpu_baseline": cb,
+                          "e2e": {"value": v, "unit": "req/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2602_12029_b200.engine import PrefillShareEngine
+    from paper_2602_12029_b200.model import LlamaConfig
+    peaks = _peaks()
+    cfg = LlamaConfig.llama8b(max_pos=PROMPT + MAX_NEW + 64)
+    S = a.sessions
+    steps_total = a.warmup + 2 * a.steps
+    pool_pages = max(2048, (steps_total + 2) * S * (PROMPT // 16 + 1))
+    eng = PrefillShareEngine(cfg, N_MOD, S, PROMPT, MAX_NEW, pool_pages=pool_pages,
+                             seed=1000 * rank + 1, device=local)
+    rng = np.random.default_rng(1234 + rank)
+    batches = [[rng.integers(0, cfg.vocab, PROMPT, dtype=np.int64) for _ in range(S)]
+               for _ in range(steps_total)]
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    eng.capture()
+    for i in range(a.warmup):
+        eng.serve(batches[i])
+    # ---- value: prompts resident in HBM
+    dev_batches = []
+    for j in range(a.steps):
+        t = torch.zeros(S, PROMPT, dtype=torch.int64, device="cuda")
+        for s in range(S):
+            t[s] = torch.from_numpy(batches[a.warmup + j][s]).cuda()
+        dev_batches.append(t)
+    st = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+    barrier()
+    with ClockSampler(local) as clk:
+        ev[0].record(st)
+        for j in range(a.steps):
+            eng.serve(batches[a.warmup + j], device_tokens=dev_batches[j])
+            ev[j + 1].record(st)
+        ev[-1].synchronize()
+    barrier()
+    step_s = [ev[j].elapsed_time(ev[j + 1]) / 1e3 for j in range(a.steps)]
+    t_val = max_over_ranks(sum(step_s))
+    # ---- e2e: host prompts through the public API
+    ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+    barrier()
+    ev2[0].record(st)
+    for j in range(a.steps):
+        eng.serve(batches[a.warmup + a.steps + j])
+        ev2[j + 1].record(st)
+    ev2[-1].synchronize()
+    barrier()
+    e2e_steps = [ev2[j].elapsed_time(ev2[j + 1]) / 1e3 for j in range(a.steps)]
+    t_e2e = max_over_ranks(sum(e2e_steps))
+    reqs = S * N_MOD * a.steps * world
+    value = reqs / t_val
+    e2e = reqs / t_e2e
+    # per-request latency = its serve() duration (all modules finish together)
+    lat = sorted(step_s)
+    p95 = lat[min(len(lat) - 1, max(0, int(np.ceil(0.95 * len(lat))) - 1))]
+    out = {"metric": METRIC, "value": round(value, 4), "unit": "req/s", "n_gpus": world,
+           "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(t_val / a.steps * 1e3, 2),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic (random-init weights, random prompt ids)", "config": config,
+           "p95_latency_ms": round(p95 * 1e3, 2),
+           "e2e": {"value": round(e2e, 4), "unit": "req/s", "h2d_bytes_per_step": S * PROMPT * 8,
+                   "d2h_bytes_per_step": S * N_MOD * MAX_NEW * 4,
+                   "p95_latency_ms": round(sorted(e2e_steps)[-1] * 1e3, 2)},
+           "gpu_launches": eng.launches_per_serve(S, S) * a.steps,
+           "clocks": clk.summary()}
+    if not a.no_extras and rank == 0:
+        out["roofline"] = gemv_roofline(eng, peaks)
+        out["decode_attn"] = decode_attn_roofline(eng, peaks)
+        out["prefill"] = prefill_roofline(eng, peaks)
+        step_bytes = eng.runner.weight_bytes_per_step
+        out["decode_step"] = {"weight_bytes": step_bytes}
+        del eng
+        torch.cuda.empty_cache()
+        out["decode_attn_fanout_32k_x16"] = decode_attn_fanout(peaks)
+        if world == 1:
+            out["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(S).items()
+                                   if k != "sample_seconds"}
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -236,7 +236,7 @@ int psk_gemm_qkv_rope_kv(const void* A, const void* Wqkv, int32_t T, int32_t K, 
 int psk_prefill_attn(const void* q_rot, int32_t T, int32_t pos0, int32_t n_q_heads, psk_kv_layout kv,
                      int32_t layer, const int32_t* page_table, void* out, void* stream);
 /* h[t,:] = table[tokens[t],:] (fp32). model.ts:276-284 (token embedding). */
-int psk_embed_tokens(const int32_t* tokens, int32_t T, const void* table, int32_t d, float* h,
+int psk_embed_tokens(const int64_t* tokens, int32_t T, const void* table, int32_t d, float* h,
                      void* stream);
 
 #if defined(__GNUC__)

@@ -27,7 +27,7 @@ constexpr int TILE = PT * HD * 2;
 constexpr int STAGE = RP * 2 * TILE;
 constexpr int SMEM = NST * STAGE;  // 96 KiB
 
-__global__ void embed_tokens_kernel(const int32_t* __restrict__ tokens,
+__global__ void embed_tokens_kernel(const int64_t* __restrict__ tokens,
                                     const __nv_bfloat16* __restrict__ table, int d,
                                     float* __restrict__ h) {
   const int t = blockIdx.x;
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(THREADS, 2) prefill_attn_kernel(Params p) {
 
 extern "C" {
 
-int psk_embed_tokens(const int32_t* tokens, int32_t T, const void* table, int32_t d, float* h,
+int psk_embed_tokens(const int64_t* tokens, int32_t T, const void* table, int32_t d, float* h,
                      void* stream) {
   PSK_CHECK_ARG(tokens && table && h && d % 8 == 0 && T >= 0, "psk_embed_tokens: bad args");
   if (T == 0) return PSK_OK;

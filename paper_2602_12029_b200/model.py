@@ -280,9 +280,28 @@ class DecodeBatch:
             _ptr(self.t_sess_pages), msp, _ptr(self.t_row_pages), mrp,
             _ptr(self.t_priv_len), _ptr(self.t_tokens))
 
+        self.max_sess_pages = msp
+        self._first = [r.first_token for r in self.rows]
+
+    def c_ref(self):
+        return C.byref(self.c)
+
     def reset(self) -> None:
         self.t_priv_len.zero_()
-        self.t_tokens.copy_(torch.tensor([r.first_token for r in self.rows], dtype=torch.int32))
+        self.t_tokens.copy_(torch.tensor(self._first, dtype=torch.int32))
+
+    def update_sessions(self, shared_lens: list[int], pages: list[list[int]],
+                        first_tokens: list[int]) -> None:
+        """Point the batch at new sessions in place (same device addresses, so
+        a captured decode graph stays valid). first_tokens: per session (the
+        session's last prompt token, which every module processes itself)."""
+        msp = self.max_sess_pages
+        if any(len(p) > msp for p in pages):
+            raise ValueError("session page table exceeds the batch's capacity")
+        self.t_sess_len.copy_(torch.tensor(shared_lens, dtype=torch.int32))
+        self.t_sess_pages.copy_(torch.tensor([p + [0] * (msp - len(p)) for p in pages], dtype=torch.int32))
+        self._first = [first_tokens[r.session] for r in self.rows]
+        self.reset()
 
 
 class DecodeRunner:
@@ -446,8 +465,8 @@ class PrefillRunner:
         return gemm + attn
 
     def run(self, tokens: torch.Tensor, pos0: int, page_table: torch.Tensor, stream: int | None = None) -> None:
-        """tokens: int32 device [T]; page_table: int32 device covering
-        positions [0, pos0+T)."""
+        """tokens: int64 device [T] (the same ids the block pool hashes);
+        page_table: int32 device covering positions [0, pos0+T)."""
         cfg, lib, w = self.cfg, self.lib, self.w
         T = int(tokens.shape[0])
         if T > self.max_tokens:

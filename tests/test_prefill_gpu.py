@@ -43,7 +43,7 @@ def test_prefill_kv_matches_oracle(shape, n):
     pages = list(np.random.default_rng(1).permutation(n_pages + 3)[:n_pages])
     kv = KVCache(cfg, n_pages + 3)
     pre = PrefillRunner(cfg, base, kv, max_tokens=n)
-    pre.run(torch.tensor(prompt, dtype=torch.int32, device="cuda"), 0,
+    pre.run(torch.tensor(prompt, dtype=torch.int64, device="cuda"), 0,
             torch.tensor(pages, dtype=torch.int32, device="cuda"))
     torch.cuda.synchronize()
     _check_kv(kv, pages, cfg, base_o.prefill(prompt), n)
@@ -60,8 +60,8 @@ def test_partial_prefill_after_prefix_hit():
     kv = KVCache(cfg, 16)
     pre = PrefillRunner(cfg, base, kv, max_tokens=150)
     pt = torch.tensor(pages, dtype=torch.int32, device="cuda")
-    pre.run(torch.tensor(prompt[:64], dtype=torch.int32, device="cuda"), 0, pt)
-    pre.run(torch.tensor(prompt[64:], dtype=torch.int32, device="cuda"), 64, pt)
+    pre.run(torch.tensor(prompt[:64], dtype=torch.int64, device="cuda"), 0, pt)
+    pre.run(torch.tensor(prompt[64:], dtype=torch.int64, device="cuda"), 64, pt)
     torch.cuda.synchronize()
     _check_kv(kv, pages, cfg, base_o.prefill(prompt), 150)
 
@@ -83,7 +83,7 @@ def test_shared_prefill_then_decode_modules(shape):
     kv = KVCache(cfg, n_pages + n_mod * priv)
     pages = list(range(n_pages))
     pre = PrefillRunner(cfg, base, kv, max_tokens=n)
-    pre.run(torch.tensor(prompt, dtype=torch.int32, device="cuda"), 0,
+    pre.run(torch.tensor(prompt, dtype=torch.int64, device="cuda"), 0,
             torch.tensor(pages, dtype=torch.int32, device="cuda"))
     rows = [DecodeRow(module=m, session=0, first_token=prompt[-1],
                       pages=list(range(n_pages + m * priv, n_pages + (m + 1) * priv)))
