@@ -1,0 +1,66 @@
+"""Drive each hot kernel a few times at the bench shapes, for ncu.
+
+    ncu --set full -k regex:<kernel> -c 2 python tools/profile_kernels.py <which>
+which: gemv | attn4k | attn32k | gemm | prefill_attn | all
+"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import ctypes as C  # noqa: E402
+
+import torch  # noqa: E402
+
+from paper_2602_12029_b200 import _lib  # noqa: E402
+from paper_2602_12029_b200.model import (DecodeBatch, DecodeRow, KVCache, LlamaConfig,  # noqa: E402
+                                         ModuleWeights, PrefillRunner, SessionSpec)
+
+which = sys.argv[1] if len(sys.argv) > 1 else "all"
+lib = _lib.load()
+s = torch.cuda.current_stream().cuda_stream
+cfg = LlamaConfig.llama8b(n_layers=2, max_pos=32768 + 512)
+
+
+def attn(shared, modules, reps=4):
+    n_sh = (shared + 15) // 16
+    kv = KVCache(cfg, n_sh + modules)
+    _lib.check(lib.psk_init_normal_bf16(kv.data.data_ptr(), kv.data.numel(), 7, 1.0, s))
+    rows = [DecodeRow(module=m, session=0, first_token=0, pages=[n_sh + m]) for m in range(modules)]
+    b = DecodeBatch([SessionSpec(shared_len=shared, pages=list(range(n_sh)))], rows, modules)
+    q = torch.randn(modules, 32, 128, device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(q)
+    nss = max(1, 2 * 148 // 8)
+    wsb = C.c_int64()
+    _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), 8, 128, nss, 1, C.byref(wsb)))
+    ws = torch.empty(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
+    for i in range(reps):
+        _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), 32, i % 2, kv.layout(), nss, 1,
+                                       ws.data_ptr(), out.data_ptr(), s))
+    torch.cuda.synchronize()
+
+
+if which in ("attn4k", "all"):
+    attn(4095, 4)
+if which in ("attn32k", "all"):
+    attn(32767, 16)
+if which in ("gemv", "all"):
+    mods = [ModuleWeights(cfg, 10 + i) for i in range(4)]
+    x = torch.randn(4, cfg.d_model, device="cuda").to(torch.bfloat16)
+    act = torch.empty(4, cfg.ffn, dtype=torch.bfloat16, device="cuda")
+    p = torch.tensor([m.wgu[0].data_ptr() for m in mods], dtype=torch.int64, device="cuda")
+    mrs = torch.tensor([0, 1, 2, 3, 4], dtype=torch.int32, device="cuda")
+    for _ in range(4):
+        _lib.check(lib.psk_gemv(x.data_ptr(), 4, cfg.d_model, p.data_ptr(), mrs.data_ptr(), 4,
+                                2 * cfg.ffn, 3, act.data_ptr(), s))
+    torch.cuda.synchronize()
+if which in ("gemm", "prefill_attn", "all"):
+    base = ModuleWeights(cfg, 3, with_head=False)
+    kv = KVCache(cfg, 300)
+    pre = PrefillRunner(cfg, base, kv, max_tokens=4096)
+    toks = torch.randint(0, cfg.vocab, (4096,), device="cuda")
+    pt = torch.arange(256, dtype=torch.int32, device="cuda")
+    for _ in range(2):
+        pre.run(toks, 0, pt)
+    torch.cuda.synchronize()
+print("done", which)
