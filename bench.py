@@ -209,7 +209,7 @@ def decode_attn_roofline(eng, peaks) -> dict:
         l = it[0] % cfg.n_layers
         it[0] += 1
         _lib.check(r.lib.psk_decode_attn(b.c_ref(), r.q_rot.data_ptr(), cfg.n_heads, l, kvl,
-                                         r.ns_shared, r.ns_priv, r.ws.data_ptr(), r.attn.data_ptr(), s))
+                                         r.cluster, r.attn.data_ptr(), s))
     dt = _time_launches(launch, 4 * cfg.n_layers)
     shared = int(b.t_sess_len.sum().item())
     priv = int((b.t_priv_len + 1).sum().item())
@@ -239,21 +239,16 @@ def decode_attn_fanout(peaks, shared_tokens=32767, modules=16) -> dict:
     b = DecodeBatch([SessionSpec(shared_len=shared_tokens, pages=list(range(n_sh)))], rows, modules)
     q = torch.randn(modules, cfg.n_heads, cfg.head_dim, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)
-    sms = torch.cuda.get_device_properties(0).multi_processor_count
-    nss = max(1, 2 * sms // cfg.n_kv_heads)
-    ws = torch.empty(1, dtype=torch.int64)
-    wsb = __import__("ctypes").c_int64()
-    _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), cfg.n_kv_heads, 128, nss, 1,
-                                             __import__("ctypes").byref(wsb)))
-    ws = torch.empty(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
+    from paper_2602_12029_b200.model import attn_cluster_size
+    cl = attn_cluster_size(n_sh, cfg.n_kv_heads)
     it = [0]
     kvl = kv.layout()
 
     def launch():
         l = it[0] % cfg.n_layers
         it[0] += 1
-        _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), cfg.n_heads, l, kvl, nss, 1,
-                                       ws.data_ptr(), out.data_ptr(), s))
+        _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), cfg.n_heads, l, kvl, cl,
+                                       out.data_ptr(), s))
     dt = _time_launches(launch, 2 * cfg.n_layers)
     per_tok = 2 * cfg.n_kv_heads * cfg.head_dim * 2
     nbytes = (shared_tokens + modules) * per_tok + 2 * modules * cfg.n_heads * cfg.head_dim * 2

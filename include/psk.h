@@ -133,6 +133,7 @@ typedef struct psk_kv_layout {
   int32_t n_kv_heads;
   int32_t head_dim;      /* 128 */
   int32_t page_tokens;   /* 16  */
+  int64_t n_pages;       /* pages in `base` (bounds TMA tensor maps)        */
 } psk_kv_layout;
 
 /* A batch of decode rows. Row r = (decode module row_mod[r], session
@@ -193,17 +194,15 @@ int psk_rope_append(const psk_decode_batch* b, const float* qkv, int32_t n_q_hea
                     const float* rope, int32_t layer, psk_kv_layout kv, void* q_rot,
                     void* stream);
 
-/* K6: shared-prefix paged decode attention for one layer. Every KV page of
- * a session's shared prefix is streamed from HBM once per step for ALL of
- * the session's decode rows (modules) and their GQA query heads; each row's
- * private suffix (incl. the token appended this step) is a second pass; the
- * partials merge by log-sum-exp. out bf16 [n_rows][nq][hd]. workspace: see
- * psk_decode_attn_workspace. */
-int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int32_t head_dim,
-                              int32_t shared_splits, int32_t priv_splits, int64_t* bytes);
+/* K6: shared-prefix paged decode attention for one layer. One thread-block
+ * cluster of `cluster` (1,2,4,8,16) CTAs per (session, KV head) streams the
+ * session's shared prompt pages and its rows' private pages (including the
+ * token appended this step) from HBM once per step, for ALL of the
+ * session's decode rows (modules) and their GQA query heads, and reduces
+ * the split-KV partials through distributed shared memory.
+ * q_rot bf16 [n_rows][nq][hd] -> out bf16 [n_rows][nq][hd]. */
 int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_heads,
-                    int32_t layer, psk_kv_layout kv, int32_t shared_splits,
-                    int32_t priv_splits, void* workspace, void* out, void* stream);
+                    int32_t layer, psk_kv_layout kv, int32_t cluster, void* out, void* stream);
 
 /* Greedy step end: tokens[r] = argmax(logits[r]) (first max, as tf.argMax /
  * torch.argmax), out_tokens[r*max_new + priv_len[r]] = it (if in range),

@@ -10,7 +10,6 @@
 // KV is paged and appended in place, and one decode step of all co-batched
 // modules reads each shared prompt page once.
 #include "common.cuh"
-#include "mma.cuh"
 
 #include <math.h>
 
@@ -245,286 +244,6 @@ __global__ void rope_append_kernel(psk_decode_batch b, const float* __restrict__
   }
 }
 
-// ------------------------------------------------------ decode attention --
-// One CTA = (session | row, kv head, split). 4 warps. The CTA streams its
-// pages (K and V 4 KiB tiles) through a 3-stage cp.async ring of 4-page
-// rounds into XOR-swizzled shared memory; warps map to (query m-tile, page
-// subset) so every page is read from HBM once and consumed by all query
-// rows of the session: GQA group x co-batched decode modules, up to 64 rows.
-constexpr int AT_WARPS = 4;
-constexpr int AT_THREADS = AT_WARPS * 32;
-constexpr int AT_RP = 4;      // pages per round
-constexpr int AT_NST = 3;     // pipeline stages
-constexpr int AT_TILE = PT * HD * 2;  // bytes per K (or V) tile: 4 KiB
-constexpr int AT_STAGE = AT_RP * 2 * AT_TILE;
-constexpr int AT_SMEM = AT_NST * AT_STAGE;  // 96 KiB
-constexpr int AT_GMAX = 64;
-
-struct AttnParams {
-  psk_decode_batch b;
-  psk_kv_layout kv;
-  const __nv_bfloat16* q;  // [rows][nq][HD]
-  int nq, grp, layer;
-  int ns_shared, ns_priv;
-  int n_shared_items;
-  int gstride;   // query slots per item in the workspace
-  float* pm;     // [items][gstride]
-  float* pl;
-  float* po;     // [items][gstride][HD]
-  float scale_log2;
-};
-
-__global__ void __launch_bounds__(AT_THREADS, 2) decode_attn_partial_kernel(AttnParams p) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkv = p.kv.n_kv_heads;
-  int item = blockIdx.x;
-  bool shared_item = item < p.n_shared_items;
-  int h, j, L, G, ns;
-  const int32_t* table;
-  int sess = -1, row = -1;
-  if (shared_item) {
-    ns = p.ns_shared;
-    sess = item / (nkv * ns);
-    h = (item / ns) % nkv;
-    j = item % ns;
-    L = p.b.sess_len[sess];
-    G = p.b.sess_nrows[sess] * p.grp;
-    table = p.b.sess_pages + (int64_t)sess * p.b.max_sess_pages;
-  } else {
-    const int it = item - p.n_shared_items;
-    ns = p.ns_priv;
-    row = it / (nkv * ns);
-    h = (it / ns) % nkv;
-    j = it % ns;
-    L = p.b.priv_len[row] + 1;  // includes the token appended this step
-    G = p.grp;
-    table = p.b.row_pages + (int64_t)row * p.b.max_row_pages;
-  }
-  const int P = (L + PT - 1) / PT;
-  const int pb = (int)((int64_t)j * P / ns), pe = (int)((int64_t)(j + 1) * P / ns);
-  const int tiles = (G + 15) / 16;
-  const int ways = tiles <= 1 ? 4 : (tiles == 2 ? 2 : 1);
-  const int my_tile = warp / ways;
-  const int my_way = warp % ways;
-  const bool active = my_tile < tiles;
-
-  // -- query fragments for my m-tile (A operand, 8 k-steps)
-  uint32_t qa[8][4];
-  {
-    const int gA = my_tile * 16 + (lane >> 2), gB = gA + 8;
-    const int t2 = (lane & 3) * 2;
-    auto qrow = [&](int g) -> const __nv_bfloat16* {
-      if (!active || g >= G) return nullptr;
-      int qr, qh;
-      if (shared_item) {
-        qr = p.b.sess_rows[(int64_t)sess * p.b.max_rows_per_sess + g / p.grp];
-        qh = h * p.grp + g % p.grp;
-      } else {
-        qr = row;
-        qh = h * p.grp + g;
-      }
-      return p.q + ((int64_t)qr * p.nq + qh) * HD;
-    };
-    const __nv_bfloat16* qA = qrow(gA);
-    const __nv_bfloat16* qB = qrow(gB);
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      const int c0 = ks * 16 + t2, c1 = c0 + 8;
-      qa[ks][0] = qA ? *reinterpret_cast<const uint32_t*>(qA + c0) : 0u;
-      qa[ks][1] = qB ? *reinterpret_cast<const uint32_t*>(qB + c0) : 0u;
-      qa[ks][2] = qA ? *reinterpret_cast<const uint32_t*>(qA + c1) : 0u;
-      qa[ks][3] = qB ? *reinterpret_cast<const uint32_t*>(qB + c1) : 0u;
-    }
-  }
-
-  float o[16][4];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-
-  const int rounds = (pe - pb + AT_RP - 1) / AT_RP;
-  const uint32_t sbase = smem_u32(smem);
-  auto issue = [&](int rd) {
-    if (rd < rounds) {
-      const uint32_t st = sbase + (rd % AT_NST) * AT_STAGE;
-      for (int e = threadIdx.x; e < AT_RP * 2 * 256; e += AT_THREADS) {
-        const int pslot = e >> 9, kvsel = (e >> 8) & 1, ce = e & 255;
-        const int pg = pb + rd * AT_RP + pslot;
-        if (pg < pe) {
-          const int page = table[pg];
-          const __nv_bfloat16* src = kv_ptr(p.kv, page, p.layer, kvsel, h, 0);
-          const int tr = ce >> 4, c = ce & 15;
-          cp_async16(st + (pslot * 2 + kvsel) * AT_TILE + swz256(tr, c), src + tr * HD + c * 8);
-        }
-      }
-    }
-    cp_async_commit();
-  };
-
-#pragma unroll
-  for (int s = 0; s < AT_NST - 1; ++s) issue(s);
-
-  for (int rd = 0; rd < rounds; ++rd) {
-    cp_async_wait<AT_NST - 2>();
-    __syncthreads();
-    issue(rd + AT_NST - 1);
-    if (active) {
-      const uint32_t st = sbase + (rd % AT_NST) * AT_STAGE;
-      for (int pslot = my_way; pslot < AT_RP; pslot += ways) {
-        const int pg = pb + rd * AT_RP + pslot;
-        if (pg >= pe) break;
-        const uint32_t kt = st + (pslot * 2 + 0) * AT_TILE;
-        const uint32_t vt = st + (pslot * 2 + 1) * AT_TILE;
-        float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-        {
-          const int mi = lane >> 3, ri = lane & 7;
-          const int tok = (mi >> 1) * 8 + ri;
-#pragma unroll
-          for (int ks = 0; ks < 8; ++ks) {
-            uint32_t b0, b1, b2, b3;
-            ldmatrix_x4(kt + swz256(tok, 2 * ks + (mi & 1)), b0, b1, b2, b3);
-            mma_bf16_16816(s[0], qa[ks], b0, b1);
-            mma_bf16_16816(s[1], qa[ks], b2, b3);
-          }
-        }
-        // scale + mask (tokens past L in the last page)
-        const int tok0 = pg * PT;
-        const int cb = (lane & 3) * 2;
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int t = tok0 + nt * 8 + cb + (e & 1);
-            s[nt][e] = t < L ? s[nt][e] * p.scale_log2 : -INFINITY;
-          }
-        float mx0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
-        float mx1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-        const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
-        const float r0 = n0 == -INFINITY ? 0.f : n0, r1 = n1 == -INFINITY ? 0.f : n1;
-        const float c0 = exp2f(m0 - r0), c1 = exp2f(m1 - r1);
-        m0 = n0;
-        m1 = n1;
-        float pr[2][4];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          pr[nt][0] = exp2f(s[nt][0] - r0);
-          pr[nt][1] = exp2f(s[nt][1] - r0);
-          pr[nt][2] = exp2f(s[nt][2] - r1);
-          pr[nt][3] = exp2f(s[nt][3] - r1);
-        }
-        l0 = l0 * c0 + pr[0][0] + pr[0][1] + pr[1][0] + pr[1][1];
-        l1 = l1 * c1 + pr[0][2] + pr[0][3] + pr[1][2] + pr[1][3];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          o[i][0] *= c0;
-          o[i][1] *= c0;
-          o[i][2] *= c1;
-          o[i][3] *= c1;
-        }
-        uint32_t pa[4];
-        pa[0] = pack_bf16(pr[0][0], pr[0][1]);
-        pa[1] = pack_bf16(pr[0][2], pr[0][3]);
-        pa[2] = pack_bf16(pr[1][0], pr[1][1]);
-        pa[3] = pack_bf16(pr[1][2], pr[1][3]);
-        {
-          const int mi = lane >> 3, ri = lane & 7;
-          const int tok = (mi & 1) * 8 + ri;
-#pragma unroll
-          for (int np = 0; np < 8; ++np) {
-            uint32_t b0, b1, b2, b3;
-            ldmatrix_x4_trans(vt + swz256(tok, 2 * np + (mi >> 1)), b0, b1, b2, b3);
-            mma_bf16_16816(o[2 * np], pa, b0, b1);
-            mma_bf16_16816(o[2 * np + 1], pa, b2, b3);
-          }
-        }
-      }
-    }
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-
-  // -- combine the `ways` warps of each m-tile through shared memory
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-  float* sO = reinterpret_cast<float*>(smem);              // [4 warps][16][HD]
-  float* sM = sO + AT_WARPS * 16 * HD;                      // [4][16]
-  float* sL = sM + AT_WARPS * 16;                           // [4][16]
-  {
-    const int ra = lane >> 2, rb = ra + 8, cb = (lane & 3) * 2;
-    float* w = sO + warp * 16 * HD;
-#pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-      w[ra * HD + nt * 8 + cb] = o[nt][0];
-      w[ra * HD + nt * 8 + cb + 1] = o[nt][1];
-      w[rb * HD + nt * 8 + cb] = o[nt][2];
-      w[rb * HD + nt * 8 + cb + 1] = o[nt][3];
-    }
-    if ((lane & 3) == 0) {
-      sM[warp * 16 + ra] = m0;
-      sM[warp * 16 + rb] = m1;
-      sL[warp * 16 + ra] = l0;
-      sL[warp * 16 + rb] = l1;
-    }
-  }
-  __syncthreads();
-  const int64_t base_slot = (int64_t)item * p.gstride;
-  for (int e = threadIdx.x; e < tiles * 16 * HD; e += AT_THREADS) {
-    const int t = e / (16 * HD), rr = (e / HD) % 16, d = e % HD;
-    const int g = t * 16 + rr;
-    if (g >= G) continue;
-    float M = -INFINITY;
-    for (int w = 0; w < ways; ++w) M = fmaxf(M, sM[(t * ways + w) * 16 + rr]);
-    const float Mr = M == -INFINITY ? 0.f : M;
-    float acc = 0.f, lsum = 0.f;
-    for (int w = 0; w < ways; ++w) {
-      const int ww = t * ways + w;
-      const float f = exp2f(sM[ww * 16 + rr] - Mr);
-      acc += f * sO[(ww * 16 + rr) * HD + d];
-      lsum += f * sL[ww * 16 + rr];
-    }
-    p.po[(base_slot + g) * HD + d] = acc;
-    if (d == 0) {
-      p.pm[base_slot + g] = M;
-      p.pl[base_slot + g] = lsum;
-    }
-  }
-}
-
-__global__ void decode_attn_merge_kernel(AttnParams p, __nv_bfloat16* __restrict__ out) {
-  const int r = blockIdx.x, qh = blockIdx.y, d = threadIdx.x;
-  const int nkv = p.kv.n_kv_heads;
-  const int h = qh / p.grp, ql = qh % p.grp;
-  const int s = p.b.row_sess[r];
-  const int gs = p.b.row_in_sess[r] * p.grp + ql;
-  float M = -INFINITY;
-  for (int j = 0; j < p.ns_shared; ++j)
-    M = fmaxf(M, p.pm[((int64_t)(s * nkv + h) * p.ns_shared + j) * p.gstride + gs]);
-  for (int j = 0; j < p.ns_priv; ++j)
-    M = fmaxf(M, p.pm[((int64_t)p.n_shared_items + (r * nkv + h) * p.ns_priv + j) * p.gstride + ql]);
-  const float Mr = M == -INFINITY ? 0.f : M;
-  float acc = 0.f, lsum = 0.f;
-  for (int j = 0; j < p.ns_shared; ++j) {
-    const int64_t sl = ((int64_t)(s * nkv + h) * p.ns_shared + j) * p.gstride + gs;
-    const float f = exp2f(p.pm[sl] - Mr);
-    acc += f * p.po[sl * HD + d];
-    lsum += f * p.pl[sl];
-  }
-  for (int j = 0; j < p.ns_priv; ++j) {
-    const int64_t sl = ((int64_t)p.n_shared_items + (r * nkv + h) * p.ns_priv + j) * p.gstride + ql;
-    const float f = exp2f(p.pm[sl] - Mr);
-    acc += f * p.po[sl * HD + d];
-    lsum += f * p.pl[sl];
-  }
-  out[((int64_t)r * p.nq + qh) * HD + d] = f2bf(acc / lsum);
-}
-
 // ---------------------------------------------------------------- argmax --
 
 __global__ void argmax_advance_kernel(psk_decode_batch b, const float* __restrict__ logits, int V,
@@ -572,14 +291,6 @@ __global__ void argmax_advance_kernel(psk_decode_batch b, const float* __restric
 using namespace psk::dec;
 
 namespace {
-
-int attn_items(const psk_decode_batch* b, int nkv, int nss, int nsp, int* n_shared, int* n_total,
-               int* gstride) {
-  *n_shared = b->n_sess * nkv * nss;
-  *n_total = *n_shared + b->n_rows * nkv * nsp;
-  (void)gstride;
-  return 0;
-}
 
 template <int MAXM>
 int launch_gemv(const void* x, int K, const void* const* W, const int32_t* mrs, int n_mod, int N,
@@ -666,58 +377,6 @@ int psk_rope_append(const psk_decode_batch* b, const float* qkv, int32_t n_q_hea
   if (b->n_rows == 0) return PSK_OK;
   rope_append_kernel<<<b->n_rows, 64, 0, psk::as_stream(stream)>>>(
       *b, qkv, n_q_heads, rope, layer, kv, reinterpret_cast<__nv_bfloat16*>(q_rot));
-  PSK_LAUNCH_CHECK();
-  return PSK_OK;
-}
-
-int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int32_t head_dim,
-                              int32_t shared_splits, int32_t priv_splits, int64_t* bytes) {
-  PSK_CHECK_ARG(b && bytes && head_dim == HD, "psk_decode_attn_workspace: bad args");
-  int ns, nt, g;
-  attn_items(b, n_kv_heads, shared_splits, priv_splits, &ns, &nt, &g);
-  *bytes = (int64_t)nt * AT_GMAX * (HD + 2) * 4;
-  return PSK_OK;
-}
-
-int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_heads, int32_t layer,
-                    psk_kv_layout kv, int32_t shared_splits, int32_t priv_splits, void* workspace,
-                    void* out, void* stream) {
-  PSK_CHECK_ARG(b && q_rot && workspace && out && kv.head_dim == HD && kv.page_tokens == PT &&
-                    shared_splits >= 1 && priv_splits >= 1 && n_q_heads % kv.n_kv_heads == 0,
-                "psk_decode_attn: bad args");
-  const int grp = n_q_heads / kv.n_kv_heads;
-  PSK_CHECK_ARG(grp * b->max_rows_per_sess <= AT_GMAX,
-                "psk_decode_attn: %d query rows per KV head exceed %d", grp * b->max_rows_per_sess,
-                AT_GMAX);
-  if (b->n_rows == 0) return PSK_OK;
-  AttnParams p;
-  p.b = *b;
-  p.kv = kv;
-  p.q = reinterpret_cast<const __nv_bfloat16*>(q_rot);
-  p.nq = n_q_heads;
-  p.grp = grp;
-  p.layer = layer;
-  p.ns_shared = shared_splits;
-  p.ns_priv = priv_splits;
-  int nt, g;
-  attn_items(b, kv.n_kv_heads, shared_splits, priv_splits, &p.n_shared_items, &nt, &g);
-  p.gstride = AT_GMAX;
-  float* ws = reinterpret_cast<float*>(workspace);
-  p.pm = ws;
-  p.pl = ws + (int64_t)nt * AT_GMAX;
-  p.po = ws + (int64_t)nt * AT_GMAX * 2;
-  p.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
-  cudaStream_t s = psk::as_stream(stream);
-  static bool attr = false;
-  if (!attr) {
-    PSK_CUDA_TRY(cudaFuncSetAttribute(decode_attn_partial_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM));
-    attr = true;
-  }
-  decode_attn_partial_kernel<<<nt, AT_THREADS, AT_SMEM, s>>>(p);
-  PSK_LAUNCH_CHECK();
-  decode_attn_merge_kernel<<<dim3(b->n_rows, n_q_heads), HD, 0, s>>>(
-      p, reinterpret_cast<__nv_bfloat16*>(out));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }

@@ -188,7 +188,7 @@ class KVCache:
     def layout(self) -> "KVLayout":
         c = self.cfg
         return KVLayout(self.data.data_ptr(), c.page_elems, c.n_layers, c.n_kv_heads, c.head_dim,
-                        PAGE_TOKENS)
+                        PAGE_TOKENS, self.n_pages)
 
     def page_view(self) -> torch.Tensor:
         c = self.cfg
@@ -304,6 +304,15 @@ class DecodeBatch:
         self.reset()
 
 
+def attn_cluster_size(max_pages: int, n_clusters: int, sms: int = 148) -> int:
+    """CTAs per (session, KV head) cluster for K6: enough to spread the page
+    stream over the SMs (>= ~8 pages per CTA), a power of two <= 16."""
+    c = 1
+    while c < 16 and max_pages // (2 * c) >= 8 and n_clusters * 2 * c <= sms:
+        c *= 2
+    return c
+
+
 class DecodeRunner:
     """Runs greedy decode steps for a DecodeBatch of heterogeneous modules.
 
@@ -314,8 +323,7 @@ class DecodeRunner:
     """
 
     def __init__(self, cfg: LlamaConfig, modules: list[ModuleWeights], kv: KVCache,
-                 batch: DecodeBatch, max_new: int, shared_splits: int | None = None,
-                 priv_splits: int = 1, device: int = 0):
+                 batch: DecodeBatch, max_new: int, cluster: int | None = None, device: int = 0):
         self.cfg, self.kv, self.b, self.max_new = cfg, kv, batch, max_new
         self.lib = _lib.load()
         dev = torch.device("cuda", device)
@@ -343,17 +351,10 @@ class DecodeRunner:
         self.logits = torch.empty(R, cfg.vocab, dtype=f32, device=dev)
         self.out_tokens = torch.full((R, max_new), -1, dtype=torch.int32, device=dev)
         self.rope = torch.from_numpy(rope_table(cfg)).to(dev)
-        if shared_splits is None:
-            # fill ~2 CTAs per SM with the shared pass
-            sms = torch.cuda.get_device_properties(dev).multi_processor_count
-            shared_splits = max(1, (2 * sms) // max(1, batch.n_sess * cfg.n_kv_heads))
-        self.ns_shared, self.ns_priv = shared_splits, priv_splits
-        ws = C.c_int64()
-        _lib.check(self.lib.psk_decode_attn_workspace(C.byref(batch.c), cfg.n_kv_heads, cfg.head_dim,
-                                                      shared_splits, priv_splits, C.byref(ws)))
-        self.ws = torch.empty(ws.value // 4 + 1, dtype=f32, device=dev)
+        self.cluster = cluster if cluster is not None else attn_cluster_size(
+            batch.max_sess_pages, batch.n_sess * cfg.n_kv_heads)
         self.graph: torch.cuda.CUDAGraph | None = None
-        self.launches_per_step = 2 + L * 9 + 3
+        self.launches_per_step = 1 + L * 8 + 3
 
     # -- one step, eager ----------------------------------------------------
     def _step(self, s: int) -> None:
@@ -371,8 +372,8 @@ class DecodeRunner:
                              1, _ptr(self.qkv), s))
             chk(lib.psk_rope_append(bc, _ptr(self.qkv), cfg.n_heads, _ptr(self.rope), l, kvl,
                                     _ptr(self.q_rot), s))
-            chk(lib.psk_decode_attn(bc, _ptr(self.q_rot), cfg.n_heads, l, kvl, self.ns_shared,
-                                    self.ns_priv, _ptr(self.ws), _ptr(self.attn), s))
+            chk(lib.psk_decode_attn(bc, _ptr(self.q_rot), cfg.n_heads, l, kvl, self.cluster,
+                                    _ptr(self.attn), s))
             chk(lib.psk_gemv(_ptr(self.attn), R, cfg.n_heads * cfg.head_dim, _ptr(self.p_wo[l]), mrs,
                              b.n_mod, d, 2, _ptr(self.h), s))
             chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_mlp_norm[l]), _ptr(b.t_row_mod),

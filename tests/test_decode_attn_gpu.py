@@ -1,0 +1,82 @@
+"""K6 shared-prefix decode attention vs a torch fp32 reference on identical
+bf16 inputs (random paged KV and queries). Covers cluster sizes 1..16,
+GQA groups 2/4, 1..16 decode rows per session, several sessions, shared
+lengths ending mid-page, empty-ish private suffixes.
+Tolerance: |out - ref| <= 2e-2 * max|ref| + 2e-3 (bf16 P in the PV MMA,
+bf16 output)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, cluster, seed=0):
+    from paper_2602_12029_b200 import _lib
+    from paper_2602_12029_b200.model import (DecodeBatch, DecodeRow, KVCache, LlamaConfig,
+                                             SessionSpec)
+    cfg = LlamaConfig(n_layers=3, d_model=nq * 128, n_heads=nq, n_kv_heads=nkv, ffn=256, vocab=64,
+                      rope_theta=1e4, max_pos=65536)
+    rng = np.random.default_rng(seed)
+    n_pages = sum((L + 15) // 16 for L in sess_lens) + sum((p + 16) // 16 for p in priv_lens) + 3
+    perm = list(rng.permutation(n_pages))
+    kv = KVCache(cfg, n_pages)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    kv.data.copy_(torch.randn(kv.data.shape, device="cuda", generator=g).to(torch.bfloat16))
+    sessions, rows = [], []
+    ri = 0
+    for s, L in enumerate(sess_lens):
+        pages = [perm.pop() for _ in range((L + 15) // 16)]
+        sessions.append(SessionSpec(shared_len=L, pages=pages))
+        for m in range(rows_per_sess[s]):
+            pl = priv_lens[ri]
+            rows.append(DecodeRow(module=m, session=s, first_token=0,
+                                  pages=[perm.pop() for _ in range((pl + 16) // 16)]))
+            ri += 1
+    n_mod = max(rows_per_sess)
+    b = DecodeBatch(sessions, rows, n_mod)
+    pl_by_batch = [priv_lens[j] for j in b.order]
+    b.t_priv_len.copy_(torch.tensor(pl_by_batch, dtype=torch.int32))
+    R = len(rows)
+    q = torch.randn(R, nq, 128, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.full_like(q, float("nan"))
+    layer = 1
+    L_ = _lib
+    L_.check(L_.load().psk_decode_attn(b.c_ref(), q.data_ptr(), nq, layer, kv.layout(), cluster,
+                                       out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    grp = nq // nkv
+    for j, row in enumerate(b.rows):
+        sp = sessions[row.session]
+        ks, vs = kv.read_positions(sp.pages, layer, sp.shared_len)
+        kp, vp = kv.read_positions(row.pages, layer, pl_by_batch[j] + 1)
+        K = torch.cat([ks, kp], 1).float()
+        V = torch.cat([vs, vp], 1).float()
+        Kq = K.repeat_interleave(grp, 0)
+        Vq = V.repeat_interleave(grp, 0)
+        sc = (q[j].float().unsqueeze(1) @ Kq.transpose(1, 2)).squeeze(1) / np.sqrt(128)
+        ref = (torch.softmax(sc, -1).unsqueeze(1) @ Vq).squeeze(1)
+        err = (out[j].float() - ref).abs().max().item()
+        assert err <= 2e-2 * ref.abs().max().item() + 2e-3, f"row {j}: err {err}"
+
+
+@pytest.mark.parametrize("cluster", [1, 2, 4, 8, 16])
+def test_one_session_four_modules(cluster):
+    _case(32, 8, [4095], [4], [0, 3, 17, 255], cluster)
+
+
+def test_sixteen_modules_fanout():
+    _case(32, 8, [2000], [16], [i * 7 for i in range(16)], 16, seed=1)
+
+
+def test_multi_session_ragged():
+    _case(32, 8, [1000, 37, 513], [2, 3, 1], [0, 5, 16, 40, 1, 200], 4, seed=2)
+
+
+def test_gqa2_tiny_shape():
+    _case(2, 1, [99, 300], [2, 2], [0, 1, 15, 31], 2, seed=3)
+
+
+def test_single_token_shared():
+    _case(32, 8, [1], [4], [0, 0, 0, 0], 1, seed=4)
