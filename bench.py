@@ -209,7 +209,7 @@ def decode_attn_roofline(eng, peaks) -> dict:
         l = it[0] % cfg.n_layers
         it[0] += 1
         _lib.check(r.lib.psk_decode_attn(b.c_ref(), r.q_rot.data_ptr(), cfg.n_heads, l, kvl,
-                                         r.cluster, r.attn.data_ptr(), s))
+                                         r.splits, r.ws.data_ptr(), r.attn.data_ptr(), s))
     dt = _time_launches(launch, 4 * cfg.n_layers)
     shared = int(b.t_sess_len.sum().item())
     priv = int((b.t_priv_len + 1).sum().item())
@@ -239,16 +239,20 @@ def decode_attn_fanout(peaks, shared_tokens=32767, modules=16) -> dict:
     b = DecodeBatch([SessionSpec(shared_len=shared_tokens, pages=list(range(n_sh)))], rows, modules)
     q = torch.randn(modules, cfg.n_heads, cfg.head_dim, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)
-    from paper_2602_12029_b200.model import attn_cluster_size
-    cl = attn_cluster_size(n_sh, cfg.n_kv_heads)
+    import ctypes
+    from paper_2602_12029_b200.model import attn_splits
+    ns = attn_splits(n_sh + modules, cfg.n_kv_heads, torch.cuda.get_device_properties(0).multi_processor_count)
+    wsb = ctypes.c_int64()
+    _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), cfg.n_kv_heads, ns, ctypes.byref(wsb)))
+    ws = torch.empty(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
     it = [0]
     kvl = kv.layout()
 
     def launch():
         l = it[0] % cfg.n_layers
         it[0] += 1
-        _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), cfg.n_heads, l, kvl, cl,
-                                       out.data_ptr(), s))
+        _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), cfg.n_heads, l, kvl, ns,
+                                       ws.data_ptr(), out.data_ptr(), s))
     dt = _time_launches(launch, 2 * cfg.n_layers)
     per_tok = 2 * cfg.n_kv_heads * cfg.head_dim * 2
     nbytes = (shared_tokens + modules) * per_tok + 2 * modules * cfg.n_heads * cfg.head_dim * 2

@@ -194,15 +194,19 @@ int psk_rope_append(const psk_decode_batch* b, const float* qkv, int32_t n_q_hea
                     const float* rope, int32_t layer, psk_kv_layout kv, void* q_rot,
                     void* stream);
 
-/* K6: shared-prefix paged decode attention for one layer. One thread-block
- * cluster of `cluster` (1,2,4,8,16) CTAs per (session, KV head) streams the
- * session's shared prompt pages and its rows' private pages (including the
- * token appended this step) from HBM once per step, for ALL of the
- * session's decode rows (modules) and their GQA query heads, and reduces
- * the split-KV partials through distributed shared memory.
- * q_rot bf16 [n_rows][nq][hd] -> out bf16 [n_rows][nq][hd]. */
+/* K6: shared-prefix paged decode attention for one layer. The page stream of
+ * each (session, KV head) — the session's shared prompt pages followed by its
+ * rows' private pages (incl. the token appended this step) — is cut into
+ * `splits` slices; every page is streamed from HBM once per step (TMA) for
+ * ALL of the session's decode rows (modules) and their GQA query heads; the
+ * split partials merge by log-sum-exp in a second, PDL-overlapped kernel.
+ * q_rot bf16 [n_rows][nq][hd] -> out bf16 [n_rows][nq][hd]. workspace: fp32,
+ * psk_decode_attn_workspace() bytes. */
+int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int32_t splits,
+                              int64_t* bytes);
 int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_heads,
-                    int32_t layer, psk_kv_layout kv, int32_t cluster, void* out, void* stream);
+                    int32_t layer, psk_kv_layout kv, int32_t splits, void* workspace, void* out,
+                    void* stream);
 
 /* Greedy step end: tokens[r] = argmax(logits[r]) (first max, as tf.argMax /
  * torch.argmax), out_tokens[r*max_new + priv_len[r]] = it (if in range),

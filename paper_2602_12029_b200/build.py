@@ -61,6 +61,10 @@ def _compile(src: Path, obj: Path, verbose: bool) -> None:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stdout}\n{r.stderr}")
     if verbose and r.stderr:
         print(r.stderr, flush=True)
+    elif r.stderr:
+        for line in r.stderr.splitlines():
+            if "spill" in line or "warning" in line.lower():
+                print(f"[{src.name}] {line}", flush=True)
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:

@@ -107,15 +107,15 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(
   int cur_row = -1, cur_slot = 0, M = 0, xbase = 0;
   const __nv_bfloat16* wrow = nullptr;
 
-  auto flush = [&]() {
-    if (cur_row < 0) return;
-#pragma unroll
-    for (int m = 0; m < MAXM; ++m) {
-      float v = warp_sum(acc[m]);
-      if (lane == 0 && m < M) slots[((int64_t)cur_row * cpr + cur_slot) * MAXM + m] = v;
-      acc[m] = 0.f;
-    }
-  };
+  // (a macro, not a by-reference lambda: that would put acc[] in local memory)
+#define GEMV_FLUSH()                                                                   \
+  if (cur_row >= 0) {                                                                  \
+    _Pragma("unroll") for (int m = 0; m < MAXM; ++m) {                                 \
+      float v = warp_sum(acc[m]);                                                      \
+      if (lane == 0 && m < M) slots[((int64_t)cur_row * cpr + cur_slot) * MAXM + m] = v; \
+      acc[m] = 0.f;                                                                    \
+    }                                                                                  \
+  }
 
   // zero all slots first (rows whose chunks are split over warps use only
   // the first chunk slot of each warp's run)
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(
     const int rl = (int)(u / cpr);
     const int ch = (int)(u % cpr);
     if (rl != cur_row) {
-      flush();
+      GEMV_FLUSH();
       cur_row = rl;
       cur_slot = ch;
       const int64_t g = g0 + rl;
@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(
       }
     }
   }
-  flush();
+  GEMV_FLUSH();
+#undef GEMV_FLUSH
   __syncthreads();
 
   // epilogue: thread per (row, m)

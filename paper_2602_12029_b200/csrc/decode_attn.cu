@@ -1,21 +1,26 @@
-// K6 — shared-prefix paged decode attention (one launch per layer).
+// K6 — shared-prefix paged decode attention (one layer per call).
 //
 // Decode modules batched on one session share the base module's prompt KV
 // (the PrefillShare cache reuse: frontend/src/evaluate.ts:21-50, one base
 // cache consumed by several decoders; the reference re-concatenates and
-// re-reads the full past per model and per step, model.ts:307-315). Here one
-// thread-block CLUSTER serves one (session, KV head):
+// re-reads the full past per model and per step, model.ts:307-315).
 //
-//   * the page stream is [shared prompt pages | row 0 private pages | row 1
-//     private pages | ...]; every page is fetched from HBM exactly once per
-//     step by TMA (128B-swizzled 4 KiB K and V tiles) into a 12-stage ring
-//     driven by a producer warp, and consumed by ALL query rows of the
-//     session (GQA group x co-batched decode modules, <= 64 rows = 4 MMA
-//     tiles); private pages mask the rows they do not belong to;
-//   * the C CTAs of the cluster split the stream; each CTA folds its warps'
-//     online-softmax partials in shared memory, then the cluster reduces the
-//     C partials through distributed shared memory (DSMEM) and writes the
-//     normalised bf16 output — no global partials, no second kernel.
+// Partial kernel: one CTA = (session, KV head, split). Its page stream is the
+// split's slice of [shared prompt pages | row 0 private pages | row 1 private
+// pages | ...]. A producer warp streams every page with TMA (two 128B-swizzled
+// [16 x 64] boxes per 4 KiB K / V tile) through an 8-stage mbarrier ring; 8
+// consumer warps map to (query m-tile, page subset), so each page is read
+// from HBM once per step for ALL query rows of the session (GQA group x
+// co-batched decode modules, <= 64 rows); private pages mask the rows they do
+// not own. Warps fold their online-softmax state in fragment order, and the
+// CTA writes one (m, l, O) partial per query row.
+// Merge kernel (launched with programmatic dependent launch so its launch
+// overlaps the partial kernel's tail): one warp per (row, q head) folds the
+// split partials by log-sum-exp and writes bf16 output.
+//
+// (A 16-CTA-cluster / DSMEM-reduction variant was measured first: at this
+// shared-memory footprint only 7 such clusters are co-resident on a B200, so
+// 8 KV heads always ran in two waves.)
 #include "common.cuh"
 #include "mma.cuh"
 #include "tma.cuh"
@@ -26,31 +31,31 @@ namespace psk {
 namespace dattn {
 
 constexpr int HD = 128, PT = 16;
-constexpr int CW = 8;                 // consumer warps
+constexpr int CW = 8;                   // consumer warps
 constexpr int THREADS = (CW + 1) * 32;  // + 1 TMA producer warp
-constexpr int NST = 12;               // pipeline stages (1 page each)
-constexpr int TILE = PT * HD * 2;     // 4 KiB
-constexpr int STAGE = 2 * TILE;       // K + V
+constexpr int NST = 8;                  // pipeline stages (1 page = K + V each)
+constexpr int TILE = PT * HD * 2;       // 4 KiB
+constexpr int STAGE = 2 * TILE;
 constexpr int GMAX = 64;
-constexpr int MAXR = 16;              // rows per session
-constexpr int OFF_Q = NST * STAGE;                  // 96 KiB
-constexpr int OFF_O = OFF_Q + GMAX * 256;           // +16 KiB
-constexpr int OFF_M = OFF_O + GMAX * HD * 4;        // +32 KiB
-constexpr int OFF_L = OFF_M + GMAX * 4;
-constexpr int OFF_BAR = OFF_L + GMAX * 4;
-constexpr int SMEM = OFF_BAR + 2 * NST * 8 + 1024;  // + alignment slack
+constexpr int MAXR = 16;                // decode rows per session
+constexpr int OFF_Q = NST * STAGE;      // 64 KiB
+constexpr int OFF_BAR = OFF_Q + GMAX * 256;  // +16 KiB
+constexpr int MAXP = 1024;              // page indices staged in smem
+constexpr int OFF_PG = OFF_BAR + 2 * NST * 8;
+constexpr int SMEM = OFF_PG + MAXP * 4 + 1024;  // ~86 KiB (+ alignment slack): 2 CTAs / SM
+constexpr int FRAG = 68;                // floats per lane in the fold scratch (64 O + m0 m1 l0 l1)
+static_assert(CW * 32 * FRAG * 4 <= OFF_BAR, "fold scratch must fit in ring + Q");
 
 struct Params {
   psk_decode_batch b;
   psk_kv_layout kv;
   const __nv_bfloat16* q;  // [rows][nq][HD]
   __nv_bfloat16* out;      // [rows][nq][HD]
-  int nq, grp, layer;
+  float* pm;               // [items][GMAX]
+  float* pl;               // [items][GMAX]
+  float* po;               // [items][GMAX][HD]
+  int nq, grp, layer, ns;
   float scale_log2;
-};
-
-struct PageMeta {
-  int page, limit, owner;  // owner: -1 shared, else row index within session
 };
 
 // SW128 address of (token row, 16-byte chunk c16 in 0..15) in a K/V tile made
@@ -59,44 +64,48 @@ __device__ __forceinline__ uint32_t tile_addr(uint32_t tile, int tok, int c16) {
   return tile + ((c16 >> 3) << 11) + tok * 128 + (((c16 & 7) ^ (tok & 7)) << 4);
 }
 
-template <int C>
-__global__ void __launch_bounds__(THREADS, 1)
-    decode_attn_kernel(const __grid_constant__ CUtensorMap kvmap, Params p) {
+__global__ void __maxnreg__(112)  // 2 CTAs x 288 threads per SM
+    decode_attn_partial(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ Params p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* empty = full + NST;
-  float* sO = reinterpret_cast<float*>(smem + OFF_O);
-  float* sM = reinterpret_cast<float*>(smem + OFF_M);
-  float* sL = reinterpret_cast<float*>(smem + OFF_L);
+  int* s_page = reinterpret_cast<int*>(smem + OFF_PG);
   __shared__ int s_rows[MAXR], s_plen[MAXR], s_pstart[MAXR + 1];
   __shared__ int s_ps, s_ls, s_total;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkv = p.kv.n_kv_heads;
-  const int cl = blockIdx.x / C;
-  const int rank = (int)tma::cluster_rank();
-  const int sess = cl / nkv, h = cl % nkv;
+  const int item = blockIdx.x;
+  const int j_split = item % p.ns;
+  const int h = (item / p.ns) % nkv;
+  const int sess = item / (p.ns * nkv);
   const int nr = p.b.sess_nrows[sess];
   const int G = nr * p.grp;
   const int T = (G + 15) / 16;
   const int Tp = T <= 1 ? 1 : (T == 2 ? 2 : 4);
   const int ways = CW / Tp;
 
+  // let the merge kernel launch now; it waits for our completion itself
+  asm volatile("griddepcontrol.launch_dependents;");
+
+  // prologue: one latency round trip for all rows (no dependent chains)
+  if (threadIdx.x < nr) {
+    const int r = p.b.sess_rows[(int64_t)sess * p.b.max_rows_per_sess + threadIdx.x];
+    s_rows[threadIdx.x] = r;
+    s_plen[threadIdx.x] = p.b.priv_len[r] + 1;  // includes the token appended this step
+  } else if (threadIdx.x == 32) {
+    s_ls = p.b.sess_len[sess];
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const int Ls = p.b.sess_len[sess];
-    const int Ps = (Ls + PT - 1) / PT;
-    s_ls = Ls;
+    const int Ps = (s_ls + PT - 1) / PT;
     s_ps = Ps;
     int acc = Ps;
     for (int i = 0; i < nr; ++i) {
-      const int r = p.b.sess_rows[(int64_t)sess * p.b.max_rows_per_sess + i];
-      const int lp = p.b.priv_len[r] + 1;  // includes the token appended this step
-      s_rows[i] = r;
-      s_plen[i] = lp;
       s_pstart[i] = acc;
-      acc += (lp + PT - 1) / PT;
+      acc += (s_plen[i] + PT - 1) / PT;
     }
     s_pstart[nr] = acc;
     s_total = acc;
@@ -107,42 +116,34 @@ __global__ void __launch_bounds__(THREADS, 1)
     tma::fence_mbar_init();
     tma::prefetch_map(&kvmap);
   }
-  // Q tile -> shared (swizzled 256 B rows), zero rows beyond G
+  __syncthreads();
+  const int total = s_total;
+  const int k0 = (int)((int64_t)j_split * total / p.ns);
+  const int k1 = (int)((int64_t)(j_split + 1) * total / p.ns);
+  const int np = k1 - k0;
+
+  auto page_of = [&](int k) -> int {
+    if (k < s_ps) return p.b.sess_pages[(int64_t)sess * p.b.max_sess_pages + k];
+    int i = 0;
+    while (k >= s_pstart[i + 1]) ++i;
+    return p.b.row_pages[(int64_t)s_rows[i] * p.b.max_row_pages + (k - s_pstart[i])];
+  };
+  // page indices and Q tile -> shared memory
+  for (int j = threadIdx.x; j < np && j < MAXP; j += THREADS) s_page[j] = page_of(k0 + j);
   {
     const uint32_t qs = smem_u32(smem + OFF_Q);
     for (int e = threadIdx.x; e < T * 16 * 16; e += THREADS) {
       const int g = e >> 4, c = e & 15;
       uint4 v = make_uint4(0, 0, 0, 0);
       if (g < G) {
-        const int r = p.b.sess_rows[(int64_t)sess * p.b.max_rows_per_sess + g / p.grp];
         const int qh = h * p.grp + g % p.grp;
-        v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)r * p.nq + qh) * HD + c * 8);
+        v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)s_rows[g / p.grp] * p.nq + qh) * HD + c * 8);
       }
       asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(qs + swz256(g, c)), "r"(v.x),
                    "r"(v.y), "r"(v.z), "r"(v.w));
     }
   }
   __syncthreads();
-  const int total = s_total;
-  const int k0 = (int)((int64_t)rank * total / C), k1 = (int)((int64_t)(rank + 1) * total / C);
-  const int np = k1 - k0;
-
-  auto meta = [&](int k) -> PageMeta {
-    PageMeta m;
-    if (k < s_ps) {
-      m.page = p.b.sess_pages[(int64_t)sess * p.b.max_sess_pages + k];
-      m.limit = min(PT, s_ls - k * PT);
-      m.owner = -1;
-    } else {
-      int i = 0;
-      while (k >= s_pstart[i + 1]) ++i;
-      const int j = k - s_pstart[i];
-      m.page = p.b.row_pages[(int64_t)s_rows[i] * p.b.max_row_pages + j];
-      m.limit = min(PT, s_plen[i] - j * PT);
-      m.owner = i;
-    }
-    return m;
-  };
 
   const uint32_t ring = smem_u32(smem);
   if (warp == CW) {
@@ -151,8 +152,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int j = 0; j < np; ++j) {
         const int st = j % NST;
         tma::mbar_wait(&empty[st], ((j / NST) & 1) ^ 1);
-        const PageMeta m = meta(k0 + j);
-        const int row_k = (int)((((int64_t)m.page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
+        const int page = j < MAXP ? s_page[j] : page_of(k0 + j);
+        const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
         const int row_v = row_k + nkv * PT;
         unsigned char* dst = smem + st * STAGE;
         tma::mbar_expect_tx(&full[st], STAGE);
@@ -170,21 +171,29 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-  const int gA = tile * 16 + (lane >> 2), gB = gA + 8;
   if (active) {
-    uint32_t qa[8][4];
-    {
-      const uint32_t qs = smem_u32(smem + OFF_Q);
-      const int mi = lane >> 3;
-      const int row = tile * 16 + (mi & 1) * 8 + (lane & 7);
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks)
-        ldmatrix_x4(qs + swz256(row, 2 * ks + (mi >> 1)), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
-    }
+    // Q fragments are re-read from shared memory per k-step (ldmatrix) rather
+    // than pinned in 32 registers: keeps the kernel at 2 CTAs / SM unspilled.
+    const uint32_t qs = smem_u32(smem + OFF_Q);
+    const int qrow = tile * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
+    const int qhalf = lane >> 4;
+    const int gA = tile * 16 + (lane >> 2), gB = gA + 8;
     const int ownA = gA < G ? gA / p.grp : -2, ownB = gB < G ? gB / p.grp : -2;
     for (int j = way; j < np; j += ways) {
       const int st = j % NST;
-      const PageMeta m = meta(k0 + j);
+      int limit, owner;
+      {
+        const int k = k0 + j;
+        if (k < s_ps) {
+          limit = min(PT, s_ls - k * PT);
+          owner = -1;
+        } else {
+          int i = 0;
+          while (k >= s_pstart[i + 1]) ++i;
+          limit = min(PT, s_plen[i] - (k - s_pstart[i]) * PT);
+          owner = i;
+        }
+      }
       tma::mbar_wait(&full[st], (j / NST) & 1);
       const uint32_t kt = ring + st * STAGE, vt = kt + TILE;
       float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -193,21 +202,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int tok = (mi >> 1) * 8 + ri;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
-          uint32_t b0, b1, b2, b3;
+          uint32_t a[4], b0, b1, b2, b3;
+          ldmatrix_x4(qs + swz256(qrow, 2 * ks + qhalf), a[0], a[1], a[2], a[3]);
           ldmatrix_x4(tile_addr(kt, tok, 2 * ks + (mi & 1)), b0, b1, b2, b3);
-          mma_bf16_16816(s[0], qa[ks], b0, b1);
-          mma_bf16_16816(s[1], qa[ks], b2, b3);
+          mma_bf16_16816(s[0], a, b0, b1);
+          mma_bf16_16816(s[1], a, b2, b3);
         }
       }
-      const bool okA = m.owner < 0 || m.owner == ownA;
-      const bool okB = m.owner < 0 || m.owner == ownB;
+      const bool okA = owner < 0 || owner == ownA;
+      const bool okB = owner < 0 || owner == ownB;
       const int cb = (lane & 3) * 2;
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int t = nt * 8 + cb + (e & 1);
-          const bool ok = t < m.limit && (e < 2 ? okA : okB);
+          const bool ok = t < limit && (e < 2 ? okA : okB);
           s[nt][e] = ok ? s[nt][e] * p.scale_log2 : -INFINITY;
         }
       float mx0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
@@ -264,76 +274,113 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();  // ring drained: every fetched page was consumed
 
-  // -- fold the `ways` warps of each m-tile (ring reused as scratch)
-  float* wO = reinterpret_cast<float*>(smem);       // [CW][16][HD+4]
-  float* wM = wO + CW * 16 * (HD + 4);              // [CW][16]
-  float* wL = wM + CW * 16;
-  constexpr int LD = HD + 4;                        // padded row: conflict-free fragment stores
+  // -- fold the `ways` warps of each m-tile in fragment order (ring + Q reused)
+  float* scr = reinterpret_cast<float*>(smem);  // [CW][32][FRAG]
   if (active) {
-    const int ra = lane >> 2, rb = ra + 8, cb = (lane & 3) * 2;
-    float* w = wO + warp * 16 * LD;
+    float4* d = reinterpret_cast<float4*>(scr + (warp * 32 + lane) * FRAG);
 #pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-      *reinterpret_cast<float2*>(w + ra * LD + nt * 8 + cb) = make_float2(o[nt][0], o[nt][1]);
-      *reinterpret_cast<float2*>(w + rb * LD + nt * 8 + cb) = make_float2(o[nt][2], o[nt][3]);
-    }
-    if ((lane & 3) == 0) {
-      wM[warp * 16 + ra] = m0;
-      wM[warp * 16 + rb] = m1;
-      wL[warp * 16 + ra] = l0;
-      wL[warp * 16 + rb] = l1;
-    }
+    for (int i = 0; i < 16; ++i) d[i] = make_float4(o[i][0], o[i][1], o[i][2], o[i][3]);
+    d[16] = make_float4(m0, m1, l0, l1);
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < T * 16 * HD; e += THREADS) {
-    const int t = e / (16 * HD), rr = (e / HD) % 16, d = e % HD;
-    float M = -INFINITY;
-    for (int w = 0; w < ways; ++w) M = fmaxf(M, wM[(t * ways + w) * 16 + rr]);
-    const float Mr = M == -INFINITY ? 0.f : M;
-    float acc = 0.f, ls = 0.f;
-    for (int w = 0; w < ways; ++w) {
-      const int ww = t * ways + w;
-      const float f = exp2f(wM[ww * 16 + rr] - Mr);
-      acc += f * wO[(ww * 16 + rr) * LD + d];
-      ls += f * wL[ww * 16 + rr];
-    }
-    const int g = t * 16 + rr;
-    sO[g * HD + d] = acc;
-    if (d == 0) {
-      sM[g] = M;
-      sL[g] = ls;
+  const int64_t base = (int64_t)item * GMAX;
+  // thread (warp w, lane l) owns fragment elements [8w, 8w+8) of lane l, per tile
+  if (warp < CW) {
+    const int ra = lane >> 2, rb = ra + 8, cb = (lane & 3) * 2;
+    for (int t = 0; t < T; ++t) {
+      float Ma = -INFINITY, Mb = -INFINITY;
+      for (int v = 0; v < ways; ++v) {
+        const float4 ml = reinterpret_cast<const float4*>(scr + ((t * ways + v) * 32 + lane) * FRAG)[16];
+        Ma = fmaxf(Ma, ml.x);
+        Mb = fmaxf(Mb, ml.y);
+      }
+      const float Mra = Ma == -INFINITY ? 0.f : Ma, Mrb = Mb == -INFINITY ? 0.f : Mb;
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      float La = 0.f, Lb = 0.f;
+      for (int v = 0; v < ways; ++v) {
+        const float* src = scr + ((t * ways + v) * 32 + lane) * FRAG;
+        const float4 ml = reinterpret_cast<const float4*>(src)[16];
+        const float fa = exp2f(ml.x - Mra), fb = exp2f(ml.y - Mrb);
+        La += fa * ml.z;
+        Lb += fb * ml.w;
+        const float4 x0 = reinterpret_cast<const float4*>(src)[2 * warp];
+        const float4 x1 = reinterpret_cast<const float4*>(src)[2 * warp + 1];
+        acc[0] += fa * x0.x; acc[1] += fa * x0.y; acc[2] += fb * x0.z; acc[3] += fb * x0.w;
+        acc[4] += fa * x1.x; acc[5] += fa * x1.y; acc[6] += fb * x1.z; acc[7] += fb * x1.w;
+      }
+      const int ga = t * 16 + ra, gb = t * 16 + rb;
+      // elements 8w..8w+7 = fragments nt = 2w, 2w+1; each (a0 a1 b0 b1)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int col = (2 * warp + q) * 8 + cb;
+        if (ga < G)
+          *reinterpret_cast<float2*>(p.po + (base + ga) * HD + col) = make_float2(acc[4 * q], acc[4 * q + 1]);
+        if (gb < G)
+          *reinterpret_cast<float2*>(p.po + (base + gb) * HD + col) = make_float2(acc[4 * q + 2], acc[4 * q + 3]);
+      }
+      if (warp == 0 && (lane & 3) == 0) {
+        if (ga < G) {
+          p.pm[base + ga] = Ma;
+          p.pl[base + ga] = La;
+        }
+        if (gb < G) {
+          p.pm[base + gb] = Mb;
+          p.pl[base + gb] = Lb;
+        }
+      }
     }
   }
+}
 
-  // -- reduce the C CTA partials of the cluster through DSMEM
-  tma::cluster_sync();
-  const int E = G * HD;
-  const int e0 = (int)((int64_t)rank * E / C), e1 = (int)((int64_t)(rank + 1) * E / C);
-  for (int e = e0 + threadIdx.x; e < e1; e += THREADS) {
-    const int g = e / HD, d = e % HD;
-    float mc[C], lc[C], oc[C];
+// One warp per (row, q head); lane owns 4 of the 128 dims.
+__global__ void __launch_bounds__(128) decode_attn_merge(const __grid_constant__ Params p) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x;
+  const int qh = blockIdx.y * 4 + warp;
+  if (qh >= p.nq) return;
+  const int nkv = p.kv.n_kv_heads;
+  const int h = qh / p.grp;
+  const int g = p.b.row_in_sess[r] * p.grp + qh % p.grp;
+  const int s = p.b.row_sess[r];
+  const int64_t base = ((int64_t)(s * nkv + h) * p.ns) * GMAX + g;
+  float M = -INFINITY, L = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int U = 8;
+  for (int j0 = 0; j0 < p.ns; j0 += U) {
+    float mj[U], lj[U];
+    float4 oj[U];
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-      mc[c] = tma::ld_dsmem_f32(tma::map_rank(&sM[g], c));
-      lc[c] = tma::ld_dsmem_f32(tma::map_rank(&sL[g], c));
-      oc[c] = tma::ld_dsmem_f32(tma::map_rank(&sO[g * HD + d], c));
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u;
+      if (j < p.ns) {
+        const int64_t sl = base + (int64_t)j * GMAX;
+        mj[u] = p.pm[sl];
+        lj[u] = p.pl[sl];
+        oj[u] = *reinterpret_cast<const float4*>(p.po + sl * HD + lane * 4);
+      } else {
+        mj[u] = -INFINITY;
+        lj[u] = 0.f;
+        oj[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
-    float M = -INFINITY;
 #pragma unroll
-    for (int c = 0; c < C; ++c) M = fmaxf(M, mc[c]);
-    const float Mr = M == -INFINITY ? 0.f : M;
-    float acc = 0.f, ls = 0.f;
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const float f = exp2f(mc[c] - Mr);
-      acc += f * oc[c];
-      ls += f * lc[c];
+    for (int u = 0; u < U; ++u) {
+      const float Mn = fmaxf(M, mj[u]);
+      if (Mn == -INFINITY) continue;
+      const float a = exp2f(M - Mn), c = exp2f(mj[u] - Mn);
+      L = L * a + lj[u] * c;
+      acc.x = acc.x * a + oj[u].x * c;
+      acc.y = acc.y * a + oj[u].y * c;
+      acc.z = acc.z * a + oj[u].z * c;
+      acc.w = acc.w * a + oj[u].w * c;
+      M = Mn;
     }
-    const int r = s_rows[g / p.grp];
-    const int qh = h * p.grp + g % p.grp;
-    p.out[((int64_t)r * p.nq + qh) * HD + d] = f2bf(ls > 0.f ? acc / ls : 0.f);
   }
-  tma::cluster_sync();  // keep our shared memory alive until every peer is done reading it
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(p.out + ((int64_t)r * p.nq + qh) * HD + lane * 4);
+  o[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+  o[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
 }
 
 // ------------------------------------------------------------ host side --
@@ -344,13 +391,15 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 static int kv_map(const psk_kv_layout& kv, CUtensorMap* out) {
-  // one-entry cache keyed by the pool geometry
-  static CUtensorMap cached;
-  static psk_kv_layout key = {};
-  if (key.base == kv.base && key.n_pages == kv.n_pages && key.page_elems == kv.page_elems) {
-    *out = cached;
-    return PSK_OK;
-  }
+  // small cache keyed by the pool geometry
+  static CUtensorMap cached[4];
+  static psk_kv_layout keys[4] = {};
+  static int next = 0;
+  for (int i = 0; i < 4; ++i)
+    if (keys[i].base == kv.base && keys[i].n_pages == kv.n_pages && keys[i].page_elems == kv.page_elems) {
+      *out = cached[i];
+      return PSK_OK;
+    }
   static EncodeTiledFn enc = nullptr;
   if (!enc) {
     void* fp = nullptr;
@@ -367,54 +416,40 @@ static int kv_map(const psk_kv_layout& kv, CUtensorMap* out) {
   cuuint64_t strides[1] = {(cuuint64_t)HD * 2};
   cuuint32_t box[2] = {64, (cuuint32_t)PT};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(&cached, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kv.base, dims, strides, box, es,
+  const int i = next;
+  next = (next + 1) % 4;
+  CUresult r = enc(&cached[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kv.base, dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
+    keys[i] = psk_kv_layout{};
     set_error("KV tensor map encode failed (%d)", (int)r);
     return PSK_ECUDA;
   }
-  key = kv;
-  *out = cached;
-  return PSK_OK;
-}
-
-template <int C>
-static int launch(const CUtensorMap& map, const Params& p, int n_clusters, cudaStream_t s) {
-  static bool init = false;
-  if (!init) {
-    PSK_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      SMEM));
-    if (C > 8)
-      PSK_CUDA_TRY(cudaFuncSetAttribute(decode_attn_kernel<C>,
-                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    init = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_clusters * C);
-  cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_kernel<C>, map, p));
+  keys[i] = kv;
+  *out = cached[i];
   return PSK_OK;
 }
 
 }  // namespace dattn
 }  // namespace psk
 
-extern "C" int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_heads,
-                               int32_t layer, psk_kv_layout kv, int32_t cluster, void* out,
-                               void* stream) {
-  using namespace psk::dattn;
-  PSK_CHECK_ARG(b && q_rot && out && kv.head_dim == HD && kv.page_tokens == PT && kv.n_pages > 0 &&
-                    n_q_heads % kv.n_kv_heads == 0,
+using namespace psk::dattn;
+
+extern "C" {
+
+int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int32_t splits,
+                              int64_t* bytes) {
+  PSK_CHECK_ARG(b && bytes && splits >= 1, "psk_decode_attn_workspace: bad args");
+  const int64_t items = (int64_t)b->n_sess * n_kv_heads * splits;
+  *bytes = items * GMAX * (HD + 2) * 4;
+  return PSK_OK;
+}
+
+int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_heads, int32_t layer,
+                    psk_kv_layout kv, int32_t splits, void* workspace, void* out, void* stream) {
+  PSK_CHECK_ARG(b && q_rot && out && workspace && kv.head_dim == HD && kv.page_tokens == PT &&
+                    kv.n_pages > 0 && n_q_heads % kv.n_kv_heads == 0 && splits >= 1,
                 "psk_decode_attn: bad args");
   const int grp = n_q_heads / kv.n_kv_heads;
   PSK_CHECK_ARG(b->max_rows_per_sess <= MAXR && grp * b->max_rows_per_sess <= GMAX,
@@ -431,17 +466,33 @@ extern "C" int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int
   p.nq = n_q_heads;
   p.grp = grp;
   p.layer = layer;
+  p.ns = splits;
+  const int64_t items = (int64_t)b->n_sess * kv.n_kv_heads * splits;
+  float* ws = reinterpret_cast<float*>(workspace);
+  p.pm = ws;
+  p.pl = ws + items * GMAX;
+  p.po = ws + 2 * items * GMAX;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
-  const int nc = b->n_sess * kv.n_kv_heads;
   cudaStream_t s = psk::as_stream(stream);
-  switch (cluster) {
-    case 1: return launch<1>(map, p, nc, s);
-    case 2: return launch<2>(map, p, nc, s);
-    case 4: return launch<4>(map, p, nc, s);
-    case 8: return launch<8>(map, p, nc, s);
-    case 16: return launch<16>(map, p, nc, s);
-    default:
-      psk::set_error("psk_decode_attn: cluster must be 1, 2, 4, 8 or 16 (got %d)", cluster);
-      return PSK_EINVAL;
+  static bool init = false;
+  if (!init) {
+    PSK_CUDA_TRY(cudaFuncSetAttribute(decode_attn_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM));
+    init = true;
   }
+  decode_attn_partial<<<(unsigned)items, THREADS, SMEM, s>>>(map, p);
+  PSK_LAUNCH_CHECK();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(b->n_rows, (n_q_heads + 3) / 4);
+  cfg.blockDim = dim3(128);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_merge, p));
+  return PSK_OK;
 }
+
+}  // extern "C"

@@ -58,7 +58,7 @@ __device__ __forceinline__ const __nv_bfloat16* tile_ptr(const psk_kv_layout& kv
          (((int64_t)layer * 2 + kvsel) * kv.n_kv_heads + head) * kv.page_tokens * kv.head_dim;
 }
 
-__global__ void __launch_bounds__(THREADS, 2) prefill_attn_kernel(Params p) {
+__global__ void __launch_bounds__(THREADS, 2) prefill_attn_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkv = p.kv.n_kv_heads;

@@ -304,13 +304,10 @@ class DecodeBatch:
         self.reset()
 
 
-def attn_cluster_size(max_pages: int, n_clusters: int, sms: int = 148) -> int:
-    """CTAs per (session, KV head) cluster for K6: enough to spread the page
-    stream over the SMs (>= ~8 pages per CTA), a power of two <= 16."""
-    c = 1
-    while c < 16 and max_pages // (2 * c) >= 8 and n_clusters * 2 * c <= sms:
-        c *= 2
-    return c
+def attn_splits(max_pages: int, n_groups: int, sms: int = 148) -> int:
+    """Split-KV factor for K6: ~2 CTAs per SM over the (session, KV head)
+    groups, at least ~4 pages per split."""
+    return max(1, min((2 * sms) // max(1, n_groups), max(1, max_pages // 4)))
 
 
 class DecodeRunner:
@@ -323,7 +320,7 @@ class DecodeRunner:
     """
 
     def __init__(self, cfg: LlamaConfig, modules: list[ModuleWeights], kv: KVCache,
-                 batch: DecodeBatch, max_new: int, cluster: int | None = None, device: int = 0):
+                 batch: DecodeBatch, max_new: int, splits: int | None = None, device: int = 0):
         self.cfg, self.kv, self.b, self.max_new = cfg, kv, batch, max_new
         self.lib = _lib.load()
         dev = torch.device("cuda", device)
@@ -351,10 +348,16 @@ class DecodeRunner:
         self.logits = torch.empty(R, cfg.vocab, dtype=f32, device=dev)
         self.out_tokens = torch.full((R, max_new), -1, dtype=torch.int32, device=dev)
         self.rope = torch.from_numpy(rope_table(cfg)).to(dev)
-        self.cluster = cluster if cluster is not None else attn_cluster_size(
-            batch.max_sess_pages, batch.n_sess * cfg.n_kv_heads)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        self.splits = splits if splits is not None else attn_splits(
+            batch.max_sess_pages + batch.max_rps * ((max_new + 15) // 16),
+            batch.n_sess * cfg.n_kv_heads, sms)
+        wsb = C.c_int64()
+        _lib.check(self.lib.psk_decode_attn_workspace(batch.c_ref(), cfg.n_kv_heads, self.splits,
+                                                      C.byref(wsb)))
+        self.ws = torch.empty(wsb.value // 4 + 1, dtype=f32, device=dev)
         self.graph: torch.cuda.CUDAGraph | None = None
-        self.launches_per_step = 1 + L * 8 + 3
+        self.launches_per_step = 1 + L * 9 + 3
 
     # -- one step, eager ----------------------------------------------------
     def _step(self, s: int) -> None:
@@ -372,8 +375,8 @@ class DecodeRunner:
                              1, _ptr(self.qkv), s))
             chk(lib.psk_rope_append(bc, _ptr(self.qkv), cfg.n_heads, _ptr(self.rope), l, kvl,
                                     _ptr(self.q_rot), s))
-            chk(lib.psk_decode_attn(bc, _ptr(self.q_rot), cfg.n_heads, l, kvl, self.cluster,
-                                    _ptr(self.attn), s))
+            chk(lib.psk_decode_attn(bc, _ptr(self.q_rot), cfg.n_heads, l, kvl, self.splits,
+                                    _ptr(self.ws), _ptr(self.attn), s))
             chk(lib.psk_gemv(_ptr(self.attn), R, cfg.n_heads * cfg.head_dim, _ptr(self.p_wo[l]), mrs,
                              b.n_mod, d, 2, _ptr(self.h), s))
             chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_mlp_norm[l]), _ptr(b.t_row_mod),

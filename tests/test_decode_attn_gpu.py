@@ -12,7 +12,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, cluster, seed=0):
+def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0):
     from paper_2602_12029_b200 import _lib
     from paper_2602_12029_b200.model import (DecodeBatch, DecodeRow, KVCache, LlamaConfig,
                                              SessionSpec)
@@ -42,9 +42,13 @@ def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, cluster, seed=0):
     q = torch.randn(R, nq, 128, device="cuda", generator=g).to(torch.bfloat16)
     out = torch.full_like(q, float("nan"))
     layer = 1
-    L_ = _lib
-    L_.check(L_.load().psk_decode_attn(b.c_ref(), q.data_ptr(), nq, layer, kv.layout(), cluster,
-                                       out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    import ctypes
+    lib = _lib.load()
+    wsb = ctypes.c_int64()
+    _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), nkv, splits, ctypes.byref(wsb)))
+    ws = torch.empty(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
+    _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), nq, layer, kv.layout(), splits,
+                                   ws.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     grp = nq // nkv
     for j, row in enumerate(b.rows):
@@ -61,9 +65,9 @@ def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, cluster, seed=0):
         assert err <= 2e-2 * ref.abs().max().item() + 2e-3, f"row {j}: err {err}"
 
 
-@pytest.mark.parametrize("cluster", [1, 2, 4, 8, 16])
-def test_one_session_four_modules(cluster):
-    _case(32, 8, [4095], [4], [0, 3, 17, 255], cluster)
+@pytest.mark.parametrize("splits", [1, 3, 8, 37, 64])
+def test_one_session_four_modules(splits):
+    _case(32, 8, [4095], [4], [0, 3, 17, 255], splits)
 
 
 def test_sixteen_modules_fanout():

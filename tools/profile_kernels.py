@@ -30,11 +30,14 @@ def attn(shared, modules, reps=4):
     b = DecodeBatch([SessionSpec(shared_len=shared, pages=list(range(n_sh)))], rows, modules)
     q = torch.randn(modules, 32, 128, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)
-    from paper_2602_12029_b200.model import attn_cluster_size
-    cl = attn_cluster_size(n_sh, 8)
+    from paper_2602_12029_b200.model import attn_splits
+    ns = attn_splits(n_sh + modules, 8)
+    wsb = C.c_int64()
+    _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), 8, ns, C.byref(wsb)))
+    ws = torch.empty(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
     for i in range(reps):
-        _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), 32, i % 2, kv.layout(), cl,
-                                       out.data_ptr(), s))
+        _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), 32, i % 2, kv.layout(), ns,
+                                       ws.data_ptr(), out.data_ptr(), s))
     torch.cuda.synchronize()
 
 
