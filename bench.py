@@ -153,17 +153,34 @@ def cpu_reference_sample(n_sessions: int = 1) -> dict:
 
 # --------------------------------------------------------- kernel timing ---
 
-def _time_launches(fn, n: int) -> float:
+def _time_launches(fn, n: int, graph: bool = True) -> float:
+    """Average device time of one fn() launch sequence: n launches captured in
+    a CUDA graph (no host launch overhead in the timing), replayed and timed
+    with CUDA events on the capturing stream."""
     import torch
-    st = torch.cuda.current_stream()
-    for _ in range(3):
-        fn()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            fn()
     st.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(st)
-    for _ in range(n):
-        fn()
-    b.record(st)
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(n):
+                fn()
+        run = g.replay
+    else:
+        def run():
+            for _ in range(n):
+                fn()
+    with torch.cuda.stream(st):
+        run()
+        st.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        run()
+        b.record(st)
     b.synchronize()
     return a.elapsed_time(b) / 1e3 / n
 
@@ -183,7 +200,8 @@ def gemv_roofline(eng, peaks) -> dict:
         l = it[0] % cfg.n_layers
         it[0] += 1
         _lib.check(lib.psk_gemv(r.xn.data_ptr(), b.n_rows, cfg.d_model, r.p_wgu[l].data_ptr(),
-                                b.t_mrs.data_ptr(), b.n_mod, 2 * cfg.ffn, 3, r.act.data_ptr(), s))
+                                b.t_mrs.data_ptr(), b.n_mod, 2 * cfg.ffn, 3, r.act.data_ptr(),
+                                torch.cuda.current_stream().cuda_stream))
     dt = _time_launches(launch, 4 * cfg.n_layers)
     nbytes = b.n_mod * 2 * cfg.ffn * cfg.d_model * 2 + b.n_rows * (cfg.d_model + cfg.ffn) * 2
     gbs = nbytes / dt / 1e9
@@ -209,7 +227,8 @@ def decode_attn_roofline(eng, peaks) -> dict:
         l = it[0] % cfg.n_layers
         it[0] += 1
         _lib.check(r.lib.psk_decode_attn(b.c_ref(), r.q_rot.data_ptr(), cfg.n_heads, l, kvl,
-                                         r.splits, r.ws.data_ptr(), r.attn.data_ptr(), s))
+                                         r.splits, r.ws.data_ptr(), r.attn.data_ptr(),
+                                         torch.cuda.current_stream().cuda_stream))
     dt = _time_launches(launch, 4 * cfg.n_layers)
     shared = int(b.t_sess_len.sum().item())
     priv = int((b.t_priv_len + 1).sum().item())
@@ -244,7 +263,7 @@ def decode_attn_fanout(peaks, shared_tokens=32767, modules=16) -> dict:
     ns = attn_splits(n_sh + modules, cfg.n_kv_heads, torch.cuda.get_device_properties(0).multi_processor_count)
     wsb = ctypes.c_int64()
     _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), cfg.n_kv_heads, ns, ctypes.byref(wsb)))
-    ws = torch.empty(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
+    ws = torch.zeros(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
     it = [0]
     kvl = kv.layout()
 
@@ -252,7 +271,8 @@ def decode_attn_fanout(peaks, shared_tokens=32767, modules=16) -> dict:
         l = it[0] % cfg.n_layers
         it[0] += 1
         _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), cfg.n_heads, l, kvl, ns,
-                                       ws.data_ptr(), out.data_ptr(), s))
+                                       ws.data_ptr(), out.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream))
     dt = _time_launches(launch, 2 * cfg.n_layers)
     per_tok = 2 * cfg.n_kv_heads * cfg.head_dim * 2
     nbytes = (shared_tokens + modules) * per_tok + 2 * modules * cfg.n_heads * cfg.head_dim * 2

@@ -8,15 +8,15 @@
 // Partial kernel: one CTA = (session, KV head, split). Its page stream is the
 // split's slice of [shared prompt pages | row 0 private pages | row 1 private
 // pages | ...]. A producer warp streams every page with TMA (two 128B-swizzled
-// [16 x 64] boxes per 4 KiB K / V tile) through an 8-stage mbarrier ring; 8
+// [16 x 64] boxes per 4 KiB K / V tile) through a 16-stage (128 KiB) mbarrier ring; 8
 // consumer warps map to (query m-tile, page subset), so each page is read
 // from HBM once per step for ALL query rows of the session (GQA group x
 // co-batched decode modules, <= 64 rows); private pages mask the rows they do
 // not own. Warps fold their online-softmax state in fragment order, and the
 // CTA writes one (m, l, O) partial per query row.
-// Merge kernel (launched with programmatic dependent launch so its launch
-// overlaps the partial kernel's tail): one warp per (row, q head) folds the
-// split partials by log-sum-exp and writes bf16 output.
+// The last CTA to finish for a (session, KV head) — found with one atomic
+// per CTA — folds the split partials by log-sum-exp and writes the bf16
+// output: no second kernel, no separate launch latency.
 //
 // (A 16-CTA-cluster / DSMEM-reduction variant was measured first: at this
 // shared-memory footprint only 7 such clusters are co-resident on a B200, so
@@ -33,16 +33,16 @@ namespace dattn {
 constexpr int HD = 128, PT = 16;
 constexpr int CW = 8;                   // consumer warps
 constexpr int THREADS = (CW + 1) * 32;  // + 1 TMA producer warp
-constexpr int NST = 8;                  // pipeline stages (1 page = K + V each)
+constexpr int NST = 16;                 // pipeline stages (1 page = K + V each): 128 KiB in flight
 constexpr int TILE = PT * HD * 2;       // 4 KiB
 constexpr int STAGE = 2 * TILE;
 constexpr int GMAX = 64;
 constexpr int MAXR = 16;                // decode rows per session
-constexpr int OFF_Q = NST * STAGE;      // 64 KiB
+constexpr int OFF_Q = NST * STAGE;      // 128 KiB
 constexpr int OFF_BAR = OFF_Q + GMAX * 256;  // +16 KiB
 constexpr int MAXP = 1024;              // page indices staged in smem
 constexpr int OFF_PG = OFF_BAR + 2 * NST * 8;
-constexpr int SMEM = OFF_PG + MAXP * 4 + 1024;  // ~86 KiB (+ alignment slack): 2 CTAs / SM
+constexpr int SMEM = OFF_PG + MAXP * 4 + 1024;  // ~150 KiB (+ alignment slack): 1 CTA / SM
 constexpr int FRAG = 68;                // floats per lane in the fold scratch (64 O + m0 m1 l0 l1)
 static_assert(CW * 32 * FRAG * 4 <= OFF_BAR, "fold scratch must fit in ring + Q");
 
@@ -54,6 +54,7 @@ struct Params {
   float* pm;               // [items][GMAX]
   float* pl;               // [items][GMAX]
   float* po;               // [items][GMAX][HD]
+  int* counters;           // [n_sess * nkv] split arrivals (zero between launches)
   int nq, grp, layer, ns;
   float scale_log2;
 };
@@ -64,7 +65,7 @@ __device__ __forceinline__ uint32_t tile_addr(uint32_t tile, int tok, int c16) {
   return tile + ((c16 >> 3) << 11) + tok * 128 + (((c16 & 7) ^ (tok & 7)) << 4);
 }
 
-__global__ void __maxnreg__(112)  // 2 CTAs x 288 threads per SM
+__global__ void __launch_bounds__(THREADS, 1)
     decode_attn_partial(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ Params p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -86,9 +87,6 @@ __global__ void __maxnreg__(112)  // 2 CTAs x 288 threads per SM
   const int T = (G + 15) / 16;
   const int Tp = T <= 1 ? 1 : (T == 2 ? 2 : 4);
   const int ways = CW / Tp;
-
-  // let the merge kernel launch now; it waits for our completion itself
-  asm volatile("griddepcontrol.launch_dependents;");
 
   // prologue: one latency round trip for all rows (no dependent chains)
   if (threadIdx.x < nr) {
@@ -172,11 +170,14 @@ __global__ void __maxnreg__(112)  // 2 CTAs x 288 threads per SM
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   if (active) {
-    // Q fragments are re-read from shared memory per k-step (ldmatrix) rather
-    // than pinned in 32 registers: keeps the kernel at 2 CTAs / SM unspilled.
-    const uint32_t qs = smem_u32(smem + OFF_Q);
-    const int qrow = tile * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
-    const int qhalf = lane >> 4;
+    uint32_t qa[8][4];
+    {
+      const uint32_t qs = smem_u32(smem + OFF_Q);
+      const int qrow = tile * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+        ldmatrix_x4(qs + swz256(qrow, 2 * ks + (lane >> 4)), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+    }
     const int gA = tile * 16 + (lane >> 2), gB = gA + 8;
     const int ownA = gA < G ? gA / p.grp : -2, ownB = gB < G ? gB / p.grp : -2;
     for (int j = way; j < np; j += ways) {
@@ -202,11 +203,10 @@ __global__ void __maxnreg__(112)  // 2 CTAs x 288 threads per SM
         const int tok = (mi >> 1) * 8 + ri;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
-          uint32_t a[4], b0, b1, b2, b3;
-          ldmatrix_x4(qs + swz256(qrow, 2 * ks + qhalf), a[0], a[1], a[2], a[3]);
+          uint32_t b0, b1, b2, b3;
           ldmatrix_x4(tile_addr(kt, tok, 2 * ks + (mi & 1)), b0, b1, b2, b3);
-          mma_bf16_16816(s[0], a, b0, b1);
-          mma_bf16_16816(s[1], a, b2, b3);
+          mma_bf16_16816(s[0], qa[ks], b0, b1);
+          mma_bf16_16816(s[1], qa[ks], b2, b3);
         }
       }
       const bool okA = owner < 0 || owner == ownA;
@@ -330,57 +330,52 @@ __global__ void __maxnreg__(112)  // 2 CTAs x 288 threads per SM
       }
     }
   }
-}
 
-// One warp per (row, q head); lane owns 4 of the 128 dims.
-__global__ void __launch_bounds__(128) decode_attn_merge(const __grid_constant__ Params p) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x;
-  const int qh = blockIdx.y * 4 + warp;
-  if (qh >= p.nq) return;
-  const int nkv = p.kv.n_kv_heads;
-  const int h = qh / p.grp;
-  const int g = p.b.row_in_sess[r] * p.grp + qh % p.grp;
-  const int s = p.b.row_sess[r];
-  const int64_t base = ((int64_t)(s * nkv + h) * p.ns) * GMAX + g;
-  float M = -INFINITY, L = 0.f;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  constexpr int U = 8;
-  for (int j0 = 0; j0 < p.ns; j0 += U) {
-    float mj[U], lj[U];
-    float4 oj[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u;
-      if (j < p.ns) {
-        const int64_t sl = base + (int64_t)j * GMAX;
-        mj[u] = p.pm[sl];
-        lj[u] = p.pl[sl];
-        oj[u] = *reinterpret_cast<const float4*>(p.po + sl * HD + lane * 4);
-      } else {
-        mj[u] = -INFINITY;
-        lj[u] = 0.f;
-        oj[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const float Mn = fmaxf(M, mj[u]);
-      if (Mn == -INFINITY) continue;
-      const float a = exp2f(M - Mn), c = exp2f(mj[u] - Mn);
-      L = L * a + lj[u] * c;
-      acc.x = acc.x * a + oj[u].x * c;
-      acc.y = acc.y * a + oj[u].y * c;
-      acc.z = acc.z * a + oj[u].z * c;
-      acc.w = acc.w * a + oj[u].w * c;
-      M = Mn;
-    }
+  // -- the last CTA to finish for this (session, KV head) merges the splits
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int old = atomicAdd(&p.counters[sess * nkv + h], 1);
+    s_last = old == p.ns - 1;
   }
-  const float inv = L > 0.f ? 1.f / L : 0.f;
-  __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(p.out + ((int64_t)r * p.nq + qh) * HD + lane * 4);
-  o[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-  o[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int64_t gbase = (int64_t)(sess * nkv + h) * p.ns * GMAX;
+  float* fac = reinterpret_cast<float*>(smem);  // [G][ns] weights, then [G] 1/L
+  float* invl = fac + GMAX * p.ns;
+  for (int g = threadIdx.x; g < G; g += THREADS) {
+    float M = -INFINITY;
+    for (int j = 0; j < p.ns; ++j) M = fmaxf(M, __ldcg(p.pm + gbase + (int64_t)j * GMAX + g));
+    const float Mr = M == -INFINITY ? 0.f : M;
+    float L = 0.f;
+    for (int j = 0; j < p.ns; ++j) {
+      const int64_t sl = gbase + (int64_t)j * GMAX + g;
+      const float f = exp2f(__ldcg(p.pm + sl) - Mr);
+      fac[g * p.ns + j] = f;
+      L += f * __ldcg(p.pl + sl);
+    }
+    invl[g] = L > 0.f ? 1.f / L : 0.f;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < G * HD; e += THREADS) {
+    const int g = e / HD, d = e % HD;
+    const float* fg = fac + g * p.ns;
+    float acc = 0.f;
+    int j = 0;
+    for (; j + 8 <= p.ns; j += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(p.po + (gbase + (int64_t)(j + u) * GMAX + g) * HD + d);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += fg[j + u] * v[u];
+    }
+    for (; j < p.ns; ++j) acc += fg[j] * __ldcg(p.po + (gbase + (int64_t)j * GMAX + g) * HD + d);
+    const int qh = h * p.grp + g % p.grp;
+    p.out[((int64_t)s_rows[g / p.grp] * p.nq + qh) * HD + d] = f2bf(acc * invl[g]);
+  }
+  if (threadIdx.x == 0) p.counters[sess * nkv + h] = 0;  // ready for the next launch
 }
 
 // ------------------------------------------------------------ host side --
@@ -431,6 +426,8 @@ static int kv_map(const psk_kv_layout& kv, CUtensorMap* out) {
   return PSK_OK;
 }
 
+static int64_t counter_bytes(int64_t n) { return ((n * 4 + 255) / 256) * 256; }
+
 }  // namespace dattn
 }  // namespace psk
 
@@ -442,7 +439,7 @@ int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int
                               int64_t* bytes) {
   PSK_CHECK_ARG(b && bytes && splits >= 1, "psk_decode_attn_workspace: bad args");
   const int64_t items = (int64_t)b->n_sess * n_kv_heads * splits;
-  *bytes = items * GMAX * (HD + 2) * 4;
+  *bytes = counter_bytes(b->n_sess * n_kv_heads) + items * GMAX * (HD + 2) * 4;
   return PSK_OK;
 }
 
@@ -468,7 +465,9 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   p.layer = layer;
   p.ns = splits;
   const int64_t items = (int64_t)b->n_sess * kv.n_kv_heads * splits;
-  float* ws = reinterpret_cast<float*>(workspace);
+  p.counters = reinterpret_cast<int*>(workspace);
+  float* ws = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
+                                       counter_bytes(b->n_sess * kv.n_kv_heads));
   p.pm = ws;
   p.pl = ws + items * GMAX;
   p.po = ws + 2 * items * GMAX;
@@ -482,16 +481,7 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   }
   decode_attn_partial<<<(unsigned)items, THREADS, SMEM, s>>>(map, p);
   PSK_LAUNCH_CHECK();
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(b->n_rows, (n_q_heads + 3) / 4);
-  cfg.blockDim = dim3(128);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_merge, p));
+
   return PSK_OK;
 }
 

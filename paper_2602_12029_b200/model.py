@@ -305,9 +305,9 @@ class DecodeBatch:
 
 
 def attn_splits(max_pages: int, n_groups: int, sms: int = 148) -> int:
-    """Split-KV factor for K6: ~2 CTAs per SM over the (session, KV head)
-    groups, at least ~4 pages per split."""
-    return max(1, min((2 * sms) // max(1, n_groups), max(1, max_pages // 4)))
+    """Split-KV factor for K6: one CTA per SM over the (session, KV head)
+    groups, at least ~4 pages per split, at most 512 splits."""
+    return max(1, min(sms // max(1, n_groups), max(1, max_pages // 4), 512))
 
 
 class DecodeRunner:
@@ -355,7 +355,7 @@ class DecodeRunner:
         wsb = C.c_int64()
         _lib.check(self.lib.psk_decode_attn_workspace(batch.c_ref(), cfg.n_kv_heads, self.splits,
                                                       C.byref(wsb)))
-        self.ws = torch.empty(wsb.value // 4 + 1, dtype=f32, device=dev)
+        self.ws = torch.zeros(wsb.value // 4 + 1, dtype=f32, device=dev)  # split counters start at 0
         self.graph: torch.cuda.CUDAGraph | None = None
         self.launches_per_step = 1 + L * 9 + 3
 

@@ -46,7 +46,7 @@ def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0):
     lib = _lib.load()
     wsb = ctypes.c_int64()
     _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), nkv, splits, ctypes.byref(wsb)))
-    ws = torch.empty(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
+    ws = torch.zeros(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
     _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), nq, layer, kv.layout(), splits,
                                    ws.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()

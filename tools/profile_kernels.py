@@ -34,7 +34,7 @@ def attn(shared, modules, reps=4):
     ns = attn_splits(n_sh + modules, 8)
     wsb = C.c_int64()
     _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), 8, ns, C.byref(wsb)))
-    ws = torch.empty(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
+    ws = torch.zeros(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
     for i in range(reps):
         _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), 32, i % 2, kv.layout(), ns,
                                        ws.data_ptr(), out.data_ptr(), s))
