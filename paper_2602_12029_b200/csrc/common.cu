@@ -2,6 +2,7 @@
 #include "common.cuh"
 
 #include <stdarg.h>
+#include <stdlib.h>
 
 namespace psk {
 
@@ -34,6 +35,45 @@ __global__ void fill_bf16_kernel(__nv_bfloat16* __restrict__ dst, int64_t n, flo
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   __nv_bfloat16 b = f2bf(v);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = b;
+}
+
+static unsigned long long* s_trace_buf = nullptr;
+static int s_trace_cap = 0;
+
+unsigned long long* trace_buffer(int n_ctas) {
+  static const bool on = getenv("PSK_TRACE") != nullptr;
+  if (!on) return nullptr;
+  if (n_ctas > s_trace_cap) {
+    if (s_trace_buf) cudaFree(s_trace_buf);
+    cudaMalloc(&s_trace_buf, sizeof(unsigned long long) * 8 * n_ctas);
+    s_trace_cap = n_ctas;
+  }
+  cudaMemset(s_trace_buf, 0, sizeof(unsigned long long) * 8 * n_ctas);
+  return s_trace_buf;
+}
+
+void trace_report(const char* kernel, int n, int nph, const char* const* names) {
+  cudaDeviceSynchronize();
+  unsigned long long* h = (unsigned long long*)malloc(sizeof(unsigned long long) * 8 * n);
+  cudaMemcpy(h, s_trace_buf, sizeof(unsigned long long) * 8 * n, cudaMemcpyDeviceToHost);
+  unsigned long long t0 = ~0ull;
+  for (int i = 0; i < n; ++i)
+    if (h[i * 8] && h[i * 8] < t0) t0 = h[i * 8];
+  fprintf(stderr, "[trace %s] %d CTAs, us since first CTA entry: min / avg / max\n", kernel, n);
+  for (int k = 0; k < nph; ++k) {
+    double mn = 1e30, mx = 0, av = 0;
+    int c = 0;
+    for (int i = 0; i < n; ++i) {
+      if (!h[i * 8 + k]) continue;
+      double v = (double)(h[i * 8 + k] - t0) / 1000.0;
+      mn = v < mn ? v : mn;
+      mx = v > mx ? v : mx;
+      av += v;
+      ++c;
+    }
+    if (c) fprintf(stderr, "  %-14s %8.2f %8.2f %8.2f  (%d CTAs)\n", names[k], mn, av / c, mx, c);
+  }
+  free(h);
 }
 
 static int grid_for(int64_t n, int threads) {

@@ -79,6 +79,33 @@ __device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
   return r;
 }
 
+// Phase tracing (debug/tuning; off unless PSK_TRACE is set in the
+// environment): thread 0 of each CTA stamps %globaltimer at up to 8 phases.
+static __device__ unsigned long long* g_trace = nullptr;  // one per translation unit
+__device__ __forceinline__ void trace_stamp(int k) {
+  unsigned long long* t = g_trace;
+  if (t != nullptr && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    t[(blockIdx.x + (size_t)blockIdx.y * gridDim.x) * 8 + k] = v;
+  }
+}
+// Host: trace_buffer() returns a zeroed device buffer for n CTAs (nullptr
+// when PSK_TRACE is unset); trace_report() prints per-phase min/avg/max (us
+// since the first CTA's stamp 0) and disarms.
+unsigned long long* trace_buffer(int n_ctas);
+void trace_report(const char* kernel, int n_ctas, int n_phases, const char* const* names);
+static inline bool trace_arm(int n_ctas) {
+  unsigned long long* b = trace_buffer(n_ctas);
+  if (!b) return false;
+  cudaMemcpyToSymbol(g_trace, &b, sizeof(void*));
+  return true;
+}
+static inline void trace_disarm() {
+  unsigned long long* nul = nullptr;
+  cudaMemcpyToSymbol(g_trace, &nul, sizeof(void*));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

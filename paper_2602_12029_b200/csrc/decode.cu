@@ -217,6 +217,8 @@ __device__ __forceinline__ __nv_bfloat16* kv_ptr(const psk_kv_layout& kv, int32_
 __global__ void rope_append_kernel(psk_decode_batch b, const float* __restrict__ qkv, int nq,
                                    const float* __restrict__ rope, int layer, psk_kv_layout kv,
                                    __nv_bfloat16* __restrict__ q_rot) {
+  // the attention kernel (PDL-launched next) may start its table prologue now
+  asm volatile("griddepcontrol.launch_dependents;");
   const int r = blockIdx.x;
   const int nkv = kv.n_kv_heads;
   const int idx = b.priv_len[r];

@@ -14,9 +14,11 @@
 // co-batched decode modules, <= 64 rows); private pages mask the rows they do
 // not own. Warps fold their online-softmax state in fragment order, and the
 // CTA writes one (m, l, O) partial per query row.
-// The last CTA to finish for a (session, KV head) — found with one atomic
-// per CTA — folds the split partials by log-sum-exp and writes the bf16
-// output: no second kernel, no separate launch latency.
+// A merge kernel (one thread per output element, all split partials in
+// flight at once) folds the partials by log-sum-exp. Both kernels use
+// programmatic dependent launch: the partial kernel's prologue (row and page
+// tables) overlaps its producer (RoPE + KV append) and the merge launch
+// overlaps the partial kernel's tail.
 //
 // (A 16-CTA-cluster / DSMEM-reduction variant was measured first: at this
 // shared-memory footprint only 7 such clusters are co-resident on a B200, so
@@ -54,7 +56,6 @@ struct Params {
   float* pm;               // [items][GMAX]
   float* pl;               // [items][GMAX]
   float* po;               // [items][GMAX][HD]
-  int* counters;           // [n_sess * nkv] split arrivals (zero between launches)
   int nq, grp, layer, ns;
   float scale_log2;
 };
@@ -76,6 +77,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __shared__ int s_rows[MAXR], s_plen[MAXR], s_pstart[MAXR + 1];
   __shared__ int s_ps, s_ls, s_total;
 
+  trace_stamp(0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkv = p.kv.n_kv_heads;
   const int item = blockIdx.x;
@@ -115,6 +117,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tma::prefetch_map(&kvmap);
   }
   __syncthreads();
+  trace_stamp(1);
   const int total = s_total;
   const int k0 = (int)((int64_t)j_split * total / p.ns);
   const int k1 = (int)((int64_t)(j_split + 1) * total / p.ns);
@@ -126,8 +129,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     while (k >= s_pstart[i + 1]) ++i;
     return p.b.row_pages[(int64_t)s_rows[i] * p.b.max_row_pages + (k - s_pstart[i])];
   };
-  // page indices and Q tile -> shared memory
+  // page indices -> shared memory (tables are static within a step)
   for (int j = threadIdx.x; j < np && j < MAXP; j += THREADS) s_page[j] = page_of(k0 + j);
+  // everything above overlaps the producer of q / the new K,V (PDL)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   {
     const uint32_t qs = smem_u32(smem + OFF_Q);
     for (int e = threadIdx.x; e < T * 16 * 16; e += THREADS) {
@@ -142,6 +147,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
   __syncthreads();
+  trace_stamp(2);
 
   const uint32_t ring = smem_u32(smem);
   if (warp == CW) {
@@ -273,6 +279,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
   }
   __syncthreads();  // ring drained: every fetched page was consumed
+  trace_stamp(3);
+  asm volatile("griddepcontrol.launch_dependents;");
 
   // -- fold the `ways` warps of each m-tile in fragment order (ring + Q reused)
   float* scr = reinterpret_cast<float*>(smem);  // [CW][32][FRAG]
@@ -331,51 +339,49 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
 
-  // -- the last CTA to finish for this (session, KV head) merges the splits
-  __shared__ int s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int old = atomicAdd(&p.counters[sess * nkv + h], 1);
-    s_last = old == p.ns - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int64_t gbase = (int64_t)(sess * nkv + h) * p.ns * GMAX;
-  float* fac = reinterpret_cast<float*>(smem);  // [G][ns] weights, then [G] 1/L
-  float* invl = fac + GMAX * p.ns;
-  for (int g = threadIdx.x; g < G; g += THREADS) {
-    float M = -INFINITY;
-    for (int j = 0; j < p.ns; ++j) M = fmaxf(M, __ldcg(p.pm + gbase + (int64_t)j * GMAX + g));
-    const float Mr = M == -INFINITY ? 0.f : M;
-    float L = 0.f;
-    for (int j = 0; j < p.ns; ++j) {
-      const int64_t sl = gbase + (int64_t)j * GMAX + g;
-      const float f = exp2f(__ldcg(p.pm + sl) - Mr);
-      fac[g * p.ns + j] = f;
-      L += f * __ldcg(p.pl + sl);
-    }
-    invl[g] = L > 0.f ? 1.f / L : 0.f;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < G * HD; e += THREADS) {
-    const int g = e / HD, d = e % HD;
-    const float* fg = fac + g * p.ns;
-    float acc = 0.f;
-    int j = 0;
-    for (; j + 8 <= p.ns; j += 8) {
-      float v[8];
+  trace_stamp(4);
+}
+
+// Merge: one CTA per (row, q head), one thread per head dim; every split's
+// (m, l, o) is loaded up front (32 splits in flight per thread) and folded by
+// log-sum-exp. Launched with programmatic dependent launch: it is scheduled
+// while the partial kernel drains and waits on griddepcontrol for its data.
+constexpr int MERGE_U = 32;
+__global__ void __launch_bounds__(HD) decode_attn_merge(const __grid_constant__ Params p) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int r = blockIdx.x, qh = blockIdx.y, d = threadIdx.x;
+  const int nkv = p.kv.n_kv_heads;
+  const int h = qh / p.grp;
+  const int g = p.b.row_in_sess[r] * p.grp + qh % p.grp;
+  const int64_t base = (int64_t)(p.b.row_sess[r] * nkv + h) * p.ns * GMAX + g;
+  float M = -INFINITY, L = 0.f, acc = 0.f;
+  for (int j0 = 0; j0 < p.ns; j0 += MERGE_U) {
+    float mj[MERGE_U], lj[MERGE_U], oj[MERGE_U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcg(p.po + (gbase + (int64_t)(j + u) * GMAX + g) * HD + d);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc += fg[j + u] * v[u];
+    for (int u = 0; u < MERGE_U; ++u) {
+      const int j = j0 + u;
+      const int64_t sl = base + (int64_t)j * GMAX;
+      const bool ok = j < p.ns;
+      mj[u] = ok ? __ldcg(p.pm + sl) : -INFINITY;
+      lj[u] = ok ? __ldcg(p.pl + sl) : 0.f;
+      oj[u] = ok ? __ldcg(p.po + sl * HD + d) : 0.f;
     }
-    for (; j < p.ns; ++j) acc += fg[j] * __ldcg(p.po + (gbase + (int64_t)j * GMAX + g) * HD + d);
-    const int qh = h * p.grp + g % p.grp;
-    p.out[((int64_t)s_rows[g / p.grp] * p.nq + qh) * HD + d] = f2bf(acc * invl[g]);
+    float Mc = M;
+#pragma unroll
+    for (int u = 0; u < MERGE_U; ++u) Mc = fmaxf(Mc, mj[u]);
+    const float Mr = Mc == -INFINITY ? 0.f : Mc;
+    const float a = exp2f(M - Mr);
+    L *= a;
+    acc *= a;
+#pragma unroll
+    for (int u = 0; u < MERGE_U; ++u) {
+      const float f = exp2f(mj[u] - Mr);
+      L += f * lj[u];
+      acc += f * oj[u];
+    }
+    M = Mc;
   }
-  if (threadIdx.x == 0) p.counters[sess * nkv + h] = 0;  // ready for the next launch
+  p.out[((int64_t)r * p.nq + qh) * HD + d] = f2bf(L > 0.f ? acc / L : 0.f);
 }
 
 // ------------------------------------------------------------ host side --
@@ -426,8 +432,6 @@ static int kv_map(const psk_kv_layout& kv, CUtensorMap* out) {
   return PSK_OK;
 }
 
-static int64_t counter_bytes(int64_t n) { return ((n * 4 + 255) / 256) * 256; }
-
 }  // namespace dattn
 }  // namespace psk
 
@@ -439,7 +443,7 @@ int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int
                               int64_t* bytes) {
   PSK_CHECK_ARG(b && bytes && splits >= 1, "psk_decode_attn_workspace: bad args");
   const int64_t items = (int64_t)b->n_sess * n_kv_heads * splits;
-  *bytes = counter_bytes(b->n_sess * n_kv_heads) + items * GMAX * (HD + 2) * 4;
+  *bytes = items * GMAX * (HD + 2) * 4;
   return PSK_OK;
 }
 
@@ -465,9 +469,7 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   p.layer = layer;
   p.ns = splits;
   const int64_t items = (int64_t)b->n_sess * kv.n_kv_heads * splits;
-  p.counters = reinterpret_cast<int*>(workspace);
-  float* ws = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
-                                       counter_bytes(b->n_sess * kv.n_kv_heads));
+  float* ws = reinterpret_cast<float*>(workspace);
   p.pm = ws;
   p.pl = ws + items * GMAX;
   p.po = ws + 2 * items * GMAX;
@@ -479,8 +481,30 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
                                       SMEM));
     init = true;
   }
-  decode_attn_partial<<<(unsigned)items, THREADS, SMEM, s>>>(map, p);
-  PSK_LAUNCH_CHECK();
+  const bool tr = psk::trace_arm((int)items);
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)items);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_partial, map, p));
+  if (tr) {
+    static const char* names[] = {"entry", "prologue", "staged", "loop-done", "folded"};
+    psk::trace_report("decode_attn", (int)items, 5, names);
+    psk::trace_disarm();
+  }
+  cudaLaunchConfig_t mcfg = {};
+  mcfg.gridDim = dim3(b->n_rows, n_q_heads);
+  mcfg.blockDim = dim3(HD);
+  mcfg.stream = s;
+  mcfg.attrs = pdl;
+  mcfg.numAttrs = 1;
+  PSK_CUDA_TRY(cudaLaunchKernelEx(&mcfg, decode_attn_merge, p));
 
   return PSK_OK;
 }
