@@ -119,10 +119,11 @@ def load() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not LIB_PATH.exists():
+    path = Path(os.environ.get("PSK_LIB", str(LIB_PATH)))  # tuning variants (build --define/--out)
+    if not path.exists():
         raise PskError(PSK_EINVAL, f"{LIB_PATH} missing: run `python -m paper_2602_12029_b200.build` "
                                    "(the CUDA extension is required; there is no CPU fallback)")
-    lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_LOCAL | os.RTLD_NOW)
+    lib = C.CDLL(str(path), mode=os.RTLD_LOCAL | os.RTLD_NOW)
     for name, args in _SIGS.items():
         fn = getattr(lib, name)
         fn.argtypes = args

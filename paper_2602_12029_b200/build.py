@@ -97,11 +97,39 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_variant(defines: list[str], out: Path) -> Path:
+    """Tuning builds: every source with extra -D flags, linked to `out`
+    (load it with PSK_LIB=<out>). No object cache."""
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        objs = []
+        extra = [f"-D{d}" for d in defines]
+        def one(src):
+            o = Path(td) / (src.stem + ".o")
+            r = subprocess.run([NVCC, *FLAGS, *extra, "-c", str(src), "-o", str(o)], capture_output=True,
+                               text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr}")
+            return o
+        with cf.ThreadPoolExecutor(max_workers=8) as ex:
+            objs = list(ex.map(one, _sources()))
+        r = subprocess.run([NVCC, *ARCH, "-shared", "-o", str(out), *map(str, objs), "-lcudart_static",
+                            "-lrt", "-ldl", "-lpthread"], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stderr}")
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--define", action="append", default=[], help="variant build: -D flag")
+    ap.add_argument("--out", type=Path, help="variant build output .so")
     a = ap.parse_args()
+    if a.define or a.out:
+        print(build_variant(a.define, a.out or PKG / "libpsk_variant.so"))
+        return
     print(build(force=a.force, verbose=a.verbose))
 
 

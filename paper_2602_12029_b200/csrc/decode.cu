@@ -81,11 +81,20 @@ __global__ void rmsnorm_rows_kernel(const float* __restrict__ h, int d,
 // fixed shared-memory slots (no atomics) and are summed in a fixed order,
 // so results are bit-reproducible run to run.
 constexpr int GEMV_THREADS = 256;
-constexpr int GEMV_V = 4;                  // 16-byte loads per lane per unit
+#ifndef PSK_GEMV_V
+#define PSK_GEMV_V 4
+#endif
+#ifndef PSK_GEMV_CTAS
+#define PSK_GEMV_CTAS 3
+#endif
+#ifndef PSK_GEMV_PIPE
+#define PSK_GEMV_PIPE 1
+#endif
+constexpr int GEMV_V = PSK_GEMV_V;         // 16-byte loads per lane per unit
 constexpr int GEMV_CH = 32 * 8 * GEMV_V;   // elements per unit (1024)
 
 template <int MAXM, int EPI>
-__global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(
+__global__ void __launch_bounds__(GEMV_THREADS, PSK_GEMV_CTAS) gemv_kernel(  // one resident wave
     const __nv_bfloat16* __restrict__ X, int K, const __nv_bfloat16* const* W,
     const int32_t* __restrict__ mrs, int n_mod, int N, int align, void* out) {
   extern __shared__ float slots[];  // [rows_cta][cpr][MAXM]
@@ -105,7 +114,6 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(
 #pragma unroll
   for (int m = 0; m < MAXM; ++m) acc[m] = 0.f;
   int cur_row = -1, cur_slot = 0, M = 0, xbase = 0;
-  const __nv_bfloat16* wrow = nullptr;
 
   // (a macro, not a by-reference lambda: that would put acc[] in local memory)
 #define GEMV_FLUSH()                                                                   \
@@ -122,27 +130,40 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(
   for (int i = threadIdx.x; i < rows * cpr * MAXM; i += GEMV_THREADS) slots[i] = 0.f;
   __syncthreads();
 
+  // Software pipeline: the weight loads of unit u+1 are issued before the
+  // FMAs of unit u, so each lane keeps 2 x GEMV_V x 16 B of HBM reads in flight.
+  uint4 wn[GEMV_V];
+  int n_rl = 0, n_ch = 0, n_M = 0, n_xb = 0;
+#define GEMV_FETCH(UU)                                                          \
+  {                                                                             \
+    n_rl = (int)((UU) / cpr);                                                   \
+    n_ch = (int)((UU) % cpr);                                                   \
+    const int64_t g_ = g0 + n_rl;                                               \
+    const int mod_ = (int)(g_ / N);                                             \
+    n_xb = mrs[mod_];                                                           \
+    n_M = mrs[mod_ + 1] - n_xb;                                                 \
+    const __nv_bfloat16* wr_ = W[mod_] + (int64_t)(g_ % N) * K;                 \
+    _Pragma("unroll") for (int j = 0; j < GEMV_V; ++j) {                        \
+      const int k = n_ch * GEMV_CH + j * 256 + lane * 8;                        \
+      wn[j] = (n_M > 0 && k < K) ? ld_stream_v4(wr_ + k) : make_uint4(0, 0, 0, 0); \
+    }                                                                           \
+  }
+  if (PSK_GEMV_PIPE && u0 < u1) GEMV_FETCH(u0);
   for (int64_t u = u0; u < u1; ++u) {
-    const int rl = (int)(u / cpr);
-    const int ch = (int)(u % cpr);
+    if (!PSK_GEMV_PIPE) GEMV_FETCH(u);
+    uint4 w[GEMV_V];
+#pragma unroll
+    for (int j = 0; j < GEMV_V; ++j) w[j] = wn[j];
+    const int rl = n_rl, ch = n_ch, uM = n_M, uxb = n_xb;
+    if (PSK_GEMV_PIPE && u + 1 < u1) GEMV_FETCH(u + 1);
     if (rl != cur_row) {
       GEMV_FLUSH();
       cur_row = rl;
       cur_slot = ch;
-      const int64_t g = g0 + rl;
-      const int mod = (int)(g / N);
-      const int n = (int)(g % N);
-      xbase = mrs[mod];
-      M = mrs[mod + 1] - xbase;
-      wrow = W[mod] + (int64_t)n * K;
+      xbase = uxb;
+      M = uM;
     }
     if (M == 0) continue;
-    uint4 w[GEMV_V];
-#pragma unroll
-    for (int j = 0; j < GEMV_V; ++j) {
-      const int k = ch * GEMV_CH + j * 256 + lane * 8;
-      w[j] = k < K ? ld_stream_v4(wrow + k) : make_uint4(0, 0, 0, 0);
-    }
 #pragma unroll
     for (int m = 0; m < MAXM; ++m) {
       if (m < M) {
@@ -164,6 +185,7 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(
   }
   GEMV_FLUSH();
 #undef GEMV_FLUSH
+#undef GEMV_FETCH
   __syncthreads();
 
   // epilogue: thread per (row, m)
@@ -301,7 +323,13 @@ int launch_gemv(const void* x, int K, const void* const* W, const int32_t* mrs, 
   const int align = epi == PSK_EPI_SILU_MUL ? 32 : 1;
   const int cpr = (K + GEMV_CH - 1) / GEMV_CH;
   const int64_t G = (int64_t)n_mod * N;
-  int grid = 148 * 4;
+  static int sms = 0;
+  if (!sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int grid = sms * PSK_GEMV_CTAS;  // one resident wave (matches the launch bounds)
   // keep the partial slots of one CTA within 64 KiB of shared memory
   const int64_t slot_bytes_per_row = (int64_t)cpr * MAXM * 4;
   while (((G + grid - 1) / grid + align) * slot_bytes_per_row > 64 * 1024) grid += 148;
