@@ -242,6 +242,15 @@ int psk_prefill_attn(const void* q_rot, int32_t T, int32_t pos0, int32_t n_q_hea
 int psk_embed_tokens(const int64_t* tokens, int32_t T, const void* table, int32_t d, float* h,
                      void* stream);
 
+/* K8 — copy whole KV pages src_base[src_pages[i]] -> dst_base[dst_pages[i]]
+ * (page_bytes each; pools addressable from the launching device: same GPU
+ * or a peer-mapped pool). Replaces the modelled handoff of
+ * src/prefillsim/costs.py:66-83 for same-process moves; cross-process
+ * handoffs use NCCL P2P of the same page units (paper_2602_12029_b200/
+ * transfer.py). */
+int psk_kv_copy_pages(const void* src_base, void* dst_base, const int32_t* src_pages,
+                      const int32_t* dst_pages, int32_t n_pages, int64_t page_bytes, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

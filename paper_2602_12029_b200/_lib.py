@@ -105,6 +105,7 @@ _SIGS: dict[str, list] = {
     "psk_gemm_qkv_rope_kv": [_P, _P, _I32, _I32, _I32, _P, _I32, KVLayout, _I32, _P, _P, _P],
     "psk_prefill_attn": [_P, _I32, _I32, _I32, KVLayout, _I32, _P, _P, _P],
     "psk_embed_tokens": [_P, _I32, _P, _I32, _P, _P],
+    "psk_kv_copy_pages": [_P, _P, _P, _P, _I32, _I64, _P],
 }
 _RESTYPE = {
     "psk_last_error": C.c_char_p,
