@@ -23,6 +23,8 @@ constexpr int PT = 16;  // tokens per KV page (= kvstore block_size)
 
 __global__ void embed_rows_kernel(psk_decode_batch b, const __nv_bfloat16* const* embed, int d,
                                   float* __restrict__ h) {
+  pdl_wait();  // first kernel of a step: the previous step is fully done
+  pdl_trigger();
   const int r = blockIdx.x;
   const __nv_bfloat16* row = embed[b.row_mod[r]] + (int64_t)b.tokens[r] * d;
   for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
@@ -40,6 +42,8 @@ __global__ void rmsnorm_rows_kernel(const float* __restrict__ h, int d,
                                     const __nv_bfloat16* const* gamma, const int32_t* row_mod,
                                     float eps, __nv_bfloat16* __restrict__ out) {
   __shared__ float s_red[32];
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const float* x = h + (int64_t)r * d;
   float ss = 0.f;
@@ -104,6 +108,7 @@ __global__ void __launch_bounds__(GEMV_THREADS, PSK_GEMV_CTAS) gemv_kernel(  // 
   const int64_t g0 = ((int64_t)blockIdx.x * ngroups / gridDim.x) * align;
   const int64_t g1 = ((int64_t)(blockIdx.x + 1) * ngroups / gridDim.x) * align;
   const int rows = (int)(g1 - g0);
+  pdl_trigger();
   if (rows <= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = GEMV_THREADS / 32;
@@ -148,7 +153,9 @@ __global__ void __launch_bounds__(GEMV_THREADS, PSK_GEMV_CTAS) gemv_kernel(  // 
       wn[j] = (n_M > 0 && k < K) ? ld_stream_v4(wr_ + k) : make_uint4(0, 0, 0, 0); \
     }                                                                           \
   }
+  // the first weight unit streams while the producer of X drains (PDL)
   if (PSK_GEMV_PIPE && u0 < u1) GEMV_FETCH(u0);
+  pdl_wait();
   for (int64_t u = u0; u < u1; ++u) {
     if (!PSK_GEMV_PIPE) GEMV_FETCH(u);
     uint4 w[GEMV_V];
@@ -251,6 +258,7 @@ __global__ void rope_append_kernel(psk_decode_batch b, const float* __restrict__
   const float* cs = rope + (int64_t)pos * HD;  // [64][2]
   const int i = threadIdx.x;                    // 0..63
   const float c = cs[2 * i], s = cs[2 * i + 1];
+  pdl_wait();  // qkv comes from the GEMV just before
   for (int h = 0; h < nq; ++h) {
     const float x1 = row[h * HD + i], x2 = row[h * HD + i + 64];
     q_rot[((int64_t)r * nq + h) * HD + i] = f2bf(x1 * c - x2 * s);
@@ -275,6 +283,7 @@ __global__ void argmax_advance_kernel(psk_decode_batch b, const float* __restric
                                       int32_t* __restrict__ out_tokens, int max_new) {
   __shared__ float s_v[32];
   __shared__ int s_i[32];
+  pdl_wait();
   const int r = blockIdx.x;
   const float* x = logits + (int64_t)r * V;
   float bv = -INFINITY;
@@ -342,7 +351,8 @@ int launch_gemv(const void* x, int K, const void* const* W, const int32_t* mrs, 
     auto k = gemv_kernel<MAXM, E>;                                                              \
     if (smem > 48 * 1024)                                                                       \
       PSK_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k<<<grid, GEMV_THREADS, smem, s>>>(xb, K, Wb, mrs, n_mod, N, align, out);                  \
+    PSK_CUDA_TRY(psk::launch_pdl(k, dim3(grid), dim3(GEMV_THREADS), smem, s, xb, K, Wb, mrs,   \
+                                 n_mod, N, align, out));                                        \
     break;                                                                                      \
   }
   switch (epi) {
@@ -367,8 +377,8 @@ int psk_embed_rows(const psk_decode_batch* b, const void* const* embed, int32_t 
                    void* stream) {
   PSK_CHECK_ARG(b && embed && h && d % 8 == 0, "psk_embed_rows: bad args");
   if (b->n_rows == 0) return PSK_OK;
-  embed_rows_kernel<<<b->n_rows, 128, 0, psk::as_stream(stream)>>>(
-      *b, reinterpret_cast<const __nv_bfloat16* const*>(embed), d, h);
+  PSK_CUDA_TRY(psk::launch_pdl(embed_rows_kernel, dim3(b->n_rows), dim3(128), 0, psk::as_stream(stream),
+                               *b, reinterpret_cast<const __nv_bfloat16* const*>(embed), d, h));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }
@@ -377,9 +387,9 @@ int psk_rmsnorm_rows(const float* h, int32_t n_rows, int32_t d, const void* cons
                      const int32_t* row_mod, float eps, void* out, void* stream) {
   PSK_CHECK_ARG(h && gamma && out && d % 4 == 0 && n_rows >= 0, "psk_rmsnorm_rows: bad args");
   if (n_rows == 0) return PSK_OK;
-  rmsnorm_rows_kernel<<<n_rows, 256, 0, psk::as_stream(stream)>>>(
-      h, d, reinterpret_cast<const __nv_bfloat16* const*>(gamma), row_mod, eps,
-      reinterpret_cast<__nv_bfloat16*>(out));
+  PSK_CUDA_TRY(psk::launch_pdl(rmsnorm_rows_kernel, dim3(n_rows), dim3(256), 0, psk::as_stream(stream),
+                               h, d, reinterpret_cast<const __nv_bfloat16* const*>(gamma), row_mod,
+                               eps, reinterpret_cast<__nv_bfloat16*>(out)));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }
@@ -406,8 +416,9 @@ int psk_rope_append(const psk_decode_batch* b, const float* qkv, int32_t n_q_hea
   PSK_CHECK_ARG(b && qkv && rope && q_rot && kv.head_dim == HD && kv.page_tokens == PT,
                 "psk_rope_append: bad args (head_dim must be 128, page_tokens 16)");
   if (b->n_rows == 0) return PSK_OK;
-  rope_append_kernel<<<b->n_rows, 64, 0, psk::as_stream(stream)>>>(
-      *b, qkv, n_q_heads, rope, layer, kv, reinterpret_cast<__nv_bfloat16*>(q_rot));
+  PSK_CUDA_TRY(psk::launch_pdl(rope_append_kernel, dim3(b->n_rows), dim3(64), 0, psk::as_stream(stream),
+                               *b, qkv, n_q_heads, rope, layer, kv,
+                               reinterpret_cast<__nv_bfloat16*>(q_rot)));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }
@@ -416,8 +427,8 @@ int psk_argmax_advance(const psk_decode_batch* b, const float* logits, int32_t v
                        int32_t* out_tokens, int32_t max_new, void* stream) {
   PSK_CHECK_ARG(b && logits && vocab > 0, "psk_argmax_advance: bad args");
   if (b->n_rows == 0) return PSK_OK;
-  argmax_advance_kernel<<<b->n_rows, 1024, 0, psk::as_stream(stream)>>>(*b, logits, vocab,
-                                                                        out_tokens, max_new);
+  PSK_CUDA_TRY(psk::launch_pdl(argmax_advance_kernel, dim3(b->n_rows), dim3(1024), 0,
+                               psk::as_stream(stream), *b, logits, vocab, out_tokens, max_new));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }

@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 constexpr int MERGE_U = 32;
 __global__ void __launch_bounds__(HD) decode_attn_merge(const __grid_constant__ Params p) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");  // the o-proj GEMV may start streaming weights
   const int r = blockIdx.x, qh = blockIdx.y, d = threadIdx.x;
   const int nkv = p.kv.n_kv_heads;
   const int h = qh / p.grp;
