@@ -421,7 +421,26 @@ def main() -> None:
         out["decode_attn"] = decode_attn_roofline(eng, peaks)
         out["prefill"] = prefill_roofline(eng, peaks)
         step_bytes = eng.runner.weight_bytes_per_step
-        out["decode_step"] = {"weight_bytes": step_bytes}
+        out["decode_step"] = {"weight_bytes": step_bytes,
+                              "ms_per_token_step": round((t_val / a.steps - out["prefill"]["ms_per_prefill"]
+                                                          * S / 1e3) / MAX_NEW * 1e3, 3)}
+        if S != 1:
+            # the same weights served one session per step (latency-optimal point)
+            e1 = PrefillShareEngine(cfg, N_MOD, 1, PROMPT, MAX_NEW, pool_pages=2 * (PROMPT // 16 + 1) * 4,
+                                    device=local, modules=eng.mods, base=eng.base)
+            e1.capture()
+            for i in range(2):
+                e1.serve(batches[i][:1])
+            ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev1[0].record(st)
+            for j in range(2):
+                e1.serve(batches[a.warmup + j][:1])
+                ev1[j + 1].record(st)
+            ev1[-1].synchronize()
+            s1 = [ev1[j].elapsed_time(ev1[j + 1]) / 1e3 for j in range(2)]
+            out["single_session"] = {"value": round(N_MOD * 2 / sum(s1), 4), "unit": "req/s",
+                                     "p95_latency_ms": round(max(s1) * 1e3, 2)}
+            del e1
         del eng
         torch.cuda.empty_cache()
         out["decode_attn_fanout_32k_x16"] = decode_attn_fanout(peaks)

@@ -10,8 +10,10 @@
 // KV is paged and appended in place, and one decode step of all co-batched
 // modules reads each shared prompt page once.
 #include "common.cuh"
+#include "mma.cuh"
 
 #include <math.h>
+#include <stdlib.h>
 
 namespace psk {
 namespace dec {
@@ -235,6 +237,124 @@ __global__ void __launch_bounds__(GEMV_THREADS, PSK_GEMV_CTAS) gemv_kernel(  // 
   }
 }
 
+// -------------------------------------------------- tensor-core GEMV ----
+// For 2..16 rows per module (multi-session decode batches) the FMA count per
+// weight byte outgrows the CUDA cores, so the dot products run on mma.sync
+// m16n8k16 (W = A operand, 16 weight rows; x = B operand, 8 activation rows
+// per n-tile). Weights are still streamed straight from HBM into registers:
+// a fixed permutation of k inside every 32-column chunk (applied identically
+// to W and x; a dot product is permutation-invariant) makes thread t of a
+// quad own physical columns [8t, 8t+8) = its A/B fragments for two k-steps,
+// so every fragment is one coalesced 16-byte load. Work unit = (16-row tile,
+// 1024-column chunk); each unit's partial lands in its own shared-memory
+// slot (deterministic, no atomics) and the epilogue is the scalar one above.
+template <int NT, int EPI>
+__global__ void __launch_bounds__(GEMV_THREADS, PSK_GEMV_CTAS) gemv_mma_kernel(
+    const __nv_bfloat16* __restrict__ X, int K, const __nv_bfloat16* const* W,
+    const int32_t* __restrict__ mrs, int n_mod, int N, int align, void* out) {
+  constexpr int MAXM = NT * 8;
+  extern __shared__ float slots[];  // [rows_cta][cpr][MAXM]
+  const int cpr = (K + GEMV_CH - 1) / GEMV_CH;
+  const int64_t G = (int64_t)n_mod * N;
+  const int64_t ngroups = G / align;
+  const int64_t g0 = ((int64_t)blockIdx.x * ngroups / gridDim.x) * align;
+  const int64_t g1 = ((int64_t)(blockIdx.x + 1) * ngroups / gridDim.x) * align;
+  const int rows = (int)(g1 - g0);
+  pdl_trigger();
+  if (rows <= 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int tiles = rows / 16;
+  const int64_t units = (int64_t)tiles * cpr;
+  const int64_t u0 = warp * units / (GEMV_THREADS / 32), u1 = (warp + 1) * units / (GEMV_THREADS / 32);
+  for (int i = threadIdx.x; i < rows * cpr * MAXM; i += GEMV_THREADS) slots[i] = 0.f;
+  __syncthreads();
+  pdl_wait();
+  for (int64_t u = u0; u < u1; ++u) {
+    const int tl = (int)(u / cpr), ch = (int)(u % cpr);
+    const int64_t r0 = g0 + (int64_t)tl * 16;
+    const int mod = (int)(r0 / N);
+    const int xb = mrs[mod], M = mrs[mod + 1] - xb;
+    if (M == 0) continue;
+    const __nv_bfloat16* wa_p = W[mod] + (r0 % N + gq) * (int64_t)K;
+    const __nv_bfloat16* wb_p = wa_p + 8 * (int64_t)K;
+    float c[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) c[nt][0] = c[nt][1] = c[nt][2] = c[nt][3] = 0.f;
+    const int cbeg = ch * GEMV_CH + tq * 8;
+    const int cend = min(K, (ch + 1) * GEMV_CH);
+#pragma unroll 1
+    for (int col0 = cbeg; col0 < cend; col0 += 4 * 32) {
+      uint4 wa[4], wb[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int col = col0 + q * 32;
+        const bool ok = col < cend;
+        wa[q] = ok ? ld_stream_v4(wa_p + col) : make_uint4(0, 0, 0, 0);
+        wb[q] = ok ? ld_stream_v4(wb_p + col) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int col = col0 + q * 32;
+        if (col >= cend) break;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int xr = nt * 8 + gq;
+          const uint4 xv = xr < M ? __ldg(reinterpret_cast<const uint4*>(X + (int64_t)(xb + xr) * K + col))
+                                  : make_uint4(0, 0, 0, 0);
+          const uint32_t a0[4] = {wa[q].x, wb[q].x, wa[q].y, wb[q].y};
+          const uint32_t a1[4] = {wa[q].z, wb[q].z, wa[q].w, wb[q].w};
+          mma_bf16_16816(c[nt], a0, xv.x, xv.y);
+          mma_bf16_16816(c[nt], a1, xv.z, xv.w);
+        }
+      }
+    }
+    // C fragment: (row gq / gq+8, cols 2tq, 2tq+1) of [16 weight rows x 8 x rows]
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int m = nt * 8 + 2 * tq;
+      float* s0 = slots + ((int64_t)(tl * 16 + gq) * cpr + ch) * MAXM;
+      float* s8 = slots + ((int64_t)(tl * 16 + gq + 8) * cpr + ch) * MAXM;
+      if (m < M) { s0[m] = c[nt][0]; s8[m] = c[nt][2]; }
+      if (m + 1 < M) { s0[m + 1] = c[nt][1]; s8[m + 1] = c[nt][3]; }
+    }
+  }
+  __syncthreads();
+  if (EPI == PSK_EPI_SILU_MUL) {
+    const int pairs = rows / 2;
+    for (int i = threadIdx.x; i < pairs * MAXM; i += GEMV_THREADS) {
+      const int pi = i / MAXM, m = i % MAXM;
+      const int rg = (pi / 16) * 32 + pi % 16, ru = rg + 16;
+      const int64_t gg = g0 + rg;
+      const int mod = (int)(gg / N);
+      const int n = (int)(gg % N);
+      if (m >= mrs[mod + 1] - mrs[mod]) continue;
+      float vg = 0.f, vu = 0.f;
+      for (int cc = 0; cc < cpr; ++cc) {
+        vg += slots[((int64_t)rg * cpr + cc) * MAXM + m];
+        vu += slots[((int64_t)ru * cpr + cc) * MAXM + m];
+      }
+      const float sg = vg / (1.f + __expf(-vg));
+      reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)(mrs[mod] + m) * (N / 2) + (n / 32) * 16 + n % 16] =
+          f2bf(sg * vu);
+    }
+  } else {
+    for (int i = threadIdx.x; i < rows * MAXM; i += GEMV_THREADS) {
+      const int rl = i / MAXM, m = i % MAXM;
+      const int64_t gg = g0 + rl;
+      const int mod = (int)(gg / N);
+      const int n = (int)(gg % N);
+      if (m >= mrs[mod + 1] - mrs[mod]) continue;
+      float v = 0.f;
+      for (int cc = 0; cc < cpr; ++cc) v += slots[((int64_t)rl * cpr + cc) * MAXM + m];
+      const int64_t o = (int64_t)(mrs[mod] + m) * N + n;
+      if (EPI == PSK_EPI_STORE_BF16) reinterpret_cast<__nv_bfloat16*>(out)[o] = f2bf(v);
+      if (EPI == PSK_EPI_STORE_F32) reinterpret_cast<float*>(out)[o] = v;
+      if (EPI == PSK_EPI_RESID_ADD) reinterpret_cast<float*>(out)[o] += v;
+    }
+  }
+}
+
 // ---------------------------------------------------- RoPE + KV append ---
 
 __device__ __forceinline__ __nv_bfloat16* kv_ptr(const psk_kv_layout& kv, int32_t page, int layer,
@@ -314,7 +434,9 @@ __global__ void argmax_advance_kernel(psk_decode_batch b, const float* __restric
       const int k = b.priv_len[r];
       if (out_tokens && k < max_new) out_tokens[(int64_t)r * max_new + k] = bi;
       b.tokens[r] = bi;
-      b.priv_len[r] = k + 1;
+      // saturate at the row's page capacity: idle continuous-batching slots keep
+      // stepping without ever indexing past their private page table
+      b.priv_len[r] = min(k + 1, b.max_row_pages * PT - 1);
     }
   }
 }
@@ -326,10 +448,10 @@ using namespace psk::dec;
 
 namespace {
 
-template <int MAXM>
+template <int MAXM, bool MMA = false>
 int launch_gemv(const void* x, int K, const void* const* W, const int32_t* mrs, int n_mod, int N,
                 int epi, void* out, cudaStream_t s) {
-  const int align = epi == PSK_EPI_SILU_MUL ? 32 : 1;
+  const int align = epi == PSK_EPI_SILU_MUL ? 32 : (MMA ? 16 : 1);
   const int cpr = (K + GEMV_CH - 1) / GEMV_CH;
   const int64_t G = (int64_t)n_mod * N;
   static int sms = 0;
@@ -339,16 +461,17 @@ int launch_gemv(const void* x, int K, const void* const* W, const int32_t* mrs, 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int grid = sms * PSK_GEMV_CTAS;  // one resident wave (matches the launch bounds)
-  // keep the partial slots of one CTA within 64 KiB of shared memory
+  // keep the partial slots of PSK_GEMV_CTAS co-resident CTAs within shared memory
   const int64_t slot_bytes_per_row = (int64_t)cpr * MAXM * 4;
-  while (((G + grid - 1) / grid + align) * slot_bytes_per_row > 64 * 1024) grid += 148;
+  const int64_t smem_cap = (225 * 1024) / PSK_GEMV_CTAS;
+  while (((G + grid - 1) / grid + align) * slot_bytes_per_row > smem_cap) grid += sms;
   if (grid > G / align) grid = (int)(G / align);
   const size_t smem = (size_t)(((G / align + grid - 1) / grid) * align) * slot_bytes_per_row;
   auto xb = reinterpret_cast<const __nv_bfloat16*>(x);
   auto Wb = reinterpret_cast<const __nv_bfloat16* const*>(W);
 #define PSK_GEMV_CASE(E)                                                                        \
   case E: {                                                                                     \
-    auto k = gemv_kernel<MAXM, E>;                                                              \
+    auto k = MMA ? gemv_mma_kernel<(MAXM + 7) / 8, E> : gemv_kernel<MAXM, E>;                   \
     if (smem > 48 * 1024)                                                                       \
       PSK_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     PSK_CUDA_TRY(psk::launch_pdl(k, dim3(grid), dim3(GEMV_THREADS), smem, s, xb, K, Wb, mrs,   \
@@ -403,6 +526,10 @@ int psk_gemv(const void* x, int32_t n_rows, int32_t K, const void* const* W,
   const int maxm = n_rows - n_mod + 1;
   cudaStream_t s = psk::as_stream(stream);
   if (maxm <= 1) return launch_gemv<1>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);
+  if (N % 16 == 0 && !getenv("PSK_GEMV_SCALAR")) {  // tensor-core path for 2..16 rows / module
+    if (maxm <= 8) return launch_gemv<8, true>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);
+    if (maxm <= 16) return launch_gemv<16, true>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);
+  }
   if (maxm <= 2) return launch_gemv<2>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);
   if (maxm <= 4) return launch_gemv<4>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);
   if (maxm <= 8) return launch_gemv<8>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);

@@ -290,6 +290,20 @@ class DecodeBatch:
         self.t_priv_len.zero_()
         self.t_tokens.copy_(torch.tensor(self._first, dtype=torch.int32))
 
+    def update_row(self, row: int, shared_len: int, pages: list[int], first_token: int) -> None:
+        """Re-point one row (that is also its own session) at a new request
+        in place, ordered on the current stream: continuous batching."""
+        msp = self.max_sess_pages
+        if len(pages) > msp:
+            raise ValueError("row page table exceeds the batch's capacity")
+        s = self.rows[row].session
+        self.t_sess_len[s] = shared_len
+        self.t_sess_pages[s].copy_(torch.tensor(pages + [pages[-1]] * (msp - len(pages)),
+                                                dtype=torch.int32), non_blocking=False)
+        self.t_priv_len[row] = 0
+        self.t_tokens[row] = first_token
+        self._first[row] = first_token
+
     def update_sessions(self, shared_lens: list[int], pages: list[list[int]],
                         first_tokens: list[int]) -> None:
         """Point the batch at new sessions in place (same device addresses, so

@@ -1,0 +1,300 @@
+"""Real-time multi-model agent serving on one B200 (BASELINE configs 3 / 5).
+
+Drives the reference's agent workload (workload.generate: Poisson sessions,
+agent chains rotated per session, synthetic packed token ids) through real
+GPU work with the reference's request life cycle (src/prefillsim/cluster.py):
+
+  arrival / admission      cluster.py:256-269 (admission cap)
+  dispatch                 cluster.py:271-318 (context = prompt + extensions +
+                           outputs; first request issued at session arrival)
+  prefill                  cluster.py:322-366: pool lookup (pins) -> forward of
+                           the uncached tokens -> insert + pin; in BASELINE mode
+                           the request's own model prefills under its own
+                           namespace, in PREFILLSHARE mode the frozen base
+                           prefills under the shared one (router.py:53-56)
+  decode                   cluster.py:414-442: one batched step advances every
+                           active request of every model (continuous batching,
+                           grouped GEMV over the modules, K6 attention)
+  completion               cluster.py:446-478: output appended (synth ids),
+                           next agent of the chain dispatched
+
+Decode rows are fixed slots (rows_per_module per model) so one CUDA graph
+serves every step; a request takes a free slot of its model. Control flow
+needs no device->host sync per step: a request of output_len L finishes after
+exactly L steps (the reference appends synthetic output ids, not the
+generated ones: cluster.py:453-457).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from collections import deque
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import workload as wl
+from .kvstore import BlockPool
+from .model import (PAGE_TOKENS, DecodeBatch, DecodeRow, DecodeRunner, KVCache, LlamaConfig,
+                    ModuleWeights, PrefillRunner, SessionSpec)
+from .router import Router, ServingMode
+
+
+@dataclass
+class RequestRecord:
+    request_id: int
+    session_id: int
+    model_id: str
+    issue_us: float
+    first_token_us: float | None = None
+    done_us: float | None = None
+    out_tokens: int = 0
+    matched: int = 0
+    prefilled: int = 0
+
+
+@dataclass
+class _Req:
+    rec: RequestRecord
+    session: int
+    ctx: np.ndarray
+    output_len: int
+    model_idx: int
+
+
+@dataclass
+class _Row:
+    req: _Req | None = None
+    steps: int = 0
+    held: list = field(default_factory=list)
+    pool: BlockPool | None = None
+
+
+class AgentServer:
+    def __init__(self, cfg: LlamaConfig, model_ids: list[str], mode: ServingMode, *,
+                 rows_per_module: int = 8, pool_pages_per_worker: int = 2048, max_context: int = 4096,
+                 max_output: int = 256, seed: int = 0, device: int = 0,
+                 modules: list[ModuleWeights] | None = None, base: ModuleWeights | None = None):
+        self.cfg, self.mode, self.model_ids = cfg, mode, list(model_ids)
+        M = len(model_ids)
+        self.router = Router(mode, model_ids)
+        self.mods = modules or [ModuleWeights(cfg, seed + 1 + i, device=device) for i in range(M)]
+        self.base = None
+        if mode is ServingMode.PREFILLSHARE:
+            self.base = base or ModuleWeights(cfg, seed, device=device, with_head=False)
+        # KV pages: [worker pools ...][row tail pages][row private pages]. The
+        # reference fleet has one prefill worker (and pool) per model; on one
+        # GPU PREFILLSHARE routes every session to one shared pool of the same
+        # total capacity, BASELINE keeps one pool per model (router.py:53-77).
+        n_workers = 1 if mode is ServingMode.PREFILLSHARE else M
+        per_pool = M * pool_pages_per_worker // n_workers
+        self.priv_pages = (max_output + PAGE_TOKENS - 1) // PAGE_TOKENS
+        self.R = M * rows_per_module
+        total = n_workers * per_pool + self.R * (1 + self.priv_pages)
+        self.kv = KVCache(cfg, total, device)
+        # each logical prefill worker owns a disjoint page range of the one cache
+        self.pools = []
+        for w in range(n_workers):
+            p = BlockPool(per_pool, PAGE_TOKENS, device=device, kv_pages=per_pool,
+                          max_query_tokens=max(1 << 16, max_context))
+            p.page_base = w * per_pool
+            self.pools.append(p)
+        producers = [self.base] if self.base is not None else self.mods
+        self.prefillers = [PrefillRunner(cfg, w, self.kv, max_tokens=max_context, device=device)
+                           for w in producers]
+        rows, sessions = [], []
+        nxt = n_workers * per_pool
+        self.tail_page = []
+        for r in range(self.R):
+            self.tail_page.append(nxt)
+            nxt += 1
+        max_sp = (max_context + PAGE_TOKENS - 1) // PAGE_TOKENS + 1
+        for m in range(M):
+            for k in range(rows_per_module):
+                r = m * rows_per_module + k
+                rows.append(DecodeRow(module=m, session=r, first_token=0,
+                                      pages=list(range(nxt, nxt + self.priv_pages))))
+                nxt += self.priv_pages
+                sessions.append(SessionSpec(shared_len=0, pages=[self.tail_page[r]] * max_sp))
+        self.batch = DecodeBatch(sessions, rows, M, device)
+        self.runner = DecodeRunner(cfg, self.mods, self.kv, self.batch, max_output, device=device)
+        self.rows = [_Row() for _ in range(self.R)]
+        self.rows_per_module = rows_per_module
+        self.max_context, self.max_output = max_context, max_output
+        self.dev = torch.device("cuda", device)
+        self._sess_len = [0] * self.R
+        self._pages = [[self.tail_page[r]] for r in range(self.R)]
+        self._first = [0] * self.R
+
+    # -- helpers -------------------------------------------------------------
+
+    def _row_of_module(self, m: int) -> int | None:
+        for k in range(self.rows_per_module):
+            r = m * self.rows_per_module + k
+            if self.rows[r].req is None:
+                return r
+        return None
+
+    def _vocab_ids(self, ctx: np.ndarray) -> torch.Tensor:
+        # model inputs: packed synthetic ids folded into the vocabulary
+        return torch.from_numpy((ctx % self.cfg.vocab).astype(np.int64)).to(self.dev, non_blocking=True)
+
+    def _prefill(self, req: _Req, now_us: int):
+        """cluster.py:322-366 on the GPU. Returns (held handles, page table,
+        matched tokens, prefilled tokens, decode row)."""
+        worker = self.router.route_prefill(req.rec, [0] * len(self.pools))
+        pool = self.pools[worker]
+        ns = self.router.prefill_namespace(req.rec.model_id)
+        n = len(req.ctx)
+        m, chain = pool.longest_prefix_match(ns, req.ctx, now_us)
+        new = pool.insert(ns, req.ctx, now_us)
+        pool.pin(new, now_us)
+        base = pool.page_base
+        pages = [base + s for s in chain.slots.tolist()] + [base + s for s in new.slots.tolist()]
+        row = self._row_of_module(req.model_idx)
+        if n % PAGE_TOKENS:
+            pages.append(self.tail_page[row])
+        # partial prefill from the last cached full block; the tail block is recomputed
+        pos0 = min(m, (n // PAGE_TOKENS) * PAGE_TOKENS)
+        runner = self.prefillers[0 if self.base is not None else req.model_idx]
+        pt = torch.tensor(pages, dtype=torch.int32, device=self.dev)
+        if n > pos0:
+            runner.run(self._vocab_ids(req.ctx[pos0:]), pos0, pt)
+        return [(pool, chain), (pool, new)], pages, m, n - pos0, row
+
+    # -- serving -------------------------------------------------------------
+
+    def run(self, sessions: list[wl.SessionSpec], max_concurrent: int | None = None,
+            time_scale: float = 1.0) -> list[RequestRecord]:
+        """Serve the workload in real time (arrival times scaled by
+        time_scale). Returns one record per request."""
+        self.runner.capture()
+        st = torch.cuda.current_stream()
+        records: list[RequestRecord] = []
+        arrivals = deque(sorted(sessions, key=lambda s: s.arrival_time))
+        waiting_admission: deque = deque()
+        active = 0
+        cap = max_concurrent or (1 << 30)
+        ctx: dict[int, list] = {}
+        step_idx: dict[int, int] = {}
+        spec_of = {s.session_id: s for s in sessions}
+        prefill_q: deque[_Req] = deque()
+        next_rid = [0]
+        t0 = time.perf_counter()
+
+        def now_us() -> float:
+            return (time.perf_counter() - t0) * 1e6
+
+        def dispatch(sid: int, issue_us: float):
+            spec = spec_of[sid]
+            k = step_idx[sid]
+            agent = spec.agent_chain[k % len(spec.agent_chain)]
+            ctx[sid].extend(wl.synth_tokens(sid, wl.extension_slot(k), agent.input_extension_len))
+            rec = RequestRecord(next_rid[0], sid, agent.model_id, issue_us)
+            next_rid[0] += 1
+            records.append(rec)
+            prefill_q.append(_Req(rec, sid, np.array(ctx[sid], dtype=np.int64), agent.output_len,
+                                  self.model_ids.index(agent.model_id)))
+
+        def activate(spec):
+            ctx[spec.session_id] = list(wl.synth_tokens(spec.session_id, wl.prompt_slot(),
+                                                       spec.initial_prompt_len))
+            step_idx[spec.session_id] = 0
+            dispatch(spec.session_id, spec.arrival_time * time_scale)  # counts admission wait
+
+        done_sessions = 0
+        n_sessions = len(sessions)
+        dirty = False
+        while done_sessions < n_sessions:
+            t = now_us()
+            while arrivals and arrivals[0].arrival_time * time_scale <= t:
+                s = arrivals.popleft()
+                if active < cap:
+                    active += 1
+                    activate(s)
+                else:
+                    waiting_admission.append(s)
+            # prefills whose model has a free decode row (handoff = zero-copy pin)
+            progressed = False
+            for _ in range(len(prefill_q)):
+                req = prefill_q.popleft()
+                if self._row_of_module(req.model_idx) is None:
+                    prefill_q.append(req)
+                    continue
+                held, pages, m, pre, row = self._prefill(req, int(now_us()))
+                req.rec.matched, req.rec.prefilled = m, pre
+                r = self.rows[row]
+                r.req, r.steps, r.held = req, 0, held
+                self._sess_len[row] = len(req.ctx) - 1
+                self._pages[row] = pages
+                self._first[row] = int(req.ctx[-1] % self.cfg.vocab)
+                self.batch.update_row(row, len(req.ctx) - 1, pages, self._first[row])
+                dirty = True
+                progressed = True
+            busy = [r for r in self.rows if r.req is not None]
+            if busy:
+                self.runner.graph.replay()
+                t_step = now_us()
+                for idx, r in enumerate(self.rows):
+                    if r.req is None:
+                        continue
+                    r.steps += 1
+                    rec = r.req.rec
+                    if r.steps == 1:
+                        rec.first_token_us = t_step
+                    if r.steps >= r.req.output_len:
+                        st.synchronize()
+                        rec.done_us = now_us()
+                        rec.out_tokens = r.steps
+                        for pool, h in r.held:
+                            pool.release(h)
+                        sid = r.req.session
+                        spec = spec_of[sid]
+                        ctx[sid].extend(wl.synth_tokens(sid, wl.output_slot(step_idx[sid]), r.req.output_len))
+                        step_idx[sid] += 1
+                        self.rows[idx] = _Row()
+                        self.batch.update_row(idx, 0, [self.tail_page[idx]], 0)
+                        if step_idx[sid] >= spec.total_requests:
+                            done_sessions += 1
+                            active -= 1
+                            if waiting_admission:
+                                active += 1
+                                activate(waiting_admission.popleft())
+                        else:
+                            dispatch(sid, rec.done_us)
+            elif not progressed:
+                if arrivals:
+                    wait = arrivals[0].arrival_time * time_scale - now_us()
+                    if wait > 0:
+                        time.sleep(min(wait / 1e6, 0.05))
+                elif not prefill_q:
+                    break
+        st.synchronize()
+        return records
+
+
+def summarize(records: list[RequestRecord], warmup_fraction: float = 0.1) -> dict:
+    """metrics.py:22-76 definitions (nearest-rank p95, post-warmup window),
+    plus req/s over the same window."""
+    done = [r for r in records if r.done_us is not None]
+    if not done:
+        return {"completed": 0}
+    t_end = max(r.done_us for r in done)
+    w0 = warmup_fraction * t_end
+    win = [r for r in done if r.done_us >= w0]
+    window_s = (t_end - w0) / 1e6
+    e2e = sorted(r.done_us - r.issue_us for r in done)
+    ttft = sorted(r.first_token_us - r.issue_us for r in done if r.first_token_us is not None)
+
+    def p95(v):
+        return v[max(math.ceil(0.95 * len(v)), 1) - 1]
+
+    lookup = sum(r.matched + r.prefilled for r in done)
+    return {"completed": len(done), "req_per_s": len(win) / window_s,
+            "tok_per_s": sum(r.out_tokens for r in win) / window_s,
+            "p95_e2e_ms": p95(e2e) / 1e3, "p95_ttft_ms": p95(ttft) / 1e3 if ttft else None,
+            "prefill_tokens": sum(r.prefilled for r in done),
+            "prefix_hit_ratio": sum(r.matched for r in done) / max(1, lookup),
+            "wall_s": t_end / 1e6}

@@ -1,0 +1,56 @@
+"""K5 grouped decode GEMV (scalar weight-streaming path for 1 row per module,
+tensor-core path for 2..16) vs a torch fp32 reference on identical bf16
+operands, all epilogues, ragged rows per module (incl. modules with no rows).
+Tolerance: |gpu - ref| <= 2e-3 * max|ref| + 1e-4 (fp32 outputs),
+1e-2 * max|ref| + 1e-3 (bf16 outputs)."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(rows_per_mod, N, K, epi, seed=0):
+    from paper_2602_12029_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    n_mod = len(rows_per_mod)
+    W = [(torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16) for _ in range(n_mod)]
+    R = sum(rows_per_mod)
+    x = torch.randn(R, K, device="cuda", generator=g).to(torch.bfloat16)
+    mrs = [0]
+    for r in rows_per_mod:
+        mrs.append(mrs[-1] + r)
+    ptrs = torch.tensor([w.data_ptr() for w in W], dtype=torch.int64, device="cuda")
+    t_mrs = torch.tensor(mrs, dtype=torch.int32, device="cuda")
+    ref = torch.zeros(R, N, device="cuda")
+    for i in range(n_mod):
+        ref[mrs[i]:mrs[i + 1]] = x[mrs[i]:mrs[i + 1]].float() @ W[i].float().T
+    if epi == 3:
+        y = ref.view(R, -1, 2, 16)
+        ref = (torch.nn.functional.silu(y[:, :, 0]) * y[:, :, 1]).reshape(R, N // 2)
+        out = torch.zeros(R, N // 2, dtype=torch.bfloat16, device="cuda")
+    elif epi == 0:
+        out = torch.zeros(R, N, dtype=torch.bfloat16, device="cuda")
+    else:
+        out = torch.randn(R, N, device="cuda", generator=g) if epi == 2 else torch.zeros(R, N, device="cuda")
+        if epi == 2:
+            ref = ref + out
+    _lib.check(_lib.load().psk_gemv(x.data_ptr(), R, K, ptrs.data_ptr(), t_mrs.data_ptr(), n_mod, N, epi,
+                                    out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    err = (out.float() - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    tol = (1e-2 * scale + 1e-3) if epi in (0, 3) else (2e-3 * scale + 1e-4)
+    assert err <= tol, f"err {err} scale {scale}"
+
+
+@pytest.mark.parametrize("rows", [[1, 1, 1, 1], [2, 2], [4, 4, 4, 4], [8, 3, 0, 5], [16, 16], [12, 1]])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_gemv_rows_and_epilogues(rows, epi):
+    _run(rows, 1536, 4096, epi)
+
+
+@pytest.mark.parametrize("N,K", [(256, 768), (4096, 14336), (6144, 4096)])
+def test_gemv_shapes(N, K):
+    _run([3, 5, 2, 6], N, K, 1, seed=1)
+    _run([1, 1, 1], N, K, 1, seed=2)
