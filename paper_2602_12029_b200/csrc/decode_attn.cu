@@ -385,6 +385,332 @@ __global__ void __launch_bounds__(HD) decode_attn_merge(const __grid_constant__ 
   p.out[((int64_t)r * p.nq + qh) * HD + d] = f2bf(L > 0.f ? acc / L : 0.f);
 }
 
+// ------------------------------------------------- tcgen05 fan-out path ----
+// When a session carries many decode rows (fan-out: up to 16 modules x 4 GQA
+// heads = 64 query rows per KV head) the mma.sync kernel above is bound by
+// the legacy tensor pipe, not HBM. This variant runs both products on the
+// 5th-gen tensor cores: per 8-page chunk (128 tokens),
+//   S[128 rows x 128 tok] = Q . K^T   (8 UMMA M=128 N=128 K=16, TMEM)
+//   D[128 rows x 128 dim] = P . V     (8 UMMA, V as an MN-major B operand)
+// A producer warp streams K/V chunks with TMA into a 2-stage ring (K boxes
+// laid out so the chunk's 128 token rows sit at a uniform 128 B stride), an
+// MMA warp issues tcgen05.mma, and 4 softmax warps own one query row each
+// (thread = TMEM lane): they read S, write bf16 P back to shared memory in
+// the UMMA K-major SW128 layout, and fold D into an fp32 O held in
+// registers with the online-softmax rescale.
+namespace tcv {
+
+constexpr int CP = 8;                  // pages per chunk
+constexpr int NSTG = 2;                // chunk stages
+constexpr int KREG = CP * TILE;        // 32 KiB: [dims 0-63 box x 8 pages][dims 64-127 box x 8 pages]
+constexpr int VREG = CP * TILE;        // 32 KiB: [page][box0 | box1]
+constexpr int STG = KREG + VREG;
+constexpr int OFF_Q = NSTG * STG;      // 128 KiB
+constexpr int OFF_P = OFF_Q + 32768;   // Q: [2 boxes][128 rows][128 B]
+constexpr int OFF_BAR = OFF_P + 32768; // P: same layout
+constexpr int OFF_PG = OFF_BAR + 256;
+constexpr int SMEM = OFF_PG + MAXP * 4 + 1024;
+constexpr int THREADS = 192;           // w0 TMA, w1 MMA (+TMEM alloc), w2-5 softmax
+constexpr int TMEM_COLS = 256;         // S: cols [0,128), D: cols [128,256)
+
+__device__ __forceinline__ uint64_t desc_k_sw128(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// MN-major SW128: 64-element MN groups at LBO, 8-row K groups at SBO.
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t addr, uint32_t lbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__host__ __device__ constexpr uint32_t idesc(bool b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(128 >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   tma::sa(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    decode_attn_tc(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ Params p) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* full = bars;            // [2]
+  uint64_t* empty = bars + 2;       // [2]
+  uint64_t* s_full = bars + 4;
+  uint64_t* s_empty = bars + 5;
+  uint64_t* p_full = bars + 6;
+  uint64_t* d_full = bars + 7;
+  uint64_t* d_empty = bars + 8;
+  int* s_page = reinterpret_cast<int*>(smem + OFF_PG);
+  __shared__ int s_rows[MAXR], s_plen[MAXR], s_pstart[MAXR + 1];
+  __shared__ int s_ps, s_ls, s_total;
+  __shared__ uint32_t s_tmem;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkv = p.kv.n_kv_heads;
+  const int item = blockIdx.x;
+  const int j_split = item % p.ns;
+  const int h = (item / p.ns) % nkv;
+  const int sess = item / (p.ns * nkv);
+  const int nr = p.b.sess_nrows[sess];
+  const int G = nr * p.grp;
+
+  if (threadIdx.x < nr) {
+    const int r = p.b.sess_rows[(int64_t)sess * p.b.max_rows_per_sess + threadIdx.x];
+    s_rows[threadIdx.x] = r;
+    s_plen[threadIdx.x] = p.b.priv_len[r] + 1;
+  } else if (threadIdx.x == 32) {
+    s_ls = p.b.sess_len[sess];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int Ps = (s_ls + PT - 1) / PT;
+    s_ps = Ps;
+    int acc = Ps;
+    for (int i = 0; i < nr; ++i) {
+      s_pstart[i] = acc;
+      acc += (s_plen[i] + PT - 1) / PT;
+    }
+    s_pstart[nr] = acc;
+    s_total = acc;
+    for (int s = 0; s < NSTG; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], 1);
+    }
+    tma::mbar_init(s_full, 1);
+    tma::mbar_init(s_empty, 128);
+    tma::mbar_init(p_full, 128);
+    tma::mbar_init(d_full, 1);
+    tma::mbar_init(d_empty, 128);
+    tma::fence_mbar_init();
+    tma::prefetch_map(&kvmap);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tma::sa(&s_tmem)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  __syncthreads();
+  const int total = s_total;
+  const int k0 = (int)((int64_t)j_split * total / p.ns);
+  const int k1 = (int)((int64_t)(j_split + 1) * total / p.ns);
+  const int np = k1 - k0;
+  const int nch = (np + CP - 1) / CP;
+  for (int j = threadIdx.x; j < np && j < MAXP; j += THREADS) {
+    const int k = k0 + j;
+    int pg;
+    if (k < s_ps) {
+      pg = p.b.sess_pages[(int64_t)sess * p.b.max_sess_pages + k];
+    } else {
+      int i = 0;
+      while (k >= s_pstart[i + 1]) ++i;
+      pg = p.b.row_pages[(int64_t)s_rows[i] * p.b.max_row_pages + (k - s_pstart[i])];
+    }
+    s_page[j] = pg;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // Q -> shared, UMMA K-major SW128: [box = dims/64][row][128 B], rows >= G zero
+  for (int e = threadIdx.x; e < 128 * 16; e += THREADS) {
+    const int g = e >> 4, c = e & 15;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (g < G) {
+      const int qh = h * p.grp + g % p.grp;
+      v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)s_rows[g / p.grp] * p.nq + qh) * HD + c * 8);
+    }
+    const uint32_t a = smem_u32(smem + OFF_Q) + (c >> 3) * 16384 + g * 128 + (((c & 7) ^ (g & 7)) << 4);
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = s_tmem;
+  const uint32_t sq = smem_u32(smem + OFF_Q), sp = smem_u32(smem + OFF_P);
+
+  if (warp == 0) {
+    if (lane == 0 && np > 0) {
+      for (int c = 0; c < nch; ++c) {
+        const int st = c % NSTG;
+        tma::mbar_wait(&empty[st], ((c / NSTG) & 1) ^ 1);
+        tma::mbar_expect_tx(&full[st], STG);
+        unsigned char* kr = smem + st * STG;
+        unsigned char* vr = kr + KREG;
+        for (int pp = 0; pp < CP; ++pp) {
+          const int j = c * CP + pp;
+          // pages past the slice reload a valid page (finite data); masked below
+          const int jj = j < np ? j : c * CP;
+          const int page = jj < MAXP ? s_page[jj] : s_page[0];
+          const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
+          const int row_v = row_k + nkv * PT;
+          tma::load_2d(&kvmap, &full[st], kr + pp * 2048, 0, row_k);
+          tma::load_2d(&kvmap, &full[st], kr + CP * 2048 + pp * 2048, 64, row_k);
+          tma::load_2d(&kvmap, &full[st], vr + pp * TILE, 0, row_v);
+          tma::load_2d(&kvmap, &full[st], vr + pp * TILE + 2048, 64, row_v);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && np > 0) {
+      constexpr uint32_t ID_QK = idesc(false), ID_PV = idesc(true);
+      for (int c = 0; c < nch; ++c) {
+        const int st = c % NSTG;
+        const uint32_t kr = smem_u32(smem + st * STG), vr = kr + KREG;
+        tma::mbar_wait(&full[st], (c / NSTG) & 1);
+        tma::mbar_wait(s_empty, (c & 1) ^ 1);
+        fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t a = desc_k_sw128(sq + (kk >> 2) * 16384) + 2 * (kk & 3);
+          const uint64_t b = desc_k_sw128(kr + (kk >> 2) * (CP * 2048)) + 2 * (kk & 3);
+          umma(tmem, a, b, ID_QK, kk > 0);
+        }
+        commit(s_full);
+        tma::mbar_wait(p_full, c & 1);
+        tma::mbar_wait(d_empty, (c & 1) ^ 1);
+        fence_after();
+#pragma unroll
+        for (int pp = 0; pp < CP; ++pp) {
+          const uint64_t a = desc_k_sw128(sp + (pp >> 2) * 16384) + 2 * (pp & 3);
+          const uint64_t b = desc_mn_sw128(vr + pp * TILE, 2048);
+          umma(tmem + 128, a, b, ID_PV, pp > 0);
+        }
+        commit(d_full);
+        commit(&empty[st]);
+      }
+    }
+  } else {
+    // ---------------- softmax: thread = query row = TMEM lane ----------------
+    const int q = warp & 3;
+    const int g = q * 32 + lane;
+    const uint32_t tS = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t tD = tS + 128;
+    const int own = g < G ? g / p.grp : -2;
+    float O[HD];
+#pragma unroll
+    for (int i = 0; i < HD; ++i) O[i] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    for (int c = 0; c < nch; ++c) {
+      int lim[CP], ownr[CP];
+#pragma unroll
+      for (int pp = 0; pp < CP; ++pp) {
+        const int j = c * CP + pp;
+        const int k = k0 + j;
+        if (j >= np) {
+          lim[pp] = 0;
+          ownr[pp] = -1;
+        } else if (k < s_ps) {
+          lim[pp] = min(PT, s_ls - k * PT);
+          ownr[pp] = -1;
+        } else {
+          int i = 0;
+          while (k >= s_pstart[i + 1]) ++i;
+          lim[pp] = min(PT, s_plen[i] - (k - s_pstart[i]) * PT);
+          ownr[pp] = i;
+        }
+        if (ownr[pp] >= 0 && ownr[pp] != own) lim[pp] = 0;
+      }
+      tma::mbar_wait(s_full, c & 1);
+      fence_after();
+      float mx = -INFINITY;
+      float v[32];
+#pragma unroll
+      for (int gi = 0; gi < 4; ++gi) {
+        ld32(tS + gi * 32, v);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int col = gi * 32 + e;
+          if ((col & 15) < lim[col >> 4]) mx = fmaxf(mx, v[e] * p.scale_log2);
+        }
+      }
+      const float mn = fmaxf(m, mx);
+      const float base = mn == -INFINITY ? 0.f : mn;
+      const float alpha = exp2f(m - base);
+      float ladd = 0.f;
+#pragma unroll
+      for (int gi = 0; gi < 4; ++gi) {
+        ld32(tS + gi * 32, v);
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const int col = gi * 32 + e;
+          const float p0 = (col & 15) < lim[col >> 4] ? exp2f(v[e] * p.scale_log2 - base) : 0.f;
+          const float p1 = ((col + 1) & 15) < lim[(col + 1) >> 4] ? exp2f(v[e + 1] * p.scale_log2 - base) : 0.f;
+          ladd += p0 + p1;
+          pk[e >> 1] = pack_bf16(p0, p1);
+        }
+        // 32 tokens = 4 16-byte chunks of this row; K-major SW128 like Q
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int chunk = gi * 4 + cc;  // 0..15 (8 tokens each)
+          const uint32_t a = sp + (chunk >> 3) * 16384 + g * 128 + (((chunk & 7) ^ (g & 7)) << 4);
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(pk[4 * cc]), "r"(pk[4 * cc + 1]),
+                       "r"(pk[4 * cc + 2]), "r"(pk[4 * cc + 3]));
+        }
+      }
+      fence_before();
+      tma::mbar_arrive(s_empty);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tma::mbar_arrive(p_full);
+      l = l * alpha + ladd;
+      tma::mbar_wait(d_full, c & 1);
+      fence_after();
+#pragma unroll
+      for (int gi = 0; gi < 4; ++gi) {
+        ld32(tD + gi * 32, v);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) O[gi * 32 + e] = O[gi * 32 + e] * alpha + v[e];
+      }
+      fence_before();
+      tma::mbar_arrive(d_empty);
+      m = mn;
+    }
+    if (g < G) {
+      const int64_t slot = (int64_t)item * GMAX + g;
+      p.pm[slot] = m;
+      p.pl[slot] = l;
+      float4* dst = reinterpret_cast<float4*>(p.po + slot * HD);
+#pragma unroll
+      for (int i = 0; i < HD / 4; ++i) dst[i] = make_float4(O[4 * i], O[4 * i + 1], O[4 * i + 2], O[4 * i + 3]);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace tcv
+
 // ------------------------------------------------------------ host side --
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -488,12 +814,26 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)items);
-  cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_partial, map, p));
+  // many query rows per KV head (fan-out) -> tcgen05 path; else mma.sync
+  static const bool force_hmma = getenv("PSK_ATTN_HMMA") != nullptr;
+  if (grp * b->max_rows_per_sess > 16 && !force_hmma) {
+    static bool tc_init = false;
+    if (!tc_init) {
+      PSK_CUDA_TRY(cudaFuncSetAttribute(tcv::decode_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        tcv::SMEM));
+      tc_init = true;
+    }
+    cfg.blockDim = dim3(tcv::THREADS);
+    cfg.dynamicSmemBytes = tcv::SMEM;
+    PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tcv::decode_attn_tc, map, p));
+  } else {
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM;
+    PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_partial, map, p));
+  }
   if (tr) {
     static const char* names[] = {"entry", "prologue", "staged", "loop-done", "folded"};
     psk::trace_report("decode_attn", (int)items, 5, names);
