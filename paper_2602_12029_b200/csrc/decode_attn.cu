@@ -718,7 +718,12 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static int kv_map(const psk_kv_layout& kv, CUtensorMap* out) {
+}  // namespace dattn
+
+// 2D TMA map over a KV page pool: rows of 128 dims (256 B), [16 x 64] boxes,
+// 128B swizzle. Cached per pool geometry. Shared by the attention kernels.
+int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out) {
+  using namespace dattn;
   // small cache keyed by the pool geometry
   static CUtensorMap cached[4];
   static psk_kv_layout keys[4] = {};
@@ -759,7 +764,6 @@ static int kv_map(const psk_kv_layout& kv, CUtensorMap* out) {
   return PSK_OK;
 }
 
-}  // namespace dattn
 }  // namespace psk
 
 using namespace psk::dattn;
@@ -784,7 +788,7 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
                 "psk_decode_attn: %d query rows per KV head exceed %d", grp * b->max_rows_per_sess, GMAX);
   if (b->n_rows == 0) return PSK_OK;
   CUtensorMap map;
-  int rc = kv_map(kv, &map);
+  int rc = psk::kv_tensor_map(kv, &map);
   if (rc) return rc;
   Params p;
   p.b = *b;

@@ -14,8 +14,11 @@
 // scheduled first. Tensor math is mma.sync m16n8k16 (bf16 -> fp32).
 #include "common.cuh"
 #include "mma.cuh"
+#include "tma.cuh"
+#include "umma.cuh"
 
 #include <math.h>
+#include <stdlib.h>
 
 namespace psk {
 namespace pre {
@@ -215,6 +218,219 @@ __global__ void __launch_bounds__(THREADS, 2) prefill_attn_kernel(const __grid_c
   }
 }
 
+// ------------------------------------------------------ tcgen05 variant ----
+// Causal prefill attention on the 5th-gen tensor cores. One CTA = (kv head,
+// block of 128/grp query positions x grp q heads = 128 query rows). Per
+// 8-page chunk (128 keys): S = Q.K^T and D = P.V are UMMAs (M=128, N=128)
+// with TMEM accumulators; a TMA producer warp streams K/V chunks (K boxes
+// laid out at a uniform 128 B row stride across the chunk's pages, V as an
+// MN-major operand); 4 softmax warps own one query row each (thread = TMEM
+// lane), apply the causal mask, write bf16 P in the UMMA K-major SW128 layout
+// and keep O in registers with the online-softmax rescale.
+namespace tc {
+
+constexpr int CP = 8, NSTG = 2;
+constexpr int KREG = CP * TILE, VREG = CP * TILE, STG = KREG + VREG;  // 32 + 32 KiB
+constexpr int OFF_Q = NSTG * STG;
+constexpr int OFF_P = OFF_Q + 32768;
+constexpr int OFF_BAR = OFF_P + 32768;
+constexpr int MAXPG = 2560;  // page table staged in smem (40k tokens)
+constexpr int OFF_PG = OFF_BAR + 256;
+constexpr int SMEM = OFF_PG + MAXPG * 4 + 1024;
+constexpr int THREADS_TC = 192;
+constexpr int TMEM_COLS = 256;
+
+struct TcParams {
+  const __nv_bfloat16* q;
+  __nv_bfloat16* out;
+  psk_kv_layout kv;
+  const int32_t* pages;
+  int T, pos0, nq, grp, layer, qb, n_qblocks;
+  float scale_log2;
+};
+
+__global__ void __launch_bounds__(THREADS_TC, 1)
+    prefill_attn_tc(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ TcParams p) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t *full = bars, *empty = bars + 2, *s_full = bars + 4, *s_empty = bars + 5, *p_full = bars + 6,
+           *d_full = bars + 7, *d_empty = bars + 8;
+  int* s_pg = reinterpret_cast<int*>(smem + OFF_PG);
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkv = p.kv.n_kv_heads;
+  const int h = blockIdx.x % nkv;
+  const int qblk = p.n_qblocks - 1 - (int)(blockIdx.x / nkv);  // heavy blocks first
+  const int t0 = qblk * p.qb;
+  const int kv_end = p.pos0 + min(t0 + p.qb, p.T);
+  const int n_pages = (kv_end + PT - 1) / PT;
+  const int nch = (n_pages + CP - 1) / CP;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTG; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], 1);
+    }
+    tma::mbar_init(s_full, 1);
+    tma::mbar_init(s_empty, 128);
+    tma::mbar_init(p_full, 128);
+    tma::mbar_init(d_full, 1);
+    tma::mbar_init(d_empty, 128);
+    tma::fence_mbar_init();
+    tma::prefetch_map(&kvmap);
+  }
+  if (warp == 1) umma::tmem_alloc(&s_tmem, TMEM_COLS);
+  for (int j = threadIdx.x; j < n_pages && j < MAXPG; j += THREADS_TC) s_pg[j] = p.pages[j];
+  const uint32_t sq = smem_u32(smem + OFF_Q), sp = smem_u32(smem + OFF_P);
+  for (int e = threadIdx.x; e < 128 * 16; e += THREADS_TC) {
+    const int g = e >> 4, c = e & 15;
+    const int t = t0 + g / p.grp;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (t < p.T) {
+      const int qh = h * p.grp + g % p.grp;
+      v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)t * p.nq + qh) * HD + c * 8);
+    }
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sq + umma::kmajor_off(g, c, 16384)), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w));
+  }
+  umma::fence_proxy_async();
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = s_tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int c = 0; c < nch; ++c) {
+        const int st = c % NSTG;
+        tma::mbar_wait(&empty[st], ((c / NSTG) & 1) ^ 1);
+        tma::mbar_expect_tx(&full[st], STG);
+        unsigned char* kr = smem + st * STG;
+        unsigned char* vr = kr + KREG;
+        for (int pp = 0; pp < CP; ++pp) {
+          const int j = c * CP + pp;
+          const int jj = j < n_pages ? j : c * CP;  // past the end: any valid page, masked
+          const int page = jj < MAXPG ? s_pg[jj] : p.pages[jj];
+          const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
+          const int row_v = row_k + nkv * PT;
+          tma::load_2d(&kvmap, &full[st], kr + pp * 2048, 0, row_k);
+          tma::load_2d(&kvmap, &full[st], kr + CP * 2048 + pp * 2048, 64, row_k);
+          tma::load_2d(&kvmap, &full[st], vr + pp * TILE, 0, row_v);
+          tma::load_2d(&kvmap, &full[st], vr + pp * TILE + 2048, 64, row_v);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t ID_QK = umma::idesc_bf16(128, 128, false), ID_PV = umma::idesc_bf16(128, 128, true);
+      for (int c = 0; c < nch; ++c) {
+        const int st = c % NSTG;
+        const uint32_t kr = smem_u32(smem + st * STG), vr = kr + KREG;
+        tma::mbar_wait(&full[st], (c / NSTG) & 1);
+        tma::mbar_wait(s_empty, (c & 1) ^ 1);
+        umma::fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma::mma(tmem, umma::desc_k_sw128(sq + (kk >> 2) * 16384) + 2 * (kk & 3),
+                    umma::desc_k_sw128(kr + (kk >> 2) * (CP * 2048)) + 2 * (kk & 3), ID_QK, kk > 0);
+        umma::commit(s_full);
+        tma::mbar_wait(p_full, c & 1);
+        tma::mbar_wait(d_empty, (c & 1) ^ 1);
+        umma::fence_after();
+#pragma unroll
+        for (int pp = 0; pp < CP; ++pp)
+          umma::mma(tmem + 128, umma::desc_k_sw128(sp + (pp >> 2) * 16384) + 2 * (pp & 3),
+                    umma::desc_mn_sw128(vr + pp * TILE, 2048), ID_PV, pp > 0);
+        umma::commit(d_full);
+        umma::commit(&empty[st]);
+      }
+    }
+  } else {
+    const int q4 = warp & 3;
+    const int g = q4 * 32 + lane;
+    const uint32_t tS = tmem + ((uint32_t)(q4 * 32) << 16), tD = tS + 128;
+    const int t = t0 + g / p.grp;
+    const int qpos = p.pos0 + t;  // keys [0, qpos] are visible
+    float O[HD];
+#pragma unroll
+    for (int i = 0; i < HD; ++i) O[i] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    for (int c = 0; c < nch; ++c) {
+      const int key0 = c * CP * PT;
+      tma::mbar_wait(s_full, c & 1);
+      umma::fence_after();
+      float v[16];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int gi = 0; gi < 8; ++gi) {
+        umma::ld16(tS + gi * 16, v);
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (key0 + gi * 16 + e <= qpos) mx = fmaxf(mx, v[e] * p.scale_log2);
+      }
+      const float mn = fmaxf(m, mx);
+      const float base = mn == -INFINITY ? 0.f : mn;
+      const float alpha = exp2f(m - base);
+      float ladd = 0.f;
+#pragma unroll
+      for (int gi = 0; gi < 8; ++gi) {
+        umma::ld16(tS + gi * 16, v);
+        uint32_t pk[8];
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          const int key = key0 + gi * 16 + e;
+          const float p0 = key <= qpos ? exp2f(v[e] * p.scale_log2 - base) : 0.f;
+          const float p1 = key + 1 <= qpos ? exp2f(v[e + 1] * p.scale_log2 - base) : 0.f;
+          ladd += p0 + p1;
+          pk[e >> 1] = pack_bf16(p0, p1);
+        }
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc)
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sp + umma::kmajor_off(g, gi * 2 + cc, 16384)),
+                       "r"(pk[4 * cc]), "r"(pk[4 * cc + 1]), "r"(pk[4 * cc + 2]), "r"(pk[4 * cc + 3]));
+      }
+      umma::fence_before();
+      tma::mbar_arrive(s_empty);
+      umma::fence_proxy_async();
+      tma::mbar_arrive(p_full);
+      l = l * alpha + ladd;
+      tma::mbar_wait(d_full, c & 1);
+      umma::fence_after();
+#pragma unroll
+      for (int gi = 0; gi < 8; ++gi) {
+        umma::ld16(tD + gi * 16, v);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) O[gi * 16 + e] = O[gi * 16 + e] * alpha + v[e];
+      }
+      umma::fence_before();
+      tma::mbar_arrive(d_empty);
+      m = mn;
+    }
+    if (t < p.T) {
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const int qh = h * p.grp + g % p.grp;
+      uint4* dst = reinterpret_cast<uint4*>(p.out + ((int64_t)t * p.nq + qh) * HD);
+#pragma unroll
+      for (int i = 0; i < HD / 8; ++i) {
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = O[8 * i + e] * inv;
+        dst[i] = f32_to_bf16x8(f);
+      }
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    umma::fence_after();
+    umma::tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+}  // namespace tc
+
 }  // namespace pre
 }  // namespace psk
 
@@ -252,6 +468,35 @@ int psk_prefill_attn(const void* q_rot, int32_t T, int32_t pos0, int32_t n_q_hea
   p.qb = 16 * (WARPS / grp);
   p.n_qblocks = (T + p.qb - 1) / p.qb;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
+  static const bool force_hmma = getenv("PSK_PREFILL_HMMA") != nullptr;
+  if (!force_hmma && kv.n_pages > 0 && 128 % grp == 0) {
+    CUtensorMap map;
+    int rc = psk::kv_tensor_map(kv, &map);
+    if (rc) return rc;
+    tc::TcParams t;
+    t.q = p.q;
+    t.out = p.out;
+    t.kv = kv;
+    t.pages = page_table;
+    t.T = T;
+    t.pos0 = pos0;
+    t.nq = n_q_heads;
+    t.grp = grp;
+    t.layer = layer;
+    t.qb = 128 / grp;
+    t.n_qblocks = (T + t.qb - 1) / t.qb;
+    t.scale_log2 = p.scale_log2;
+    static bool tc_attr = false;
+    if (!tc_attr) {
+      PSK_CUDA_TRY(cudaFuncSetAttribute(tc::prefill_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        tc::SMEM));
+      tc_attr = true;
+    }
+    tc::prefill_attn_tc<<<t.n_qblocks * kv.n_kv_heads, tc::THREADS_TC, tc::SMEM, psk::as_stream(stream)>>>(
+        map, t);
+    PSK_LAUNCH_CHECK();
+    return PSK_OK;
+  }
   static bool attr = false;
   if (!attr) {
     PSK_CUDA_TRY(cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -81,3 +81,9 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t addr) {
 
 }  // namespace tma
 }  // namespace psk
+
+#include "../../include/psk.h"
+namespace psk {
+// 2D TMA map over a paged KV pool (decode_attn.cu): [16 token x 64 dim] SW128 boxes.
+int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out);
+}  // namespace psk
