@@ -200,7 +200,7 @@ def gemv_roofline(eng, peaks) -> dict:
         l = it[0] % cfg.n_layers
         it[0] += 1
         _lib.check(lib.psk_gemv(r.xn.data_ptr(), b.n_rows, cfg.d_model, r.p_wgu[l].data_ptr(),
-                                b.t_mrs.data_ptr(), b.n_mod, 2 * cfg.ffn, 3, r.act.data_ptr(),
+                                b.t_mrs.data_ptr(), b.n_mod, b.max_rpm, 2 * cfg.ffn, 3, r.act.data_ptr(),
                                 torch.cuda.current_stream().cuda_stream))
     dt = _time_launches(launch, 4 * cfg.n_layers)
     nbytes = b.n_mod * 2 * cfg.ffn * cfg.d_model * 2 + b.n_rows * (cfg.d_model + cfg.ffn) * 2

@@ -177,14 +177,16 @@ int psk_rmsnorm_rows(const float* h, int32_t n_rows, int32_t d, const void* cons
 
 /* Grouped weight-streaming GEMV (K5): for each module i and each of its
  * rows r, y[r, n] = sum_k x[r, k] * W_i[n, k]  (x bf16 [n_rows][K], W_i bf16
- * [N][K] row-major). Epilogues: */
+ * [N][K] row-major; K % 8 == 0, N % 16 == 0). Rows of module i are
+ * [mod_row_start[i], mod_row_start[i+1]); max_rows_per_mod bounds any
+ * module's row count (<= 32; 0 = use n_rows). Epilogues: */
 #define PSK_EPI_STORE_BF16 0   /* out bf16 [n_rows][N]                          */
 #define PSK_EPI_STORE_F32 1    /* out fp32 [n_rows][N]                          */
 #define PSK_EPI_RESID_ADD 2    /* out fp32 [n_rows][N] += y (residual stream)   */
-#define PSK_EPI_SILU_MUL 3     /* W rows interleaved [gate16|up16]...; out bf16 [n_rows][N/2] = silu(g)*u */
+#define PSK_EPI_SILU_MUL 3     /* W rows interleaved [gate8|up8]...; out bf16 [n_rows][N/2] = silu(g)*u */
 int psk_gemv(const void* x, int32_t n_rows, int32_t K, const void* const* W,
-             const int32_t* mod_row_start, int32_t n_mod, int32_t N, int32_t epilogue,
-             void* out, void* stream);
+             const int32_t* mod_row_start, int32_t n_mod, int32_t max_rows_per_mod,
+             int32_t N, int32_t epilogue, void* out, void* stream);
 
 /* RoPE (rotate-half, Llama) on q and k of the fused qkv rows (fp32
  * [n_rows][(nq+2*nkv)*hd]) at position sess_len[sess]+priv_len[r]; writes

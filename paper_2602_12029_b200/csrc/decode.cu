@@ -1,6 +1,6 @@
-// Decode-module step kernels: embedding, RMSNorm, grouped weight-streaming
-// GEMV (K5), RoPE + paged KV append, shared-prefix paged decode attention
-// (K6) and greedy argmax.
+// Decode-module step kernels: embedding, RMSNorm, RoPE + paged KV append
+// and greedy argmax (the grouped GEMV K5 is in gemv.cu, the shared-prefix
+// decode attention K6 in decode_attn.cu).
 //
 // Reference semantics: a decode module consumes the frozen base module's
 // prompt KV for positions [0, n-1) and processes the last prompt token
@@ -77,284 +77,6 @@ __global__ void rmsnorm_rows_kernel(const float* __restrict__ h, int d,
   }
 }
 
-// ------------------------------------------------------------------ GEMV --
-// Persistent, deterministic weight-streaming GEMV. The (module, row) space
-// is cut into contiguous, `align`-row-aligned CTA ranges of near-equal size
-// (so a 4-module QKV step spreads its 4 x 50 MB of weights over every SM);
-// inside a CTA each warp takes a contiguous run of (row, 1024-element chunk)
-// units, streams 4 x 16 B of W per lane per unit with L1-bypassing loads and
-// keeps the few activation rows of that module in L1. Partials land in
-// fixed shared-memory slots (no atomics) and are summed in a fixed order,
-// so results are bit-reproducible run to run.
-constexpr int GEMV_THREADS = 256;
-#ifndef PSK_GEMV_V
-#define PSK_GEMV_V 4
-#endif
-#ifndef PSK_GEMV_CTAS
-#define PSK_GEMV_CTAS 3
-#endif
-#ifndef PSK_GEMV_PIPE
-#define PSK_GEMV_PIPE 1
-#endif
-constexpr int GEMV_V = PSK_GEMV_V;         // 16-byte loads per lane per unit
-constexpr int GEMV_CH = 32 * 8 * GEMV_V;   // elements per unit (1024)
-
-template <int MAXM, int EPI>
-__global__ void __launch_bounds__(GEMV_THREADS, PSK_GEMV_CTAS) gemv_kernel(  // one resident wave
-    const __nv_bfloat16* __restrict__ X, int K, const __nv_bfloat16* const* W,
-    const int32_t* __restrict__ mrs, int n_mod, int N, int align, void* out) {
-  extern __shared__ float slots[];  // [rows_cta][cpr][MAXM]
-  const int cpr = (K + GEMV_CH - 1) / GEMV_CH;
-  const int64_t G = (int64_t)n_mod * N;
-  const int64_t ngroups = G / align;
-  const int64_t g0 = ((int64_t)blockIdx.x * ngroups / gridDim.x) * align;
-  const int64_t g1 = ((int64_t)(blockIdx.x + 1) * ngroups / gridDim.x) * align;
-  const int rows = (int)(g1 - g0);
-  pdl_trigger();
-  if (rows <= 0) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = GEMV_THREADS / 32;
-  const int64_t units = (int64_t)rows * cpr;
-  const int64_t u0 = warp * units / nw, u1 = (warp + 1) * units / nw;
-
-  float acc[MAXM];
-#pragma unroll
-  for (int m = 0; m < MAXM; ++m) acc[m] = 0.f;
-  int cur_row = -1, cur_slot = 0, M = 0, xbase = 0;
-
-  // (a macro, not a by-reference lambda: that would put acc[] in local memory)
-#define GEMV_FLUSH()                                                                   \
-  if (cur_row >= 0) {                                                                  \
-    _Pragma("unroll") for (int m = 0; m < MAXM; ++m) {                                 \
-      float v = warp_sum(acc[m]);                                                      \
-      if (lane == 0 && m < M) slots[((int64_t)cur_row * cpr + cur_slot) * MAXM + m] = v; \
-      acc[m] = 0.f;                                                                    \
-    }                                                                                  \
-  }
-
-  // zero all slots first (rows whose chunks are split over warps use only
-  // the first chunk slot of each warp's run)
-  for (int i = threadIdx.x; i < rows * cpr * MAXM; i += GEMV_THREADS) slots[i] = 0.f;
-  __syncthreads();
-
-  // Software pipeline: the weight loads of unit u+1 are issued before the
-  // FMAs of unit u, so each lane keeps 2 x GEMV_V x 16 B of HBM reads in flight.
-  uint4 wn[GEMV_V];
-  int n_rl = 0, n_ch = 0, n_M = 0, n_xb = 0;
-#define GEMV_FETCH(UU)                                                          \
-  {                                                                             \
-    n_rl = (int)((UU) / cpr);                                                   \
-    n_ch = (int)((UU) % cpr);                                                   \
-    const int64_t g_ = g0 + n_rl;                                               \
-    const int mod_ = (int)(g_ / N);                                             \
-    n_xb = mrs[mod_];                                                           \
-    n_M = mrs[mod_ + 1] - n_xb;                                                 \
-    const __nv_bfloat16* wr_ = W[mod_] + (int64_t)(g_ % N) * K;                 \
-    _Pragma("unroll") for (int j = 0; j < GEMV_V; ++j) {                        \
-      const int k = n_ch * GEMV_CH + j * 256 + lane * 8;                        \
-      wn[j] = (n_M > 0 && k < K) ? ld_stream_v4(wr_ + k) : make_uint4(0, 0, 0, 0); \
-    }                                                                           \
-  }
-  // the first weight unit streams while the producer of X drains (PDL)
-  if (PSK_GEMV_PIPE && u0 < u1) GEMV_FETCH(u0);
-  pdl_wait();
-  for (int64_t u = u0; u < u1; ++u) {
-    if (!PSK_GEMV_PIPE) GEMV_FETCH(u);
-    uint4 w[GEMV_V];
-#pragma unroll
-    for (int j = 0; j < GEMV_V; ++j) w[j] = wn[j];
-    const int rl = n_rl, ch = n_ch, uM = n_M, uxb = n_xb;
-    if (PSK_GEMV_PIPE && u + 1 < u1) GEMV_FETCH(u + 1);
-    if (rl != cur_row) {
-      GEMV_FLUSH();
-      cur_row = rl;
-      cur_slot = ch;
-      xbase = uxb;
-      M = uM;
-    }
-    if (M == 0) continue;
-#pragma unroll
-    for (int m = 0; m < MAXM; ++m) {
-      if (m < M) {
-        const __nv_bfloat16* xr = X + (int64_t)(xbase + m) * K;
-#pragma unroll
-        for (int j = 0; j < GEMV_V; ++j) {
-          const int k = ch * GEMV_CH + j * 256 + lane * 8;
-          if (k < K) {
-            uint4 xv = __ldg(reinterpret_cast<const uint4*>(xr + k));
-            float wf[8], xf[8];
-            bf16x8_to_f32(w[j], wf);
-            bf16x8_to_f32(xv, xf);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[m] = fmaf(wf[e], xf[e], acc[m]);
-          }
-        }
-      }
-    }
-  }
-  GEMV_FLUSH();
-#undef GEMV_FLUSH
-#undef GEMV_FETCH
-  __syncthreads();
-
-  // epilogue: thread per (row, m)
-  if (EPI == PSK_EPI_SILU_MUL) {
-    // rows come in groups of 32: [gate 16 | up 16] -> 16 outputs
-    const int pairs = rows / 2;
-    for (int i = threadIdx.x; i < pairs * MAXM; i += GEMV_THREADS) {
-      const int pi = i / MAXM, m = i % MAXM;
-      const int grp = pi / 16, lo = pi % 16;
-      const int rg = grp * 32 + lo, ru = rg + 16;
-      const int64_t gg = g0 + rg;
-      const int mod = (int)(gg / N);
-      const int n = (int)(gg % N);
-      const int Mm = mrs[mod + 1] - mrs[mod];
-      if (m >= Mm) continue;
-      float vg = 0.f, vu = 0.f;
-      for (int c = 0; c < cpr; ++c) {
-        vg += slots[((int64_t)rg * cpr + c) * MAXM + m];
-        vu += slots[((int64_t)ru * cpr + c) * MAXM + m];
-      }
-      const float s = vg / (1.f + __expf(-vg));
-      const int f = (n / 32) * 16 + (n % 16);
-      reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)(mrs[mod] + m) * (N / 2) + f] = f2bf(s * vu);
-    }
-  } else {
-    for (int i = threadIdx.x; i < rows * MAXM; i += GEMV_THREADS) {
-      const int rl = i / MAXM, m = i % MAXM;
-      const int64_t gg = g0 + rl;
-      const int mod = (int)(gg / N);
-      const int n = (int)(gg % N);
-      const int Mm = mrs[mod + 1] - mrs[mod];
-      if (m >= Mm) continue;
-      float v = 0.f;
-      for (int c = 0; c < cpr; ++c) v += slots[((int64_t)rl * cpr + c) * MAXM + m];
-      const int64_t o = (int64_t)(mrs[mod] + m) * N + n;
-      if (EPI == PSK_EPI_STORE_BF16) reinterpret_cast<__nv_bfloat16*>(out)[o] = f2bf(v);
-      if (EPI == PSK_EPI_STORE_F32) reinterpret_cast<float*>(out)[o] = v;
-      if (EPI == PSK_EPI_RESID_ADD) reinterpret_cast<float*>(out)[o] += v;
-    }
-  }
-}
-
-// -------------------------------------------------- tensor-core GEMV ----
-// For 2..16 rows per module (multi-session decode batches) the FMA count per
-// weight byte outgrows the CUDA cores, so the dot products run on mma.sync
-// m16n8k16 (W = A operand, 16 weight rows; x = B operand, 8 activation rows
-// per n-tile). Weights are still streamed straight from HBM into registers:
-// a fixed permutation of k inside every 32-column chunk (applied identically
-// to W and x; a dot product is permutation-invariant) makes thread t of a
-// quad own physical columns [8t, 8t+8) = its A/B fragments for two k-steps,
-// so every fragment is one coalesced 16-byte load. Work unit = (16-row tile,
-// 1024-column chunk); each unit's partial lands in its own shared-memory
-// slot (deterministic, no atomics) and the epilogue is the scalar one above.
-template <int NT, int EPI>
-__global__ void __launch_bounds__(GEMV_THREADS, PSK_GEMV_CTAS) gemv_mma_kernel(
-    const __nv_bfloat16* __restrict__ X, int K, const __nv_bfloat16* const* W,
-    const int32_t* __restrict__ mrs, int n_mod, int N, int align, void* out) {
-  constexpr int MAXM = NT * 8;
-  extern __shared__ float slots[];  // [rows_cta][cpr][MAXM]
-  const int cpr = (K + GEMV_CH - 1) / GEMV_CH;
-  const int64_t G = (int64_t)n_mod * N;
-  const int64_t ngroups = G / align;
-  const int64_t g0 = ((int64_t)blockIdx.x * ngroups / gridDim.x) * align;
-  const int64_t g1 = ((int64_t)(blockIdx.x + 1) * ngroups / gridDim.x) * align;
-  const int rows = (int)(g1 - g0);
-  pdl_trigger();
-  if (rows <= 0) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gq = lane >> 2, tq = lane & 3;
-  const int tiles = rows / 16;
-  const int64_t units = (int64_t)tiles * cpr;
-  const int64_t u0 = warp * units / (GEMV_THREADS / 32), u1 = (warp + 1) * units / (GEMV_THREADS / 32);
-  for (int i = threadIdx.x; i < rows * cpr * MAXM; i += GEMV_THREADS) slots[i] = 0.f;
-  __syncthreads();
-  pdl_wait();
-  for (int64_t u = u0; u < u1; ++u) {
-    const int tl = (int)(u / cpr), ch = (int)(u % cpr);
-    const int64_t r0 = g0 + (int64_t)tl * 16;
-    const int mod = (int)(r0 / N);
-    const int xb = mrs[mod], M = mrs[mod + 1] - xb;
-    if (M == 0) continue;
-    const __nv_bfloat16* wa_p = W[mod] + (r0 % N + gq) * (int64_t)K;
-    const __nv_bfloat16* wb_p = wa_p + 8 * (int64_t)K;
-    float c[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) c[nt][0] = c[nt][1] = c[nt][2] = c[nt][3] = 0.f;
-    const int cbeg = ch * GEMV_CH + tq * 8;
-    const int cend = min(K, (ch + 1) * GEMV_CH);
-#pragma unroll 1
-    for (int col0 = cbeg; col0 < cend; col0 += 4 * 32) {
-      uint4 wa[4], wb[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int col = col0 + q * 32;
-        const bool ok = col < cend;
-        wa[q] = ok ? ld_stream_v4(wa_p + col) : make_uint4(0, 0, 0, 0);
-        wb[q] = ok ? ld_stream_v4(wb_p + col) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int col = col0 + q * 32;
-        if (col >= cend) break;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int xr = nt * 8 + gq;
-          const uint4 xv = xr < M ? __ldg(reinterpret_cast<const uint4*>(X + (int64_t)(xb + xr) * K + col))
-                                  : make_uint4(0, 0, 0, 0);
-          const uint32_t a0[4] = {wa[q].x, wb[q].x, wa[q].y, wb[q].y};
-          const uint32_t a1[4] = {wa[q].z, wb[q].z, wa[q].w, wb[q].w};
-          mma_bf16_16816(c[nt], a0, xv.x, xv.y);
-          mma_bf16_16816(c[nt], a1, xv.z, xv.w);
-        }
-      }
-    }
-    // C fragment: (row gq / gq+8, cols 2tq, 2tq+1) of [16 weight rows x 8 x rows]
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int m = nt * 8 + 2 * tq;
-      float* s0 = slots + ((int64_t)(tl * 16 + gq) * cpr + ch) * MAXM;
-      float* s8 = slots + ((int64_t)(tl * 16 + gq + 8) * cpr + ch) * MAXM;
-      if (m < M) { s0[m] = c[nt][0]; s8[m] = c[nt][2]; }
-      if (m + 1 < M) { s0[m + 1] = c[nt][1]; s8[m + 1] = c[nt][3]; }
-    }
-  }
-  __syncthreads();
-  if (EPI == PSK_EPI_SILU_MUL) {
-    const int pairs = rows / 2;
-    for (int i = threadIdx.x; i < pairs * MAXM; i += GEMV_THREADS) {
-      const int pi = i / MAXM, m = i % MAXM;
-      const int rg = (pi / 16) * 32 + pi % 16, ru = rg + 16;
-      const int64_t gg = g0 + rg;
-      const int mod = (int)(gg / N);
-      const int n = (int)(gg % N);
-      if (m >= mrs[mod + 1] - mrs[mod]) continue;
-      float vg = 0.f, vu = 0.f;
-      for (int cc = 0; cc < cpr; ++cc) {
-        vg += slots[((int64_t)rg * cpr + cc) * MAXM + m];
-        vu += slots[((int64_t)ru * cpr + cc) * MAXM + m];
-      }
-      const float sg = vg / (1.f + __expf(-vg));
-      reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)(mrs[mod] + m) * (N / 2) + (n / 32) * 16 + n % 16] =
-          f2bf(sg * vu);
-    }
-  } else {
-    for (int i = threadIdx.x; i < rows * MAXM; i += GEMV_THREADS) {
-      const int rl = i / MAXM, m = i % MAXM;
-      const int64_t gg = g0 + rl;
-      const int mod = (int)(gg / N);
-      const int n = (int)(gg % N);
-      if (m >= mrs[mod + 1] - mrs[mod]) continue;
-      float v = 0.f;
-      for (int cc = 0; cc < cpr; ++cc) v += slots[((int64_t)rl * cpr + cc) * MAXM + m];
-      const int64_t o = (int64_t)(mrs[mod] + m) * N + n;
-      if (EPI == PSK_EPI_STORE_BF16) reinterpret_cast<__nv_bfloat16*>(out)[o] = f2bf(v);
-      if (EPI == PSK_EPI_STORE_F32) reinterpret_cast<float*>(out)[o] = v;
-      if (EPI == PSK_EPI_RESID_ADD) reinterpret_cast<float*>(out)[o] += v;
-    }
-  }
-}
-
 // ---------------------------------------------------- RoPE + KV append ---
 
 __device__ __forceinline__ __nv_bfloat16* kv_ptr(const psk_kv_layout& kv, int32_t page, int layer,
@@ -408,10 +130,33 @@ __global__ void argmax_advance_kernel(psk_decode_batch b, const float* __restric
   const float* x = logits + (int64_t)r * V;
   float bv = -INFINITY;
   int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) {
-    const float v = x[i];
-    if (v > bv) { bv = v; bi = i; }
+  // ties resolve to the lowest index (first maximum, as the reference argmax)
+#define PSK_TAKE(v, i) \
+  if ((v) > bv || ((v) == bv && (i) < bi)) { bv = (v); bi = (i); }
+  int tail = 0;
+  if ((V & 3) == 0) {
+    // 4 independent float4 loads in flight per thread (the logits sit in L2)
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const int V4 = V >> 2, step = blockDim.x;
+    int i = threadIdx.x;
+    for (; i + 3 * step < V4; i += 4 * step) {
+      float4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = __ldg(x4 + i + u * step);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = (i + u * step) * 4;
+        PSK_TAKE(q[u].x, e) PSK_TAKE(q[u].y, e + 1) PSK_TAKE(q[u].z, e + 2) PSK_TAKE(q[u].w, e + 3)
+      }
+    }
+    for (; i < V4; i += step) {
+      const float4 q = __ldg(x4 + i);
+      PSK_TAKE(q.x, 4 * i) PSK_TAKE(q.y, 4 * i + 1) PSK_TAKE(q.z, 4 * i + 2) PSK_TAKE(q.w, 4 * i + 3)
+    }
+    tail = V;
   }
+  for (int i = tail + threadIdx.x; i < V; i += blockDim.x) PSK_TAKE(__ldg(x + i), i)
+#undef PSK_TAKE
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -446,53 +191,6 @@ __global__ void argmax_advance_kernel(psk_decode_batch b, const float* __restric
 
 using namespace psk::dec;
 
-namespace {
-
-template <int MAXM, bool MMA = false>
-int launch_gemv(const void* x, int K, const void* const* W, const int32_t* mrs, int n_mod, int N,
-                int epi, void* out, cudaStream_t s) {
-  const int align = epi == PSK_EPI_SILU_MUL ? 32 : (MMA ? 16 : 1);
-  const int cpr = (K + GEMV_CH - 1) / GEMV_CH;
-  const int64_t G = (int64_t)n_mod * N;
-  static int sms = 0;
-  if (!sms) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int grid = sms * PSK_GEMV_CTAS;  // one resident wave (matches the launch bounds)
-  // keep the partial slots of PSK_GEMV_CTAS co-resident CTAs within shared memory
-  const int64_t slot_bytes_per_row = (int64_t)cpr * MAXM * 4;
-  const int64_t smem_cap = (225 * 1024) / PSK_GEMV_CTAS;
-  while (((G + grid - 1) / grid + align) * slot_bytes_per_row > smem_cap) grid += sms;
-  if (grid > G / align) grid = (int)(G / align);
-  const size_t smem = (size_t)(((G / align + grid - 1) / grid) * align) * slot_bytes_per_row;
-  auto xb = reinterpret_cast<const __nv_bfloat16*>(x);
-  auto Wb = reinterpret_cast<const __nv_bfloat16* const*>(W);
-#define PSK_GEMV_CASE(E)                                                                        \
-  case E: {                                                                                     \
-    auto k = MMA ? gemv_mma_kernel<(MAXM + 7) / 8, E> : gemv_kernel<MAXM, E>;                   \
-    if (smem > 48 * 1024)                                                                       \
-      PSK_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    PSK_CUDA_TRY(psk::launch_pdl(k, dim3(grid), dim3(GEMV_THREADS), smem, s, xb, K, Wb, mrs,   \
-                                 n_mod, N, align, out));                                        \
-    break;                                                                                      \
-  }
-  switch (epi) {
-    PSK_GEMV_CASE(PSK_EPI_STORE_BF16)
-    PSK_GEMV_CASE(PSK_EPI_STORE_F32)
-    PSK_GEMV_CASE(PSK_EPI_RESID_ADD)
-    PSK_GEMV_CASE(PSK_EPI_SILU_MUL)
-    default:
-      psk::set_error("psk_gemv: unknown epilogue %d", epi);
-      return PSK_EINVAL;
-  }
-#undef PSK_GEMV_CASE
-  PSK_LAUNCH_CHECK();
-  return PSK_OK;
-}
-
-}  // namespace
 
 extern "C" {
 
@@ -515,27 +213,6 @@ int psk_rmsnorm_rows(const float* h, int32_t n_rows, int32_t d, const void* cons
                                eps, reinterpret_cast<__nv_bfloat16*>(out)));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
-}
-
-int psk_gemv(const void* x, int32_t n_rows, int32_t K, const void* const* W,
-             const int32_t* mod_row_start, int32_t n_mod, int32_t N, int32_t epilogue, void* out,
-             void* stream) {
-  PSK_CHECK_ARG(x && W && mod_row_start && out && K % 8 == 0 && N > 0 && n_mod > 0,
-                "psk_gemv: bad args");
-  PSK_CHECK_ARG(epilogue != PSK_EPI_SILU_MUL || N % 32 == 0, "psk_gemv: SILU_MUL needs N%%32==0");
-  const int maxm = n_rows - n_mod + 1;
-  cudaStream_t s = psk::as_stream(stream);
-  if (maxm <= 1) return launch_gemv<1>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);
-  if (N % 16 == 0 && !getenv("PSK_GEMV_SCALAR")) {  // tensor-core path for 2..16 rows / module
-    if (maxm <= 8) return launch_gemv<8, true>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);
-    if (maxm <= 16) return launch_gemv<16, true>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);
-  }
-  if (maxm <= 2) return launch_gemv<2>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);
-  if (maxm <= 4) return launch_gemv<4>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);
-  if (maxm <= 8) return launch_gemv<8>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);
-  if (maxm <= 16) return launch_gemv<16>(x, K, W, mod_row_start, n_mod, N, epilogue, out, s);
-  psk::set_error("psk_gemv: more than 16 rows per module (%d)", maxm);
-  return PSK_EINVAL;
 }
 
 int psk_rope_append(const psk_decode_batch* b, const float* qkv, int32_t n_q_heads,

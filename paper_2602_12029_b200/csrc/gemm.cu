@@ -17,7 +17,7 @@
 // Tiles are walked m-fastest so one wave shares its B (weight) tiles in L2.
 //
 // Fused epilogues: bf16 store, fp32 residual add, SiLU(gate)*up over the
-// [gate16|up16]-interleaved weight layout, and QKV -> RoPE (rotate-half) ->
+// [gate8|up8]-interleaved weight layout, and QKV -> RoPE (rotate-half) ->
 // q_rot + paged K/V write (K2, model.ts:307-311 cache push, done in place).
 #include "common.cuh"
 
@@ -233,10 +233,12 @@ __device__ void epilogue_tile(const Epi& e, uint32_t tacc, int row, bool row_ok,
         d[i] = o;
       }
     } else if (e.mode == PSK_EPI_SILU_MUL) {
+      // 32 columns = [gate 8 | up 8 | gate 8 | up 8] -> 16 outputs
       float o[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const float g = v[i], u = v[16 + i];
+        const int b = (i >> 3) * 16 + (i & 7);
+        const float g = v[b], u = v[b + 8];
         o[i] = g / (1.f + __expf(-g)) * u;
       }
       __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(e.out) + (int64_t)row * e.ldo + col / 2;

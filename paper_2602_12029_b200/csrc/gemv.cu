@@ -1,0 +1,297 @@
+// K5 — grouped decode GEMV: y[r, n] = sum_k x[r, k] * W_mod(r)[n, k] for the
+// 1..32 decode rows of each of n_mod co-batched decode modules.
+//
+// Decode is weight-streaming: every step reads each module's full weight
+// set once (4 x 15 GB at the 8B shape) while the activation side is a few
+// rows. The kernel is therefore built around keeping HBM saturated:
+//
+//   * persistent, one CTA per SM; the (module, weight-row) space is cut into
+//     16-row tiles and each CTA owns a contiguous run of tiles (balanced to
+//     within one tile; tiles never straddle modules since N % 16 == 0);
+//   * warp 8 is a producer that streams each tile as 1024-column stages
+//     (16 rows x 2 KiB) with cp.async.bulk (TMA bulk copies, L2 evict-first)
+//     into a 5-6 stage shared-memory ring (~200 KiB in flight per SM) — it
+//     does not wait on the previous kernel (PDL), so the first stages land
+//     while that kernel drains;
+//   * warps 0-7 each own 128 columns of every stage and run mma.sync
+//     m16n8k16 (weights = A, 16 rows; activations = B, 8 rows per n-tile)
+//     with a fixed k-permutation inside every 32-column group (applied to W
+//     and x alike: a dot product is order-invariant) so every fragment is
+//     one 16-byte shared-memory read (rows padded by 64 B: conflict-free);
+//     x fragments come from L2 and are prefetched one stage ahead;
+//   * at the end of a tile the 8 warps' partials meet in shared memory
+//     (double-buffered, one named barrier per tile) and are summed in a
+//     fixed order — results are bit-reproducible — then the fused epilogue
+//     stores bf16 / fp32, adds into the fp32 residual stream, or applies
+//     SiLU(gate)*up: gate/up rows are interleaved in 8-row groups, so each
+//     16-row tile holds 8 gate + 8 matching up rows.
+//
+// Replaces the per-module dense projections of the reference decode forward
+// (frontend/src/model.ts:298-306 q/k/v, :318 o-proj, :322-323 MLP, :334
+// logits), executed here for all decode modules of a step in one launch.
+#include "common.cuh"
+#include "mma.cuh"
+#include "tma.cuh"
+
+namespace psk {
+namespace gemv {
+
+constexpr int CW = 8;                      // consumer warps
+constexpr int THREADS = (CW + 1) * 32;     // + one producer warp
+constexpr int TR = 16;                     // weight rows per tile (MMA M)
+constexpr int KC = CW * 128;               // columns per stage (128 per consumer warp)
+constexpr int ROW_BYTES = KC * 2 + 64;     // padded shared-memory row
+constexpr int STAGE_BYTES = TR * ROW_BYTES;
+constexpr int SMEM_LIMIT = 227 * 1024;
+
+template <int NT>
+struct Cfg {
+  static constexpr int MAXM = NT * 8;  // activation rows per module
+  static constexpr int RED_BYTES = 2 * CW * TR * MAXM * 4;
+  static constexpr int STAGES = (SMEM_LIMIT - RED_BYTES - 256) / STAGE_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + RED_BYTES + 256;
+  static_assert(STAGES >= 3, "ring too shallow");
+};
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// 1-D TMA bulk copy global -> shared completing on `bar` (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+      "[%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(tma::sa(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint4 lds128(const unsigned char* p) {
+  return *reinterpret_cast<const uint4*>(p);
+}
+
+// x fragments (B operand) of stage `j` for this thread: row nt*8+gq of the
+// tile's module, columns [8tq, 8tq+8) of each of the warp's four 32-column
+// groups; zero outside the module's rows or past K.
+template <int NT>
+__device__ __forceinline__ void load_x(uint4 (&xf)[NT][4], const __nv_bfloat16* __restrict__ X, int K,
+                                       const int32_t* __restrict__ mrs, int tpm, int t, int c, int warp,
+                                       int gq, int tq) {
+  const int mod = t / tpm;
+  const int xb = mrs[mod], M = mrs[mod + 1] - xb;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int row = nt * 8 + gq;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const int col = c * KC + warp * 128 + g * 32 + tq * 8;
+      xf[nt][g] = (row < M && col < K)
+                      ? __ldg(reinterpret_cast<const uint4*>(X + (int64_t)(xb + row) * K + col))
+                      : make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
+template <int NT, int EPI>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemv_kernel(const __nv_bfloat16* __restrict__ X, int K, const __nv_bfloat16* const* __restrict__ W,
+                const int32_t* __restrict__ mrs, int n_mod, int N, void* __restrict__ out) {
+  using C = Cfg<NT>;
+  constexpr int MAXM = C::MAXM;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* red = reinterpret_cast<float*>(smem + C::STAGES * STAGE_BYTES);  // [2][CW][TR][MAXM]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * STAGE_BYTES + C::RED_BYTES);
+  uint64_t* empty = full + C::STAGES;
+
+  const int tpm = N / TR;  // tiles per module
+  const int tiles = n_mod * tpm;
+  const int t0 = (int)((int64_t)blockIdx.x * tiles / gridDim.x);
+  const int t1 = (int)((int64_t)(blockIdx.x + 1) * tiles / gridDim.x);
+  const int cpt = (K + KC - 1) / KC;  // stages per tile
+  const int n_stages = (t1 - t0) * cpt;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], CW);
+    }
+    tma::fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+
+  if (warp == CW) {
+    // ---- producer: weights do not depend on the previous kernel ----
+    const uint64_t pol = policy_evict_first();
+    for (int j = 0; j < n_stages; ++j) {
+      const int s = j % C::STAGES;
+      tma::mbar_wait(&empty[s], ((j / C::STAGES) & 1) ^ 1);
+      const int t = t0 + j / cpt, c = j % cpt;
+      const int mod = t / tpm;
+      if (mrs[mod + 1] == mrs[mod]) {  // module without rows this step
+        if (lane == 0) tma::mbar_arrive(&full[s]);
+        continue;
+      }
+      const int cols = min(KC, K - c * KC);
+      if (lane == 0) tma::mbar_expect_tx(&full[s], TR * cols * 2);
+      __syncwarp();
+      if (lane < TR) {
+        const __nv_bfloat16* src = W[mod] + ((int64_t)(t % tpm) * TR + lane) * K + (int64_t)c * KC;
+        bulk_g2s(tma::sa(smem + s * STAGE_BYTES + lane * ROW_BYTES), src, cols * 2, &full[s], pol);
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----
+  const int gq = lane >> 2, tq = lane & 3;
+  float acc[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+  uint4 xn[NT][4];
+  pdl_wait();  // x (and the residual stream) come from the previous kernel
+  if (n_stages > 0) load_x<NT>(xn, X, K, mrs, tpm, t0, 0, warp, gq, tq);
+  int buf = 0;
+  for (int j = 0; j < n_stages; ++j) {
+    const int s = j % C::STAGES;
+    const int t = t0 + j / cpt, c = j % cpt;
+    const int mod = t / tpm;
+    const int xb = mrs[mod], M = mrs[mod + 1] - xb;
+    uint4 xc[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int g = 0; g < 4; ++g) xc[nt][g] = xn[nt][g];
+    if (j + 1 < n_stages) {
+      const int jn = j + 1;
+      load_x<NT>(xn, X, K, mrs, tpm, t0 + jn / cpt, jn % cpt, warp, gq, tq);
+    }
+    tma::mbar_wait(&full[s], (j / C::STAGES) & 1);
+    if (M > 0) {
+      const unsigned char* st = smem + s * STAGE_BYTES + (warp * 128 + tq * 8) * 2;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const bool ok = c * KC + warp * 128 + g * 32 + tq * 8 < K;
+        const uint4 wa = ok ? lds128(st + gq * ROW_BYTES + g * 64) : make_uint4(0, 0, 0, 0);
+        const uint4 wb = ok ? lds128(st + (gq + 8) * ROW_BYTES + g * 64) : make_uint4(0, 0, 0, 0);
+        const uint32_t a0[4] = {wa.x, wb.x, wa.y, wb.y};
+        const uint32_t a1[4] = {wa.z, wb.z, wa.w, wb.w};
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          if (nt * 8 >= M) break;
+          mma_bf16_16816(acc[nt], a0, xc[nt][g].x, xc[nt][g].y);
+          mma_bf16_16816(acc[nt], a1, xc[nt][g].z, xc[nt][g].w);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) tma::mbar_arrive(&empty[s]);
+    if (c != cpt - 1) continue;
+
+    // ---- tile complete: reduce the 8 warps' partials, fused epilogue ----
+    float* rb = red + (size_t)buf * CW * TR * MAXM;
+    if (M > 0) {
+      float* mine = rb + warp * TR * MAXM;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int m = nt * 8 + 2 * tq;
+        mine[gq * MAXM + m] = acc[nt][0];
+        mine[gq * MAXM + m + 1] = acc[nt][1];
+        mine[(gq + 8) * MAXM + m] = acc[nt][2];
+        mine[(gq + 8) * MAXM + m + 1] = acc[nt][3];
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+    asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
+    if (M > 0) {
+      const int n0 = (t % tpm) * TR;
+      if (EPI == PSK_EPI_SILU_MUL) {
+        for (int i = threadIdx.x; i < 8 * M; i += CW * 32) {
+          const int r = i & 7, m = i >> 3;
+          float gv = 0.f, uv = 0.f;
+#pragma unroll
+          for (int w = 0; w < CW; ++w) {
+            gv += rb[(w * TR + r) * MAXM + m];
+            uv += rb[(w * TR + r + 8) * MAXM + m];
+          }
+          const float sg = gv / (1.f + __expf(-gv));
+          reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)(xb + m) * (N / 2) + n0 / 2 + r] = f2bf(sg * uv);
+        }
+      } else {
+        for (int i = threadIdx.x; i < TR * M; i += CW * 32) {
+          const int r = i & (TR - 1), m = i / TR;
+          float v = 0.f;
+#pragma unroll
+          for (int w = 0; w < CW; ++w) v += rb[(w * TR + r) * MAXM + m];
+          const int64_t o = (int64_t)(xb + m) * N + n0 + r;
+          if (EPI == PSK_EPI_STORE_BF16) reinterpret_cast<__nv_bfloat16*>(out)[o] = f2bf(v);
+          if (EPI == PSK_EPI_STORE_F32) reinterpret_cast<float*>(out)[o] = v;
+          if (EPI == PSK_EPI_RESID_ADD) reinterpret_cast<float*>(out)[o] += v;
+        }
+      }
+    }
+    buf ^= 1;
+  }
+}
+
+template <int NT, int EPI>
+int launch(const void* x, int K, const void* const* W, const int32_t* mrs, int n_mod, int N, void* out,
+           cudaStream_t s) {
+  static bool attr_set = false;
+  auto k = gemv_kernel<NT, EPI>;
+  if (!attr_set) {
+    PSK_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NT>::SMEM));
+    attr_set = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int tiles = n_mod * (N / TR);
+  const int grid = tiles < sms ? tiles : sms;
+  PSK_CUDA_TRY(psk::launch_pdl(k, dim3(grid), dim3(THREADS), (size_t)Cfg<NT>::SMEM, s,
+                               reinterpret_cast<const __nv_bfloat16*>(x), K,
+                               reinterpret_cast<const __nv_bfloat16* const*>(W), mrs, n_mod, N, out));
+  PSK_LAUNCH_CHECK();
+  return PSK_OK;
+}
+
+template <int NT>
+int dispatch(int epi, const void* x, int K, const void* const* W, const int32_t* mrs, int n_mod, int N,
+             void* out, cudaStream_t s) {
+  switch (epi) {
+    case PSK_EPI_STORE_BF16: return launch<NT, PSK_EPI_STORE_BF16>(x, K, W, mrs, n_mod, N, out, s);
+    case PSK_EPI_STORE_F32: return launch<NT, PSK_EPI_STORE_F32>(x, K, W, mrs, n_mod, N, out, s);
+    case PSK_EPI_RESID_ADD: return launch<NT, PSK_EPI_RESID_ADD>(x, K, W, mrs, n_mod, N, out, s);
+    case PSK_EPI_SILU_MUL: return launch<NT, PSK_EPI_SILU_MUL>(x, K, W, mrs, n_mod, N, out, s);
+  }
+  psk::set_error("psk_gemv: unknown epilogue %d", epi);
+  return PSK_EINVAL;
+}
+
+}  // namespace gemv
+}  // namespace psk
+
+extern "C" int psk_gemv(const void* x, int32_t n_rows, int32_t K, const void* const* W,
+                        const int32_t* mod_row_start, int32_t n_mod, int32_t max_rows_per_mod, int32_t N,
+                        int32_t epilogue, void* out, void* stream) {
+  PSK_CHECK_ARG(x && W && mod_row_start && out && n_rows >= 0 && K > 0 && K % 8 == 0 && n_mod > 0,
+                "psk_gemv: bad args (K must be a positive multiple of 8)");
+  PSK_CHECK_ARG(N > 0 && N % 16 == 0, "psk_gemv: N must be a positive multiple of 16");
+  const int maxm = max_rows_per_mod > 0 ? max_rows_per_mod : n_rows;
+  if (n_rows == 0) return PSK_OK;
+  cudaStream_t s = psk::as_stream(stream);
+  using namespace psk::gemv;
+  if (maxm <= 8) return dispatch<1>(epilogue, x, K, W, mod_row_start, n_mod, N, out, s);
+  if (maxm <= 16) return dispatch<2>(epilogue, x, K, W, mod_row_start, n_mod, N, out, s);
+  if (maxm <= 32) return dispatch<4>(epilogue, x, K, W, mod_row_start, n_mod, N, out, s);
+  psk::set_error("psk_gemv: more than 32 rows per module (%d)", maxm);
+  return PSK_EINVAL;
+}

@@ -103,8 +103,10 @@ def _mix(*parts: int) -> int:
 
 class ModuleWeights:
     """One module's bf16 weights in the kernels' fused layouts:
-    wqkv [q|k|v rows][d]; wgu rows interleaved in 16-row groups
-    [gate 16 | up 16] so the gate/up GEMV epilogue fuses SiLU*mul."""
+    wqkv [q|k|v rows][d]; wgu rows interleaved in 8-row groups
+    [gate 8 | up 8], so every 16-row MMA tile of the gate/up GEMV (and
+    every 32-column slice of the prefill GEMM) holds matching gate and up
+    rows and the epilogue fuses SiLU*mul."""
 
     def __init__(self, cfg: LlamaConfig, seed: int, device: int = 0, with_head: bool = True,
                  std: float = 0.02):
@@ -165,7 +167,7 @@ class ModuleWeights:
         qd, kd = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
         for l in range(c.n_layers):
             qkv = f(self.wqkv[l])
-            gu = f(self.wgu[l]).view(-1, 2, 16, c.d_model)
+            gu = f(self.wgu[l]).view(-1, 2, 8, c.d_model)
             out["layers"].append({
                 "attn_norm": f(self.attn_norm[l]), "wq": qkv[:qd], "wk": qkv[qd:qd + kd],
                 "wv": qkv[qd + kd:], "wo": f(self.wo[l]), "mlp_norm": f(self.mlp_norm[l]),
@@ -258,6 +260,7 @@ class DecodeBatch:
             row_in_sess.append(len(sess_rows[r.session]))
             sess_rows[r.session].append(j)
         self.max_rps = max(1, max(len(x) for x in sess_rows))
+        self.max_rpm = max(mrs[i + 1] - mrs[i] for i in range(len(self.mod_ids)))  # rows per module
         msp = max(1, max(len(s.pages) for s in sessions))
         mrp = max(1, max(len(r.pages) for r in self.rows))
         i32 = lambda x: torch.tensor(x, dtype=torch.int32, device=dev)  # noqa: E731
@@ -385,23 +388,23 @@ class DecodeRunner:
         for l in range(cfg.n_layers):
             chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_attn_norm[l]), _ptr(b.t_row_mod),
                                      C.c_float(cfg.norm_eps), _ptr(self.xn), s))
-            chk(lib.psk_gemv(_ptr(self.xn), R, d, _ptr(self.p_wqkv[l]), mrs, b.n_mod, cfg.qkv_dim,
+            chk(lib.psk_gemv(_ptr(self.xn), R, d, _ptr(self.p_wqkv[l]), mrs, b.n_mod, b.max_rpm, cfg.qkv_dim,
                              1, _ptr(self.qkv), s))
             chk(lib.psk_rope_append(bc, _ptr(self.qkv), cfg.n_heads, _ptr(self.rope), l, kvl,
                                     _ptr(self.q_rot), s))
             chk(lib.psk_decode_attn(bc, _ptr(self.q_rot), cfg.n_heads, l, kvl, self.splits,
                                     _ptr(self.ws), _ptr(self.attn), s))
             chk(lib.psk_gemv(_ptr(self.attn), R, cfg.n_heads * cfg.head_dim, _ptr(self.p_wo[l]), mrs,
-                             b.n_mod, d, 2, _ptr(self.h), s))
+                             b.n_mod, b.max_rpm, d, 2, _ptr(self.h), s))
             chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_mlp_norm[l]), _ptr(b.t_row_mod),
                                      C.c_float(cfg.norm_eps), _ptr(self.xn), s))
-            chk(lib.psk_gemv(_ptr(self.xn), R, d, _ptr(self.p_wgu[l]), mrs, b.n_mod, 2 * cfg.ffn, 3,
+            chk(lib.psk_gemv(_ptr(self.xn), R, d, _ptr(self.p_wgu[l]), mrs, b.n_mod, b.max_rpm, 2 * cfg.ffn, 3,
                              _ptr(self.act), s))
-            chk(lib.psk_gemv(_ptr(self.act), R, cfg.ffn, _ptr(self.p_wdown[l]), mrs, b.n_mod, d, 2,
+            chk(lib.psk_gemv(_ptr(self.act), R, cfg.ffn, _ptr(self.p_wdown[l]), mrs, b.n_mod, b.max_rpm, d, 2,
                              _ptr(self.h), s))
         chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_final_norm), _ptr(b.t_row_mod),
                                  C.c_float(cfg.norm_eps), _ptr(self.xn), s))
-        chk(lib.psk_gemv(_ptr(self.xn), R, d, _ptr(self.p_head), mrs, b.n_mod, cfg.vocab, 1,
+        chk(lib.psk_gemv(_ptr(self.xn), R, d, _ptr(self.p_head), mrs, b.n_mod, b.max_rpm, cfg.vocab, 1,
                          _ptr(self.logits), s))
         chk(lib.psk_argmax_advance(bc, _ptr(self.logits), cfg.vocab, _ptr(self.out_tokens),
                                    self.max_new, s))

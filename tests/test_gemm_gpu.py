@@ -59,7 +59,7 @@ def test_gemm_silu_mul_interleaved():
     M, F, K = 200, 768, 256
     A = _rand(M, K, seed=5)
     Wg, Wu = _rand(F, K, std=0.05, seed=6), _rand(F, K, std=0.05, seed=7)
-    Wgu = torch.stack([Wg.view(-1, 16, K), Wu.view(-1, 16, K)], 1).reshape(2 * F, K).contiguous()
+    Wgu = torch.stack([Wg.view(-1, 8, K), Wu.view(-1, 8, K)], 1).reshape(2 * F, K).contiguous()
     ref = torch.nn.functional.silu(A.float() @ Wg.float().T) * (A.float() @ Wu.float().T)
     out = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
     _gemm(A, Wgu, 3, out, F)

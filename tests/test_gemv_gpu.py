@@ -1,6 +1,7 @@
-"""K5 grouped decode GEMV (scalar weight-streaming path for 1 row per module,
-tensor-core path for 2..16) vs a torch fp32 reference on identical bf16
-operands, all epilogues, ragged rows per module (incl. modules with no rows).
+"""K5 grouped decode GEMV (TMA-bulk weight stream + mma.sync, 1..32 rows per
+module) vs a torch fp32 reference on identical bf16 operands, all
+epilogues, ragged rows per module (incl. modules with no rows, one module
+holding every row, K not a multiple of the 1024-column stage).
 Tolerance: |gpu - ref| <= 2e-3 * max|ref| + 1e-4 (fp32 outputs),
 1e-2 * max|ref| + 1e-3 (bf16 outputs)."""
 
@@ -26,7 +27,7 @@ def _run(rows_per_mod, N, K, epi, seed=0):
     for i in range(n_mod):
         ref[mrs[i]:mrs[i + 1]] = x[mrs[i]:mrs[i + 1]].float() @ W[i].float().T
     if epi == 3:
-        y = ref.view(R, -1, 2, 16)
+        y = ref.view(R, -1, 2, 8)
         ref = (torch.nn.functional.silu(y[:, :, 0]) * y[:, :, 1]).reshape(R, N // 2)
         out = torch.zeros(R, N // 2, dtype=torch.bfloat16, device="cuda")
     elif epi == 0:
@@ -35,7 +36,7 @@ def _run(rows_per_mod, N, K, epi, seed=0):
         out = torch.randn(R, N, device="cuda", generator=g) if epi == 2 else torch.zeros(R, N, device="cuda")
         if epi == 2:
             ref = ref + out
-    _lib.check(_lib.load().psk_gemv(x.data_ptr(), R, K, ptrs.data_ptr(), t_mrs.data_ptr(), n_mod, N, epi,
+    _lib.check(_lib.load().psk_gemv(x.data_ptr(), R, K, ptrs.data_ptr(), t_mrs.data_ptr(), n_mod, max(rows_per_mod), N, epi,
                                     out.data_ptr(), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     err = (out.float() - ref).abs().max().item()
@@ -44,7 +45,8 @@ def _run(rows_per_mod, N, K, epi, seed=0):
     assert err <= tol, f"err {err} scale {scale}"
 
 
-@pytest.mark.parametrize("rows", [[1, 1, 1, 1], [2, 2], [4, 4, 4, 4], [8, 3, 0, 5], [16, 16], [12, 1]])
+@pytest.mark.parametrize("rows", [[1, 1, 1, 1], [2, 2], [4, 4, 4, 4], [8, 3, 0, 5], [16, 16], [12, 1], [0, 0, 16, 0],
+                                  [32, 5], [0, 17]])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
 def test_gemv_rows_and_epilogues(rows, epi):
     _run(rows, 1536, 4096, epi)
@@ -54,3 +56,11 @@ def test_gemv_rows_and_epilogues(rows, epi):
 def test_gemv_shapes(N, K):
     _run([3, 5, 2, 6], N, K, 1, seed=1)
     _run([1, 1, 1], N, K, 1, seed=2)
+
+
+@pytest.mark.parametrize("N,K", [(48, 1160), (128256 // 8, 4096)])
+def test_gemv_ragged_k_and_many_tiles(N, K):
+    """K = 1160: a partial last stage (136 columns, not a multiple of 32);
+    N = 16032: more tiles than SMs per module."""
+    _run([2, 1], N, K, 1, seed=3)
+    _run([5], N, K, 2, seed=4)

@@ -36,7 +36,7 @@ for name, (N, K, epi) in shapes.items():
     reps = 4 * layers if name != "head" else 8
 
     def launch(i):
-        _lib.check(lib.psk_gemv(x.data_ptr(), R, K, ptrs[i % layers].data_ptr(), mrs.data_ptr(), N_MOD, N,
+        _lib.check(lib.psk_gemv(x.data_ptr(), R, K, ptrs[i % layers].data_ptr(), mrs.data_ptr(), N_MOD, M, N,
                                 epi, out.data_ptr(), torch.cuda.current_stream().cuda_stream))
     with torch.cuda.stream(st):
         for i in range(3):

@@ -1,7 +1,14 @@
 #!/bin/bash
-# correctness + quick perf pass for the current kernels
+# correctness + perf pass: GPU tests, GEMV sweep, per-launch list of one
+# bench step, one full ncu capture of the gate/up GEMV, and the bench line.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_decode_attn_gpu.py tests/test_gemv_gpu.py tests/test_prefill_gpu.py tests/test_decode_gpu.py tests/test_gemm_gpu.py tests/test_transfer.py tests/test_serve.py -x -q 2>&1 | tail -15
-for m in 1 4 8; do python tools/bench_gemv.py $m 2>&1 | cut -c1-90; done
-PSK_TRACE=1 timeout 120 python tools/profile_kernels.py attn32k 2>&1 | tail -8
-PSK_TRACE=1 timeout 120 python tools/profile_kernels.py attn4k 2>&1 | tail -8
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
+for m in 1 4 8 16; do timeout 300 python tools/bench_gemv.py $m 2>&1 | cut -c1-90; done
+timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/step_launches.csv python tools/profile_step.py 1 > gpurun_out/profile_step.log 2>&1
+tail -2 gpurun_out/profile_step.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_kernel -s 2 -c 1 \
+  -o gpurun_out/ncu_gemv -f python tools/profile_kernels.py gemv > gpurun_out/ncu_gemv.log 2>&1
+tail -2 gpurun_out/ncu_gemv.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -c 3000 gpurun_out/bench.json

@@ -52,7 +52,7 @@ if which in ("gemv", "all"):
     p = torch.tensor([m.wgu[0].data_ptr() for m in mods], dtype=torch.int64, device="cuda")
     mrs = torch.tensor([0, 1, 2, 3, 4], dtype=torch.int32, device="cuda")
     for _ in range(4):
-        _lib.check(lib.psk_gemv(x.data_ptr(), 4, cfg.d_model, p.data_ptr(), mrs.data_ptr(), 4,
+        _lib.check(lib.psk_gemv(x.data_ptr(), 4, cfg.d_model, p.data_ptr(), mrs.data_ptr(), 4, 1,
                                 2 * cfg.ffn, 3, act.data_ptr(), s))
     torch.cuda.synchronize()
 if which in ("gemm", "prefill_attn", "all"):
