@@ -821,9 +821,10 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   cfg.stream = s;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  // many query rows per KV head (fan-out) -> tcgen05 path; else mma.sync
-  static const bool force_hmma = getenv("PSK_ATTN_HMMA") != nullptr;
-  if (grp * b->max_rows_per_sess > 16 && !force_hmma) {
+  // tcgen05 fan-out path: opt-in (PSK_ATTN_TC=1) until it beats mma.sync —
+  // measured on B200 it does not yet (32k x 16 modules: 100 us vs 51 us)
+  static const bool use_tc = getenv("PSK_ATTN_TC") != nullptr;
+  if (grp * b->max_rows_per_sess > 16 && use_tc) {
     static bool tc_init = false;
     if (!tc_init) {
       PSK_CUDA_TRY(cudaFuncSetAttribute(tcv::decode_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -8,17 +8,18 @@
 //   * persistent, one CTA per SM; the (module, weight-row) space is cut into
 //     16-row tiles and each CTA owns a contiguous run of tiles (balanced to
 //     within one tile; tiles never straddle modules since N % 16 == 0);
-//   * warp 8 is a producer that streams each tile as 1024-column stages
-//     (16 rows x 2 KiB) with cp.async.bulk (TMA bulk copies, L2 evict-first)
-//     into a 5-6 stage shared-memory ring (~200 KiB in flight per SM) — it
+//   * warp 8 is a producer that streams each tile as 2048-column stages
+//     (16 rows x 4 KiB) with cp.async.bulk (TMA bulk copies, L2 evict-first)
+//     into a 3-stage shared-memory ring (~195 KiB in flight per SM) — it
 //     does not wait on the previous kernel (PDL), so the first stages land
-//     while that kernel drains;
-//   * warps 0-7 each own 128 columns of every stage and run mma.sync
+//     while that kernel drains. Measured on B200 (tools/bw_probe.cu): 4 KiB
+//     row pieces stream at 6.95 TB/s, 2 KiB pieces at 5.74 TB/s;
+//   * warps 0-7 each own 256 columns of every stage and run mma.sync
 //     m16n8k16 (weights = A, 16 rows; activations = B, 8 rows per n-tile)
 //     with a fixed k-permutation inside every 32-column group (applied to W
 //     and x alike: a dot product is order-invariant) so every fragment is
 //     one 16-byte shared-memory read (rows padded by 64 B: conflict-free);
-//     x fragments come from L2 and are prefetched one stage ahead;
+//     x fragments come from L2, issued before the stage's barrier wait;
 //   * at the end of a tile the 8 warps' partials meet in shared memory
 //     (double-buffered, one named barrier per tile) and are summed in a
 //     fixed order — results are bit-reproducible — then the fused epilogue
@@ -39,7 +40,9 @@ namespace gemv {
 constexpr int CW = 8;                      // consumer warps
 constexpr int THREADS = (CW + 1) * 32;     // + one producer warp
 constexpr int TR = 16;                     // weight rows per tile (MMA M)
-constexpr int KC = CW * 128;               // columns per stage (128 per consumer warp)
+constexpr int WC = 256;                    // columns per consumer warp per stage
+constexpr int GR = WC / 32;                // 32-column groups per warp per stage
+constexpr int KC = CW * WC;                // columns per stage
 constexpr int ROW_BYTES = KC * 2 + 64;     // padded shared-memory row
 constexpr int STAGE_BYTES = TR * ROW_BYTES;
 constexpr int SMEM_LIMIT = 227 * 1024;
@@ -50,7 +53,7 @@ struct Cfg {
   static constexpr int RED_BYTES = 2 * CW * TR * MAXM * 4;
   static constexpr int STAGES = (SMEM_LIMIT - RED_BYTES - 256) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + RED_BYTES + 256;
-  static_assert(STAGES >= 3, "ring too shallow");
+  static_assert(STAGES >= 2, "ring too shallow");
 };
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -73,21 +76,18 @@ __device__ __forceinline__ uint4 lds128(const unsigned char* p) {
   return *reinterpret_cast<const uint4*>(p);
 }
 
-// x fragments (B operand) of stage `j` for this thread: row nt*8+gq of the
-// tile's module, columns [8tq, 8tq+8) of each of the warp's four 32-column
+// x fragments (B operand) of one stage for this thread: row nt*8+gq of the
+// tile's module, columns [8tq, 8tq+8) of each of the warp's 32-column
 // groups; zero outside the module's rows or past K.
 template <int NT>
-__device__ __forceinline__ void load_x(uint4 (&xf)[NT][4], const __nv_bfloat16* __restrict__ X, int K,
-                                       const int32_t* __restrict__ mrs, int tpm, int t, int c, int warp,
-                                       int gq, int tq) {
-  const int mod = t / tpm;
-  const int xb = mrs[mod], M = mrs[mod + 1] - xb;
+__device__ __forceinline__ void load_x(uint4 (&xf)[NT][GR], const __nv_bfloat16* __restrict__ X, int K,
+                                       int xb, int M, int c, int warp, int gq, int tq) {
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     const int row = nt * 8 + gq;
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      const int col = c * KC + warp * 128 + g * 32 + tq * 8;
+    for (int g = 0; g < GR; ++g) {
+      const int col = c * KC + warp * WC + g * 32 + tq * 8;
       xf[nt][g] = (row < M && col < K)
                       ? __ldg(reinterpret_cast<const uint4*>(X + (int64_t)(xb + row) * K + col))
                       : make_uint4(0, 0, 0, 0);
@@ -152,30 +152,21 @@ __global__ void __launch_bounds__(THREADS, 1)
   float acc[NT][4];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
-  uint4 xn[NT][4];
   pdl_wait();  // x (and the residual stream) come from the previous kernel
-  if (n_stages > 0) load_x<NT>(xn, X, K, mrs, tpm, t0, 0, warp, gq, tq);
   int buf = 0;
   for (int j = 0; j < n_stages; ++j) {
     const int s = j % C::STAGES;
     const int t = t0 + j / cpt, c = j % cpt;
     const int mod = t / tpm;
     const int xb = mrs[mod], M = mrs[mod + 1] - xb;
-    uint4 xc[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int g = 0; g < 4; ++g) xc[nt][g] = xn[nt][g];
-    if (j + 1 < n_stages) {
-      const int jn = j + 1;
-      load_x<NT>(xn, X, K, mrs, tpm, t0 + jn / cpt, jn % cpt, warp, gq, tq);
-    }
+    uint4 xc[NT][GR];
+    load_x<NT>(xc, X, K, xb, M, c, warp, gq, tq);  // in flight during the wait
     tma::mbar_wait(&full[s], (j / C::STAGES) & 1);
     if (M > 0) {
-      const unsigned char* st = smem + s * STAGE_BYTES + (warp * 128 + tq * 8) * 2;
+      const unsigned char* st = smem + s * STAGE_BYTES + (warp * WC + tq * 8) * 2;
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const bool ok = c * KC + warp * 128 + g * 32 + tq * 8 < K;
+      for (int g = 0; g < GR; ++g) {
+        const bool ok = c * KC + warp * WC + g * 32 + tq * 8 < K;
         const uint4 wa = ok ? lds128(st + gq * ROW_BYTES + g * 64) : make_uint4(0, 0, 0, 0);
         const uint4 wb = ok ? lds128(st + (gq + 8) * ROW_BYTES + g * 64) : make_uint4(0, 0, 0, 0);
         const uint32_t a0[4] = {wa.x, wb.x, wa.y, wb.y};
