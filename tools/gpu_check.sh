@@ -1,14 +1,16 @@
 #!/bin/bash
-# correctness + perf pass: GPU tests, GEMV sweep, per-launch list of one
-# bench step, one full ncu capture of the gate/up GEMV, and the bench line.
+# correctness + perf pass: GPU tests, per-launch list of one bench step,
+# full ncu captures of the gate/up GEMV (1 and 8 rows/module), bench line.
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
-for m in 1 4 8 16; do timeout 300 python tools/bench_gemv.py $m 2>&1 | cut -c1-90; done
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+S=${S:-8}
 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/step_launches.csv python tools/profile_step.py 1 > gpurun_out/profile_step.log 2>&1
-tail -2 gpurun_out/profile_step.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_kernel -s 2 -c 1 \
-  -o gpurun_out/ncu_gemv -f python tools/profile_kernels.py gemv > gpurun_out/ncu_gemv.log 2>&1
-tail -2 gpurun_out/ncu_gemv.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-tail -c 3000 gpurun_out/bench.json
+  --log-file gpurun_out/step_launches_s$S.csv python tools/profile_step.py $S > gpurun_out/profile_step.log 2>&1
+tail -1 gpurun_out/profile_step.log
+for m in 1 8; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_kernel -s 2 -c 1 \
+    -o gpurun_out/ncu_gemv_m$m -f python tools/profile_kernels.py gemv $m > gpurun_out/ncu_gemv_m$m.log 2>&1
+  tail -1 gpurun_out/ncu_gemv_m$m.log
+done
+timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -c 4000 gpurun_out/bench.json; tail -3 gpurun_out/bench.err

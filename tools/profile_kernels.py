@@ -1,6 +1,6 @@
 """Drive each hot kernel a few times at the bench shapes, for ncu.
 
-    ncu --set full -k regex:<kernel> -c 2 python tools/profile_kernels.py <which>
+    ncu --set full -k regex:<kernel> -c 2 python tools/profile_kernels.py <which> [rows/module]
 which: gemv | attn4k | attn32k | gemm | prefill_attn | all
 """
 import sys
@@ -46,13 +46,14 @@ if which in ("attn4k", "all"):
 if which in ("attn32k", "all"):
     attn(32767, 16)
 if which in ("gemv", "all"):
+    M = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # rows per module
     mods = [ModuleWeights(cfg, 10 + i) for i in range(4)]
-    x = torch.randn(4, cfg.d_model, device="cuda").to(torch.bfloat16)
-    act = torch.empty(4, cfg.ffn, dtype=torch.bfloat16, device="cuda")
+    x = torch.randn(4 * M, cfg.d_model, device="cuda").to(torch.bfloat16)
+    act = torch.empty(4 * M, cfg.ffn, dtype=torch.bfloat16, device="cuda")
     p = torch.tensor([m.wgu[0].data_ptr() for m in mods], dtype=torch.int64, device="cuda")
-    mrs = torch.tensor([0, 1, 2, 3, 4], dtype=torch.int32, device="cuda")
+    mrs = torch.tensor([i * M for i in range(5)], dtype=torch.int32, device="cuda")
     for _ in range(4):
-        _lib.check(lib.psk_gemv(x.data_ptr(), 4, cfg.d_model, p.data_ptr(), mrs.data_ptr(), 4, 1,
+        _lib.check(lib.psk_gemv(x.data_ptr(), 4 * M, cfg.d_model, p.data_ptr(), mrs.data_ptr(), 4, M,
                                 2 * cfg.ffn, 3, act.data_ptr(), s))
     torch.cuda.synchronize()
 if which in ("gemm", "prefill_attn", "all"):
