@@ -7,8 +7,9 @@
 //
 // Partial kernel: one CTA = (session, KV head, split). Its page stream is the
 // split's slice of [shared prompt pages | row 0 private pages | row 1 private
-// pages | ...]. A producer warp streams every page with TMA (two 128B-swizzled
-// [16 x 64] boxes per 4 KiB K / V tile) through a 16-stage (128 KiB) mbarrier ring; 8
+// pages | ...]. A producer warp streams every page with TMA (one 4-D
+// 128B-swizzled box = the page's 8 KiB of K and V for this head and layer)
+// through a 16-stage (128 KiB) mbarrier ring; 8
 // consumer warps map to (query m-tile, page subset), so each page is read
 // from HBM once per step for ALL query rows of the session (GQA group x
 // co-batched decode modules, <= 64 rows); private pages mask the rows they do
@@ -35,12 +36,15 @@ namespace dattn {
 constexpr int HD = 128, PT = 16;
 constexpr int CW = 8;                   // consumer warps
 constexpr int THREADS = (CW + 1) * 32;  // + 1 TMA producer warp
-constexpr int NST = 16;                 // pipeline stages (1 page = K + V each): 128 KiB in flight
+#ifndef PSK_ATTN_NST
+#define PSK_ATTN_NST 16
+#endif
+constexpr int NST = PSK_ATTN_NST;       // pipeline stages (1 page = K + V each, 8 KiB)
 constexpr int TILE = PT * HD * 2;       // 4 KiB
 constexpr int STAGE = 2 * TILE;
 constexpr int GMAX = 64;
 constexpr int MAXR = 16;                // decode rows per session
-constexpr int OFF_Q = NST * STAGE;      // 128 KiB
+constexpr int OFF_Q = NST * STAGE;
 constexpr int OFF_BAR = OFF_Q + GMAX * 256;  // +16 KiB
 constexpr int MAXP = 1024;              // page indices staged in smem
 constexpr int OFF_PG = OFF_BAR + 2 * NST * 8;
@@ -158,13 +162,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma::mbar_wait(&empty[st], ((j / NST) & 1) ^ 1);
         const int page = j < MAXP ? s_page[j] : page_of(k0 + j);
         const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
-        const int row_v = row_k + nkv * PT;
-        unsigned char* dst = smem + st * STAGE;
         tma::mbar_expect_tx(&full[st], STAGE);
-        tma::load_2d(&kvmap, &full[st], dst, 0, row_k);
-        tma::load_2d(&kvmap, &full[st], dst + 2048, 64, row_k);
-        tma::load_2d(&kvmap, &full[st], dst + TILE, 0, row_v);
-        tma::load_2d(&kvmap, &full[st], dst + TILE + 2048, 64, row_v);
+        tma::load_4d(&kvmap, &full[st], smem + st * STAGE, 0, row_k, 0, 0);  // K and V, 8 KiB
       }
     }
   }
@@ -722,14 +721,16 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 
 // 2D TMA map over a KV page pool: rows of 128 dims (256 B), [16 x 64] boxes,
 // 128B swizzle. Cached per pool geometry. Shared by the attention kernels.
-int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out) {
+int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out, bool page_box) {
   using namespace dattn;
-  // small cache keyed by the pool geometry
-  static CUtensorMap cached[4];
-  static psk_kv_layout keys[4] = {};
+  // small cache keyed by the pool geometry and the box kind
+  static CUtensorMap cached[8];
+  static psk_kv_layout keys[8] = {};
+  static bool kinds[8] = {};
   static int next = 0;
-  for (int i = 0; i < 4; ++i)
-    if (keys[i].base == kv.base && keys[i].n_pages == kv.n_pages && keys[i].page_elems == kv.page_elems) {
+  for (int i = 0; i < 8; ++i)
+    if (keys[i].base == kv.base && keys[i].n_pages == kv.n_pages && keys[i].page_elems == kv.page_elems &&
+        kinds[i] == page_box) {
       *out = cached[i];
       return PSK_OK;
     }
@@ -745,21 +746,35 @@ int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out) {
     enc = reinterpret_cast<EncodeTiledFn>(fp);
   }
   const cuuint64_t rows = (cuuint64_t)kv.n_pages * (cuuint64_t)kv.page_elems / HD;
-  cuuint64_t dims[2] = {(cuuint64_t)HD, rows};
-  cuuint64_t strides[1] = {(cuuint64_t)HD * 2};
-  cuuint32_t box[2] = {64, (cuuint32_t)PT};
-  cuuint32_t es[2] = {1, 1};
   const int i = next;
-  next = (next + 1) % 4;
-  CUresult r = enc(&cached[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kv.base, dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  next = (next + 1) % 8;
+  CUresult r;
+  if (!page_box) {
+    cuuint64_t dims[2] = {(cuuint64_t)HD, rows};
+    cuuint64_t strides[1] = {(cuuint64_t)HD * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)PT};
+    cuuint32_t es[2] = {1, 1};
+    r = enc(&cached[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kv.base, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    // (dim, token row, half, K|V): the V tile of a (page, layer, head) sits
+    // n_kv_heads tiles after its K tile
+    cuuint64_t dims[4] = {64, rows, 2, 2};
+    cuuint64_t strides[3] = {(cuuint64_t)HD * 2, 128, (cuuint64_t)kv.n_kv_heads * PT * HD * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)PT, 2, 2};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    r = enc(&cached[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, kv.base, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (r != CUDA_SUCCESS) {
     keys[i] = psk_kv_layout{};
     set_error("KV tensor map encode failed (%d)", (int)r);
     return PSK_ECUDA;
   }
   keys[i] = kv;
+  kinds[i] = page_box;
   *out = cached[i];
   return PSK_OK;
 }
@@ -787,8 +802,12 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   PSK_CHECK_ARG(b->max_rows_per_sess <= MAXR && grp * b->max_rows_per_sess <= GMAX,
                 "psk_decode_attn: %d query rows per KV head exceed %d", grp * b->max_rows_per_sess, GMAX);
   if (b->n_rows == 0) return PSK_OK;
+  // tcgen05 fan-out path: opt-in (PSK_ATTN_TC=1) until it beats mma.sync —
+  // measured on B200 it does not yet (32k x 16 modules: 100 us vs 51 us)
+  static const bool use_tc_env = getenv("PSK_ATTN_TC") != nullptr;
+  const bool use_tc = grp * b->max_rows_per_sess > 16 && use_tc_env;
   CUtensorMap map;
-  int rc = psk::kv_tensor_map(kv, &map);
+  int rc = psk::kv_tensor_map(kv, &map, /*page_box=*/!use_tc);
   if (rc) return rc;
   Params p;
   p.b = *b;
@@ -821,10 +840,7 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   cfg.stream = s;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  // tcgen05 fan-out path: opt-in (PSK_ATTN_TC=1) until it beats mma.sync —
-  // measured on B200 it does not yet (32k x 16 modules: 100 us vs 51 us)
-  static const bool use_tc = getenv("PSK_ATTN_TC") != nullptr;
-  if (grp * b->max_rows_per_sess > 16 && use_tc) {
+  if (use_tc) {
     static bool tc_init = false;
     if (!tc_init) {
       PSK_CUDA_TRY(cudaFuncSetAttribute(tcv::decode_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,

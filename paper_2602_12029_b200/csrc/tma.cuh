@@ -49,6 +49,16 @@ __device__ __forceinline__ void load_2d(const CUtensorMap* map, uint64_t* bar, v
       : "memory");
 }
 
+// 4D tiled TMA load (box given by the tensor map) completing on `bar`.
+__device__ __forceinline__ void load_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                                        int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2];" ::"r"(sa(dst)),
+      "l"(map), "r"(sa(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -84,6 +94,10 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t addr) {
 
 #include "../../include/psk.h"
 namespace psk {
-// 2D TMA map over a paged KV pool (decode_attn.cu): [16 token x 64 dim] SW128 boxes.
-int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out);
+// TMA maps over a paged KV pool (decode_attn.cu), 128B-swizzled:
+//  page_box = false: 2D, [16 token x 64 dim] boxes (one half of a K or V tile);
+//  page_box = true : 4D (64 dim, 16 token, 2 halves, K|V), one box = the whole
+//                    8 KiB K+V of one (page, layer, head), landing as
+//                    [K half0 | K half1 | V half0 | V half1] x [16][128 B].
+int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out, bool page_box = false);
 }  // namespace psk

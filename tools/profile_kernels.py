@@ -1,7 +1,7 @@
 """Drive each hot kernel a few times at the bench shapes, for ncu.
 
     ncu --set full -k regex:<kernel> -c 2 python tools/profile_kernels.py <which> [rows/module]
-which: gemv | attn4k | attn32k | gemm | prefill_attn | all
+which: gemv | attn4k | attn4k_s8 | attn32k | gemm | prefill_attn | all
 """
 import sys
 from pathlib import Path
@@ -22,16 +22,21 @@ s = torch.cuda.current_stream().cuda_stream
 cfg = LlamaConfig.llama8b(n_layers=2, max_pos=32768 + 512)
 
 
-def attn(shared, modules, reps=4):
+def attn(shared, modules, reps=4, sessions=1):
     n_sh = (shared + 15) // 16
-    kv = KVCache(cfg, n_sh + modules)
+    kv = KVCache(cfg, sessions * (n_sh + modules))
     _lib.check(lib.psk_init_normal_bf16(kv.data.data_ptr(), kv.data.numel(), 7, 1.0, s))
-    rows = [DecodeRow(module=m, session=0, first_token=0, pages=[n_sh + m]) for m in range(modules)]
-    b = DecodeBatch([SessionSpec(shared_len=shared, pages=list(range(n_sh)))], rows, modules)
-    q = torch.randn(modules, 32, 128, device="cuda").to(torch.bfloat16)
+    rows, sess = [], []
+    for si in range(sessions):
+        base = si * (n_sh + modules)
+        sess.append(SessionSpec(shared_len=shared, pages=list(range(base, base + n_sh))))
+        rows += [DecodeRow(module=m, session=si, first_token=0, pages=[base + n_sh + m])
+                 for m in range(modules)]
+    b = DecodeBatch(sess, rows, modules)
+    q = torch.randn(sessions * modules, 32, 128, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)
     from paper_2602_12029_b200.model import attn_splits
-    ns = attn_splits(n_sh + modules, 8)
+    ns = attn_splits(n_sh + modules, 8 * sessions, torch.cuda.get_device_properties(0).multi_processor_count)
     wsb = C.c_int64()
     _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), 8, ns, C.byref(wsb)))
     ws = torch.zeros(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
@@ -43,6 +48,8 @@ def attn(shared, modules, reps=4):
 
 if which in ("attn4k", "all"):
     attn(4095, 4)
+if which in ("attn4k_s8", "all"):
+    attn(4095, 4, sessions=8)
 if which in ("attn32k", "all"):
     attn(32767, 16)
 if which in ("gemv", "all"):
