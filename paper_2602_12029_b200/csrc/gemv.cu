@@ -19,10 +19,14 @@
 //     with a fixed k-permutation inside every 32-column group (applied to W
 //     and x alike: a dot product is order-invariant) so every fragment is
 //     one 16-byte shared-memory read (rows padded by 64 B: conflict-free);
-//     x fragments come from L2, issued before the stage's barrier wait;
-//   * at the end of a tile the 8 warps' partials meet in shared memory
-//     (double-buffered, one named barrier per tile) and are summed in a
-//     fixed order — results are bit-reproducible — then the fused epilogue
+//     x fragments come from L2 (ncu: re-reading them per tile cost 1.3 GB
+//     of L2 traffic per gate/up launch at 8 rows/module; per group: 1/TG);
+//   * tiles are walked in groups of up to TG (7 / 3 / 1 for <= 8 / 16 / 32
+//     rows per module) with the K chunks outer: x fragments are loaded once
+//     per (group, chunk) and reused for every tile of the group, the group's
+//     accumulators stay in registers, and at the end of a group the 8 warps'
+//     partials meet in shared memory and are summed in a fixed order —
+//     results are bit-reproducible — then the fused epilogue
 //     stores bf16 / fp32, adds into the fp32 residual stream, or applies
 //     SiLU(gate)*up: gate/up rows are interleaved in 8-row groups, so each
 //     16-row tile holds 8 gate + 8 matching up rows.
@@ -50,10 +54,13 @@ constexpr int SMEM_LIMIT = 227 * 1024;
 template <int NT>
 struct Cfg {
   static constexpr int MAXM = NT * 8;  // activation rows per module
-  static constexpr int RED_BYTES = 2 * CW * TR * MAXM * 4;
-  static constexpr int STAGES = (SMEM_LIMIT - RED_BYTES - 256) / STAGE_BYTES;
+  static constexpr int STAGES = 3;
+  // tiles per group: their accumulators stay in registers across the K
+  // chunks and meet once in `red` [CW][TG*TR][MAXM] for the cross-warp sum
+  static constexpr int TG = (SMEM_LIMIT - STAGES * STAGE_BYTES - 256) / (CW * TR * MAXM * 4);
+  static constexpr int RED_BYTES = CW * TG * TR * MAXM * 4;
   static constexpr int SMEM = STAGES * STAGE_BYTES + RED_BYTES + 256;
-  static_assert(STAGES >= 2, "ring too shallow");
+  static_assert(TG >= 1 && SMEM <= SMEM_LIMIT, "shared memory budget");
 };
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -95,14 +102,22 @@ __device__ __forceinline__ void load_x(uint4 (&xf)[NT][GR], const __nv_bfloat16*
   }
 }
 
+// Walk order of one CTA: its tiles are cut into groups of <= TG consecutive
+// tiles of one module; per group the K chunks are the outer loop, so each
+// warp loads its x fragments of a chunk once and reuses them for every tile
+// of the group (x is re-read from L2 once per group, not once per tile).
+__device__ __forceinline__ int group_end(int gt0, int t1, int tg, int tpm) {
+  return min(min(gt0 + tg, t1), (gt0 / tpm + 1) * tpm);
+}
+
 template <int NT, int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     gemv_kernel(const __nv_bfloat16* __restrict__ X, int K, const __nv_bfloat16* const* __restrict__ W,
                 const int32_t* __restrict__ mrs, int n_mod, int N, void* __restrict__ out) {
   using C = Cfg<NT>;
-  constexpr int MAXM = C::MAXM;
+  constexpr int MAXM = C::MAXM, TG = C::TG;
   extern __shared__ __align__(128) unsigned char smem[];
-  float* red = reinterpret_cast<float*>(smem + C::STAGES * STAGE_BYTES);  // [2][CW][TR][MAXM]
+  float* red = reinterpret_cast<float*>(smem + C::STAGES * STAGE_BYTES);  // [CW][TG*TR][MAXM]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * STAGE_BYTES + C::RED_BYTES);
   uint64_t* empty = full + C::STAGES;
 
@@ -110,8 +125,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int tiles = n_mod * tpm;
   const int t0 = (int)((int64_t)blockIdx.x * tiles / gridDim.x);
   const int t1 = (int)((int64_t)(blockIdx.x + 1) * tiles / gridDim.x);
-  const int cpt = (K + KC - 1) / KC;  // stages per tile
-  const int n_stages = (t1 - t0) * cpt;
+  const int cpt = (K + KC - 1) / KC;  // K chunks (stages) per tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -127,106 +141,129 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == CW) {
     // ---- producer: weights do not depend on the previous kernel ----
     const uint64_t pol = policy_evict_first();
-    for (int j = 0; j < n_stages; ++j) {
-      const int s = j % C::STAGES;
-      tma::mbar_wait(&empty[s], ((j / C::STAGES) & 1) ^ 1);
-      const int t = t0 + j / cpt, c = j % cpt;
-      const int mod = t / tpm;
-      if (mrs[mod + 1] == mrs[mod]) {  // module without rows this step
-        if (lane == 0) tma::mbar_arrive(&full[s]);
-        continue;
+    int j = 0;
+    for (int gt0 = t0; gt0 < t1;) {
+      const int gt1 = group_end(gt0, t1, TG, tpm);
+      const int mod = gt0 / tpm;
+      const bool live = mrs[mod + 1] > mrs[mod];  // module without rows this step: no loads
+      for (int c = 0; c < cpt; ++c) {
+        const int cols = min(KC, K - c * KC);
+        for (int t = gt0; t < gt1; ++t, ++j) {
+          const int s = j % C::STAGES;
+          tma::mbar_wait(&empty[s], ((j / C::STAGES) & 1) ^ 1);
+          if (!live) {
+            if (lane == 0) tma::mbar_arrive(&full[s]);
+            continue;
+          }
+          if (lane == 0) tma::mbar_expect_tx(&full[s], TR * cols * 2);
+          __syncwarp();
+          if (lane < TR) {
+            const __nv_bfloat16* src = W[mod] + ((int64_t)(t % tpm) * TR + lane) * K + (int64_t)c * KC;
+            bulk_g2s(tma::sa(smem + s * STAGE_BYTES + lane * ROW_BYTES), src, cols * 2, &full[s], pol);
+          }
+        }
       }
-      const int cols = min(KC, K - c * KC);
-      if (lane == 0) tma::mbar_expect_tx(&full[s], TR * cols * 2);
-      __syncwarp();
-      if (lane < TR) {
-        const __nv_bfloat16* src = W[mod] + ((int64_t)(t % tpm) * TR + lane) * K + (int64_t)c * KC;
-        bulk_g2s(tma::sa(smem + s * STAGE_BYTES + lane * ROW_BYTES), src, cols * 2, &full[s], pol);
-      }
+      gt0 = gt1;
     }
     return;
   }
 
   // ---- consumers ----
   const int gq = lane >> 2, tq = lane & 3;
-  float acc[NT][4];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
   pdl_wait();  // x (and the residual stream) come from the previous kernel
-  int buf = 0;
-  for (int j = 0; j < n_stages; ++j) {
-    const int s = j % C::STAGES;
-    const int t = t0 + j / cpt, c = j % cpt;
-    const int mod = t / tpm;
+  int j = 0;
+  for (int gt0 = t0; gt0 < t1;) {
+    const int gt1 = group_end(gt0, t1, TG, tpm);
+    const int ng = gt1 - gt0;
+    const int mod = gt0 / tpm;
     const int xb = mrs[mod], M = mrs[mod + 1] - xb;
-    uint4 xc[NT][GR];
-    load_x<NT>(xc, X, K, xb, M, c, warp, gq, tq);  // in flight during the wait
-    tma::mbar_wait(&full[s], (j / C::STAGES) & 1);
-    if (M > 0) {
-      const unsigned char* st = smem + s * STAGE_BYTES + (warp * WC + tq * 8) * 2;
+    float acc[TG][NT][4];
 #pragma unroll
-      for (int g = 0; g < GR; ++g) {
-        const bool ok = c * KC + warp * WC + g * 32 + tq * 8 < K;
-        const uint4 wa = ok ? lds128(st + gq * ROW_BYTES + g * 64) : make_uint4(0, 0, 0, 0);
-        const uint4 wb = ok ? lds128(st + (gq + 8) * ROW_BYTES + g * 64) : make_uint4(0, 0, 0, 0);
-        const uint32_t a0[4] = {wa.x, wb.x, wa.y, wb.y};
-        const uint32_t a1[4] = {wa.z, wb.z, wa.w, wb.w};
+    for (int i = 0; i < TG; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[i][nt][0] = acc[i][nt][1] = acc[i][nt][2] = acc[i][nt][3] = 0.f;
+    for (int c = 0; c < cpt; ++c) {
+      uint4 xc[NT][GR];
+      load_x<NT>(xc, X, K, xb, M, c, warp, gq, tq);  // once per (group, chunk)
+#pragma unroll
+      for (int i = 0; i < TG; ++i) {
+        if (i >= ng) break;
+        const int s = j % C::STAGES;
+        tma::mbar_wait(&full[s], (j / C::STAGES) & 1);
+        if (M > 0) {
+          const unsigned char* st = smem + s * STAGE_BYTES + (warp * WC + tq * 8) * 2;
+#pragma unroll
+          for (int g = 0; g < GR; ++g) {
+            const bool ok = c * KC + warp * WC + g * 32 + tq * 8 < K;
+            const uint4 wa = ok ? lds128(st + gq * ROW_BYTES + g * 64) : make_uint4(0, 0, 0, 0);
+            const uint4 wb = ok ? lds128(st + (gq + 8) * ROW_BYTES + g * 64) : make_uint4(0, 0, 0, 0);
+            const uint32_t a0[4] = {wa.x, wb.x, wa.y, wb.y};
+            const uint32_t a1[4] = {wa.z, wb.z, wa.w, wb.w};
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              if (nt * 8 >= M) break;
+              mma_bf16_16816(acc[i][nt], a0, xc[nt][g].x, xc[nt][g].y);
+              mma_bf16_16816(acc[i][nt], a1, xc[nt][g].z, xc[nt][g].w);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) tma::mbar_arrive(&empty[s]);
+        ++j;
+      }
+    }
+
+    // ---- group complete: reduce the 8 warps' partials, fused epilogue ----
+    if (M > 0) {
+      float* mine = red + warp * TG * TR * MAXM;
+#pragma unroll
+      for (int i = 0; i < TG; ++i) {
+        if (i >= ng) break;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          if (nt * 8 >= M) break;
-          mma_bf16_16816(acc[nt], a0, xc[nt][g].x, xc[nt][g].y);
-          mma_bf16_16816(acc[nt], a1, xc[nt][g].z, xc[nt][g].w);
+          const int m = nt * 8 + 2 * tq;
+          float* r0 = mine + (i * TR + gq) * MAXM + m;
+          float* r8 = r0 + 8 * MAXM;
+          r0[0] = acc[i][nt][0];
+          r0[1] = acc[i][nt][1];
+          r8[0] = acc[i][nt][2];
+          r8[1] = acc[i][nt][3];
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) tma::mbar_arrive(&empty[s]);
-    if (c != cpt - 1) continue;
-
-    // ---- tile complete: reduce the 8 warps' partials, fused epilogue ----
-    float* rb = red + (size_t)buf * CW * TR * MAXM;
-    if (M > 0) {
-      float* mine = rb + warp * TR * MAXM;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int m = nt * 8 + 2 * tq;
-        mine[gq * MAXM + m] = acc[nt][0];
-        mine[gq * MAXM + m + 1] = acc[nt][1];
-        mine[(gq + 8) * MAXM + m] = acc[nt][2];
-        mine[(gq + 8) * MAXM + m + 1] = acc[nt][3];
-      }
-    }
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
     asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");
     if (M > 0) {
-      const int n0 = (t % tpm) * TR;
+      const int n0 = (gt0 % tpm) * TR;  // first weight row of the group in its module
       if (EPI == PSK_EPI_SILU_MUL) {
-        for (int i = threadIdx.x; i < 8 * M; i += CW * 32) {
-          const int r = i & 7, m = i >> 3;
+        // tile = [gate 8 | up 8] rows -> 8 outputs
+        for (int e = threadIdx.x; e < ng * 8 * M; e += CW * 32) {
+          const int m = e / (ng * 8), q = e % (ng * 8);
+          const int i = q >> 3, r = q & 7;
           float gv = 0.f, uv = 0.f;
 #pragma unroll
           for (int w = 0; w < CW; ++w) {
-            gv += rb[(w * TR + r) * MAXM + m];
-            uv += rb[(w * TR + r + 8) * MAXM + m];
+            const float* rw = red + ((w * TG + i) * TR + r) * MAXM + m;
+            gv += rw[0];
+            uv += rw[8 * MAXM];
           }
           const float sg = gv / (1.f + __expf(-gv));
-          reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)(xb + m) * (N / 2) + n0 / 2 + r] = f2bf(sg * uv);
+          reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)(xb + m) * (N / 2) + n0 / 2 + q] = f2bf(sg * uv);
         }
       } else {
-        for (int i = threadIdx.x; i < TR * M; i += CW * 32) {
-          const int r = i & (TR - 1), m = i / TR;
+        for (int e = threadIdx.x; e < ng * TR * M; e += CW * 32) {
+          const int m = e / (ng * TR), q = e % (ng * TR);  // q = row within the group
           float v = 0.f;
 #pragma unroll
-          for (int w = 0; w < CW; ++w) v += rb[(w * TR + r) * MAXM + m];
-          const int64_t o = (int64_t)(xb + m) * N + n0 + r;
+          for (int w = 0; w < CW; ++w) v += red[((w * TG) * TR + q) * MAXM + m];
+          const int64_t o = (int64_t)(xb + m) * N + n0 + q;
           if (EPI == PSK_EPI_STORE_BF16) reinterpret_cast<__nv_bfloat16*>(out)[o] = f2bf(v);
           if (EPI == PSK_EPI_STORE_F32) reinterpret_cast<float*>(out)[o] = v;
           if (EPI == PSK_EPI_RESID_ADD) reinterpret_cast<float*>(out)[o] += v;
         }
       }
     }
-    buf ^= 1;
+    asm volatile("bar.sync 1, %0;" ::"r"(CW * 32) : "memory");  // red is rewritten by the next group
+    gt0 = gt1;
   }
 }
 
