@@ -300,6 +300,63 @@ def decode_attn_fanout(peaks, shared_tokens=32767, modules=16) -> dict:
             "per_model_reread_bytes": modules * shared_tokens * per_tok}
 
 
+def pool_ops(n_tokens: int = PROMPT, reps: int = 50) -> dict:
+    """K7 through the BlockPool drop-in API (host query staging + kernel +
+    result read-back per call, as the engine calls it) vs the CPU oracle pool
+    (oracle/pool.py, the reference kvstore.py algorithm) on identical ops:
+    insert of a fresh 4096-token prompt (256 blocks) and its full-hit lookup."""
+    import numpy as np
+    from oracle.pool import OraclePool
+    from paper_2602_12029_b200.kvstore import SHARED_NS, BlockPool
+    rng = np.random.default_rng(5)
+    prompts = [rng.integers(0, 1 << 40, n_tokens, dtype=np.int64) for _ in range(reps)]
+    cap = reps * (n_tokens // 16) + 16
+    out = {"tokens": n_tokens, "blocks": n_tokens // 16}
+    for name, pool in (("gpu", BlockPool(cap, 16)), ("cpu_oracle", OraclePool(cap, 16))):
+        tup = [tuple(int(x) for x in p) for p in prompts] if name == "cpu_oracle" else prompts
+        t0 = time.perf_counter()
+        for i, p in enumerate(tup):
+            pool.insert(SHARED_NS, p, i)
+        t1 = time.perf_counter()
+        for i, p in enumerate(tup):
+            if name == "gpu":
+                m, chain = pool.longest_prefix_match(SHARED_NS, p, reps + i)
+                pool.release(chain)
+            else:
+                ids = pool.lookup(SHARED_NS, p, reps + i)
+                pool.release(ids)
+                m = len(ids) * 16
+            assert m == n_tokens
+        t2 = time.perf_counter()
+        out[name] = {"insert_us": round((t1 - t0) / reps * 1e6, 1),
+                     "lookup_hit_us": round((t2 - t1) / reps * 1e6, 1)}
+    out["cpu_oracle"].update(cores=1, kind="port")
+    return out
+
+
+def kv_copy_roofline(eng, peaks, n_pages: int = PROMPT // 16 + 1) -> dict:
+    """K8: move one 4k-token context's pages (257 x 2 MiB, all layers) inside
+    the pool, as the same-process handoff does (transfer.copy_pages)."""
+    import torch
+    from paper_2602_12029_b200 import _lib
+    kv = eng.kv
+    P = kv.data.shape[0]
+    src = torch.arange(0, n_pages, dtype=torch.int32, device="cuda")
+    dst = torch.arange(P - n_pages, P, dtype=torch.int32, device="cuda")
+    page_bytes = kv.data[0].numel() * 2
+    lib = _lib.load()
+
+    def launch():
+        _lib.check(lib.psk_kv_copy_pages(kv.data.data_ptr(), kv.data.data_ptr(), src.data_ptr(),
+                                         dst.data_ptr(), n_pages, page_bytes,
+                                         torch.cuda.current_stream().cuda_stream))
+    dt = _time_launches(launch, 8)
+    nbytes = 2 * n_pages * page_bytes  # read + write
+    gbs = nbytes / dt / 1e9
+    return {"bound": "hbm", "pages": n_pages, "bytes_per_launch": nbytes, "us_per_launch": round(dt * 1e6, 2),
+            "achieved": round(gbs, 1), "unit": "GB/s", "frac": round(gbs / peaks["hbm"], 4)}
+
+
 def prefill_roofline(eng, peaks) -> dict:
     import torch
     T = PROMPT
@@ -435,6 +492,7 @@ def main() -> None:
         out["roofline"] = gemv_roofline(eng, peaks)
         out["decode_attn"] = decode_attn_roofline(eng, peaks)
         out["prefill"] = prefill_roofline(eng, peaks)
+        out["kv_copy"] = kv_copy_roofline(eng, peaks)
         step_bytes = eng.runner.weight_bytes_per_step
         out["decode_step"] = {"weight_bytes": step_bytes,
                               "ms_per_token_step": round((t_val / a.steps - out["prefill"]["ms_per_prefill"]
@@ -459,6 +517,7 @@ def main() -> None:
         del eng
         torch.cuda.empty_cache()
         out["decode_attn_fanout_32k_x16"] = decode_attn_fanout(peaks)
+        out["pool"] = pool_ops()
         if world == 1:
             out["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(S).items()
                                    if k != "sample_seconds"}

@@ -431,6 +431,243 @@ __global__ void __launch_bounds__(THREADS_TC, 1)
 
 }  // namespace tc
 
+// ------------------------------------------------------ ping-pong tcgen05 ---
+// One CTA = (kv head, 256 query rows = two 128-row tiles of (position, q
+// head of the GQA group)); both tiles consume every 64-key K/V chunk.
+//   warp 0      TMA producer: K and V of 4 pages per chunk, 3-stage ring
+//   warp 1      MMA issuer (+ TMEM owner): S_t = Q_t K^T (M128 N64), then
+//               O_t += P_t V (M128 N128 K16 per page); issue order
+//               PV0(c) S0(c+1) PV1(c) S1(c+1) so one tile's softmax runs
+//               while the tensor core works on the other tile
+//   warps 2-5   softmax of tile 0, warps 6-9 tile 1 (thread = query row =
+//               TMEM lane): one pass over S (64 fp32 from TMEM), exp2 with
+//               a lazily updated base max (O in TMEM is rescaled only when
+//               the row max grows by > 2^8; the final 1/l makes it exact),
+//               P (bf16) -> shared memory in the UMMA K-major layout
+// TMEM columns: S0 [0,64) S1 [64,128) O0 [128,256) O1 [256,384).
+namespace pp {
+
+constexpr int KC = 64;                   // keys per chunk
+constexpr int CPG = KC / PT;             // pages per chunk
+constexpr int NSTG = 3;
+constexpr int KBYTES = CPG * TILE;       // 16 KiB: [dims 0-63 box x 4 pages][dims 64-127 box x 4 pages]
+constexpr int STG = 2 * KBYTES;          // + V 16 KiB: [page][box0 | box1]
+constexpr int QBYTES = 128 * HD * 2;     // 32 KiB per tile: [2 boxes][128 rows][128 B]
+constexpr int PBYTES = 128 * KC * 2;     // 16 KiB per tile: [128 rows][128 B]
+constexpr int OFF_Q = NSTG * STG;
+constexpr int OFF_P = OFF_Q + 2 * QBYTES;
+constexpr int OFF_BAR = OFF_P + 2 * PBYTES;
+constexpr int MAXPG = 2560;
+constexpr int OFF_PG = OFF_BAR + 256;
+constexpr int SMEM = OFF_PG + MAXPG * 4 + 1024;
+constexpr int THREADS = 320;
+constexpr float RESCALE_LOG2 = 8.f;      // lazy-rescale threshold (log2 units)
+
+__global__ void __launch_bounds__(THREADS, 1)
+    prefill_attn_pp(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ tc::TcParams p) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t *full = bars, *empty = bars + NSTG, *s_full = bars + 2 * NSTG, *p_full = s_full + 2,
+           *pv_done = p_full + 2;
+  int* s_pg = reinterpret_cast<int*>(smem + OFF_PG);
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkv = p.kv.n_kv_heads;
+  const int h = blockIdx.x % nkv;
+  const int qblk = p.n_qblocks - 1 - (int)(blockIdx.x / nkv);  // heavy blocks first
+  const int t0 = qblk * p.qb;                                  // p.qb = 256 / grp positions
+  const int kv_end = p.pos0 + min(t0 + p.qb, p.T);
+  const int n_pages = (kv_end + PT - 1) / PT;
+  const int nch = (kv_end + KC - 1) / KC;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTG; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      tma::mbar_init(&s_full[t], 1);
+      tma::mbar_init(&p_full[t], 128);
+      tma::mbar_init(&pv_done[t], 1);
+    }
+    tma::fence_mbar_init();
+    tma::prefetch_map(&kvmap);
+  }
+  if (warp == 1) umma::tmem_alloc(&s_tmem, 512);
+  for (int j = threadIdx.x; j < n_pages && j < MAXPG; j += THREADS) s_pg[j] = p.pages[j];
+  const uint32_t sq = smem_u32(smem + OFF_Q), sp = smem_u32(smem + OFF_P);
+  // Q rows -> shared memory (K-major, 128B swizzle), row r = (position, head)
+  for (int e = threadIdx.x; e < 256 * 16; e += THREADS) {
+    const int r = e >> 4, c = e & 15;
+    const int t = t0 + r / p.grp;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (t < p.T) {
+      const int qh = h * p.grp + r % p.grp;
+      v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)t * p.nq + qh) * HD + c * 8);
+    }
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sq + (r >> 7) * QBYTES +
+                                                               umma::kmajor_off(r & 127, c, 16384)),
+                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+  }
+  umma::fence_proxy_async();
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = s_tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int c = 0; c < nch; ++c) {
+        const int st = c % NSTG;
+        tma::mbar_wait(&empty[st], ((c / NSTG) & 1) ^ 1);
+        tma::mbar_expect_tx(&full[st], STG);
+        unsigned char* kr = smem + st * STG;
+        unsigned char* vr = kr + KBYTES;
+        for (int pp = 0; pp < CPG; ++pp) {
+          const int j = c * CPG + pp;
+          const int jj = j < n_pages ? j : c * CPG;  // past the end: any valid page, masked
+          const int page = jj < MAXPG ? s_pg[jj] : p.pages[jj];
+          const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
+          const int row_v = row_k + nkv * PT;
+          tma::load_2d(&kvmap, &full[st], kr + pp * 2048, 0, row_k);
+          tma::load_2d(&kvmap, &full[st], kr + CPG * 2048 + pp * 2048, 64, row_k);
+          tma::load_2d(&kvmap, &full[st], vr + pp * TILE, 0, row_v);
+          tma::load_2d(&kvmap, &full[st], vr + pp * TILE + 2048, 64, row_v);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t ID_S = umma::idesc_bf16(128, KC, false), ID_PV = umma::idesc_bf16(128, HD, true);
+      auto issue_s = [&](int t, int c) {
+        const uint32_t kr = smem_u32(smem + (c % NSTG) * STG);
+        const uint32_t qt = sq + t * QBYTES;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma::mma(tmem + t * KC, umma::desc_k_sw128(qt + (kk >> 2) * 16384) + 2 * (kk & 3),
+                    umma::desc_k_sw128(kr + (kk >> 2) * (CPG * 2048)) + 2 * (kk & 3), ID_S, kk > 0);
+        umma::commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int c) {
+        const uint32_t vr = smem_u32(smem + (c % NSTG) * STG) + KBYTES;
+        const uint32_t pt = sp + t * PBYTES;
+#pragma unroll
+        for (int pp = 0; pp < CPG; ++pp)
+          umma::mma(tmem + 128 + t * HD, umma::desc_k_sw128(pt) + 2 * pp,
+                    umma::desc_mn_sw128(vr + pp * TILE, 2048), ID_PV, (c > 0 || pp > 0) ? 1u : 0u);
+        umma::commit(&pv_done[t]);
+      };
+      tma::mbar_wait(&full[0], 0);
+      umma::fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int c = 0; c < nch; ++c) {
+        const bool more = c + 1 < nch;
+        if (more) tma::mbar_wait(&full[(c + 1) % NSTG], ((c + 1) / NSTG) & 1);
+        for (int t = 0; t < 2; ++t) {
+          tma::mbar_wait(&p_full[t], c & 1);  // P_t(c) written, S_t(c) consumed, O_t settled
+          umma::fence_after();
+          issue_pv(t, c);
+          if (more) issue_s(t, c + 1);
+        }
+        umma::commit(&empty[c % NSTG]);  // K/V stage free once both PVs completed
+      }
+    }
+  } else {
+    const int t = (warp - 2) >> 2;   // tile
+    const int lq = (warp & 3) * 32;  // TMEM lane quarter of this warp
+    const int g = lq + lane;         // row in the tile
+    const int r = t * 128 + g;       // row in the CTA
+    const uint32_t tS = tmem + ((uint32_t)lq << 16) + t * KC;
+    const uint32_t tO = tmem + ((uint32_t)lq << 16) + 128 + t * HD;
+    const uint32_t prow = sp + t * PBYTES + g * 128;
+    const int qpos = p.pos0 + t0 + r / p.grp;  // keys [0, qpos] visible
+    float m_used = -INFINITY, l = 0.f;
+    for (int c = 0; c < nch; ++c) {
+      const int key0 = c * KC;
+      tma::mbar_wait(&s_full[t], c & 1);
+      umma::fence_after();
+      uint32_t sr[KC];
+      umma::ld32_async(tS, sr);
+      umma::ld32_async(tS + 32, sr + 32);
+      umma::wait_ld();
+      float mx = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < KC; ++e) {
+        const float v = key0 + e <= qpos ? __uint_as_float(sr[e]) * p.scale_log2 : -INFINITY;
+        sr[e] = __float_as_uint(v);
+        mx = fmaxf(mx, v);
+      }
+      // PV_t(c-1) must be done before P_t is overwritten or O_t rescaled
+      if (c > 0) tma::mbar_wait(&pv_done[t], (c - 1) & 1);
+      const bool grow = mx > m_used + RESCALE_LOG2 || (m_used == -INFINITY && mx > -INFINITY);
+      if (__any_sync(0xffffffffu, grow && c > 0)) {
+        umma::fence_after();
+        const float alpha = grow ? exp2f(m_used - mx) : 1.f;
+#pragma unroll 1
+        for (int q = 0; q < HD / 32; ++q) {
+          uint32_t o[32];
+          umma::ld32_async(tO + q * 32, o);
+          umma::wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          umma::st32(tO + q * 32, o);
+        }
+        umma::wait_st();
+        l *= alpha;
+      }
+      if (grow) m_used = mx;
+      const float base = m_used == -INFINITY ? 0.f : m_used;
+#pragma unroll
+      for (int q = 0; q < KC / 8; ++q) {
+        float pf[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          pf[i] = exp2f(__uint_as_float(sr[8 * q + i]) - base);  // masked: exp2(-inf) = 0
+          l += pf[i];
+        }
+        const uint4 v = f32_to_bf16x8(pf);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(prow + (((q ^ (g & 7))) << 4)), "r"(v.x),
+                     "r"(v.y), "r"(v.z), "r"(v.w));
+      }
+      umma::fence_proxy_async();
+      umma::fence_before();
+      tma::mbar_arrive(&p_full[t]);
+    }
+    // epilogue: O_t / l -> bf16 rows of the output
+    tma::mbar_wait(&pv_done[t], (nch - 1) & 1);
+    umma::fence_after();
+    const int tpos = t0 + r / p.grp;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* dst = p.out + ((int64_t)tpos * p.nq + h * p.grp + r % p.grp) * HD;
+#pragma unroll 1
+    for (int q = 0; q < HD / 32; ++q) {
+      uint32_t o[32];
+      umma::ld32_async(tO + q * 32, o);
+      umma::wait_ld();
+      if (tpos < p.T) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float f[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(o[8 * i + e]) * inv;
+          reinterpret_cast<uint4*>(dst + q * 32)[i] = f32_to_bf16x8(f);
+        }
+      }
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    umma::fence_after();
+    umma::tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace pp
+
 }  // namespace pre
 }  // namespace psk
 
@@ -483,9 +720,24 @@ int psk_prefill_attn(const void* q_rot, int32_t T, int32_t pos0, int32_t n_q_hea
     t.nq = n_q_heads;
     t.grp = grp;
     t.layer = layer;
+    t.scale_log2 = p.scale_log2;
+    static const bool tc1 = getenv("PSK_PREFILL_TC1") != nullptr;
+    if (!tc1) {
+      t.qb = 256 / grp;
+      t.n_qblocks = (T + t.qb - 1) / t.qb;
+      static bool pp_attr = false;
+      if (!pp_attr) {
+        PSK_CUDA_TRY(cudaFuncSetAttribute(pp::prefill_attn_pp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          pp::SMEM));
+        pp_attr = true;
+      }
+      pp::prefill_attn_pp<<<t.n_qblocks * kv.n_kv_heads, pp::THREADS, pp::SMEM, psk::as_stream(stream)>>>(
+          map, t);
+      PSK_LAUNCH_CHECK();
+      return PSK_OK;
+    }
     t.qb = 128 / grp;
     t.n_qblocks = (T + t.qb - 1) / t.qb;
-    t.scale_log2 = p.scale_log2;
     static bool tc_attr = false;
     if (!tc_attr) {
       PSK_CUDA_TRY(cudaFuncSetAttribute(tc::prefill_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
