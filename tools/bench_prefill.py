@@ -42,3 +42,30 @@ def attn():
 da = bench._time_launches(attn, 16)
 afl = 4 * cfg.n_heads * cfg.head_dim * (T * (T + 1) / 2)  # QK^T + PV over the causal triangle
 print(f"prefill attention T={T}: {da * 1e6:.1f} us/layer  {afl / da / 1e12:.1f} TFLOP/s (causal flops)")
+
+# in-situ ablation: prefill with one launch kind replaced by a no-op
+kinds = {"gemm": ["psk_gemm", "psk_gemm_qkv_rope_kv"], "attention": ["psk_prefill_attn"],
+         "rmsnorm": ["psk_rmsnorm_rows"], "embed": ["psk_embed_tokens"]}
+for name, fns in kinds.items():
+    saved = {f: getattr(lib, f) for f in fns}
+    for f in fns:
+        setattr(lib, f, lambda *a: 0)
+    t = bench._time_launches(lambda: pre.run(toks, 0, pt), 3)
+    for f, fn in saved.items():
+        setattr(lib, f, fn)
+    print(f"  without {name:10s} {t * 1e3:8.2f} ms -> in-situ {(dt - t) * 1e3:7.2f} ms")
+
+# each GEMM shape alone (weights of all layers cycled)
+A = torch.randn(T, 14336, device="cuda").to(torch.bfloat16)
+shapes = {"qkv": (cfg.qkv_dim, 4096, base.wqkv), "o": (4096, 4096, base.wo), "gate_up": (2 * cfg.ffn, 4096, base.wgu),
+          "down": (4096, cfg.ffn, base.wdown)}
+for name, (N, K, ws) in shapes.items():
+    o = torch.empty(T, N, dtype=torch.bfloat16, device="cuda")
+    it2 = [0]
+
+    def g():
+        _lib.check(lib.psk_gemm(A.data_ptr(), ws[it2[0] % cfg.n_layers].data_ptr(), T, N, K, 0, o.data_ptr(), N,
+                                torch.cuda.current_stream().cuda_stream))
+        it2[0] += 1
+    dg = bench._time_launches(g, 16)
+    print(f"  gemm {name:8s} M={T} N={N:6d} K={K:6d}: {dg * 1e6:8.1f} us {2 * T * N * K / dg / 1e12:7.1f} TFLOP/s")
