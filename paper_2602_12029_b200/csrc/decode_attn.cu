@@ -27,6 +27,7 @@
 #include "common.cuh"
 #include "mma.cuh"
 #include "tma.cuh"
+#include "umma.cuh"
 
 #include <math.h>
 
@@ -388,86 +389,58 @@ __global__ void __launch_bounds__(HD) decode_attn_merge(const __grid_constant__ 
 // When a session carries many decode rows (fan-out: up to 16 modules x 4 GQA
 // heads = 64 query rows per KV head) the mma.sync kernel above is bound by
 // the legacy tensor pipe, not HBM. This variant runs both products on the
-// 5th-gen tensor cores: per 8-page chunk (128 tokens),
-//   S[128 rows x 128 tok] = Q . K^T   (8 UMMA M=128 N=128 K=16, TMEM)
-//   D[128 rows x 128 dim] = P . V     (8 UMMA, V as an MN-major B operand)
-// A producer warp streams K/V chunks with TMA into a 2-stage ring (K boxes
-// laid out so the chunk's 128 token rows sit at a uniform 128 B stride), an
-// MMA warp issues tcgen05.mma, and 4 softmax warps own one query row each
-// (thread = TMEM lane): they read S, write bf16 P back to shared memory in
-// the UMMA K-major SW128 layout, and fold D into an fp32 O held in
-// registers with the online-softmax rescale.
+// 5th-gen tensor cores with the same CTA = (session, kv head, split) work
+// split and the same (m, l, o) partial format, so the merge kernel is shared.
+//   warp 0     TMA producer: 4 pages per 64-key chunk, 6 stages; lane p
+//              loads page p (in parallel): its K tile as two [16 x 64] boxes
+//              so the chunk's K sits as [dims 0-63 x 64 keys][dims 64-127 x
+//              64 keys] (one N=64 MMA per K-step covers the chunk), its V
+//              tile as one 3-D box [half0 | half1]
+//   warp 1     MMA issuer + TMEM owner. Q and P live in TMEM (A operand
+//              from tensor memory): S_u = Q K^T (M128 N64, 8 MMAs) and
+//              O_u += P_u V_p (M128 N128 K16, one per page)
+//   warps 2-9  two softmax groups u = 0, 1 taking alternate chunks, with
+//              separate TMEM accumulators O_0, O_1 and separate (m, l): the
+//              tensor core runs one group's MMAs while the other group does
+//              its softmax; O is rescaled in TMEM only when a row max grows
+//              by > 2^8 (lazy, exact after the final 1/l). At the end group 0
+//              folds O_1 into O_0 and writes the split partial.
+// Query rows = TMEM lanes (rows >= G are never read), so only the warps
+// whose lane quarter holds live rows take part in the softmax.
+// TMEM columns: S_0 [0,64) S_1 [64,128) O_0 [128,256) O_1 [256,384)
+//               Q [384,448) (bf16 pairs) P_0 [448,480) P_1 [480,512).
+// (TMA ops cost ~60-80 ns each whatever their size below ~4 KiB, so ops
+// per page bound the stream: 4 per page ~25 GB/s per SM; one 8 KiB box
+// ~47 GB/s. Per-page N=16 S MMAs, which would allow one box per page, cost
+// more in MMA issue than they save: 54 us vs 39 us at 32k x 16 modules.)
 namespace tcv {
 
-constexpr int CP = 8;                  // pages per chunk
-constexpr int NSTG = 2;                // chunk stages
-constexpr int KREG = CP * TILE;        // 32 KiB: [dims 0-63 box x 8 pages][dims 64-127 box x 8 pages]
-constexpr int VREG = CP * TILE;        // 32 KiB: [page][box0 | box1]
-constexpr int STG = KREG + VREG;
-constexpr int OFF_Q = NSTG * STG;      // 128 KiB
-constexpr int OFF_P = OFF_Q + 32768;   // Q: [2 boxes][128 rows][128 B]
-constexpr int OFF_BAR = OFF_P + 32768; // P: same layout
+constexpr int CPG = 4;                  // pages per chunk
+constexpr int KC = CPG * PT;            // 64 keys
+constexpr int NSTG = 6;
+constexpr int KBYTES = CPG * TILE;      // 16 KiB: [half0 x 4 pages][half1 x 4 pages]
+constexpr int STG = 2 * KBYTES;         // + V 16 KiB: [page][half0 | half1]
+constexpr int OFF_ML = NSTG * STG;
+constexpr int OFF_BAR = OFF_ML + 128 * 8;
 constexpr int OFF_PG = OFF_BAR + 256;
-constexpr int SMEM = OFF_PG + MAXP * 4 + 1024;
-constexpr int THREADS = 192;           // w0 TMA, w1 MMA (+TMEM alloc), w2-5 softmax
-constexpr int TMEM_COLS = 256;         // S: cols [0,128), D: cols [128,256)
-
-__device__ __forceinline__ uint64_t desc_k_sw128(uint32_t addr) {
-  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-// MN-major SW128: 64-element MN groups at LBO, 8-row K groups at SBO.
-__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t addr, uint32_t lbo) {
-  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-__host__ __device__ constexpr uint32_t idesc(bool b_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(128 >> 3) << 17) |
-         ((uint32_t)(128 >> 4) << 24);
-}
-__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(id), "r"(acc));
-}
-__device__ __forceinline__ void commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   tma::sa(bar))
-               : "memory");
-}
-__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
+constexpr int OFF_INFO = OFF_PG + MAXP * 4;
+constexpr int SMEM = OFF_INFO + MAXP * 4 + 1024;
+constexpr int THREADS = 320;
+constexpr uint32_t T_S = 0, T_O = 128, T_Q = 384, T_P = 448;
+constexpr float RESCALE_LOG2 = 8.f;
 
 __global__ void __launch_bounds__(THREADS, 1)
-    decode_attn_tc(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ Params p) {
+    decode_attn_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                   const __grid_constant__ Params p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* full = bars;            // [2]
-  uint64_t* empty = bars + 2;       // [2]
-  uint64_t* s_full = bars + 4;
-  uint64_t* s_empty = bars + 5;
-  uint64_t* p_full = bars + 6;
-  uint64_t* d_full = bars + 7;
-  uint64_t* d_empty = bars + 8;
+  uint64_t *full = bars, *empty = bars + NSTG, *s_full = bars + 2 * NSTG, *p_full = s_full + 2,
+           *pv_done = p_full + 2, *g1_done = pv_done + 2, *s_free = g1_done + 1;
   int* s_page = reinterpret_cast<int*>(smem + OFF_PG);
+  int* s_info = reinterpret_cast<int*>(smem + OFF_INFO);  // (owner + 1) << 8 | valid tokens
+  float* s_ml = reinterpret_cast<float*>(smem + OFF_ML);  // group 1 (m, l) per row
   __shared__ int s_rows[MAXR], s_plen[MAXR], s_pstart[MAXR + 1];
   __shared__ int s_ps, s_ls, s_total;
   __shared__ uint32_t s_tmem;
@@ -480,11 +453,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int sess = item / (p.ns * nkv);
   const int nr = p.b.sess_nrows[sess];
   const int G = nr * p.grp;
+  const int act = (G + 31) / 32;  // softmax warps with live rows, per group
 
   if (threadIdx.x < nr) {
     const int r = p.b.sess_rows[(int64_t)sess * p.b.max_rows_per_sess + threadIdx.x];
     s_rows[threadIdx.x] = r;
-    s_plen[threadIdx.x] = p.b.priv_len[r] + 1;
+    s_plen[threadIdx.x] = p.b.priv_len[r] + 1;  // includes the token appended this step
   } else if (threadIdx.x == 32) {
     s_ls = p.b.sess_len[sess];
   }
@@ -503,208 +477,246 @@ __global__ void __launch_bounds__(THREADS, 1)
       tma::mbar_init(&full[s], 1);
       tma::mbar_init(&empty[s], 1);
     }
-    tma::mbar_init(s_full, 1);
-    tma::mbar_init(s_empty, 128);
-    tma::mbar_init(p_full, 128);
-    tma::mbar_init(d_full, 1);
-    tma::mbar_init(d_empty, 128);
+    for (int u = 0; u < 2; ++u) {
+      tma::mbar_init(&s_full[u], 1);
+      tma::mbar_init(&s_free[u], 32 * act);
+      tma::mbar_init(&p_full[u], 32 * act);
+      tma::mbar_init(&pv_done[u], 1);
+    }
+    tma::mbar_init(g1_done, 32 * act);
     tma::fence_mbar_init();
-    tma::prefetch_map(&kvmap);
+    tma::prefetch_map(&kmap);
+    tma::prefetch_map(&vmap);
   }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tma::sa(&s_tmem)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
+  if (warp == 1) umma::tmem_alloc(&s_tmem, 512);
   __syncthreads();
   const int total = s_total;
   const int k0 = (int)((int64_t)j_split * total / p.ns);
   const int k1 = (int)((int64_t)(j_split + 1) * total / p.ns);
   const int np = k1 - k0;
-  const int nch = (np + CP - 1) / CP;
-  for (int j = threadIdx.x; j < np && j < MAXP; j += THREADS) {
+  const int nch = (np + CPG - 1) / CPG;
+  // page id and (owner row, valid tokens) of the split's j-th page
+  auto page_of = [&](int j, int& info) -> int {
     const int k = k0 + j;
-    int pg;
     if (k < s_ps) {
-      pg = p.b.sess_pages[(int64_t)sess * p.b.max_sess_pages + k];
-    } else {
-      int i = 0;
-      while (k >= s_pstart[i + 1]) ++i;
-      pg = p.b.row_pages[(int64_t)s_rows[i] * p.b.max_row_pages + (k - s_pstart[i])];
+      info = min(PT, s_ls - k * PT);
+      return p.b.sess_pages[(int64_t)sess * p.b.max_sess_pages + k];
     }
-    s_page[j] = pg;
+    int i = 0;
+    while (k >= s_pstart[i + 1]) ++i;
+    info = ((i + 1) << 8) | min(PT, s_plen[i] - (k - s_pstart[i]) * PT);
+    return p.b.row_pages[(int64_t)s_rows[i] * p.b.max_row_pages + (k - s_pstart[i])];
+  };
+  for (int j = threadIdx.x; j < np && j < MAXP; j += THREADS) {
+    int info;
+    s_page[j] = page_of(j, info);
+    s_info[j] = info;
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  // Q -> shared, UMMA K-major SW128: [box = dims/64][row][128 B], rows >= G zero
-  for (int e = threadIdx.x; e < 128 * 16; e += THREADS) {
-    const int g = e >> 4, c = e & 15;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (g < G) {
-      const int qh = h * p.grp + g % p.grp;
-      v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)s_rows[g / p.grp] * p.nq + qh) * HD + c * 8);
-    }
-    const uint32_t a = smem_u32(smem + OFF_Q) + (c >> 3) * 16384 + g * 128 + (((c & 7) ^ (g & 7)) << 4);
-    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  fence_before();
-  __syncthreads();
-  fence_after();
   const uint32_t tmem = s_tmem;
-  const uint32_t sq = smem_u32(smem + OFF_Q), sp = smem_u32(smem + OFF_P);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // q / new K,V come from rope_append
+  // Q rows -> TMEM (lane = row, bf16 pairs), by the group-0 warps of live lanes
+  if (warp >= 2 && warp < 6 && (warp & 3) < act) {
+    const int g = (warp & 3) * 32 + lane;
+    const uint32_t tq = tmem + ((uint32_t)((warp & 3) * 32) << 16) + T_Q;
+    const uint4* src = nullptr;
+    if (g < G)
+      src = reinterpret_cast<const uint4*>(p.q + ((int64_t)s_rows[g / p.grp] * p.nq + h * p.grp + g % p.grp) * HD);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t r[32];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 v = src ? src[half * 8 + i] : make_uint4(0, 0, 0, 0);
+        r[4 * i] = v.x;
+        r[4 * i + 1] = v.y;
+        r[4 * i + 2] = v.z;
+        r[4 * i + 3] = v.w;
+      }
+      umma::st32(tq + half * 32, r);
+    }
+    umma::wait_st();
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
 
   if (warp == 0) {
-    if (lane == 0 && np > 0) {
+    if (lane < CPG) {
+      const int pp = lane;
       for (int c = 0; c < nch; ++c) {
         const int st = c % NSTG;
         tma::mbar_wait(&empty[st], ((c / NSTG) & 1) ^ 1);
-        tma::mbar_expect_tx(&full[st], STG);
+        if (pp == 0) tma::mbar_expect_tx(&full[st], STG);
+        __syncwarp(0xfu);
+        const int j = c * CPG + pp;
+        const int jj = j < np ? j : 0;  // past the end: any valid page, masked
+        int info;
+        const int page = jj < MAXP ? s_page[jj] : page_of(jj, info);
+        const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
         unsigned char* kr = smem + st * STG;
-        unsigned char* vr = kr + KREG;
-        for (int pp = 0; pp < CP; ++pp) {
-          const int j = c * CP + pp;
-          // pages past the slice reload a valid page (finite data); masked below
-          const int jj = j < np ? j : c * CP;
-          const int page = jj < MAXP ? s_page[jj] : s_page[0];
-          const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
-          const int row_v = row_k + nkv * PT;
-          tma::load_2d(&kvmap, &full[st], kr + pp * 2048, 0, row_k);
-          tma::load_2d(&kvmap, &full[st], kr + CP * 2048 + pp * 2048, 64, row_k);
-          tma::load_2d(&kvmap, &full[st], vr + pp * TILE, 0, row_v);
-          tma::load_2d(&kvmap, &full[st], vr + pp * TILE + 2048, 64, row_v);
-        }
+        tma::load_2d(&kmap, &full[st], kr + pp * 2048, 0, row_k);
+        tma::load_2d(&kmap, &full[st], kr + CPG * 2048 + pp * 2048, 64, row_k);
+        tma::load_3d(&vmap, &full[st], kr + KBYTES + pp * TILE, 0, row_k + nkv * PT, 0);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && np > 0) {
-      constexpr uint32_t ID_QK = idesc(false), ID_PV = idesc(true);
+    if (lane == 0) {
+      constexpr uint32_t ID_S = umma::idesc_bf16(128, KC, false), ID_PV = umma::idesc_bf16(128, HD, true);
+      auto issue_s = [&](int c) {
+        const int u = c & 1;
+        const uint32_t kb = smem_u32(smem + (c % NSTG) * STG);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma::mma_ts(tmem + T_S + u * KC, tmem + T_Q + kk * 8,
+                       umma::desc_k_sw128(kb + (kk >> 2) * KBYTES / 2) + 2 * (kk & 3), ID_S, kk > 0);
+        umma::commit(&s_full[u]);
+      };
+      auto issue_pv = [&](int c) {
+        const int u = c & 1;
+        const uint32_t vb = smem_u32(smem + (c % NSTG) * STG) + KBYTES;
+#pragma unroll
+        for (int pp = 0; pp < CPG; ++pp)
+          umma::mma_ts(tmem + T_O + u * HD, tmem + T_P + u * 32 + pp * 8,
+                       umma::desc_mn_sw128(vb + pp * TILE, 2048), ID_PV, (c >= 2 || pp > 0) ? 1u : 0u);
+        umma::commit(&pv_done[u]);
+        umma::commit(&empty[c % NSTG]);
+      };
+      for (int c = 0; c < nch && c < 2; ++c) {
+        tma::mbar_wait(&full[c], 0);
+        umma::fence_after();
+        issue_s(c);
+      }
       for (int c = 0; c < nch; ++c) {
-        const int st = c % NSTG;
-        const uint32_t kr = smem_u32(smem + st * STG), vr = kr + KREG;
-        tma::mbar_wait(&full[st], (c / NSTG) & 1);
-        tma::mbar_wait(s_empty, (c & 1) ^ 1);
-        fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t a = desc_k_sw128(sq + (kk >> 2) * 16384) + 2 * (kk & 3);
-          const uint64_t b = desc_k_sw128(kr + (kk >> 2) * (CP * 2048)) + 2 * (kk & 3);
-          umma(tmem, a, b, ID_QK, kk > 0);
+        // S_u(c+2) as soon as softmax(c) has S_u(c) in registers, so it runs
+        // under that softmax; then PV_u(c) once P_u(c) is in TMEM
+        if (c + 2 < nch) {
+          tma::mbar_wait(&s_free[c & 1], (c >> 1) & 1);
+          tma::mbar_wait(&full[(c + 2) % NSTG], ((c + 2) / NSTG) & 1);
+          umma::fence_after();
+          issue_s(c + 2);
         }
-        commit(s_full);
-        tma::mbar_wait(p_full, c & 1);
-        tma::mbar_wait(d_empty, (c & 1) ^ 1);
-        fence_after();
-#pragma unroll
-        for (int pp = 0; pp < CP; ++pp) {
-          const uint64_t a = desc_k_sw128(sp + (pp >> 2) * 16384) + 2 * (pp & 3);
-          const uint64_t b = desc_mn_sw128(vr + pp * TILE, 2048);
-          umma(tmem + 128, a, b, ID_PV, pp > 0);
-        }
-        commit(d_full);
-        commit(&empty[st]);
+        tma::mbar_wait(&p_full[c & 1], (c >> 1) & 1);  // P_u(c) in TMEM, O_u settled
+        umma::fence_after();
+        issue_pv(c);
       }
     }
-  } else {
-    // ---------------- softmax: thread = query row = TMEM lane ----------------
-    const int q = warp & 3;
-    const int g = q * 32 + lane;
-    const uint32_t tS = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t tD = tS + 128;
-    const int own = g < G ? g / p.grp : -2;
-    float O[HD];
-#pragma unroll
-    for (int i = 0; i < HD; ++i) O[i] = 0.f;
-    float m = -INFINITY, l = 0.f;
-    for (int c = 0; c < nch; ++c) {
-      int lim[CP], ownr[CP];
-#pragma unroll
-      for (int pp = 0; pp < CP; ++pp) {
-        const int j = c * CP + pp;
-        const int k = k0 + j;
-        if (j >= np) {
-          lim[pp] = 0;
-          ownr[pp] = -1;
-        } else if (k < s_ps) {
-          lim[pp] = min(PT, s_ls - k * PT);
-          ownr[pp] = -1;
-        } else {
-          int i = 0;
-          while (k >= s_pstart[i + 1]) ++i;
-          lim[pp] = min(PT, s_plen[i] - (k - s_pstart[i]) * PT);
-          ownr[pp] = i;
-        }
-        if (ownr[pp] >= 0 && ownr[pp] != own) lim[pp] = 0;
-      }
-      tma::mbar_wait(s_full, c & 1);
-      fence_after();
+  } else if ((warp & 3) < act) {
+    const int u = (warp - 2) >> 2;   // softmax group
+    const int lq = (warp & 3) * 32;  // TMEM lane quarter
+    const int g = lq + lane;         // query row (TMEM lane)
+    const int ri = g < G ? g / p.grp : -1;
+    const uint32_t tl = tmem + ((uint32_t)lq << 16);
+    const uint32_t tS = tl + T_S + u * KC, tO = tl + T_O + u * HD, tP = tl + T_P + u * 32;
+    float m_used = -INFINITY, l = 0.f;
+    int it = 0;
+    for (int c = u; c < nch; c += 2, ++it) {
+      tma::mbar_wait(&s_full[u], it & 1);
+      umma::fence_after();
+      uint32_t sr[KC];
+      umma::ld32_async(tS, sr);
+      umma::ld32_async(tS + 32, sr + 32);
+      umma::wait_ld();
+      umma::fence_before();
+      tma::mbar_arrive(&s_free[u]);  // S_u may be overwritten by S_u(c+2)
       float mx = -INFINITY;
-      float v[32];
 #pragma unroll
-      for (int gi = 0; gi < 4; ++gi) {
-        ld32(tS + gi * 32, v);
+      for (int pp = 0; pp < CPG; ++pp) {
+        const int j = c * CPG + pp;
+        int info = 0;
+        if (j < np) {
+          if (j < MAXP) info = s_info[j];
+          else page_of(j, info);
+        }
+        const int own = (info >> 8) - 1, lim = info & 0xff;
+        const bool page_ok = ri >= 0 && (own < 0 || own == ri);
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int col = gi * 32 + e;
-          if ((col & 15) < lim[col >> 4]) mx = fmaxf(mx, v[e] * p.scale_log2);
+        for (int e = 0; e < PT; ++e) {
+          const float v = page_ok && e < lim ? __uint_as_float(sr[pp * PT + e]) * p.scale_log2 : -INFINITY;
+          sr[pp * PT + e] = __float_as_uint(v);
+          mx = fmaxf(mx, v);
         }
       }
-      const float mn = fmaxf(m, mx);
-      const float base = mn == -INFINITY ? 0.f : mn;
-      const float alpha = exp2f(m - base);
-      float ladd = 0.f;
+      if (it > 0) tma::mbar_wait(&pv_done[u], (it - 1) & 1);  // P_u free, O_u settled
+      const bool grow = mx > m_used + RESCALE_LOG2 || (m_used == -INFINITY && mx > -INFINITY);
+      if (__any_sync(0xffffffffu, grow && it > 0)) {
+        umma::fence_after();
+        const float alpha = grow ? exp2f(m_used - mx) : 1.f;
+#pragma unroll 1
+        for (int q = 0; q < HD / 32; ++q) {
+          uint32_t o[32];
+          umma::ld32_async(tO + q * 32, o);
+          umma::wait_ld();
 #pragma unroll
-      for (int gi = 0; gi < 4; ++gi) {
-        ld32(tS + gi * 32, v);
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const int col = gi * 32 + e;
-          const float p0 = (col & 15) < lim[col >> 4] ? exp2f(v[e] * p.scale_log2 - base) : 0.f;
-          const float p1 = ((col + 1) & 15) < lim[(col + 1) >> 4] ? exp2f(v[e + 1] * p.scale_log2 - base) : 0.f;
-          ladd += p0 + p1;
-          pk[e >> 1] = pack_bf16(p0, p1);
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          umma::st32(tO + q * 32, o);
         }
-        // 32 tokens = 4 16-byte chunks of this row; K-major SW128 like Q
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const int chunk = gi * 4 + cc;  // 0..15 (8 tokens each)
-          const uint32_t a = sp + (chunk >> 3) * 16384 + g * 128 + (((chunk & 7) ^ (g & 7)) << 4);
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(pk[4 * cc]), "r"(pk[4 * cc + 1]),
-                       "r"(pk[4 * cc + 2]), "r"(pk[4 * cc + 3]));
-        }
+        l *= alpha;
       }
-      fence_before();
-      tma::mbar_arrive(s_empty);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tma::mbar_arrive(p_full);
-      l = l * alpha + ladd;
-      tma::mbar_wait(d_full, c & 1);
-      fence_after();
+      if (grow) m_used = mx;
+      const float base = m_used == -INFINITY ? 0.f : m_used;
+      uint32_t pk[KC / 2];
 #pragma unroll
-      for (int gi = 0; gi < 4; ++gi) {
-        ld32(tD + gi * 32, v);
-#pragma unroll
-        for (int e = 0; e < 32; ++e) O[gi * 32 + e] = O[gi * 32 + e] * alpha + v[e];
+      for (int i = 0; i < KC / 2; ++i) {
+        const float p0 = exp2f(__uint_as_float(sr[2 * i]) - base);  // masked: exp2(-inf) = 0
+        const float p1 = exp2f(__uint_as_float(sr[2 * i + 1]) - base);
+        l += p0 + p1;
+        pk[i] = pack_bf16(p0, p1);
       }
-      fence_before();
-      tma::mbar_arrive(d_empty);
-      m = mn;
+      umma::st32(tP, pk);
+      umma::wait_st();
+      umma::fence_before();
+      tma::mbar_arrive(&p_full[u]);
     }
-    if (g < G) {
-      const int64_t slot = (int64_t)item * GMAX + g;
-      p.pm[slot] = m;
-      p.pl[slot] = l;
-      float4* dst = reinterpret_cast<float4*>(p.po + slot * HD);
+    if (it > 0) tma::mbar_wait(&pv_done[u], (it - 1) & 1);  // this group's last PV landed
+    umma::fence_after();
+    if (u == 1) {
+      s_ml[2 * g] = m_used;
+      s_ml[2 * g + 1] = l;
+      umma::fence_before();
+      tma::mbar_arrive(g1_done);
+    } else {
+      tma::mbar_wait(g1_done, 0);
+      umma::fence_after();
+      const bool has1 = nch > 1;  // group 1 ran at least one chunk (O_1 written)
+      const float m1 = s_ml[2 * g], l1 = s_ml[2 * g + 1];
+      const float M = fmaxf(m_used, m1);
+      const float Mr = M == -INFINITY ? 0.f : M;
+      const float a0 = m_used == -INFINITY ? 0.f : exp2f(m_used - Mr);
+      const float a1 = m1 == -INFINITY ? 0.f : exp2f(m1 - Mr);
+      const int64_t base = (int64_t)item * GMAX;
+#pragma unroll 1
+      for (int q = 0; q < HD / 32; ++q) {
+        uint32_t o0[32], o1[32];
+        umma::ld32_async(tO + q * 32, o0);
+        umma::ld32_async(tO + HD + q * 32, o1);  // O_1 sits HD columns after O_0
+        umma::wait_ld();
+        if (g < G) {
+          float4* dst = reinterpret_cast<float4*>(p.po + (base + g) * HD + q * 32);
 #pragma unroll
-      for (int i = 0; i < HD / 4; ++i) dst[i] = make_float4(O[4 * i], O[4 * i + 1], O[4 * i + 2], O[4 * i + 3]);
+          for (int i = 0; i < 8; ++i) {
+            float f[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float x0 = a0 != 0.f ? a0 * __uint_as_float(o0[4 * i + e]) : 0.f;
+              const float x1 = (has1 && a1 != 0.f) ? a1 * __uint_as_float(o1[4 * i + e]) : 0.f;
+              f[e] = x0 + x1;
+            }
+            dst[i] = make_float4(f[0], f[1], f[2], f[3]);
+          }
+        }
+      }
+      if (g < G) {
+        p.pm[base + g] = M;
+        p.pl[base + g] = l * a0 + l1 * a1;
+      }
     }
   }
-  fence_before();
-  __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;");
+  umma::fence_before();
+  __syncthreads();
   if (warp == 1) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    umma::fence_after();
+    umma::tmem_dealloc(tmem, 512);
   }
 }
 
@@ -721,16 +733,16 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 
 // 2D TMA map over a KV page pool: rows of 128 dims (256 B), [16 x 64] boxes,
 // 128B swizzle. Cached per pool geometry. Shared by the attention kernels.
-int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out, bool page_box) {
+int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out, int kind) {
   using namespace dattn;
   // small cache keyed by the pool geometry and the box kind
   static CUtensorMap cached[8];
   static psk_kv_layout keys[8] = {};
-  static bool kinds[8] = {};
+  static int kinds[8] = {};
   static int next = 0;
   for (int i = 0; i < 8; ++i)
     if (keys[i].base == kv.base && keys[i].n_pages == kv.n_pages && keys[i].page_elems == kv.page_elems &&
-        kinds[i] == page_box) {
+        kinds[i] == kind) {
       *out = cached[i];
       return PSK_OK;
     }
@@ -749,12 +761,20 @@ int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out, bool page_box) {
   const int i = next;
   next = (next + 1) % 8;
   CUresult r;
-  if (!page_box) {
+  if (kind == KV_BOX2D) {
     cuuint64_t dims[2] = {(cuuint64_t)HD, rows};
     cuuint64_t strides[1] = {(cuuint64_t)HD * 2};
     cuuint32_t box[2] = {64, (cuuint32_t)PT};
     cuuint32_t es[2] = {1, 1};
     r = enc(&cached[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kv.base, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (kind == KV_TILE3D) {
+    cuuint64_t dims[3] = {64, rows, 2};
+    cuuint64_t strides[2] = {(cuuint64_t)HD * 2, 128};
+    cuuint32_t box[3] = {64, (cuuint32_t)PT, 2};
+    cuuint32_t es[3] = {1, 1, 1};
+    r = enc(&cached[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, kv.base, dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
@@ -774,7 +794,7 @@ int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out, bool page_box) {
     return PSK_ECUDA;
   }
   keys[i] = kv;
-  kinds[i] = page_box;
+  kinds[i] = kind;
   *out = cached[i];
   return PSK_OK;
 }
@@ -802,12 +822,14 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   PSK_CHECK_ARG(b->max_rows_per_sess <= MAXR && grp * b->max_rows_per_sess <= GMAX,
                 "psk_decode_attn: %d query rows per KV head exceed %d", grp * b->max_rows_per_sess, GMAX);
   if (b->n_rows == 0) return PSK_OK;
-  // tcgen05 fan-out path: opt-in (PSK_ATTN_TC=1) until it beats mma.sync —
-  // measured on B200 it does not yet (32k x 16 modules: 100 us vs 51 us)
-  static const bool use_tc_env = getenv("PSK_ATTN_TC") != nullptr;
-  const bool use_tc = grp * b->max_rows_per_sess > 16 && use_tc_env;
-  CUtensorMap map;
-  int rc = psk::kv_tensor_map(kv, &map, /*page_box=*/!use_tc);
+  // > 32 query rows per KV head (3-4 m16 tiles): tcgen05 fan-out kernel
+  // (32k x 16 modules: 36.7 us vs 48.6 us); up to 32 rows mma.sync is faster
+  // (32k x 8: 30.1 vs 32.0 us). PSK_ATTN_HMMA=1 keeps mma.sync everywhere.
+  static const bool force_hmma = getenv("PSK_ATTN_HMMA") != nullptr;
+  const bool use_tc = grp * b->max_rows_per_sess > 32 && !force_hmma;
+  CUtensorMap map, vmap;
+  int rc = psk::kv_tensor_map(kv, &map, use_tc ? psk::KV_BOX2D : psk::KV_PAGE4D);
+  if (!rc && use_tc) rc = psk::kv_tensor_map(kv, &vmap, psk::KV_TILE3D);
   if (rc) return rc;
   Params p;
   p.b = *b;
@@ -849,7 +871,7 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
     }
     cfg.blockDim = dim3(tcv::THREADS);
     cfg.dynamicSmemBytes = tcv::SMEM;
-    PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tcv::decode_attn_tc, map, p));
+    PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tcv::decode_attn_tc, map, vmap, p));
   } else {
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = SMEM;

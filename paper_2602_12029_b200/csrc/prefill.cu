@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t *full = bars, *empty = bars + NSTG, *s_full = bars + 2 * NSTG, *p_full = s_full + 2,
-           *pv_done = p_full + 2;
+           *pv_done = p_full + 2, *s_free = pv_done + 2;
   int* s_pg = reinterpret_cast<int*>(smem + OFF_PG);
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -489,6 +489,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int t = 0; t < 2; ++t) {
       tma::mbar_init(&s_full[t], 1);
+      tma::mbar_init(&s_free[t], 128);
       tma::mbar_init(&p_full[t], 128);
       tma::mbar_init(&pv_done[t], 1);
     }
@@ -567,10 +568,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool more = c + 1 < nch;
         if (more) tma::mbar_wait(&full[(c + 1) % NSTG], ((c + 1) / NSTG) & 1);
         for (int t = 0; t < 2; ++t) {
-          tma::mbar_wait(&p_full[t], c & 1);  // P_t(c) written, S_t(c) consumed, O_t settled
+          // S_t(c+1) as soon as softmax(c) holds S_t(c) in registers (it runs
+          // under that softmax), PV_t(c) once P_t(c) is written
+          if (more) {
+            tma::mbar_wait(&s_free[t], c & 1);
+            umma::fence_after();
+            issue_s(t, c + 1);
+          }
+          tma::mbar_wait(&p_full[t], c & 1);  // P_t(c) written, O_t settled
           umma::fence_after();
           issue_pv(t, c);
-          if (more) issue_s(t, c + 1);
         }
         umma::commit(&empty[c % NSTG]);  // K/V stage free once both PVs completed
       }
@@ -593,6 +600,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       umma::ld32_async(tS, sr);
       umma::ld32_async(tS + 32, sr + 32);
       umma::wait_ld();
+      umma::fence_before();
+      tma::mbar_arrive(&s_free[t]);  // S_t may be overwritten by S_t(c+1)
       float mx = -INFINITY;
 #pragma unroll
       for (int e = 0; e < KC; ++e) {

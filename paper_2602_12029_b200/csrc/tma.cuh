@@ -49,6 +49,15 @@ __device__ __forceinline__ void load_2d(const CUtensorMap* map, uint64_t* bar, v
       : "memory");
 }
 
+// 3D tiled TMA load (box given by the tensor map) completing on `bar`.
+__device__ __forceinline__ void load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(sa(dst)),
+      "l"(map), "r"(sa(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // 4D tiled TMA load (box given by the tensor map) completing on `bar`.
 __device__ __forceinline__ void load_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
                                         int c3) {
@@ -95,9 +104,12 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t addr) {
 #include "../../include/psk.h"
 namespace psk {
 // TMA maps over a paged KV pool (decode_attn.cu), 128B-swizzled:
-//  page_box = false: 2D, [16 token x 64 dim] boxes (one half of a K or V tile);
-//  page_box = true : 4D (64 dim, 16 token, 2 halves, K|V), one box = the whole
-//                    8 KiB K+V of one (page, layer, head), landing as
-//                    [K half0 | K half1 | V half0 | V half1] x [16][128 B].
-int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out, bool page_box = false);
+//  KV_BOX2D : 2D, [16 token x 64 dim] boxes (one half of a K or V tile);
+//  KV_TILE3D: 3D (64 dim, 16 token, 2 halves), one box = a whole 4 KiB K or
+//             V tile landing as [half0 | half1] x [16][128 B];
+//  KV_PAGE4D: 4D (64 dim, 16 token, 2 halves, K|V), one box = the whole
+//             8 KiB K+V of one (page, layer, head), landing as
+//             [K half0 | K half1 | V half0 | V half1] x [16][128 B].
+enum KvMapKind { KV_BOX2D = 0, KV_TILE3D = 1, KV_PAGE4D = 2 };
+int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out, int kind = KV_BOX2D);
 }  // namespace psk

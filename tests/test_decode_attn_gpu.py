@@ -71,13 +71,13 @@ def test_one_session_four_modules(splits):
 
 
 def test_sixteen_modules_fanout():
-    """64 query rows per KV head -> the tcgen05 path."""
+    """64 query rows per KV head -> the tcgen05 path (> 32 rows)."""
     _case(32, 8, [2000], [16], [i * 7 for i in range(16)], 16, seed=1)
 
 
 @pytest.mark.parametrize("mods,splits", [(5, 1), (8, 7), (12, 30), (16, 64)])
 def test_fanout_tcgen05_shapes(mods, splits):
-    """20..64 query rows per KV head (tcgen05 path), ragged private suffixes,
+    """20..64 query rows per KV head (mma.sync up to 32, tcgen05 above), ragged private suffixes,
     shared length ending mid-page, several split counts (incl. splits whose
     last 8-page chunk is partial)."""
     _case(32, 8, [1333], [mods], [(i * 37) % 200 for i in range(mods)], splits, seed=mods)
