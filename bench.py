@@ -255,27 +255,39 @@ def decode_attn_roofline(eng, peaks) -> dict:
             "bytes_per_launch": nbytes, "us_per_launch": round(dt * 1e6, 2)}
 
 
-def decode_attn_fanout(peaks, shared_tokens=32767, modules=16) -> dict:
-    """K6 at the config-4 fan-out shape: one 32k-token shared context read by
-    16 decode modules (64 query heads per KV head), random KV / queries,
-    32 layers cycled (4 GiB working set)."""
+def decode_attn_fanout(peaks, shared_tokens=32767, modules=16, sessions=1, priv=1) -> dict:
+    """K6 at a fan-out shape: `sessions` shared contexts of `shared_tokens`,
+    each read by `modules` decode modules (4 query heads per KV head each)
+    with `priv` private tokens per row, random KV / queries, 32 layers cycled
+    (working set > L2). Default: the config-4 shape (32k x 16 modules)."""
     import torch
     from paper_2602_12029_b200 import _lib
     from paper_2602_12029_b200.model import (DecodeBatch, DecodeRow, KVCache, LlamaConfig,
                                              SessionSpec)
-    cfg = LlamaConfig.llama8b(max_pos=shared_tokens + 64)
+    cfg = LlamaConfig.llama8b(max_pos=shared_tokens + priv + 64)
     n_sh = (shared_tokens + 15) // 16
-    kv = KVCache(cfg, n_sh + modules)
+    n_pr = (priv + 15) // 16
+    per_sess = n_sh + modules * n_pr
+    kv = KVCache(cfg, sessions * per_sess)
     lib = _lib.load()
     s = torch.cuda.current_stream().cuda_stream
     _lib.check(lib.psk_init_normal_bf16(kv.data.data_ptr(), kv.data.numel(), 99, 1.0, s))
-    rows = [DecodeRow(module=m, session=0, first_token=0, pages=[n_sh + m]) for m in range(modules)]
-    b = DecodeBatch([SessionSpec(shared_len=shared_tokens, pages=list(range(n_sh)))], rows, modules)
-    q = torch.randn(modules, cfg.n_heads, cfg.head_dim, device="cuda").to(torch.bfloat16)
+    rows, sess = [], []
+    for si in range(sessions):
+        base = si * per_sess
+        sess.append(SessionSpec(shared_len=shared_tokens, pages=list(range(base, base + n_sh))))
+        rows += [DecodeRow(module=m, session=si, first_token=0,
+                           pages=list(range(base + n_sh + m * n_pr, base + n_sh + (m + 1) * n_pr)))
+                 for m in range(modules)]
+    b = DecodeBatch(sess, rows, modules)
+    b.t_priv_len.fill_(priv - 1)
+    R = sessions * modules
+    q = torch.randn(R, cfg.n_heads, cfg.head_dim, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)
     import ctypes
     from paper_2602_12029_b200.model import attn_splits
-    ns = attn_splits(n_sh + modules, cfg.n_kv_heads, torch.cuda.get_device_properties(0).multi_processor_count)
+    ns = attn_splits(per_sess, cfg.n_kv_heads * sessions,
+                     torch.cuda.get_device_properties(0).multi_processor_count)
     wsb = ctypes.c_int64()
     _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), cfg.n_kv_heads, ns, ctypes.byref(wsb)))
     ws = torch.zeros(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
@@ -290,14 +302,15 @@ def decode_attn_fanout(peaks, shared_tokens=32767, modules=16) -> dict:
                                        torch.cuda.current_stream().cuda_stream))
     dt = _time_launches(launch, 2 * cfg.n_layers)
     per_tok = 2 * cfg.n_kv_heads * cfg.head_dim * 2
-    nbytes = (shared_tokens + modules) * per_tok + 2 * modules * cfg.n_heads * cfg.head_dim * 2
+    nbytes = sessions * (shared_tokens + modules * priv) * per_tok + 2 * R * cfg.n_heads * cfg.head_dim * 2
     gbs = nbytes / dt / 1e9
     del kv
     torch.cuda.empty_cache()
-    return {"shape": f"1 session x {shared_tokens} shared tokens, {modules} modules",
+    return {"shape": f"{sessions} session(s) x {shared_tokens} shared tokens, {modules} modules, "
+                     f"{priv} private tokens/row",
             "achieved": round(gbs, 1), "unit": "GB/s", "frac": round(gbs / peaks["hbm"], 4),
             "bytes_per_launch": nbytes, "us_per_launch": round(dt * 1e6, 2),
-            "per_model_reread_bytes": modules * shared_tokens * per_tok}
+            "per_model_reread_bytes": sessions * modules * shared_tokens * per_tok}
 
 
 def pool_ops(n_tokens: int = PROMPT, reps: int = 50) -> dict:

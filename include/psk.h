@@ -188,6 +188,21 @@ int psk_gemv(const void* x, int32_t n_rows, int32_t K, const void* const* W,
              const int32_t* mod_row_start, int32_t n_mod, int32_t max_rows_per_mod,
              int32_t N, int32_t epilogue, void* out, void* stream);
 
+/* K5-TC: the same grouped GEMV on tcgen05 (M = 128 weight rows, N = rows of a
+ * module padded to 16/32/64, accumulator in TMEM), for 9..64 rows per module.
+ * W_host: HOST array of the n_mod (<= 16) weight pointers (TMA tensor maps
+ * are encoded per call; capture the call in a CUDA graph). K % 64 == 0,
+ * N % 128 == 0. The CTAs split the (128-row block, 64-column chunk) space
+ * evenly (stream-K) and reduce split blocks in a fixed order through the
+ * workspace. Replaces the same reference projections as psk_gemv. */
+int psk_gemv_tc(const void* x, int32_t n_rows, int32_t K, const void* const* W_host,
+                const int32_t* mod_row_start, int32_t n_mod, int32_t max_rows_per_mod,
+                int32_t N, int32_t epilogue, void* out, void* workspace, void* stream);
+/* Bytes of the psk_gemv_tc workspace (stream-K partials + flags); allocate
+ * once ZEROED and reuse for every call on the stream (the kernel leaves the
+ * flags zeroed). */
+int psk_gemv_tc_workspace(int64_t* bytes);
+
 /* RoPE (rotate-half, Llama) on q and k of the fused qkv rows (fp32
  * [n_rows][(nq+2*nkv)*hd]) at position sess_len[sess]+priv_len[r]; writes
  * q_rot bf16 [n_rows][nq][hd] and appends k,v (bf16) to the row's private

@@ -130,6 +130,18 @@ static inline void trace_disarm() {
   cudaMemcpyToSymbol(g_trace, &nul, sizeof(void*));
 }
 
+// 2^x on the MUFU (ex2.approx.ftz): 2^-inf = 0, no denormal range fix-up
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// bar.sync on a named barrier (id 1..15) among `threads` threads (multiple of 32)
+__device__ __forceinline__ void named_barrier_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

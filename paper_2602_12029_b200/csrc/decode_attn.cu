@@ -40,7 +40,10 @@ constexpr int THREADS = (CW + 1) * 32;  // + 1 TMA producer warp
 #ifndef PSK_ATTN_NST
 #define PSK_ATTN_NST 16
 #endif
-constexpr int NST = PSK_ATTN_NST;       // pipeline stages (1 page = K + V each, 8 KiB)
+constexpr int NST = PSK_ATTN_NST;
+#ifndef PSK_ATTN_EARLY
+#define PSK_ATTN_EARLY 0  // 1: the TMA producer streams shared pages before the PDL wait (measured slower: 4k x 8 sessions 36.7 -> 43.9 us)
+#endif       // pipeline stages (1 page = K + V each, 8 KiB)
 constexpr int TILE = PT * HD * 2;       // 4 KiB
 constexpr int STAGE = 2 * TILE;
 constexpr int GMAX = 64;
@@ -136,11 +139,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   };
   // page indices -> shared memory (tables are static within a step)
   for (int j = threadIdx.x; j < np && j < MAXP; j += THREADS) s_page[j] = page_of(k0 + j);
-  // everything above overlaps the producer of q / the new K,V (PDL)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  {
+  __syncthreads();
+  // Everything above overlaps the producer of q / the new K,V (PDL). The TMA
+  // producer streams the shared prompt pages without waiting: only q and the
+  // private pages (which hold this step's appended token) come from
+  // rope_append; no kernel of a decode step writes shared pages.
+  if (warp < CW) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint32_t qs = smem_u32(smem + OFF_Q);
-    for (int e = threadIdx.x; e < T * 16 * 16; e += THREADS) {
+    for (int e = threadIdx.x; e < T * 16 * 16; e += CW * 32) {
       const int g = e >> 4, c = e & 15;
       uint4 v = make_uint4(0, 0, 0, 0);
       if (g < G) {
@@ -150,16 +157,21 @@ __global__ void __launch_bounds__(THREADS, 1)
       asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(qs + swz256(g, c)), "r"(v.x),
                    "r"(v.y), "r"(v.z), "r"(v.w));
     }
+    named_barrier_sync(1, CW * 32);  // Q staged (consumer warps only)
   }
-  __syncthreads();
   trace_stamp(2);
 
   const uint32_t ring = smem_u32(smem);
   if (warp == CW) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
+      bool dep = false;
       for (int j = 0; j < np; ++j) {
         const int st = j % NST;
+        if (!dep && (k0 + j >= s_ps || !PSK_ATTN_EARLY)) {  // first private page: wait for rope_append
+          asm volatile("griddepcontrol.wait;" ::: "memory");
+          dep = true;
+        }
         tma::mbar_wait(&empty[st], ((j / NST) & 1) ^ 1);
         const int page = j < MAXP ? s_page[j] : page_of(k0 + j);
         const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
@@ -348,13 +360,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 // while the partial kernel drains and waits on griddepcontrol for its data.
 constexpr int MERGE_U = 32;
 __global__ void __launch_bounds__(HD) decode_attn_merge(const __grid_constant__ Params p) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");  // the o-proj GEMV may start streaming weights
   const int r = blockIdx.x, qh = blockIdx.y, d = threadIdx.x;
   const int nkv = p.kv.n_kv_heads;
   const int h = qh / p.grp;
+  // the row tables are static within a step: read them before the wait
   const int g = p.b.row_in_sess[r] * p.grp + qh % p.grp;
   const int64_t base = (int64_t)(p.b.row_sess[r] * nkv + h) * p.ns * GMAX + g;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");  // the o-proj GEMV may start streaming weights
   float M = -INFINITY, L = 0.f, acc = 0.f;
   for (int j0 = 0; j0 < p.ns; j0 += MERGE_U) {
     float mj[MERGE_U], lj[MERGE_U], oj[MERGE_U];
@@ -453,8 +466,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int sess = item / (p.ns * nkv);
   const int nr = p.b.sess_nrows[sess];
   const int G = nr * p.grp;
-  const int act = (G + 31) / 32;  // softmax warps with live rows, per group
+  // Query row g sits in TMEM lane 32 * (g / 16) + g % 16: 16 live lanes per
+  // lane quarter, so all four SM sub-partitions run softmax warps.
+  const int act = (G + 15) / 16;  // softmax warps with live rows, per group
 
+  trace_stamp(0);
   if (threadIdx.x < nr) {
     const int r = p.b.sess_rows[(int64_t)sess * p.b.max_rows_per_sess + threadIdx.x];
     s_rows[threadIdx.x] = r;
@@ -490,6 +506,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   if (warp == 1) umma::tmem_alloc(&s_tmem, 512);
   __syncthreads();
+  trace_stamp(1);
   const int total = s_total;
   const int k0 = (int)((int64_t)j_split * total / p.ns);
   const int k1 = (int)((int64_t)(j_split + 1) * total / p.ns);
@@ -512,11 +529,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     s_page[j] = page_of(j, info);
     s_info[j] = info;
   }
+  __syncthreads();
   const uint32_t tmem = s_tmem;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // q / new K,V come from rope_append
+  // The producer (warp 0) streams the shared prompt pages at once (no kernel
+  // of a decode step writes them); q and the private pages (this step's
+  // appended token) come from rope_append, so everyone else waits (PDL).
+  if (warp != 0) asm volatile("griddepcontrol.wait;" ::: "memory");
   // Q rows -> TMEM (lane = row, bf16 pairs), by the group-0 warps of live lanes
   if (warp >= 2 && warp < 6 && (warp & 3) < act) {
-    const int g = (warp & 3) * 32 + lane;
+    const int g = lane < 16 ? (warp & 3) * 16 + lane : G;
     const uint32_t tq = tmem + ((uint32_t)((warp & 3) * 32) << 16) + T_Q;
     const uint4* src = nullptr;
     if (g < G)
@@ -536,13 +557,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     umma::wait_st();
   }
-  umma::fence_before();
-  __syncthreads();
-  umma::fence_after();
+  if (warp != 0) {
+    umma::fence_before();
+    named_barrier_sync(1, THREADS - 32);  // Q in TMEM (all but the producer)
+    umma::fence_after();
+  }
+  trace_stamp(2);
 
   if (warp == 0) {
     if (lane < CPG) {
       const int pp = lane;
+      bool dep = false;
       for (int c = 0; c < nch; ++c) {
         const int st = c % NSTG;
         tma::mbar_wait(&empty[st], ((c / NSTG) & 1) ^ 1);
@@ -550,6 +575,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp(0xfu);
         const int j = c * CPG + pp;
         const int jj = j < np ? j : 0;  // past the end: any valid page, masked
+        if (!dep && (k0 + jj >= s_ps || !PSK_ATTN_EARLY)) {  // private page: wait for rope_append
+          asm volatile("griddepcontrol.wait;" ::: "memory");
+          dep = true;
+        }
         int info;
         const int page = jj < MAXP ? s_page[jj] : page_of(jj, info);
         const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
@@ -559,6 +588,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma::load_3d(&vmap, &full[st], kr + KBYTES + pp * TILE, 0, row_k + nkv * PT, 0);
       }
     }
+    trace_stamp(3);
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t ID_S = umma::idesc_bf16(128, KC, false), ID_PV = umma::idesc_bf16(128, HD, true);
@@ -601,119 +631,218 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if ((warp & 3) < act) {
-    const int u = (warp - 2) >> 2;   // softmax group
-    const int lq = (warp & 3) * 32;  // TMEM lane quarter
-    const int g = lq + lane;         // query row (TMEM lane)
-    const int ri = g < G ? g / p.grp : -1;
-    const uint32_t tl = tmem + ((uint32_t)lq << 16);
+    // Softmax warp: TMEM lane quarter q4, its 16 live lanes read with the
+    // 16-lane shapes so all 32 threads work: thread t owns query rows
+    // gA = 16 q4 + t/4 and gB = gA + 8, keys 8i + 2(t%4) + {0,1} of the
+    // chunk (i = 0..7); the 4 threads of a row reduce with two shuffles.
+    const int u = (warp - 2) >> 2;  // softmax group
+    const int q4 = warp & 3;        // TMEM lane quarter
+    const int t0 = lane & 3;
+    const int gA = 16 * q4 + (lane >> 2), gB = gA + 8;
+    const int riA = gA < G ? gA / p.grp : -2, riB = gB < G ? gB / p.grp : -2;
+    const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
     const uint32_t tS = tl + T_S + u * KC, tO = tl + T_O + u * HD, tP = tl + T_P + u * 32;
-    float m_used = -INFINITY, l = 0.f;
+    const float sc = p.scale_log2;
+    float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;  // m in scaled log2 units
     int it = 0;
     for (int c = u; c < nch; c += 2, ++it) {
       tma::mbar_wait(&s_full[u], it & 1);
       umma::fence_after();
-      uint32_t sr[KC];
-      umma::ld32_async(tS, sr);
-      umma::ld32_async(tS + 32, sr + 32);
+      uint32_t sr[32];
+      umma::ld16x256b_x8(tS, sr);
       umma::wait_ld();
       umma::fence_before();
       tma::mbar_arrive(&s_free[u]);  // S_u may be overwritten by S_u(c+2)
-      float mx = -INFINITY;
+      float xa[16], xb[16];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        xa[2 * i] = __uint_as_float(sr[4 * i]);
+        xa[2 * i + 1] = __uint_as_float(sr[4 * i + 1]);
+        xb[2 * i] = __uint_as_float(sr[4 * i + 2]);
+        xb[2 * i + 1] = __uint_as_float(sr[4 * i + 3]);
+      }
+      int info[CPG];
+      bool full = true;
 #pragma unroll
       for (int pp = 0; pp < CPG; ++pp) {
         const int j = c * CPG + pp;
-        int info = 0;
+        info[pp] = 0;
         if (j < np) {
-          if (j < MAXP) info = s_info[j];
-          else page_of(j, info);
+          if (j < MAXP) info[pp] = s_info[j];
+          else page_of(j, info[pp]);
         }
-        const int own = (info >> 8) - 1, lim = info & 0xff;
-        const bool page_ok = ri >= 0 && (own < 0 || own == ri);
+        full = full && info[pp] == PT;  // whole shared page
+      }
+      if (!full) {  // warp-uniform: partial / private / past-the-end pages
 #pragma unroll
-        for (int e = 0; e < PT; ++e) {
-          const float v = page_ok && e < lim ? __uint_as_float(sr[pp * PT + e]) * p.scale_log2 : -INFINITY;
-          sr[pp * PT + e] = __float_as_uint(v);
-          mx = fmaxf(mx, v);
+        for (int i = 0; i < 8; ++i) {
+          const int inf = info[i >> 1];
+          const int own = (inf >> 8) - 1, lim = inf & 0xff;
+          const bool okA = own < 0 || own == riA, okB = own < 0 || own == riB;
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int e = 8 * (i & 1) + 2 * t0 + b;
+            if (!(okA && e < lim)) xa[2 * i + b] = -INFINITY;
+            if (!(okB && e < lim)) xb[2 * i + b] = -INFINITY;
+          }
         }
       }
+      if (riA < 0) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) xa[k] = -INFINITY;
+      }
+      if (riB < 0) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) xb[k] = -INFINITY;
+      }
+      // tree max over the thread's 16 keys, then over the row's 4 threads
+      float ta[8], tb[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        ta[k] = fmaxf(xa[2 * k], xa[2 * k + 1]);
+        tb[k] = fmaxf(xb[2 * k], xb[2 * k + 1]);
+      }
+#pragma unroll
+      for (int w = 4; w >= 1; w >>= 1)
+#pragma unroll
+        for (int k = 0; k < w; ++k) {
+          ta[k] = fmaxf(ta[k], ta[k + w]);
+          tb[k] = fmaxf(tb[k], tb[k + w]);
+        }
+      float mxA = ta[0], mxB = tb[0];
+      mxA = fmaxf(mxA, __shfl_xor_sync(0xffffffffu, mxA, 1));
+      mxB = fmaxf(mxB, __shfl_xor_sync(0xffffffffu, mxB, 1));
+      mxA = fmaxf(mxA, __shfl_xor_sync(0xffffffffu, mxA, 2));
+      mxB = fmaxf(mxB, __shfl_xor_sync(0xffffffffu, mxB, 2));
+      mxA *= sc;
+      mxB *= sc;
       if (it > 0) tma::mbar_wait(&pv_done[u], (it - 1) & 1);  // P_u free, O_u settled
-      const bool grow = mx > m_used + RESCALE_LOG2 || (m_used == -INFINITY && mx > -INFINITY);
-      if (__any_sync(0xffffffffu, grow && it > 0)) {
+      const bool growA = mxA > mA + RESCALE_LOG2 || (mA == -INFINITY && mxA > -INFINITY);
+      const bool growB = mxB > mB + RESCALE_LOG2 || (mB == -INFINITY && mxB > -INFINITY);
+      if (__any_sync(0xffffffffu, (growA || growB) && it > 0)) {
         umma::fence_after();
-        const float alpha = grow ? exp2f(m_used - mx) : 1.f;
+        const float alA = growA ? exp2f(mA - mxA) : 1.f, alB = growB ? exp2f(mB - mxB) : 1.f;
 #pragma unroll 1
-        for (int q = 0; q < HD / 32; ++q) {
+        for (int hh = 0; hh < 2; ++hh) {
           uint32_t o[32];
-          umma::ld32_async(tO + q * 32, o);
+          umma::ld16x256b_x8(tO + hh * 64, o);
           umma::wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          umma::st32(tO + q * 32, o);
+          for (int i = 0; i < 8; ++i) {
+            o[4 * i] = __float_as_uint(__uint_as_float(o[4 * i]) * alA);
+            o[4 * i + 1] = __float_as_uint(__uint_as_float(o[4 * i + 1]) * alA);
+            o[4 * i + 2] = __float_as_uint(__uint_as_float(o[4 * i + 2]) * alB);
+            o[4 * i + 3] = __float_as_uint(__uint_as_float(o[4 * i + 3]) * alB);
+          }
+          umma::st16x256b_x8(tO + hh * 64, o);
         }
-        l *= alpha;
+        lA *= alA;
+        lB *= alB;
       }
-      if (grow) m_used = mx;
-      const float base = m_used == -INFINITY ? 0.f : m_used;
-      uint32_t pk[KC / 2];
+      if (growA) mA = mxA;
+      if (growB) mB = mxB;
+      const float bA = mA == -INFINITY ? 0.f : mA, bB = mB == -INFINITY ? 0.f : mB;
+      // p = 2^(s * scale - m): masked keys are -inf -> 0
+      uint32_t pk[16];
+      float sa[8], sb[8];
 #pragma unroll
-      for (int i = 0; i < KC / 2; ++i) {
-        const float p0 = exp2f(__uint_as_float(sr[2 * i]) - base);  // masked: exp2(-inf) = 0
-        const float p1 = exp2f(__uint_as_float(sr[2 * i + 1]) - base);
-        l += p0 + p1;
-        pk[i] = pack_bf16(p0, p1);
+      for (int i = 0; i < 8; ++i) {
+        const float a0 = fast_exp2(fmaf(xa[2 * i], sc, -bA)), a1 = fast_exp2(fmaf(xa[2 * i + 1], sc, -bA));
+        const float b0 = fast_exp2(fmaf(xb[2 * i], sc, -bB)), b1 = fast_exp2(fmaf(xb[2 * i + 1], sc, -bB));
+        sa[i] = a0 + a1;
+        sb[i] = b0 + b1;
+        pk[2 * i] = pack_bf16(a0, a1);      // row A, P column 4i + t0 = keys 8i + 2 t0 + {0,1}
+        pk[2 * i + 1] = pack_bf16(b0, b1);  // row B
       }
-      umma::st32(tP, pk);
+      umma::st16x128b_x8(tP, pk);
+#pragma unroll
+      for (int w = 4; w >= 1; w >>= 1)
+#pragma unroll
+        for (int k = 0; k < w; ++k) {
+          sa[k] += sa[k + w];
+          sb[k] += sb[k + w];
+        }
+      lA += sa[0];
+      lB += sb[0];
       umma::wait_st();
       umma::fence_before();
       tma::mbar_arrive(&p_full[u]);
     }
     if (it > 0) tma::mbar_wait(&pv_done[u], (it - 1) & 1);  // this group's last PV landed
     umma::fence_after();
+    lA += __shfl_xor_sync(0xffffffffu, lA, 1);
+    lB += __shfl_xor_sync(0xffffffffu, lB, 1);
+    lA += __shfl_xor_sync(0xffffffffu, lA, 2);
+    lB += __shfl_xor_sync(0xffffffffu, lB, 2);
     if (u == 1) {
-      s_ml[2 * g] = m_used;
-      s_ml[2 * g + 1] = l;
+      if (t0 == 0) {
+        s_ml[2 * gA] = mA;
+        s_ml[2 * gA + 1] = lA;
+        s_ml[2 * gB] = mB;
+        s_ml[2 * gB + 1] = lB;
+      }
       umma::fence_before();
       tma::mbar_arrive(g1_done);
     } else {
       tma::mbar_wait(g1_done, 0);
       umma::fence_after();
       const bool has1 = nch > 1;  // group 1 ran at least one chunk (O_1 written)
-      const float m1 = s_ml[2 * g], l1 = s_ml[2 * g + 1];
-      const float M = fmaxf(m_used, m1);
-      const float Mr = M == -INFINITY ? 0.f : M;
-      const float a0 = m_used == -INFINITY ? 0.f : exp2f(m_used - Mr);
-      const float a1 = m1 == -INFINITY ? 0.f : exp2f(m1 - Mr);
+      float a0[2], a1[2];
+      const float m0r[2] = {mA, mB}, l0r[2] = {lA, lB};
+      float Mr[2], Lr[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int g = r ? gB : gA;
+        const float m1 = s_ml[2 * g], l1 = s_ml[2 * g + 1];
+        const float M = fmaxf(m0r[r], m1);
+        const float Mx = M == -INFINITY ? 0.f : M;
+        a0[r] = m0r[r] == -INFINITY ? 0.f : exp2f(m0r[r] - Mx);
+        a1[r] = (has1 && m1 != -INFINITY) ? exp2f(m1 - Mx) : 0.f;
+        Mr[r] = M;
+        Lr[r] = l0r[r] * a0[r] + (has1 ? l1 * a1[r] : 0.f);
+      }
       const int64_t base = (int64_t)item * GMAX;
 #pragma unroll 1
-      for (int q = 0; q < HD / 32; ++q) {
+      for (int hh = 0; hh < 2; ++hh) {
         uint32_t o0[32], o1[32];
-        umma::ld32_async(tO + q * 32, o0);
-        umma::ld32_async(tO + HD + q * 32, o1);  // O_1 sits HD columns after O_0
+        umma::ld16x256b_x8(tO + hh * 64, o0);
+        umma::ld16x256b_x8(tO + HD + hh * 64, o1);  // O_1 sits HD columns after O_0
         umma::wait_ld();
-        if (g < G) {
-          float4* dst = reinterpret_cast<float4*>(p.po + (base + g) * HD + q * 32);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int g = r ? gB : gA;
+          if (g >= G) continue;
+          float* dst = p.po + (base + g) * HD + hh * 64 + 2 * t0;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            float f[4];
+            float f[2];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float x0 = a0 != 0.f ? a0 * __uint_as_float(o0[4 * i + e]) : 0.f;
-              const float x1 = (has1 && a1 != 0.f) ? a1 * __uint_as_float(o1[4 * i + e]) : 0.f;
+            for (int e = 0; e < 2; ++e) {
+              const int k = 4 * i + 2 * r + e;
+              const float x0 = a0[r] != 0.f ? a0[r] * __uint_as_float(o0[k]) : 0.f;
+              const float x1 = a1[r] != 0.f ? a1[r] * __uint_as_float(o1[k]) : 0.f;
               f[e] = x0 + x1;
             }
-            dst[i] = make_float4(f[0], f[1], f[2], f[3]);
+            *reinterpret_cast<float2*>(dst + 8 * i) = make_float2(f[0], f[1]);
           }
         }
       }
-      if (g < G) {
-        p.pm[base + g] = M;
-        p.pl[base + g] = l * a0 + l1 * a1;
+      if (t0 == 0) {
+        if (gA < G) {
+          p.pm[base + gA] = Mr[0];
+          p.pl[base + gA] = Lr[0];
+        }
+        if (gB < G) {
+          p.pm[base + gB] = Mr[1];
+          p.pl[base + gB] = Lr[1];
+        }
       }
     }
   }
   asm volatile("griddepcontrol.launch_dependents;");
   umma::fence_before();
   __syncthreads();
+  trace_stamp(4);
   if (warp == 1) {
     umma::fence_after();
     umma::tmem_dealloc(tmem, 512);
@@ -878,7 +1007,9 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
     PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_partial, map, p));
   }
   if (tr) {
-    static const char* names[] = {"entry", "prologue", "staged", "loop-done", "folded"};
+    static const char* names_h[] = {"entry", "prologue", "staged", "loop-done", "folded"};
+    static const char* names_t[] = {"entry", "tmem+bars", "q-staged", "tma-issued", "done"};
+    const char* const* names = use_tc ? names_t : names_h;
     psk::trace_report("decode_attn", (int)items, 5, names);
     psk::trace_disarm();
   }

@@ -1,0 +1,436 @@
+// K5-TC — grouped decode GEMV on the 5th-gen tensor cores, for 9..64 decode
+// rows per module (the co-batched fan-out regime: many sessions x modules).
+//
+// Same contract as psk_gemv (gemv.cu): for each module i and each of its rows
+// r, y[r, n] = sum_k x[r, k] * W_i[n, k], fused epilogues. At <= 8 rows per
+// module the mma.sync kernel streams weights at the HBM roofline; above that
+// its register-resident x fragments and cross-warp reductions make it
+// compute/L2-bound (16 rows: ~1.2x, 32 rows: ~2.7x the weight-stream time).
+// Here the skinny GEMM D[128 weight rows, M rows] = W_blk . X^T runs as
+// tcgen05.mma M=128, N=MN (16/32/64), K=16 with the accumulator in TMEM: no
+// cross-warp reduction, x is staged once per k-chunk by TMA, and the kernel
+// is a pure TMA weight stream again.
+//
+// Persistent, one CTA per SM, 6 warps:
+//   warp 0   TMA producer: per 64-column k-chunk one 128x64 weight box
+//            (16 KiB, SW128) + one MNx64 x box, into a ~200 KiB ring; the
+//            weight boxes of the first ring fill are issued before the PDL
+//            wait (weights never depend on the previous kernel)
+//   warp 1   MMA issuer (one lane): 4 x tcgen05.mma per chunk into one of two
+//            TMEM accumulators (double-buffered across segments)
+//   warps 2-5  epilogue: tcgen05.ld 32x32b (thread = weight row, one column
+//            per activation row), fused store / residual add / SiLU*mul
+// Work unit = (module, 128-row weight block) x K; the CTAs split the
+// (unit, 64-column chunk) space stream-K style (below).
+//
+// Replaces the per-module dense projections of the reference decode forward
+// (frontend/src/model.ts:298-306 q/k/v, :318 o-proj, :322-323 MLP, :334
+// logits), for all decode modules of a step in one launch.
+#include "common.cuh"
+#include "tma.cuh"
+#include "umma.cuh"
+
+namespace psk {
+namespace gemv_tc {
+
+constexpr int BN = 128;             // weight rows per unit (UMMA M)
+constexpr int BK = 64;              // columns per k-chunk (one 128 B swizzle atom)
+constexpr int A_BYTES = BN * BK * 2;  // 16 KiB
+constexpr int THREADS = 192;
+constexpr int MAXMOD = 16;
+constexpr int RING_BYTES = 200 * 1024;
+
+template <int MN>
+struct Cfg {
+  static constexpr int B_BYTES = MN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = RING_BYTES / STAGE;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = 2 * MN < 32 ? 32 : 2 * MN;
+  static_assert(STAGE % 1024 == 0, "SW128 tiles need 1 KiB alignment");
+};
+
+struct Maps {
+  CUtensorMap w[MAXMOD];  // per-module weight [N][K], box {64, 128}
+  CUtensorMap x;          // activations [n_rows][K], box {64, MN}
+};
+
+__device__ __forceinline__ void tmem_ld32_cols(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  umma::ld32_async(taddr, r);
+  umma::wait_ld();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld16_cols(uint32_t taddr, float* v) { umma::ld16(taddr, v); }
+
+// Stream-K work split: the (unit, k-chunk) space is cut into gridDim.x equal
+// runs of chunks, so every CTA streams the same number of weight bytes
+// whatever the unit count (o/down: 128 units, qkv: 192, gate/up: 896 on 148
+// SMs). A run is a sequence of segments, one per unit it touches. The segment
+// holding a unit's chunk 0 is the unit's owner (it is the run's LAST segment
+// when the unit continues into the next runs); a segment without chunk 0 is
+// a contributor and is always the run's FIRST segment, so each CTA has at
+// most one contributor segment (one fp32 partial slot [MN][128] + a flag).
+// Contributors publish early (start of their run); the owner reaches the
+// unit at the end of its run, sums its accumulator and the partials of the
+// following CTAs in a fixed order (bit-reproducible), then runs the fused
+// epilogue. Waits only point to higher CTAs, whose first segments never
+// wait, and all CTAs are co-resident (grid <= SMs): no deadlock.
+struct Seg {
+  int unit, k0, k1;  // chunks [k0, k1) of `unit`
+};
+
+__device__ __forceinline__ int run_begin(int cta, int64_t total, int grid) {
+  return (int)((int64_t)cta * total / grid);
+}
+
+template <int MN, int EPI>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemv_tc_kernel(const __grid_constant__ Maps maps, const int32_t* __restrict__ mrs, int n_mod, int N, int K,
+                   void* __restrict__ out, float* __restrict__ part, int* __restrict__ flags) {
+  using C = Cfg<MN>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = N / BN;
+  const int kcn = (K + BK - 1) / BK;
+  const int64_t total = (int64_t)n_mod * nb * kcn;
+  const int cta = blockIdx.x, grid = gridDim.x;
+  const int c0 = run_begin(cta, total, grid), c1 = run_begin(cta + 1, total, grid);
+  // segment iterator over [c0, c1)
+  auto seg_at = [&](int c) -> Seg {
+    const int unit = c / kcn;
+    const int k0 = c % kcn;
+    const int k1 = min(kcn, k0 + (c1 - c));
+    return Seg{unit, k0, k1};
+  };
+  auto live = [&](int unit) -> bool {
+    const int mod = unit / nb;
+    return mrs[mod + 1] > mrs[mod];
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tma::mbar_init(&tfull[s], 1);
+      tma::mbar_init(&tempty[s], 128);
+    }
+    tma::fence_mbar_init();
+  }
+  if (warp == 1) umma::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  pdl_trigger();  // the next kernel may start streaming its weights as our CTAs drain
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int m = 0; m < n_mod && m < MAXMOD; ++m) tma::prefetch_map(&maps.w[m]);
+      tma::prefetch_map(&maps.x);
+      // x rows come from the previous kernel: the first ring fill issues the
+      // weight boxes at once and the x boxes after the PDL wait
+      int pend_k[C::STAGES], pend_row[C::STAGES];
+      int npend = 0;
+      bool waited = false;
+      int j = 0;
+      for (int c = c0; c < c1;) {
+        const Seg sg = seg_at(c);
+        c += sg.k1 - sg.k0;
+        if (!live(sg.unit)) continue;  // module without rows this step
+        const int mod = sg.unit / nb, blk = sg.unit % nb;
+        const int xb = mrs[mod];
+        for (int kc = sg.k0; kc < sg.k1; ++kc, ++j) {
+          const int s = j % C::STAGES;
+          if (!waited && j == C::STAGES) {
+            pdl_wait();
+            for (int i = 0; i < npend; ++i)
+              tma::load_2d(&maps.x, &full[i], smem + i * C::STAGE + A_BYTES, pend_k[i], pend_row[i]);
+            waited = true;
+          }
+          tma::mbar_wait(&empty[s], ((j / C::STAGES) & 1) ^ 1);
+          tma::mbar_expect_tx(&full[s], C::STAGE);
+          unsigned char* st = smem + s * C::STAGE;
+          tma::load_2d(&maps.w[mod], &full[s], st, kc * BK, blk * BN);
+          if (waited) {
+            tma::load_2d(&maps.x, &full[s], st + A_BYTES, kc * BK, xb);
+          } else {
+            pend_k[npend] = kc * BK;
+            pend_row[npend] = xb;
+            ++npend;
+          }
+        }
+      }
+      if (!waited) {
+        pdl_wait();
+        for (int i = 0; i < npend; ++i)
+          tma::load_2d(&maps.x, &full[i], smem + i * C::STAGE + A_BYTES, pend_k[i], pend_row[i]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma::idesc_bf16(BN, MN, false);
+      int j = 0, it = 0;
+      for (int c = c0; c < c1;) {
+        const Seg sg = seg_at(c);
+        c += sg.k1 - sg.k0;
+        if (!live(sg.unit)) continue;
+        const int acc = it & 1;
+        tma::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        umma::fence_after();
+        const uint32_t tacc = tmem + acc * MN;
+        for (int kc = sg.k0; kc < sg.k1; ++kc, ++j) {
+          const int s = j % C::STAGES;
+          tma::mbar_wait(&full[s], (j / C::STAGES) & 1);
+          umma::fence_after();
+          const uint32_t a = tma::sa(smem + s * C::STAGE);
+          const uint64_t da = umma::desc_k_sw128(a), db = umma::desc_k_sw128(a + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma::mma(tacc, da + 2 * k, db + 2 * k, idesc, (kc != sg.k0 || k != 0) ? 1u : 0u);
+          umma::commit(&empty[s]);
+        }
+        umma::commit(&tfull[acc]);
+        ++it;
+      }
+    }
+  } else {
+    // epilogue: warp w reads TMEM lane quarter w % 4 = weight rows 32q..32q+31
+    const int q = warp & 3;
+    const int r = q * 32 + lane;  // weight row within the unit
+    pdl_wait();                   // out (residual stream) is written by earlier kernels
+    int it = 0;
+    for (int c = c0; c < c1;) {
+      const Seg sg = seg_at(c);
+      c += sg.k1 - sg.k0;
+      if (!live(sg.unit)) continue;
+      const int mod = sg.unit / nb, blk = sg.unit % nb;
+      const int xb = mrs[mod], M = mrs[mod + 1] - xb;
+      const bool owner = sg.k0 == 0;
+      const int n = blk * BN + r;
+      float v[MN];
+      // residual prefetch: its latency overlaps this segment's MMAs
+      if (EPI == PSK_EPI_RESID_ADD && owner) {
+#pragma unroll
+        for (int m = 0; m < MN; ++m)
+          v[m] = m < M ? reinterpret_cast<const float*>(out)[(int64_t)(xb + m) * N + n] : 0.f;
+      } else {
+#pragma unroll
+        for (int m = 0; m < MN; ++m) v[m] = 0.f;
+      }
+      const int acc = it & 1;
+      tma::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      umma::fence_after();
+      {
+        const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + acc * MN;
+        float a[MN];
+        if (MN == 16) {
+          umma::ld16(tacc, a);
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < MN / 32; ++cc) {
+            uint32_t t[32];
+            umma::ld32_async(tacc + cc * 32, t);
+            umma::wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) a[cc * 32 + i] = __uint_as_float(t[i]);
+          }
+        }
+        umma::fence_before();
+        tma::mbar_arrive(&tempty[acc]);  // the MMA of segment it+2 may overwrite it
+        if (!owner) {
+          // contributor (this run's first segment): publish the fp32 partial
+          float* slot = part + (int64_t)cta * MN * BN;
+#pragma unroll
+          for (int m = 0; m < MN; ++m) slot[m * BN + r] = a[m];
+          __threadfence();
+          named_barrier_sync(2, 128);
+          if (threadIdx.x == 64) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + cta), "r"(1) : "memory");
+          ++it;
+          continue;
+        }
+        // owner: own accumulator + partials of the following runs, fixed order
+        const int64_t unit_end = (int64_t)(sg.unit + 1) * kcn;
+        if (sg.k1 < kcn) {
+          for (int j2 = cta + 1; j2 < grid && run_begin(j2, total, grid) < unit_end; ++j2) {
+            if (threadIdx.x == 64) {
+              int f = 0;
+              do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(flags + j2) : "memory");
+              } while (f == 0);
+              flags[j2] = 0;  // consumed: ready for the next launch
+            }
+            named_barrier_sync(2, 128);
+            const float* slot = part + (int64_t)j2 * MN * BN;
+#pragma unroll
+            for (int m = 0; m < MN; ++m) a[m] += __ldcg(slot + m * BN + r);
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < MN; ++m) v[m] += a[m];
+      }
+      if (EPI == PSK_EPI_SILU_MUL) {
+        // rows interleaved [gate 8 | up 8]: the up row of gate row n is n + 8,
+        // held by lane + 8 of this warp
+        const bool gate = (r & 15) < 8;
+        const int o = (blk * BN + (r & ~15)) / 2 + (r & 7);
+#pragma unroll
+        for (int m = 0; m < MN; ++m) {
+          const float up = __shfl_down_sync(0xffffffffu, v[m], 8);
+          if (gate && m < M) {
+            const float g = v[m];
+            reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)(xb + m) * (N / 2) + o] =
+                f2bf(g / (1.f + __expf(-g)) * up);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < MN; ++m) {
+          if (m >= M) break;
+          const int64_t o = (int64_t)(xb + m) * N + n;
+          if (EPI == PSK_EPI_STORE_BF16) reinterpret_cast<__nv_bfloat16*>(out)[o] = f2bf(v[m]);
+          if (EPI == PSK_EPI_STORE_F32 || EPI == PSK_EPI_RESID_ADD) reinterpret_cast<float*>(out)[o] = v[m];
+        }
+      }
+      ++it;
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    umma::fence_after();
+    umma::tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------ host side --
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// bf16 [rows][cols] row-major, [box_rows x 64] SW128 boxes
+static int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int box_rows,
+                    CUtensorMapL2promotion promo) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return PSK_ECUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("psk_gemv_tc: cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return PSK_ECUDA;
+  }
+  return PSK_OK;
+}
+
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+constexpr int FLAG_BYTES = 4096;  // one int per CTA (<= 1024 SMs)
+
+template <int MN, int EPI>
+static int launch(const void* x, int n_rows, int K, const void* const* W_host, const int32_t* mrs, int n_mod,
+                  int N, void* out, void* ws, cudaStream_t s) {
+  Maps maps;
+  for (int m = 0; m < n_mod; ++m) {
+    int rc = make_map(&maps.w[m], W_host[m], N, K, BN, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (rc) return rc;
+  }
+  int rc = make_map(&maps.x, x, n_rows, K, MN, CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
+  if (rc) return rc;
+  auto k = gemv_tc_kernel<MN, EPI>;
+  static bool attr = false;
+  if (!attr) {
+    PSK_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<MN>::SMEM));
+    attr = true;
+  }
+  const int sms = sm_count();
+  const int64_t chunks = (int64_t)n_mod * (N / BN) * ((K + BK - 1) / BK);
+  const int grid = chunks < sms ? (int)chunks : sms;
+  int* flags = reinterpret_cast<int*>(ws);
+  float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + FLAG_BYTES);
+  PSK_CUDA_TRY(psk::launch_pdl(k, dim3(grid), dim3(THREADS), (size_t)Cfg<MN>::SMEM, s, maps, mrs, n_mod, N, K,
+                               out, part, flags));
+  PSK_LAUNCH_CHECK();
+  return PSK_OK;
+}
+
+template <int MN>
+static int dispatch(int epi, const void* x, int n_rows, int K, const void* const* W, const int32_t* mrs,
+                    int n_mod, int N, void* out, void* ws, cudaStream_t s) {
+  switch (epi) {
+    case PSK_EPI_STORE_BF16: return launch<MN, PSK_EPI_STORE_BF16>(x, n_rows, K, W, mrs, n_mod, N, out, ws, s);
+    case PSK_EPI_STORE_F32: return launch<MN, PSK_EPI_STORE_F32>(x, n_rows, K, W, mrs, n_mod, N, out, ws, s);
+    case PSK_EPI_RESID_ADD: return launch<MN, PSK_EPI_RESID_ADD>(x, n_rows, K, W, mrs, n_mod, N, out, ws, s);
+    case PSK_EPI_SILU_MUL: return launch<MN, PSK_EPI_SILU_MUL>(x, n_rows, K, W, mrs, n_mod, N, out, ws, s);
+  }
+  set_error("psk_gemv_tc: unknown epilogue %d", epi);
+  return PSK_EINVAL;
+}
+
+}  // namespace gemv_tc
+}  // namespace psk
+
+extern "C" int psk_gemv_tc_workspace(int64_t* bytes) {
+  PSK_CHECK_ARG(bytes != nullptr, "psk_gemv_tc_workspace: null out");
+  using namespace psk::gemv_tc;
+  *bytes = FLAG_BYTES + (int64_t)sm_count() * 64 * BN * 4;
+  return PSK_OK;
+}
+
+extern "C" int psk_gemv_tc(const void* x, int32_t n_rows, int32_t K, const void* const* W_host,
+                           const int32_t* mod_row_start, int32_t n_mod, int32_t max_rows_per_mod, int32_t N,
+                           int32_t epilogue, void* out, void* workspace, void* stream) {
+  using namespace psk::gemv_tc;
+  PSK_CHECK_ARG(x && W_host && mod_row_start && out && workspace && n_rows >= 0 && K > 0 && K % 64 == 0 &&
+                    n_mod > 0 && n_mod <= MAXMOD,
+                "psk_gemv_tc: bad args (K %% 64 == 0, 1..%d modules, workspace)", MAXMOD);
+  PSK_CHECK_ARG(N > 0 && N % BN == 0, "psk_gemv_tc: N must be a positive multiple of %d", BN);
+  const int maxm = max_rows_per_mod > 0 ? max_rows_per_mod : n_rows;
+  if (n_rows == 0) return PSK_OK;
+  cudaStream_t s = psk::as_stream(stream);
+  if (maxm <= 16) return dispatch<16>(epilogue, x, n_rows, K, W_host, mod_row_start, n_mod, N, out, workspace, s);
+  if (maxm <= 32) return dispatch<32>(epilogue, x, n_rows, K, W_host, mod_row_start, n_mod, N, out, workspace, s);
+  if (maxm <= 64) return dispatch<64>(epilogue, x, n_rows, K, W_host, mod_row_start, n_mod, N, out, workspace, s);
+  psk::set_error("psk_gemv_tc: more than 64 rows per module (%d)", maxm);
+  return PSK_EINVAL;
+}

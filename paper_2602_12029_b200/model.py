@@ -321,6 +321,9 @@ class DecodeBatch:
         self.reset()
 
 
+GEMV_MMA_MAX_ROWS = 8  # rows per module up to which the mma.sync GEMV (K5) beats K5-TC
+
+
 def attn_splits(max_pages: int, n_groups: int, sms: int = 148) -> int:
     """Split-KV factor for K6: one CTA per SM over the (session, KV head)
     groups, at least ~4 pages per split, at most 512 splits."""
@@ -353,6 +356,17 @@ class DecodeRunner:
         self.p_wdown = [ptrs([m.wdown[l] for m in mods]) for l in range(L)]
         self.p_final_norm = ptrs([m.final_norm for m in mods])
         self.p_head = ptrs([m.head for m in mods])
+        # > 8 rows per module: the tcgen05 GEMV (K5-TC) takes host pointer arrays
+        self.use_tc_gemv = batch.max_rpm > GEMV_MMA_MAX_ROWS
+        hptrs = lambda ts: (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])  # noqa: E731
+        self.h_wqkv = [hptrs([m.wqkv[l] for m in mods]) for l in range(L)]
+        self.h_wo = [hptrs([m.wo[l] for m in mods]) for l in range(L)]
+        self.h_wgu = [hptrs([m.wgu[l] for m in mods]) for l in range(L)]
+        self.h_wdown = [hptrs([m.wdown[l] for m in mods]) for l in range(L)]
+        self.h_head = hptrs([m.head for m in mods])
+        gwb = C.c_int64()
+        _lib.check(self.lib.psk_gemv_tc_workspace(C.byref(gwb)))
+        self.gemv_ws = torch.zeros(gwb.value, dtype=torch.uint8, device=dev)  # flags start (and end) at 0
         self.weight_bytes_per_step = sum(m.layer_bytes() for m in mods)
         R, d = batch.n_rows, cfg.d_model
         f32, bf = torch.float32, torch.bfloat16
@@ -376,36 +390,41 @@ class DecodeRunner:
         self.graph: torch.cuda.CUDAGraph | None = None
         self.launches_per_step = 1 + L * 9 + 3
 
+    def _gemv(self, x, K: int, p_dev, p_host, N: int, epi: int, out, s: int) -> None:
+        """K5 (mma.sync, <= 8 rows per module) or K5-TC (tcgen05, 9..64)."""
+        b = self.b
+        if self.use_tc_gemv:
+            _lib.check(self.lib.psk_gemv_tc(_ptr(x), b.n_rows, K, p_host, _ptr(b.t_mrs), b.n_mod, b.max_rpm, N,
+                                            epi, _ptr(out), _ptr(self.gemv_ws), s))
+        else:
+            _lib.check(self.lib.psk_gemv(_ptr(x), b.n_rows, K, _ptr(p_dev), _ptr(b.t_mrs), b.n_mod, b.max_rpm, N,
+                                         epi, _ptr(out), s))
+
     # -- one step, eager ----------------------------------------------------
     def _step(self, s: int) -> None:
         lib, cfg, b = self.lib, self.cfg, self.b
         bc = C.byref(b.c)
         R, d = b.n_rows, cfg.d_model
         kvl = self.kv.layout()
-        mrs = _ptr(b.t_mrs)
         chk = _lib.check
+        gemv = self._gemv
         chk(lib.psk_embed_rows(bc, _ptr(self.p_embed), d, _ptr(self.h), s))
         for l in range(cfg.n_layers):
             chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_attn_norm[l]), _ptr(b.t_row_mod),
                                      C.c_float(cfg.norm_eps), _ptr(self.xn), s))
-            chk(lib.psk_gemv(_ptr(self.xn), R, d, _ptr(self.p_wqkv[l]), mrs, b.n_mod, b.max_rpm, cfg.qkv_dim,
-                             1, _ptr(self.qkv), s))
+            gemv(self.xn, d, self.p_wqkv[l], self.h_wqkv[l], cfg.qkv_dim, 1, self.qkv, s)
             chk(lib.psk_rope_append(bc, _ptr(self.qkv), cfg.n_heads, _ptr(self.rope), l, kvl,
                                     _ptr(self.q_rot), s))
             chk(lib.psk_decode_attn(bc, _ptr(self.q_rot), cfg.n_heads, l, kvl, self.splits,
                                     _ptr(self.ws), _ptr(self.attn), s))
-            chk(lib.psk_gemv(_ptr(self.attn), R, cfg.n_heads * cfg.head_dim, _ptr(self.p_wo[l]), mrs,
-                             b.n_mod, b.max_rpm, d, 2, _ptr(self.h), s))
+            gemv(self.attn, cfg.n_heads * cfg.head_dim, self.p_wo[l], self.h_wo[l], d, 2, self.h, s)
             chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_mlp_norm[l]), _ptr(b.t_row_mod),
                                      C.c_float(cfg.norm_eps), _ptr(self.xn), s))
-            chk(lib.psk_gemv(_ptr(self.xn), R, d, _ptr(self.p_wgu[l]), mrs, b.n_mod, b.max_rpm, 2 * cfg.ffn, 3,
-                             _ptr(self.act), s))
-            chk(lib.psk_gemv(_ptr(self.act), R, cfg.ffn, _ptr(self.p_wdown[l]), mrs, b.n_mod, b.max_rpm, d, 2,
-                             _ptr(self.h), s))
+            gemv(self.xn, d, self.p_wgu[l], self.h_wgu[l], 2 * cfg.ffn, 3, self.act, s)
+            gemv(self.act, cfg.ffn, self.p_wdown[l], self.h_wdown[l], d, 2, self.h, s)
         chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_final_norm), _ptr(b.t_row_mod),
                                  C.c_float(cfg.norm_eps), _ptr(self.xn), s))
-        chk(lib.psk_gemv(_ptr(self.xn), R, d, _ptr(self.p_head), mrs, b.n_mod, b.max_rpm, cfg.vocab, 1,
-                         _ptr(self.logits), s))
+        gemv(self.xn, d, self.p_head, self.h_head, cfg.vocab, 1, self.logits, s)
         chk(lib.psk_argmax_advance(bc, _ptr(self.logits), cfg.vocab, _ptr(self.out_tokens),
                                    self.max_new, s))
 

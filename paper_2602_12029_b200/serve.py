@@ -53,6 +53,7 @@ class RequestRecord:
     out_tokens: int = 0
     matched: int = 0
     prefilled: int = 0
+    failed: bool = False
 
 
 @dataclass
@@ -149,7 +150,12 @@ class AgentServer:
         ns = self.router.prefill_namespace(req.rec.model_id)
         n = len(req.ctx)
         m, chain = pool.longest_prefix_match(ns, req.ctx, now_us)
-        new = pool.insert(ns, req.ctx, now_us)
+        try:
+            new = pool.insert(ns, req.ctx, now_us)
+        except pool.CapacityError:
+            # cluster.py:348-350: release the matched pins and fail the request
+            pool.release(chain)
+            return None
         pool.pin(new, now_us)
         base = pool.page_base
         pages = [base + s for s in chain.slots.tolist()] + [base + s for s in new.slots.tolist()]
@@ -161,8 +167,25 @@ class AgentServer:
         runner = self.prefillers[0 if self.base is not None else req.model_idx]
         pt = torch.tensor(pages, dtype=torch.int32, device=self.dev)
         if n > pos0:
+            ev = self._events("prefill")
             runner.run(self._vocab_ids(req.ctx[pos0:]), pos0, pt)
+            ev[1].record()
         return [(pool, chain), (pool, new)], pages, m, n - pos0, row
+
+    def _events(self, kind: str):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        self._ev.append((kind, a, b))
+        return a, b
+
+    def gpu_time(self) -> dict:
+        """Device time spent in prefill forwards and decode steps over the
+        last run() (CUDA events around each launch sequence)."""
+        out = {"prefill_ms": 0.0, "decode_ms": 0.0, "prefill_calls": 0, "decode_steps": 0}
+        for kind, a, b in self._ev:
+            out[kind + "_ms"] += a.elapsed_time(b)
+            out["prefill_calls" if kind == "prefill" else "decode_steps"] += 1
+        return {k: round(v, 1) if isinstance(v, float) else v for k, v in out.items()}
 
     # -- serving -------------------------------------------------------------
 
@@ -171,6 +194,7 @@ class AgentServer:
         """Serve the workload in real time (arrival times scaled by
         time_scale). Returns one record per request."""
         self.runner.capture()
+        self._ev = []
         st = torch.cuda.current_stream()
         records: list[RequestRecord] = []
         arrivals = deque(sorted(sessions, key=lambda s: s.arrival_time))
@@ -223,7 +247,18 @@ class AgentServer:
                 if self._row_of_module(req.model_idx) is None:
                     prefill_q.append(req)
                     continue
-                held, pages, m, pre, row = self._prefill(req, int(now_us()))
+                got = self._prefill(req, int(now_us()))
+                progressed = True
+                if got is None:
+                    # cluster.py:480-490: the request and its session fail
+                    req.rec.failed = True
+                    done_sessions += 1
+                    active -= 1
+                    if waiting_admission:
+                        active += 1
+                        activate(waiting_admission.popleft())
+                    continue
+                held, pages, m, pre, row = got
                 req.rec.matched, req.rec.prefilled = m, pre
                 r = self.rows[row]
                 r.req, r.steps, r.held = req, 0, held
@@ -235,7 +270,9 @@ class AgentServer:
                 progressed = True
             busy = [r for r in self.rows if r.req is not None]
             if busy:
+                ev = self._events("decode")
                 self.runner.graph.replay()
+                ev[1].record()
                 t_step = now_us()
                 for idx, r in enumerate(self.rows):
                     if r.req is None:
@@ -279,8 +316,9 @@ def summarize(records: list[RequestRecord], warmup_fraction: float = 0.1) -> dic
     """metrics.py:22-76 definitions (nearest-rank p95, post-warmup window),
     plus req/s over the same window."""
     done = [r for r in records if r.done_us is not None]
+    failed = sum(1 for r in records if r.failed)
     if not done:
-        return {"completed": 0}
+        return {"completed": 0, "failed": failed}
     t_end = max(r.done_us for r in done)
     w0 = warmup_fraction * t_end
     win = [r for r in done if r.done_us >= w0]
@@ -292,7 +330,7 @@ def summarize(records: list[RequestRecord], warmup_fraction: float = 0.1) -> dic
         return v[max(math.ceil(0.95 * len(v)), 1) - 1]
 
     lookup = sum(r.matched + r.prefilled for r in done)
-    return {"completed": len(done), "req_per_s": len(win) / window_s,
+    return {"completed": len(done), "failed": failed, "req_per_s": len(win) / window_s,
             "tok_per_s": sum(r.out_tokens for r in win) / window_s,
             "p95_e2e_ms": p95(e2e) / 1e3, "p95_ttft_ms": p95(ttft) / 1e3 if ttft else None,
             "prefill_tokens": sum(r.prefilled for r in done),

@@ -141,3 +141,39 @@ def test_8b_shape_two_layer_truncation():
     prompt = rng.integers(0, cfg.vocab, 200).tolist()
     _, res = _run_case(cfg, [prompt], [(m, 0) for m in range(4)], max_new=8)
     assert sum(f for _, _, f in res) <= 2
+
+
+def test_tiny_twelve_rows_per_module_tc_gemv():
+    """12 sessions x 2 modules = 12 rows per module: the decode GEMVs run on
+    the tcgen05 kernel (K5-TC, MN = 16)."""
+    from paper_2602_12029_b200.model import LlamaConfig
+    cfg = LlamaConfig.tiny()
+    rng = np.random.default_rng(4)
+    prompts = [rng.integers(0, cfg.vocab, int(n)).tolist() for n in rng.integers(5, 120, 12)]
+    attach = [(m, s) for s in range(12) for m in range(2)]
+    runner, res = _run_case(cfg, prompts, attach, max_new=6)
+    assert runner.use_tc_gemv
+    assert sum(f for _, _, f in res) <= 4
+
+
+def test_tiny_forty_rows_one_module_tc_gemv():
+    """40 sessions on one decode module (K5-TC with MN = 64)."""
+    from paper_2602_12029_b200.model import LlamaConfig
+    cfg = LlamaConfig.tiny()
+    rng = np.random.default_rng(5)
+    prompts = [rng.integers(0, cfg.vocab, int(n)).tolist() for n in rng.integers(3, 50, 40)]
+    runner, res = _run_case(cfg, prompts, [(0, s) for s in range(40)], max_new=4)
+    assert runner.use_tc_gemv
+    assert sum(f for _, _, f in res) <= 4
+
+
+def test_8b_shape_twenty_rows_per_module():
+    """8B width, 2 layers, 10 sessions x 2 modules (K5-TC, MN = 16 / 32 incl.
+    the 128256-row LM head)."""
+    from paper_2602_12029_b200.model import LlamaConfig
+    cfg = LlamaConfig.llama8b(n_layers=2, max_pos=1024)
+    rng = np.random.default_rng(6)
+    prompts = [rng.integers(0, cfg.vocab, int(n)).tolist() for n in rng.integers(20, 90, 20)]
+    runner, res = _run_case(cfg, prompts, [(m, s) for s in range(20) for m in range(2)], max_new=3)
+    assert runner.use_tc_gemv
+    assert sum(f for _, _, f in res) <= 4

@@ -1,5 +1,5 @@
 """K5 grouped decode GEMV (TMA-bulk weight stream + mma.sync, 1..32 rows per
-module) vs a torch fp32 reference on identical bf16 operands, all
+module) and K5-TC (tcgen05, 9..64 rows per module) vs a torch fp32 reference on identical bf16 operands, all
 epilogues, ragged rows per module (incl. modules with no rows, one module
 holding every row, K not a multiple of the 1024-column stage).
 Tolerance: |gpu - ref| <= 2e-3 * max|ref| + 1e-4 (fp32 outputs),
@@ -11,7 +11,8 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _run(rows_per_mod, N, K, epi, seed=0):
+def _run(rows_per_mod, N, K, epi, seed=0, tc=False):
+    import ctypes
     from paper_2602_12029_b200 import _lib
     g = torch.Generator(device="cuda").manual_seed(seed)
     n_mod = len(rows_per_mod)
@@ -36,8 +37,21 @@ def _run(rows_per_mod, N, K, epi, seed=0):
         out = torch.randn(R, N, device="cuda", generator=g) if epi == 2 else torch.zeros(R, N, device="cuda")
         if epi == 2:
             ref = ref + out
-    _lib.check(_lib.load().psk_gemv(x.data_ptr(), R, K, ptrs.data_ptr(), t_mrs.data_ptr(), n_mod, max(rows_per_mod), N, epi,
-                                    out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    lib = _lib.load()
+    if tc:
+        hp = (ctypes.c_void_p * n_mod)(*[w.data_ptr() for w in W])
+        wsb = ctypes.c_int64()
+        _lib.check(lib.psk_gemv_tc_workspace(ctypes.byref(wsb)))
+        ws = torch.zeros(wsb.value, dtype=torch.uint8, device="cuda")
+        for _ in range(2):  # twice: the stream-K flags must come back zeroed
+            o2 = out.clone()
+            _lib.check(lib.psk_gemv_tc(x.data_ptr(), R, K, hp, t_mrs.data_ptr(), n_mod, max(rows_per_mod), N,
+                                       epi, o2.data_ptr(), ws.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        assert int(ws[:4096].view(torch.int32).abs().sum().item()) == 0
+        out = o2
+    else:
+        _lib.check(lib.psk_gemv(x.data_ptr(), R, K, ptrs.data_ptr(), t_mrs.data_ptr(), n_mod, max(rows_per_mod), N,
+                                epi, out.data_ptr(), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     err = (out.float() - ref).abs().max().item()
     scale = ref.abs().max().item()
@@ -64,3 +78,16 @@ def test_gemv_ragged_k_and_many_tiles(N, K):
     N = 16032: more tiles than SMs per module."""
     _run([2, 1], N, K, 1, seed=3)
     _run([5], N, K, 2, seed=4)
+
+
+@pytest.mark.parametrize("rows", [[9, 16, 3, 16], [32, 5], [0, 17], [64, 64, 1, 40], [33], [0, 0, 48, 0],
+                                  [16] * 8, [20] * 16])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_gemv_tc_rows_and_epilogues(rows, epi):
+    _run(rows, 1536, 4096, epi, tc=True)
+
+
+@pytest.mark.parametrize("N,K", [(4096, 14336), (6144, 4096), (16384, 4096), (128, 64)])
+def test_gemv_tc_shapes(N, K):
+    _run([30, 31, 2, 16], N, K, 1, seed=1, tc=True)
+    _run([12], N, K, 2, seed=2, tc=True)

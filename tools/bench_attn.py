@@ -10,8 +10,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 import bench  # noqa: E402
 
-peaks = {"hbm": 6539.2}
-for shared, mods in [(4095, 4), (4095, 16), (32767, 4), (32767, 8), (32767, 16)]:
-    r = bench.decode_attn_fanout(peaks, shared_tokens=shared, modules=mods)
-    print(f"shared={shared:6d} modules={mods:3d}: {r['us_per_launch']:8.2f} us "
+peaks = bench._peaks()
+for shared, mods, sess, priv in [(4095, 4, 8, 256), (4095, 4, 1, 1), (4095, 16, 1, 1), (32767, 4, 1, 1),
+                                 (32767, 8, 1, 1), (32767, 16, 1, 1)]:
+    r = bench.decode_attn_fanout(peaks, shared_tokens=shared, modules=mods, sessions=sess, priv=priv)
+    print(f"sessions={sess} shared={shared:6d} modules={mods:3d} priv={priv:4d}: {r['us_per_launch']:8.2f} us "
           f"{r['achieved']:8.1f} GB/s ({r['frac']:.3f})", flush=True)

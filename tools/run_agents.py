@@ -26,10 +26,10 @@ def main():
     ap.add_argument("--rate", type=float, default=1.0)
     ap.add_argument("--duration", type=float, default=10.0)
     ap.add_argument("--pattern", default="react")
-    ap.add_argument("--rows", type=int, default=8)
+    ap.add_argument("--rows", type=int, default=16)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--time-scale", type=float, default=1.0)
-    ap.add_argument("--pool-pages", type=int, default=1024)
+    ap.add_argument("--pool-pages", type=int, default=7500)
     a = ap.parse_args()
     cfg = LlamaConfig.llama8b(max_pos=4096 + 512) if a.shape == "8b" else LlamaConfig.tiny(max_pos=4096)
     models = list(wl.DEFAULT_MODELS)
@@ -45,6 +45,7 @@ def main():
                           max_context=4096, max_output=256, modules=mods, base=base)
         recs = srv.run(sessions, time_scale=a.time_scale)
         out[mode.value] = summarize(recs)
+        out[mode.value]["gpu_time"] = srv.gpu_time()
         del srv
         torch.cuda.empty_cache()
     b, p = out["baseline"], out["prefillshare"]
