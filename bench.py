@@ -2,13 +2,14 @@
 
 Workload (N=1): Llama-3.1-8B-shape frozen prefill module + 4 decode modules
 (random init, bf16) on one B200. One step = one serve() of a batch of
---sessions concurrent agent sessions (default 8), each a fresh synthetic
+--sessions concurrent agent sessions (default 32), each a fresh synthetic
 4096-token prompt: GPU block-pool lookup/insert (K7), shared prefill of each
 prompt (K1-K3), then every decode module generates 256 tokens greedily from
-the shared KV (K5/K6), all sessions x modules co-batched in one decode step.
+the shared KV (K5/K5-TC GEMV, K6 attention), all sessions x modules
+co-batched in one decode step.
 A request = one decode module's 256-token generation on one session; its
-latency is the serve() duration. The single-session point (S=1, the
-latency-optimal configuration) is reported under "single_session".
+latency is the serve() duration. Other batch sizes (S = 1, the latency-optimal
+point, 8 and 64) are reported under "sessions_sweep".
 
   value : req/s with prompts resident in HBM (device tokens), CUDA events.
   e2e   : req/s through PrefillShareEngine.serve() with HOST prompts
@@ -199,12 +200,11 @@ def gemv_roofline(eng, peaks) -> dict:
     s = torch.cuda.current_stream().cuda_stream
     it = [0]
 
-    def launch():
+    def launch():  # the engine's own dispatch: K5 (<= 8 rows/module) or K5-TC
         l = it[0] % cfg.n_layers
         it[0] += 1
-        _lib.check(lib.psk_gemv(r.xn.data_ptr(), b.n_rows, cfg.d_model, r.p_wgu[l].data_ptr(),
-                                b.t_mrs.data_ptr(), b.n_mod, b.max_rpm, 2 * cfg.ffn, 3, r.act.data_ptr(),
-                                torch.cuda.current_stream().cuda_stream))
+        r._gemv(r.xn, cfg.d_model, r.p_wgu[l], r.h_wgu[l], 2 * cfg.ffn, 3, r.act,
+                torch.cuda.current_stream().cuda_stream)
     dt = _time_launches(launch, 4 * cfg.n_layers)
     nbytes = b.n_mod * 2 * cfg.ffn * cfg.d_model * 2 + b.n_rows * (cfg.d_model + cfg.ffn) * 2
     gbs = nbytes / dt / 1e9
@@ -213,10 +213,11 @@ def gemv_roofline(eng, peaks) -> dict:
     traffic, tsrc = None, None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
-        t = json.loads(tf.read_text()).get(f"gemv_gate_up_m{b.max_rpm}")
+        t = json.loads(tf.read_text()).get(f"gemv_gate_up_m{b.max_rpm}" + ("_tc" if r.use_tc_gemv else ""))
         if t:
             traffic, tsrc = t["dram_bytes"], t["source"]
-    return {"bound": "hbm", "kernel": "psk_gemv (gate/up, SiLU*mul epilogue)", "achieved": round(gbs, 1),
+    kname = "psk_gemv_tc (tcgen05" if r.use_tc_gemv else "psk_gemv (mma.sync"
+    return {"bound": "hbm", "kernel": f"{kname}; gate/up, SiLU*mul epilogue)", "achieved": round(gbs, 1),
             "peak": peaks["hbm"], "unit": "GB/s", "frac": round(gbs / peaks["hbm"], 4),
             "traffic": traffic, "traffic_source": tsrc, "bytes_per_launch": nbytes,
             "us_per_launch": round(dt * 1e6, 2), "rows_per_module": b.max_rpm,
@@ -370,6 +371,33 @@ def kv_copy_roofline(eng, peaks, n_pages: int = PROMPT // 16 + 1) -> dict:
             "achieved": round(gbs, 1), "unit": "GB/s", "frac": round(gbs / peaks["hbm"], 4)}
 
 
+def serve_point(cfg, mods, base, S: int, batches, device: int, steps: int = 2) -> dict:
+    """req/s and p95 serve latency of an engine serving S sessions per step
+    on the given weights (prompts resident in HBM is not needed: host
+    prompts, the e2e path). One warm-up serve, then `steps` timed serves."""
+    import numpy as np
+    import torch
+    from paper_2602_12029_b200.engine import PrefillShareEngine
+    e = PrefillShareEngine(cfg, N_MOD, S, PROMPT, MAX_NEW, pool_pages=S * (PROMPT // 16 + 1) + 64,
+                           device=device, modules=mods, base=base)
+    e.capture()
+    rng = np.random.default_rng(77 + S)
+    prompts = [[rng.integers(0, cfg.vocab, PROMPT, dtype=np.int64) for _ in range(S)] for _ in range(steps + 1)]
+    e.serve(prompts[0])
+    st = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record(st)
+    for j in range(steps):
+        e.serve(prompts[j + 1])
+        ev[j + 1].record(st)
+    ev[-1].synchronize()
+    ts = [ev[j].elapsed_time(ev[j + 1]) / 1e3 for j in range(steps)]
+    del e
+    torch.cuda.empty_cache()
+    return {"sessions": S, "value": round(S * N_MOD * steps / sum(ts), 4), "unit": "req/s",
+            "p95_latency_ms": round(max(ts) * 1e3, 2)}
+
+
 def prefill_roofline(eng, peaks) -> dict:
     import torch
     T = PROMPT
@@ -391,7 +419,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sessions", type=int, default=8, help="concurrent sessions per serve() batch")
+    ap.add_argument("--sessions", type=int, default=32, help="concurrent sessions per serve() batch")
     ap.add_argument("--no-extras", action="store_true", help="skip kernel rooflines / cpu baseline")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
@@ -510,24 +538,14 @@ def main() -> None:
         out["decode_step"] = {"weight_bytes": step_bytes,
                               "ms_per_token_step": round((t_val / a.steps - out["prefill"]["ms_per_prefill"]
                                                           * S / 1e3) / MAX_NEW * 1e3, 3)}
-        if S != 1:
-            # the same weights served one session per step (latency-optimal point)
-            e1 = PrefillShareEngine(cfg, N_MOD, 1, PROMPT, MAX_NEW, pool_pages=2 * (PROMPT // 16 + 1) * 4,
-                                    device=local, modules=eng.mods, base=eng.base)
-            e1.capture()
-            for i in range(2):
-                e1.serve(batches[i][:1])
-            ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            ev1[0].record(st)
-            for j in range(2):
-                e1.serve(batches[a.warmup + j][:1])
-                ev1[j + 1].record(st)
-            ev1[-1].synchronize()
-            s1 = [ev1[j].elapsed_time(ev1[j + 1]) / 1e3 for j in range(2)]
-            out["single_session"] = {"value": round(N_MOD * 2 / sum(s1), 4), "unit": "req/s",
-                                     "p95_latency_ms": round(max(s1) * 1e3, 2)}
-            del e1
+        # throughput / latency at other batch sizes, same weights (the KV
+        # pool of the main engine is freed first)
+        mods, base = eng.mods, eng.base
         del eng
+        torch.cuda.empty_cache()
+        out["sessions_sweep"] = [serve_point(cfg, mods, base, n, batches, local)
+                                 for n in (1, 8, 64) if n != S]
+        del mods, base
         torch.cuda.empty_cache()
         out["decode_attn_fanout_32k_x16"] = decode_attn_fanout(peaks)
         out["pool"] = pool_ops()

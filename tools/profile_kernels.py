@@ -1,7 +1,7 @@
 """Drive each hot kernel a few times at the bench shapes, for ncu.
 
     ncu --set full -k regex:<kernel> -c 2 python tools/profile_kernels.py <which> [rows/module]
-which: gemv | attn4k | attn4k_s8 | attn32k | gemm | prefill_attn | all
+which: gemv | gemv_tc | attn4k | attn4k_s8 | attn32k | gemm | prefill_attn | all
 """
 import sys
 from pathlib import Path
@@ -52,6 +52,21 @@ if which in ("attn4k_s8", "all"):
     attn(4095, 4, sessions=8)
 if which in ("attn32k", "all"):
     attn(32767, 16)
+if which == "gemv_tc":
+    import ctypes
+    M = int(sys.argv[2]) if len(sys.argv) > 2 else 32  # rows per module
+    mods = [ModuleWeights(cfg, 10 + i) for i in range(4)]
+    x = torch.randn(4 * M, cfg.d_model, device="cuda").to(torch.bfloat16)
+    act = torch.empty(4 * M, cfg.ffn, dtype=torch.bfloat16, device="cuda")
+    hp = (ctypes.c_void_p * 4)(*[m.wgu[0].data_ptr() for m in mods])
+    mrs = torch.tensor([i * M for i in range(5)], dtype=torch.int32, device="cuda")
+    wsb = ctypes.c_int64()
+    _lib.check(lib.psk_gemv_tc_workspace(ctypes.byref(wsb)))
+    ws = torch.zeros(wsb.value, dtype=torch.uint8, device="cuda")
+    for _ in range(4):
+        _lib.check(lib.psk_gemv_tc(x.data_ptr(), 4 * M, cfg.d_model, hp, mrs.data_ptr(), 4, M,
+                                   2 * cfg.ffn, 3, act.data_ptr(), ws.data_ptr(), s))
+    torch.cuda.synchronize()
 if which in ("gemv", "all"):
     M = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # rows per module
     mods = [ModuleWeights(cfg, 10 + i) for i in range(4)]
