@@ -602,13 +602,21 @@ __global__ void __launch_bounds__(THREADS, 1)
       umma::wait_ld();
       umma::fence_before();
       tma::mbar_arrive(&s_free[t]);  // S_t may be overwritten by S_t(c+1)
-      float mx = -INFINITY;
+      // causal mask only on the chunks that cross the warp's diagonal
+      if (!__all_sync(0xffffffffu, key0 + KC - 1 <= qpos)) {
 #pragma unroll
-      for (int e = 0; e < KC; ++e) {
-        const float v = key0 + e <= qpos ? __uint_as_float(sr[e]) * p.scale_log2 : -INFINITY;
-        sr[e] = __float_as_uint(v);
-        mx = fmaxf(mx, v);
+        for (int e = 0; e < KC; ++e)
+          if (key0 + e > qpos) sr[e] = __float_as_uint(-INFINITY);
       }
+      // tree max of the raw scores (no serial chain), then into log2 units
+      float tm[KC / 2];
+#pragma unroll
+      for (int k = 0; k < KC / 2; ++k) tm[k] = fmaxf(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1]));
+#pragma unroll
+      for (int w = KC / 4; w >= 1; w >>= 1)
+#pragma unroll
+        for (int k = 0; k < w; ++k) tm[k] = fmaxf(tm[k], tm[k + w]);
+      const float mx = tm[0] * p.scale_log2;
       // PV_t(c-1) must be done before P_t is overwritten or O_t rescaled
       if (c > 0) tma::mbar_wait(&pv_done[t], (c - 1) & 1);
       const bool grow = mx > m_used + RESCALE_LOG2 || (m_used == -INFINITY && mx > -INFINITY);
@@ -629,18 +637,19 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (grow) m_used = mx;
       const float base = m_used == -INFINITY ? 0.f : m_used;
+      float ls[KC / 8];
 #pragma unroll
       for (int q = 0; q < KC / 8; ++q) {
         float pf[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          pf[i] = exp2f(__uint_as_float(sr[8 * q + i]) - base);  // masked: exp2(-inf) = 0
-          l += pf[i];
-        }
+        for (int i = 0; i < 8; ++i)  // p = 2^(s * scale - m); masked: 2^-inf = 0
+          pf[i] = fast_exp2(fmaf(__uint_as_float(sr[8 * q + i]), p.scale_log2, -base));
+        ls[q] = ((pf[0] + pf[1]) + (pf[2] + pf[3])) + ((pf[4] + pf[5]) + (pf[6] + pf[7]));
         const uint4 v = f32_to_bf16x8(pf);
         asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(prow + (((q ^ (g & 7))) << 4)), "r"(v.x),
                      "r"(v.y), "r"(v.z), "r"(v.w));
       }
+      l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
       umma::fence_proxy_async();
       umma::fence_before();
       tma::mbar_arrive(&p_full[t]);
