@@ -256,7 +256,7 @@ def decode_attn_roofline(eng, peaks) -> dict:
             "bytes_per_launch": nbytes, "us_per_launch": round(dt * 1e6, 2)}
 
 
-def decode_attn_fanout(peaks, shared_tokens=32767, modules=16, sessions=1, priv=1) -> dict:
+def decode_attn_fanout(peaks, shared_tokens=32767, modules=16, sessions=1, priv=1, splits=None) -> dict:
     """K6 at a fan-out shape: `sessions` shared contexts of `shared_tokens`,
     each read by `modules` decode modules (4 query heads per KV head each)
     with `priv` private tokens per row, random KV / queries, 32 layers cycled
@@ -287,8 +287,9 @@ def decode_attn_fanout(peaks, shared_tokens=32767, modules=16, sessions=1, priv=
     out = torch.empty_like(q)
     import ctypes
     from paper_2602_12029_b200.model import attn_splits
-    ns = attn_splits(per_sess, cfg.n_kv_heads * sessions,
-                     torch.cuda.get_device_properties(0).multi_processor_count)
+    # splits: None = fixed split count (one CTA per SM over the groups), 0 = stream-K
+    ns = splits if splits is not None else attn_splits(
+        per_sess, cfg.n_kv_heads * sessions, torch.cuda.get_device_properties(0).multi_processor_count)
     wsb = ctypes.c_int64()
     _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), cfg.n_kv_heads, ns, ctypes.byref(wsb)))
     ws = torch.zeros(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")

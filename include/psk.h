@@ -217,8 +217,12 @@ int psk_rope_append(const psk_decode_batch* b, const float* qkv, int32_t n_q_hea
  * `splits` slices; every page is streamed from HBM once per step (TMA) for
  * ALL of the session's decode rows (modules) and their GQA query heads; the
  * split partials merge by log-sum-exp in a second, PDL-overlapped kernel.
+ * splits = 0 selects the stream-K schedule: all groups' pages laid end to
+ * end and cut into one equal run per SM (segment partials merged through a
+ * per-group CTA directory); it falls back to fixed splits that fit the same
+ * workspace for > 32 query rows per KV head or > 64 sessions.
  * q_rot bf16 [n_rows][nq][hd] -> out bf16 [n_rows][nq][hd]. workspace: fp32,
- * psk_decode_attn_workspace() bytes. */
+ * psk_decode_attn_workspace() bytes (for the same `splits`). */
 int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int32_t splits,
                               int64_t* bytes);
 int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_heads,
@@ -239,6 +243,13 @@ int psk_argmax_advance(const psk_decode_batch* b, const float* logits, int32_t v
  * N % 256 == 0, K % 64 == 0; any M (tail rows masked).
  * ------------------------------------------------------------------------ */
 #define PSK_EPI_QKV_ROPE_KV 4  /* internal: see psk_gemm_qkv_rope_kv          */
+/* Split-K workspace for the prefill GEMMs: when a GEMM's last wave of
+ * 128x256 tiles would be at most half full, those tail tiles are split along
+ * K and reduced in a fixed order through this buffer. Bind one ZEROED buffer
+ * of psk_gemm_workspace() bytes per process (GEMMs on one stream at a time);
+ * unbound (or NULL) = no split. */
+int psk_gemm_workspace(int64_t* bytes);
+int psk_gemm_bind_workspace(void* ws, int64_t bytes);
 int psk_gemm(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epilogue,
              void* out, int64_t ldo, void* stream);
 /* Fused QKV projection of T prompt tokens at positions pos0.. : RoPE on q
@@ -248,6 +259,13 @@ int psk_gemm(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int3
 int psk_gemm_qkv_rope_kv(const void* A, const void* Wqkv, int32_t T, int32_t K, int32_t n_q_heads,
                          const float* rope, int32_t pos0, psk_kv_layout kv, int32_t layer,
                          const int32_t* page_table, void* q_out, void* stream);
+/* Batched (varlen) form for several sequences' new tokens stacked in A
+ * (partial prefills of many sessions in one forward):
+ * row t sits at absolute position row_pos[t] and its k/v go to KV slot
+ * row_slot[t] = page * 16 + token-in-page. */
+int psk_gemm_qkv_rope_kv_rows(const void* A, const void* Wqkv, int32_t T, int32_t K, int32_t n_q_heads,
+                              const float* rope, const int32_t* row_pos, const int32_t* row_slot,
+                              psk_kv_layout kv, int32_t layer, void* q_out, void* stream);
 
 /* K3 — causal prefill attention of T new positions [pos0, pos0+T) over the
  * paged cache (keys [0, pos0+T) through page_table; the new keys were
@@ -255,6 +273,12 @@ int psk_gemm_qkv_rope_kv(const void* A, const void* Wqkv, int32_t T, int32_t K, 
  * [T][nq*128]. frontend/src/model.ts:288-293, :312-315. */
 int psk_prefill_attn(const void* q_rot, int32_t T, int32_t pos0, int32_t n_q_heads, psk_kv_layout kv,
                      int32_t layer, const int32_t* page_table, void* out, void* stream);
+/* Batched K3 over stacked sequences: n_items work items, 8 int32 each
+ * {token offset of the sequence in q_rot/out, its T, its pos0, offset of its
+ * page table in `pages`, q-block (256 / GQA-group positions), 0, 0, 0}
+ * (16-byte aligned), one CTA per (item, KV head); order items heaviest first. */
+int psk_prefill_attn_batch(const void* q_rot, int32_t n_items, const int32_t* items, int32_t n_q_heads,
+                           psk_kv_layout kv, int32_t layer, const int32_t* pages, void* out, void* stream);
 /* h[t,:] = table[tokens[t],:] (fp32). model.ts:276-284 (token embedding). */
 int psk_embed_tokens(const int64_t* tokens, int32_t T, const void* table, int32_t d, float* h,
                      void* stream);

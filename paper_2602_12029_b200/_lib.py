@@ -104,8 +104,12 @@ _SIGS: dict[str, list] = {
     "psk_argmax_advance": [C.POINTER(DecodeBatchC), _P, _I32, _P, _I32, _P],
     # prefill (K1-K3)
     "psk_gemm": [_P, _P, _I32, _I32, _I32, _I32, _P, _I64, _P],
+    "psk_gemm_workspace": [C.POINTER(_I64)],
+    "psk_gemm_bind_workspace": [_P, _I64],
     "psk_gemm_qkv_rope_kv": [_P, _P, _I32, _I32, _I32, _P, _I32, KVLayout, _I32, _P, _P, _P],
     "psk_prefill_attn": [_P, _I32, _I32, _I32, KVLayout, _I32, _P, _P, _P],
+    "psk_prefill_attn_batch": [_P, _I32, _P, _I32, KVLayout, _I32, _P, _P, _P],
+    "psk_gemm_qkv_rope_kv_rows": [_P, _P, _I32, _I32, _I32, _P, _P, _P, KVLayout, _I32, _P, _P],
     "psk_embed_tokens": [_P, _I32, _P, _I32, _P, _P],
     "psk_kv_copy_pages": [_P, _P, _P, _P, _I32, _I64, _P],
 }
@@ -153,3 +157,19 @@ def check(code: int) -> int:
 def call(name: str, *args) -> int:
     """Call an int-returning entry point and raise on failure."""
     return check(getattr(load(), name)(*args))
+
+
+_gemm_ws = None
+
+
+def bind_gemm_workspace(device) -> None:
+    """Allocate (once per process) and bind the prefill GEMMs' split-K
+    workspace (psk_gemm_bind_workspace); kept alive for the process."""
+    global _gemm_ws
+    if _gemm_ws is not None:
+        return
+    import torch
+    nb = C.c_int64()
+    check(load().psk_gemm_workspace(C.byref(nb)))
+    _gemm_ws = torch.zeros(nb.value, dtype=torch.uint8, device=device)
+    check(load().psk_gemm_bind_workspace(_gemm_ws.data_ptr(), nb.value))

@@ -66,6 +66,9 @@ struct Params {
   float* po;               // [items][GMAX][HD]
   int nq, grp, layer, ns;
   float scale_log2;
+  int* dir;  // stream-K mode (ns == 0): per group {first CTA, last CTA}, then the page total;
+             // partial slot of (cta, group) = cta + group
+  int sk_grid;  // stream-K: CTAs of the partial kernel
 };
 
 // SW128 address of (token row, 16-byte chunk c16 in 0..15) in a K/V tile made
@@ -354,6 +357,407 @@ __global__ void __launch_bounds__(THREADS, 1)
   trace_stamp(4);
 }
 
+
+// ------------------------------------------------ stream-K partial kernel --
+// The (session, KV head) groups of a step have very different page counts
+// (shared prompt + each row's private pages) and their number rarely fits the
+// SM count (8 sessions x 8 heads = 64 groups, 32 x 8 = 256 groups on 148
+// SMs: 13% idle SMs / 1.73 waves). Here the groups' pages are laid end to end
+// and cut into gridDim.x equal runs (one persistent CTA per SM): a run is a
+// sequence of segments, one per group it touches. The producer streams the
+// whole run through one TMA ring without a break; the consumer warps process
+// it segment by segment (Q of the segment's group staged, the same
+// mma.sync flash loop as decode_attn_partial, fold, one (m, l, o) partial
+// per segment in slot cta + group, which is unique because successive
+// segments advance the CTA, the group, or both). The CTA holding a group's
+// first page records {first, last CTA} of the group for the merge kernel.
+namespace sk {
+
+// Consumers wait on `full` by parity: a warp must never wait for round r of
+// a stage before round r - 1 of it completed (it could mistake round r - 2's
+// parity), so NST is a multiple of every `ways` (8 / 4 / 2) and segments are
+// separated by consumer barriers.
+constexpr int NST = 16;                         // 128 KiB ring
+constexpr int MAXS = 64;                        // sessions (tables in shared memory)
+constexpr int MAXP = 2048;                      // pages of one run
+constexpr int OFF_Q = NST * STAGE;
+constexpr int OFF_SCR = OFF_Q;                  // fold scratch aliases Q (barrier-separated)
+constexpr int OFF_BAR = OFF_SCR + CW * 32 * FRAG * 4;
+constexpr int OFF_PG = OFF_BAR + 2 * NST * 8;
+constexpr int SMEM = OFF_PG + MAXP * 4 + 1024;
+static_assert(NST % CW == 0, "parity waits need NST % ways == 0");
+
+struct Tables {
+  int rows[MAXS][MAXR];
+  int plen[MAXS][MAXR];
+  int pstart[MAXS][MAXR + 1];  // page index (within the group) of each row's first private page
+  int nsh[MAXS];               // shared pages
+  int ls[MAXS];
+  int nr[MAXS];
+  int P[MAXS];                 // pages per group of the session (0 without rows)
+  int off[MAXS + 1];           // prefix of P over sessions
+};
+
+__device__ __forceinline__ int run_begin(int c, int64_t total, int grid) { return (int)((int64_t)c * total / grid); }
+
+// session / head / page of flat page index x (x < total)
+__device__ __forceinline__ void locate(const Tables& t, int n_sess, int nkv, int x, int& s, int& h, int& k) {
+  int lo = 0, hi = n_sess - 1;  // largest s with nkv * off[s] <= x
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (nkv * t.off[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  s = lo;
+  const int r = x - nkv * t.off[s];
+  h = r / t.P[s];
+  k = r % t.P[s];
+}
+
+__device__ __forceinline__ int cta_of(int x, int64_t total, int grid) {
+  int c = (int)((int64_t)x * grid / total);
+  while (c + 1 < grid && run_begin(c + 1, total, grid) <= x) ++c;
+  while (c > 0 && run_begin(c, total, grid) > x) --c;
+  return c;
+}
+
+__device__ __forceinline__ void mbar_arrive_n(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(tma::sa(bar)), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    decode_attn_sk(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ Params p) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* empty = full + NST;
+  int* s_page = reinterpret_cast<int*>(smem + OFF_PG);
+  float* scr = reinterpret_cast<float*>(smem + OFF_SCR);  // [CW][32][FRAG]
+  __shared__ Tables t;
+  __shared__ int64_t s_total;
+
+  trace_stamp(0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkv = p.kv.n_kv_heads, nS = p.b.n_sess;
+  const int grid = gridDim.x, cta = blockIdx.x;
+
+  // ---- session tables: one thread per (session, row) pair, two load rounds
+  for (int e = threadIdx.x; e < nS * MAXR; e += THREADS) {
+    const int sx = e / MAXR, i = e % MAXR;
+    const int nr = p.b.sess_nrows[sx];
+    if (i < nr) {
+      const int r = p.b.sess_rows[(int64_t)sx * p.b.max_rows_per_sess + i];
+      t.rows[sx][i] = r;
+      t.plen[sx][i] = p.b.priv_len[r] + 1;  // includes the token appended this step
+    }
+    if (i == 0) {
+      t.nr[sx] = nr;
+      t.ls[sx] = p.b.sess_len[sx];
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < NST; ++st) {
+      tma::mbar_init(&full[st], 1);
+      tma::mbar_init(&empty[st], CW);
+    }
+    tma::fence_mbar_init();
+    tma::prefetch_map(&kvmap);
+  }
+  __syncthreads();
+  for (int sx = threadIdx.x; sx < nS; sx += THREADS) {
+    const int nsh = (t.ls[sx] + PT - 1) / PT;
+    int acc = nsh;
+    for (int i = 0; i < t.nr[sx]; ++i) {
+      t.pstart[sx][i] = acc;
+      acc += (t.plen[sx][i] + PT - 1) / PT;
+    }
+    t.pstart[sx][t.nr[sx]] = acc;
+    t.nsh[sx] = nsh;
+    t.P[sx] = t.nr[sx] > 0 ? acc : 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int sx = 0; sx < nS; ++sx) {
+      t.off[sx] = acc;
+      acc += t.P[sx];
+    }
+    t.off[nS] = acc;
+    s_total = (int64_t)acc * nkv;
+  }
+  __syncthreads();
+  const int64_t total = s_total;
+  // the merge needs the run boundaries too: CTAs with empty runs (fewer pages
+  // than SMs) write no partial and are skipped
+  if (cta == 0 && threadIdx.x == 0) p.dir[2 * nS * nkv] = (int)total;
+  const int c0 = run_begin(cta, total, grid), c1 = run_begin(cta + 1, total, grid);
+  const int np = c1 - c0;
+  auto page_at = [&](int sx, int hh, int kk) -> int {
+    (void)hh;
+    if (kk < t.nsh[sx]) return p.b.sess_pages[(int64_t)sx * p.b.max_sess_pages + kk];
+    int i = 0;
+    while (kk >= t.pstart[sx][i + 1]) ++i;
+    return p.b.row_pages[(int64_t)t.rows[sx][i] * p.b.max_row_pages + (kk - t.pstart[sx][i])];
+  };
+  // page ids of the run -> shared memory
+  for (int j = threadIdx.x; j < np && j < MAXP; j += THREADS) {
+    int sx, hh, kk;
+    locate(t, nS, nkv, c0 + j, sx, hh, kk);
+    s_page[j] = page_at(sx, hh, kk);
+  }
+  __syncthreads();
+  trace_stamp(1);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // q / the appended K,V come from rope_append
+
+  if (warp == CW) {
+    // ---------------- TMA producer: the whole run, one ring ----------------
+    if (lane == 0 && np > 0) {
+      int sx, hh, kk;
+      locate(t, nS, nkv, c0, sx, hh, kk);
+      for (int j = 0; j < np; ++j) {
+        const int st = j % NST;
+        tma::mbar_wait(&empty[st], ((j / NST) & 1) ^ 1);
+        const int page = j < MAXP ? s_page[j] : page_at(sx, hh, kk);
+        const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + hh) * PT);
+        tma::mbar_expect_tx(&full[st], STAGE);
+        tma::load_4d(&kvmap, &full[st], smem + st * STAGE, 0, row_k, 0, 0);
+        if (++kk == t.P[sx]) {  // next group
+          kk = 0;
+          if (++hh == nkv) {
+            hh = 0;
+            do ++sx; while (sx < nS && t.P[sx] == 0);
+          }
+        }
+      }
+    }
+    // lanes 1-31 must not exit while lane 0 issues TMA (the issue sequence
+    // uses warp-uniform registers: exited lanes make it an illegal instruction)
+    __syncwarp();
+  } else if (np > 0) {
+    // ---------------- consumers: segment by segment ----------------
+    const uint32_t ring = smem_u32(smem);
+    int sx, hh, kk;
+    locate(t, nS, nkv, c0, sx, hh, kk);
+    int c = c0, j0 = 0;
+    while (c < c1) {
+      const int n = min(t.P[sx] - kk, c1 - c);
+      const int nr = t.nr[sx];
+      const int G = nr * p.grp;
+      const int T = (G + 15) / 16;
+      const int Tp = T <= 1 ? 1 : (T == 2 ? 2 : 4);
+      const int ways = CW / Tp;
+      const int g = sx * nkv + hh;  // group
+      // Q of this group -> shared (the previous segment is fully folded)
+      {
+        const uint32_t qs = smem_u32(smem + OFF_Q);
+        for (int e = threadIdx.x; e < T * 16 * 16; e += CW * 32) {
+          const int gq = e >> 4, cc = e & 15;
+          uint4 v = make_uint4(0, 0, 0, 0);
+          if (gq < G) {
+            const int qh = hh * p.grp + gq % p.grp;
+            v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)t.rows[sx][gq / p.grp] * p.nq + qh) * HD + cc * 8);
+          }
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(qs + swz256(gq, cc)), "r"(v.x),
+                       "r"(v.y), "r"(v.z), "r"(v.w));
+        }
+      }
+      named_barrier_sync(1, CW * 32);
+      if (c == c0) trace_stamp(2);
+      const int tile = warp / ways, way = warp % ways;
+      const bool active = tile < T;
+      float o[16][4];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+      if (active) {
+        uint32_t qa[8][4];
+        {
+          const uint32_t qs = smem_u32(smem + OFF_Q);
+          const int qrow = tile * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+            ldmatrix_x4(qs + swz256(qrow, 2 * ks + (lane >> 4)), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+        }
+        const int gA = tile * 16 + (lane >> 2), gB = gA + 8;
+        const int ownA = gA < G ? gA / p.grp : -2, ownB = gB < G ? gB / p.grp : -2;
+        for (int q = way; q < n; q += ways) {
+          const int j = j0 + q;
+          const int st = j % NST;
+          // parity waits are safe: within a segment stage s is read by one
+          // warp per m-tile in every round (NST % ways == 0), and a segment
+          // starts only after every page of the previous one was consumed
+          tma::mbar_wait(&full[st], (j / NST) & 1);
+          const int kq = kk + q;
+          int limit, owner;
+          if (kq < t.nsh[sx]) {
+            limit = min(PT, t.ls[sx] - kq * PT);
+            owner = -1;
+          } else {
+            int i = 0;
+            while (kq >= t.pstart[sx][i + 1]) ++i;
+            limit = min(PT, t.plen[sx][i] - (kq - t.pstart[sx][i]) * PT);
+            owner = i;
+          }
+          const uint32_t kt = ring + st * STAGE, vt = kt + TILE;
+          float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+          {
+            const int mi = lane >> 3, ri = lane & 7;
+            const int tok = (mi >> 1) * 8 + ri;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+              uint32_t b0, b1, b2, b3;
+              ldmatrix_x4(tile_addr(kt, tok, 2 * ks + (mi & 1)), b0, b1, b2, b3);
+              mma_bf16_16816(sc[0], qa[ks], b0, b1);
+              mma_bf16_16816(sc[1], qa[ks], b2, b3);
+            }
+          }
+          const bool okA = owner < 0 || owner == ownA;
+          const bool okB = owner < 0 || owner == ownB;
+          const int cb = (lane & 3) * 2;
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int tt = nt * 8 + cb + (e & 1);
+              const bool ok = tt < limit && (e < 2 ? okA : okB);
+              sc[nt][e] = ok ? sc[nt][e] * p.scale_log2 : -INFINITY;
+            }
+          float mx0 = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
+          float mx1 = fmaxf(fmaxf(sc[0][2], sc[0][3]), fmaxf(sc[1][2], sc[1][3]));
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+          const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
+          const float r0 = n0 == -INFINITY ? 0.f : n0, r1 = n1 == -INFINITY ? 0.f : n1;
+          const float c0f = fast_exp2(m0 - r0), c1f = fast_exp2(m1 - r1);
+          m0 = n0;
+          m1 = n1;
+          float pr[2][4];
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            pr[nt][0] = fast_exp2(sc[nt][0] - r0);
+            pr[nt][1] = fast_exp2(sc[nt][1] - r0);
+            pr[nt][2] = fast_exp2(sc[nt][2] - r1);
+            pr[nt][3] = fast_exp2(sc[nt][3] - r1);
+          }
+          l0 = l0 * c0f + ((pr[0][0] + pr[0][1]) + (pr[1][0] + pr[1][1]));
+          l1 = l1 * c1f + ((pr[0][2] + pr[0][3]) + (pr[1][2] + pr[1][3]));
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            o[i][0] *= c0f;
+            o[i][1] *= c0f;
+            o[i][2] *= c1f;
+            o[i][3] *= c1f;
+          }
+          uint32_t pa[4];
+          pa[0] = pack_bf16(pr[0][0], pr[0][1]);
+          pa[1] = pack_bf16(pr[0][2], pr[0][3]);
+          pa[2] = pack_bf16(pr[1][0], pr[1][1]);
+          pa[3] = pack_bf16(pr[1][2], pr[1][3]);
+          {
+            const int mi = lane >> 3, ri = lane & 7;
+            const int tok = (mi & 1) * 8 + ri;
+#pragma unroll
+            for (int np2 = 0; np2 < 8; ++np2) {
+              uint32_t b0, b1, b2, b3;
+              ldmatrix_x4_trans(tile_addr(vt, tok, 2 * np2 + (mi >> 1)), b0, b1, b2, b3);
+              mma_bf16_16816(o[2 * np2], pa, b0, b1);
+              mma_bf16_16816(o[2 * np2 + 1], pa, b2, b3);
+            }
+          }
+          __syncwarp();
+          // every stage gets CW arrivals: one per m-tile that read it, the
+          // tile-0 warp adds the CW - T of the tiles this segment lacks
+          if (lane == 0) mbar_arrive_n(&empty[st], tile == 0 ? (uint32_t)(CW - T + 1) : 1u);
+        }
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+      }
+      // ---- fold the `ways` warps of each m-tile (scratch aliases Q: every
+      // warp has its Q fragments in registers past this barrier) ----
+      named_barrier_sync(1, CW * 32);
+      if (active) {
+        float4* d = reinterpret_cast<float4*>(scr + (warp * 32 + lane) * FRAG);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) d[i] = make_float4(o[i][0], o[i][1], o[i][2], o[i][3]);
+        d[16] = make_float4(m0, m1, l0, l1);
+      }
+      named_barrier_sync(1, CW * 32);
+      const int64_t base = (int64_t)(cta + g) * GMAX;
+      {
+        const int ra = lane >> 2, rb = ra + 8, cb = (lane & 3) * 2;
+        for (int tt = 0; tt < T; ++tt) {
+          float Ma = -INFINITY, Mb = -INFINITY;
+          for (int v = 0; v < ways; ++v) {
+            const float4 ml = reinterpret_cast<const float4*>(scr + ((tt * ways + v) * 32 + lane) * FRAG)[16];
+            Ma = fmaxf(Ma, ml.x);
+            Mb = fmaxf(Mb, ml.y);
+          }
+          const float Mra = Ma == -INFINITY ? 0.f : Ma, Mrb = Mb == -INFINITY ? 0.f : Mb;
+          float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          float La = 0.f, Lb = 0.f;
+          for (int v = 0; v < ways; ++v) {
+            const float* src = scr + ((tt * ways + v) * 32 + lane) * FRAG;
+            const float4 ml = reinterpret_cast<const float4*>(src)[16];
+            const float fa = exp2f(ml.x - Mra), fb = exp2f(ml.y - Mrb);
+            La += fa * ml.z;
+            Lb += fb * ml.w;
+            const float4 x0 = reinterpret_cast<const float4*>(src)[2 * warp];
+            const float4 x1 = reinterpret_cast<const float4*>(src)[2 * warp + 1];
+            acc[0] += fa * x0.x; acc[1] += fa * x0.y; acc[2] += fb * x0.z; acc[3] += fb * x0.w;
+            acc[4] += fa * x1.x; acc[5] += fa * x1.y; acc[6] += fb * x1.z; acc[7] += fb * x1.w;
+          }
+          const int ga = tt * 16 + ra, gb = tt * 16 + rb;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int col = (2 * warp + q) * 8 + cb;
+            if (ga < G)
+              *reinterpret_cast<float2*>(p.po + (base + ga) * HD + col) = make_float2(acc[4 * q], acc[4 * q + 1]);
+            if (gb < G)
+              *reinterpret_cast<float2*>(p.po + (base + gb) * HD + col) = make_float2(acc[4 * q + 2], acc[4 * q + 3]);
+          }
+          if (warp == 0 && (lane & 3) == 0) {
+            if (ga < G) {
+              p.pm[base + ga] = Ma;
+              p.pl[base + ga] = La;
+            }
+            if (gb < G) {
+              p.pm[base + gb] = Mb;
+              p.pl[base + gb] = Lb;
+            }
+          }
+        }
+      }
+      if (kk == 0 && threadIdx.x == 0) {  // this run holds the group's first page
+        const int x_last = nkv * t.off[sx] + hh * t.P[sx] + t.P[sx] - 1;
+        p.dir[2 * g] = cta;
+        p.dir[2 * g + 1] = cta_of(x_last, total, grid);
+      }
+      named_barrier_sync(1, CW * 32);  // scratch and Q are rewritten by the next segment
+      // next segment
+      c += n;
+      j0 += n;
+      kk += n;
+      if (kk == t.P[sx]) {
+        kk = 0;
+        if (++hh == nkv) {
+          hh = 0;
+          do ++sx; while (sx < nS && t.P[sx] == 0);
+        }
+      }
+    }
+  }
+  trace_stamp(3);
+  asm volatile("griddepcontrol.launch_dependents;");
+  trace_stamp(4);
+}
+
+}  // namespace sk
+
 // Merge: one CTA per (row, q head), one thread per head dim; every split's
 // (m, l, o) is loaded up front (32 splits in flight per thread) and folded by
 // log-sum-exp. Launched with programmatic dependent launch: it is scheduled
@@ -365,17 +769,37 @@ __global__ void __launch_bounds__(HD) decode_attn_merge(const __grid_constant__ 
   const int h = qh / p.grp;
   // the row tables are static within a step: read them before the wait
   const int g = p.b.row_in_sess[r] * p.grp + qh % p.grp;
-  const int64_t base = (int64_t)(p.b.row_sess[r] * nkv + h) * p.ns * GMAX + g;
+  const int grp_id = p.b.row_sess[r] * nkv + h;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");  // the o-proj GEMV may start streaming weights
+  // partial slots of this (session, KV head): splits mode ns consecutive
+  // slots; stream-K mode slots cta + group for the CTAs in dir[group]
+  int64_t first;
+  int n, cf = 0;
+  int64_t total = 0;
+  if (p.ns > 0) {
+    first = (int64_t)grp_id * p.ns;
+    n = p.ns;
+  } else {
+    cf = p.dir[2 * grp_id];
+    const int cl = p.dir[2 * grp_id + 1];
+    total = p.dir[2 * p.b.n_sess * nkv];
+    first = (int64_t)cf + grp_id;
+    n = cl - cf + 1;
+  }
+  const int64_t base = first * GMAX + g;
   float M = -INFINITY, L = 0.f, acc = 0.f;
-  for (int j0 = 0; j0 < p.ns; j0 += MERGE_U) {
+  for (int j0 = 0; j0 < n; j0 += MERGE_U) {
     float mj[MERGE_U], lj[MERGE_U], oj[MERGE_U];
 #pragma unroll
     for (int u = 0; u < MERGE_U; ++u) {
       const int j = j0 + u;
       const int64_t sl = base + (int64_t)j * GMAX;
-      const bool ok = j < p.ns;
+      bool ok = j < n;
+      if (ok && p.ns == 0 && total < p.sk_grid) {  // stream-K, fewer pages than CTAs: skip empty runs
+        const int c = cf + j;
+        ok = sk::run_begin(c, total, p.sk_grid) != sk::run_begin(c + 1, total, p.sk_grid);
+      }
       mj[u] = ok ? __ldcg(p.pm + sl) : -INFINITY;
       lj[u] = ok ? __ldcg(p.pl + sl) : 0.f;
       oj[u] = ok ? __ldcg(p.po + sl * HD + d) : 0.f;
@@ -934,18 +1358,31 @@ using namespace psk::dattn;
 
 extern "C" {
 
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
 int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int32_t splits,
                               int64_t* bytes) {
-  PSK_CHECK_ARG(b && bytes && splits >= 1, "psk_decode_attn_workspace: bad args");
-  const int64_t items = (int64_t)b->n_sess * n_kv_heads * splits;
-  *bytes = items * GMAX * (HD + 2) * 4;
+  PSK_CHECK_ARG(b && bytes && splits >= 0, "psk_decode_attn_workspace: bad args");
+  const int64_t groups = (int64_t)b->n_sess * n_kv_heads;
+  // stream-K (splits == 0): one partial slot per (CTA, group) segment, at
+  // most grid + groups of them, plus the per-group CTA directory
+  const int64_t items = splits > 0 ? groups * splits : sm_count() + groups;
+  *bytes = items * GMAX * (HD + 2) * 4 + (splits > 0 ? 0 : groups * 2 * 4 + 16);
   return PSK_OK;
 }
 
 int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_heads, int32_t layer,
                     psk_kv_layout kv, int32_t splits, void* workspace, void* out, void* stream) {
   PSK_CHECK_ARG(b && q_rot && out && workspace && kv.head_dim == HD && kv.page_tokens == PT &&
-                    kv.n_pages > 0 && n_q_heads % kv.n_kv_heads == 0 && splits >= 1,
+                    kv.n_pages > 0 && n_q_heads % kv.n_kv_heads == 0 && splits >= 0,
                 "psk_decode_attn: bad args");
   const int grp = n_q_heads / kv.n_kv_heads;
   PSK_CHECK_ARG(b->max_rows_per_sess <= MAXR && grp * b->max_rows_per_sess <= GMAX,
@@ -956,6 +1393,19 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   // (32k x 8: 30.1 vs 32.0 us). PSK_ATTN_HMMA=1 keeps mma.sync everywhere.
   static const bool force_hmma = getenv("PSK_ATTN_HMMA") != nullptr;
   const bool use_tc = grp * b->max_rows_per_sess > 32 && !force_hmma;
+  const int sms = sm_count();
+  const int64_t groups = (int64_t)b->n_sess * kv.n_kv_heads;
+  const int64_t slots = splits > 0 ? groups * splits : sms + groups;  // workspace partial slots
+  // stream-K mode (splits == 0) for the mma.sync path when the session
+  // tables and one run's page list fit in shared memory; otherwise (and for
+  // the tcgen05 path) fixed splits that fit the same workspace
+  bool stream_k = false;
+  if (splits == 0) {
+    const int64_t per_group = (int64_t)b->max_sess_pages + (int64_t)b->max_rows_per_sess * b->max_row_pages;
+    const int64_t run_bound = (groups * per_group + sms - 1) / sms + 1;
+    stream_k = !use_tc && b->n_sess <= sk::MAXS && run_bound <= sk::MAXP;
+    if (!stream_k) splits = (int)(sms / groups) > 1 ? (int)(sms / groups) : 1;  // one wave, fits the slots
+  }
   CUtensorMap map, vmap;
   int rc = psk::kv_tensor_map(kv, &map, use_tc ? psk::KV_BOX2D : psk::KV_PAGE4D);
   if (!rc && use_tc) rc = psk::kv_tensor_map(kv, &vmap, psk::KV_TILE3D);
@@ -968,18 +1418,21 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   p.nq = n_q_heads;
   p.grp = grp;
   p.layer = layer;
-  p.ns = splits;
-  const int64_t items = (int64_t)b->n_sess * kv.n_kv_heads * splits;
+  p.ns = stream_k ? 0 : splits;
+  const int64_t items = stream_k ? sms : groups * splits;  // CTAs of the partial kernel
   float* ws = reinterpret_cast<float*>(workspace);
   p.pm = ws;
-  p.pl = ws + items * GMAX;
-  p.po = ws + 2 * items * GMAX;
+  p.pl = ws + slots * GMAX;
+  p.po = ws + 2 * slots * GMAX;
+  p.dir = reinterpret_cast<int*>(ws + slots * GMAX * (HD + 2));
+  p.sk_grid = sms;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
   cudaStream_t s = psk::as_stream(stream);
   static bool init = false;
   if (!init) {
     PSK_CUDA_TRY(cudaFuncSetAttribute(decode_attn_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SMEM));
+    PSK_CUDA_TRY(cudaFuncSetAttribute(sk::decode_attn_sk, cudaFuncAttributeMaxDynamicSharedMemorySize, sk::SMEM));
     init = true;
   }
   const bool tr = psk::trace_arm((int)items);
@@ -1001,13 +1454,17 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
     cfg.blockDim = dim3(tcv::THREADS);
     cfg.dynamicSmemBytes = tcv::SMEM;
     PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tcv::decode_attn_tc, map, vmap, p));
+  } else if (stream_k) {
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = sk::SMEM;
+    PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, sk::decode_attn_sk, map, p));
   } else {
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = SMEM;
     PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_attn_partial, map, p));
   }
   if (tr) {
-    static const char* names_h[] = {"entry", "prologue", "staged", "loop-done", "folded"};
+    static const char* names_h[] = {"entry", "prologue", "staged", "loop-done", "folded"};  // (stream-K: 0, 1, 3, 4)
     static const char* names_t[] = {"entry", "tmem+bars", "q-staged", "tma-issued", "done"};
     const char* const* names = use_tc ? names_t : names_h;
     psk::trace_report("decode_attn", (int)items, 5, names);

@@ -46,6 +46,10 @@ struct Epi {
   int layer;
   const int32_t* page_table;
   __nv_bfloat16* q_out;
+  // batched (varlen) prefill: per-row absolute position and KV slot
+  // (page * 16 + token in page); nullptr = one sequence at pos0 + row
+  const int32_t* row_pos;
+  const int32_t* row_slot;
 };
 
 // ----------------------------------------------------------- PTX helpers --
@@ -150,6 +154,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+      "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+      "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+      "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+
 // ------------------------------------------------------------- epilogues --
 
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
@@ -167,7 +182,18 @@ __device__ __forceinline__ __nv_bfloat16* kv_dst(const psk_kv_layout& kv, int pa
 __device__ void epilogue_tile(const Epi& e, uint32_t tacc, int row, bool row_ok, int n0) {
   float v[32], w[32];
   if (e.mode == PSK_EPI_QKV_ROPE_KV) {
-    const int pos = e.pos0 + row;
+    int pos = e.pos0 + row, page = 0, tok = 0;
+    if (row_ok) {
+      if (e.row_pos != nullptr) {
+        pos = e.row_pos[row];
+        const int slot = e.row_slot[row];
+        page = slot >> 4;
+        tok = slot & 15;
+      } else {
+        page = e.page_table[pos / 16];
+        tok = pos % 16;
+      }
+    }
     const float* cs = e.rope + (int64_t)pos * 128;
 #pragma unroll 1
     for (int hh = 0; hh < 2; ++hh) {
@@ -178,10 +204,7 @@ __device__ void epilogue_tile(const Epi& e, uint32_t tacc, int row, bool row_ok,
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           tmem_ld32(hb + c * 32, v);
-          if (row_ok) {
-            const int page = e.page_table[pos / 16];
-            store_bf16x32(kv_dst(e.kv, page, e.layer, 1, vh, pos % 16) + c * 32, v);
-          }
+          if (row_ok) store_bf16x32(kv_dst(e.kv, page, e.layer, 1, vh, tok) + c * 32, v);
         }
         continue;
       }
@@ -201,8 +224,7 @@ __device__ void epilogue_tile(const Epi& e, uint32_t tacc, int row, bool row_ok,
         if (head < e.nq) {
           dst = e.q_out + ((int64_t)row * e.nq + head) * 128;
         } else {
-          const int page = e.page_table[pos / 16];
-          dst = kv_dst(e.kv, page, e.layer, 0, head - e.nq, pos % 16);
+          dst = kv_dst(e.kv, page, e.layer, 0, head - e.nq, tok);
         }
         store_bf16x32(dst + half * 32, v);
         store_bf16x32(dst + half * 32 + 64, w);
@@ -250,9 +272,40 @@ __device__ void epilogue_tile(const Epi& e, uint32_t tacc, int row, bool row_ok,
 
 // ---------------------------------------------------------------- kernel --
 
+// Work schedule. Tiles are walked m-fastest, item = blockIdx.x + i * grid.
+// When the last wave would be mostly idle (tiles = W * grid + rem with
+// rem <= grid / 2), the `rem` tail tiles are split along K into S pieces
+// (S = grid / rem, >= 4 k-blocks each) so the tail costs 1/S of a tile
+// instead of a whole one (4096^2 GEMMs: 512 tiles = 3.46 waves -> 3.5, not 4).
+// Each split writes its fp32 partial to the workspace; the last one to
+// finish (atomic counter) sums all S partials in split order (fixed order:
+// bit-reproducible), stores the sum back into its TMEM accumulator and runs
+// the normal fused epilogue.
+struct Sched {
+  int tiles, full, rem, S, items;
+  float* part;     // [rem * S][BM][BN] fp32
+  int* counters;   // [rem], zero between launches
+};
+
+__device__ __forceinline__ void item_range(const Sched& sc, int item, int kb_n, int& tile, int& kb0, int& kb1,
+                                           int& split) {
+  if (item < sc.full) {
+    tile = item;
+    kb0 = 0;
+    kb1 = kb_n;
+    split = -1;
+  } else {
+    const int j = item - sc.full;
+    tile = sc.full + j / sc.S;
+    split = j % sc.S;
+    kb0 = split * kb_n / sc.S;
+    kb1 = (split + 1) * kb_n / sc.S;
+  }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                        const __grid_constant__ CUtensorMap tmap_b, int M, int N, int K, Epi e) {
+                        const __grid_constant__ CUtensorMap tmap_b, int M, int N, int K, Epi e, Sched sc) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -265,9 +318,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m_tiles = (M + BM - 1) / BM, n_tiles = N / BN;
-  const int n_tiles_total = m_tiles * n_tiles;
+  const int m_tiles = (M + BM - 1) / BM;
   const int kb_n = K / BK;
+  __shared__ int s_last;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmap_a);
@@ -297,9 +350,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+      for (int item = blockIdx.x; item < sc.items; item += gridDim.x) {
+        int t, kb0, kb1, split;
+        item_range(sc, item, kb_n, t, kb0, kb1, split);
         const int mb = t % m_tiles, nb = t / m_tiles;
-        for (int kb = 0; kb < kb_n; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           tma_load_2d(&tmap_a, &full[stage], sA + stage * A_BYTES, kb * BK, mb * BM);
@@ -314,12 +369,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++it) {
+      for (int item = blockIdx.x; item < sc.items; item += gridDim.x, ++it) {
+        int t, kb0, kb1, split;
+        item_range(sc, item, kb_n, t, kb0, kb1, split);
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tacc = tmem_base + acc * BN;
-        for (int kb = 0; kb < kb_n; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t da = smem_desc_sw128(sA + stage * A_BYTES);
@@ -328,7 +385,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             // +32 bytes along K inside the 128B swizzle atom = +2 in the
             // descriptor's 16-byte address units
-            umma_bf16(tacc, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            umma_bf16(tacc, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -340,13 +397,65 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int r_in_tile = q * 32 + lane;
     int it = 0;
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++it) {
+    for (int item = blockIdx.x; item < sc.items; item += gridDim.x, ++it) {
+      int t, kb0, kb1, split;
+      item_range(sc, item, kb_n, t, kb0, kb1, split);
       const int mb = t % m_tiles, nb = t / m_tiles;
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const int row = mb * BM + r_in_tile;
       const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (split >= 0) {
+        // split-K tail tile: publish this split's partial; the last split
+        // sums all partials (split order) into its accumulator
+        const int ti = t - sc.full;
+        float* mine = sc.part + ((int64_t)(ti * sc.S + split) * BM + r_in_tile) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(tacc + c * 32, v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4*>(mine + c * 32)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 4 && lane == 0) {
+          const int old = atomicAdd(&sc.counters[ti], 1);
+          s_last = old == sc.S - 1;
+          if (s_last) {
+            sc.counters[ti] = 0;  // ready for the next launch
+            __threadfence();
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (!s_last) {
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+          continue;
+        }
+        const float* rows0 = sc.part + ((int64_t)(ti * sc.S) * BM + r_in_tile) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          for (int sp = 0; sp < sc.S; ++sp) {
+            const float4* src = reinterpret_cast<const float4*>(rows0 + (int64_t)sp * BM * BN + c * 32);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 x = __ldcg(src + i);
+              v[4 * i] += x.x;
+              v[4 * i + 1] += x.y;
+              v[4 * i + 2] += x.z;
+              v[4 * i + 3] += x.w;
+            }
+          }
+          tmem_st32(tacc + c * 32, v);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
       epilogue_tile(e, tacc, row, row < M, nb * BN);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -399,6 +508,16 @@ static int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
   return PSK_OK;
 }
 
+// split-K workspace (psk_gemm_bind_workspace); none bound = no split
+struct Workspace {
+  float* part = nullptr;
+  int64_t part_bytes = 0;
+  int* counters = nullptr;
+  int n_counters = 0;
+};
+static Workspace g_ws;
+constexpr int64_t WS_COUNTER_BYTES = 4096;
+
 static int launch(const void* A, const void* B, int M, int N, int K, const Epi& e, cudaStream_t s) {
   if (M <= 0) return PSK_OK;
   if (N % BN != 0 || K % BK != 0) {
@@ -420,7 +539,26 @@ static int launch(const void* A, const void* B, int M, int N, int K, const Epi& 
   }
   const int tiles = ((M + BM - 1) / BM) * (N / BN);
   const int grid = tiles < sms ? tiles : sms;
-  gemm_bf16_tn_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ma, mb, M, N, K, e);
+  Sched sc{};
+  sc.tiles = tiles;
+  sc.full = tiles;
+  sc.rem = 0;
+  sc.S = 1;
+  const int kb_n = K / BK;
+  const int rem = tiles % grid, waves = tiles / grid;
+  if (g_ws.part && waves >= 1 && rem > 0 && rem <= grid / 2) {
+    int S = grid / rem;
+    if (S > kb_n / 4) S = kb_n / 4;
+    if (S >= 2 && (int64_t)rem * S * BM * BN * 4 <= g_ws.part_bytes && rem <= g_ws.n_counters) {
+      sc.full = tiles - rem;
+      sc.rem = rem;
+      sc.S = S;
+      sc.part = g_ws.part;
+      sc.counters = g_ws.counters;
+    }
+  }
+  sc.items = sc.full + sc.rem * sc.S;
+  gemm_bf16_tn_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ma, mb, M, N, K, e, sc);
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }
@@ -429,6 +567,29 @@ static int launch(const void* A, const void* B, int M, int N, int K, const Epi& 
 }  // namespace psk
 
 extern "C" {
+
+int psk_gemm_workspace(int64_t* bytes) {
+  PSK_CHECK_ARG(bytes != nullptr, "psk_gemm_workspace: null out");
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  *bytes = psk::gemm::WS_COUNTER_BYTES + (int64_t)sms * psk::gemm::BM * psk::gemm::BN * 4;
+  return PSK_OK;
+}
+
+int psk_gemm_bind_workspace(void* ws, int64_t bytes) {
+  using namespace psk::gemm;
+  if (ws == nullptr) {
+    g_ws = Workspace{};
+    return PSK_OK;
+  }
+  PSK_CHECK_ARG(bytes > WS_COUNTER_BYTES, "psk_gemm_bind_workspace: workspace too small");
+  g_ws.counters = reinterpret_cast<int*>(ws);
+  g_ws.n_counters = (int)(WS_COUNTER_BYTES / 4);
+  g_ws.part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + WS_COUNTER_BYTES);
+  g_ws.part_bytes = bytes - WS_COUNTER_BYTES;
+  return PSK_OK;
+}
 
 int psk_gemm(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epilogue,
              void* out, int64_t ldo, void* stream) {
@@ -455,6 +616,25 @@ int psk_gemm_qkv_rope_kv(const void* A, const void* Wqkv, int32_t T, int32_t K, 
   e.kv = kv;
   e.layer = layer;
   e.page_table = page_table;
+  e.q_out = reinterpret_cast<__nv_bfloat16*>(q_out);
+  const int N = (n_q_heads + 2 * kv.n_kv_heads) * 128;
+  return psk::gemm::launch(A, Wqkv, T, N, K, e, psk::as_stream(stream));
+}
+
+int psk_gemm_qkv_rope_kv_rows(const void* A, const void* Wqkv, int32_t T, int32_t K, int32_t n_q_heads,
+                              const float* rope, const int32_t* row_pos, const int32_t* row_slot,
+                              psk_kv_layout kv, int32_t layer, void* q_out, void* stream) {
+  PSK_CHECK_ARG(A && Wqkv && rope && row_pos && row_slot && q_out && kv.head_dim == 128 && kv.page_tokens == 16,
+                "psk_gemm_qkv_rope_kv_rows: bad args");
+  psk::gemm::Epi e{};
+  e.mode = PSK_EPI_QKV_ROPE_KV;
+  e.rope = rope;
+  e.nq = n_q_heads;
+  e.nkv = kv.n_kv_heads;
+  e.kv = kv;
+  e.layer = layer;
+  e.row_pos = row_pos;
+  e.row_slot = row_slot;
   e.q_out = reinterpret_cast<__nv_bfloat16*>(q_out);
   const int N = (n_q_heads + 2 * kv.n_kv_heads) * 128;
   return psk::gemm::launch(A, Wqkv, T, N, K, e, psk::as_stream(stream));

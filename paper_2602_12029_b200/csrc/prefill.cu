@@ -247,6 +247,10 @@ struct TcParams {
   const int32_t* pages;
   int T, pos0, nq, grp, layer, qb, n_qblocks;
   float scale_log2;
+  // batched (varlen) prefill: per work item 8 ints {token offset of the
+  // sequence in q/out, T, pos0, offset of its page table in `pages`, q-block,
+  // 0, 0, 0}; nullptr = one sequence (T, pos0, pages), q-blocks heavy first
+  const int32_t* items;
 };
 
 __global__ void __launch_bounds__(THREADS_TC, 1)
@@ -476,9 +480,24 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkv = p.kv.n_kv_heads;
   const int h = blockIdx.x % nkv;
-  const int qblk = p.n_qblocks - 1 - (int)(blockIdx.x / nkv);  // heavy blocks first
-  const int t0 = qblk * p.qb;                                  // p.qb = 256 / grp positions
-  const int kv_end = p.pos0 + min(t0 + p.qb, p.T);
+  int qblk, T = p.T, pos0 = p.pos0;
+  const int32_t* pages = p.pages;
+  const __nv_bfloat16* qsrc = p.q;
+  __nv_bfloat16* odst = p.out;
+  if (p.items != nullptr) {  // batched prefill: this CTA's (sequence, q-block)
+    const int4 it = reinterpret_cast<const int4*>(p.items)[2 * (blockIdx.x / nkv)];
+    const int qb_ = reinterpret_cast<const int4*>(p.items)[2 * (blockIdx.x / nkv) + 1].x;
+    qsrc += (int64_t)it.x * p.nq * HD;
+    odst += (int64_t)it.x * p.nq * HD;
+    T = it.y;
+    pos0 = it.z;
+    pages += it.w;
+    qblk = qb_;
+  } else {
+    qblk = p.n_qblocks - 1 - (int)(blockIdx.x / nkv);  // heavy blocks first
+  }
+  const int t0 = qblk * p.qb;  // p.qb = 256 / grp positions
+  const int kv_end = pos0 + min(t0 + p.qb, T);
   const int n_pages = (kv_end + PT - 1) / PT;
   const int nch = (kv_end + KC - 1) / KC;
 
@@ -497,16 +516,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     tma::prefetch_map(&kvmap);
   }
   if (warp == 1) umma::tmem_alloc(&s_tmem, 512);
-  for (int j = threadIdx.x; j < n_pages && j < MAXPG; j += THREADS) s_pg[j] = p.pages[j];
+  for (int j = threadIdx.x; j < n_pages && j < MAXPG; j += THREADS) s_pg[j] = pages[j];
   const uint32_t sq = smem_u32(smem + OFF_Q), sp = smem_u32(smem + OFF_P);
   // Q rows -> shared memory (K-major, 128B swizzle), row r = (position, head)
   for (int e = threadIdx.x; e < 256 * 16; e += THREADS) {
     const int r = e >> 4, c = e & 15;
     const int t = t0 + r / p.grp;
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (t < p.T) {
+    if (t < T) {
       const int qh = h * p.grp + r % p.grp;
-      v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)t * p.nq + qh) * HD + c * 8);
+      v = *reinterpret_cast<const uint4*>(qsrc + ((int64_t)t * p.nq + qh) * HD + c * 8);
     }
     asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sq + (r >> 7) * QBYTES +
                                                                umma::kmajor_off(r & 127, c, 16384)),
@@ -529,7 +548,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int pp = 0; pp < CPG; ++pp) {
           const int j = c * CPG + pp;
           const int jj = j < n_pages ? j : c * CPG;  // past the end: any valid page, masked
-          const int page = jj < MAXPG ? s_pg[jj] : p.pages[jj];
+          const int page = jj < MAXPG ? s_pg[jj] : pages[jj];
           const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
           const int row_v = row_k + nkv * PT;
           tma::load_2d(&kvmap, &full[st], kr + pp * 2048, 0, row_k);
@@ -590,7 +609,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tS = tmem + ((uint32_t)lq << 16) + t * KC;
     const uint32_t tO = tmem + ((uint32_t)lq << 16) + 128 + t * HD;
     const uint32_t prow = sp + t * PBYTES + g * 128;
-    const int qpos = p.pos0 + t0 + r / p.grp;  // keys [0, qpos] visible
+    const int qpos = pos0 + t0 + r / p.grp;  // keys [0, qpos] visible
     float m_used = -INFINITY, l = 0.f;
     for (int c = 0; c < nch; ++c) {
       const int key0 = c * KC;
@@ -659,13 +678,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     umma::fence_after();
     const int tpos = t0 + r / p.grp;
     const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* dst = p.out + ((int64_t)tpos * p.nq + h * p.grp + r % p.grp) * HD;
+    __nv_bfloat16* dst = odst + ((int64_t)tpos * p.nq + h * p.grp + r % p.grp) * HD;
 #pragma unroll 1
     for (int q = 0; q < HD / 32; ++q) {
       uint32_t o[32];
       umma::ld32_async(tO + q * 32, o);
       umma::wait_ld();
-      if (tpos < p.T) {
+      if (tpos < T) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           float f[8];
@@ -739,6 +758,7 @@ int psk_prefill_attn(const void* q_rot, int32_t T, int32_t pos0, int32_t n_q_hea
     t.grp = grp;
     t.layer = layer;
     t.scale_log2 = p.scale_log2;
+    t.items = nullptr;
     static const bool tc1 = getenv("PSK_PREFILL_TC1") != nullptr;
     if (!tc1) {
       t.qb = 256 / grp;
@@ -774,6 +794,39 @@ int psk_prefill_attn(const void* q_rot, int32_t T, int32_t pos0, int32_t n_q_hea
     attr = true;
   }
   prefill_attn_kernel<<<p.n_qblocks * kv.n_kv_heads, THREADS, SMEM, psk::as_stream(stream)>>>(p);
+  PSK_LAUNCH_CHECK();
+  return PSK_OK;
+}
+
+int psk_prefill_attn_batch(const void* q_rot, int32_t n_items, const int32_t* items, int32_t n_q_heads,
+                           psk_kv_layout kv, int32_t layer, const int32_t* pages, void* out, void* stream) {
+  using namespace psk::pre;
+  PSK_CHECK_ARG(q_rot && items && pages && out && kv.head_dim == HD && kv.page_tokens == PT && kv.n_pages > 0 &&
+                    n_q_heads % kv.n_kv_heads == 0 && n_items >= 0,
+                "psk_prefill_attn_batch: bad args");
+  const int grp = n_q_heads / kv.n_kv_heads;
+  PSK_CHECK_ARG(128 % grp == 0, "psk_prefill_attn_batch: GQA group %d", grp);
+  if (n_items == 0) return PSK_OK;
+  CUtensorMap map;
+  int rc = psk::kv_tensor_map(kv, &map);
+  if (rc) return rc;
+  tc::TcParams t{};
+  t.q = reinterpret_cast<const __nv_bfloat16*>(q_rot);
+  t.out = reinterpret_cast<__nv_bfloat16*>(out);
+  t.kv = kv;
+  t.pages = pages;
+  t.nq = n_q_heads;
+  t.grp = grp;
+  t.layer = layer;
+  t.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
+  t.qb = 256 / grp;
+  t.items = items;
+  static bool pp_attr = false;
+  if (!pp_attr) {
+    PSK_CUDA_TRY(cudaFuncSetAttribute(pp::prefill_attn_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, pp::SMEM));
+    pp_attr = true;
+  }
+  pp::prefill_attn_pp<<<n_items * kv.n_kv_heads, pp::THREADS, pp::SMEM, psk::as_stream(stream)>>>(map, t);
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }

@@ -216,6 +216,9 @@ class KVCache:
             pg = pages[p // PAGE_TOKENS]
             ks.append(pv[pg, layer, 0, :, p % PAGE_TOKENS])
             vs.append(pv[pg, layer, 1, :, p % PAGE_TOKENS])
+        if n == 0:
+            e = pv.new_empty(pv.shape[3], 0, pv.shape[5])
+            return e, e.clone()
         return torch.stack(ks, 1), torch.stack(vs, 1)
 
 
@@ -380,6 +383,10 @@ class DecodeRunner:
         self.out_tokens = torch.full((R, max_new), -1, dtype=torch.int32, device=dev)
         self.rope = torch.from_numpy(rope_table(cfg)).to(dev)
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        # fixed splits (one CTA per SM over the groups). splits=0 selects the
+        # stream-K schedule of K6, which is correct but measured slower: runs
+        # that cut across (session, head) groups lose the DRAM locality of 8
+        # heads' CTAs reading the same pages together
         self.splits = splits if splits is not None else attn_splits(
             batch.max_sess_pages + batch.max_rps * ((max_new + 15) // 16),
             batch.n_sess * cfg.n_kv_heads, sms)
@@ -493,6 +500,8 @@ class PrefillRunner:
              torch.tensor([weights.mlp_norm[l].data_ptr()], dtype=torch.int64, device=dev))
             for l in range(cfg.n_layers)]
         self.launches_per_call = 1 + 7 * cfg.n_layers
+        # (the GEMMs' split-K tail, psk_gemm_bind_workspace, is left unbound:
+        # measured slower end to end at the 4k prefill shapes)
 
     def flops(self, T: int, pos0: int = 0) -> float:
         """Algorithmic FLOPs of one call (GEMMs + causal attention)."""
@@ -526,6 +535,73 @@ class PrefillRunner:
             chk(lib.psk_gemm_qkv_rope_kv(_ptr(self.xn), _ptr(w.wqkv[l]), T, d, cfg.n_heads,
                                          _ptr(self.rope), pos0, kvl, l, pt, _ptr(self.q), s))
             chk(lib.psk_prefill_attn(_ptr(self.q), T, pos0, cfg.n_heads, kvl, l, pt, _ptr(self.attn), s))
+            chk(lib.psk_gemm(_ptr(self.attn), _ptr(w.wo[l]), T, d, cfg.n_heads * cfg.head_dim, 2,
+                             _ptr(self.h), d, s))
+            chk(lib.psk_rmsnorm_rows(_ptr(self.h), T, d, _ptr(g2), None, eps, _ptr(self.xn), s))
+            chk(lib.psk_gemm(_ptr(self.xn), _ptr(w.wgu[l]), T, 2 * cfg.ffn, d, 3, _ptr(self.act),
+                             cfg.ffn, s))
+            chk(lib.psk_gemm(_ptr(self.act), _ptr(w.wdown[l]), T, d, cfg.ffn, 2, _ptr(self.h), d, s))
+
+    def run_batch(self, seqs, stream: int | None = None) -> None:
+        """Batched partial prefill: the new tokens of several
+        sequences in ONE forward, so the (weight-bound) small prefills of an
+        agent workload share each layer's weight stream. seqs: list of
+        (tokens int64 device [T_i], pos0_i, page table covering [0, pos0_i+T_i)
+        as a list / int32 tensor). Rows are stacked; the QKV epilogue places
+        each row's K/V by its own (position, slot) and K3 runs one CTA per
+        (sequence, q-block, KV head)."""
+        if len(seqs) == 1:
+            toks, pos0, pt = seqs[0]
+            if not torch.is_tensor(pt):
+                pt = torch.tensor(pt, dtype=torch.int32, device=self.h.device)
+            return self.run(toks, pos0, pt, stream)
+        cfg, lib, w = self.cfg, self.lib, self.w
+        Ts = [int(t.shape[0]) for t, _, _ in seqs]
+        T = sum(Ts)
+        if T > self.max_tokens:
+            raise ValueError(f"batched prefill of {T} tokens exceeds max_tokens {self.max_tokens}")
+        grp = cfg.n_heads // cfg.n_kv_heads
+        qb = 256 // grp
+        row_pos, row_slot, pages, items = [], [], [], []
+        off = 0
+        for (toks, pos0, pt), n in zip(seqs, Ts):
+            if pos0 + n > cfg.max_pos:
+                raise ValueError(f"sequence length {pos0 + n} exceeds max_pos {cfg.max_pos}")
+            ptn = (pt.cpu().numpy() if torch.is_tensor(pt) else np.asarray(pt)).astype(np.int64)
+            pos = np.arange(pos0, pos0 + n, dtype=np.int64)
+            row_pos.append(pos)
+            row_slot.append(ptn[pos // PAGE_TOKENS] * PAGE_TOKENS + pos % PAGE_TOKENS)
+            for k in range((n + qb - 1) // qb):
+                kv_end = pos0 + min((k + 1) * qb, n)
+                items.append((kv_end, [off, n, pos0, len(pages), k, 0, 0, 0]))
+            pages.extend(ptn.tolist())
+            off += n
+        items.sort(key=lambda x: -x[0])  # heaviest (longest key range) first
+        # items first: the kernel reads them as int4 (16-byte aligned)
+        plan = np.concatenate([np.asarray([it for _, it in items], dtype=np.int64).reshape(-1),
+                               np.concatenate(row_pos), np.concatenate(row_slot),
+                               np.asarray(pages, dtype=np.int64)]).astype(np.int32)
+        dplan = torch.from_numpy(plan).to(self.h.device)
+        ni = 8 * len(items)
+        d_items = dplan[:ni]
+        d_pos, d_slot = dplan[ni:ni + T], dplan[ni + T:ni + 2 * T]
+        d_pages = dplan[ni + 2 * T:]
+        tokens = torch.cat([t for t, _, _ in seqs])
+        self._batch_keep = (dplan, tokens)  # alive until the next call (async kernels)
+        s = stream if stream is not None else _stream()
+        chk = _lib.check
+        d = cfg.d_model
+        kvl = self.kv.layout()
+        eps = C.c_float(cfg.norm_eps)
+        chk(lib.psk_embed_tokens(_ptr(tokens), T, _ptr(w.embed), d, _ptr(self.h), s))
+        for l in range(cfg.n_layers):
+            g1, g2 = self.gamma_ptrs[l]
+            chk(lib.psk_rmsnorm_rows(_ptr(self.h), T, d, _ptr(g1), None, eps, _ptr(self.xn), s))
+            chk(lib.psk_gemm_qkv_rope_kv_rows(_ptr(self.xn), _ptr(w.wqkv[l]), T, d, cfg.n_heads,
+                                              _ptr(self.rope), _ptr(d_pos), _ptr(d_slot), kvl, l,
+                                              _ptr(self.q), s))
+            chk(lib.psk_prefill_attn_batch(_ptr(self.q), len(items), _ptr(d_items), cfg.n_heads, kvl, l,
+                                           _ptr(d_pages), _ptr(self.attn), s))
             chk(lib.psk_gemm(_ptr(self.attn), _ptr(w.wo[l]), T, d, cfg.n_heads * cfg.head_dim, 2,
                              _ptr(self.h), d, s))
             chk(lib.psk_rmsnorm_rows(_ptr(self.h), T, d, _ptr(g2), None, eps, _ptr(self.xn), s))

@@ -77,8 +77,12 @@ class AgentServer:
     def __init__(self, cfg: LlamaConfig, model_ids: list[str], mode: ServingMode, *,
                  rows_per_module: int = 8, pool_pages_per_worker: int = 2048, max_context: int = 4096,
                  max_output: int = 256, seed: int = 0, device: int = 0,
-                 modules: list[ModuleWeights] | None = None, base: ModuleWeights | None = None):
+                 modules: list[ModuleWeights] | None = None, base: ModuleWeights | None = None,
+                 prefill_batch: bool = True):
         self.cfg, self.mode, self.model_ids = cfg, mode, list(model_ids)
+        self.prefill_batch = prefill_batch
+        self._pending: list = []
+        self._pending_slots: set = set()
         M = len(model_ids)
         self.router = Router(mode, model_ids)
         self.mods = modules or [ModuleWeights(cfg, seed + 1 + i, device=device) for i in range(M)]
@@ -143,13 +147,21 @@ class AgentServer:
         return torch.from_numpy((ctx % self.cfg.vocab).astype(np.int64)).to(self.dev, non_blocking=True)
 
     def _prefill(self, req: _Req, now_us: int):
-        """cluster.py:322-366 on the GPU. Returns (held handles, page table,
-        matched tokens, prefilled tokens, decode row)."""
+        """cluster.py:322-366 pool side: lookup (pins), insert + pin of the
+        new blocks, decode row claimed. The forward itself is queued in
+        self._pending and run by _flush_prefills (batched per prefill
+        module). Returns (held handles, page table, matched tokens,
+        prefilled tokens, decode row), or None on CapacityExhausted."""
         worker = self.router.route_prefill(req.rec, [0] * len(self.pools))
         pool = self.pools[worker]
         ns = self.router.prefill_namespace(req.rec.model_id)
         n = len(req.ctx)
         m, chain = pool.longest_prefix_match(ns, req.ctx, now_us)
+        base = pool.page_base
+        hit = [base + s for s in chain.slots.tolist()]
+        if self._pending_slots.intersection(hit):
+            # this prefix is written by a forward still queued in the batch
+            self._flush_prefills()
         try:
             new = pool.insert(ns, req.ctx, now_us)
         except pool.CapacityError:
@@ -157,20 +169,41 @@ class AgentServer:
             pool.release(chain)
             return None
         pool.pin(new, now_us)
-        base = pool.page_base
-        pages = [base + s for s in chain.slots.tolist()] + [base + s for s in new.slots.tolist()]
+        fresh = [base + s for s in new.slots.tolist()]
+        pages = hit + fresh
         row = self._row_of_module(req.model_idx)
         if n % PAGE_TOKENS:
             pages.append(self.tail_page[row])
         # partial prefill from the last cached full block; the tail block is recomputed
         pos0 = min(m, (n // PAGE_TOKENS) * PAGE_TOKENS)
-        runner = self.prefillers[0 if self.base is not None else req.model_idx]
-        pt = torch.tensor(pages, dtype=torch.int32, device=self.dev)
         if n > pos0:
-            ev = self._events("prefill")
-            runner.run(self._vocab_ids(req.ctx[pos0:]), pos0, pt)
-            ev[1].record()
+            ri = 0 if self.base is not None else req.model_idx
+            self._pending.append((ri, self._vocab_ids(req.ctx[pos0:]), pos0, pages))
+            self._pending_slots.update(fresh)
+            if not self.prefill_batch:
+                self._flush_prefills()
         return [(pool, chain), (pool, new)], pages, m, n - pos0, row
+
+    def _flush_prefills(self) -> None:
+        """Run the queued forwards: one batched forward per prefill module and
+        <= max_context stacked tokens (small partial
+        prefills share each layer's weight stream)."""
+        by_runner: dict[int, list] = {}
+        for ri, toks, pos0, pages in self._pending:
+            by_runner.setdefault(ri, []).append((toks, pos0, pages))
+        self._pending, self._pending_slots = [], set()
+        for ri, seqs in by_runner.items():
+            runner = self.prefillers[ri]
+            chunk, tot = [], 0
+            for sq in seqs + [None]:
+                if sq is None or (chunk and tot + int(sq[0].shape[0]) > runner.max_tokens):
+                    ev = self._events("prefill")
+                    runner.run_batch(chunk)
+                    ev[1].record()
+                    chunk, tot = [], 0
+                if sq is not None:
+                    chunk.append(sq)
+                    tot += int(sq[0].shape[0])
 
     def _events(self, kind: str):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -268,6 +301,8 @@ class AgentServer:
                 self.batch.update_row(row, len(req.ctx) - 1, pages, self._first[row])
                 dirty = True
                 progressed = True
+            if self._pending:
+                self._flush_prefills()
             busy = [r for r in self.rows if r.req is not None]
             if busy:
                 ev = self._events("decode")

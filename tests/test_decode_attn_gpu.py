@@ -12,7 +12,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0):
+def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0, dirty_ws=False):
     from paper_2602_12029_b200 import _lib
     from paper_2602_12029_b200.model import (DecodeBatch, DecodeRow, KVCache, LlamaConfig,
                                              SessionSpec)
@@ -47,6 +47,8 @@ def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0):
     wsb = ctypes.c_int64()
     _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), nkv, splits, ctypes.byref(wsb)))
     ws = torch.zeros(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
+    if dirty_ws:  # stale partials / directory from earlier launches must not leak in
+        ws.uniform_(-50.0, 50.0)
     _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), nq, layer, kv.layout(), splits,
                                    ws.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
@@ -97,3 +99,23 @@ def test_gqa2_tiny_shape():
 
 def test_single_token_shared():
     _case(32, 8, [1], [4], [0, 0, 0, 0], 1, seed=4)
+
+
+@pytest.mark.parametrize("case", [
+    (32, 8, [4095], [4], [0, 3, 17, 255]),
+    (32, 8, [4095] * 8, [4] * 8, [255] * 32),                     # the bench shape (8 sessions)
+    (32, 8, [1000, 37, 513], [2, 3, 1], [0, 5, 16, 40, 1, 200]),
+    (2, 1, [99, 300], [2, 2], [0, 1, 15, 31]),
+    (32, 8, [1], [4], [0, 0, 0, 0]),
+    (32, 8, [0, 5, 0, 3000], [1, 1, 1, 1], [0, 7, 200, 16]),      # rows without a shared prefix
+    (32, 8, [37 * i % 700 for i in range(40)], [1] * 40, [i % 33 for i in range(40)]),  # agent-style
+    (32, 8, [12000, 3], [8, 8], [i * 11 for i in range(16)]),     # one long group, one tiny
+    (2, 1, [99], [2], [16, 17]),                                   # fewer pages than SMs (empty runs)
+])
+def test_stream_k_schedule(case):
+    """splits = 0: the stream-K partial kernel (runs of equal page counts
+    across (session, KV head) groups, segment partials in slot cta + group,
+    merge through the group directory) on the shapes above; the fan-out
+    (> 32 rows per KV head) sessions fall back to fixed splits."""
+    nq, nkv, lens, rps, priv = case
+    _case(nq, nkv, lens, rps, priv, 0, seed=len(lens), dirty_ws=True)

@@ -23,6 +23,16 @@ def _rand(*shape, std=1.0, seed=0):
     return (torch.randn(*shape, device="cuda", generator=g) * std).to(torch.bfloat16)
 
 
+@pytest.fixture
+def split_ws():
+    """Bind the split-K workspace for the test, unbind afterwards."""
+    L = _lib()
+    L.bind_gemm_workspace(torch.device("cuda", 0))
+    yield
+    L.check(L.load().psk_gemm_bind_workspace(None, 0))
+    L._gemm_ws = None
+
+
 def _gemm(A, B, epi, out, ldo):
     L = _lib()
     L.check(L.load().psk_gemm(A.data_ptr(), B.data_ptr(), A.shape[0], B.shape[0], A.shape[1], epi,
@@ -67,8 +77,9 @@ def test_gemm_silu_mul_interleaved():
     assert (out.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item() + 1e-3
 
 
-@pytest.mark.parametrize("nq,nkv,T,pos0", [(2, 1, 100, 0), (32, 8, 300, 32), (32, 8, 17, 4080)])
-def test_gemm_qkv_rope_paged_kv(nq, nkv, T, pos0):
+@pytest.mark.parametrize("nq,nkv,T,pos0", [(2, 1, 100, 0), (32, 8, 300, 32), (32, 8, 17, 4080), (32, 8, 4096, 16)])
+def test_gemm_qkv_rope_paged_kv(nq, nkv, T, pos0, split_ws):
+    """(T = 4096 at the 8B width: 768 tiles, the last-wave tiles run split-K.)"""
     from paper_2602_12029_b200.model import KVCache, LlamaConfig, rope_table
     from oracle.model import _rope, rope_cos_sin
     d = 256 if nq == 2 else 4096
@@ -100,3 +111,31 @@ def test_gemm_qkv_rope_paged_kv(nq, nkv, T, pos0):
     # layer 0 untouched
     k0, _ = kv.read_positions(pages, 0, T, start=pos0)
     assert k0.abs().max().item() == 0
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 4096, 4096), (4096, 6144, 4096), (2560, 2048, 4096),
+                                   (4096, 4096, 14336), (4000, 4096, 1024)])
+def test_gemm_split_k_tail(M, N, K, split_ws):
+    """Last-wave tiles split along K (workspace bound): store / residual add /
+    SiLU*mul epilogues; repeated launches (the tail counters re-arm)."""
+    A, B = _rand(M, K, seed=11), _rand(N, K, std=0.02, seed=12)
+    ref = A.float() @ B.float().T
+    scale = ref.abs().max().item()
+    out = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+    for _ in range(2):
+        _gemm(A, B, 1, out, N)
+    torch.cuda.synchronize()
+    assert (out - ref).abs().max().item() <= 2e-3 * scale + 1e-4
+    h = torch.randn(M, N, device="cuda")
+    want = h + ref
+    _gemm(A, B, 2, h, N)
+    torch.cuda.synchronize()
+    assert (h - want).abs().max().item() <= 2e-3 * want.abs().max().item() + 1e-4
+    F = N // 2
+    silu_ref = ref.view(M, -1, 2, 8)
+    silu_ref = (torch.nn.functional.silu(silu_ref[:, :, 0]) * silu_ref[:, :, 1]).reshape(M, F)
+    o = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+    _gemm(A, B, 3, o, F)
+    torch.cuda.synchronize()
+    assert (o.float() - silu_ref).abs().max().item() <= 1e-2 * silu_ref.abs().max().item() + 1e-3
+    assert int(_lib()._gemm_ws[:4096].view(torch.int32).abs().sum().item()) == 0

@@ -102,3 +102,50 @@ def test_shared_prefill_then_decode_modules(shape):
                 top2 = torch.topk(lgs[t], 2).values
                 assert float(top2[0] - top2[1]) <= 2e-2 * float(lgs[t].abs().max())
     assert flips <= n_mod
+
+
+@pytest.mark.parametrize("shape", ["tiny", "8b2"])
+def test_batched_partial_prefill_bit_identical(shape):
+    """run_batch (stacked varlen rows: per-row RoPE position + KV slot in the
+    QKV epilogue, one K3 CTA per (sequence, q-block)) writes exactly the KV
+    and hidden rows that one run() per sequence writes: partial prefills
+    after cached prefixes (pos0 > 0, block-aligned and mid-page tails),
+    scattered page tables, sequences longer than one q-block."""
+    from paper_2602_12029_b200.model import KVCache, LlamaConfig, ModuleWeights, PrefillRunner
+    cfg = LlamaConfig.tiny() if shape == "tiny" else LlamaConfig.llama8b(n_layers=2, max_pos=1024)
+    base = ModuleWeights(cfg, 5, with_head=False)
+    rng = np.random.default_rng(7)
+    specs = [(0, 300), (64, 21), (32, 1), (160, 77)]  # (pos0, new tokens)
+    n_pages = sum((p + n + 15) // 16 for p, n in specs) + 4
+    perm = rng.permutation(n_pages).tolist()
+    seqs, pts = [], []
+    for p0, n in specs:
+        pt = [perm.pop() for _ in range((p0 + n + 15) // 16)]
+        pts.append(pt)
+        seqs.append((torch.from_numpy(rng.integers(0, cfg.vocab, n)).cuda(), p0, pt))
+    prefix = [torch.from_numpy(rng.integers(0, cfg.vocab, p0)).cuda() for p0, _ in specs]
+    outs = []
+    for batched in (False, True):
+        kv = KVCache(cfg, n_pages)
+        kv.data.zero_()
+        pre = PrefillRunner(cfg, base, kv, max_tokens=1024)
+        for (p0, _), pt, pf in zip(specs, pts, prefix):  # cached prefixes, one sequence each
+            if p0:
+                pre.run(pf, 0, torch.tensor(pt, dtype=torch.int32, device="cuda"))
+        hs = []
+        if batched:
+            pre.run_batch(seqs)
+            off = 0
+            for _, n in specs:
+                hs.append(pre.h[off:off + n].clone())
+                off += n
+        else:
+            for toks, p0, pt in seqs:
+                pre.run(toks, p0, torch.tensor(pt, dtype=torch.int32, device="cuda"))
+                hs.append(pre.h[:toks.shape[0]].clone())
+        torch.cuda.synchronize()
+        outs.append((kv.data.clone(), hs))
+    (kv_a, h_a), (kv_b, h_b) = outs
+    assert torch.equal(kv_a, kv_b)
+    for a, b in zip(h_a, h_b):
+        assert torch.equal(a, b)

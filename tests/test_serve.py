@@ -23,11 +23,15 @@ def test_summarize_nearest_rank_and_window():
     t_end = max(r.done_us for r in recs)
     win = [r for r in recs if r.done_us >= 0.1 * t_end]
     assert abs(s["req_per_s"] - len(win) / (0.9 * t_end / 1e6)) < 1e-9
-    assert summarize([]) == {"completed": 0}
+    assert summarize([]) == {"completed": 0, "failed": 0}
 
 
 @pytest.mark.gpu
-def test_agent_workload_tiny_both_modes():
+@pytest.mark.parametrize("rows,batch", [(4, False), (4, True), (12, True)])
+def test_agent_workload_tiny_both_modes(rows, batch):
+    """Both serving modes through the real engine: FCFS one-forward-per-request
+    prefills and batched partial prefills; 12 rows per module runs the decode
+    GEMVs on K5-TC."""
     from paper_2602_12029_b200 import workload as wl
     from paper_2602_12029_b200.model import LlamaConfig, ModuleWeights
     from paper_2602_12029_b200.router import ServingMode
@@ -41,12 +45,14 @@ def test_agent_workload_tiny_both_modes():
     base = ModuleWeights(cfg, 9, with_head=False)
     res = {}
     for mode in (ServingMode.BASELINE, ServingMode.PREFILLSHARE):
-        srv = AgentServer(cfg, models, mode, rows_per_module=4, pool_pages_per_worker=512,
-                          max_context=4096, max_output=128, modules=mods, base=base)
+        srv = AgentServer(cfg, models, mode, rows_per_module=rows, pool_pages_per_worker=512,
+                          max_context=4096, max_output=128, modules=mods, base=base, prefill_batch=batch)
         recs = srv.run(sessions)
         assert len(recs) == n_req and all(r.done_us is not None for r in recs)
         assert all(r.out_tokens == 128 for r in recs)
         res[mode] = summarize(recs)
+        gt = srv.gpu_time()
+        assert gt["decode_steps"] > 0 and gt["prefill_calls"] > 0
     b, p = res[ServingMode.BASELINE], res[ServingMode.PREFILLSHARE]
     assert p["prefill_tokens"] < b["prefill_tokens"]
     assert p["prefix_hit_ratio"] > b["prefix_hit_ratio"]

@@ -36,7 +36,10 @@ def attn(shared, modules, reps=4, sessions=1):
     q = torch.randn(sessions * modules, 32, 128, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)
     from paper_2602_12029_b200.model import attn_splits
+    import os
     ns = attn_splits(n_sh + modules, 8 * sessions, torch.cuda.get_device_properties(0).multi_processor_count)
+    if os.environ.get("PSK_SPLITS") is not None:  # 0 = stream-K
+        ns = int(os.environ["PSK_SPLITS"])
     wsb = C.c_int64()
     _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), 8, ns, C.byref(wsb)))
     ws = torch.zeros(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")

@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--time-scale", type=float, default=1.0)
     ap.add_argument("--pool-pages", type=int, default=7500)
+    ap.add_argument("--no-batch", action="store_true", help="one prefill forward per request (FCFS)")
+    ap.add_argument("--modes", default="baseline,prefillshare")
     a = ap.parse_args()
     cfg = LlamaConfig.llama8b(max_pos=4096 + 512) if a.shape == "8b" else LlamaConfig.tiny(max_pos=4096)
     models = list(wl.DEFAULT_MODELS)
@@ -40,15 +42,17 @@ def main():
     out = {"workload": {"pattern": a.pattern, "rate": a.rate, "duration_s": a.duration,
                         "sessions": len(sessions), "requests": sum(s.total_requests for s in sessions)},
            "shape": a.shape}
-    for mode in (ServingMode.BASELINE, ServingMode.PREFILLSHARE):
+    out["prefill_batch"] = not a.no_batch
+    for mode in (ServingMode(m) for m in a.modes.split(",")):
         srv = AgentServer(cfg, models, mode, rows_per_module=a.rows, pool_pages_per_worker=a.pool_pages,
-                          max_context=4096, max_output=256, modules=mods, base=base)
+                          max_context=4096, max_output=256, modules=mods, base=base,
+                          prefill_batch=not a.no_batch)
         recs = srv.run(sessions, time_scale=a.time_scale)
         out[mode.value] = summarize(recs)
         out[mode.value]["gpu_time"] = srv.gpu_time()
         del srv
         torch.cuda.empty_cache()
-    b, p = out["baseline"], out["prefillshare"]
+    b, p = out.get("baseline", {}), out.get("prefillshare", {})
     if b.get("req_per_s") and p.get("req_per_s"):
         out["throughput_ratio"] = p["req_per_s"] / b["req_per_s"]
         out["p95_ratio"] = b["p95_e2e_ms"] / p["p95_e2e_ms"]
