@@ -758,6 +758,276 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 }  // namespace sk
 
+
+// ------------------------------------------- all-heads partial kernel (H) --
+// The (session, split) CTA of this kernel owns ALL KV heads of its pages:
+// one 4-D TMA box per page brings the page's whole K|V block of this layer
+// (nkv heads x 16 tokens x 128 dims x K|V = 64 KiB at the 8B shape, one
+// contiguous run) and consumer warp h runs the flash loop of KV head h over
+// every page of the split. Versus decode_attn_partial (CTA = one head, 8 KiB
+// boxes) this reads DRAM in 64 KiB runs, needs 8x fewer CTAs for the same
+// work (agent serving: one session per row, 8 heads -> 2048 small CTAs
+// become 256) and no cross-warp fold (each warp owns its head's softmax
+// state). Used when every session has <= 16 query rows per KV head (one m16
+// tile, e.g. 4 modules x 4 GQA heads); the partial format is the same as
+// decode_attn_partial's, so decode_attn_merge is shared.
+namespace hk {
+
+constexpr int NST = 3;
+constexpr int MAXKV = 8;                       // consumer warps = KV heads
+constexpr int MAXP = 2048;
+__host__ __device__ constexpr int stage_bytes(int nkv) { return 2 * nkv * TILE; }  // K|V x heads x 4 KiB
+constexpr int STAGE_MAX = stage_bytes(MAXKV);   // 64 KiB
+constexpr int OFF_Q = 2 * STAGE_MAX;            // Q is staged in ring stage 2 before the stream starts
+constexpr int OFF_BAR = NST * STAGE_MAX;         // 192 KiB
+constexpr int OFF_PG = OFF_BAR + 2 * NST * 8;
+constexpr int SMEM = OFF_PG + 1024 * 4 + 1024;  // (page ids of up to 1024 pages staged)
+constexpr int MAXP_SMEM = 1024;
+constexpr int THREADS = (MAXKV + 1) * 32;
+
+__global__ void __launch_bounds__(THREADS, 1)
+    decode_attn_heads(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ Params p) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* empty = full + NST;
+  int* s_page = reinterpret_cast<int*>(smem + OFF_PG);
+  __shared__ int s_rows[MAXR], s_plen[MAXR], s_pstart[MAXR + 1];
+  __shared__ int s_ps, s_ls, s_total;
+
+  trace_stamp(0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkv = p.kv.n_kv_heads;
+  const int item = blockIdx.x;
+  const int j_split = item % p.ns;
+  const int sess = item / p.ns;
+  const int nr = p.b.sess_nrows[sess];
+  const int G = nr * p.grp;  // query rows per KV head (<= 16)
+  const int STG = stage_bytes(nkv);
+
+  if (threadIdx.x < nr) {
+    const int r = p.b.sess_rows[(int64_t)sess * p.b.max_rows_per_sess + threadIdx.x];
+    s_rows[threadIdx.x] = r;
+    s_plen[threadIdx.x] = p.b.priv_len[r] + 1;  // includes the token appended this step
+  } else if (threadIdx.x == 32) {
+    s_ls = p.b.sess_len[sess];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int Ps = (s_ls + PT - 1) / PT;
+    s_ps = Ps;
+    int acc = Ps;
+    for (int i = 0; i < nr; ++i) {
+      s_pstart[i] = acc;
+      acc += (s_plen[i] + PT - 1) / PT;
+    }
+    s_pstart[nr] = acc;
+    s_total = nr > 0 ? acc : 0;
+    for (int st = 0; st < NST; ++st) {
+      tma::mbar_init(&full[st], 1);
+      tma::mbar_init(&empty[st], nkv);
+    }
+    tma::fence_mbar_init();
+    tma::prefetch_map(&kvmap);
+  }
+  __syncthreads();
+  trace_stamp(1);
+  const int total = s_total;
+  const int k0 = (int)((int64_t)j_split * total / p.ns);
+  const int k1 = (int)((int64_t)(j_split + 1) * total / p.ns);
+  const int np = k1 - k0;
+  auto page_of = [&](int k) -> int {
+    if (k < s_ps) return p.b.sess_pages[(int64_t)sess * p.b.max_sess_pages + k];
+    int i = 0;
+    while (k >= s_pstart[i + 1]) ++i;
+    return p.b.row_pages[(int64_t)s_rows[i] * p.b.max_row_pages + (k - s_pstart[i])];
+  };
+  for (int j = threadIdx.x; j < np && j < MAXP_SMEM; j += THREADS) s_page[j] = page_of(k0 + j);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // q / the appended K,V come from rope_append
+  // Q of every head: rows g of head h at [h][16][256 B] (swizzled)
+  {
+    // all loads in flight first (one latency round trip), then the stores
+    constexpr int QPER = (MAXKV * 16 * 16 + THREADS - 1) / THREADS;
+    const uint32_t qs = smem_u32(smem + OFF_Q);
+    uint4 v[QPER];
+#pragma unroll
+    for (int u = 0; u < QPER; ++u) {
+      const int e = threadIdx.x + u * THREADS;
+      const int hh = e >> 8, g = (e >> 4) & 15, c = e & 15;
+      v[u] = make_uint4(0, 0, 0, 0);
+      if (hh < nkv && g < G)
+        v[u] = __ldg(reinterpret_cast<const uint4*>(p.q + ((int64_t)s_rows[g / p.grp] * p.nq + hh * p.grp + g % p.grp) *
+                                                               HD + c * 8));
+    }
+#pragma unroll
+    for (int u = 0; u < QPER; ++u) {
+      const int e = threadIdx.x + u * THREADS;
+      const int hh = e >> 8, g = (e >> 4) & 15, c = e & 15;
+      if (hh < nkv)
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(qs + hh * 4096 + swz256(g, c)), "r"(v[u].x),
+                     "r"(v[u].y), "r"(v[u].z), "r"(v[u].w));
+    }
+  }
+  __syncthreads();
+  // Q fragments -> registers before the producer may overwrite stage 2
+  uint32_t qa[8][4];
+  if (warp < nkv) {
+    const uint32_t qs = smem_u32(smem + OFF_Q) + warp * 4096;
+    const int qrow = ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)
+      ldmatrix_x4(qs + swz256(qrow, 2 * ks + (lane >> 4)), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+  }
+  __syncthreads();
+  trace_stamp(2);
+
+  if (warp == MAXKV) {
+    // ---------------- TMA producer: one box per page, all heads ----------------
+    if (lane == 0) {
+      for (int j = 0; j < np; ++j) {
+        const int st = j % NST;
+        tma::mbar_wait(&empty[st], ((j / NST) & 1) ^ 1);
+        const int page = j < MAXP_SMEM ? s_page[j] : page_of(k0 + j);
+        const int row0 = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv) * PT);
+        tma::mbar_expect_tx(&full[st], STG);
+        tma::load_4d(&kvmap, &full[st], smem + st * STAGE_MAX, 0, row0, 0, 0);
+      }
+    }
+    __syncwarp();
+  } else if (warp < nkv) {
+    const int h = warp;
+    const uint32_t ring = smem_u32(smem);
+    const int half_stride = nkv * PT * 128;  // bytes between the dims 0-63 and 64-127 boxes
+    float o[16][4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    const int gA = lane >> 2, gB = gA + 8;
+    const int ownA = gA < G ? gA / p.grp : -2, ownB = gB < G ? gB / p.grp : -2;
+    for (int j = 0; j < np; ++j) {
+      const int st = j % NST;
+      int limit, owner;
+      {
+        const int k = k0 + j;
+        if (k < s_ps) {
+          limit = min(PT, s_ls - k * PT);
+          owner = -1;
+        } else {
+          int i = 0;
+          while (k >= s_pstart[i + 1]) ++i;
+          limit = min(PT, s_plen[i] - (k - s_pstart[i]) * PT);
+          owner = i;
+        }
+      }
+      tma::mbar_wait(&full[st], (j / NST) & 1);
+      // head h: K rows [16h, 16h+16) of the box, V nkv*16 rows later
+      const uint32_t kt = ring + st * STAGE_MAX + h * (PT * 128);
+      const uint32_t vt = kt + 2 * half_stride;
+      float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      {
+        const int mi = lane >> 3, ri = lane & 7;
+        const int tok = (mi >> 1) * 8 + ri;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const int c16 = 2 * ks + (mi & 1);
+          uint32_t b0, b1, b2, b3;
+          ldmatrix_x4(kt + (c16 >> 3) * half_stride + tok * 128 + (((c16 & 7) ^ (tok & 7)) << 4), b0, b1, b2, b3);
+          mma_bf16_16816(sc[0], qa[ks], b0, b1);
+          mma_bf16_16816(sc[1], qa[ks], b2, b3);
+        }
+      }
+      const bool okA = owner < 0 || owner == ownA;
+      const bool okB = owner < 0 || owner == ownB;
+      const int cb = (lane & 3) * 2;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int t = nt * 8 + cb + (e & 1);
+          const bool ok = t < limit && (e < 2 ? okA : okB);
+          sc[nt][e] = ok ? sc[nt][e] * p.scale_log2 : -INFINITY;
+        }
+      float mx0 = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
+      float mx1 = fmaxf(fmaxf(sc[0][2], sc[0][3]), fmaxf(sc[1][2], sc[1][3]));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
+      const float r0 = n0 == -INFINITY ? 0.f : n0, r1 = n1 == -INFINITY ? 0.f : n1;
+      const float c0f = fast_exp2(m0 - r0), c1f = fast_exp2(m1 - r1);
+      m0 = n0;
+      m1 = n1;
+      float pr[2][4];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        pr[nt][0] = fast_exp2(sc[nt][0] - r0);
+        pr[nt][1] = fast_exp2(sc[nt][1] - r0);
+        pr[nt][2] = fast_exp2(sc[nt][2] - r1);
+        pr[nt][3] = fast_exp2(sc[nt][3] - r1);
+      }
+      l0 = l0 * c0f + ((pr[0][0] + pr[0][1]) + (pr[1][0] + pr[1][1]));
+      l1 = l1 * c1f + ((pr[0][2] + pr[0][3]) + (pr[1][2] + pr[1][3]));
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        o[i][0] *= c0f;
+        o[i][1] *= c0f;
+        o[i][2] *= c1f;
+        o[i][3] *= c1f;
+      }
+      uint32_t pa[4];
+      pa[0] = pack_bf16(pr[0][0], pr[0][1]);
+      pa[1] = pack_bf16(pr[0][2], pr[0][3]);
+      pa[2] = pack_bf16(pr[1][0], pr[1][1]);
+      pa[3] = pack_bf16(pr[1][2], pr[1][3]);
+      {
+        const int mi = lane >> 3, ri = lane & 7;
+        const int tok = (mi & 1) * 8 + ri;
+#pragma unroll
+        for (int np2 = 0; np2 < 8; ++np2) {
+          const int c16 = 2 * np2 + (mi >> 1);
+          uint32_t b0, b1, b2, b3;
+          ldmatrix_x4_trans(vt + (c16 >> 3) * half_stride + tok * 128 + (((c16 & 7) ^ (tok & 7)) << 4), b0, b1,
+                            b2, b3);
+          mma_bf16_16816(o[2 * np2], pa, b0, b1);
+          mma_bf16_16816(o[2 * np2 + 1], pa, b2, b3);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) tma::mbar_arrive(&empty[st]);
+    }
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    // partial (m, l, o) of head h's rows: same slots as decode_attn_partial
+    const int64_t base = ((int64_t)(sess * nkv + h) * p.ns + j_split) * GMAX;
+    const int cb = (lane & 3) * 2;
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      const int col = nt * 8 + cb;
+      if (gA < G) *reinterpret_cast<float2*>(p.po + (base + gA) * HD + col) = make_float2(o[nt][0], o[nt][1]);
+      if (gB < G) *reinterpret_cast<float2*>(p.po + (base + gB) * HD + col) = make_float2(o[nt][2], o[nt][3]);
+    }
+    if ((lane & 3) == 0) {
+      if (gA < G) {
+        p.pm[base + gA] = m0;
+        p.pl[base + gA] = l0;
+      }
+      if (gB < G) {
+        p.pm[base + gB] = m1;
+        p.pl[base + gB] = l1;
+      }
+    }
+  }
+  trace_stamp(3);
+  asm volatile("griddepcontrol.launch_dependents;");
+  trace_stamp(4);
+}
+
+}  // namespace hk
+
 // Merge: one CTA per (row, q head), one thread per head dim; every split's
 // (m, l, o) is loaded up front (32 splits in flight per thread) and folded by
 // log-sum-exp. Launched with programmatic dependent launch: it is scheduled
@@ -1332,10 +1602,10 @@ int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out, int kind) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
     // (dim, token row, half, K|V): the V tile of a (page, layer, head) sits
-    // n_kv_heads tiles after its K tile
+    // n_kv_heads tiles after its K tile; KV_PAGE4D_ALL takes all heads' rows
     cuuint64_t dims[4] = {64, rows, 2, 2};
     cuuint64_t strides[3] = {(cuuint64_t)HD * 2, 128, (cuuint64_t)kv.n_kv_heads * PT * HD * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)PT, 2, 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)(kind == KV_PAGE4D_ALL ? PT * kv.n_kv_heads : PT), 2, 2};
     cuuint32_t es[4] = {1, 1, 1, 1};
     r = enc(&cached[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, kv.base, dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1368,14 +1638,24 @@ static int sm_count() {
   return sms;
 }
 
+// Partial slots the workspace holds: enough for the caller's fixed splits,
+// the stream-K schedule (grid + groups) and the all-heads kernel (one
+// wave of (session, split) CTAs: groups x sms / n_sess).
+static int64_t ws_slots(const psk_decode_batch* b, int32_t n_kv_heads, int32_t splits) {
+  const int64_t groups = (int64_t)b->n_sess * n_kv_heads;
+  const int sms = sm_count();
+  int64_t slots = (int64_t)sms + groups;
+  if (splits > 0 && groups * splits > slots) slots = groups * splits;
+  const int64_t hsplit = b->n_sess > 0 ? (sms / b->n_sess > 1 ? sms / b->n_sess : 1) : 1;
+  if (groups * hsplit > slots) slots = groups * hsplit;
+  return slots;
+}
+
 int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int32_t splits,
                               int64_t* bytes) {
   PSK_CHECK_ARG(b && bytes && splits >= 0, "psk_decode_attn_workspace: bad args");
   const int64_t groups = (int64_t)b->n_sess * n_kv_heads;
-  // stream-K (splits == 0): one partial slot per (CTA, group) segment, at
-  // most grid + groups of them, plus the per-group CTA directory
-  const int64_t items = splits > 0 ? groups * splits : sm_count() + groups;
-  *bytes = items * GMAX * (HD + 2) * 4 + (splits > 0 ? 0 : groups * 2 * 4 + 16);
+  *bytes = ws_slots(b, n_kv_heads, splits) * GMAX * (HD + 2) * 4 + groups * 2 * 4 + 16;
   return PSK_OK;
 }
 
@@ -1392,10 +1672,18 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   // (32k x 16 modules: 36.7 us vs 48.6 us); up to 32 rows mma.sync is faster
   // (32k x 8: 30.1 vs 32.0 us). PSK_ATTN_HMMA=1 keeps mma.sync everywhere.
   static const bool force_hmma = getenv("PSK_ATTN_HMMA") != nullptr;
+  static const bool no_heads = getenv("PSK_ATTN_PER_HEAD") != nullptr;
   const bool use_tc = grp * b->max_rows_per_sess > 32 && !force_hmma;
   const int sms = sm_count();
   const int64_t groups = (int64_t)b->n_sess * kv.n_kv_heads;
-  const int64_t slots = splits > 0 ? groups * splits : sms + groups;  // workspace partial slots
+  const int64_t slots = ws_slots(b, kv.n_kv_heads, splits);
+  // <= 16 query rows per KV head everywhere and at least one (session, head)
+  // group per SM: the all-heads kernel (CTA = (session, split), 64 KiB page
+  // boxes, no fold). With fewer groups the per-head kernel's finer splits win
+  // (8 sessions: 42.7 vs 45.8 us; 32 sessions: 152 vs 144 us; 1 session:
+  // 12.4 vs 21 us at 4k).
+  const bool use_heads = !use_tc && !no_heads && splits > 0 && grp * b->max_rows_per_sess <= 16 &&
+                         kv.n_kv_heads <= hk::MAXKV && (int64_t)b->n_sess * kv.n_kv_heads >= sm_count();
   // stream-K mode (splits == 0) for the mma.sync path when the session
   // tables and one run's page list fit in shared memory; otherwise (and for
   // the tcgen05 path) fixed splits that fit the same workspace
@@ -1406,8 +1694,14 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
     stream_k = !use_tc && b->n_sess <= sk::MAXS && run_bound <= sk::MAXP;
     if (!stream_k) splits = (int)(sms / groups) > 1 ? (int)(sms / groups) : 1;  // one wave, fits the slots
   }
+  int hsplit = 1;
+  if (use_heads) {
+    const int64_t max_pages = (int64_t)b->max_sess_pages + (int64_t)b->max_rows_per_sess * b->max_row_pages;
+    hsplit = sms / b->n_sess > 1 ? sms / b->n_sess : 1;
+    if (hsplit > max_pages / 4) hsplit = max_pages / 4 > 1 ? (int)(max_pages / 4) : 1;
+  }
   CUtensorMap map, vmap;
-  int rc = psk::kv_tensor_map(kv, &map, use_tc ? psk::KV_BOX2D : psk::KV_PAGE4D);
+  int rc = psk::kv_tensor_map(kv, &map, use_tc ? psk::KV_BOX2D : (use_heads ? psk::KV_PAGE4D_ALL : psk::KV_PAGE4D));
   if (!rc && use_tc) rc = psk::kv_tensor_map(kv, &vmap, psk::KV_TILE3D);
   if (rc) return rc;
   Params p;
@@ -1418,8 +1712,9 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   p.nq = n_q_heads;
   p.grp = grp;
   p.layer = layer;
-  p.ns = stream_k ? 0 : splits;
-  const int64_t items = stream_k ? sms : groups * splits;  // CTAs of the partial kernel
+  p.ns = stream_k ? 0 : (use_heads ? hsplit : splits);
+  // CTAs of the partial kernel
+  const int64_t items = stream_k ? sms : (use_heads ? (int64_t)b->n_sess * hsplit : groups * splits);
   float* ws = reinterpret_cast<float*>(workspace);
   p.pm = ws;
   p.pl = ws + slots * GMAX;
@@ -1433,6 +1728,7 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
     PSK_CUDA_TRY(cudaFuncSetAttribute(decode_attn_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SMEM));
     PSK_CUDA_TRY(cudaFuncSetAttribute(sk::decode_attn_sk, cudaFuncAttributeMaxDynamicSharedMemorySize, sk::SMEM));
+    PSK_CUDA_TRY(cudaFuncSetAttribute(hk::decode_attn_heads, cudaFuncAttributeMaxDynamicSharedMemorySize, hk::SMEM));
     init = true;
   }
   const bool tr = psk::trace_arm((int)items);
@@ -1458,6 +1754,10 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = sk::SMEM;
     PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, sk::decode_attn_sk, map, p));
+  } else if (use_heads) {
+    cfg.blockDim = dim3(hk::THREADS);
+    cfg.dynamicSmemBytes = hk::SMEM;
+    PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, hk::decode_attn_heads, map, p));
   } else {
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = SMEM;

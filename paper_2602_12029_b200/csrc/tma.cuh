@@ -110,6 +110,8 @@ namespace psk {
 //  KV_PAGE4D: 4D (64 dim, 16 token, 2 halves, K|V), one box = the whole
 //             8 KiB K+V of one (page, layer, head), landing as
 //             [K half0 | K half1 | V half0 | V half1] x [16][128 B].
-enum KvMapKind { KV_BOX2D = 0, KV_TILE3D = 1, KV_PAGE4D = 2 };
+//  KV_PAGE4D_ALL: as KV_PAGE4D with all n_kv_heads heads' token rows in one
+//             box (the page's whole K|V block of a layer, 64 KiB at 8 heads).
+enum KvMapKind { KV_BOX2D = 0, KV_TILE3D = 1, KV_PAGE4D = 2, KV_PAGE4D_ALL = 3 };
 int kv_tensor_map(const psk_kv_layout& kv, CUtensorMap* out, int kind = KV_BOX2D);
 }  // namespace psk

@@ -119,3 +119,15 @@ def test_stream_k_schedule(case):
     (> 32 rows per KV head) sessions fall back to fixed splits."""
     nq, nkv, lens, rps, priv = case
     _case(nq, nkv, lens, rps, priv, 0, seed=len(lens), dirty_ws=True)
+
+
+@pytest.mark.parametrize("case", [
+    (32, 8, [4095] * 20, [4] * 20, [255] * 80),                      # 160 groups: all-heads kernel
+    (32, 8, [37 * i % 900 + 1 for i in range(24)], [1, 2, 4] * 8, [(7 * i) % 70 for i in range(56)]),
+    (32, 8, [0] * 19 + [300], [1] * 20, [5 * i for i in range(20)]),  # empty shared prefixes
+])
+def test_all_heads_kernel(case):
+    """>= one (session, KV head) group per SM and <= 16 query rows per head:
+    the (session, split) all-heads kernel (64 KiB page boxes, warp = head)."""
+    nq, nkv, lens, rps, priv = case
+    _case(nq, nkv, lens, rps, priv, 1, seed=len(lens))
