@@ -1032,7 +1032,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // (m, l, o) is loaded up front (32 splits in flight per thread) and folded by
 // log-sum-exp. Launched with programmatic dependent launch: it is scheduled
 // while the partial kernel drains and waits on griddepcontrol for its data.
-constexpr int MERGE_U = 32;
+constexpr int MERGE_U = 8;  // partials in flight per iteration (32 held 124 registers: 4 CTAs/SM)
 __global__ void __launch_bounds__(HD) decode_attn_merge(const __grid_constant__ Params p) {
   const int r = blockIdx.x, qh = blockIdx.y, d = threadIdx.x;
   const int nkv = p.kv.n_kv_heads;
