@@ -27,6 +27,7 @@ generated ones: cluster.py:453-457).
 
 from __future__ import annotations
 
+import json
 import math
 import time
 from collections import deque
@@ -228,6 +229,7 @@ class AgentServer:
         time_scale). Returns one record per request."""
         self.runner.capture()
         self._ev = []
+        self.token_completions: list[tuple[int, int]] = []
         st = torch.cuda.current_stream()
         records: list[RequestRecord] = []
         arrivals = deque(sorted(sessions, key=lambda s: s.arrival_time))
@@ -309,6 +311,7 @@ class AgentServer:
                 self.runner.graph.replay()
                 ev[1].record()
                 t_step = now_us()
+                self.token_completions.append((int(t_step), len(busy)))  # cluster.py:434
                 for idx, r in enumerate(self.rows):
                     if r.req is None:
                         continue
@@ -371,3 +374,75 @@ def summarize(records: list[RequestRecord], warmup_fraction: float = 0.1) -> dic
             "prefill_tokens": sum(r.prefilled for r in done),
             "prefix_hit_ratio": sum(r.matched for r in done) / max(1, lookup),
             "wall_s": t_end / 1e6}
+
+
+# -- the reference's output formats (src/prefillsim/metrics.py:17-91) --------
+
+SCHEMA_VERSION = 1
+CSV_HEADER = "request_id,session_id,model_id,ttft_us,e2e_us,out_tokens"
+
+
+def _percentile(values, p):
+    ordered = sorted(values)
+    return ordered[max(math.ceil(p / 100.0 * len(ordered)), 1) - 1]
+
+
+def build_report(server: "AgentServer", records: list[RequestRecord], config_echo: dict,
+                 warmup_fraction: float = 0.1) -> dict:
+    """report.json of a real-engine run in the reference's versioned schema
+    (metrics.py:44-80; pool aggregates as cluster.py:232-252): every field is
+    the reference's, measured on the GPU in real time (microseconds since the
+    run started) instead of virtual time. staging_handoff_count is 0: one GPU
+    hands off by pinning."""
+    end = max([t for t, _ in server.token_completions] + [int(r.done_us or 0) for r in records] + [0])
+    done = [r for r in records if r.done_us is not None and not r.failed]
+    ttfts = [int(r.first_token_us - r.issue_us) for r in done if r.first_token_us is not None]
+    e2es = [int(r.done_us - r.issue_us) for r in done]
+    w0 = warmup_fraction * end
+    toks = sum(n for t, n in server.token_completions if t >= w0)
+    win = (end - w0) / 1e6
+    matched = sum(p.matched_tokens for p in server.pools)
+    lookups = sum(p.lookup_tokens for p in server.pools)
+    peak: dict[str, int] = {}
+    for p in server.pools:
+        for ns, t in p.peak_footprint_tokens().items():
+            peak[ns] = peak.get(ns, 0) + t
+    return {
+        "schema_version": SCHEMA_VERSION,
+        "config": config_echo,
+        "metadata": {
+            "hit_ratio_definition": "cumulative matched_tokens / lookup_tokens over prefill lookups",
+            "throughput_definition": "generated output tokens completed in the post-warmup window",
+            "warmup_fraction": warmup_fraction,
+            "engine": "paper_2602_12029_b200 on one B200 (real time)",
+        },
+        "end_time_us": end,
+        "request_count": len(records),
+        "completed_count": len(done),
+        "failure_count": sum(1 for r in records if r.failed),
+        "staging_handoff_count": 0,
+        "p95_e2e_us": _percentile(e2es, 95) if e2es else None,
+        "mean_ttft_us": sum(ttfts) / len(ttfts) if ttfts else None,
+        "p95_ttft_us": _percentile(ttfts, 95) if ttfts else None,
+        "throughput_tok_per_s": toks / win if win > 0 else 0.0,
+        "prefix_hit_ratio": matched / lookups if lookups else 0.0,
+        "matched_tokens": matched,
+        "lookup_tokens": lookups,
+        "eviction_count": sum(p.eviction_count for p in server.pools),
+        "peak_footprint_tokens": dict(sorted(peak.items())),
+        "peak_footprint_total": sum(peak.values()),
+    }
+
+
+def report_to_json(report: dict) -> str:
+    return json.dumps(report, sort_keys=True, indent=1)
+
+
+def records_to_csv(records: list[RequestRecord]) -> str:
+    """requests.csv (metrics.py:86-94), one line per request in issue order."""
+    lines = [CSV_HEADER]
+    for r in sorted(records, key=lambda x: x.request_id):
+        ttft = "" if r.first_token_us is None or r.failed else str(int(r.first_token_us - r.issue_us))
+        e2e = "" if r.done_us is None or r.failed else str(int(r.done_us - r.issue_us))
+        lines.append(f"{r.request_id},{r.session_id},{r.model_id},{ttft},{e2e},{r.out_tokens}")
+    return "\n".join(lines) + "\n"

@@ -53,6 +53,51 @@ def test_agent_workload_tiny_both_modes(rows, batch):
         res[mode] = summarize(recs)
         gt = srv.gpu_time()
         assert gt["decode_steps"] > 0 and gt["prefill_calls"] > 0
+        from paper_2602_12029_b200.serve import build_report, records_to_csv
+        rep = build_report(srv, recs, {"mode": mode.value})
+        assert set(rep) == REPORT_KEYS and rep["completed_count"] == n_req and rep["failure_count"] == 0
+        assert rep["throughput_tok_per_s"] > 0 and len(records_to_csv(recs).splitlines()) == n_req + 1
     b, p = res[ServingMode.BASELINE], res[ServingMode.PREFILLSHARE]
     assert p["prefill_tokens"] < b["prefill_tokens"]
     assert p["prefix_hit_ratio"] > b["prefix_hit_ratio"]
+
+
+REPORT_KEYS = {"schema_version", "config", "metadata", "end_time_us", "request_count", "completed_count",
+               "failure_count", "staging_handoff_count", "p95_e2e_us", "mean_ttft_us", "p95_ttft_us",
+               "throughput_tok_per_s", "prefix_hit_ratio", "matched_tokens", "lookup_tokens",
+               "eviction_count", "peak_footprint_tokens", "peak_footprint_total"}
+
+
+def test_report_and_csv_follow_reference_schema():
+    """report.json / requests.csv of a real-engine run use the reference's
+    fields and definitions (metrics.py:17-94): nearest-rank p95, windowed
+    token throughput over per-step completions, pool aggregates summed over
+    workers (cluster.py:232-252)."""
+    from types import SimpleNamespace as NS
+
+    from paper_2602_12029_b200.serve import (CSV_HEADER, RequestRecord, build_report, records_to_csv,
+                                             report_to_json)
+    recs = [RequestRecord(i, i // 2, f"model_{'ab'[i % 2]}", 100.0 * i, 100.0 * i + 50 + i, 100.0 * i + 900 + 7 * i,
+                          128, 16 * i, 40) for i in range(20)]
+    recs.append(RequestRecord(20, 10, "model_a", 2000.0, failed=True))
+    pools = [NS(matched_tokens=300, lookup_tokens=1000, eviction_count=2,
+                peak_footprint_tokens=lambda: {"shared": 640}),
+             NS(matched_tokens=100, lookup_tokens=1000, eviction_count=1,
+                peak_footprint_tokens=lambda: {"shared": 160, "model:x": 32})]
+    comps = [(100 * k, 3) for k in range(1, 40)]
+    srv = NS(token_completions=comps, pools=pools)
+    rep = build_report(srv, recs, {"mode": "prefillshare"})
+    assert set(rep) == REPORT_KEYS and rep["schema_version"] == 1
+    e2e = sorted(int(r.done_us - r.issue_us) for r in recs[:20])
+    assert rep["p95_e2e_us"] == e2e[18]                      # ceil(0.95 * 20) - 1
+    assert rep["completed_count"] == 20 and rep["failure_count"] == 1 and rep["request_count"] == 21
+    end = rep["end_time_us"]
+    assert end == max(comps[-1][0], int(max(r.done_us for r in recs[:20])))
+    want_tok = sum(n for t, n in comps if t >= 0.1 * end) / ((end - 0.1 * end) / 1e6)
+    assert abs(rep["throughput_tok_per_s"] - want_tok) < 1e-9
+    assert rep["prefix_hit_ratio"] == 400 / 2000 and rep["eviction_count"] == 3
+    assert rep["peak_footprint_tokens"] == {"model:x": 32, "shared": 800} and rep["peak_footprint_total"] == 832
+    assert report_to_json(rep).startswith("{")
+    csv = records_to_csv(recs).splitlines()
+    assert csv[0] == CSV_HEADER and len(csv) == 22
+    assert csv[1] == "0,0,model_a,50,900,128" and csv[-1] == "20,10,model_a,,,0"

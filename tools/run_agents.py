@@ -1,9 +1,13 @@
 """Run the multi-model agent workload (BASELINE configs 3/5 semantics) on one
 GPU in both serving modes and print req/s, p95 E2E, prefill tokens and the
-prefix hit ratio.
+prefix hit ratio; one JSON line per (rate, cap) point, so lists sweep the
+reference's arrival-rate (A4) and concurrency-cap (A3) axes on the real
+engine. --out DIR writes, per point and mode, the
+reference's output files: workload.json, report.json, requests.csv
+(schemas of metrics.py:17-91 / workload.py:159-195).
 
-    python tools/run_agents.py [--shape 8b|tiny] [--rate 1.0] [--duration 10]
-                               [--pattern react] [--rows 8] [--time-scale 1]
+    python tools/run_agents.py [--shape 8b|tiny] [--rate 8[,4,...]] [--cap 0[,40,...]]
+                               [--duration 20] [--pattern react] [--rows 64] [--out DIR]
 """
 import argparse
 import json
@@ -17,16 +21,19 @@ import torch  # noqa: E402
 from paper_2602_12029_b200 import workload as wl  # noqa: E402
 from paper_2602_12029_b200.model import LlamaConfig, ModuleWeights  # noqa: E402
 from paper_2602_12029_b200.router import ServingMode  # noqa: E402
-from paper_2602_12029_b200.serve import AgentServer, summarize  # noqa: E402
+from paper_2602_12029_b200.serve import (AgentServer, build_report, records_to_csv,  # noqa: E402
+                                         report_to_json, summarize)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", default="8b")
-    ap.add_argument("--rate", type=float, default=1.0)
+    ap.add_argument("--rate", default="8", help="arrival rate(s), comma-separated")
+    ap.add_argument("--cap", default="0", help="max concurrent sessions (0 = unbounded), comma-separated")
+    ap.add_argument("--out", default=None, help="directory for workload.json / report.json / requests.csv")
     ap.add_argument("--duration", type=float, default=10.0)
     ap.add_argument("--pattern", default="react")
-    ap.add_argument("--rows", type=int, default=16)
+    ap.add_argument("--rows", type=int, default=64)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--time-scale", type=float, default=1.0)
     ap.add_argument("--pool-pages", type=int, default=7500)
@@ -35,28 +42,39 @@ def main():
     a = ap.parse_args()
     cfg = LlamaConfig.llama8b(max_pos=4096 + 512) if a.shape == "8b" else LlamaConfig.tiny(max_pos=4096)
     models = list(wl.DEFAULT_MODELS)
-    sessions = wl.generate(wl.WorkloadConfig(pattern=a.pattern, arrival_rate_per_s=a.rate,
-                                             duration_s=a.duration, seed=a.seed))
     mods = [ModuleWeights(cfg, 100 + i) for i in range(len(models))]
     base = ModuleWeights(cfg, 99, with_head=False)
-    out = {"workload": {"pattern": a.pattern, "rate": a.rate, "duration_s": a.duration,
-                        "sessions": len(sessions), "requests": sum(s.total_requests for s in sessions)},
-           "shape": a.shape}
-    out["prefill_batch"] = not a.no_batch
-    for mode in (ServingMode(m) for m in a.modes.split(",")):
-        srv = AgentServer(cfg, models, mode, rows_per_module=a.rows, pool_pages_per_worker=a.pool_pages,
-                          max_context=4096, max_output=256, modules=mods, base=base,
-                          prefill_batch=not a.no_batch)
-        recs = srv.run(sessions, time_scale=a.time_scale)
-        out[mode.value] = summarize(recs)
-        out[mode.value]["gpu_time"] = srv.gpu_time()
-        del srv
-        torch.cuda.empty_cache()
-    b, p = out.get("baseline", {}), out.get("prefillshare", {})
-    if b.get("req_per_s") and p.get("req_per_s"):
-        out["throughput_ratio"] = p["req_per_s"] / b["req_per_s"]
-        out["p95_ratio"] = b["p95_e2e_ms"] / p["p95_e2e_ms"]
-    print(json.dumps(out))
+    for rate in (float(x) for x in a.rate.split(",")):
+        for cap in (int(x) for x in a.cap.split(",")):
+            sessions = wl.generate(wl.WorkloadConfig(pattern=a.pattern, arrival_rate_per_s=rate,
+                                                     duration_s=a.duration, seed=a.seed))
+            out = {"workload": {"pattern": a.pattern, "rate": rate, "duration_s": a.duration, "cap": cap,
+                                "sessions": len(sessions), "requests": sum(s.total_requests for s in sessions)},
+                   "shape": a.shape, "prefill_batch": not a.no_batch, "rows_per_model": a.rows}
+            point = None
+            if a.out:
+                point = Path(a.out) / f"{a.pattern}_rate{rate:g}_cap{cap}"
+                point.mkdir(parents=True, exist_ok=True)
+                (point / "workload.json").write_text(wl.export_sessions(sessions))
+            for mode in (ServingMode(m) for m in a.modes.split(",")):
+                srv = AgentServer(cfg, models, mode, rows_per_module=a.rows, pool_pages_per_worker=a.pool_pages,
+                                  max_context=4096, max_output=256, modules=mods, base=base,
+                                  prefill_batch=not a.no_batch)
+                recs = srv.run(sessions, max_concurrent=cap or None, time_scale=a.time_scale)
+                out[mode.value] = summarize(recs)
+                out[mode.value]["gpu_time"] = srv.gpu_time()
+                if point is not None:
+                    echo = {"mode": mode.value, "workload": out["workload"], "shape": a.shape,
+                            "rows_per_model": a.rows, "pool_blocks_per_worker": a.pool_pages}
+                    (point / f"report_{mode.value}.json").write_text(report_to_json(build_report(srv, recs, echo)))
+                    (point / f"requests_{mode.value}.csv").write_text(records_to_csv(recs))
+                del srv
+                torch.cuda.empty_cache()
+            b, p = out.get("baseline", {}), out.get("prefillshare", {})
+            if b.get("req_per_s") and p.get("req_per_s"):
+                out["throughput_ratio"] = p["req_per_s"] / b["req_per_s"]
+                out["p95_ratio"] = b["p95_e2e_ms"] / p["p95_e2e_ms"]
+            print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":
