@@ -12,7 +12,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0, dirty_ws=False):
+def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0, dirty_ws=False, ramp=False):
     from paper_2602_12029_b200 import _lib
     from paper_2602_12029_b200.model import (DecodeBatch, DecodeRow, KVCache, LlamaConfig,
                                              SessionSpec)
@@ -24,6 +24,10 @@ def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0, dirty_ws
     kv = KVCache(cfg, n_pages)
     g = torch.Generator(device="cuda").manual_seed(seed)
     kv.data.copy_(torch.randn(kv.data.shape, device="cuda", generator=g).to(torch.bfloat16))
+    if ramp:  # K of later pages scaled up: row maxima grow along the stream (lazy O rescale path)
+        pv = kv.page_view()
+        for i, pg in enumerate(sorted(set(perm))):
+            pv[pg, :, 0] *= 1.0 + 3.0 * (i % 7) / 6.0
     sessions, rows = [], []
     ri = 0
     for s, L in enumerate(sess_lens):
@@ -131,3 +135,10 @@ def test_all_heads_kernel(case):
     the (session, split) all-heads kernel (64 KiB page boxes, warp = head)."""
     nq, nkv, lens, rps, priv = case
     _case(nq, nkv, lens, rps, priv, 1, seed=len(lens))
+
+
+@pytest.mark.parametrize("mods,splits", [(16, 1), (16, 5), (12, 3), (5, 2)])
+def test_growing_scores_rescale(mods, splits):
+    """Scores whose maxima grow along the page stream: the fan-out kernel's
+    lazy O rescale (and the mma.sync online softmax) under real growth."""
+    _case(32, 8, [3000], [mods], [(i * 13) % 100 for i in range(mods)], splits, seed=40 + mods, ramp=True)
