@@ -1124,19 +1124,16 @@ namespace tcv {
 
 constexpr int CPG = 4;                  // pages per chunk
 constexpr int KC = CPG * PT;            // 64 keys
-constexpr int NSTG = 5;
+constexpr int NSTG = 6;
 constexpr int KBYTES = CPG * TILE;      // 16 KiB: [half0 x 4 pages][half1 x 4 pages]
 constexpr int STG = 2 * KBYTES;         // + V 16 KiB: [page][half0 | half1]
-constexpr int OFF_Q = NSTG * STG;       // Q (A operand of S = QK^T): [2 halves][128 rows][128 B], SW128
-constexpr int OFF_ML = OFF_Q + 2 * 128 * 128;
+constexpr int OFF_ML = NSTG * STG;
 constexpr int OFF_BAR = OFF_ML + 128 * 8;
 constexpr int OFF_PG = OFF_BAR + 256;
 constexpr int OFF_INFO = OFF_PG + MAXP * 4;
 constexpr int SMEM = OFF_INFO + MAXP * 4 + 1024;
 constexpr int THREADS = 320;
-// TMEM: S_u [64u, 64u+64), O_u [128 + 128u, ...), P_{u,b} (bf16 pairs,
-// double-buffered so softmax(c+2) never waits for PV(c)) at 384 + 32(2u+b).
-constexpr uint32_t T_S = 0, T_O = 128, T_P = 384;
+constexpr uint32_t T_S = 0, T_O = 128, T_Q = 384, T_P = 448;
 constexpr float RESCALE_LOG2 = 8.f;
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -1147,7 +1144,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t *full = bars, *empty = bars + NSTG, *s_full = bars + 2 * NSTG, *p_full = s_full + 2,
-           *pv_done = p_full + 2, *g1_done = pv_done + 4, *s_free = g1_done + 1;  // pv_done[2u + b]
+           *pv_done = p_full + 2, *g1_done = pv_done + 2, *s_free = g1_done + 1;
   int* s_page = reinterpret_cast<int*>(smem + OFF_PG);
   int* s_info = reinterpret_cast<int*>(smem + OFF_INFO);  // (owner + 1) << 8 | valid tokens
   float* s_ml = reinterpret_cast<float*>(smem + OFF_ML);  // group 1 (m, l) per row
@@ -1194,8 +1191,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tma::mbar_init(&s_full[u], 1);
       tma::mbar_init(&s_free[u], 32 * act);
       tma::mbar_init(&p_full[u], 32 * act);
-      tma::mbar_init(&pv_done[2 * u], 1);
-      tma::mbar_init(&pv_done[2 * u + 1], 1);
+      tma::mbar_init(&pv_done[u], 1);
     }
     tma::mbar_init(g1_done, 32 * act);
     tma::fence_mbar_init();
@@ -1233,23 +1229,31 @@ __global__ void __launch_bounds__(THREADS, 1)
   // of a decode step writes them); q and the private pages (this step's
   // appended token) come from rope_append, so everyone else waits (PDL).
   if (warp != 0) asm volatile("griddepcontrol.wait;" ::: "memory");
-  // Q rows -> shared memory (K-major SW128; row = the query row's TMEM lane
-  // 32 (g / 16) + g % 16, dead rows zero), all threads but the producer
-  if (warp != 0) {
-    const uint32_t qs = smem_u32(smem + OFF_Q);
-    for (int e = threadIdx.x - 32; e < 128 * 16; e += THREADS - 32) {
-      const int r = e >> 4, c16 = e & 15;
-      const int g = (r & 31) < 16 ? (r >> 5) * 16 + (r & 31) : G;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (g < G)
-        v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)s_rows[g / p.grp] * p.nq + h * p.grp + g % p.grp) * HD +
-                                            c16 * 8);
-      asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(qs + umma::kmajor_off(r, c16, 16384)), "r"(v.x),
-                   "r"(v.y), "r"(v.z), "r"(v.w));
+  // Q rows -> TMEM (lane = row, bf16 pairs), by the group-0 warps of live lanes
+  if (warp >= 2 && warp < 6 && (warp & 3) < act) {
+    const int g = lane < 16 ? (warp & 3) * 16 + lane : G;
+    const uint32_t tq = tmem + ((uint32_t)((warp & 3) * 32) << 16) + T_Q;
+    const uint4* src = nullptr;
+    if (g < G)
+      src = reinterpret_cast<const uint4*>(p.q + ((int64_t)s_rows[g / p.grp] * p.nq + h * p.grp + g % p.grp) * HD);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t r[32];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 v = src ? src[half * 8 + i] : make_uint4(0, 0, 0, 0);
+        r[4 * i] = v.x;
+        r[4 * i + 1] = v.y;
+        r[4 * i + 2] = v.z;
+        r[4 * i + 3] = v.w;
+      }
+      umma::st32(tq + half * 32, r);
     }
-    umma::fence_proxy_async();
+    umma::wait_st();
+  }
+  if (warp != 0) {
     umma::fence_before();
-    named_barrier_sync(1, THREADS - 32);  // Q in shared memory (all but the producer)
+    named_barrier_sync(1, THREADS - 32);  // Q in TMEM (all but the producer)
     umma::fence_after();
   }
   trace_stamp(2);
@@ -1286,21 +1290,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int u = c & 1;
         const uint32_t kb = smem_u32(smem + (c % NSTG) * STG);
 #pragma unroll
-        const uint32_t qs = smem_u32(smem + OFF_Q);
-#pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma::mma(tmem + T_S + u * KC, umma::desc_k_sw128(qs + (kk >> 2) * 16384) + 2 * (kk & 3),
-                    umma::desc_k_sw128(kb + (kk >> 2) * KBYTES / 2) + 2 * (kk & 3), ID_S, kk > 0);
+          umma::mma_ts(tmem + T_S + u * KC, tmem + T_Q + kk * 8,
+                       umma::desc_k_sw128(kb + (kk >> 2) * KBYTES / 2) + 2 * (kk & 3), ID_S, kk > 0);
         umma::commit(&s_full[u]);
       };
       auto issue_pv = [&](int c) {
-        const int u = c & 1, b = (c >> 1) & 1;  // group, P buffer
+        const int u = c & 1;
         const uint32_t vb = smem_u32(smem + (c % NSTG) * STG) + KBYTES;
 #pragma unroll
         for (int pp = 0; pp < CPG; ++pp)
-          umma::mma_ts(tmem + T_O + u * HD, tmem + T_P + (2 * u + b) * 32 + pp * 8,
+          umma::mma_ts(tmem + T_O + u * HD, tmem + T_P + u * 32 + pp * 8,
                        umma::desc_mn_sw128(vb + pp * TILE, 2048), ID_PV, (c >= 2 || pp > 0) ? 1u : 0u);
-        umma::commit(&pv_done[2 * u + b]);
+        umma::commit(&pv_done[u]);
         umma::commit(&empty[c % NSTG]);
       };
       for (int c = 0; c < nch && c < 2; ++c) {
@@ -1333,7 +1335,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int gA = 16 * q4 + (lane >> 2), gB = gA + 8;
     const int riA = gA < G ? gA / p.grp : -2, riB = gB < G ? gB / p.grp : -2;
     const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
-    const uint32_t tS = tl + T_S + u * KC, tO = tl + T_O + u * HD, tP0 = tl + T_P + 2 * u * 32;
+    const uint32_t tS = tl + T_S + u * KC, tO = tl + T_O + u * HD, tP = tl + T_P + u * 32;
     const float sc = p.scale_log2;
     float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;  // m in scaled log2 units
     int it = 0;
@@ -1408,14 +1410,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mxB = fmaxf(mxB, __shfl_xor_sync(0xffffffffu, mxB, 2));
       mxA *= sc;
       mxB *= sc;
-      // P buffer b = it & 1 was last read by PV(it - 2): wait for that one only
-      const int b = it & 1;
-      if (it >= 2) tma::mbar_wait(&pv_done[2 * u + b], ((it >> 1) - 1) & 1);
+      if (it > 0) tma::mbar_wait(&pv_done[u], (it - 1) & 1);  // P_u free, O_u settled
       const bool growA = mxA > mA + RESCALE_LOG2 || (mA == -INFINITY && mxA > -INFINITY);
       const bool growB = mxB > mB + RESCALE_LOG2 || (mB == -INFINITY && mxB > -INFINITY);
       if (__any_sync(0xffffffffu, (growA || growB) && it > 0)) {
-        // rescaling O_u needs every earlier PV into it landed: PV(it - 1)
-        tma::mbar_wait(&pv_done[2 * u + ((it - 1) & 1)], ((it - 1) >> 1) & 1);
         umma::fence_after();
         const float alA = growA ? exp2f(mA - mxA) : 1.f, alB = growB ? exp2f(mB - mxB) : 1.f;
 #pragma unroll 1
@@ -1450,7 +1448,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         pk[2 * i] = pack_bf16(a0, a1);      // row A, P column 4i + t0 = keys 8i + 2 t0 + {0,1}
         pk[2 * i + 1] = pack_bf16(b0, b1);  // row B
       }
-      umma::st16x128b_x8(tP0 + b * 32, pk);
+      umma::st16x128b_x8(tP, pk);
 #pragma unroll
       for (int w = 4; w >= 1; w >>= 1)
 #pragma unroll
@@ -1464,7 +1462,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       umma::fence_before();
       tma::mbar_arrive(&p_full[u]);
     }
-    if (it > 0) tma::mbar_wait(&pv_done[2 * u + ((it - 1) & 1)], ((it - 1) >> 1) & 1);  // last PV (and all before)
+    if (it > 0) tma::mbar_wait(&pv_done[u], (it - 1) & 1);  // this group's last PV landed
     umma::fence_after();
     lA += __shfl_xor_sync(0xffffffffu, lA, 1);
     lB += __shfl_xor_sync(0xffffffffu, lB, 1);
