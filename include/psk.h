@@ -234,6 +234,9 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
  * then priv_len[r] += 1 (the row's KV for this step was appended). */
 int psk_argmax_advance(const psk_decode_batch* b, const float* logits, int32_t vocab,
                        int32_t* out_tokens, int32_t max_new, void* stream);
+/* out[r] = argmax(logits[r, 0:vocab]) (first maximum) — greedy prediction of
+ * evaluateSharing (frontend/src/evaluate.ts:36-42). */
+int psk_argmax_rows(const float* logits, int32_t n_rows, int32_t vocab, int32_t* out, void* stream);
 
 /* ------------------------------------------------------------------------ *
  * K1/K2 — prefill GEMMs on tcgen05 (TMA -> smem -> UMMA -> TMEM).

@@ -102,6 +102,7 @@ _SIGS: dict[str, list] = {
     "psk_decode_attn_workspace": [C.POINTER(DecodeBatchC), _I32, _I32, C.POINTER(_I64)],
     "psk_decode_attn": [C.POINTER(DecodeBatchC), _P, _I32, _I32, KVLayout, _I32, _P, _P, _P],
     "psk_argmax_advance": [C.POINTER(DecodeBatchC), _P, _I32, _P, _I32, _P],
+    "psk_argmax_rows": [_P, _I32, _I32, _P, _P],
     # prefill (K1-K3)
     "psk_gemm": [_P, _P, _I32, _I32, _I32, _I32, _P, _I64, _P],
     "psk_gemm_workspace": [C.POINTER(_I64)],

@@ -121,13 +121,9 @@ __global__ void rope_append_kernel(psk_decode_batch b, const float* __restrict__
 
 // ---------------------------------------------------------------- argmax --
 
-__global__ void argmax_advance_kernel(psk_decode_batch b, const float* __restrict__ logits, int V,
-                                      int32_t* __restrict__ out_tokens, int max_new) {
-  __shared__ float s_v[32];
-  __shared__ int s_i[32];
-  pdl_wait();
-  const int r = blockIdx.x;
-  const float* x = logits + (int64_t)r * V;
+// Block-wide first-maximum argmax of x[0, V) (tf.argMax / torch.argmax tie
+// rule); the result is valid in thread 0.
+__device__ int block_argmax(const float* __restrict__ x, int V, float* s_v, int* s_i) {
   float bv = -INFINITY;
   int bi = 0x7fffffff;
   // ties resolve to the lowest index (first maximum, as the reference argmax)
@@ -175,15 +171,32 @@ __global__ void argmax_advance_kernel(psk_decode_batch b, const float* __restric
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
     }
-    if (threadIdx.x == 0) {
-      const int k = b.priv_len[r];
-      if (out_tokens && k < max_new) out_tokens[(int64_t)r * max_new + k] = bi;
-      b.tokens[r] = bi;
-      // saturate at the row's page capacity: idle continuous-batching slots keep
-      // stepping without ever indexing past their private page table
-      b.priv_len[r] = min(k + 1, b.max_row_pages * PT - 1);
-    }
   }
+  return bi;
+}
+
+__global__ void argmax_advance_kernel(psk_decode_batch b, const float* __restrict__ logits, int V,
+                                      int32_t* __restrict__ out_tokens, int max_new) {
+  __shared__ float s_v[32];
+  __shared__ int s_i[32];
+  pdl_wait();
+  const int r = blockIdx.x;
+  const int bi = block_argmax(logits + (int64_t)r * V, V, s_v, s_i);
+  if (threadIdx.x == 0) {
+    const int k = b.priv_len[r];
+    if (out_tokens && k < max_new) out_tokens[(int64_t)r * max_new + k] = bi;
+    b.tokens[r] = bi;
+    // saturate at the row's page capacity: idle continuous-batching slots keep
+    // stepping without ever indexing past their private page table
+    b.priv_len[r] = min(k + 1, b.max_row_pages * PT - 1);
+  }
+}
+
+__global__ void argmax_rows_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ out) {
+  __shared__ float s_v[32];
+  __shared__ int s_i[32];
+  const int bi = block_argmax(logits + (int64_t)blockIdx.x * V, V, s_v, s_i);
+  if (threadIdx.x == 0) out[blockIdx.x] = bi;
 }
 
 }  // namespace dec
@@ -233,6 +246,14 @@ int psk_argmax_advance(const psk_decode_batch* b, const float* logits, int32_t v
   if (b->n_rows == 0) return PSK_OK;
   PSK_CUDA_TRY(psk::launch_pdl(argmax_advance_kernel, dim3(b->n_rows), dim3(1024), 0,
                                psk::as_stream(stream), *b, logits, vocab, out_tokens, max_new));
+  PSK_LAUNCH_CHECK();
+  return PSK_OK;
+}
+
+int psk_argmax_rows(const float* logits, int32_t n_rows, int32_t vocab, int32_t* out, void* stream) {
+  PSK_CHECK_ARG(logits && out && vocab > 0 && n_rows >= 0, "psk_argmax_rows: bad args");
+  if (n_rows == 0) return PSK_OK;
+  psk::dec::argmax_rows_kernel<<<n_rows, 1024, 0, psk::as_stream(stream)>>>(logits, vocab, out);
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }
