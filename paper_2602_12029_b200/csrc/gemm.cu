@@ -179,7 +179,7 @@ __device__ __forceinline__ __nv_bfloat16* kv_dst(const psk_kv_layout& kv, int pa
 }
 
 // Epilogue for one 128x256 tile; thread owns tile row `r` (TMEM lane).
-__device__ void epilogue_tile(const Epi& e, uint32_t tacc, int row, bool row_ok, int n0) {
+__device__ void epilogue_tile(const Epi& e, uint32_t tacc, int row, bool row_ok, int n0, int ncols = BN) {
   float v[32], w[32];
   if (e.mode == PSK_EPI_QKV_ROPE_KV) {
     int pos = e.pos0 + row, page = 0, tok = 0;
@@ -196,7 +196,7 @@ __device__ void epilogue_tile(const Epi& e, uint32_t tacc, int row, bool row_ok,
     }
     const float* cs = e.rope + (int64_t)pos * 128;
 #pragma unroll 1
-    for (int hh = 0; hh < 2; ++hh) {
+    for (int hh = 0; hh < ncols / 128; ++hh) {
       const int head = (n0 >> 7) + hh;
       const uint32_t hb = tacc + hh * 128;
       if (head >= e.nq + e.nkv) {  // V head: plain copy into the page
@@ -233,7 +233,7 @@ __device__ void epilogue_tile(const Epi& e, uint32_t tacc, int row, bool row_ok,
     return;
   }
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  for (int c = 0; c < ncols / 32; ++c) {
     tmem_ld32(tacc + c * 32, v);
     if (!row_ok) continue;
     const int col = n0 + c * 32;
@@ -280,32 +280,43 @@ __device__ void epilogue_tile(const Epi& e, uint32_t tacc, int row, bool row_ok,
 // Each split writes its fp32 partial to the workspace; the last one to
 // finish (atomic counter) sums all S partials in split order (fixed order:
 // bit-reproducible), stores the sum back into its TMEM accumulator and runs
-// the normal fused epilogue.
+// the normal fused epilogue. That reduction (one CTA re-reading S x 128 KiB)
+// measured slower end to end, so by default (no workspace bound) the tail
+// tiles are split along N instead: S independent 128 x (256 / S) pieces
+// (MMA N = 256 / S, B box of 256 / S rows, the epilogue on those columns),
+// no reduction at all (S <= 2 for the QKV/RoPE epilogue: whole heads).
 struct Sched {
   int tiles, full, rem, S, items;
+  int split_n;     // 1: tail pieces along N; 0: along K (workspace)
   float* part;     // [rem * S][BM][BN] fp32
   int* counters;   // [rem], zero between launches
 };
 
 __device__ __forceinline__ void item_range(const Sched& sc, int item, int kb_n, int& tile, int& kb0, int& kb1,
-                                           int& split) {
+                                           int& split, int& piece) {
+  piece = -1;
+  split = -1;
+  kb0 = 0;
+  kb1 = kb_n;
   if (item < sc.full) {
     tile = item;
-    kb0 = 0;
-    kb1 = kb_n;
-    split = -1;
   } else {
     const int j = item - sc.full;
     tile = sc.full + j / sc.S;
-    split = j % sc.S;
-    kb0 = split * kb_n / sc.S;
-    kb1 = (split + 1) * kb_n / sc.S;
+    if (sc.split_n) {
+      piece = j % sc.S;
+    } else {
+      split = j % sc.S;
+      kb0 = split * kb_n / sc.S;
+      kb1 = (split + 1) * kb_n / sc.S;
+    }
   }
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                        const __grid_constant__ CUtensorMap tmap_b, int M, int N, int K, Epi e, Sched sc) {
+                        const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_bp,
+                        int M, int N, int K, Epi e, Sched sc) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -351,11 +362,19 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int item = blockIdx.x; item < sc.items; item += gridDim.x) {
-        int t, kb0, kb1, split;
-        item_range(sc, item, kb_n, t, kb0, kb1, split);
+        int t, kb0, kb1, split, piece;
+        item_range(sc, item, kb_n, t, kb0, kb1, split, piece);
         const int mb = t % m_tiles, nb = t / m_tiles;
+        const int pn = BN / sc.S;  // N-piece width
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (piece >= 0) {  // tail piece: A tile + a (256 / S)-row B box
+            mbar_expect_tx(&full[stage], A_BYTES + pn * BK * 2);
+            tma_load_2d(&tmap_a, &full[stage], sA + stage * A_BYTES, kb * BK, mb * BM);
+            tma_load_2d(&tmap_bp, &full[stage], sB + stage * B_BYTES, kb * BK, nb * BN + piece * pn);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           tma_load_2d(&tmap_a, &full[stage], sA + stage * A_BYTES, kb * BK, mb * BM);
           tma_load_2d(&tmap_b, &full[stage], sB + stage * B_BYTES, kb * BK, nb * BN);
@@ -365,13 +384,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(BM, BN);
+      constexpr uint32_t idesc_full = idesc_bf16(BM, BN);
+      const uint32_t idesc_piece = idesc_bf16(BM, BN / (sc.S > 0 ? sc.S : 1));
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int item = blockIdx.x; item < sc.items; item += gridDim.x, ++it) {
-        int t, kb0, kb1, split;
-        item_range(sc, item, kb_n, t, kb0, kb1, split);
+        int t, kb0, kb1, split, piece;
+        item_range(sc, item, kb_n, t, kb0, kb1, split, piece);
+        const uint32_t idesc = piece >= 0 ? idesc_piece : idesc_full;
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -398,8 +419,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int r_in_tile = q * 32 + lane;
     int it = 0;
     for (int item = blockIdx.x; item < sc.items; item += gridDim.x, ++it) {
-      int t, kb0, kb1, split;
-      item_range(sc, item, kb_n, t, kb0, kb1, split);
+      int t, kb0, kb1, split, piece;
+      item_range(sc, item, kb_n, t, kb0, kb1, split, piece);
       const int mb = t % m_tiles, nb = t / m_tiles;
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
@@ -456,7 +477,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
-      epilogue_tile(e, tacc, row, row < M, nb * BN);
+      if (piece >= 0)
+        epilogue_tile(e, tacc, row, row < M, nb * BN + piece * (BN / sc.S), BN / sc.S);
+      else
+        epilogue_tile(e, tacc, row, row < M, nb * BN);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -544,8 +568,21 @@ static int launch(const void* A, const void* B, int M, int N, int K, const Epi& 
   sc.full = tiles;
   sc.rem = 0;
   sc.S = 1;
+  sc.split_n = 0;
   const int kb_n = K / BK;
   const int rem = tiles % grid, waves = tiles / grid;
+  CUtensorMap mbp = mb;
+  if (!g_ws.part && waves >= 1 && rem > 0 && rem <= grid / 2) {
+    // split-N tail: S pieces of 256 / S columns (QKV/RoPE: whole 128-column heads)
+    int S = grid / rem >= 4 ? 4 : 2;
+    if (e.mode == PSK_EPI_QKV_ROPE_KV) S = 2;
+    rc = make_map(&mbp, B, N, K, BN / S);
+    if (rc) return rc;
+    sc.full = tiles - rem;
+    sc.rem = rem;
+    sc.S = S;
+    sc.split_n = 1;
+  }
   if (g_ws.part && waves >= 1 && rem > 0 && rem <= grid / 2) {
     int S = grid / rem;
     if (S > kb_n / 4) S = kb_n / 4;
@@ -558,7 +595,7 @@ static int launch(const void* A, const void* B, int M, int N, int K, const Epi& 
     }
   }
   sc.items = sc.full + sc.rem * sc.S;
-  gemm_bf16_tn_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ma, mb, M, N, K, e, sc);
+  gemm_bf16_tn_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ma, mb, mbp, M, N, K, e, sc);
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }

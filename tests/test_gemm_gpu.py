@@ -78,8 +78,18 @@ def test_gemm_silu_mul_interleaved():
 
 
 @pytest.mark.parametrize("nq,nkv,T,pos0", [(2, 1, 100, 0), (32, 8, 300, 32), (32, 8, 17, 4080), (32, 8, 4096, 16)])
-def test_gemm_qkv_rope_paged_kv(nq, nkv, T, pos0, split_ws):
-    """(T = 4096 at the 8B width: 768 tiles, the last-wave tiles run split-K.)"""
+def test_gemm_qkv_rope_paged_kv(nq, nkv, T, pos0):
+    """(T = 4096 at the 8B width: 768 tiles, the last-wave tiles run as
+    128-column (one head) pieces: split-N.)"""
+    _qkv_case(nq, nkv, T, pos0)
+
+
+def test_gemm_qkv_rope_paged_kv_split_k(split_ws):
+    """The same with the split-K workspace bound."""
+    _qkv_case(32, 8, 4096, 16)
+
+
+def _qkv_case(nq, nkv, T, pos0):
     from paper_2602_12029_b200.model import KVCache, LlamaConfig, rope_table
     from oracle.model import _rope, rope_cos_sin
     d = 256 if nq == 2 else 4096
@@ -139,3 +149,30 @@ def test_gemm_split_k_tail(M, N, K, split_ws):
     torch.cuda.synchronize()
     assert (o.float() - silu_ref).abs().max().item() <= 1e-2 * silu_ref.abs().max().item() + 1e-3
     assert int(_lib()._gemm_ws[:4096].view(torch.int32).abs().sum().item()) == 0
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 4096, 4096), (4096, 6144, 4096), (2560, 2048, 4096),
+                                   (4096, 28672, 4096), (4000, 4096, 1024)])
+def test_gemm_split_n_tail(M, N, K):
+    """Default tail schedule (no workspace): last-wave tiles split along N
+    into 64/128-column pieces; store / residual add / SiLU*mul epilogues."""
+    assert _lib()._gemm_ws is None
+    A, B = _rand(M, K, seed=21), _rand(N, K, std=0.02, seed=22)
+    ref = A.float() @ B.float().T
+    scale = ref.abs().max().item()
+    out = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+    _gemm(A, B, 1, out, N)
+    torch.cuda.synchronize()
+    assert (out - ref).abs().max().item() <= 2e-3 * scale + 1e-4
+    h = torch.randn(M, N, device="cuda")
+    want = h + ref
+    _gemm(A, B, 2, h, N)
+    torch.cuda.synchronize()
+    assert (h - want).abs().max().item() <= 2e-3 * want.abs().max().item() + 1e-4
+    F = N // 2
+    silu_ref = ref.view(M, -1, 2, 8)
+    silu_ref = (torch.nn.functional.silu(silu_ref[:, :, 0]) * silu_ref[:, :, 1]).reshape(M, F)
+    o = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+    _gemm(A, B, 3, o, F)
+    torch.cuda.synchronize()
+    assert (o.float() - silu_ref).abs().max().item() <= 1e-2 * silu_ref.abs().max().item() + 1e-3
