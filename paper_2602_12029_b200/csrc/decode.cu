@@ -40,40 +40,60 @@ __global__ void embed_rows_kernel(psk_decode_batch b, const __nv_bfloat16* const
 
 // --------------------------------------------------------------- RMSNorm --
 
-__global__ void rmsnorm_rows_kernel(const float* __restrict__ h, int d,
+// One CTA (256 threads) per row; the row stays in registers between the
+// sum of squares and the scaled store (one HBM read of h), gamma is read
+// before the PDL wait (weights never depend on the previous kernel).
+constexpr int NORM_THREADS = 256;
+constexpr int NORM_VPT = 8;  // float4 per thread: d <= 8192
+
+__global__ void __launch_bounds__(NORM_THREADS) rmsnorm_rows_kernel(const float* __restrict__ h, int d,
                                     const __nv_bfloat16* const* gamma, const int32_t* row_mod,
                                     float eps, __nv_bfloat16* __restrict__ out) {
   __shared__ float s_red[32];
   pdl_trigger();
-  pdl_wait();
   const int r = blockIdx.x;
-  const float* x = h + (int64_t)r * d;
-  float ss = 0.f;
-  for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
-    float4 v = *reinterpret_cast<const float4*>(x + i);
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  const __nv_bfloat16* g = gamma[row_mod ? row_mod[r] : 0];
+  const int n4 = d >> 2;
+  uint2 gv[NORM_VPT];
+#pragma unroll
+  for (int u = 0; u < NORM_VPT; ++u) {
+    const int i = threadIdx.x + u * NORM_THREADS;
+    gv[u] = i < n4 ? __ldg(reinterpret_cast<const uint2*>(g) + i) : make_uint2(0, 0);
   }
+  pdl_wait();
+  const float4* x = reinterpret_cast<const float4*>(h + (int64_t)r * d);
+  float4 v[NORM_VPT];
+  float ss = 0.f;
+#pragma unroll
+  for (int u = 0; u < NORM_VPT; ++u) {
+    const int i = threadIdx.x + u * NORM_THREADS;
+    v[u] = i < n4 ? x[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int u = 0; u < NORM_VPT; ++u) ss += v[u].x * v[u].x + v[u].y * v[u].y + v[u].z * v[u].z + v[u].w * v[u].w;
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ss;
   __syncthreads();
   if (threadIdx.x < 32) {
-    float t = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : 0.f;
+    float t = threadIdx.x < (NORM_THREADS >> 5) ? s_red[threadIdx.x] : 0.f;
     t = warp_sum(t);
     if (threadIdx.x == 0) s_red[0] = t;
   }
   __syncthreads();
   const float inv = rsqrtf(s_red[0] / (float)d + eps);
-  const __nv_bfloat16* g = gamma[row_mod ? row_mod[r] : 0];
-  __nv_bfloat16* o = out + (int64_t)r * d;
-  for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
-    float4 v = *reinterpret_cast<const float4*>(x + i);
-    __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162*>(g + i);
-    __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162*>(g + i + 2);
-    float2 a = __bfloat1622float2(g01), c = __bfloat1622float2(g23);
-    __nv_bfloat162 o01 = __floats2bfloat162_rn(v.x * inv * a.x, v.y * inv * a.y);
-    __nv_bfloat162 o23 = __floats2bfloat162_rn(v.z * inv * c.x, v.w * inv * c.y);
-    *reinterpret_cast<__nv_bfloat162*>(o + i) = o01;
-    *reinterpret_cast<__nv_bfloat162*>(o + i + 2) = o23;
+  uint2* o = reinterpret_cast<uint2*>(out + (int64_t)r * d);
+#pragma unroll
+  for (int u = 0; u < NORM_VPT; ++u) {
+    const int i = threadIdx.x + u * NORM_THREADS;
+    if (i >= n4) continue;
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gv[u].x));
+    const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gv[u].y));
+    const __nv_bfloat162 o01 = __floats2bfloat162_rn(v[u].x * inv * a.x, v[u].y * inv * a.y);
+    const __nv_bfloat162 o23 = __floats2bfloat162_rn(v[u].z * inv * c.x, v[u].w * inv * c.y);
+    uint2 w;
+    w.x = *reinterpret_cast<const uint32_t*>(&o01);
+    w.y = *reinterpret_cast<const uint32_t*>(&o23);
+    o[i] = w;
   }
 }
 
@@ -85,9 +105,14 @@ __device__ __forceinline__ __nv_bfloat16* kv_ptr(const psk_kv_layout& kv, int32_
          ((((int64_t)layer * 2 + kvsel) * kv.n_kv_heads + head) * kv.page_tokens + tok) * kv.head_dim;
 }
 
-__global__ void rope_append_kernel(psk_decode_batch b, const float* __restrict__ qkv, int nq,
-                                   const float* __restrict__ rope, int layer, psk_kv_layout kv,
-                                   __nv_bfloat16* __restrict__ q_rot) {
+// One CTA per row, 64 x 8 threads: thread (i, j) rotates dims (i, i + 64) of
+// heads j, j + 8, ... (q heads, then k), copies v; all of a thread's loads
+// are independent (no per-head dependent chain).
+constexpr int ROPE_HG = 8;
+
+__global__ void __launch_bounds__(64 * ROPE_HG) rope_append_kernel(psk_decode_batch b, const float* __restrict__ qkv,
+                                                                  int nq, const float* __restrict__ rope, int layer,
+                                                                  psk_kv_layout kv, __nv_bfloat16* __restrict__ q_rot) {
   // the attention kernel (PDL-launched next) may start its table prologue now
   asm volatile("griddepcontrol.launch_dependents;");
   const int r = blockIdx.x;
@@ -98,22 +123,21 @@ __global__ void rope_append_kernel(psk_decode_batch b, const float* __restrict__
   const int off = idx % PT;
   const float* row = qkv + (int64_t)r * (nq + 2 * nkv) * HD;
   const float* cs = rope + (int64_t)pos * HD;  // [64][2]
-  const int i = threadIdx.x;                    // 0..63
+  const int i = threadIdx.x & 63, j = threadIdx.x >> 6;
   const float c = cs[2 * i], s = cs[2 * i + 1];
   pdl_wait();  // qkv comes from the GEMV just before
-  for (int h = 0; h < nq; ++h) {
+  // q and k heads: rotate-half
+#pragma unroll 4
+  for (int h = j; h < nq + nkv; h += ROPE_HG) {
     const float x1 = row[h * HD + i], x2 = row[h * HD + i + 64];
-    q_rot[((int64_t)r * nq + h) * HD + i] = f2bf(x1 * c - x2 * s);
-    q_rot[((int64_t)r * nq + h) * HD + i + 64] = f2bf(x2 * c + x1 * s);
+    const __nv_bfloat16 y1 = f2bf(x1 * c - x2 * s), y2 = f2bf(x2 * c + x1 * s);
+    __nv_bfloat16* d = h < nq ? q_rot + ((int64_t)r * nq + h) * HD : kv_ptr(kv, page, layer, 0, h - nq, off);
+    d[i] = y1;
+    d[i + 64] = y2;
   }
-  for (int h = 0; h < nkv; ++h) {
-    const float* kr = row + (nq + h) * HD;
+  for (int h = j; h < nkv; h += ROPE_HG) {
     const float* vr = row + (nq + nkv + h) * HD;
-    __nv_bfloat16* kd = kv_ptr(kv, page, layer, 0, h, off);
     __nv_bfloat16* vd = kv_ptr(kv, page, layer, 1, h, off);
-    const float x1 = kr[i], x2 = kr[i + 64];
-    kd[i] = f2bf(x1 * c - x2 * s);
-    kd[i + 64] = f2bf(x2 * c + x1 * s);
     vd[i] = f2bf(vr[i]);
     vd[i + 64] = f2bf(vr[i + 64]);
   }
@@ -219,9 +243,10 @@ int psk_embed_rows(const psk_decode_batch* b, const void* const* embed, int32_t 
 
 int psk_rmsnorm_rows(const float* h, int32_t n_rows, int32_t d, const void* const* gamma,
                      const int32_t* row_mod, float eps, void* out, void* stream) {
-  PSK_CHECK_ARG(h && gamma && out && d % 4 == 0 && n_rows >= 0, "psk_rmsnorm_rows: bad args");
+  PSK_CHECK_ARG(h && gamma && out && d % 4 == 0 && n_rows >= 0 && d <= 4 * NORM_THREADS * NORM_VPT,
+                "psk_rmsnorm_rows: bad args (d %% 4 == 0, d <= %d)", 4 * NORM_THREADS * NORM_VPT);
   if (n_rows == 0) return PSK_OK;
-  PSK_CUDA_TRY(psk::launch_pdl(rmsnorm_rows_kernel, dim3(n_rows), dim3(256), 0, psk::as_stream(stream),
+  PSK_CUDA_TRY(psk::launch_pdl(rmsnorm_rows_kernel, dim3(n_rows), dim3(NORM_THREADS), 0, psk::as_stream(stream),
                                h, d, reinterpret_cast<const __nv_bfloat16* const*>(gamma), row_mod,
                                eps, reinterpret_cast<__nv_bfloat16*>(out)));
   PSK_LAUNCH_CHECK();
@@ -233,7 +258,7 @@ int psk_rope_append(const psk_decode_batch* b, const float* qkv, int32_t n_q_hea
   PSK_CHECK_ARG(b && qkv && rope && q_rot && kv.head_dim == HD && kv.page_tokens == PT,
                 "psk_rope_append: bad args (head_dim must be 128, page_tokens 16)");
   if (b->n_rows == 0) return PSK_OK;
-  PSK_CUDA_TRY(psk::launch_pdl(rope_append_kernel, dim3(b->n_rows), dim3(64), 0, psk::as_stream(stream),
+  PSK_CUDA_TRY(psk::launch_pdl(rope_append_kernel, dim3(b->n_rows), dim3(64 * ROPE_HG), 0, psk::as_stream(stream),
                                *b, qkv, n_q_heads, rope, layer, kv,
                                reinterpret_cast<__nv_bfloat16*>(q_rot)));
   PSK_LAUNCH_CHECK();

@@ -50,7 +50,7 @@ def time_step(n=40):
 
 
 kinds = {"rmsnorm": ["psk_rmsnorm_rows"], "rope_append": ["psk_rope_append"], "attention": ["psk_decode_attn"],
-         "gemv": ["psk_gemv"], "embed+argmax": ["psk_embed_rows", "psk_argmax_advance"]}
+         "gemv": ["psk_gemv", "psk_gemv_tc"], "embed+argmax": ["psk_embed_rows", "psk_argmax_advance"]}
 full = time_step()
 print(f"S={S}: full step {full:9.1f} us")
 for name, fns in kinds.items():
