@@ -38,12 +38,15 @@ constexpr int BK = 64;              // columns per k-chunk (one 128 B swizzle at
 constexpr int A_BYTES = BN * BK * 2;  // 16 KiB
 constexpr int THREADS = 192;
 constexpr int MAXMOD = 16;
-constexpr int RING_BYTES = 200 * 1024;
-
+constexpr int RING_BYTES = 216 * 1024;
+// k-chunks per ring stage: the producer issues CH weight boxes back to back
+// per mbarrier (tools/bw_probe.cu: 128x64 SW128 boxes stream at 6.35 TB/s
+// one per stage, 6.97-7.0 TB/s three or four per stage)
 template <int MN>
 struct Cfg {
+  static constexpr int CH = MN <= 16 ? 4 : (MN <= 32 ? 3 : 2);
   static constexpr int B_BYTES = MN * BK * 2;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGE = CH * (A_BYTES + B_BYTES);  // [CH weight boxes][CH x boxes]
   static constexpr int STAGES = RING_BYTES / STAGE;
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int TMEM_COLS = 2 * MN < 32 ? 32 : 2 * MN;
@@ -141,32 +144,37 @@ __global__ void __launch_bounds__(THREADS, 1)
       tma::prefetch_map(&maps.x);
       // x rows come from the previous kernel: the first ring fill issues the
       // weight boxes at once and the x boxes after the PDL wait
-      int pend_k[C::STAGES], pend_row[C::STAGES];
+      int pend_k[C::STAGES], pend_n[C::STAGES], pend_row[C::STAGES];
       int npend = 0;
       bool waited = false;
-      int j = 0;
+      int j = 0;  // stage counter
+      auto load_x = [&](int s, int k0c, int n, int row) {
+        for (int b = 0; b < n; ++b)
+          tma::load_2d(&maps.x, &full[s], smem + s * C::STAGE + C::CH * A_BYTES + b * C::B_BYTES, (k0c + b) * BK, row);
+      };
       for (int c = c0; c < c1;) {
         const Seg sg = seg_at(c);
         c += sg.k1 - sg.k0;
         if (!live(sg.unit)) continue;  // module without rows this step
         const int mod = sg.unit / nb, blk = sg.unit % nb;
         const int xb = mrs[mod];
-        for (int kc = sg.k0; kc < sg.k1; ++kc, ++j) {
+        for (int kc = sg.k0; kc < sg.k1; kc += C::CH, ++j) {
+          const int n = min(C::CH, sg.k1 - kc);
           const int s = j % C::STAGES;
           if (!waited && j == C::STAGES) {
             pdl_wait();
-            for (int i = 0; i < npend; ++i)
-              tma::load_2d(&maps.x, &full[i], smem + i * C::STAGE + A_BYTES, pend_k[i], pend_row[i]);
+            for (int i = 0; i < npend; ++i) load_x(i, pend_k[i], pend_n[i], pend_row[i]);
             waited = true;
           }
           tma::mbar_wait(&empty[s], ((j / C::STAGES) & 1) ^ 1);
-          tma::mbar_expect_tx(&full[s], C::STAGE);
+          tma::mbar_expect_tx(&full[s], n * (A_BYTES + C::B_BYTES));
           unsigned char* st = smem + s * C::STAGE;
-          tma::load_2d(&maps.w[mod], &full[s], st, kc * BK, blk * BN);
+          for (int b = 0; b < n; ++b) tma::load_2d(&maps.w[mod], &full[s], st + b * A_BYTES, (kc + b) * BK, blk * BN);
           if (waited) {
-            tma::load_2d(&maps.x, &full[s], st + A_BYTES, kc * BK, xb);
+            load_x(s, kc, n, xb);
           } else {
-            pend_k[npend] = kc * BK;
+            pend_k[npend] = kc;
+            pend_n[npend] = n;
             pend_row[npend] = xb;
             ++npend;
           }
@@ -174,8 +182,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (!waited) {
         pdl_wait();
-        for (int i = 0; i < npend; ++i)
-          tma::load_2d(&maps.x, &full[i], smem + i * C::STAGE + A_BYTES, pend_k[i], pend_row[i]);
+        for (int i = 0; i < npend; ++i) load_x(i, pend_k[i], pend_n[i], pend_row[i]);
       }
     }
   } else if (warp == 1) {
@@ -190,15 +197,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         umma::fence_after();
         const uint32_t tacc = tmem + acc * MN;
-        for (int kc = sg.k0; kc < sg.k1; ++kc, ++j) {
+        for (int kc = sg.k0; kc < sg.k1; kc += C::CH, ++j) {
+          const int n = min(C::CH, sg.k1 - kc);
           const int s = j % C::STAGES;
           tma::mbar_wait(&full[s], (j / C::STAGES) & 1);
           umma::fence_after();
           const uint32_t a = tma::sa(smem + s * C::STAGE);
-          const uint64_t da = umma::desc_k_sw128(a), db = umma::desc_k_sw128(a + A_BYTES);
+          for (int b = 0; b < n; ++b) {
+            const uint64_t da = umma::desc_k_sw128(a + b * A_BYTES);
+            const uint64_t db = umma::desc_k_sw128(a + C::CH * A_BYTES + b * C::B_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma::mma(tacc, da + 2 * k, db + 2 * k, idesc, (kc != sg.k0 || k != 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k)
+              umma::mma(tacc, da + 2 * k, db + 2 * k, idesc, (kc + b != sg.k0 || k != 0) ? 1u : 0u);
+          }
           umma::commit(&empty[s]);
         }
         umma::commit(&tfull[acc]);

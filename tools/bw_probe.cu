@@ -5,6 +5,10 @@
 //           `stages` x `stage_kb` KiB; stage = `rows` pieces of (stage/rows)
 //           bytes taken from rows `row_kb` KiB apart (rows=1: contiguous)
 //   ldg   — every thread streams 16 B loads, `unroll` in flight
+//   tma   — the K5-TC weight pattern: a bf16 [rows][4096] matrix streamed as
+//           SW128 2-D boxes of 128 rows x 64 columns (128 B per row), `nbox`
+//           consecutive k-chunk boxes per stage
+#include <cuda.h>
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
@@ -72,6 +76,64 @@ __global__ void bulk_kernel(const char* __restrict__ src, int64_t bytes, int sta
   if (acc == 12345.f) *sink = acc;
 }
 
+
+__global__ void tma_kernel(const __grid_constant__ CUtensorMap map, int64_t row_blocks, int kchunks, int stages,
+                           int nbox, float* sink) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
+  const int stage_bytes = nbox * 16384;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)stages * stage_bytes);
+  uint64_t* empty = full + stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x / 32 - 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&empty[s])), "r"(nw));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  const int per_unit = kchunks / nbox;
+  const int64_t units = row_blocks * per_unit;
+  const int64_t u0 = blockIdx.x * units / gridDim.x, u1 = (blockIdx.x + 1) * units / gridDim.x;
+  if (warp == nw) {
+    if (lane == 0) {
+      for (int64_t u = u0; u < u1; ++u) {
+        const int j = (int)(u - u0), s = j % stages;
+        const uint32_t par = ((j / stages) & 1) ^ 1;
+        asm volatile("{\n.reg .pred P;\nW: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n@!P bra W;\n}" ::"r"(
+                         sa(&empty[s])), "r"(par));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[s])), "r"(stage_bytes));
+        const int64_t rb = u / per_unit;
+        const int kc0 = (int)(u % per_unit) * nbox;
+        for (int b = 0; b < nbox; ++b)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+                  sa(sm + (size_t)s * stage_bytes + b * 16384)),
+              "l"(&map), "r"(sa(&full[s])), "r"((kc0 + b) * 64), "r"((int)(rb * 128))
+              : "memory");
+      }
+    }
+    __syncwarp();
+    return;
+  }
+  float acc = 0.f;
+  for (int64_t u = u0; u < u1; ++u) {
+    const int j = (int)(u - u0), s = j % stages;
+    const uint32_t par = (j / stages) & 1;
+    asm volatile("{\n.reg .pred P;\nW: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n@!P bra W;\n}" ::"r"(
+                     sa(&full[s])), "r"(par));
+    acc += reinterpret_cast<const float*>(sm + (size_t)s * stage_bytes)[threadIdx.x];
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&empty[s])));
+  }
+  if (acc == 12345.f) *sink = acc;
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
 template <int U>
 __global__ void ldg_kernel(const uint4* __restrict__ src, int64_t n16, float* sink) {
   float acc = 0.f;
@@ -128,6 +190,30 @@ int main() {
     const int64_t rs = (int64_t)c.row_kb * 1024;
     timeit([&] { bulk_kernel<<<sms * c.ctas, 288, smem>>>(buf, bytes, c.stages, stage_bytes, c.rows, rs, sink); },
            name);
+  }
+  {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
+    EncodeFn enc = reinterpret_cast<EncodeFn>(fp);
+    const int64_t K = 4096, rows = bytes / (K * 2);
+    CUtensorMap map;
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+    for (int promo = 0; promo < 2; ++promo) {
+      enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, promo ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      struct T { int stages, nbox; } tc[] = {{12, 1}, {6, 2}, {3, 4}, {4, 3}};
+      for (auto t : tc) {
+        const int smem = t.stages * t.nbox * 16384 + 1024 + 256;
+        cudaFuncSetAttribute(tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        char name[128];
+        snprintf(name, sizeof name, "tma 128x64 SW128 boxes: %d stages x %d boxes promo=%d", t.stages, t.nbox, promo);
+        timeit([&] { tma_kernel<<<sms, 288, smem>>>(map, rows / 128, (int)(K / 64), t.stages, t.nbox, sink); }, name);
+      }
+    }
   }
   timeit([&] { ldg_kernel<4><<<sms * 4, 256>>>((const uint4*)buf, bytes / 16, sink); }, "ldg v4 unroll4 4x256/sm");
   timeit([&] { ldg_kernel<8><<<sms * 4, 256>>>((const uint4*)buf, bytes / 16, sink); }, "ldg v4 unroll8 4x256/sm");
