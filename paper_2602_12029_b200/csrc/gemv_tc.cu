@@ -42,14 +42,17 @@ constexpr int RING_BYTES = 216 * 1024;
 // k-chunks per ring stage: the producer issues CH weight boxes back to back
 // per mbarrier (tools/bw_probe.cu: 128x64 SW128 boxes stream at 6.35 TB/s
 // one per stage, 6.97-7.0 TB/s three or four per stage)
-template <int MN>
+// UW = 128-row weight blocks per work unit. UW = 2 (N % 256 == 0): one x box
+// per k-chunk serves two M=128 MMAs into two TMEM accumulators, halving the
+// x traffic and putting 192 KiB of weights in flight in two stages.
+template <int MN, int UW>
 struct Cfg {
-  static constexpr int CH = MN <= 16 ? 4 : (MN <= 32 ? 3 : 2);
+  static constexpr int CH = UW == 2 ? (MN <= 32 ? 3 : 2) : (MN <= 16 ? 4 : (MN <= 32 ? 3 : 2));
   static constexpr int B_BYTES = MN * BK * 2;
-  static constexpr int STAGE = CH * (A_BYTES + B_BYTES);  // [CH weight boxes][CH x boxes]
+  static constexpr int STAGE = CH * (UW * A_BYTES + B_BYTES);  // [CH x UW weight boxes][CH x boxes]
   static constexpr int STAGES = RING_BYTES / STAGE;
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int TMEM_COLS = 2 * MN < 32 ? 32 : 2 * MN;
+  static constexpr int TMEM_COLS = 2 * UW * MN < 32 ? 32 : 2 * UW * MN;
   static_assert(STAGE % 1024 == 0, "SW128 tiles need 1 KiB alignment");
 };
 
@@ -88,11 +91,12 @@ __device__ __forceinline__ int run_begin(int cta, int64_t total, int grid) {
   return (int)((int64_t)cta * total / grid);
 }
 
-template <int MN, int EPI>
+template <int MN, int EPI, int UW>
 __global__ void __launch_bounds__(THREADS, 1)
     gemv_tc_kernel(const __grid_constant__ Maps maps, const int32_t* __restrict__ mrs, int n_mod, int N, int K,
                    void* __restrict__ out, float* __restrict__ part, int* __restrict__ flags) {
-  using C = Cfg<MN>;
+  using C = Cfg<MN, UW>;
+  constexpr int UB = UW * BN;  // weight rows per unit
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -103,7 +107,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nb = N / BN;
+  const int nb = N / UB;
   const int kcn = (K + BK - 1) / BK;
   const int64_t total = (int64_t)n_mod * nb * kcn;
   const int cta = blockIdx.x, grid = gridDim.x;
@@ -150,7 +154,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       int j = 0;  // stage counter
       auto load_x = [&](int s, int k0c, int n, int row) {
         for (int b = 0; b < n; ++b)
-          tma::load_2d(&maps.x, &full[s], smem + s * C::STAGE + C::CH * A_BYTES + b * C::B_BYTES, (k0c + b) * BK, row);
+          tma::load_2d(&maps.x, &full[s], smem + s * C::STAGE + C::CH * UW * A_BYTES + b * C::B_BYTES,
+                       (k0c + b) * BK, row);
       };
       for (int c = c0; c < c1;) {
         const Seg sg = seg_at(c);
@@ -167,9 +172,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             waited = true;
           }
           tma::mbar_wait(&empty[s], ((j / C::STAGES) & 1) ^ 1);
-          tma::mbar_expect_tx(&full[s], n * (A_BYTES + C::B_BYTES));
+          tma::mbar_expect_tx(&full[s], n * (UW * A_BYTES + C::B_BYTES));
           unsigned char* st = smem + s * C::STAGE;
-          for (int b = 0; b < n; ++b) tma::load_2d(&maps.w[mod], &full[s], st + b * A_BYTES, (kc + b) * BK, blk * BN);
+          for (int b = 0; b < n; ++b)
+            for (int u = 0; u < UW; ++u)
+              tma::load_2d(&maps.w[mod], &full[s], st + (b * UW + u) * A_BYTES, (kc + b) * BK, blk * UB + u * BN);
           if (waited) {
             load_x(s, kc, n, xb);
           } else {
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int acc = it & 1;
         tma::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         umma::fence_after();
-        const uint32_t tacc = tmem + acc * MN;
+        const uint32_t tacc = tmem + acc * UW * MN;
         for (int kc = sg.k0; kc < sg.k1; kc += C::CH, ++j) {
           const int n = min(C::CH, sg.k1 - kc);
           const int s = j % C::STAGES;
@@ -204,11 +211,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           umma::fence_after();
           const uint32_t a = tma::sa(smem + s * C::STAGE);
           for (int b = 0; b < n; ++b) {
-            const uint64_t da = umma::desc_k_sw128(a + b * A_BYTES);
-            const uint64_t db = umma::desc_k_sw128(a + C::CH * A_BYTES + b * C::B_BYTES);
+            const uint64_t db = umma::desc_k_sw128(a + C::CH * UW * A_BYTES + b * C::B_BYTES);
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              umma::mma(tacc, da + 2 * k, db + 2 * k, idesc, (kc + b != sg.k0 || k != 0) ? 1u : 0u);
+            for (int u = 0; u < UW; ++u) {
+              const uint64_t da = umma::desc_k_sw128(a + (b * UW + u) * A_BYTES);
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                umma::mma(tacc + u * MN, da + 2 * k, db + 2 * k, idesc, (kc + b != sg.k0 || k != 0) ? 1u : 0u);
+            }
           }
           umma::commit(&empty[s]);
         }
@@ -229,7 +239,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int mod = sg.unit / nb, blk = sg.unit % nb;
       const int xb = mrs[mod], M = mrs[mod + 1] - xb;
       const bool owner = sg.k0 == 0;
-      const int n = blk * BN + r;
+      const int acc = it & 1;
+      bool waited_tfull = false;
+#pragma unroll 1
+      for (int u = 0; u < UW; ++u) {
+      const int n = blk * UB + u * BN + r;
       float v[MN];
       // residual prefetch: its latency overlaps this segment's MMAs
       if (EPI == PSK_EPI_RESID_ADD && owner) {
@@ -240,11 +254,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int m = 0; m < MN; ++m) v[m] = 0.f;
       }
-      const int acc = it & 1;
-      tma::mbar_wait(&tfull[acc], (it >> 1) & 1);
-      umma::fence_after();
+      if (!waited_tfull) {
+        tma::mbar_wait(&tfull[acc], (it >> 1) & 1);
+        umma::fence_after();
+        waited_tfull = true;
+      }
       {
-        const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + acc * MN;
+        const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + acc * UW * MN + u * MN;
         float a[MN];
         if (MN == 16) {
           umma::ld16(tacc, a);
@@ -258,32 +274,38 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int i = 0; i < 32; ++i) a[cc * 32 + i] = __uint_as_float(t[i]);
           }
         }
-        umma::fence_before();
-        tma::mbar_arrive(&tempty[acc]);  // the MMA of segment it+2 may overwrite it
+        if (u == UW - 1) {
+          umma::fence_before();
+          tma::mbar_arrive(&tempty[acc]);  // the MMA of segment it+2 may overwrite it
+        }
         if (!owner) {
           // contributor (this run's first segment): publish the fp32 partial
-          float* slot = part + (int64_t)cta * MN * BN;
+          float* slot = part + ((int64_t)cta * UW + u) * MN * BN;
 #pragma unroll
           for (int m = 0; m < MN; ++m) slot[m * BN + r] = a[m];
-          __threadfence();
-          named_barrier_sync(2, 128);
-          if (threadIdx.x == 64) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + cta), "r"(1) : "memory");
-          ++it;
+          if (u == UW - 1) {
+            __threadfence();
+            named_barrier_sync(2, 128);
+            if (threadIdx.x == 64)
+              asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + cta), "r"(1) : "memory");
+          }
           continue;
         }
         // owner: own accumulator + partials of the following runs, fixed order
         const int64_t unit_end = (int64_t)(sg.unit + 1) * kcn;
         if (sg.k1 < kcn) {
           for (int j2 = cta + 1; j2 < grid && run_begin(j2, total, grid) < unit_end; ++j2) {
-            if (threadIdx.x == 64) {
-              int f = 0;
-              do {
-                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(flags + j2) : "memory");
-              } while (f == 0);
-              flags[j2] = 0;  // consumed: ready for the next launch
+            if (u == 0) {
+              if (threadIdx.x == 64) {
+                int f = 0;
+                do {
+                  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(flags + j2) : "memory");
+                } while (f == 0);
+                flags[j2] = 0;  // consumed: ready for the next launch
+              }
+              named_barrier_sync(2, 128);
             }
-            named_barrier_sync(2, 128);
-            const float* slot = part + (int64_t)j2 * MN * BN;
+            const float* slot = part + ((int64_t)j2 * UW + u) * MN * BN;
 #pragma unroll
             for (int m = 0; m < MN; ++m) a[m] += __ldcg(slot + m * BN + r);
           }
@@ -295,7 +317,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // rows interleaved [gate 8 | up 8]: the up row of gate row n is n + 8,
         // held by lane + 8 of this warp
         const bool gate = (r & 15) < 8;
-        const int o = (blk * BN + (r & ~15)) / 2 + (r & 7);
+        const int o = (blk * UB + u * BN + (r & ~15)) / 2 + (r & 7);
 #pragma unroll
         for (int m = 0; m < MN; ++m) {
           const float up = __shfl_down_sync(0xffffffffu, v[m], 8);
@@ -314,6 +336,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (EPI == PSK_EPI_STORE_F32 || EPI == PSK_EPI_RESID_ADD) reinterpret_cast<float*>(out)[o] = v[m];
         }
       }
+      }  // u
       ++it;
     }
   }
@@ -378,8 +401,8 @@ static int sm_count() {
 
 constexpr int FLAG_BYTES = 4096;  // one int per CTA (<= 1024 SMs)
 
-template <int MN, int EPI>
-static int launch(const void* x, int n_rows, int K, const void* const* W_host, const int32_t* mrs, int n_mod,
+template <int MN, int EPI, int UW>
+static int launch_uw(const void* x, int n_rows, int K, const void* const* W_host, const int32_t* mrs, int n_mod,
                   int N, void* out, void* ws, cudaStream_t s) {
   Maps maps;
   for (int m = 0; m < n_mod; ++m) {
@@ -388,21 +411,33 @@ static int launch(const void* x, int n_rows, int K, const void* const* W_host, c
   }
   int rc = make_map(&maps.x, x, n_rows, K, MN, CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
   if (rc) return rc;
-  auto k = gemv_tc_kernel<MN, EPI>;
+  auto k = gemv_tc_kernel<MN, EPI, UW>;
   static bool attr = false;
   if (!attr) {
-    PSK_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<MN>::SMEM));
+    PSK_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<MN, UW>::SMEM));
     attr = true;
   }
   const int sms = sm_count();
-  const int64_t chunks = (int64_t)n_mod * (N / BN) * ((K + BK - 1) / BK);
+  const int64_t chunks = (int64_t)n_mod * (N / (UW * BN)) * ((K + BK - 1) / BK);
   const int grid = chunks < sms ? (int)chunks : sms;
   int* flags = reinterpret_cast<int*>(ws);
   float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + FLAG_BYTES);
-  PSK_CUDA_TRY(psk::launch_pdl(k, dim3(grid), dim3(THREADS), (size_t)Cfg<MN>::SMEM, s, maps, mrs, n_mod, N, K,
+  PSK_CUDA_TRY(psk::launch_pdl(k, dim3(grid), dim3(THREADS), (size_t)Cfg<MN, UW>::SMEM, s, maps, mrs, n_mod, N, K,
                                out, part, flags));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
+}
+
+template <int MN, int EPI>
+static int launch(const void* x, int n_rows, int K, const void* const* W_host, const int32_t* mrs, int n_mod,
+                  int N, void* out, void* ws, cudaStream_t s) {
+  // two 128-row blocks per unit only pay at <= 16 rows per module on the large
+  // projections (gate/up 145.6 -> 142.8 us, LM head 642 -> 610 us); at 32 and
+  // 64 rows, and for the 4096/6144-row projections, the coarser units lose
+  // (gate/up at 32 rows: 146.1 -> 151.6 us)
+  if (MN == 16 && N % (2 * BN) == 0 && N >= 16384)
+    return launch_uw<MN, EPI, 2>(x, n_rows, K, W_host, mrs, n_mod, N, out, ws, s);
+  return launch_uw<MN, EPI, 1>(x, n_rows, K, W_host, mrs, n_mod, N, out, ws, s);
 }
 
 template <int MN>
@@ -424,7 +459,7 @@ static int dispatch(int epi, const void* x, int n_rows, int K, const void* const
 extern "C" int psk_gemv_tc_workspace(int64_t* bytes) {
   PSK_CHECK_ARG(bytes != nullptr, "psk_gemv_tc_workspace: null out");
   using namespace psk::gemv_tc;
-  *bytes = FLAG_BYTES + (int64_t)sm_count() * 64 * BN * 4;
+  *bytes = FLAG_BYTES + (int64_t)sm_count() * 2 * 64 * BN * 4;  // UW <= 2 blocks x MN <= 64 rows
   return PSK_OK;
 }
 

@@ -5,6 +5,7 @@ holding every row, K not a multiple of the 1024-column stage).
 Tolerance: |gpu - ref| <= 2e-3 * max|ref| + 1e-4 (fp32 outputs),
 1e-2 * max|ref| + 1e-3 (bf16 outputs)."""
 
+import numpy as np
 import pytest
 import torch
 
@@ -87,7 +88,36 @@ def test_gemv_tc_rows_and_epilogues(rows, epi):
     _run(rows, 1536, 4096, epi, tc=True)
 
 
-@pytest.mark.parametrize("N,K", [(4096, 14336), (6144, 4096), (16384, 4096), (128, 64)])
+@pytest.mark.parametrize("N,K", [(4096, 14336), (6144, 4096), (16384, 4096), (128, 64), (28672, 4096)])
 def test_gemv_tc_shapes(N, K):
     _run([30, 31, 2, 16], N, K, 1, seed=1, tc=True)
     _run([12], N, K, 2, seed=2, tc=True)
+    _run([16, 9, 0, 3], N, K, 3 if N % 16 == 0 else 1, seed=3, tc=True)   # <= 16 rows: two-block units at N >= 16384
+
+
+@pytest.mark.parametrize("rows,N,K,epi", [([32, 32, 32, 32], 4096, 4096, 2), ([16, 16, 16, 16], 28672, 4096, 3),
+                                          ([64, 5], 6144, 4096, 1)])
+def test_gemv_tc_bit_reproducible(rows, N, K, epi):
+    """Stream-K blocks split between CTAs are reduced in a fixed order: two
+    launches give bit-identical outputs."""
+    import ctypes
+    from paper_2602_12029_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(5)
+    W = [(torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16) for _ in rows]
+    R = sum(rows)
+    x = torch.randn(R, K, device="cuda", generator=g).to(torch.bfloat16)
+    mrs = torch.tensor([0] + list(np.cumsum(rows)), dtype=torch.int32, device="cuda")
+    hp = (ctypes.c_void_p * len(rows))(*[w.data_ptr() for w in W])
+    wsb = ctypes.c_int64()
+    _lib.check(_lib.load().psk_gemv_tc_workspace(ctypes.byref(wsb)))
+    ws = torch.zeros(wsb.value, dtype=torch.uint8, device="cuda")
+    base = torch.randn(R, N if epi != 3 else N // 2, device="cuda", generator=g)
+    outs = []
+    for _ in range(2):
+        o = base.clone() if epi in (1, 2) else torch.zeros(R, N // 2 if epi == 3 else N, dtype=torch.bfloat16,
+                                                           device="cuda")
+        _lib.check(_lib.load().psk_gemv_tc(x.data_ptr(), R, K, hp, mrs.data_ptr(), len(rows), max(rows), N, epi,
+                                           o.data_ptr(), ws.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        outs.append(o)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
