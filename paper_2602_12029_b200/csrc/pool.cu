@@ -396,7 +396,6 @@ __global__ void __launch_bounds__(kThreads, 1) insert_kernel(Dev d, OpIO io, Can
   __shared__ uint64_t s_warp[32];
   __shared__ int64_t s_chain;
   __shared__ int64_t s_used, s_evicted;
-  __shared__ int s_status;
   const int tid = threadIdx.x;
   const int64_t bs = d.bs;
   const int64_t n_full = io.n_tokens / bs;
@@ -406,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1) insert_kernel(Dev d, OpIO io, Can
     if (tid == 0) publish(d, io.res, PSK_OK, 0, -1, 0);
     return;
   }
-  if (tid == 0) { s_used = d.st->used; s_evicted = 0; s_status = PSK_OK; }
+  if (tid == 0) { s_used = d.st->used; s_evicted = 0; }
   if (need > d.capacity) {  // kvstore.py:197-200, raised before any eviction
     if (tid == 0) publish(d, io.res, PSK_ECAPACITY_NEED, 0, -1, 0);
     return;

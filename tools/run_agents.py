@@ -39,8 +39,12 @@ def main():
     ap.add_argument("--pool-pages", type=int, default=7500)
     ap.add_argument("--no-batch", action="store_true", help="one prefill forward per request (FCFS)")
     ap.add_argument("--modes", default="baseline,prefillshare")
+    ap.add_argument("--max-context", type=int, default=None,
+                    help="longest context (default: 4096 for react, 5120 for reflexion: 512 + 12 x (96 + 256))")
     a = ap.parse_args()
-    cfg = LlamaConfig.llama8b(max_pos=4096 + 512) if a.shape == "8b" else LlamaConfig.tiny(max_pos=4096)
+    max_ctx = a.max_context or (5120 if a.pattern == "reflexion" else 4096)
+    cfg = (LlamaConfig.llama8b(max_pos=max_ctx + 512) if a.shape == "8b"
+           else LlamaConfig.tiny(max_pos=max_ctx + 512))
     models = list(wl.DEFAULT_MODELS)
     mods = [ModuleWeights(cfg, 100 + i) for i in range(len(models))]
     base = ModuleWeights(cfg, 99, with_head=False)
@@ -58,7 +62,7 @@ def main():
                 (point / "workload.json").write_text(wl.export_sessions(sessions))
             for mode in (ServingMode(m) for m in a.modes.split(",")):
                 srv = AgentServer(cfg, models, mode, rows_per_module=a.rows, pool_pages_per_worker=a.pool_pages,
-                                  max_context=4096, max_output=256, modules=mods, base=base,
+                                  max_context=max_ctx, max_output=256, modules=mods, base=base,
                                   prefill_batch=not a.no_batch)
                 recs = srv.run(sessions, max_concurrent=cap or None, time_scale=a.time_scale)
                 out[mode.value] = summarize(recs)
