@@ -41,6 +41,7 @@ from .kvstore import BlockPool
 from .model import (PAGE_TOKENS, DecodeBatch, DecodeRow, DecodeRunner, KVCache, LlamaConfig,
                     ModuleWeights, PrefillRunner, SessionSpec)
 from .router import Router, ServingMode
+from .staging import HostKVTier, block_keys
 
 
 @dataclass
@@ -79,7 +80,7 @@ class AgentServer:
                  rows_per_module: int = 8, pool_pages_per_worker: int = 2048, max_context: int = 4096,
                  max_output: int = 256, seed: int = 0, device: int = 0,
                  modules: list[ModuleWeights] | None = None, base: ModuleWeights | None = None,
-                 prefill_batch: bool = True):
+                 prefill_batch: bool = True, host_tier_blocks: int = 0):
         self.cfg, self.mode, self.model_ids = cfg, mode, list(model_ids)
         self.prefill_batch = prefill_batch
         self._pending: list = []
@@ -128,6 +129,9 @@ class AgentServer:
         self.runner = DecodeRunner(cfg, self.mods, self.kv, self.batch, max_output, device=device)
         self.rows = [_Row() for _ in range(self.R)]
         self.rows_per_module = rows_per_module
+        # host staging tier behind the prefix pool(s) (staging.py; 0 = off)
+        self.tier = HostKVTier(self.kv, host_tier_blocks) if host_tier_blocks > 0 else None
+        self._pending_store: list = []
         self.max_context, self.max_output = max_context, max_output
         self.dev = torch.device("cuda", device)
         self._sess_len = [0] * self.R
@@ -176,7 +180,19 @@ class AgentServer:
         if n % PAGE_TOKENS:
             pages.append(self.tail_page[row])
         # partial prefill from the last cached full block; the tail block is recomputed
-        pos0 = min(m, (n // PAGE_TOKENS) * PAGE_TOKENS)
+        nfull = n // PAGE_TOKENS
+        pos0 = min(m, nfull * PAGE_TOKENS)
+        if self.tier is not None and nfull > 0:
+            # GPU misses found in the host tier are reloaded instead of recomputed
+            keys = block_keys(ns, req.ctx, nfull)
+            mb = m // PAGE_TOKENS
+            slots = self.tier.lookup(keys[mb:nfull])
+            if slots:
+                self.tier.reload(slots, fresh[:len(slots)])
+            pos0 = min(m + PAGE_TOKENS * len(slots), nfull * PAGE_TOKENS)
+            h = len(slots)
+            if nfull - mb > h:  # write-through of the blocks this forward computes
+                self._pending_store.append((keys[mb + h:nfull], fresh[h:nfull - mb]))
         if n > pos0:
             ri = 0 if self.base is not None else req.model_idx
             self._pending.append((ri, self._vocab_ids(req.ctx[pos0:]), pos0, pages))
@@ -193,6 +209,8 @@ class AgentServer:
         for ri, toks, pos0, pages in self._pending:
             by_runner.setdefault(ri, []).append((toks, pos0, pages))
         self._pending, self._pending_slots = [], set()
+        if self.tier is not None:
+            self.tier.fence()
         for ri, seqs in by_runner.items():
             runner = self.prefillers[ri]
             chunk, tot = [], 0
@@ -205,6 +223,10 @@ class AgentServer:
                 if sq is not None:
                     chunk.append(sq)
                     tot += int(sq[0].shape[0])
+        if self.tier is not None:
+            for keys, pages in self._pending_store:
+                self.tier.store(keys, pages)
+            self._pending_store = []
 
     def _events(self, kind: str):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

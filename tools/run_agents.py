@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--pool-pages", type=int, default=7500)
     ap.add_argument("--no-batch", action="store_true", help="one prefill forward per request (FCFS)")
     ap.add_argument("--modes", default="baseline,prefillshare")
+    ap.add_argument("--host-tier-blocks", type=int, default=0, help="host staging tier behind the prefix pool")
     ap.add_argument("--max-context", type=int, default=None,
                     help="longest context (default: 4096 for react, 5120 for reflexion: 512 + 12 x (96 + 256))")
     a = ap.parse_args()
@@ -63,10 +64,12 @@ def main():
             for mode in (ServingMode(m) for m in a.modes.split(",")):
                 srv = AgentServer(cfg, models, mode, rows_per_module=a.rows, pool_pages_per_worker=a.pool_pages,
                                   max_context=max_ctx, max_output=256, modules=mods, base=base,
-                                  prefill_batch=not a.no_batch)
+                                  prefill_batch=not a.no_batch, host_tier_blocks=a.host_tier_blocks)
                 recs = srv.run(sessions, max_concurrent=cap or None, time_scale=a.time_scale)
                 out[mode.value] = summarize(recs)
                 out[mode.value]["gpu_time"] = srv.gpu_time()
+                if srv.tier is not None:
+                    out[mode.value]["host_tier"] = srv.tier.stats()
                 if point is not None:
                     echo = {"mode": mode.value, "workload": out["workload"], "shape": a.shape,
                             "rows_per_model": a.rows, "pool_blocks_per_worker": a.pool_pages}
