@@ -13,7 +13,8 @@
 //
 // Persistent, one CTA per SM, 6 warps:
 //   warp 0   TMA producer: per 64-column k-chunk one 128x64 weight box
-//            (16 KiB, SW128) + one MNx64 x box, into a ~200 KiB ring; the
+//            (16 KiB, SW128) per 128-row block + one MNx64 x box; 2-4
+//            chunks per ring stage behind one mbarrier (216 KiB ring); the
 //            weight boxes of the first ring fill are issued before the PDL
 //            wait (weights never depend on the previous kernel)
 //   warp 1   MMA issuer (one lane): 4 x tcgen05.mma per chunk into one of two
