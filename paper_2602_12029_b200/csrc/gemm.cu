@@ -15,6 +15,10 @@
 //              epilogue, stores; accumulator stage released via mbarrier so
 //              the MMA of tile i+1 overlaps the epilogue of tile i.
 // Tiles are walked m-fastest so one wave shares its B (weight) tiles in L2.
+// Default kernel: the CTA-pair variant below (gemm_pair_kernel, 256x256
+// tiles on two SMs with tcgen05 cta_group::2, half of B staged per SM);
+// PSK_GEMM_PAIR=0 selects this 1-SM kernel, which also remains the split-K
+// path when a workspace is bound.
 //
 // Fused epilogues: bf16 store, fp32 residual add, SiLU(gate)*up over the
 // [gate8|up8]-interleaved weight layout, and QKV -> RoPE (rotate-half) ->
@@ -493,6 +497,203 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ------------------------------------------------ CTA-pair (2-SM) variant --
+//
+// One cluster of two CTAs on a TPC computes a 256x256 tile with
+// tcgen05.mma.cta_group::2 (M = 256: each CTA's TMEM holds its own 128 rows
+// x 256 fp32 columns). Each CTA stages its 128 A rows and HALF of the B tile
+// (128 of the 256 weight rows); the pair's tensor cores read the other half
+// across the TPC, so per SM a k-block moves 32 KiB of operands through
+// shared memory / L2 instead of 48 KiB (the 1-SM kernel's limit: 148 SMs x
+// 48 KiB per 512-cycle k-block is above what L2 delivers). Only the leader
+// (rank 0) issues MMAs; both CTAs' TMA loads complete on the leader's `full`
+// barrier; the leader's commits multicast `empty` / `tfull` to both CTAs;
+// both epilogues release the accumulator on the leader's `tempty` (256
+// arrivals). Tail tiles split along N (pieces of 256 / S columns, MMA N =
+// 256 / S, each CTA loads 128 / S weight rows) exactly like the 1-SM kernel.
+namespace pair {
+
+constexpr int BM2 = 256;                     // pair tile rows (128 per CTA)
+constexpr int A_BYTES = BM * BK * 2;         // per CTA: 128 x 64
+constexpr int B_BYTES = (BN / 2) * BK * 2;   // per CTA: 128 x 64 (half of B)
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int STAGES = 6;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t peer_addr(const void* local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(local)), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// TMA load whose completion (complete_tx) lands on the LEADER CTA's barrier:
+// the barrier's shared::cta address with the peer bit (24) cleared.
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(smem_addr(bar) & 0xFEFFFFFFu), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma2_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+// arrive (once, when this thread's prior MMAs complete) on `bar` in both CTAs
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_addr(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                     const __grid_constant__ CUtensorMap tmap_bp, int M, int N, int K, Epi e, Sched sc) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int m_tiles = (M + BM2 - 1) / BM2;
+  const int kb_n = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmap_a);
+    tma_prefetch(&tmap_b);
+    tma_prefetch(&tmap_bp);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int item = pair; item < sc.items; item += n_pairs) {
+        int t, kb0, kb1, split, piece;
+        item_range(sc, item, kb_n, t, kb0, kb1, split, piece);
+        const int mb = t % m_tiles, nb = t / m_tiles;
+        const int row0 = mb * BM2 + (int)rank * BM;
+        const int hp = BN / sc.S / 2;  // this CTA's share of a tail piece's weight rows
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (piece >= 0) {
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * (A_BYTES + hp * BK * 2));
+            tma_load_2d_pair(&tmap_a, &full[stage], sA + stage * A_BYTES, kb * BK, row0);
+            tma_load_2d_pair(&tmap_bp, &full[stage], sB + stage * B_BYTES, kb * BK,
+                             nb * BN + piece * 2 * hp + (int)rank * hp);
+          } else {
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+            tma_load_2d_pair(&tmap_a, &full[stage], sA + stage * A_BYTES, kb * BK, row0);
+            tma_load_2d_pair(&tmap_b, &full[stage], sB + stage * B_BYTES, kb * BK, nb * BN + (int)rank * (BN / 2));
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc_full = idesc_bf16(BM2, BN);
+      const uint32_t idesc_piece = idesc_bf16(BM2, BN / sc.S);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int item = pair; item < sc.items; item += n_pairs, ++it) {
+        int t, kb0, kb1, split, piece;
+        item_range(sc, item, kb_n, t, kb0, kb1, split, piece);
+        const uint32_t idesc = piece >= 0 ? idesc_piece : idesc_full;
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tacc = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t da = smem_desc_sw128(sA + stage * A_BYTES);
+          const uint64_t db = smem_desc_sw128(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma2_bf16(tacc, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          umma2_commit_both(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma2_commit_both(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int r_in_tile = q * 32 + lane;
+    const uint32_t tempty_leader = peer_addr(tempty, 0);
+    int it = 0;
+    for (int item = pair; item < sc.items; item += n_pairs, ++it) {
+      int t, kb0, kb1, split, piece;
+      item_range(sc, item, kb_n, t, kb0, kb1, split, piece);
+      const int mb = t % m_tiles, nb = t / m_tiles;
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int row = mb * BM2 + (int)rank * BM + r_in_tile;
+      const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (piece >= 0)
+        epilogue_tile(e, tacc, row, row < M, nb * BN + piece * (BN / sc.S), BN / sc.S);
+      else
+        epilogue_tile(e, tacc, row, row < M, nb * BN);
+      tc_fence_before();
+      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader + acc * 8)
+                   : "memory");
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace pair
+
 // ------------------------------------------------------------ host side --
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -542,6 +743,54 @@ struct Workspace {
 static Workspace g_ws;
 constexpr int64_t WS_COUNTER_BYTES = 4096;
 
+// CTA-pair kernel unless PSK_GEMM_PAIR=0 (1-SM kernel, kept for A/B runs
+// and as the split-K path when a workspace is bound).
+static bool use_pair() {
+  static int v = -1;
+  if (v < 0) {
+    const char* env = getenv("PSK_GEMM_PAIR");
+    v = (env && env[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static int launch_pair(const CUtensorMap& ma, const void* B, int M, int N, int K, const Epi& e, cudaStream_t s,
+                       int sms) {
+  static bool attr = false;
+  if (!attr) {
+    PSK_CUDA_TRY(cudaFuncSetAttribute(pair::gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      pair::SMEM_BYTES));
+    attr = true;
+  }
+  CUtensorMap mb, mbp;
+  int rc = make_map(&mb, B, N, K, BN / 2);
+  if (rc) return rc;
+  const int tiles = ((M + pair::BM2 - 1) / pair::BM2) * (N / BN);
+  const int max_pairs = sms / 2;
+  const int pairs = tiles < max_pairs ? tiles : max_pairs;
+  Sched sc{};
+  sc.tiles = tiles;
+  sc.full = tiles;
+  sc.S = 1;
+  sc.split_n = 1;
+  mbp = mb;
+  const int rem = tiles % pairs, waves = tiles / pairs;
+  if (waves >= 1 && rem > 0 && rem <= pairs / 2) {
+    // split-N tail pieces of 256 / S columns (QKV/RoPE: whole heads)
+    int S = pairs / rem >= 4 ? 4 : 2;
+    if (e.mode == PSK_EPI_QKV_ROPE_KV) S = 2;
+    rc = make_map(&mbp, B, N, K, BN / S / 2);
+    if (rc) return rc;
+    sc.full = tiles - rem;
+    sc.rem = rem;
+    sc.S = S;
+  }
+  sc.items = sc.full + sc.rem * sc.S;
+  pair::gemm_pair_kernel<<<2 * pairs, THREADS, pair::SMEM_BYTES, s>>>(ma, mb, mbp, M, N, K, e, sc);
+  PSK_LAUNCH_CHECK();
+  return PSK_OK;
+}
+
 static int launch(const void* A, const void* B, int M, int N, int K, const Epi& e, cudaStream_t s) {
   if (M <= 0) return PSK_OK;
   if (N % BN != 0 || K % BK != 0) {
@@ -561,6 +810,7 @@ static int launch(const void* A, const void* B, int M, int N, int K, const Epi& 
     PSK_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SMEM_BYTES));
   }
+  if (!g_ws.part && use_pair()) return launch_pair(ma, B, M, N, K, e, s, sms);
   const int tiles = ((M + BM - 1) / BM) * (N / BN);
   const int grid = tiles < sms ? tiles : sms;
   Sched sc{};

@@ -5,6 +5,7 @@ outputs rounded to bf16 where the kernel stores bf16:
   |gpu - ref| <= 2e-3 * max|ref| + 1e-4  (fp32 outputs)"""
 
 import ctypes as C
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -176,3 +177,29 @@ def test_gemm_split_n_tail(M, N, K):
     _gemm(A, B, 3, o, F)
     torch.cuda.synchronize()
     assert (o.float() - silu_ref).abs().max().item() <= 1e-2 * silu_ref.abs().max().item() + 1e-3
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 512, 256), (257, 6144, 4096), (4096, 6144, 4096), (2560, 2048, 4096)])
+def test_gemm_pair_matches_one_sm(M, N, K, tmp_path):
+    """The CTA-pair kernel (default) and the 1-SM kernel (PSK_GEMM_PAIR=0,
+    read once per process, so it runs in a child) are the same fp32 sums in
+    the same k order per output: bit-identical fp32 outputs, fully
+    out-of-range second-CTA rows included (M=257, 300)."""
+    import os
+    import subprocess
+    import sys
+    A, B = _rand(M, K, seed=31), _rand(N, K, std=0.02, seed=32)
+    out = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    _gemm(A, B, 1, out, N)
+    torch.cuda.synchronize()
+    torch.save({"A": A.cpu(), "B": B.cpu()}, tmp_path / "ab.pt")
+    code = ("import sys, torch; sys.path.insert(0, %r); from paper_2602_12029_b200 import _lib; L = _lib.load();"
+            "d = torch.load(%r); A, B = d['A'].cuda(), d['B'].cuda();"
+            "o = torch.empty(A.shape[0], B.shape[0], dtype=torch.float32, device='cuda');"
+            "_lib.check(L.psk_gemm(A.data_ptr(), B.data_ptr(), A.shape[0], B.shape[0], A.shape[1], 1, o.data_ptr(),"
+            " B.shape[0], torch.cuda.current_stream().cuda_stream)); torch.save(o.cpu(), %r)"
+            % (str(Path(__file__).resolve().parent.parent), str(tmp_path / "ab.pt"), str(tmp_path / "o.pt")))
+    env = dict(os.environ, PSK_GEMM_PAIR="0")
+    subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=300)
+    one_sm = torch.load(tmp_path / "o.pt")
+    assert torch.equal(out.cpu(), one_sm)

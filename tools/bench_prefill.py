@@ -2,7 +2,7 @@
 causal attention alone (K3, per layer), CUDA-graph replay, CUDA events.
 PSK_PREFILL_TC1=1 selects the previous single-tile tcgen05 kernel.
 
-    python tools/bench_prefill.py [T]
+    python tools/bench_prefill.py [T] [quick]   (quick: whole-prefill line only)
 """
 import ctypes as C
 import sys
@@ -26,6 +26,8 @@ pt = torch.arange(T // 16 + 1, dtype=torch.int32, device="cuda")
 dt = bench._time_launches(lambda: pre.run(toks, 0, pt), 3)
 fl = pre.flops(T)
 print(f"prefill T={T}: {dt * 1e3:.2f} ms  {fl / dt / 1e12:.1f} TFLOP/s")
+if "quick" in sys.argv[2:]:
+    sys.exit(0)
 lib = _lib.load()
 q = torch.randn(T, cfg.n_heads, cfg.head_dim, device="cuda").to(torch.bfloat16)
 out = torch.empty_like(q)
