@@ -36,6 +36,12 @@ int psk_abi_version(void);
 const char* psk_last_error(void);
 /* SM count of `device` (grid sizing is a multiple of it). */
 int psk_sm_count(int device, int32_t* out);
+/* SM budget for the persistent kernels' grids (0 = every SM). Lets a
+ * serving loop run prefill kernels on a share of the SMs beside decode on
+ * another stream; set before the launches (or graph capture) it applies to.
+ * Process-wide, not per stream. No reference counterpart (a B200 serving knob). */
+int psk_set_sm_budget(int32_t n);
+int psk_get_sm_budget(int32_t* out);
 
 /* ------------------------------------------------------------------------ *
  * Deterministic weight init (random-init models; no checkpoints).

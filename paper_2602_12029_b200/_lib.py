@@ -74,6 +74,8 @@ _SIGS: dict[str, list] = {
     "psk_abi_version": [],
     "psk_last_error": [],
     "psk_sm_count": [C.c_int, C.POINTER(_I32)],
+    "psk_set_sm_budget": [_I32],
+    "psk_get_sm_budget": [C.POINTER(_I32)],
     "psk_init_normal_bf16": [_P, _I64, _U64, _F, _P],
     "psk_fill_bf16": [_P, _I64, _F, _P],
     # K7 pool
@@ -174,3 +176,16 @@ def bind_gemm_workspace(device) -> None:
     check(load().psk_gemm_workspace(C.byref(nb)))
     _gemm_ws = torch.zeros(nb.value, dtype=torch.uint8, device=device)
     check(load().psk_gemm_bind_workspace(_gemm_ws.data_ptr(), nb.value))
+
+
+def sm_budget() -> int:
+    """SMs the persistent kernels currently size their grids for."""
+    v = _I32()
+    check(load().psk_get_sm_budget(C.byref(v)))
+    return int(v.value)
+
+
+def set_sm_budget(n: int) -> None:
+    """0 = all SMs; else the grid budget for the launches (and graph
+    captures) that follow, process-wide."""
+    check(load().psk_set_sm_budget(int(n)))

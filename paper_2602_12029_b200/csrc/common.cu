@@ -76,6 +76,23 @@ void trace_report(const char* kernel, int n, int nph, const char* const* names) 
   free(h);
 }
 
+static int g_sm_budget = 0;
+
+int device_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+int sm_budget() {
+  const int d = device_sms();
+  return g_sm_budget > 0 && g_sm_budget < d ? g_sm_budget : d;
+}
+
 static int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   if (g > 148 * 16) g = 148 * 16;
@@ -96,6 +113,19 @@ int psk_sm_count(int device, int32_t* out) {
   int v = 0;
   PSK_CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
   *out = v;
+  return PSK_OK;
+}
+
+int psk_set_sm_budget(int32_t n) {
+  PSK_CHECK_ARG(n >= 0, "psk_set_sm_budget: negative budget");
+  PSK_CHECK_ARG(n == 0 || n >= 2, "psk_set_sm_budget: budget must be 0 (all SMs) or >= 2");
+  psk::g_sm_budget = n;
+  return PSK_OK;
+}
+
+int psk_get_sm_budget(int32_t* out) {
+  PSK_CHECK_ARG(out != nullptr, "psk_get_sm_budget: null out");
+  *out = psk::sm_budget();
   return PSK_OK;
 }
 

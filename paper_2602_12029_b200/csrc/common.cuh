@@ -23,6 +23,12 @@ void set_error(const char* fmt, ...);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// SMs the persistent kernels size their grids for: the device's count, or
+// the budget set with psk_set_sm_budget (a spatial share of the GPU for
+// kernels that run beside another stream's work, e.g. prefill beside decode).
+int sm_budget();
+int device_sms();
+
 }  // namespace psk
 
 #define PSK_CHECK_ARG(cond, ...)                       \

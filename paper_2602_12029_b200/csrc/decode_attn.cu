@@ -1628,22 +1628,14 @@ using namespace psk::dattn;
 
 extern "C" {
 
-static int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
-}
+static int sm_count() { return psk::sm_budget(); }
 
 // Partial slots the workspace holds: enough for the caller's fixed splits,
 // the stream-K schedule (grid + groups) and the all-heads kernel (one
 // wave of (session, split) CTAs: groups x sms / n_sess).
 static int64_t ws_slots(const psk_decode_batch* b, int32_t n_kv_heads, int32_t splits) {
   const int64_t groups = (int64_t)b->n_sess * n_kv_heads;
-  const int sms = sm_count();
+  const int sms = psk::device_sms();  // any budget <= the device count fits
   int64_t slots = (int64_t)sms + groups;
   if (splits > 0 && groups * splits > slots) slots = groups * splits;
   const int64_t hsplit = b->n_sess > 0 ? (sms / b->n_sess > 1 ? sms / b->n_sess : 1) : 1;

@@ -802,14 +802,13 @@ static int launch(const void* A, const void* B, int M, int N, int K, const Epi& 
   if (rc) return rc;
   rc = make_map(&mb, B, N, K, BN);
   if (rc) return rc;
-  static int sms = 0;
-  if (!sms) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static bool attr = false;
+  if (!attr) {
     PSK_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SMEM_BYTES));
+    attr = true;
   }
+  const int sms = sm_budget();
   if (!g_ws.part && use_pair()) return launch_pair(ma, B, M, N, K, e, s, sms);
   const int tiles = ((M + BM - 1) / BM) * (N / BN);
   const int grid = tiles < sms ? tiles : sms;
@@ -857,9 +856,7 @@ extern "C" {
 
 int psk_gemm_workspace(int64_t* bytes) {
   PSK_CHECK_ARG(bytes != nullptr, "psk_gemm_workspace: null out");
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = psk::device_sms();
   *bytes = psk::gemm::WS_COUNTER_BYTES + (int64_t)sms * psk::gemm::BM * psk::gemm::BN * 4;
   return PSK_OK;
 }

@@ -276,12 +276,7 @@ int launch(const void* x, int K, const void* const* W, const int32_t* mrs, int n
     PSK_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NT>::SMEM));
     attr_set = true;
   }
-  static int sms = 0;
-  if (!sms) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = psk::sm_budget();
   const int tiles = n_mod * (N / TR);
   const int grid = tiles < sms ? tiles : sms;
   PSK_CUDA_TRY(psk::launch_pdl(k, dim3(grid), dim3(THREADS), (size_t)Cfg<NT>::SMEM, s,

@@ -390,15 +390,7 @@ static int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
   return PSK_OK;
 }
 
-static int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
-}
+static int sm_count() { return psk::sm_budget(); }
 
 constexpr int FLAG_BYTES = 4096;  // one int per CTA (<= 1024 SMs)
 
@@ -460,7 +452,7 @@ static int dispatch(int epi, const void* x, int n_rows, int K, const void* const
 extern "C" int psk_gemv_tc_workspace(int64_t* bytes) {
   PSK_CHECK_ARG(bytes != nullptr, "psk_gemv_tc_workspace: null out");
   using namespace psk::gemv_tc;
-  *bytes = FLAG_BYTES + (int64_t)sm_count() * 2 * 64 * BN * 4;  // UW <= 2 blocks x MN <= 64 rows
+  *bytes = FLAG_BYTES + (int64_t)psk::device_sms() * 2 * 64 * BN * 4;  // UW <= 2 blocks x MN <= 64 rows
   return PSK_OK;
 }
 

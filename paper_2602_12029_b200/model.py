@@ -382,7 +382,7 @@ class DecodeRunner:
         self.logits = torch.empty(R, cfg.vocab, dtype=f32, device=dev)
         self.out_tokens = torch.full((R, max_new), -1, dtype=torch.int32, device=dev)
         self.rope = torch.from_numpy(rope_table(cfg)).to(dev)
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        sms = _lib.sm_budget()  # the SMs this runner's kernels are sized for
         # fixed splits (one CTA per SM over the groups). splits=0 selects the
         # stream-K schedule of K6, which is correct but measured slower: runs
         # that cut across (session, head) groups lose the DRAM locality of 8
