@@ -317,6 +317,22 @@ __device__ __forceinline__ void item_range(const Sched& sc, int item, int kb_n, 
   }
 }
 
+// Tile order: m-fastest inside groups of GROUP_ROWS rows, group by group.
+// Inside a group a wave shares its weight (B) tiles in L2 and the group's A
+// rows (4096 x K bf16 <= 117 MiB at K = 14336, 33.5 MiB at K = 4096) stay
+// L2-resident while every n column passes over them; plain m-fastest order
+// over a taller A re-streams all of A from HBM once per n column.
+constexpr int GROUP_ROWS = 4096;
+
+__device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int gm, int& mb, int& nb) {
+  const int g = t / (gm * n_tiles);
+  const int m0 = g * gm;
+  const int rows = m_tiles - m0 < gm ? m_tiles - m0 : gm;
+  const int r = t - g * gm * n_tiles;
+  mb = m0 + r % rows;
+  nb = r / rows;
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmap_a,
                         const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_bp,
@@ -368,7 +384,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int item = blockIdx.x; item < sc.items; item += gridDim.x) {
         int t, kb0, kb1, split, piece;
         item_range(sc, item, kb_n, t, kb0, kb1, split, piece);
-        const int mb = t % m_tiles, nb = t / m_tiles;
+        int mb, nb;
+        tile_coords(t, m_tiles, N / BN, GROUP_ROWS / BM, mb, nb);
         const int pn = BN / sc.S;  // N-piece width
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -425,7 +442,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int item = blockIdx.x; item < sc.items; item += gridDim.x, ++it) {
       int t, kb0, kb1, split, piece;
       item_range(sc, item, kb_n, t, kb0, kb1, split, piece);
-      const int mb = t % m_tiles, nb = t / m_tiles;
+      int mb, nb;
+      tile_coords(t, m_tiles, N / BN, GROUP_ROWS / BM, mb, nb);
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
@@ -611,7 +629,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int item = pair; item < sc.items; item += n_pairs) {
         int t, kb0, kb1, split, piece;
         item_range(sc, item, kb_n, t, kb0, kb1, split, piece);
-        const int mb = t % m_tiles, nb = t / m_tiles;
+        int mb, nb;
+        tile_coords(t, m_tiles, N / BN, GROUP_ROWS / BM2, mb, nb);
         const int row0 = mb * BM2 + (int)rank * BM;
         const int hp = BN / sc.S / 2;  // this CTA's share of a tail piece's weight rows
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -669,7 +688,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     for (int item = pair; item < sc.items; item += n_pairs, ++it) {
       int t, kb0, kb1, split, piece;
       item_range(sc, item, kb_n, t, kb0, kb1, split, piece);
-      const int mb = t % m_tiles, nb = t / m_tiles;
+      int mb, nb;
+      tile_coords(t, m_tiles, N / BN, GROUP_ROWS / BM2, mb, nb);
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();

@@ -324,6 +324,7 @@ class DecodeBatch:
         self.reset()
 
 
+PER_SEQ_ATTN_MIN_TOKENS = 1024  # batched prefill: per-sequence K3 when every sequence has this many new tokens
 GEMV_MMA_MAX_ROWS = 8  # rows per module up to which the mma.sync GEMV (K5) beats K5-TC
 
 
@@ -587,6 +588,17 @@ class PrefillRunner:
         d_pos, d_slot = dplan[ni:ni + T], dplan[ni + T:ni + 2 * T]
         d_pages = dplan[ni + 2 * T:]
         tokens = torch.cat([t for t, _, _ in seqs])
+        # >= 1024 new tokens in every sequence: per-sequence K3 launches (the
+        # single-sequence kernel's 128-row ping-pong tiles beat the batched
+        # kernel's 64-token q-blocks there); GEMMs stay batched
+        per_seq = []
+        if min(Ts) >= PER_SEQ_ATTN_MIN_TOKENS:
+            o_, pg_ = 0, 0
+            for (_, pos0, pt), n in zip(seqs, Ts):
+                per_seq.append((o_, n, pos0, pg_))
+                o_ += n
+                pg_ += len(pt)
+        qrow = cfg.n_heads * cfg.head_dim * 2  # bytes per token row of q / attn
         self._batch_keep = (dplan, tokens)  # alive until the next call (async kernels)
         s = stream if stream is not None else _stream()
         chk = _lib.check
@@ -600,8 +612,13 @@ class PrefillRunner:
             chk(lib.psk_gemm_qkv_rope_kv_rows(_ptr(self.xn), _ptr(w.wqkv[l]), T, d, cfg.n_heads,
                                               _ptr(self.rope), _ptr(d_pos), _ptr(d_slot), kvl, l,
                                               _ptr(self.q), s))
-            chk(lib.psk_prefill_attn_batch(_ptr(self.q), len(items), _ptr(d_items), cfg.n_heads, kvl, l,
-                                           _ptr(d_pages), _ptr(self.attn), s))
+            if per_seq:  # long sequences: the single-sequence ping-pong K3 on each row range
+                for (o_, n_, p0_, pg_) in per_seq:
+                    chk(lib.psk_prefill_attn(_ptr(self.q) + o_ * qrow, n_, p0_, cfg.n_heads, kvl, l,
+                                             _ptr(d_pages) + 4 * pg_, _ptr(self.attn) + o_ * qrow, s))
+            else:
+                chk(lib.psk_prefill_attn_batch(_ptr(self.q), len(items), _ptr(d_items), cfg.n_heads, kvl, l,
+                                               _ptr(d_pages), _ptr(self.attn), s))
             chk(lib.psk_gemm(_ptr(self.attn), _ptr(w.wo[l]), T, d, cfg.n_heads * cfg.head_dim, 2,
                              _ptr(self.h), d, s))
             chk(lib.psk_rmsnorm_rows(_ptr(self.h), T, d, _ptr(g2), None, eps, _ptr(self.xn), s))

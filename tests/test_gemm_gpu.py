@@ -41,7 +41,8 @@ def _gemm(A, B, epi, out, ldo):
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (1, 256, 256), (300, 512, 256),
-                                   (4096, 6144, 4096), (1000, 1024, 14336), (129, 4096, 4096)])
+                                   (4096, 6144, 4096), (1000, 1024, 14336), (129, 4096, 4096),
+                                   (9000, 1024, 512), (12288, 2048, 256)])
 def test_gemm_store(M, N, K):
     A, B = _rand(M, K, seed=1), _rand(N, K, std=0.02, seed=2)
     ref = A.float() @ B.float().T

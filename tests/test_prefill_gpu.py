@@ -104,7 +104,7 @@ def test_shared_prefill_then_decode_modules(shape):
     assert flips <= n_mod
 
 
-@pytest.mark.parametrize("shape", ["tiny", "8b2"])
+@pytest.mark.parametrize("shape", ["tiny", "8b2", "8b2-long"])
 def test_batched_partial_prefill_bit_identical(shape):
     """run_batch (stacked varlen rows: per-row RoPE position + KV slot in the
     QKV epilogue, one K3 CTA per (sequence, q-block)) writes exactly the KV
@@ -112,10 +112,13 @@ def test_batched_partial_prefill_bit_identical(shape):
     after cached prefixes (pos0 > 0, block-aligned and mid-page tails),
     scattered page tables, sequences longer than one q-block."""
     from paper_2602_12029_b200.model import KVCache, LlamaConfig, ModuleWeights, PrefillRunner
-    cfg = LlamaConfig.tiny() if shape == "tiny" else LlamaConfig.llama8b(n_layers=2, max_pos=1024)
+    cfg = LlamaConfig.tiny() if shape == "tiny" else LlamaConfig.llama8b(n_layers=2, max_pos=4096)
     base = ModuleWeights(cfg, 5, with_head=False)
     rng = np.random.default_rng(7)
     specs = [(0, 300), (64, 21), (32, 1), (160, 77)]  # (pos0, new tokens)
+    if shape == "8b2-long":  # every sequence >= 1024 new tokens: per-sequence K3 launches
+        specs = [(0, 1100), (48, 1030), (0, 1024)]
+    max_tokens = max(1024, sum(n for _, n in specs))
     n_pages = sum((p + n + 15) // 16 for p, n in specs) + 4
     perm = rng.permutation(n_pages).tolist()
     seqs, pts = [], []
@@ -128,7 +131,7 @@ def test_batched_partial_prefill_bit_identical(shape):
     for batched in (False, True):
         kv = KVCache(cfg, n_pages)
         kv.data.zero_()
-        pre = PrefillRunner(cfg, base, kv, max_tokens=1024)
+        pre = PrefillRunner(cfg, base, kv, max_tokens=max_tokens)
         for (p0, _), pt, pf in zip(specs, pts, prefix):  # cached prefixes, one sequence each
             if p0:
                 pre.run(pf, 0, torch.tensor(pt, dtype=torch.int32, device="cuda"))

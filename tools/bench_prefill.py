@@ -28,6 +28,22 @@ fl = pre.flops(T)
 print(f"prefill T={T}: {dt * 1e3:.2f} ms  {fl / dt / 1e12:.1f} TFLOP/s")
 if "quick" in sys.argv[2:]:
     sys.exit(0)
+if "batch" in sys.argv[2:]:  # G sequences of T tokens: G x run() vs one run_batch()
+    for G in (2, 4):
+        kvb = KVCache(cfg, G * (T // 16 + 1) + 8)
+        preb = PrefillRunner(cfg, base, kvb, max_tokens=G * T)
+        seqs = [(torch.randint(0, cfg.vocab, (T,), device="cuda"), 0,
+                 list(range(g * (T // 16 + 1), (g + 1) * (T // 16 + 1)))) for g in range(G)]
+        pts = [torch.tensor(p_, dtype=torch.int32, device="cuda") for _, _, p_ in seqs]
+
+        def each():
+            for (t_, p0, _), pt_ in zip(seqs, pts):
+                preb.run(t_, p0, pt_)
+        de = bench._time_launches(each, 3, graph=False)
+        db = bench._time_launches(lambda: preb.run_batch(seqs), 3, graph=False)
+        print(f"G={G} x T={T}: {G} x run {de * 1e3:.2f} ms | run_batch {db * 1e3:.2f} ms "
+              f"({de / db:.3f}x)", flush=True)
+    sys.exit(0)
 lib = _lib.load()
 q = torch.randn(T, cfg.n_heads, cfg.head_dim, device="cuda").to(torch.bfloat16)
 out = torch.empty_like(q)
