@@ -358,12 +358,12 @@ class BlockPool:
         if code not in (_lib.PSK_OK, _lib.PSK_ECAPACITY, _lib.PSK_ECAPACITY_NEED):
             _lib.check(code)
         self._absorb()
-        if code == _lib.PSK_ECAPACITY_NEED:
-            need = n // self.block_size - len(self._walk(ns, seq))
-            raise self.CapacityError(
-                f"need {need} blocks exceeds capacity {self.capacity_blocks}")
-        if code == _lib.PSK_ECAPACITY:
-            raise self.CapacityError("cannot free blocks: all remaining blocks pinned")
+        if code in (_lib.PSK_ECAPACITY_NEED, _lib.PSK_ECAPACITY):
+            need = n // self.block_size - len(self._walk(ns, seq))  # kvstore.py:150
+            if code == _lib.PSK_ECAPACITY_NEED:
+                raise self.CapacityError(
+                    f"need {need} blocks exceeds capacity {self.capacity_blocks}")
+            raise self.CapacityError(f"cannot free {need} blocks: all remaining blocks pinned")
         m = self._res.count
         if m and ns not in self._ns_inserted:
             self._ns_inserted.append(ns)

@@ -58,6 +58,16 @@ class RequestRecord:
     failed: bool = False
 
 
+TRACE_KINDS = ("SessionArrival", "PrefillStart", "PrefillComplete", "HandoffComplete", "DecodeStep",
+               "RequestComplete", "SessionComplete")  # core.py:124-131
+
+
+def trace_line(t_us: float, seq: int, kind: str, session: int = -1, request: int = -1, worker: int = -1,
+               detail: str = "") -> str:
+    """SimEvent.trace_line (core.py:146-150), byte for byte."""
+    return f"{int(t_us)} {seq} {kind} {session} {request} {worker} {detail}"
+
+
 @dataclass
 class _Req:
     rec: RequestRecord
@@ -83,6 +93,9 @@ class AgentServer:
                  prefill_batch: bool = True, host_tier_blocks: int = 0):
         self.cfg, self.mode, self.model_ids = cfg, mode, list(model_ids)
         self.prefill_batch = prefill_batch
+        self.trace: list[str] | None = None
+        self._seq = 0
+        self._fail_reason = ""
         self._pending: list = []
         self._pending_slots: set = set()
         M = len(model_ids)
@@ -158,6 +171,7 @@ class AgentServer:
         module). Returns (held handles, page table, matched tokens,
         prefilled tokens, decode row), or None on CapacityExhausted."""
         worker = self.router.route_prefill(req.rec, [0] * len(self.pools))
+        self._emit(now_us, "PrefillStart", req.session, req.rec.request_id, worker)
         pool = self.pools[worker]
         ns = self.router.prefill_namespace(req.rec.model_id)
         n = len(req.ctx)
@@ -169,9 +183,10 @@ class AgentServer:
             self._flush_prefills()
         try:
             new = pool.insert(ns, req.ctx, now_us)
-        except pool.CapacityError:
+        except pool.CapacityError as exc:
             # cluster.py:348-350: release the matched pins and fail the request
             pool.release(chain)
+            self._fail_reason = str(exc)
             return None
         pool.pin(new, now_us)
         fresh = [base + s for s in new.slots.tolist()]
@@ -193,6 +208,9 @@ class AgentServer:
             h = len(slots)
             if nfull - mb > h:  # write-through of the blocks this forward computes
                 self._pending_store.append((keys[mb + h:nfull], fresh[h:nfull - mb]))
+        # cluster.py:333-337 / 384-389: the reference's matched / new split
+        self._emit(now_us, "PrefillComplete", req.session, req.rec.request_id, worker, f"matched={m} new={n - m}")
+        self._emit(now_us, "HandoffComplete", req.session, req.rec.request_id, worker, f"tokens={n} staged=0")
         if n > pos0:
             ri = 0 if self.base is not None else req.model_idx
             self._pending.append((ri, self._vocab_ids(req.ctx[pos0:]), pos0, pages))
@@ -228,6 +246,15 @@ class AgentServer:
                 self.tier.store(keys, pages)
             self._pending_store = []
 
+    def _emit(self, t_us: float, kind: str, session: int = -1, request: int = -1, worker: int = -1,
+              detail: str = "") -> None:
+        """One trace line in the reference's format (core.py:146-150):
+        `time seq kind session request worker detail`; time = host us since
+        the run started, at which the engine issued / observed the event."""
+        if self.trace is not None:
+            self.trace.append(trace_line(t_us, self._seq, kind, session, request, worker, detail))
+            self._seq += 1
+
     def _events(self, kind: str):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -246,9 +273,12 @@ class AgentServer:
     # -- serving -------------------------------------------------------------
 
     def run(self, sessions: list[wl.SessionSpec], max_concurrent: int | None = None,
-            time_scale: float = 1.0) -> list[RequestRecord]:
+            time_scale: float = 1.0, record_trace: bool = False) -> list[RequestRecord]:
         """Serve the workload in real time (arrival times scaled by
-        time_scale). Returns one record per request."""
+        time_scale). Returns one record per request. record_trace: keep the
+        event trace (self.trace, the reference's trace.txt lines)."""
+        self.trace = [] if record_trace else None
+        self._seq = 0
         self.runner.capture()
         self._ev = []
         self.token_completions: list[tuple[int, int]] = []
@@ -292,6 +322,7 @@ class AgentServer:
             t = now_us()
             while arrivals and arrivals[0].arrival_time * time_scale <= t:
                 s = arrivals.popleft()
+                self._emit(t, "SessionArrival", s.session_id)
                 if active < cap:
                     active += 1
                     activate(s)
@@ -309,6 +340,7 @@ class AgentServer:
                 if got is None:
                     # cluster.py:480-490: the request and its session fail
                     req.rec.failed = True
+                    self._emit(now_us(), "SessionComplete", req.session, detail=f"failed: {self._fail_reason}")
                     done_sessions += 1
                     active -= 1
                     if waiting_admission:
@@ -334,6 +366,12 @@ class AgentServer:
                 ev[1].record()
                 t_step = now_us()
                 self.token_completions.append((int(t_step), len(busy)))  # cluster.py:434
+                if self.trace is not None:  # one DecodeStep per decode worker (model) with rows in flight
+                    M = len(self.model_ids)
+                    for m in range(M):
+                        nb = sum(1 for r in busy if r.req.model_idx == m)
+                        if nb:
+                            self._emit(t_step, "DecodeStep", worker=M + m, detail=f"batch={nb}")
                 for idx, r in enumerate(self.rows):
                     if r.req is None:
                         continue
@@ -345,6 +383,8 @@ class AgentServer:
                         st.synchronize()
                         rec.done_us = now_us()
                         rec.out_tokens = r.steps
+                        self._emit(rec.done_us, "RequestComplete", r.req.session, rec.request_id,
+                                   len(self.model_ids) + r.req.model_idx)
                         for pool, h in r.held:
                             pool.release(h)
                         sid = r.req.session
@@ -354,6 +394,7 @@ class AgentServer:
                         self.rows[idx] = _Row()
                         self.batch.update_row(idx, 0, [self.tail_page[idx]], 0)
                         if step_idx[sid] >= spec.total_requests:
+                            self._emit(rec.done_us, "SessionComplete", sid)
                             done_sessions += 1
                             active -= 1
                             if waiting_admission:

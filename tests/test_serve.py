@@ -26,6 +26,38 @@ def test_summarize_nearest_rank_and_window():
     assert summarize([]) == {"completed": 0, "failed": 0}
 
 
+def test_trace_line_matches_reference_format():
+    """Lines produced by the reference's SimEvent.trace_line (core.py:146-150)
+    for the same events, trailing space of an empty detail included."""
+    from paper_2602_12029_b200.serve import trace_line
+    assert trace_line(0, 0, "SessionArrival", 3) == "0 0 SessionArrival 3 -1 -1 "
+    assert trace_line(1250.7, 7, "PrefillComplete", 3, 5, 0, "matched=32 new=100") == \
+        "1250 7 PrefillComplete 3 5 0 matched=32 new=100"
+    assert trace_line(99, 8, "DecodeStep", worker=4, detail="batch=2") == "99 8 DecodeStep -1 -1 4 batch=2"
+
+
+def check_trace(trace, sessions, n_req, n_models):
+    """Engine trace invariants: (time, seq) ordered, one arrival / completion
+    per session, the request lifecycle in order, decode workers M + model."""
+    from paper_2602_12029_b200.serve import TRACE_KINDS
+    rows = [ln.split(" ", 6) for ln in trace]
+    assert [int(r[1]) for r in rows] == list(range(len(rows)))
+    times = [int(r[0]) for r in rows]
+    assert times == sorted(times)
+    kinds = [r[2] for r in rows]
+    assert set(kinds) <= set(TRACE_KINDS)
+    assert kinds.count("SessionArrival") == len(sessions) == kinds.count("SessionComplete")
+    assert kinds.count("PrefillStart") == n_req == kinds.count("RequestComplete")
+    order = {}
+    for i, r in enumerate(rows):
+        if r[2] in ("PrefillStart", "PrefillComplete", "HandoffComplete", "RequestComplete"):
+            order.setdefault(int(r[4]), []).append(r[2])
+        if r[2] in ("DecodeStep", "RequestComplete"):
+            assert n_models <= int(r[5]) < 2 * n_models
+    assert all(v == ["PrefillStart", "PrefillComplete", "HandoffComplete", "RequestComplete"]
+               for v in order.values())
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("rows,batch", [(4, False), (4, True), (12, True)])
 def test_agent_workload_tiny_both_modes(rows, batch):
@@ -47,8 +79,9 @@ def test_agent_workload_tiny_both_modes(rows, batch):
     for mode in (ServingMode.BASELINE, ServingMode.PREFILLSHARE):
         srv = AgentServer(cfg, models, mode, rows_per_module=rows, pool_pages_per_worker=512,
                           max_context=4096, max_output=128, modules=mods, base=base, prefill_batch=batch)
-        recs = srv.run(sessions)
+        recs = srv.run(sessions, record_trace=True)
         assert len(recs) == n_req and all(r.done_us is not None for r in recs)
+        check_trace(srv.trace, sessions, n_req, len(models))
         assert all(r.out_tokens == 128 for r in recs)
         res[mode] = summarize(recs)
         gt = srv.gpu_time()

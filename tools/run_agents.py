@@ -3,7 +3,7 @@ GPU in both serving modes and print req/s, p95 E2E, prefill tokens and the
 prefix hit ratio; one JSON line per (rate, cap) point, so lists sweep the
 reference's arrival-rate (A4) and concurrency-cap (A3) axes on the real
 engine. --out DIR writes, per point and mode, the
-reference's output files: workload.json, report.json, requests.csv
+reference's output files: workload.json, report.json, requests.csv, trace.txt
 (schemas of metrics.py:17-91 / workload.py:159-195).
 
     python tools/run_agents.py [--shape 8b|tiny] [--rate 8[,4,...]] [--cap 0[,40,...]]
@@ -65,7 +65,8 @@ def main():
                 srv = AgentServer(cfg, models, mode, rows_per_module=a.rows, pool_pages_per_worker=a.pool_pages,
                                   max_context=max_ctx, max_output=256, modules=mods, base=base,
                                   prefill_batch=not a.no_batch, host_tier_blocks=a.host_tier_blocks)
-                recs = srv.run(sessions, max_concurrent=cap or None, time_scale=a.time_scale)
+                recs = srv.run(sessions, max_concurrent=cap or None, time_scale=a.time_scale,
+                               record_trace=point is not None)
                 out[mode.value] = summarize(recs)
                 out[mode.value]["gpu_time"] = srv.gpu_time()
                 if srv.tier is not None:
@@ -75,6 +76,7 @@ def main():
                             "rows_per_model": a.rows, "pool_blocks_per_worker": a.pool_pages}
                     (point / f"report_{mode.value}.json").write_text(report_to_json(build_report(srv, recs, echo)))
                     (point / f"requests_{mode.value}.csv").write_text(records_to_csv(recs))
+                    (point / f"trace_{mode.value}.txt").write_text("\n".join(srv.trace) + "\n")
                 del srv
                 torch.cuda.empty_cache()
             b, p = out.get("baseline", {}), out.get("prefillshare", {})
