@@ -376,9 +376,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: let the next kernel's CTAs start their prologue as SMs free up; the
+  // activations (A, the residual, KV pages) are read only after the wait
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
+      pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
       for (int item = blockIdx.x; item < sc.items; item += gridDim.x) {
@@ -436,6 +440,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp >= 4) {
+    pdl_wait();
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int r_in_tile = q * 32 + lane;
     int it = 0;
@@ -621,9 +626,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: let the next kernel's CTAs start their prologue as SMs free up; the
+  // activations (A, the residual, KV pages) are read only after the wait
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
+      pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
       for (int item = pair; item < sc.items; item += n_pairs) {
@@ -681,6 +690,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     __syncwarp();
   } else if (warp >= 4) {
+    pdl_wait();
     const int q = warp & 3;
     const int r_in_tile = q * 32 + lane;
     const uint32_t tempty_leader = peer_addr(tempty, 0);
@@ -806,7 +816,8 @@ static int launch_pair(const CUtensorMap& ma, const void* B, int M, int N, int K
     sc.S = S;
   }
   sc.items = sc.full + sc.rem * sc.S;
-  pair::gemm_pair_kernel<<<2 * pairs, THREADS, pair::SMEM_BYTES, s>>>(ma, mb, mbp, M, N, K, e, sc);
+  PSK_CUDA_TRY(launch_pdl(pair::gemm_pair_kernel, dim3(2 * pairs), dim3(THREADS), (size_t)pair::SMEM_BYTES, s,
+                          ma, mb, mbp, M, N, K, e, sc));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }
@@ -864,7 +875,8 @@ static int launch(const void* A, const void* B, int M, int N, int K, const Epi& 
     }
   }
   sc.items = sc.full + sc.rem * sc.S;
-  gemm_bf16_tn_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ma, mb, mbp, M, N, K, e, sc);
+  PSK_CUDA_TRY(launch_pdl(gemm_bf16_tn_kernel, dim3(grid), dim3(THREADS), (size_t)SMEM_BYTES, s, ma, mb, mbp, M, N,
+                          K, e, sc));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }

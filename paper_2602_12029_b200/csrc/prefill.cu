@@ -518,6 +518,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 1) umma::tmem_alloc(&s_tmem, 512);
   for (int j = threadIdx.x; j < n_pages && j < MAXPG; j += THREADS) s_pg[j] = pages[j];
   const uint32_t sq = smem_u32(smem + OFF_Q), sp = smem_u32(smem + OFF_P);
+  // PDL: the page table and items are host-written before the forward; q and
+  // the layer's K/V come from the QKV GEMM just before this kernel
+  psk::pdl_wait();
   // Q rows -> shared memory (K-major, 128B swizzle), row r = (position, head)
   for (int e = threadIdx.x; e < 256 * 16; e += THREADS) {
     const int r = e >> 4, c = e & 15;
@@ -536,6 +539,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = s_tmem;
+  psk::pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -769,8 +773,8 @@ int psk_prefill_attn(const void* q_rot, int32_t T, int32_t pos0, int32_t n_q_hea
                                           pp::SMEM));
         pp_attr = true;
       }
-      pp::prefill_attn_pp<<<t.n_qblocks * kv.n_kv_heads, pp::THREADS, pp::SMEM, psk::as_stream(stream)>>>(
-          map, t);
+      PSK_CUDA_TRY(psk::launch_pdl(pp::prefill_attn_pp, dim3(t.n_qblocks * kv.n_kv_heads), dim3(pp::THREADS),
+                                   (size_t)pp::SMEM, psk::as_stream(stream), map, t));
       PSK_LAUNCH_CHECK();
       return PSK_OK;
     }
@@ -826,7 +830,8 @@ int psk_prefill_attn_batch(const void* q_rot, int32_t n_items, const int32_t* it
     PSK_CUDA_TRY(cudaFuncSetAttribute(pp::prefill_attn_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, pp::SMEM));
     pp_attr = true;
   }
-  pp::prefill_attn_pp<<<n_items * kv.n_kv_heads, pp::THREADS, pp::SMEM, psk::as_stream(stream)>>>(map, t);
+  PSK_CUDA_TRY(psk::launch_pdl(pp::prefill_attn_pp, dim3(n_items * kv.n_kv_heads), dim3(pp::THREADS),
+                               (size_t)pp::SMEM, psk::as_stream(stream), map, t));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }
