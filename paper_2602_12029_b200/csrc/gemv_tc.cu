@@ -411,8 +411,16 @@ static int launch_uw(const void* x, int n_rows, int K, const void* const* W_host
     attr = true;
   }
   const int sms = sm_count();
-  const int64_t chunks = (int64_t)n_mod * (N / (UW * BN)) * ((K + BK - 1) / BK);
-  const int grid = chunks < sms ? (int)chunks : sms;
+  const int64_t units = (int64_t)n_mod * (N / (UW * BN));
+  const int64_t chunks = units * ((K + BK - 1) / BK);
+  int grid = chunks < sms ? (int)chunks : sms;
+  // <= one unit per SM: one CTA per whole unit, no stream-K split and no
+  // partial reduction (o-proj at 32 rows/module 26.6 -> 24.8 us, down 76.0 ->
+  // 73.2 us); above that the stream-K split balances the SMs (qkv's 192
+  // units as 96 CTAs x 2 measured 35.0 -> 37.8 us). PSK_GEMV_GRID=0: always
+  // stream-K.
+  static const bool whole_units = !(getenv("PSK_GEMV_GRID") && getenv("PSK_GEMV_GRID")[0] == '0');
+  if (whole_units && units <= sms) grid = (int)units;
   int* flags = reinterpret_cast<int*>(ws);
   float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + FLAG_BYTES);
   PSK_CUDA_TRY(psk::launch_pdl(k, dim3(grid), dim3(THREADS), (size_t)Cfg<MN, UW>::SMEM, s, maps, mrs, n_mod, N, K,
