@@ -1638,7 +1638,11 @@ static int64_t ws_slots(const psk_decode_batch* b, int32_t n_kv_heads, int32_t s
   const int sms = psk::device_sms();  // any budget <= the device count fits
   int64_t slots = (int64_t)sms + groups;
   if (splits > 0 && groups * splits > slots) slots = groups * splits;
-  const int64_t hsplit = b->n_sess > 0 ? (sms / b->n_sess > 1 ? sms / b->n_sess : 1) : 1;
+  // all-heads kernel: at most 8 waves of CTAs and 4 pages per split (launch)
+  const int64_t max_pages = (int64_t)b->max_sess_pages + (int64_t)b->max_rows_per_sess * b->max_row_pages;
+  int64_t hsplit = b->n_sess > 0 ? 8 * (int64_t)sms / b->n_sess : 1;
+  if (hsplit > max_pages / 4) hsplit = max_pages / 4;
+  if (hsplit < 1) hsplit = 1;
   if (groups * hsplit > slots) slots = groups * hsplit;
   return slots;
 }
@@ -1689,8 +1693,17 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   int hsplit = 1;
   if (use_heads) {
     const int64_t max_pages = (int64_t)b->max_sess_pages + (int64_t)b->max_rows_per_sess * b->max_row_pages;
+    // splits per session: one wave of (session, split) CTAs. Measured at 4k
+    // shared tokens x 4 modules (tools/hsplit_ab.py): 32 sessions 4 splits
+    // 114.5 us vs 5 / 6 / 7 / 8 / 9 splits 142.8 / 124.8 / 118.3 / 117.1 /
+    // 122.6 us (more, shorter CTAs lose to their per-CTA prologue and odd
+    // splits to DRAM locality); 64 sessions 2 splits 216.9 us, 4 splits 213.1.
+    // PSK_ATTN_HSPLIT=n overrides (bounded by the workspace's 8 waves).
+    static const int force = getenv("PSK_ATTN_HSPLIT") ? atoi(getenv("PSK_ATTN_HSPLIT")) : 0;
+    const int64_t hmax = max_pages / 4 > 1 ? max_pages / 4 : 1;
     hsplit = sms / b->n_sess > 1 ? sms / b->n_sess : 1;
-    if (hsplit > max_pages / 4) hsplit = max_pages / 4 > 1 ? (int)(max_pages / 4) : 1;
+    if (hsplit > hmax) hsplit = (int)hmax;
+    if (force > 0 && force <= hmax && b->n_sess * force <= 8 * (int64_t)sms) hsplit = force;
   }
   CUtensorMap map, vmap;
   int rc = psk::kv_tensor_map(kv, &map, use_tc ? psk::KV_BOX2D : (use_heads ? psk::KV_PAGE4D_ALL : psk::KV_PAGE4D));

@@ -142,3 +142,17 @@ def test_growing_scores_rescale(mods, splits):
     """Scores whose maxima grow along the page stream: the fan-out kernel's
     lazy O rescale (and the mma.sync online softmax) under real growth."""
     _case(32, 8, [3000], [mods], [(i * 13) % 100 for i in range(mods)], splits, seed=40 + mods, ramp=True)
+
+
+@pytest.mark.parametrize("hsplit", ["7", "13"])
+def test_all_heads_kernel_forced_splits(hsplit):
+    """The all-heads kernel with more (session, split) CTAs than one wave
+    (PSK_ATTN_HSPLIT, read once per process: runs the all-heads cases in a
+    child) still matches the reference."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PSK_ATTN_HSPLIT=hsplit)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", __file__, "-k", "test_all_heads_kernel and not forced",
+                        "-p", "no:cacheprovider"], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
