@@ -496,9 +496,11 @@ def main() -> None:
     barrier()
     with ClockSampler(local) as clk:
         ev[0].record(st)
+        phases = []
         for j in range(a.steps):
             eng.serve(batches[a.warmup + j], device_tokens=dev_batches[j])
             ev[j + 1].record(st)
+            phases.append(eng.last_phase_ms)
         ev[-1].synchronize()
     barrier()
     step_s = [ev[j].elapsed_time(ev[j + 1]) / 1e3 for j in range(a.steps)]
@@ -529,6 +531,8 @@ def main() -> None:
                    "d2h_bytes_per_step": S * N_MOD * MAX_NEW * 4,
                    "p95_latency_ms": round(sorted(e2e_steps)[-1] * 1e3, 2)},
            "gpu_launches": eng.launches_per_serve(S, S) * a.steps,
+           # device time per serve: prefill phase (pool ops + grouped prefills) / decode phase
+           "serve_phases_ms": {k: round(sum(p[k] for p in phases) / len(phases), 1) for k in ("prefill", "decode")},
            "clocks": clk.summary()}
     if not a.no_extras and rank == 0:
         out["roofline"] = gemv_roofline(eng, peaks)
@@ -537,8 +541,7 @@ def main() -> None:
         out["kv_copy"] = kv_copy_roofline(eng, peaks)
         step_bytes = eng.runner.weight_bytes_per_step
         out["decode_step"] = {"weight_bytes": step_bytes,
-                              "ms_per_token_step": round((t_val / a.steps - out["prefill"]["ms_per_prefill"]
-                                                          * S / 1e3) / MAX_NEW * 1e3, 3)}
+                              "ms_per_token_step": round(out["serve_phases_ms"]["decode"] / MAX_NEW, 3)}
         # throughput / latency at other batch sizes, same weights (the KV
         # pool of the main engine is freed first)
         mods, base = eng.mods, eng.base

@@ -56,7 +56,12 @@ class PrefillShareEngine:
         self.pool_pages = pool_pages
         extra = max_sessions * (1 + n_modules * self.priv_pages)
         self.kv = KVCache(cfg, pool_pages + extra, device)
+        # the pool's kernels and host syncs run on their own (high-priority)
+        # stream: a lookup for the next sessions does not wait for the
+        # prefills already queued, so the host stays ahead of the GPU
+        self.pool_stream = torch.cuda.Stream(device=device, priority=-1)
         self.pool = BlockPool(capacity_blocks=pool_pages, block_size=PAGE_TOKENS, device=device,
+                              stream=self.pool_stream.cuda_stream,
                               kv_pages=pool_pages, max_query_tokens=max(1 << 17, max_prompt))
         self.prefill = PrefillRunner(cfg, self.base, self.kv, max_tokens=max_prompt * self.prefill_group,
                                      device=device)
@@ -112,6 +117,8 @@ class PrefillShareEngine:
         if S > self.S:
             raise ValueError("more sessions than the engine was built for")
         self._now = self._now + 1 if now is None else now
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
         now = self._now
         lens = [len(p) for p in prompts]
         if max(lens) > self.max_prompt or min(lens) < 2:
@@ -150,10 +157,14 @@ class PrefillShareEngine:
         lens_full = [n - 1 for n in lens] + [0] * (self.S - S)
         firsts = [int(p[-1]) for p in prompts] + [0] * (self.S - S)
         self.batch.update_sessions(lens_full, tables, firsts)
+        ev[1].record()
         out = self.runner.run(self.max_new)
+        ev[2].record()
         self._out_host.copy_(out, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         for h in held:
             self.pool.release(h)
+        # device time of the two phases (prefill phase includes the pool ops' gaps)
+        self.last_phase_ms = {"prefill": ev[0].elapsed_time(ev[1]), "decode": ev[1].elapsed_time(ev[2])}
         res = self._out_host.numpy().reshape(self.S, self.M, self.max_new)[:S].copy()
         return ServeResult(tokens=res, matched=matched, prefill_tokens=pref)

@@ -61,3 +61,17 @@ for name, fns in kinds.items():
     for f, fn in saved.items():
         setattr(lib, f, fn)
     print(f"  without {name:14s} {t:9.1f} us  -> in-situ cost {full - t:8.1f} us/step")
+
+# each GEMV kind alone (the runner's dispatch no-op'ed for one (N, K) shape)
+d, f, v = cfg.d_model, cfg.ffn, cfg.vocab
+gemv_kinds = {"gemv qkv": (cfg.qkv_dim, d), "gemv o": (d, cfg.n_heads * cfg.head_dim), "gemv gate_up": (2 * f, d),
+              "gemv down": (d, f), "gemv head": (v, d)}
+orig = r._gemv
+for name, (N0, K0) in gemv_kinds.items():
+    def filt(x, K, p_dev, p_host, N, epi, out, s, N0=N0, K0=K0):
+        if (N, K) != (N0, K0):
+            orig(x, K, p_dev, p_host, N, epi, out, s)
+    r._gemv = filt
+    t = time_step()
+    r._gemv = orig
+    print(f"  without {name:14s} {t:9.1f} us  -> in-situ cost {full - t:8.1f} us/step", flush=True)
