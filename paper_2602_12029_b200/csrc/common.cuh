@@ -143,6 +143,19 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (the MUFU ex2 unit is the softmax limiter in K3):
+// x = n + f with n = rint(x) via the 1.5 * 2^23 magic add, 2^f on
+// [-0.5, 0.5] by a degree-3 minimax polynomial (max rel err 7.5e-5, far
+// below bf16 P's 2^-8), n added into the exponent bits. Inputs are clamped
+// at -125 (masked -inf scores give ~2^-125, negligible in sums of >= 1).
+__device__ __forceinline__ float exp2_fma(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05517167f, f, 0.24261115f), f, 0.69326097f), f, 0.99992806f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
 // bar.sync on a named barrier (id 1..15) among `threads` threads (multiple of 32)
 __device__ __forceinline__ void named_barrier_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");

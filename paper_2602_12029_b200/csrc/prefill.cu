@@ -449,6 +449,13 @@ __global__ void __launch_bounds__(THREADS_TC, 1)
 //               the row max grows by > 2^8; the final 1/l makes it exact),
 //               P (bf16) -> shared memory in the UMMA K-major layout
 // TMEM columns: S0 [0,64) S1 [64,128) O0 [128,256) O1 [256,384).
+#ifndef PP_EMU
+// K3 softmax: exponentials per 8 computed on the FMA pipe (exp2_fma). Off:
+// alternating A/B at 4k (tools/ab_prefill.sh) measured 188 us/layer with 0,
+// 202 with 3, 217 with 2, 238 with 4 -- MUFU is not this kernel's limiter.
+#define PP_EMU 0
+#endif
+
 namespace pp {
 
 constexpr int KC = 64;                   // keys per chunk
@@ -665,8 +672,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int q = 0; q < KC / 8; ++q) {
         float pf[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)  // p = 2^(s * scale - m); masked: 2^-inf = 0
-          pf[i] = fast_exp2(fmaf(__uint_as_float(sr[8 * q + i]), p.scale_log2, -base));
+        for (int i = 0; i < 8; ++i) {  // p = 2^(s * scale - m); masked: 2^-inf = 0
+          const float x = fmaf(__uint_as_float(sr[8 * q + i]), p.scale_log2, -base);
+          // PP_EMU of every 8 exponentials on the FMA pipe, the rest on MUFU
+          pf[i] = i >= 8 - PP_EMU ? exp2_fma(x) : fast_exp2(x);
+        }
         ls[q] = ((pf[0] + pf[1]) + (pf[2] + pf[3])) + ((pf[4] + pf[5]) + (pf[6] + pf[7]));
         const uint4 v = f32_to_bf16x8(pf);
         asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(prow + (((q ^ (g & 7))) << 4)), "r"(v.x),

@@ -60,6 +60,8 @@ def attn():
 da = bench._time_launches(attn, 16)
 afl = 4 * cfg.n_heads * cfg.head_dim * (T * (T + 1) / 2)  # QK^T + PV over the causal triangle
 print(f"prefill attention T={T}: {da * 1e6:.1f} us/layer  {afl / da / 1e12:.1f} TFLOP/s (causal flops)")
+if "attn" in sys.argv[2:]:
+    sys.exit(0)
 
 # in-situ ablation: prefill with one launch kind replaced by a no-op
 kinds = {"gemm": ["psk_gemm", "psk_gemm_qkv_rope_kv"], "attention": ["psk_prefill_attn"],
