@@ -468,7 +468,7 @@ class GpuPrefillBackend(PrefillBackend):
     def forward(self, seqs) -> None:
         V = self.cfg.vocab
         self.runner.run_batch([(torch.from_numpy((t % V).astype(np.int64)).to(self.dev), p0, pt)
-                               for t, p0, pt in seqs])
+                               for t, p0, pt in seqs], kv_only=True)
 
 
 class GpuDecodeBackend(DecodeBackend):

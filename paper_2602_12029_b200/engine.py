@@ -97,7 +97,7 @@ class PrefillShareEngine:
         while left > 0:
             g = min(left, self.prefill_group)
             attn = g if (g == 1 or new_tokens >= PER_SEQ_ATTN_MIN_TOKENS) else 1
-            pre += 1 + self.cfg.n_layers * (6 + attn)
+            pre += 1 + (self.cfg.n_layers - 1) * (6 + attn) + 2  # kv_only: the last layer stops after QKV
             left -= g
         return 5 * n_sessions + pre + self.max_new * self.runner.launches_per_step
 
@@ -143,13 +143,13 @@ class PrefillShareEngine:
             if n > m:
                 pending.append((toks[s, m:n], m, pages))
                 if len(pending) == self.prefill_group:
-                    self.prefill.run_batch(pending)
+                    self.prefill.run_batch(pending, kv_only=True)
                     pending = []
             matched.append(m)
             pref.append(n - m)
             tables.append(pages)
         if pending:
-            self.prefill.run_batch(pending)
+            self.prefill.run_batch(pending, kv_only=True)
         # decode modules read the base KV of positions [0, n-1) and process the
         # last prompt token themselves (model.ts:372-374, evaluate.ts:16-19)
         while len(tables) < self.S:  # idle session slots: point at a valid page

@@ -59,7 +59,7 @@ class SharingEvaluator:
         T = self.n - m
         if m > 0:
             PrefillRunner(cfg, base, self.kv, max_tokens=B * m).run_batch(
-                [(t[:m], 0, pt) for t, pt in zip(toks, tables)])
+                [(t[:m], 0, pt) for t, pt in zip(toks, tables)], kv_only=True)
         runner = PrefillRunner(cfg, dec, self.kv, max_tokens=B * T)
         runner.run_batch([(t[m:], m, pt) for t, pt in zip(toks, tables)])
         s = _stream()

@@ -514,9 +514,15 @@ class PrefillRunner:
         attn = 4.0 * c.n_layers * c.n_heads * c.head_dim * keys
         return gemm + attn
 
-    def run(self, tokens: torch.Tensor, pos0: int, page_table: torch.Tensor, stream: int | None = None) -> None:
+    def run(self, tokens: torch.Tensor, pos0: int, page_table: torch.Tensor, stream: int | None = None,
+            kv_only: bool = False) -> None:
         """tokens: int64 device [T] (the same ids the block pool hashes);
-        page_table: int32 device covering positions [0, pos0+T)."""
+        page_table: int32 device covering positions [0, pos0+T).
+        kv_only: stop after the last layer's QKV GEMM (its K/V written). A
+        prefill that only builds the shared cache (buildBaseCache,
+        model.ts:340; the decode modules process the last prompt token
+        themselves) never reads the last layer's attention / MLP output, so
+        the KV pages are identical and ~1/32 of the forward is skipped."""
         cfg, lib, w = self.cfg, self.lib, self.w
         T = int(tokens.shape[0])
         if T > self.max_tokens:
@@ -535,6 +541,8 @@ class PrefillRunner:
             chk(lib.psk_rmsnorm_rows(_ptr(self.h), T, d, _ptr(g1), None, eps, _ptr(self.xn), s))
             chk(lib.psk_gemm_qkv_rope_kv(_ptr(self.xn), _ptr(w.wqkv[l]), T, d, cfg.n_heads,
                                          _ptr(self.rope), pos0, kvl, l, pt, _ptr(self.q), s))
+            if kv_only and l == cfg.n_layers - 1:
+                break
             chk(lib.psk_prefill_attn(_ptr(self.q), T, pos0, cfg.n_heads, kvl, l, pt, _ptr(self.attn), s))
             chk(lib.psk_gemm(_ptr(self.attn), _ptr(w.wo[l]), T, d, cfg.n_heads * cfg.head_dim, 2,
                              _ptr(self.h), d, s))
@@ -543,7 +551,7 @@ class PrefillRunner:
                              cfg.ffn, s))
             chk(lib.psk_gemm(_ptr(self.act), _ptr(w.wdown[l]), T, d, cfg.ffn, 2, _ptr(self.h), d, s))
 
-    def run_batch(self, seqs, stream: int | None = None) -> None:
+    def run_batch(self, seqs, stream: int | None = None, kv_only: bool = False) -> None:
         """Batched partial prefill: the new tokens of several
         sequences in ONE forward, so the (weight-bound) small prefills of an
         agent workload share each layer's weight stream. seqs: list of
@@ -555,7 +563,7 @@ class PrefillRunner:
             toks, pos0, pt = seqs[0]
             if not torch.is_tensor(pt):
                 pt = torch.tensor(pt, dtype=torch.int32, device=self.h.device)
-            return self.run(toks, pos0, pt, stream)
+            return self.run(toks, pos0, pt, stream, kv_only)
         cfg, lib, w = self.cfg, self.lib, self.w
         Ts = [int(t.shape[0]) for t, _, _ in seqs]
         T = sum(Ts)
@@ -612,6 +620,8 @@ class PrefillRunner:
             chk(lib.psk_gemm_qkv_rope_kv_rows(_ptr(self.xn), _ptr(w.wqkv[l]), T, d, cfg.n_heads,
                                               _ptr(self.rope), _ptr(d_pos), _ptr(d_slot), kvl, l,
                                               _ptr(self.q), s))
+            if kv_only and l == cfg.n_layers - 1:
+                break
             if per_seq:  # long sequences: the single-sequence ping-pong K3 on each row range
                 for (o_, n_, p0_, pg_) in per_seq:
                     chk(lib.psk_prefill_attn(_ptr(self.q) + o_ * qrow, n_, p0_, cfg.n_heads, kvl, l,

@@ -235,7 +235,7 @@ class AgentServer:
             for sq in seqs + [None]:
                 if sq is None or (chunk and tot + int(sq[0].shape[0]) > runner.max_tokens):
                     ev = self._events("prefill")
-                    runner.run_batch(chunk)
+                    runner.run_batch(chunk, kv_only=True)  # decode processes the last token
                     ev[1].record()
                     chunk, tot = [], 0
                 if sq is not None:

@@ -152,3 +152,32 @@ def test_batched_partial_prefill_bit_identical(shape):
     assert torch.equal(kv_a, kv_b)
     for a, b in zip(h_a, h_b):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("batched", [False, True])
+def test_kv_only_prefill_writes_identical_kv(batched):
+    """kv_only stops after the last layer's QKV GEMM: the KV pages of every
+    layer are bit-identical to the full forward's."""
+    from paper_2602_12029_b200.model import KVCache, LlamaConfig, ModuleWeights, PrefillRunner
+    cfg = LlamaConfig.llama8b(n_layers=3, max_pos=2048)
+    base = ModuleWeights(cfg, 8, with_head=False)
+    rng = np.random.default_rng(3)
+    lens = [1100, 1030] if batched else [777]
+    seqs, off = [], 0
+    for n in lens:
+        pages = list(range(off, off + (n + 15) // 16))
+        off += len(pages)
+        seqs.append((torch.from_numpy(rng.integers(0, cfg.vocab, n)).cuda(), 0, pages))
+    outs = []
+    for kv_only in (False, True):
+        kv = KVCache(cfg, off + 1)
+        kv.data.zero_()
+        pre = PrefillRunner(cfg, base, kv, max_tokens=sum(lens))
+        if batched:
+            pre.run_batch(seqs, kv_only=kv_only)
+        else:
+            t, p0, pg = seqs[0]
+            pre.run(t, p0, torch.tensor(pg, dtype=torch.int32, device="cuda"), kv_only=kv_only)
+        torch.cuda.synchronize()
+        outs.append(kv.data.clone())
+    assert torch.equal(outs[0], outs[1]) and outs[0].abs().sum().item() > 0
