@@ -116,9 +116,12 @@ class AgentServer:
         self.kv = KVCache(cfg, total, device)
         # each logical prefill worker owns a disjoint page range of the one cache
         self.pools = []
+        # pool kernels + their host syncs on a side stream: a lookup does not
+        # wait for the prefill forwards and decode steps already queued
+        self.pool_stream = torch.cuda.Stream(device=device, priority=-1)
         for w in range(n_workers):
             p = BlockPool(per_pool, PAGE_TOKENS, device=device, kv_pages=per_pool,
-                          max_query_tokens=max(1 << 16, max_context))
+                          max_query_tokens=max(1 << 16, max_context), stream=self.pool_stream.cuda_stream)
             p.page_base = w * per_pool
             self.pools.append(p)
         producers = [self.base] if self.base is not None else self.mods
