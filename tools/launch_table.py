@@ -15,10 +15,13 @@ def table(path):
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.OrderedDict()
     for r in rows[hi + 1:]:
         if len(r) <= vi or not r[vi]:
             continue
+        if (mi is not None and r[mi] != "gpu__time_duration.sum") or r[ui] not in SCALE:
+            continue  # other metrics in the same list (grid size, DRAM bytes)
         us = float(r[vi].replace(",", "")) * SCALE[r[ui]]
         k = r[ki].split("(")[0].replace("void ", "")[:58]
         a = agg.setdefault(k, [0, 0.0])
