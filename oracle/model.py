@@ -42,6 +42,46 @@ def _rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor
     return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], dim=-1)
 
 
+def layer_forward(cfg, lw: dict, x: torch.Tensor, past, cos_t: torch.Tensor, sin_t: torch.Tensor):
+    """One decoder layer (model.ts:296-325, Llama-style): x [T, d] holds the
+    new positions [S, S+T); past = (K, V) [n_kv, S, hd] or None. Returns
+    (x after the layer, (K, V) covering [0, S+T)). Used whole-model by
+    LlamaOracle.forward and layer by layer (weights streamed per layer) by
+    the full-size parity tests."""
+    T = x.shape[0]
+    S = past[0].shape[1] if past is not None else 0
+    hd, H, Hk = cfg.head_dim, cfg.n_heads, cfg.n_kv_heads
+    cos, sin = cos_t[S:S + T], sin_t[S:S + T]
+    h = _rms(x, lw["attn_norm"], cfg.norm_eps)
+    q = (h @ lw["wq"].T).view(T, H, hd).transpose(0, 1)
+    k = (h @ lw["wk"].T).view(T, Hk, hd).transpose(0, 1)
+    v = (h @ lw["wv"].T).view(T, Hk, hd).transpose(0, 1)
+    q, k = _rope(q, cos, sin), _rope(k, cos, sin)
+    if past is not None:
+        k = torch.cat([past[0], k], dim=1)
+        v = torch.cat([past[1], v], dim=1)
+    # key j visible to new position i iff j <= S + i (model.ts:288-293)
+    mask = torch.arange(S + T)[None, :] <= (S + torch.arange(T))[:, None]
+    grp = H // Hk
+    o = torch.empty(H, T, hd)
+    for g in range(Hk):  # per KV head: no repeat_interleave copy of a long cache
+        qg = q[g * grp:(g + 1) * grp]
+        sc = (qg @ k[g].T) / math.sqrt(hd)
+        sc = sc.masked_fill(~mask, float("-inf"))
+        o[g * grp:(g + 1) * grp] = torch.softmax(sc, dim=-1) @ v[g]
+    x = x + o.transpose(0, 1).reshape(T, H * hd) @ lw["wo"].T
+    h2 = _rms(x, lw["mlp_norm"], cfg.norm_eps)
+    g_ = h2 @ lw["w_gate"].T
+    u = h2 @ lw["w_up"].T
+    x = x + (torch.nn.functional.silu(g_) * u) @ lw["w_down"].T
+    return x, (k, v)
+
+
+def final_logits(cfg, final_norm: torch.Tensor, head: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+    """Final RMSNorm -> LM head (model.ts:327-328)."""
+    return _rms(x, final_norm, cfg.norm_eps) @ head.T
+
+
 class LlamaOracle:
     """weights: dict from ModuleWeights.reference_layout() (fp32 CPU)."""
 
@@ -59,35 +99,14 @@ class LlamaOracle:
         S = past[0][0].shape[1] if past else 0
         if S + T > c.max_pos:
             raise ValueError(f"sequence length {S + T} exceeds max_pos {c.max_pos}")
-        hd, H, Hk = c.head_dim, c.n_heads, c.n_kv_heads
         x = w["embed"][torch.tensor(tokens, dtype=torch.long)]
-        cos, sin = self.cos[S:S + T], self.sin[S:S + T]
-        # key j visible to new position i iff j <= S + i (model.ts:288-293)
-        mask = torch.arange(S + T)[None, :] <= (S + torch.arange(T))[:, None]
         cache = []
         for l, lw in enumerate(w["layers"]):
-            h = _rms(x, lw["attn_norm"], c.norm_eps)
-            q = (h @ lw["wq"].T).view(T, H, hd).transpose(0, 1)
-            k = (h @ lw["wk"].T).view(T, Hk, hd).transpose(0, 1)
-            v = (h @ lw["wv"].T).view(T, Hk, hd).transpose(0, 1)
-            q, k = _rope(q, cos, sin), _rope(k, cos, sin)
-            if past:
-                k = torch.cat([past[l][0], k], dim=1)
-                v = torch.cat([past[l][1], v], dim=1)
-            cache.append((k, v))
-            kk = k.repeat_interleave(H // Hk, dim=0)
-            vv = v.repeat_interleave(H // Hk, dim=0)
-            sc = (q @ kk.transpose(1, 2)) / math.sqrt(hd)
-            sc = sc.masked_fill(~mask, float("-inf"))
-            o = torch.softmax(sc, dim=-1) @ vv
-            x = x + o.transpose(0, 1).reshape(T, H * hd) @ lw["wo"].T
-            h2 = _rms(x, lw["mlp_norm"], c.norm_eps)
-            g = h2 @ lw["w_gate"].T
-            u = h2 @ lw["w_up"].T
-            x = x + (torch.nn.functional.silu(g) * u) @ lw["w_down"].T
+            x, kv = layer_forward(c, lw, x, past[l] if past else None, self.cos, self.sin)
+            cache.append(kv)
         logits = None
         if with_logits:
-            logits = _rms(x, w["final_norm"], c.norm_eps) @ w["head"].T
+            logits = final_logits(c, w["final_norm"], w["head"], x)
         return logits, cache
 
     def prefill(self, tokens):

@@ -157,24 +157,28 @@ class ModuleWeights:
                      3 * c.ffn * c.d_model + 2 * c.d_model) * 2
         return c.n_layers * per_layer + (c.vocab * c.d_model * 2 if self.head is not None else 0)
 
-    def reference_layout(self) -> dict:
-        """fp32 CPU copies in the standard (un-fused) layout, for the oracle."""
+    def layer_reference(self, l: int) -> dict:
+        """fp32 CPU copy of layer l in the standard (un-fused) layout, for the
+        oracle (test infrastructure; full-size parity streams layers one at
+        a time so host memory stays near one layer)."""
         c = self.cfg
-        f = lambda t: t.float().cpu()  # noqa: E731
-        out = {"embed": f(self.embed), "final_norm": f(self.final_norm), "layers": []}
-        if self.head is not None:
-            out["head"] = f(self.head)
+        f = lambda t: t.cpu().float()  # noqa: E731
         qd, kd = c.n_heads * c.head_dim, c.n_kv_heads * c.head_dim
-        for l in range(c.n_layers):
-            qkv = f(self.wqkv[l])
-            gu = f(self.wgu[l]).view(-1, 2, 8, c.d_model)
-            out["layers"].append({
-                "attn_norm": f(self.attn_norm[l]), "wq": qkv[:qd], "wk": qkv[qd:qd + kd],
+        qkv = f(self.wqkv[l])
+        gu = f(self.wgu[l]).view(-1, 2, 8, c.d_model)
+        return {"attn_norm": f(self.attn_norm[l]), "wq": qkv[:qd], "wk": qkv[qd:qd + kd],
                 "wv": qkv[qd + kd:], "wo": f(self.wo[l]), "mlp_norm": f(self.mlp_norm[l]),
                 "w_gate": gu[:, 0].reshape(c.ffn, c.d_model),
                 "w_up": gu[:, 1].reshape(c.ffn, c.d_model),
-                "w_down": f(self.wdown[l]),
-            })
+                "w_down": f(self.wdown[l])}
+
+    def reference_layout(self) -> dict:
+        """fp32 CPU copies in the standard (un-fused) layout, for the oracle."""
+        f = lambda t: t.cpu().float()  # noqa: E731
+        out = {"embed": f(self.embed), "final_norm": f(self.final_norm),
+               "layers": [self.layer_reference(l) for l in range(self.cfg.n_layers)]}
+        if self.head is not None:
+            out["head"] = f(self.head)
         return out
 
 
@@ -322,6 +326,37 @@ class DecodeBatch:
         self.t_sess_pages.copy_(torch.tensor([p + [0] * (msp - len(p)) for p in pages], dtype=torch.int32))
         self._first = [first_tokens[r.session] for r in self.rows]
         self.reset()
+
+
+def batch_plan(cfg: LlamaConfig, seqs) -> tuple[np.ndarray, int]:
+    """Device plan of a batched partial prefill (run_batch / K3 batch form).
+    seqs: list of (new tokens T_i, pos0_i, page table covering [0, pos0_i+T_i)).
+    Returns (int32 array [items x 8 | row positions | row KV slots | pages],
+    number of work items). A work item is one (sequence, 256/grp-row q-block):
+    (row offset, T_i, pos0_i, page offset, q-block, 0, 0, 0), sorted heaviest
+    (longest key range) first."""
+    grp = cfg.n_heads // cfg.n_kv_heads
+    qb = 256 // grp
+    row_pos, row_slot, pages, items = [], [], [], []
+    off = 0
+    for n, pos0, pt in seqs:
+        if pos0 + n > cfg.max_pos:
+            raise ValueError(f"sequence length {pos0 + n} exceeds max_pos {cfg.max_pos}")
+        ptn = (pt.cpu().numpy() if torch.is_tensor(pt) else np.asarray(pt)).astype(np.int64)
+        pos = np.arange(pos0, pos0 + n, dtype=np.int64)
+        row_pos.append(pos)
+        row_slot.append(ptn[pos // PAGE_TOKENS] * PAGE_TOKENS + pos % PAGE_TOKENS)
+        for k in range((n + qb - 1) // qb):
+            kv_end = pos0 + min((k + 1) * qb, n)
+            items.append((kv_end, [off, n, pos0, len(pages), k, 0, 0, 0]))
+        pages.extend(ptn.tolist())
+        off += n
+    items.sort(key=lambda x: -x[0])  # heaviest (longest key range) first
+    # items first: the kernel reads them as int4 (16-byte aligned)
+    plan = np.concatenate([np.asarray([it for _, it in items], dtype=np.int64).reshape(-1),
+                           np.concatenate(row_pos), np.concatenate(row_slot),
+                           np.asarray(pages, dtype=np.int64)]).astype(np.int32)
+    return plan, len(items)
 
 
 PER_SEQ_ATTN_MIN_TOKENS = 1024  # batched prefill: per-sequence K3 when every sequence has this many new tokens
@@ -569,29 +604,9 @@ class PrefillRunner:
         T = sum(Ts)
         if T > self.max_tokens:
             raise ValueError(f"batched prefill of {T} tokens exceeds max_tokens {self.max_tokens}")
-        grp = cfg.n_heads // cfg.n_kv_heads
-        qb = 256 // grp
-        row_pos, row_slot, pages, items = [], [], [], []
-        off = 0
-        for (toks, pos0, pt), n in zip(seqs, Ts):
-            if pos0 + n > cfg.max_pos:
-                raise ValueError(f"sequence length {pos0 + n} exceeds max_pos {cfg.max_pos}")
-            ptn = (pt.cpu().numpy() if torch.is_tensor(pt) else np.asarray(pt)).astype(np.int64)
-            pos = np.arange(pos0, pos0 + n, dtype=np.int64)
-            row_pos.append(pos)
-            row_slot.append(ptn[pos // PAGE_TOKENS] * PAGE_TOKENS + pos % PAGE_TOKENS)
-            for k in range((n + qb - 1) // qb):
-                kv_end = pos0 + min((k + 1) * qb, n)
-                items.append((kv_end, [off, n, pos0, len(pages), k, 0, 0, 0]))
-            pages.extend(ptn.tolist())
-            off += n
-        items.sort(key=lambda x: -x[0])  # heaviest (longest key range) first
-        # items first: the kernel reads them as int4 (16-byte aligned)
-        plan = np.concatenate([np.asarray([it for _, it in items], dtype=np.int64).reshape(-1),
-                               np.concatenate(row_pos), np.concatenate(row_slot),
-                               np.asarray(pages, dtype=np.int64)]).astype(np.int32)
+        plan, n_items = batch_plan(cfg, [(n, pos0, pt) for (_, pos0, pt), n in zip(seqs, Ts)])
         dplan = torch.from_numpy(plan).to(self.h.device)
-        ni = 8 * len(items)
+        ni = 8 * n_items
         d_items = dplan[:ni]
         d_pos, d_slot = dplan[ni:ni + T], dplan[ni + T:ni + 2 * T]
         d_pages = dplan[ni + 2 * T:]
@@ -627,7 +642,7 @@ class PrefillRunner:
                     chk(lib.psk_prefill_attn(_ptr(self.q) + o_ * qrow, n_, p0_, cfg.n_heads, kvl, l,
                                              _ptr(d_pages) + 4 * pg_, _ptr(self.attn) + o_ * qrow, s))
             else:
-                chk(lib.psk_prefill_attn_batch(_ptr(self.q), len(items), _ptr(d_items), cfg.n_heads, kvl, l,
+                chk(lib.psk_prefill_attn_batch(_ptr(self.q), n_items, _ptr(d_items), cfg.n_heads, kvl, l,
                                                _ptr(d_pages), _ptr(self.attn), s))
             chk(lib.psk_gemm(_ptr(self.attn), _ptr(w.wo[l]), T, d, cfg.n_heads * cfg.head_dim, 2,
                              _ptr(self.h), d, s))

@@ -1,7 +1,7 @@
 """Drive each hot kernel a few times at the bench shapes, for ncu.
 
     ncu --set full -k regex:<kernel> -c 2 python tools/profile_kernels.py <which> [rows/module]
-which: gemv | gemv_tc | attn4k | attn4k_s8 | attn32k | gemm | prefill_attn | all
+which: gemv | gemv_tc | attn4k | attn4k_s8 | attn4k_s32 | attn32k | gemm | prefill_attn | all
 """
 import sys
 from pathlib import Path
@@ -53,6 +53,8 @@ if which in ("attn4k", "all"):
     attn(4095, 4)
 if which in ("attn4k_s8", "all"):
     attn(4095, 4, sessions=8)
+if which == "attn4k_s32":  # the bench batch: 32 sessions x 4 modules
+    attn(4095, 4, sessions=32)
 if which in ("attn32k", "all"):
     attn(32767, 16)
 if which == "gemv_tc":
