@@ -42,21 +42,35 @@ def _rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor
     return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], dim=-1)
 
 
-def layer_forward(cfg, lw: dict, x: torch.Tensor, past, cos_t: torch.Tensor, sin_t: torch.Tensor):
+def _bf(t: torch.Tensor) -> torch.Tensor:
+    return t.to(torch.bfloat16).float()
+
+
+def layer_forward(cfg, lw: dict, x: torch.Tensor, past, cos_t: torch.Tensor, sin_t: torch.Tensor,
+                  bf16_storage: bool = False):
     """One decoder layer (model.ts:296-325, Llama-style): x [T, d] holds the
     new positions [S, S+T); past = (K, V) [n_kv, S, hd] or None. Returns
     (x after the layer, (K, V) covering [0, S+T)). Used whole-model by
     LlamaOracle.forward and layer by layer (weights streamed per layer) by
-    the full-size parity tests."""
+    the full-size parity tests.
+
+    bf16_storage=True is the PRECISION MODEL of the same algorithm: every
+    tensor the kernels store in bf16 is rounded to bf16 at that point (norm
+    outputs, rotated q/k and v (the paged cache), softmax probabilities
+    before P.V, the attention output, the SwiGLU activation), everything else
+    fp32 with exact max-subtracted softmax. The full-size parity test runs it
+    beside the fp32 chain: the GPU must stay within a small factor of the
+    error that bf16 storage alone implies."""
+    r = _bf if bf16_storage else (lambda t: t)  # noqa: E731
     T = x.shape[0]
     S = past[0].shape[1] if past is not None else 0
     hd, H, Hk = cfg.head_dim, cfg.n_heads, cfg.n_kv_heads
     cos, sin = cos_t[S:S + T], sin_t[S:S + T]
-    h = _rms(x, lw["attn_norm"], cfg.norm_eps)
+    h = r(_rms(x, lw["attn_norm"], cfg.norm_eps))
     q = (h @ lw["wq"].T).view(T, H, hd).transpose(0, 1)
     k = (h @ lw["wk"].T).view(T, Hk, hd).transpose(0, 1)
-    v = (h @ lw["wv"].T).view(T, Hk, hd).transpose(0, 1)
-    q, k = _rope(q, cos, sin), _rope(k, cos, sin)
+    v = r((h @ lw["wv"].T).view(T, Hk, hd).transpose(0, 1))
+    q, k = r(_rope(q, cos, sin)), r(_rope(k, cos, sin))
     if past is not None:
         k = torch.cat([past[0], k], dim=1)
         v = torch.cat([past[1], v], dim=1)
@@ -68,18 +82,24 @@ def layer_forward(cfg, lw: dict, x: torch.Tensor, past, cos_t: torch.Tensor, sin
         qg = q[g * grp:(g + 1) * grp]
         sc = (qg @ k[g].T) / math.sqrt(hd)
         sc = sc.masked_fill(~mask, float("-inf"))
-        o[g * grp:(g + 1) * grp] = torch.softmax(sc, dim=-1) @ v[g]
-    x = x + o.transpose(0, 1).reshape(T, H * hd) @ lw["wo"].T
-    h2 = _rms(x, lw["mlp_norm"], cfg.norm_eps)
+        if bf16_storage:
+            e = torch.exp(sc - sc.max(dim=-1, keepdim=True).values)
+            o[g * grp:(g + 1) * grp] = (r(e) @ v[g]) / e.sum(dim=-1, keepdim=True)
+        else:
+            o[g * grp:(g + 1) * grp] = torch.softmax(sc, dim=-1) @ v[g]
+    x = x + r(o.transpose(0, 1).reshape(T, H * hd)) @ lw["wo"].T
+    h2 = r(_rms(x, lw["mlp_norm"], cfg.norm_eps))
     g_ = h2 @ lw["w_gate"].T
     u = h2 @ lw["w_up"].T
-    x = x + (torch.nn.functional.silu(g_) * u) @ lw["w_down"].T
+    x = x + r(torch.nn.functional.silu(g_) * u) @ lw["w_down"].T
     return x, (k, v)
 
 
-def final_logits(cfg, final_norm: torch.Tensor, head: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+def final_logits(cfg, final_norm: torch.Tensor, head: torch.Tensor, x: torch.Tensor,
+                 bf16_storage: bool = False) -> torch.Tensor:
     """Final RMSNorm -> LM head (model.ts:327-328)."""
-    return _rms(x, final_norm, cfg.norm_eps) @ head.T
+    h = _rms(x, final_norm, cfg.norm_eps)
+    return (_bf(h) if bf16_storage else h) @ head.T
 
 
 class LlamaOracle:

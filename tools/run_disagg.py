@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--pool-pages", type=int, default=7500, help="per prefill worker")
     ap.add_argument("--steps-per-round", type=int, default=8)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--max-context", type=int, default=None)
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -53,7 +54,10 @@ def main():
     mode = ServingMode(a.mode)
     models = list(wl.DEFAULT_MODELS)
     M = len(models)
-    cfg = LlamaConfig.llama8b(max_pos=4096 + 512) if a.shape == "8b" else LlamaConfig.tiny(max_pos=4096)
+    # longest context: react 4096, reflexion 512 + 12 x (96 + 256) = 4736 (as run_agents.py)
+    max_ctx = a.max_context or (5120 if a.pattern == "reflexion" else 4096)
+    cfg = (LlamaConfig.llama8b(max_pos=max_ctx + 512) if a.shape == "8b"
+           else LlamaConfig.tiny(max_pos=max_ctx + 512))
     n_prefill = M if mode is ServingMode.BASELINE else (a.prefill_gpus or max(1, world // 4))
     if world == 1:
         place = Placement.colocated(M, n_prefill)
@@ -64,10 +68,10 @@ def main():
     mine_d = [m for m, r in enumerate(place.decode_gpus) if r == rank]
     base = ModuleWeights(cfg, 99, with_head=False, device=local) if (mine_p and mode is ServingMode.PREFILLSHARE) else None
     mods = {m: ModuleWeights(cfg, 100 + m, device=local) for m in set(mine_d) | (set(mine_p) if mode is ServingMode.BASELINE else set())}
-    prefill = {w: GpuPrefillBackend(cfg, base if base is not None else mods[w], a.pool_pages, 4096, 256, local)
+    prefill = {w: GpuPrefillBackend(cfg, base if base is not None else mods[w], a.pool_pages, max_ctx, 256, local)
                for w in mine_p}
-    decode = (GpuDecodeBackend(cfg, {m: mods[m] for m in mine_d}, a.rows, ctx_pages=len(mine_d) * a.rows * 260,
-                               max_context=4096, max_output=256, device=local) if mine_d else None)
+    decode = (GpuDecodeBackend(cfg, {m: mods[m] for m in mine_d}, a.rows, ctx_pages=len(mine_d) * a.rows * (max_ctx // 16 + 4),
+                               max_context=max_ctx, max_output=256, device=local) if mine_d else None)
     srv = DisaggServer(place, models, mode, prefill, decode, a.rows, ctrl_group=ctrl, data_group=data)
     coord = None
     if rank == 0:
