@@ -20,7 +20,8 @@ point, 8 and 64) are reported under "sessions_sweep".
           at the config-2 and config-4 (32k x 16 modules) shapes and the
           prefill (tcgen05) TFLOP/s.
   cpu_baseline : the fp32 CPU oracle on a bounded sample of the same
-          workload (1 of 32 layers, 3 decode steps), scaled to req/s.
+          workload, batched like the GPU arm (2 of 32 layers of a prefill and
+          of one module's 32-row decode step, one LM head), scaled to req/s.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Under torchrun each rank serves its own batch (weak scaling, no data-path
@@ -106,53 +107,85 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU oracle ---
 
-def cpu_reference_sample(n_sessions: int = 1) -> dict:
-    """Time the fp32 CPU oracle (oracle/model.py, the reference path restated)
-    on a bounded sample of the same workload and scale it to req/s:
-    1 full-width layer of the 4096-token prefill + 3 single-token decode
-    steps of 1 layer with the 4095-token shared KV (per module) + a 16384-row
-    slice of the LM head; the per-request time is
-    32*prefill_layer/4 + 256*(32*decode_layer + head)."""
-    import torch
-    from oracle.model import LlamaOracle
-    from paper_2602_12029_b200.model import LlamaConfig
+class CpuReference:
+    """The fp32 CPU oracle (oracle/model.py, the reference path restated) on
+    a bounded sample of the same workload, run the way a batched CPU server
+    would run it, scaled to req/s. One sample():
+      * prefill: 2 full-width layers of one 4096-token prompt (t_pre2);
+      * decode: 2 full-width layers of ONE module's co-batched step over its
+        n_sessions rows (weights read once per step for all rows; each row
+        attends over its own session's 4095-token shared KV plus its own
+        token: oracle.decode_layer_batched) (t_dec2), and the module's LM
+        head over those rows (t_head, full 128256 vocab);
+      * per serve: n_sessions x 16 x t_pre2 + 256 x 4 modules x
+        (16 x t_dec2 + t_head).
+    The extrapolation factors (x16 layers, x4 modules of identical shape,
+    x256 steps) are stated in the sample text. Weights and caches are built
+    once (__init__), outside the timed samples."""
 
-    torch.manual_seed(0)
-    full = LlamaConfig.llama8b()
-    cfg = LlamaConfig(n_layers=1, d_model=full.d_model, n_heads=full.n_heads,
-                      n_kv_heads=full.n_kv_heads, ffn=full.ffn, vocab=4096,
-                      rope_theta=full.rope_theta, max_pos=PROMPT + MAX_NEW)
-    d, f, hd = cfg.d_model, cfg.ffn, cfg.head_dim
-    r = lambda *s: torch.randn(*s) * 0.02  # noqa: E731
-    lw = {"attn_norm": torch.ones(d), "wq": r(cfg.n_heads * hd, d), "wk": r(cfg.n_kv_heads * hd, d),
-          "wv": r(cfg.n_kv_heads * hd, d), "wo": r(d, cfg.n_heads * hd), "mlp_norm": torch.ones(d),
-          "w_gate": r(f, d), "w_up": r(f, d), "w_down": r(d, f)}
-    w = {"embed": r(4096, d), "final_norm": torch.ones(d), "head": r(4096, d), "layers": [lw]}
-    o = LlamaOracle(cfg, w)
-    prompt = torch.randint(0, 4096, (PROMPT,)).tolist()
-    with torch.no_grad():
-        t0 = time.perf_counter()
-        kv = o.forward(prompt[:-1], None, with_logits=False)[1]
-        t_pre = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        cache = kv
-        for i in range(3):
-            _, cache = o.forward([prompt[-1] if i == 0 else 7], cache, with_logits=False)
-        t_dec = (time.perf_counter() - t0) / 3
-        head = r(16384, d)
-        x = torch.randn(1, d)
-        t0 = time.perf_counter()
-        for _ in range(3):
-            _ = x @ head.T
-        t_head = (time.perf_counter() - t0) / 3 * (full.vocab / 16384)
-    per_session = full.n_layers * t_pre + MAX_NEW * N_MOD * (full.n_layers * t_dec + t_head)
-    reqs = n_sessions * N_MOD
-    value = reqs / (n_sessions * per_session)
-    return {"value": value, "unit": "req/s", "cores": torch.get_num_threads(), "kind": "port",
-            "sample": (f"fp32 CPU oracle: 1 of 32 layers at full 8B width (4096-token prefill "
-                       f"{t_pre:.2f}s, decode layer-step {t_dec * 1e3:.1f}ms x {N_MOD} modules, LM head "
-                       f"{t_head * 1e3:.1f}ms/step), scaled to 32 layers x 256 tokens"),
-            "sample_seconds": t_pre + 3 * t_dec + 3 * t_head / (full.vocab / 16384)}
+    L = 2
+
+    def __init__(self, n_sessions: int = 32):
+        import torch
+        from oracle.model import layer_forward, rope_cos_sin
+        from paper_2602_12029_b200.model import LlamaConfig
+        torch.manual_seed(0)
+        self.full = full = LlamaConfig.llama8b()
+        self.cfg = cfg = LlamaConfig(n_layers=self.L, d_model=full.d_model, n_heads=full.n_heads,
+                                     n_kv_heads=full.n_kv_heads, ffn=full.ffn, vocab=full.vocab,
+                                     rope_theta=full.rope_theta, max_pos=PROMPT + MAX_NEW)
+        d, f, hd = cfg.d_model, cfg.ffn, cfg.head_dim
+        r = lambda *s: torch.randn(*s) * 0.02  # noqa: E731
+
+        def layer():
+            return {"attn_norm": 1 + 0.1 * torch.randn(d), "wq": r(cfg.n_heads * hd, d),
+                    "wk": r(cfg.n_kv_heads * hd, d), "wv": r(cfg.n_kv_heads * hd, d),
+                    "wo": r(d, cfg.n_heads * hd), "mlp_norm": 1 + 0.1 * torch.randn(d),
+                    "w_gate": r(f, d), "w_up": r(f, d), "w_down": r(d, f)}
+        self.base_l = [layer() for _ in range(self.L)]
+        self.mod_l = [layer() for _ in range(self.L)]
+        self.head = r(full.vocab, d)
+        self.cos, self.sin = rope_cos_sin(cfg.max_pos, hd, cfg.rope_theta)
+        self.R = n_sessions
+        self.x_pre = r(PROMPT - 1, d) * 50
+        self.x_dec = r(n_sessions, d) * 50
+        with torch.inference_mode():
+            x, kvs = self.x_pre, []
+            for lw in self.base_l:
+                x, kv = layer_forward(cfg, lw, x, None, self.cos, self.sin)
+                kvs.append(kv)
+        # every row of the batch attends over its own session's shared KV in
+        # its own memory (R x 2 layers x 33.5 MB; one prompt's values
+        # replicated: the arithmetic and the bytes read are a real batch's)
+        self.pasts = [(k.unsqueeze(0).repeat(n_sessions, 1, 1, 1), v.unsqueeze(0).repeat(n_sessions, 1, 1, 1))
+                      for k, v in kvs]
+
+    def sample(self) -> dict:
+        import torch
+        from oracle.model import decode_layer_batched, layer_forward
+        cfg = self.cfg
+        with torch.inference_mode():
+            t0 = time.perf_counter()
+            x = self.x_pre
+            for lw in self.base_l:
+                x, _ = layer_forward(cfg, lw, x, None, self.cos, self.sin)
+            t_pre2 = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            xs = self.x_dec
+            for lw, (kp, vp) in zip(self.mod_l, self.pasts):
+                xs, _ = decode_layer_batched(cfg, lw, xs, kp, vp, self.cos, self.sin)
+            t_dec2 = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            _ = xs @ self.head.T
+            t_head = time.perf_counter() - t0
+        S, lf = self.R, self.full.n_layers // self.L
+        per_serve = S * lf * t_pre2 + MAX_NEW * N_MOD * (lf * t_dec2 + t_head)
+        return {"value": S * N_MOD / per_serve, "unit": "req/s", "cores": torch.get_num_threads(), "kind": "port",
+                "sample": (f"fp32 CPU oracle, batched like the GPU arm: 2 of 32 full-width layers of a 4096-token "
+                           f"prefill ({t_pre2:.2f} s), 2 layers of one module's decode step over {S} co-batched "
+                           f"rows ({t_dec2 * 1e3:.1f} ms), one module's LM head over {S} rows "
+                           f"({t_head * 1e3:.1f} ms); scaled x{lf} layers, x{N_MOD} modules of the same shape, "
+                           f"x{MAX_NEW} steps, x{S} prefills per serve of {S} sessions")}
 
 
 # --------------------------------------------------------- kernel timing ---
@@ -399,6 +432,42 @@ def serve_point(cfg, mods, base, S: int, batches, device: int, steps: int = 2) -
             "p95_latency_ms": round(max(ts) * 1e3, 2)}
 
 
+def agents_point(cfg, mods, base, rate: float = 8.0, duration: float = 20.0, rows: int = 64,
+                 pool_pages: int = 7500) -> dict:
+    """BASELINE configs 3 / 5 on one GPU: the reference's agent workload
+    (workload.generate, ReAct, Poisson arrivals at `rate` sessions/s for
+    `duration` s, seed 0) served in real time by serve.AgentServer in both
+    modes on the same weights: per-request p95 E2E / TTFT under arrivals
+    (metrics.py definitions, GPU-completion timestamps) next to the batch
+    number. BASELINE: one prefill worker + pool per model; PREFILLSHARE: the
+    frozen base module prefills for every model, sessions pinned to the
+    least-queued of the per-worker pools (router.py:58-77), 7500 blocks per
+    worker (config.py:39), 64 decode rows per model (max_batch)."""
+    import torch
+    from paper_2602_12029_b200 import workload as wl
+    from paper_2602_12029_b200.router import ServingMode
+    from paper_2602_12029_b200.serve import AgentServer, summarize
+    models = list(wl.DEFAULT_MODELS)
+    sessions = wl.generate(wl.WorkloadConfig(pattern="react", arrival_rate_per_s=rate, duration_s=duration,
+                                             seed=0))
+    out = {"workload": f"configs[2]/[4] on 1 GPU: react, {rate:g} sessions/s for {duration:g} s, "
+                       f"{len(sessions)} sessions, {sum(s.total_requests for s in sessions)} requests",
+           "rows_per_model": rows, "pool_blocks_per_worker": pool_pages}
+    for mode in (ServingMode.BASELINE, ServingMode.PREFILLSHARE):
+        srv = AgentServer(cfg, models, mode, rows_per_module=rows, pool_pages_per_worker=pool_pages,
+                          max_context=4096, max_output=256, modules=mods, base=base)
+        recs = srv.run(sessions)
+        sm = summarize(recs)
+        out[mode.value] = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in sm.items()}
+        del srv
+        torch.cuda.empty_cache()
+    b, p = out["baseline"], out["prefillshare"]
+    if b.get("req_per_s") and p.get("req_per_s"):
+        out["req_per_s_ratio"] = round(p["req_per_s"] / b["req_per_s"], 3)
+        out["p95_e2e_ratio"] = round(b["p95_e2e_ms"] / p["p95_e2e_ms"], 3)
+    return out
+
+
 def prefill_roofline(eng, peaks) -> dict:
     import torch
     T = PROMPT
@@ -436,11 +505,11 @@ def main() -> None:
     if a.impl == "reference":
         if rank != 0:
             return
-        samples = [cpu_reference_sample(a.sessions) for _ in range(a.warmup + a.steps)][a.warmup:]
+        ref = CpuReference(a.sessions)
+        samples = [ref.sample() for _ in range(a.warmup + a.steps)][a.warmup:]
         v = statistics.median(s["value"] for s in samples)
         cb = dict(samples[-1])
         cb["value"] = v
-        cb.pop("sample_seconds", None)
         print(json.dumps({"metric": METRIC, "value": v, "unit": "req/s", "impl": "reference",
                           "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
                           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -549,13 +618,16 @@ def main() -> None:
         torch.cuda.empty_cache()
         out["sessions_sweep"] = [serve_point(cfg, mods, base, n, batches, local)
                                  for n in (1, 8, 64) if n != S]
+        out["agents"] = agents_point(cfg, mods, base)
         del mods, base
         torch.cuda.empty_cache()
         out["decode_attn_fanout_32k_x16"] = decode_attn_fanout(peaks)
         out["pool"] = pool_ops()
         if world == 1:
-            out["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(S).items()
-                                   if k != "sample_seconds"}
+            ref = CpuReference(S)
+            ref.sample()  # warm-up
+            out["cpu_baseline"] = ref.sample()
+            del ref
     if rank == 0:
         print(json.dumps(out))
     if world > 1:

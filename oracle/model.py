@@ -95,6 +95,33 @@ def layer_forward(cfg, lw: dict, x: torch.Tensor, past, cos_t: torch.Tensor, sin
     return x, (k, v)
 
 
+def decode_layer_batched(cfg, lw: dict, x: torch.Tensor, k_past: torch.Tensor, v_past: torch.Tensor,
+                         cos_t: torch.Tensor, sin_t: torch.Tensor):
+    """One decoder layer for R decode rows at once (one new token each, all
+    at position S = k_past.shape[2]), each row over its own past K/V
+    [R, n_kv, S, hd]: the batched form of layer_forward(T=1) that a CPU
+    serving loop would run (every module's weights read once per step for
+    all of its rows). Returns (x [R, d], (k, v) [R, n_kv, 1, hd] of the new
+    token)."""
+    R = x.shape[0]
+    S = k_past.shape[2]
+    hd, H, Hk = cfg.head_dim, cfg.n_heads, cfg.n_kv_heads
+    cos, sin = cos_t[S:S + 1], sin_t[S:S + 1]
+    h = _rms(x, lw["attn_norm"], cfg.norm_eps)
+    q = _rope((h @ lw["wq"].T).view(R, H, 1, hd), cos, sin)
+    k = _rope((h @ lw["wk"].T).view(R, Hk, 1, hd), cos, sin)
+    v = (h @ lw["wv"].T).view(R, Hk, 1, hd)
+    grp = H // Hk
+    qg = q.view(R, Hk, grp, hd)
+    sc = torch.cat([qg @ k_past.transpose(2, 3), qg @ k.transpose(2, 3)], dim=3) / math.sqrt(hd)
+    pr = torch.softmax(sc, dim=-1)
+    o = pr[..., :S] @ v_past + pr[..., S:] @ v  # [R, Hk, grp, hd]
+    x = x + o.reshape(R, H * hd) @ lw["wo"].T
+    h2 = _rms(x, lw["mlp_norm"], cfg.norm_eps)
+    x = x + (torch.nn.functional.silu(h2 @ lw["w_gate"].T) * (h2 @ lw["w_up"].T)) @ lw["w_down"].T
+    return x, (k, v)
+
+
 def final_logits(cfg, final_norm: torch.Tensor, head: torch.Tensor, x: torch.Tensor,
                  bf16_storage: bool = False) -> torch.Tensor:
     """Final RMSNorm -> LM head (model.ts:327-328)."""

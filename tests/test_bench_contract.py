@@ -9,11 +9,14 @@ def test_reference_arm_json_line(monkeypatch, capsys):
     import bench
     calls = []
 
-    def fake_sample(n_sessions=1):
-        calls.append(n_sessions)
-        return {"value": 0.01, "unit": "req/s", "cores": 4, "kind": "port", "sample": "stub",
-                "sample_seconds": 0.0}
-    monkeypatch.setattr(bench, "cpu_reference_sample", fake_sample)
+    class FakeRef:
+        def __init__(self, n_sessions=32):
+            self.n = n_sessions
+
+        def sample(self):
+            calls.append(self.n)
+            return {"value": 0.01, "unit": "req/s", "cores": 4, "kind": "port", "sample": "stub"}
+    monkeypatch.setattr(bench, "CpuReference", FakeRef)
     monkeypatch.setattr(sys, "argv", ["bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1"])
     monkeypatch.delenv("RANK", raising=False)
     bench.main()
@@ -31,7 +34,7 @@ def test_reference_arm_json_line(monkeypatch, capsys):
 
 def test_reference_arm_other_ranks_exit_quietly(monkeypatch, capsys):
     import bench
-    monkeypatch.setattr(bench, "cpu_reference_sample", lambda n=1: (_ for _ in ()).throw(AssertionError))
+    monkeypatch.setattr(bench, "CpuReference", lambda n=1: (_ for _ in ()).throw(AssertionError))
     monkeypatch.setattr(sys, "argv", ["bench.py", "--impl", "reference"])
     monkeypatch.setenv("RANK", "1")
     bench.main()

@@ -93,3 +93,27 @@ def test_incremental_equals_full_recompute():
             full.append(int(torch.argmax(lg[-1])))
             seq.append(full[-1])
         assert inc == full
+
+
+def test_batched_decode_layer_matches_per_row_layer():
+    """oracle.decode_layer_batched (the CPU arm's batched decode step) equals
+    layer_forward(T=1) row by row."""
+    import torch
+    from oracle.model import decode_layer_batched, layer_forward, rope_cos_sin
+    from paper_2602_12029_b200.model import LlamaConfig
+    cfg = LlamaConfig(n_layers=1, d_model=256, n_heads=4, n_kv_heads=2, ffn=512, vocab=64, rope_theta=1e4,
+                      max_pos=256)
+    g = torch.Generator().manual_seed(0)
+    r = lambda *s: torch.randn(*s, generator=g) * 0.05  # noqa: E731
+    d, hd = cfg.d_model, cfg.head_dim
+    lw = {"attn_norm": 1 + r(d), "wq": r(4 * hd, d), "wk": r(2 * hd, d), "wv": r(2 * hd, d), "wo": r(d, 4 * hd),
+          "mlp_norm": 1 + r(d), "w_gate": r(512, d), "w_up": r(512, d), "w_down": r(d, 512)}
+    cos, sin = rope_cos_sin(cfg.max_pos, hd, cfg.rope_theta)
+    R, S = 3, 37
+    x = r(R, d) * 20
+    kp, vp = r(R, 2, S, hd) * 20, r(R, 2, S, hd) * 20
+    xb, (kb, vb) = decode_layer_batched(cfg, lw, x, kp, vp, cos, sin)
+    for i in range(R):
+        xi, (ki, vi) = layer_forward(cfg, lw, x[i:i + 1], (kp[i], vp[i]), cos, sin)
+        assert torch.allclose(xb[i], xi[0], atol=1e-5, rtol=1e-4)
+        assert torch.allclose(kb[i, :, 0], ki[:, S], atol=1e-5) and torch.allclose(vb[i, :, 0], vi[:, S], atol=1e-5)

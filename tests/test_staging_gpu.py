@@ -51,9 +51,10 @@ def test_agent_server_reloads_evicted_prefix_blocks():
     base = ModuleWeights(cfg, 9, with_head=False)
     res = {}
     for tier in (0, 4096):
-        # a small shared pool (4 x 130 blocks, active sessions compete): later agents' prefixes get evicted
+        # a small merged shared pool (4 x 130 blocks, active sessions compete): later agents' prefixes get evicted
         srv = AgentServer(cfg, models, ServingMode.PREFILLSHARE, rows_per_module=1, pool_pages_per_worker=130,
-                          max_context=2048, max_output=128, modules=mods, base=base, host_tier_blocks=tier)
+                          max_context=2048, max_output=128, modules=mods, base=base, host_tier_blocks=tier,
+                          merged_pool=True)
         recs = srv.run(sessions, time_scale=0.2)
         assert all(r.done_us is not None and not r.failed for r in recs) and len(recs) == n_req
         res[tier] = (summarize(recs), srv.tier.stats() if srv.tier else None, srv.pools[0].eviction_count)
