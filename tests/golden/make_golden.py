@@ -209,6 +209,132 @@ def pool_fixtures(wl, BlockPool, CapacityExhausted):
     return streams
 
 
+def _compress_tokens(toks) -> dict:
+    """Packed synthetic ids (workload.py:142-154) as [sid, purpose, n] runs
+    when the context is made of whole segments from index 0, else raw."""
+    segs, i, n = [], 0, len(toks)
+    while i < n:
+        t = toks[i]
+        sid, purpose, idx = (t >> 32) - 1, (t >> 16) & 0xFFFF, t & 0xFFFF
+        if idx != 0 or sid < 0:
+            return {"tokens": list(toks)}
+        j = i
+        while j < n and toks[j] == (((sid + 1) << 32) | (purpose << 16) | (j - i)):
+            j += 1
+        segs.append([sid, purpose, j - i])
+        i = j
+    return {"segs": segs}
+
+
+def des_call_logs(runs=((7500, "baseline"), (7500, "prefillshare"), (1500, "baseline"),
+                        (1500, "prefillshare"), (100, "prefillshare"))):
+    """The REAL call pattern at the drop-in seam (cluster.py:30):
+    run prefillsim.cluster.Simulation on configs/fast_react.toml (60 s ReAct
+    workload, the reference fleet) in both modes, with prefillsim.cluster's
+    BlockPool replaced by a recording subclass. Every pool op of every
+    prefill worker is logged in the pool-stream format (pin / release
+    reference the lookup / insert results they were given: release gets the
+    matched chain extended in place by the allocation, cluster.py:330, 347,
+    409), with the reference's outcome, counters and a state digest every
+    25 ops. Runs with 1500- and 100-block pools add eviction pressure and
+    capacity failures (contexts longer than the pool: CapacityExhausted,
+    caught by class, cluster.py:348). The recorded run's report is checked to be identical to an
+    unrecorded run's (the subclass does not perturb the simulation)."""
+    import dataclasses
+
+    from prefillsim import cluster, config as pconfig, experiment, kvstore
+    base_cfg = pconfig.load_config("/root/reference/pkg/configs/fast_react.toml")
+    logs = []
+    for cap, mode in runs:
+        if True:
+            cfg = dataclasses.replace(base_cfg, run=dataclasses.replace(base_cfg.run, mode=mode),
+                                      cache=dataclasses.replace(base_cfg.cache, prefill_capacity_blocks=cap))
+            _, plain = experiment.run_once(cfg)
+            pools = []
+
+            class RecordingPool(kvstore.BlockPool):
+                def __init__(self, capacity_blocks, block_size):
+                    super().__init__(capacity_blocks, block_size)
+                    self.log, self.expect = [], []
+                    self.obj_op = {}   # id(list returned by lookup) -> op index
+                    self.ins_op = {}   # tuple(ids) of an insert result -> op index
+                    pools.append(self)
+
+                def _record(self, op, res, err):
+                    rec = {"error": err, "used": self.used_blocks, "evictions": self.eviction_count,
+                           "matched_tokens": self.matched_tokens, "lookup_tokens": self.lookup_tokens}
+                    rec.update(res)
+                    if len(self.log) % 25 == 0:
+                        rec["digest"] = state_digest(self._blocks.values())
+                    self.log.append(op)
+                    self.expect.append(rec)
+
+                def _refs(self, blocks):
+                    ids = [b.block_id for b in blocks]
+                    if id(blocks) in self.obj_op:  # the matched chain, maybe extended by the allocation
+                        i = self.obj_op[id(blocks)]
+                        n0 = len(self.expect[i]["ids"])
+                        refs = [i]
+                        if len(ids) > n0:
+                            refs.append(self.ins_op[tuple(ids[n0:])])
+                        return refs
+                    return [self.ins_op[tuple(ids)]]
+
+                def longest_prefix_match(self, ns, query, now):
+                    m, blocks = super().longest_prefix_match(ns, query, now)
+                    i = len(self.log)
+                    self.obj_op[id(blocks)] = i
+                    self._record(dict({"op": "lookup", "ns": ns, "now": now}, **_compress_tokens(query)),
+                                 {"matched": m, "ids": [b.block_id for b in blocks]}, None)
+                    return m, blocks
+
+                def insert(self, ns, seq, now):
+                    op = dict({"op": "insert", "ns": ns, "now": now}, **_compress_tokens(seq))
+                    try:
+                        new = super().insert(ns, seq, now)
+                    except kvstore.CapacityExhausted:
+                        self._record(op, {}, "capacity")
+                        raise
+                    self.ins_op[tuple(b.block_id for b in new)] = len(self.log)
+                    self._record(op, {"ids": [b.block_id for b in new]}, None)
+                    return new
+
+                def pin(self, blocks, now):
+                    refs = self._refs(blocks)
+                    super().pin(blocks, now)
+                    self._record({"op": "pin", "refs": refs, "now": now}, {}, None)
+
+                def release(self, blocks):
+                    refs = self._refs(blocks)
+                    super().release(blocks)
+                    self._record({"op": "release", "refs": refs}, {}, None)
+
+            saved = cluster.BlockPool
+            cluster.BlockPool = RecordingPool
+            try:
+                _, rec_report = experiment.run_once(cfg)
+            finally:
+                cluster.BlockPool = saved
+            assert json.dumps(rec_report, sort_keys=True) == json.dumps(plain, sort_keys=True)
+            for w, pool in enumerate(pools):
+                final = sorted(
+                    (b.block_id, b.namespace, list(b.token_span), b.parent_id, b.ref_count,
+                     b.last_access, b.child_count)
+                    for b in pool._blocks.values())
+                pool.expect[-1]["digest"] = state_digest(pool._blocks.values())
+                # (the full final state is covered by the last op's digest;
+                # dump_tree kept for worker 0)
+                del final
+                logs.append({"name": f"des_fast_react_{mode}_cap{cap}_w{w}", "capacity": cap,
+                             "block_size": pool.block_size, "ops": pool.log, "expect": pool.expect,
+                             "footprint": dict(pool.footprint_tokens()),
+                             "peak": dict(pool.peak_footprint_tokens()),
+                             **({"dump_tree": pool.dump_tree()} if w == 0 else {}),
+                             "report": {k: plain[k] for k in ("prefix_hit_ratio", "eviction_count",
+                                                              "failure_count", "request_count")}})
+    return logs
+
+
 def router_fixtures(core, router):
     rng = random.Random(99)
     models = ["model_a", "model_b", "model_c", "model_d"]
@@ -256,6 +382,10 @@ def main() -> None:
                       separators=(",", ":")).encode()
     (OUT / "pool_streams.json.gz").write_bytes(gzip.compress(blob, 9, mtime=0))
     (OUT / "router_traces.json").write_text(json.dumps(router_fixtures(core, router)))
+    blob = json.dumps({"generator": "prefillsim.cluster.Simulation + recording prefillsim.kvstore.BlockPool "
+                                    "(configs/fast_react.toml)", "streams": des_call_logs()},
+                      separators=(",", ":")).encode()
+    (OUT / "des_pool_log.json.gz").write_bytes(gzip.compress(blob, 9, mtime=0))
     (OUT / "workload.json").write_text(json.dumps(workload_fixtures(wl), indent=0))
     n_ops = sum(len(s["ops"]) for s in pools)
     print(f"pool streams: {len(pools)} ({n_ops} ops); router traces; workload vectors")

@@ -12,7 +12,7 @@ import random
 
 import pytest
 
-from pool_replay import GpuAdapter, OracleAdapter, expand_tokens, load_streams, replay
+from pool_replay import GpuAdapter, OracleAdapter, expand_tokens, load_des_logs, load_streams, replay
 
 
 def _stream_ids():
@@ -33,6 +33,30 @@ def test_golden_streams_cover_edge_cases():
     assert evictions > 1000
     assert any(len(expand_tokens(op)) >= 4096 for s in streams for op in s["ops"]
                if op["op"] == "insert")
+
+
+def _des_ids():
+    return [s["name"] for s in load_des_logs()]
+
+
+def test_des_call_logs_cover_the_seam():
+    """The recorded reference runs exercise every seam op, heavy eviction and
+    capacity failures, in both serving modes."""
+    logs = load_des_logs()
+    assert {s["name"].split("_")[3] for s in logs} == {"baseline", "prefillshare"}
+    kinds = {op["op"] for s in logs for op in s["ops"]}
+    assert kinds == {"lookup", "insert", "pin", "release"}
+    assert any(len(op["refs"]) == 2 for s in logs for op in s["ops"] if op["op"] == "release")
+    assert sum(s["expect"][-1]["evictions"] for s in logs) > 500_000
+    assert sum(1 for s in logs for e in s["expect"] if e["error"] == "capacity") > 100
+
+
+@pytest.mark.parametrize("name", [n for n in _des_ids() if "cap100_" in n or n.endswith("prefillshare_cap7500_w3")])
+def test_oracle_matches_des_call_logs(name):
+    """The oracle pool on the reference's recorded seam traffic (the small
+    pools: the oracle's argmin-scan eviction is O(capacity) per eviction)."""
+    stream = next(s for s in load_des_logs() if s["name"] == name)
+    replay(stream, OracleAdapter, check_digest_every=25)
 
 
 # ----------------------------------------------------------------- GPU ----
@@ -205,3 +229,19 @@ def test_gpu_pool_long_contexts_and_growth():
         g.release(chain)
         o.release(chain.ids.tolist())
     assert g.used_blocks == o.used_blocks == 6 * 2048
+
+
+@gpu
+@pytest.mark.parametrize("name", _des_ids())
+def test_gpu_pool_matches_des_call_logs(name):
+    """The pool seam proven on the reference's own traffic: every BlockPool
+    call prefillsim.cluster.Simulation made while serving
+    configs/fast_react.toml (both modes; 7500-, 1500- and 100-block pools)
+    replayed through the GPU pool. Every outcome (matched tokens, block ids,
+    CapacityExhausted), every counter after every op, the full block state
+    every 25 ops and at the end, footprints and dump_tree equal the
+    reference's."""
+    stream = next(s for s in load_des_logs() if s["name"] == name)
+    a = replay(stream, GpuAdapter, check_digest_every=25)
+    if "dump_tree" in stream:
+        assert a.p.dump_tree() == stream["dump_tree"]
