@@ -41,7 +41,7 @@ from .kvstore import BlockPool
 from .model import (PAGE_TOKENS, DecodeBatch, DecodeRow, DecodeRunner, KVCache, LlamaConfig,
                     ModuleWeights, PrefillRunner, SessionSpec)
 from .router import Router, ServingMode
-from .staging import HostKVTier, block_keys
+from .staging import HostKVTier, block_edges, block_keys
 
 
 @dataclass
@@ -208,13 +208,14 @@ class AgentServer:
             # GPU misses found in the host tier are reloaded instead of recomputed
             keys = block_keys(ns, req.ctx, nfull)
             mb = m // PAGE_TOKENS
-            slots = self.tier.lookup(keys[mb:nfull])
+            slots = self.tier.lookup(keys[mb:nfull], block_edges(ns, req.ctx, keys, mb, nfull))
             if slots:
                 self.tier.reload(slots, fresh[:len(slots)])
             pos0 = min(m + PAGE_TOKENS * len(slots), nfull * PAGE_TOKENS)
             h = len(slots)
             if nfull - mb > h:  # write-through of the blocks this forward computes
-                self._pending_store.append((keys[mb + h:nfull], fresh[h:nfull - mb]))
+                self._pending_store.append((keys[mb + h:nfull], block_edges(ns, req.ctx, keys, mb + h, nfull),
+                                            fresh[h:nfull - mb]))
         # cluster.py:333-337 / 384-389: the reference's matched / new split;
         # stamped when the forward that computes the request's KV has run on
         # the GPU (immediately when nothing is left to compute)
@@ -272,8 +273,8 @@ class AgentServer:
                     chunk.append(sq)
                     tot += int(sq[0].shape[0])
         if self.tier is not None:
-            for keys, pages in self._pending_store:
-                self.tier.store(keys, pages)
+            for keys, edges, pages in self._pending_store:
+                self.tier.store(keys, edges, pages)
             self._pending_store = []
 
     def _emit(self, t_us: float, kind: str, session: int = -1, request: int = -1, worker: int = -1,

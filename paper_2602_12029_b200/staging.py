@@ -5,8 +5,9 @@ Under load the shared prefix pool fills up and evicts LRU blocks
 (kvstore.py:191-235); a later request of the same session then misses and
 the base module recomputes those tokens. The tier keeps a write-through copy
 of every computed full block in pinned host memory (LRU over its own
-capacity), keyed by namespace + the block's full token path (a block's KV is
-a function of exactly that prefix). On a GPU miss, the pool still allocates
+capacity), found by a rolling key of namespace + the block's full token path
+(a block's KV is a function of exactly that prefix) and verified by the
+block's exact edge (namespace, parent key, 16 tokens) before any reload. On a GPU miss, the pool still allocates
 the blocks exactly as the reference does (hit / miss / eviction accounting
 is unchanged); the consecutive missing blocks found in the tier are copied
 back host -> device into their new pages instead of being recomputed, so the
@@ -25,8 +26,13 @@ import torch
 from .model import PAGE_TOKENS, KVCache
 
 
+ROOT_KEY = 0  # parent key of a context's first block
+
+
 def block_keys(ns: str, ctx: np.ndarray, n_blocks: int) -> list[int]:
-    """Rolling key of each full block: hash(namespace, tokens[0, 16(k+1)))."""
+    """Rolling key of each full block: hash(namespace, tokens[0, 16(k+1))).
+    A key only FINDS a candidate; TierIndex.lookup verifies the candidate's
+    exact edge before it is reloaded."""
     keys, h = [], hash(("psk-tier", ns))
     for k in range(n_blocks):
         h = hash((h, ctx[k * PAGE_TOKENS:(k + 1) * PAGE_TOKENS].tobytes()))
@@ -34,27 +40,72 @@ def block_keys(ns: str, ctx: np.ndarray, n_blocks: int) -> list[int]:
     return keys
 
 
+def block_edges(ns: str, ctx: np.ndarray, keys: list[int], first: int, last: int) -> list[tuple]:
+    """Exact identity of blocks [first, last): (namespace, parent block's
+    key, the block's 16 tokens) -- the reference's edge key
+    (ns, parent, token_span), kvstore.py:69-70."""
+    return [(ns, keys[k - 1] if k > 0 else ROOT_KEY, ctx[k * PAGE_TOKENS:(k + 1) * PAGE_TOKENS].tobytes())
+            for k in range(first, last)]
+
+
+class TierIndex:
+    """Host-side index of the tier: key -> slot (LRU order) plus each slot's
+    exact edge. Lookup walks the context's blocks from the first requested
+    one and stops at the first block whose key is absent OR whose stored edge
+    (namespace, parent key, 16 tokens) differs from the context's: a 64-bit
+    key collision can never reload another path's KV. (By induction from
+    the first block: equal tokens at every level and equal parent keys mean
+    the stored block's full token path is the context's.)"""
+
+    def __init__(self, capacity: int):
+        self.capacity = capacity
+        self.lru: OrderedDict[int, int] = OrderedDict()  # key -> slot
+        self.edge: dict[int, tuple] = {}                 # slot -> (ns, parent key, token bytes)
+        self.free = list(range(capacity - 1, -1, -1))
+        self.collisions = 0
+
+    def lookup(self, keys: list[int], edges: list[tuple]) -> list[int]:
+        out = []
+        for k, e in zip(keys, edges):
+            s = self.lru.get(k)
+            if s is None:
+                break
+            if self.edge[s] != e:  # same key, different block: a collision
+                self.collisions += 1
+                break
+            self.lru.move_to_end(k)
+            out.append(s)
+        return out
+
+    def place(self, key: int, edge: tuple) -> int | None:
+        """Slot for a new block (None: already present). Evicts the LRU entry
+        when full."""
+        if key in self.lru:
+            self.lru.move_to_end(key)
+            return None
+        if self.free:
+            s = self.free.pop()
+        else:
+            _, s = self.lru.popitem(last=False)
+        self.lru[key] = s
+        self.edge[s] = edge
+        return s
+
+
 class HostKVTier:
     def __init__(self, kv: KVCache, capacity_blocks: int):
         self.kv = kv
         self.capacity = capacity_blocks
         self.buf = torch.empty(capacity_blocks, kv.data.shape[1], dtype=kv.data.dtype).pin_memory()
-        self.lru: OrderedDict[int, int] = OrderedDict()  # key -> host slot
-        self.free = list(range(capacity_blocks - 1, -1, -1))
+        self.index = TierIndex(capacity_blocks)
         self.d2h = torch.cuda.Stream(device=kv.data.device)
         self.stored = 0
         self.reloaded = 0
 
-    def lookup(self, keys: list[int]) -> list[int]:
-        """Host slots of the longest run of `keys` present (LRU-touched)."""
-        out = []
-        for k in keys:
-            s = self.lru.get(k)
-            if s is None:
-                break
-            self.lru.move_to_end(k)
-            out.append(s)
-        return out
+    def lookup(self, keys: list[int], edges: list[tuple]) -> list[int]:
+        """Host slots of the longest verified run of blocks present
+        (LRU-touched); edges from block_edges()."""
+        return self.index.lookup(keys, edges)
 
     def reload(self, slots: list[int], pages: list[int]) -> None:
         """H2D into the pool's new pages, ordered on the current stream (after
@@ -64,21 +115,16 @@ class HostKVTier:
             self.kv.data[p].copy_(self.buf[s], non_blocking=True)
         self.reloaded += len(slots)
 
-    def store(self, keys: list[int], pages: list[int]) -> None:
+    def store(self, keys: list[int], edges: list[tuple], pages: list[int]) -> None:
         """Write-through of freshly computed blocks (after the forward that
         wrote them, on a side stream)."""
         cur = torch.cuda.current_stream(self.kv.data.device)
         self.d2h.wait_stream(cur)  # the forward (and any reload reading a slot reused below) is done
         with torch.cuda.stream(self.d2h):
-            for k, p in zip(keys, pages):
-                if k in self.lru:
-                    self.lru.move_to_end(k)
+            for k, e, p in zip(keys, edges, pages):
+                s = self.index.place(k, e)
+                if s is None:
                     continue
-                if self.free:
-                    s = self.free.pop()
-                else:
-                    _, s = self.lru.popitem(last=False)
-                self.lru[k] = s
                 self.buf[s].copy_(self.kv.data[p], non_blocking=True)
                 self.stored += 1
 
@@ -88,5 +134,5 @@ class HostKVTier:
         torch.cuda.current_stream(self.kv.data.device).wait_stream(self.d2h)
 
     def stats(self) -> dict:
-        return {"capacity_blocks": self.capacity, "resident_blocks": len(self.lru), "stored": self.stored,
-                "reloaded": self.reloaded}
+        return {"capacity_blocks": self.capacity, "resident_blocks": len(self.index.lru), "stored": self.stored,
+                "reloaded": self.reloaded, "key_collisions_rejected": self.index.collisions}

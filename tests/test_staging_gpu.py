@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 
 def test_tier_roundtrip_bit_exact():
     from paper_2602_12029_b200.model import KVCache, LlamaConfig, ModuleWeights, PrefillRunner
-    from paper_2602_12029_b200.staging import HostKVTier, block_keys
+    from paper_2602_12029_b200.staging import HostKVTier, block_edges, block_keys
     cfg = LlamaConfig.tiny()
     base = ModuleWeights(cfg, 1, with_head=False)
     kv = KVCache(cfg, 40)
@@ -22,11 +22,12 @@ def test_tier_roundtrip_bit_exact():
     pre.run(torch.from_numpy(ctx).cuda(), 0, torch.tensor(pages, dtype=torch.int32, device="cuda"))
     tier = HostKVTier(kv, capacity_blocks=8)
     keys = block_keys("shared", ctx, 18)
-    tier.store(keys[:6], pages[:6])
-    tier.store(keys[6:14], pages[6:14])  # LRU: the first 6 are evicted from the 8-block tier
+    ed = block_edges("shared", ctx, keys, 0, 18)
+    tier.store(keys[:6], ed[:6], pages[:6])
+    tier.store(keys[6:14], ed[6:14], pages[6:14])  # LRU: the first 6 are evicted from the 8-block tier
     want = kv.data[pages[6:14]].clone()
-    assert tier.lookup(keys[:6]) == []
-    slots = tier.lookup(keys[6:14])
+    assert tier.lookup(keys[:6], ed[:6]) == []
+    slots = tier.lookup(keys[6:14], ed[6:14])
     assert len(slots) == 8
     new_pages = list(range(25, 33))
     kv.data[new_pages].zero_()
