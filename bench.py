@@ -468,6 +468,80 @@ def agents_point(cfg, mods, base, rate: float = 8.0, duration: float = 20.0, row
     return out
 
 
+def pd_split_point(world: int, rank: int, local: int, ctrl, duration: float = 10.0, rows: int = 32,
+                   pool_pages: int = 7500, cfg=None, place=None, max_context: int = 4096,
+                   max_output: int = 256) -> dict | None:
+    """BASELINE configs 3 / 5 on the N-GPU prefill/decode split
+    (north_star: "2/4/8-GPU prefill/decode splits"): the reference fleet's
+    4 logical prefill workers (own 7500-block pools) on P = max(1, N/4)
+    prefill GPUs, the 4 models' decode workers replicated over the other
+    N - P GPUs (router.Placement.split(replicate=True): 2P + 6D uses all six
+    decode GPUs), disagg.DisaggServer serving workload.generate (ReAct,
+    Poisson arrivals at 4 x N sessions/s for `duration` s: the offered load
+    grows with the fleet) in real time, BASELINE then PREFILLSHARE on the
+    same weights. Per mode: req/s, p95 E2E / TTFT (GPU completion times),
+    prefix hit ratio, and the cross-GPU KV handoff volume and GB/s (packed
+    per peer pair, NCCL P2P over NVLink; sender-side pack + transfer time).
+    Every rank runs it; rank 0 returns the dict."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_12029_b200 import workload as wl
+    from paper_2602_12029_b200.disagg import (Coordinator, DisaggServer, GpuDecodeBackend, GpuPrefillBackend,
+                                              summarize)
+    from paper_2602_12029_b200.model import LlamaConfig, ModuleWeights
+    from paper_2602_12029_b200.router import Placement, Router, ServingMode
+    models = list(wl.DEFAULT_MODELS)
+    M = len(models)
+    if place is None:
+        P = max(1, world // 4)
+        place = Placement.split(M, list(range(P)), list(range(P, world)), M, replicate=True)
+    cfg = cfg or LlamaConfig.llama8b(max_pos=max_context + 512)
+    ctx_pages_per_row = max_context // 16 + 4
+    mine_p = [w for w, r in enumerate(place.prefill_gpus) if r == rank]
+    mine_d = place.decode_models_on(rank)
+    rate = 4.0 * world
+    sessions = wl.generate(wl.WorkloadConfig(pattern="react", arrival_rate_per_s=rate, duration_s=duration, seed=0))
+    out = {"workload": f"configs[2]/[4]: react, {rate:g} sessions/s for {duration:g} s, {len(sessions)} sessions, "
+                       f"{sum(s.total_requests for s in sessions)} requests",
+           "placement": {"prefill_gpus": list(place.prefill_gpus),
+                         "decode_replicas": [list(place.replicas(m)) for m in range(M)]},
+           "rows_per_model_replica": rows, "pool_blocks_per_worker": pool_pages}
+    for mode in (ServingMode.BASELINE, ServingMode.PREFILLSHARE):
+        base = (ModuleWeights(cfg, 99, with_head=False, device=local)
+                if mine_p and mode is ServingMode.PREFILLSHARE else None)
+        need = set(mine_d) | (set(mine_p) if mode is ServingMode.BASELINE else set())
+        mods = {m: ModuleWeights(cfg, 100 + m, device=local) for m in sorted(need)}
+        prefill = {w: GpuPrefillBackend(cfg, base if base is not None else mods[w], pool_pages, max_context, 256,
+                                        local) for w in mine_p}
+        decode = (GpuDecodeBackend(cfg, {m: mods[m] for m in mine_d}, rows,
+                                   ctx_pages=len(mine_d) * rows * ctx_pages_per_row, max_context=max_context,
+                                   max_output=max_output, device=local) if mine_d else None)
+        srv = DisaggServer(place, models, mode, prefill, decode, rows, ctrl_group=ctrl)
+        coord = Coordinator(sessions, models, Router(mode, models), place, steps_per_round=8) if rank == 0 else None
+        torch.cuda.synchronize()
+        dist.barrier(group=ctrl)
+        recs = srv.run(coord)
+        torch.cuda.synchronize()
+        hs = [None] * world if rank == 0 else None
+        dist.gather_object(srv.handoff_stats(), hs, dst=0, group=ctrl)
+        if rank == 0:
+            sm = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in summarize(recs).items()}
+            nb = sum(h["bytes"] for h in hs)
+            sec = max(h["seconds"] for h in hs)
+            sm["handoff"] = {"bytes": nb, "gbs_per_sender": [round(h["gbs"], 1) if h["gbs"] else None for h in hs],
+                             "aggregate_gbs": round(nb / sec / 1e9, 1) if sec > 0 else None}
+            out[mode.value] = sm
+        del srv, prefill, decode, mods, base
+        torch.cuda.empty_cache()
+    if rank != 0:
+        return None
+    b, p = out["baseline"], out["prefillshare"]
+    if b.get("req_per_s") and p.get("req_per_s"):
+        out["req_per_s_ratio"] = round(p["req_per_s"] / b["req_per_s"], 3)
+        out["p95_e2e_ratio"] = round(b["p95_e2e_ms"] / p["p95_e2e_ms"], 3)
+    return out
+
+
 def prefill_roofline(eng, peaks) -> dict:
     import torch
     T = PROMPT
@@ -522,8 +596,13 @@ def main() -> None:
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
+    ctrl = None
     if world > 1:
+        import datetime
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # host control plane of the P/D split (and a long-timeout barrier
+        # while rank 0 runs the single-GPU extras)
+        ctrl = dist.new_group(backend="gloo", timeout=datetime.timedelta(hours=1))
     from paper_2602_12029_b200.engine import PrefillShareEngine
     from paper_2602_12029_b200.model import LlamaConfig
     peaks = _peaks()
@@ -616,9 +695,10 @@ def main() -> None:
         mods, base = eng.mods, eng.base
         del eng
         torch.cuda.empty_cache()
-        out["sessions_sweep"] = [serve_point(cfg, mods, base, n, batches, local)
-                                 for n in (1, 8, 64) if n != S]
-        out["agents"] = agents_point(cfg, mods, base)
+        if world == 1:  # single-GPU serving points (N > 1: the P/D split below)
+            out["sessions_sweep"] = [serve_point(cfg, mods, base, n, batches, local)
+                                     for n in (1, 8, 64) if n != S]
+            out["agents"] = agents_point(cfg, mods, base)
         del mods, base
         torch.cuda.empty_cache()
         out["decode_attn_fanout_32k_x16"] = decode_attn_fanout(peaks)
@@ -628,6 +708,15 @@ def main() -> None:
             ref.sample()  # warm-up
             out["cpu_baseline"] = ref.sample()
             del ref
+    if world > 1 and not a.no_extras:
+        # every rank: the prefill/decode split on this node's N GPUs
+        if "eng" in locals():
+            del eng
+        torch.cuda.empty_cache()
+        dist.barrier(group=ctrl)
+        pd = pd_split_point(world, rank, local, ctrl)
+        if rank == 0:
+            out["pd_split"] = pd
     if rank == 0:
         print(json.dumps(out))
     if world > 1:

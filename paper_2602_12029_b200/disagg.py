@@ -117,6 +117,11 @@ class PrefillBackend:
         """seqs: (token ids of positions [pos0, pos0 + T), pos0, page table)."""
         raise NotImplementedError
 
+    def pack(self, pages: list[int]) -> torch.Tensor:
+        """The pages, gathered into one contiguous [n, page] buffer (one P2P
+        message per peer per round instead of one per 2 MiB page)."""
+        return self.kv_pages[torch.as_tensor(pages, dtype=torch.long, device=self.kv_pages.device)]
+
 
 class DecodeBackend:
     """What a decode worker needs: a page store with an allocator, a fixed
@@ -157,6 +162,10 @@ class DecodeBackend:
         """Same-rank handoff."""
         for s, d in zip(src_pages, dst_pages):
             self.kv_pages[d].copy_(src[s])
+
+    def unpack(self, buf: torch.Tensor, pages: list[int]) -> None:
+        """Scatter a received contiguous buffer into the allocated pages."""
+        self.kv_pages[torch.as_tensor(pages, dtype=torch.long, device=self.kv_pages.device)] = buf
 
 
 # ----------------------------------------------------------- coordinator ----
@@ -205,9 +214,12 @@ class Coordinator:
         self.queue.append(Job(rid, sid, m, np.asarray(self.ctx[sid], dtype=np.int64), agent.output_len, w,
                               self.place.prefill_gpus[w], self.place.decode_gpus[m]))
 
-    def plan(self, free_rows: dict[int, int]) -> Round:
+    def plan(self, free_rows: dict[tuple[int, int], int]) -> Round:
         """Arrivals up to now, then the queued jobs whose model has a free
-        decode row (free_rows: model -> free rows after the last round)."""
+        decode row on one of its replicas (free_rows: (model, rank) -> free
+        rows after the last round). A job goes to the replica with the most
+        free rows (ties -> lowest rank): a placement choice only, the
+        logical decode worker (router.py:79-85) is the model's."""
         t = self.now_us()
         while self.arrivals and self.arrivals[0].arrival_time * self.time_scale <= t:
             s = self.arrivals.popleft()
@@ -218,8 +230,10 @@ class Coordinator:
         rows = dict(free_rows)
         while self.queue:
             j = self.queue.popleft()
-            if rows.get(j.model, 0) > 0:
-                rows[j.model] -= 1
+            best = max(self.place.replicas(j.model), key=lambda g: (rows.get((j.model, g), 0), -g))
+            if rows.get((j.model, best), 0) > 0:
+                rows[(j.model, best)] -= 1
+                j.dst = best
                 jobs.append(j)
                 self.inflight[j.rid] = j
                 self.remaining[j.rid] = j.out_len
@@ -285,6 +299,12 @@ class DisaggServer:
         self.world = dist.get_world_size()
         # decode-side state of this rank: row -> [job, pages, steps done]
         self.rows: dict[int, list] = {}
+        # cross-rank handoffs sent by this rank: bytes and sender-side time
+        # (pack + transfer, CUDA events on the handoff stream on GPUs)
+        self.handoff_bytes = 0
+        self.handoff_s = 0.0
+        self._hev: list = []
+        self._side = None
 
     # -- one round on this rank ------------------------------------------
     def _prefill_phase(self, rnd: Round):
@@ -324,12 +344,31 @@ class DisaggServer:
                 be.forward(seqs)
         return report, out, held
 
+    def _stream_ctx(self, t: torch.Tensor):
+        """Handoff work on a side stream (GPU): it waits only for the work it
+        needs, not for the decode steps queued on the main stream."""
+        import contextlib
+        if not t.is_cuda:
+            return contextlib.nullcontext()
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=t.device)
+        return torch.cuda.stream(self._side)
+
     def _handoff(self, rnd: Round, out) -> list:
-        """All pages of all contexts this round, one batched P2P exchange.
-        Sends and receives are posted in PLAN order on every rank, so the
-        n-th message between two ranks is the same job on both sides."""
+        """All pages of all contexts this round: per (src, dst) rank pair ONE
+        contiguous message, the pair's jobs' pages packed in plan order (K8
+        page copies on GPUs), exchanged in one batch_isend_irecv per rank
+        (NCCL over NVLink on GPUs, gloo on CPU; sizes follow from the context
+        lengths, so no headers and no ordering deadlock), unpacked into pages
+        from the receiver's allocator. Sender and receiver run it on a side
+        stream: the prefill forward it needs is awaited, the receiver's
+        queued decode steps are not (the reference serializes ingest with
+        decode steps, cluster.py:370-390; here they overlap). A handoff
+        inside one rank is a page copy."""
         mine = {j.rid: (be, pages) for j, be, pages in out}
-        ops, arrived, local = [], [], []
+        send: dict[int, list] = {}
+        recv: dict[int, list] = {}
+        local = []
         for j in rnd.jobs:
             if j.rid not in self._ok_all:
                 continue
@@ -337,20 +376,74 @@ class DisaggServer:
                 be, pages = mine[j.rid]
                 local.append((j, be, pages))
             elif j.src == self.rank:
-                be, pages = mine[j.rid]
-                ops += [dist.P2POp(dist.isend, be.kv_pages[p], j.dst, group=self.data) for p in pages]
+                send.setdefault(j.dst, []).append(mine[j.rid])
             elif j.dst == self.rank:
-                pages = self.decode.alloc(j.n_pages)
-                ops += [dist.P2POp(dist.irecv, self.decode.kv_pages[p], j.src, group=self.data) for p in pages]
-                arrived.append((j, pages))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
+                recv.setdefault(j.src, []).append((j, self.decode.alloc(j.n_pages)))
+        arrived = []
+        if send or recv:
+            ref = next(iter(self.prefill.values())).kv_pages if self.prefill else self.decode.kv_pages
+            cuda = ref.is_cuda
+            main = torch.cuda.current_stream(ref.device) if cuda else None
+            with self._stream_ctx(ref):
+                if cuda:
+                    if send:
+                        self._side.wait_stream(main)  # the prefill forwards whose pages are packed
+                    ev0 = torch.cuda.Event(enable_timing=True)
+                    ev0.record()
+                t0 = time.perf_counter()
+                ops, bufs = [], []
+                nbytes = 0
+                for dst in sorted(send):
+                    parts = [be.pack(pages) for be, pages in send[dst]]
+                    buf = parts[0] if len(parts) == 1 else torch.cat(parts)
+                    nbytes += buf.numel() * buf.element_size()
+                    ops.append(dist.P2POp(dist.isend, buf, dst, group=self.data))
+                    bufs.append(buf)
+                for src in sorted(recv):
+                    n = sum(j.n_pages for j, _ in recv[src])
+                    buf = torch.empty((n,) + tuple(self.decode.kv_pages.shape[1:]), dtype=self.decode.kv_pages.dtype,
+                                      device=self.decode.kv_pages.device)
+                    ops.append(dist.P2POp(dist.irecv, buf, src, group=self.data))
+                    bufs.append((src, buf))
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+                if cuda and recv:
+                    # freed pages being written may still be read by decode
+                    # steps queued before them; the receive itself did not wait
+                    self._side.wait_stream(main)
+                for item in bufs:
+                    if isinstance(item, tuple):
+                        src, buf = item
+                        off = 0
+                        for j, pages in recv[src]:
+                            self.decode.unpack(buf[off:off + j.n_pages], pages)
+                            off += j.n_pages
+                            arrived.append((j, pages))
+                if nbytes:
+                    self.handoff_bytes += nbytes
+                    if cuda:
+                        ev1 = torch.cuda.Event(enable_timing=True)
+                        ev1.record()
+                        self._hev.append((ev0, ev1))
+                    else:
+                        self.handoff_s += time.perf_counter() - t0
+            if cuda:
+                main.wait_stream(self._side)  # decode steps read the received pages
         for j, be, pages in local:
             dst = self.decode.alloc(j.n_pages)
             self.decode.copy_pages(be.kv_pages, pages, dst)
             arrived.append((j, dst))
         return arrived
+
+    def handoff_stats(self) -> dict:
+        """Bytes this rank sent to other ranks and the sender-side time
+        (pack + transfer), GB/s."""
+        for a, b in self._hev:
+            b.synchronize()
+            self.handoff_s += a.elapsed_time(b) / 1e3
+        self._hev = []
+        return {"bytes": self.handoff_bytes, "seconds": self.handoff_s,
+                "gbs": self.handoff_bytes / self.handoff_s / 1e9 if self.handoff_s > 0 else None}
 
     def _decode_phase(self, rnd: Round, arrived) -> list:
         report = []
@@ -382,15 +475,14 @@ class DisaggServer:
             report.append((rid, first, n_done, times[k]))
         return report
 
-    def free_rows(self) -> dict[int, int]:
-        """Free decode rows per model hosted on this rank."""
+    def free_rows(self) -> dict[tuple[int, int], int]:
+        """Free decode rows per (model, this rank) for the replicas hosted here."""
         if self.decode is None:
             return {}
         out = {}
-        for m in range(len(self.model_ids)):
-            if self.place.decode_gpus[m] == self.rank:
-                busy = sum(1 for st in self.rows.values() if st[0].model == m)
-                out[m] = self.rows_per_model - busy
+        for m in self.place.decode_models_on(self.rank):
+            busy = sum(1 for st in self.rows.values() if st[0].model == m)
+            out[(m, self.rank)] = self.rows_per_model - busy
         return out
 
     def run(self, coord: Coordinator | None, max_rounds: int = 1 << 30) -> dict[int, Record] | None:
@@ -415,9 +507,10 @@ class DisaggServer:
             for pool, h in held:  # cluster.py:404-412: pins drop once the handoff is done
                 pool.release(h)
             dec_rep = self._decode_phase(rnd, arrived) if self.decode is not None else []
-            all_dec = self._gather(dec_rep)
-            free = self._gather(self.free_rows())
+            both = self._gather((dec_rep, self.free_rows()))  # one control message per rank
             if self.rank == 0:
+                all_dec = [b[0] for b in both]
+                free = [b[1] for b in both]
                 coord.absorb(rnd, all_pre, all_dec)
         return coord.records if self.rank == 0 else None
 
@@ -482,6 +575,13 @@ class GpuPrefillBackend(PrefillBackend):
         if k >= self.max_jobs:
             raise ValueError("more prefill jobs in a round than tail pages")
         return self.pool_pages + k
+
+    def pack(self, pages):
+        from .transfer import copy_pages
+        buf = torch.empty((len(pages),) + tuple(self.kv_pages.shape[1:]), dtype=self.kv_pages.dtype,
+                          device=self.kv_pages.device)
+        copy_pages(self.kv_pages, buf, pages, list(range(len(pages))))
+        return buf
 
     def forward(self, seqs) -> None:
         V = self.cfg.vocab
@@ -563,3 +663,7 @@ class GpuDecodeBackend(DecodeBackend):
     def copy_pages(self, src, src_pages, dst_pages):
         from .transfer import copy_pages
         copy_pages(src, self.kv_pages, src_pages, dst_pages)
+
+    def unpack(self, buf, pages):
+        from .transfer import copy_pages
+        copy_pages(buf, self.kv_pages, list(range(len(pages))), pages)

@@ -85,10 +85,26 @@ class Router:
 @dataclass(frozen=True)
 class Placement:
     """Logical workers -> GPUs. prefill_gpus[i]: GPU of logical prefill worker
-    i; decode_gpus[j]: GPU of model j's decode worker."""
+    i; decode_gpus[j]: GPU of model j's decode worker (its first replica).
+    decode_replicas[j] (optional): every GPU holding a replica of model j's
+    decode worker. The logical decode worker id stays n_models + j
+    (router.py:79-85, bit-exact); which replica serves a request is a
+    placement decision (the coordinator picks the one with the most free
+    rows), so 2 prefill + 6 decode GPUs use all six decode GPUs for four
+    models."""
 
     prefill_gpus: tuple[int, ...]
     decode_gpus: tuple[int, ...]
+    decode_replicas: tuple[tuple[int, ...], ...] | None = None
+
+    def replicas(self, model_index: int) -> tuple[int, ...]:
+        if self.decode_replicas is None:
+            return (self.decode_gpus[model_index],)
+        return self.decode_replicas[model_index]
+
+    def decode_models_on(self, gpu: int) -> list[int]:
+        """Models with a decode replica on `gpu`."""
+        return [m for m in range(len(self.decode_gpus)) if gpu in self.replicas(m)]
 
     @staticmethod
     def colocated(n_models: int, n_prefill: int | None = None, gpu: int = 0) -> "Placement":
@@ -97,12 +113,19 @@ class Placement:
 
     @staticmethod
     def split(n_models: int, prefill_gpus: list[int], decode_gpus: list[int],
-              n_prefill: int | None = None) -> "Placement":
+              n_prefill: int | None = None, replicate: bool = False) -> "Placement":
         """Round-robin logical workers over disjoint prefill / decode GPU sets
-        (BASELINE.json config 3: 2 prefill GPUs + 6 decode GPUs)."""
+        (BASELINE.json config 3: 2 prefill GPUs + 6 decode GPUs). replicate:
+        decode GPU k holds a replica of model k % n_models, so every decode
+        GPU serves (with fewer decode GPUs than models, GPUs host several
+        models as without replicas)."""
         n_prefill = n_models if n_prefill is None else n_prefill
-        return Placement(tuple(prefill_gpus[i % len(prefill_gpus)] for i in range(n_prefill)),
-                         tuple(decode_gpus[j % len(decode_gpus)] for j in range(n_models)))
+        pre = tuple(prefill_gpus[i % len(prefill_gpus)] for i in range(n_prefill))
+        first = tuple(decode_gpus[j % len(decode_gpus)] for j in range(n_models))
+        if not replicate or len(decode_gpus) <= n_models:
+            return Placement(pre, first)
+        reps = tuple(tuple(g for k, g in enumerate(decode_gpus) if k % n_models == j) for j in range(n_models))
+        return Placement(pre, first, reps)
 
     def handoff_is_local(self, prefill_worker: int, model_index: int) -> bool:
         return self.prefill_gpus[prefill_worker] == self.decode_gpus[model_index]

@@ -82,6 +82,7 @@ class _FakeDecode(DecodeBackend):
         self.busy = [False] * (len(self.models) * rows)
         self.checked = 0
         self.bad = 0
+        self.per_model = {}
 
     def alloc(self, n):
         return self.alloc_.alloc(n)
@@ -101,6 +102,7 @@ class _FakeDecode(DecodeBackend):
         self.busy[row] = True
         got = self.kv_pages[pages].reshape(-1)[:len(job.ctx)].numpy()
         self.checked += 1
+        self.per_model[job.model] = self.per_model.get(job.model, 0) + 1
         if not np.array_equal(got, job.ctx):
             self.bad += 1
 
@@ -115,23 +117,34 @@ class _FakeDecode(DecodeBackend):
             self.kv_pages[d].copy_(src[s])
 
 
-def _worker(rank, port, mode_name, q):
+def _placement(mode, world):
+    from paper_2602_12029_b200.router import Placement, ServingMode
+    if world == 3:
+        if mode is ServingMode.PREFILLSHARE:
+            return Placement((0, 1), (2, 2, 1, 1))      # 2 shared prefill workers
+        return Placement((0, 0, 1, 1), (2, 2, 1, 1))    # one prefill worker per model
+    # world 4: rank 0 prefills only; decode replicas 1:many (models 0 and 3
+    # on two ranks each), rank 3 also hosts a prefill worker
+    reps = ((1, 2), (3,), (1,), (2, 3))
+    if mode is ServingMode.PREFILLSHARE:
+        return Placement((0, 3), (1, 3, 1, 2), reps)
+    return Placement((0, 0, 3, 3), (1, 3, 1, 2), reps)
+
+
+def _worker(rank, port, mode_name, q, world=3):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=3)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2602_12029_b200 import workload as wl
         from paper_2602_12029_b200.disagg import Coordinator, DisaggServer, summarize
-        from paper_2602_12029_b200.router import Placement, Router, ServingMode
+        from paper_2602_12029_b200.router import Router, ServingMode
         mode = ServingMode(mode_name)
         models = list(wl.DEFAULT_MODELS)
-        if mode is ServingMode.PREFILLSHARE:
-            place = Placement((0, 1), (2, 2, 1, 1))      # 2 shared prefill workers
-        else:
-            place = Placement((0, 0, 1, 1), (2, 2, 1, 1))  # one prefill worker per model
+        place = _placement(mode, world)
         mine = [w for w, r in enumerate(place.prefill_gpus) if r == rank]
         prefill = {w: _FakePrefill() for w in mine}
-        hosted = [m for m, r in enumerate(place.decode_gpus) if r == rank]
+        hosted = place.decode_models_on(rank)
         decode = _FakeDecode(hosted, rows=3) if hosted else None
         srv = DisaggServer(place, models, mode, prefill, decode, rows_per_model=3)
         coord = None
@@ -141,7 +154,8 @@ def _worker(rank, port, mode_name, q):
             coord = Coordinator(sessions, models, Router(mode, models), place, time_scale=0.02,
                                 steps_per_round=48)
         recs = srv.run(coord, max_rounds=5000)
-        out = {"rank": rank, "checked": decode.checked if decode else 0, "bad": decode.bad if decode else 0}
+        out = {"rank": rank, "checked": decode.checked if decode else 0, "bad": decode.bad if decode else 0,
+               "per_model": decode.per_model if decode else {}, "handoff": srv.handoff_stats()}
         if rank == 0:
             out["n_req"] = sum(s.total_requests for s in sessions)
             out["summary"] = summarize(recs)
@@ -155,13 +169,30 @@ def _worker(rank, port, mode_name, q):
 
 @pytest.mark.parametrize("mode", ["prefillshare", "baseline"])
 def test_disaggregated_serving_gloo_three_ranks(mode):
+    by = _spawn(mode, 3)
+    assert by[1]["checked"] > 0 and by[2]["checked"] > 0   # same-rank and cross-rank handoffs
+
+
+@pytest.mark.parametrize("mode", ["prefillshare", "baseline"])
+def test_decode_replicas_gloo_four_ranks(mode):
+    """1:many placement: models 0 and 3 have decode replicas on two ranks;
+    the coordinator spreads their requests over both replicas (most free
+    rows), every context arrives intact, rank 0 (prefill only) decodes
+    nothing."""
+    by = _spawn(mode, 4)
+    assert by[0]["checked"] == 0
+    assert by[1]["per_model"].get(0, 0) > 0 and by[2]["per_model"].get(0, 0) > 0
+    assert by[2]["per_model"].get(3, 0) > 0 and by[3]["per_model"].get(3, 0) > 0
+
+
+def _spawn(mode, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, port, mode, q)) for r in range(3)]
+    ps = [ctx.Process(target=_worker, args=(r, port, mode, q, world)) for r in range(world)]
     for p in ps:
         p.start()
-    res = [q.get(timeout=300) for _ in range(3)]
+    res = [q.get(timeout=300) for _ in range(world)]
     for p in ps:
         p.join(60)
     assert all(p.exitcode == 0 for p in ps)
@@ -169,7 +200,9 @@ def test_disaggregated_serving_gloo_three_ranks(mode):
     r0 = by[0]
     assert r0["done"] == r0["n_req"] and r0["failed"] == 0
     checked = sum(r["checked"] for r in res)
+    # every admitted context's pages hold exactly its token ids
     assert checked == r0["n_req"] and sum(r["bad"] for r in res) == 0
-    assert by[1]["checked"] > 0 and by[2]["checked"] > 0   # same-rank and cross-rank handoffs
     if mode == "prefillshare":
         assert r0["matched"] > 0                             # later agents hit the shared prefix
+    assert sum(r["handoff"]["bytes"] for r in res) > 0      # packed cross-rank messages moved
+    return by

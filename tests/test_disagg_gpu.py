@@ -57,3 +57,29 @@ def test_disagg_colocated_tiny(mode_name):
             assert s["prefix_hit_ratio"] > 0.3
     finally:
         dist.destroy_process_group()
+
+
+def test_bench_pd_split_point_colocated_tiny():
+    """bench.pd_split_point end to end on one GPU (tiny shape, every role
+    co-located, world 1): both modes served, stats gathered, memory freed.
+    The N-GPU NCCL path differs only in the handoff transport (gloo-tested
+    at world 3/4 in test_disagg.py)."""
+    import bench
+    from paper_2602_12029_b200 import workload as wl
+    from paper_2602_12029_b200.model import LlamaConfig
+    from paper_2602_12029_b200.router import Placement
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_port())
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        cfg = LlamaConfig.tiny(max_pos=4096 + 512)
+        out = bench.pd_split_point(1, 0, 0, None, duration=1.0, rows=4, pool_pages=1024, cfg=cfg,
+                                   place=Placement.colocated(len(wl.DEFAULT_MODELS)), max_context=4096,
+                                   max_output=256)
+        for mode in ("baseline", "prefillshare"):
+            assert out[mode]["completed"] > 0 and out[mode]["failed"] == 0
+            assert out[mode]["handoff"]["bytes"] == 0  # co-located: page copies, no P2P
+        assert out["prefillshare"]["prefix_hit_ratio"] > out["baseline"]["prefix_hit_ratio"]
+        assert "req_per_s_ratio" in out
+    finally:
+        dist.destroy_process_group()

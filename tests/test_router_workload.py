@@ -43,6 +43,25 @@ def test_placement_split_and_colocated():
     assert not p.handoff_is_local(0, 0)
     c = R.Placement.colocated(4)
     assert c.handoff_is_local(3, 2)
+    assert p.replicas(1) == (3,) and p.decode_models_on(4) == [2]
+
+
+def test_placement_decode_replicas_use_every_decode_gpu():
+    """2 prefill + 6 decode GPUs, 4 models: every decode GPU holds a replica
+    (models 0 and 1 get two), the logical decode worker ids are unchanged."""
+    p = R.Placement.split(4, [0, 1], [2, 3, 4, 5, 6, 7], n_prefill=2, replicate=True)
+    assert p.prefill_gpus == (0, 1) and p.decode_gpus == (2, 3, 4, 5)
+    assert [p.replicas(m) for m in range(4)] == [(2, 6), (3, 7), (4,), (5,)]
+    assert sorted(g for m in range(4) for g in p.replicas(m)) == [2, 3, 4, 5, 6, 7]
+    assert p.decode_models_on(6) == [0] and p.decode_models_on(0) == []
+    r = R.Router(R.ServingMode.PREFILLSHARE, ["a", "b", "c", "d"])
+
+    class Req:
+        model_id = "b"
+    assert r.decode_worker(Req) == 5  # n_models + index, whatever the replicas
+    # fewer decode GPUs than models: no replicas, GPUs host several models
+    q = R.Placement.split(4, [0], [1, 2], replicate=True)
+    assert q.decode_replicas is None and q.decode_gpus == (1, 2, 1, 2)
 
 
 def test_workload_matches_reference():

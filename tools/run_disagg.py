@@ -58,14 +58,16 @@ def main():
     max_ctx = a.max_context or (5120 if a.pattern == "reflexion" else 4096)
     cfg = (LlamaConfig.llama8b(max_pos=max_ctx + 512) if a.shape == "8b"
            else LlamaConfig.tiny(max_pos=max_ctx + 512))
-    n_prefill = M if mode is ServingMode.BASELINE else (a.prefill_gpus or max(1, world // 4))
+    # the reference fleet: one logical prefill worker (own pool) per model in
+    # both modes (cluster.py:156-160), placed round-robin on the prefill GPUs
+    n_prefill = M
     if world == 1:
         place = Placement.colocated(M, n_prefill)
     else:
         P = a.prefill_gpus or max(1, world // 4)
-        place = Placement.split(M, list(range(P)), list(range(P, world)), n_prefill)
+        place = Placement.split(M, list(range(P)), list(range(P, world)), n_prefill, replicate=True)
     mine_p = [w for w, r in enumerate(place.prefill_gpus) if r == rank]
-    mine_d = [m for m, r in enumerate(place.decode_gpus) if r == rank]
+    mine_d = place.decode_models_on(rank)
     base = ModuleWeights(cfg, 99, with_head=False, device=local) if (mine_p and mode is ServingMode.PREFILLSHARE) else None
     mods = {m: ModuleWeights(cfg, 100 + m, device=local) for m in set(mine_d) | (set(mine_p) if mode is ServingMode.BASELINE else set())}
     prefill = {w: GpuPrefillBackend(cfg, base if base is not None else mods[w], a.pool_pages, max_ctx, 256, local)
@@ -81,7 +83,7 @@ def main():
     recs = srv.run(coord)
     if rank == 0:
         out = {"mode": a.mode, "gpus": world, "placement": {"prefill": list(place.prefill_gpus),
-                                                           "decode": list(place.decode_gpus)},
+                                                           "decode": [list(place.replicas(m)) for m in range(M)]},
                "workload": {"pattern": a.pattern, "rate": a.rate, "duration_s": a.duration,
                             "sessions": len(sessions), "requests": sum(s.total_requests for s in sessions)},
                "summary": summarize(recs)}
