@@ -256,8 +256,10 @@ def des_call_logs(runs=((7500, "baseline"), (7500, "prefillshare"), (1500, "base
                 def __init__(self, capacity_blocks, block_size):
                     super().__init__(capacity_blocks, block_size)
                     self.log, self.expect = [], []
-                    self.obj_op = {}   # id(list returned by lookup) -> op index
-                    self.ins_op = {}   # tuple(ids) of an insert result -> op index
+                    # id(list returned by lookup / insert) -> (op index, the list): the
+                    # list is kept alive so its id is never reused by a later list
+                    self.obj_op = {}
+                    self.ins_op = {}
                     pools.append(self)
 
                 def _record(self, op, res, err):
@@ -270,20 +272,22 @@ def des_call_logs(runs=((7500, "baseline"), (7500, "prefillshare"), (1500, "base
                     self.expect.append(rec)
 
                 def _refs(self, blocks):
-                    ids = [b.block_id for b in blocks]
-                    if id(blocks) in self.obj_op:  # the matched chain, maybe extended by the allocation
-                        i = self.obj_op[id(blocks)]
-                        n0 = len(self.expect[i]["ids"])
-                        refs = [i]
-                        if len(ids) > n0:
-                            refs.append(self.ins_op[tuple(ids[n0:])])
-                        return refs
-                    return [self.ins_op[tuple(ids)]]
+                    if id(blocks) in self.ins_op:  # pin(allocated), cluster.py:346
+                        return [self.ins_op[id(blocks)][0]]
+                    # release(matched chain extended in place by the allocation), cluster.py:347, 349, 409
+                    i = self.obj_op[id(blocks)][0]
+                    n0 = len(self.expect[i]["ids"])
+                    refs = [i]
+                    if len(blocks) > n0:
+                        tail = [b.block_id for b in blocks[n0:]]
+                        refs.append(next(k for k in range(len(self.log) - 1, i, -1)
+                                         if self.log[k]["op"] == "insert" and self.expect[k].get("ids") == tail))
+                    return refs
 
                 def longest_prefix_match(self, ns, query, now):
                     m, blocks = super().longest_prefix_match(ns, query, now)
                     i = len(self.log)
-                    self.obj_op[id(blocks)] = i
+                    self.obj_op[id(blocks)] = (i, blocks)
                     self._record(dict({"op": "lookup", "ns": ns, "now": now}, **_compress_tokens(query)),
                                  {"matched": m, "ids": [b.block_id for b in blocks]}, None)
                     return m, blocks
@@ -295,7 +299,7 @@ def des_call_logs(runs=((7500, "baseline"), (7500, "prefillshare"), (1500, "base
                     except kvstore.CapacityExhausted:
                         self._record(op, {}, "capacity")
                         raise
-                    self.ins_op[tuple(b.block_id for b in new)] = len(self.log)
+                    self.ins_op[id(new)] = (len(self.log), new)
                     self._record(op, {"ids": [b.block_id for b in new]}, None)
                     return new
 
@@ -335,6 +339,49 @@ def des_call_logs(runs=((7500, "baseline"), (7500, "prefillshare"), (1500, "base
     return logs
 
 
+def check_logs_replay(logs, kvstore):
+    """Self-check of the recorded logs: replayed through a fresh reference
+    BlockPool with the tests' replay harness, every outcome and digest must
+    reproduce (catches a wrongly resolved pin / release argument)."""
+    sys.path.insert(0, str(OUT.parent))
+    import pool_replay as pr
+
+    class RefAdapter:
+        def __init__(self, cap, bs):
+            self.p = kvstore.BlockPool(cap, bs)
+            self.cap_exc = kvstore.CapacityExhausted
+
+        def lookup(self, ns, q, now):
+            m, b = self.p.longest_prefix_match(ns, q, now)
+            return m, [x.block_id for x in b], b
+
+        def insert(self, ns, q, now):
+            b = self.p.insert(ns, q, now)
+            return [x.block_id for x in b], b
+
+        def pin(self, h, now):
+            self.p.pin(h, now)
+
+        def release(self, h):
+            self.p.release(h)
+
+        def concat(self, hs):
+            return [b for h in hs for b in h]
+
+        def counters(self):
+            p = self.p
+            return p.used_blocks, p.eviction_count, p.matched_tokens, p.lookup_tokens
+
+        def rows(self):
+            return sorted((b.block_id, b.namespace, b.token_span, b.parent_id, b.ref_count, b.last_access,
+                           b.child_count) for b in self.p._blocks.values())
+
+        def footprints(self):
+            return self.p.footprint_tokens(), self.p.peak_footprint_tokens()
+    for st in logs:
+        pr.replay(st, RefAdapter, check_digest_every=25)
+
+
 def router_fixtures(core, router):
     rng = random.Random(99)
     models = ["model_a", "model_b", "model_c", "model_d"]
@@ -357,6 +404,34 @@ def router_fixtures(core, router):
                 steps.append({"session": sid, "model": m, "depths": depths, "error": "config"})
         traces.append({"mode": mode.value, "models": models, "steps": steps})
     return traces
+
+
+def sweep_fixtures():
+    """experiment.py's sweep protocol: per-cell workload seeds of both axes
+    and the sweep table of synthetic cells (incl. auto-concurrency cells)."""
+    import dataclasses
+
+    from prefillsim import config as pconfig, experiment
+    cfg = pconfig.load_config("/root/reference/pkg/configs/fast_react.toml")
+    cfg = dataclasses.replace(cfg, run=dataclasses.replace(cfg.run, seed=7))
+    seeds = []
+    for axis, values in (("arrival_rate", [0.5, 1, 2, 4, 8, 16.25]), ("max_concurrent_sessions", [10, 20, 160])):
+        for v in values:
+            c = experiment._cell_config(cfg, axis, v)
+            seeds.append({"axis": axis, "value": v, "seed": str(c.run.seed),
+                          "rate": c.workload.arrival_rate_per_s, "cap": c.run.max_concurrent_sessions})
+    cells, spec = [], []
+    for i, (axis, value, mode, cap, chosen) in enumerate([
+            ("arrival_rate", 4.0, "baseline", 0, 40), ("arrival_rate", 4.0, "prefillshare", 0, 160),
+            ("max_concurrent_sessions", 20, "prefillshare", 20, None),
+            ("max_concurrent_sessions", 160, "baseline", 160, None)]):
+        rep = {"config": {"run": {"max_concurrent_sessions": cap}}, "throughput_tok_per_s": 1234.5678 * (i + 1),
+               "p95_e2e_us": None if i == 3 else 1000 * (i + 7), "mean_ttft_us": None if i == 2 else 12.25 * i,
+               "prefix_hit_ratio": 0.8627450980392157 / (i + 1), "failure_count": i}
+        cells.append(experiment.SweepCell(axis=axis, value=float(value), mode=mode, report=rep, chosen_cap=chosen))
+        spec.append({"axis": axis, "value": value, "mode": mode, "cap": cap, "chosen_cap": chosen, "report": rep})
+    return {"cell_seeds": seeds, "table_cells": spec, "table": experiment.sweep_table(cells),
+            "cap_grid": list(experiment.DEFAULT_CAP_GRID)}
 
 
 def workload_fixtures(wl):
@@ -382,11 +457,15 @@ def main() -> None:
                       separators=(",", ":")).encode()
     (OUT / "pool_streams.json.gz").write_bytes(gzip.compress(blob, 9, mtime=0))
     (OUT / "router_traces.json").write_text(json.dumps(router_fixtures(core, router)))
+    logs = des_call_logs()
+    check_logs_replay(logs, kvstore)
     blob = json.dumps({"generator": "prefillsim.cluster.Simulation + recording prefillsim.kvstore.BlockPool "
-                                    "(configs/fast_react.toml)", "streams": des_call_logs()},
+                                    "(configs/fast_react.toml)", "streams": logs},
                       separators=(",", ":")).encode()
     (OUT / "des_pool_log.json.gz").write_bytes(gzip.compress(blob, 9, mtime=0))
-    (OUT / "workload.json").write_text(json.dumps(workload_fixtures(wl), indent=0))
+    wf = workload_fixtures(wl)
+    wf["sweep"] = sweep_fixtures()
+    (OUT / "workload.json").write_text(json.dumps(wf, indent=0))
     n_ops = sum(len(s["ops"]) for s in pools)
     print(f"pool streams: {len(pools)} ({n_ops} ops); router traces; workload vectors")
 

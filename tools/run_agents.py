@@ -8,6 +8,9 @@ reference's output files: workload.json, report.json, requests.csv, trace.txt
 
     python tools/run_agents.py [--shape 8b|tiny] [--rate 8[,4,...]] [--cap 0[,40,...]]
                                [--duration 20] [--pattern react] [--rows 64] [--out DIR]
+    python tools/run_agents.py --sweep arrival_rate --values 2,4,8 --auto-concurrency [--out DIR]
+        (the reference's sweep protocol, experiment.py: per-cell seeds,
+        best cap of DEFAULT_CAP_GRID per cell, sweep.csv)
 """
 import argparse
 import json
@@ -42,6 +45,14 @@ def main():
     ap.add_argument("--host-tier-blocks", type=int, default=0, help="host staging tier behind the prefix pool")
     ap.add_argument("--max-context", type=int, default=None,
                     help="longest context (default: 4096 for react, 5120 for reflexion: 512 + 12 x (96 + 256))")
+    ap.add_argument("--sweep", default=None, choices=["arrival_rate", "max_concurrent_sessions"],
+                    help="the reference's sweep protocol (experiment.py): one axis, per-cell seeds, sweep.csv")
+    ap.add_argument("--values", default=None, help="sweep axis values, comma-separated")
+    ap.add_argument("--auto-concurrency", action="store_true",
+                    help="arrival_rate sweeps: best cap of DEFAULT_CAP_GRID per cell (throughput)")
+    ap.add_argument("--cap-grid", default=None, help="override DEFAULT_CAP_GRID, comma-separated")
+    ap.add_argument("--initial-prompt-len", type=int, default=None)
+    ap.add_argument("--merged-pool", action="store_true", help="PREFILLSHARE: one merged pool (not the fleet's)")
     a = ap.parse_args()
     max_ctx = a.max_context or (5120 if a.pattern == "reflexion" else 4096)
     cfg = (LlamaConfig.llama8b(max_pos=max_ctx + 512) if a.shape == "8b"
@@ -49,6 +60,8 @@ def main():
     models = list(wl.DEFAULT_MODELS)
     mods = [ModuleWeights(cfg, 100 + i) for i in range(len(models))]
     base = ModuleWeights(cfg, 99, with_head=False)
+    if a.sweep:
+        return run_sweep(a, cfg, models, mods, base, max_ctx)
     for rate in (float(x) for x in a.rate.split(",")):
         for cap in (int(x) for x in a.cap.split(",")):
             sessions = wl.generate(wl.WorkloadConfig(pattern=a.pattern, arrival_rate_per_s=rate,
@@ -64,7 +77,8 @@ def main():
             for mode in (ServingMode(m) for m in a.modes.split(",")):
                 srv = AgentServer(cfg, models, mode, rows_per_module=a.rows, pool_pages_per_worker=a.pool_pages,
                                   max_context=max_ctx, max_output=256, modules=mods, base=base,
-                                  prefill_batch=not a.no_batch, host_tier_blocks=a.host_tier_blocks)
+                                  prefill_batch=not a.no_batch, host_tier_blocks=a.host_tier_blocks,
+                                  merged_pool=a.merged_pool)
                 recs = srv.run(sessions, max_concurrent=cap or None, time_scale=a.time_scale,
                                record_trace=point is not None)
                 out[mode.value] = summarize(recs)
@@ -84,6 +98,48 @@ def main():
                 out["throughput_ratio"] = p["req_per_s"] / b["req_per_s"]
                 out["p95_ratio"] = b["p95_e2e_ms"] / p["p95_e2e_ms"]
             print(json.dumps(out), flush=True)
+
+
+def run_sweep(a, cfg, models, mods, base, max_ctx):
+    """the reference's sweep protocol on the real engine."""
+    from paper_2602_12029_b200 import sweep
+    out = Path(a.out) if a.out else None
+    if out:
+        out.mkdir(parents=True, exist_ok=True)
+
+    def run(sessions, mode, cap):
+        srv = AgentServer(cfg, models, ServingMode(mode), rows_per_module=a.rows, pool_pages_per_worker=a.pool_pages,
+                          max_context=max_ctx, max_output=256, modules=mods, base=base,
+                          prefill_batch=not a.no_batch, merged_pool=a.merged_pool)
+        recs = srv.run(sessions, max_concurrent=cap or None, time_scale=a.time_scale)
+        echo = {"mode": mode, "cap": cap, "shape": a.shape, "rows_per_model": a.rows,
+                "pool_blocks_per_worker": a.pool_pages, "sessions": len(sessions)}
+        rep = build_report(srv, recs, echo)
+        rep["summary"] = summarize(recs)
+        rep["gpu_time"] = srv.gpu_time()
+        line = {"mode": mode, "cap": cap, **{k: rep[k] for k in ("throughput_tok_per_s", "p95_e2e_us", "mean_ttft_us",
+                                                                  "prefix_hit_ratio", "eviction_count",
+                                                                  "failure_count")},
+                "req_per_s": rep["summary"].get("req_per_s")}
+        print(json.dumps(line), flush=True)
+        del srv
+        torch.cuda.empty_cache()
+        return rep
+
+    base_wl = wl.WorkloadConfig(pattern=a.pattern, arrival_rate_per_s=float(a.rate.split(",")[0]),
+                                duration_s=a.duration, initial_prompt_len=a.initial_prompt_len)
+    grid = tuple(int(x) for x in a.cap_grid.split(",")) if a.cap_grid else sweep.DEFAULT_CAP_GRID
+    values = [float(x) if a.sweep == "arrival_rate" else int(x) for x in a.values.split(",")]
+    cells = sweep.run_sweep(run, base_wl, a.seed, a.sweep, values, a.modes.split(","),
+                            auto_concurrency=a.auto_concurrency, cap_grid=grid,
+                            default_cap=int(a.cap.split(",")[0]))
+    table = sweep.sweep_table(cells)
+    print(table, flush=True)
+    if out:
+        (out / "sweep.csv").write_text(table)
+        (out / "cells.jsonl").write_text("".join(json.dumps({"axis": c.axis, "value": c.value, "mode": c.mode,
+                                                             "cap": c.cap, "chosen_cap": c.chosen_cap,
+                                                             "report": c.report}) + "\n" for c in cells))
 
 
 if __name__ == "__main__":
