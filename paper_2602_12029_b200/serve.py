@@ -75,6 +75,7 @@ class _Req:
     ctx: np.ndarray
     output_len: int
     model_idx: int
+    worker: int = 0
 
 
 @dataclass
@@ -83,6 +84,8 @@ class _Row:
     steps: int = 0
     held: list = field(default_factory=list)
     pool: BlockPool | None = None
+    ready: bool = True            # handoff="copy": its context is resident in decode pages
+    dpages: list = field(default_factory=list)
 
 
 class AgentServer:
@@ -90,7 +93,8 @@ class AgentServer:
                  rows_per_module: int = 8, pool_pages_per_worker: int = 2048, max_context: int = 4096,
                  max_output: int = 256, seed: int = 0, device: int = 0,
                  modules: list[ModuleWeights] | None = None, base: ModuleWeights | None = None,
-                 prefill_batch: bool = True, host_tier_blocks: int = 0, merged_pool: bool = False):
+                 prefill_batch: bool = True, host_tier_blocks: int = 0, merged_pool: bool = False,
+                 handoff: str = "pin", decode_capacity_blocks: int = 4500, staging_threshold: float = 0.9):
         self.cfg, self.mode, self.model_ids = cfg, mode, list(model_ids)
         self.prefill_batch = prefill_batch
         self.trace: list[str] | None = None
@@ -116,7 +120,20 @@ class AgentServer:
         per_pool = M * pool_pages_per_worker // n_workers
         self.priv_pages = (max_output + PAGE_TOKENS - 1) // PAGE_TOKENS
         self.R = M * rows_per_module
-        total = n_workers * per_pool + self.R * (1 + self.priv_pages)
+        # handoff="pin": the decode rows read the prefill pool's pages in
+        # place (zero copy on one GPU; the pins last until the request
+        # completes). handoff="copy": the reference's fleet semantics -- the
+        # context moves into its decode worker's own KV budget
+        # (decode_capacity_blocks per model, config.py:40) and the prefill
+        # pins drop at handoff (cluster.py:404-412); a handoff arriving while
+        # the decode worker's resident fraction exceeds staging_threshold
+        # (or that does not fit) is staged in pinned host memory and
+        # reloaded when the budget has room (costs.py:66-83, App. B)
+        if handoff not in ("pin", "copy"):
+            raise ValueError("handoff must be 'pin' or 'copy'")
+        self.handoff = handoff
+        dec_pages = M * decode_capacity_blocks if handoff == "copy" else 0
+        total = n_workers * per_pool + self.R * (1 + self.priv_pages) + dec_pages
         self.kv = KVCache(cfg, total, device)
         # each logical prefill worker owns a disjoint page range of the one cache
         self.pools = []
@@ -149,14 +166,19 @@ class AgentServer:
         self.runner = DecodeRunner(cfg, self.mods, self.kv, self.batch, max_output, device=device)
         self.rows = [_Row() for _ in range(self.R)]
         self.rows_per_module = rows_per_module
+        self.residency = []
+        self._handoffs: list = []
+        self._staged: list[deque] = [deque() for _ in range(M)]
+        if handoff == "copy":
+            from .staging import DecodeResidency
+            first = total - dec_pages
+            self.residency = [DecodeResidency(self.kv, first + m * decode_capacity_blocks, decode_capacity_blocks,
+                                              staging_threshold) for m in range(M)]
         # host staging tier behind the prefix pool(s) (staging.py; 0 = off)
         self.tier = HostKVTier(self.kv, host_tier_blocks) if host_tier_blocks > 0 else None
         self._pending_store: list = []
         self.max_context, self.max_output = max_context, max_output
         self.dev = torch.device("cuda", device)
-        self._sess_len = [0] * self.R
-        self._pages = [[self.tail_page[r]] for r in range(self.R)]
-        self._first = [0] * self.R
 
     # -- helpers -------------------------------------------------------------
 
@@ -178,6 +200,7 @@ class AgentServer:
         module). Returns (held handles, page table, matched tokens,
         prefilled tokens, decode row), or None on CapacityExhausted."""
         worker = self.router.route_prefill(req.rec, self._queue_depths())
+        req.worker = worker
         self._emit(now_us, "PrefillStart", req.session, req.rec.request_id, worker)
         pool = self.pools[worker]
         ns = self.router.prefill_namespace(req.rec.model_id)
@@ -219,7 +242,7 @@ class AgentServer:
         # cluster.py:333-337 / 384-389: the reference's matched / new split;
         # stamped when the forward that computes the request's KV has run on
         # the GPU (immediately when nothing is left to compute)
-        done_info = (req.session, req.rec.request_id, worker, m, n)
+        done_info = (req.session, req.rec.request_id, worker, m, n, self.handoff == "pin")
         if n > pos0:
             ri = 0 if self.base is not None else req.model_idx
             self._pending.append((ri, self._vocab_ids(req.ctx[pos0:]), pos0, pages, done_info))
@@ -245,9 +268,53 @@ class AgentServer:
         return d
 
     def _prefill_done(self, t_us: float, info) -> None:
-        sess, rid, worker, m, n = info
+        sess, rid, worker, m, n, handoff_too = info
         self._emit(t_us, "PrefillComplete", sess, rid, worker, f"matched={m} new={n - m}")
-        self._emit(t_us, "HandoffComplete", sess, rid, worker, f"tokens={n} staged=0")
+        if handoff_too:  # handoff="pin": zero copy, complete with the prefill
+            self._emit(t_us, "HandoffComplete", sess, rid, worker, f"tokens={n} staged=0")
+
+    # -- handoff="copy": decode-side residency and staging --------------------
+
+    def _hand_off(self) -> None:
+        """Move the contexts whose prefill forwards are queued into their
+        decode workers' budgets (K8 page copy, ordered after the forward) or
+        stage them to host memory; drop the prefill pins (cluster.py:404-412)."""
+        for req, row, pages, held, worker in self._handoffs:
+            res = self.residency[req.model_idx]
+            n = len(pages)
+            if n > res.capacity:
+                raise ValueError(f"a {n}-page context exceeds the decode budget of {res.capacity} pages "
+                                 "(decode_capacity_blocks)")
+            if res.must_stage(n):
+                self._staged[req.model_idx].append((req, row, res.stage(pages), n, worker))
+            else:
+                dp = res.take(n)
+                from .transfer import copy_pages
+                copy_pages(self.kv.data.view(self.kv.n_pages, -1), self.kv.data.view(self.kv.n_pages, -1), pages, dp)
+                self._activate(req, row, dp, worker, staged=False)
+            for pool, h in held:
+                pool.release(h)
+            self.rows[row].held = []
+        self._handoffs = []
+
+    def _reload_staged(self) -> None:
+        """Staged contexts back into decode pages, FIFO per decode worker,
+        as its budget frees up."""
+        for m, q in enumerate(self._staged):
+            res = self.residency[m] if self.residency else None
+            while q and res.can_take(q[0][3]):
+                req, row, host, n, worker = q.popleft()
+                dp = res.take(n)
+                res.reload(host, dp)
+                self._activate(req, row, dp, worker, staged=True)
+
+    def _activate(self, req, row, dpages, worker, staged: bool) -> None:
+        r = self.rows[row]
+        r.dpages, r.ready = dpages, True
+        self.batch.update_row(row, len(req.ctx) - 1, dpages, int(req.ctx[-1] % self.cfg.vocab))
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self._inflight.append(("handoff", ev, [(req.session, req.rec.request_id, worker, len(req.ctx), staged)]))
 
     def _flush_prefills(self) -> None:
         """Run the queued forwards: one batched forward per prefill module and
@@ -259,6 +326,8 @@ class AgentServer:
         self._pending, self._pending_slots = [], set()
         if self.tier is not None:
             self.tier.fence()
+        for res in self.residency:  # pending stagings read pages these forwards may overwrite
+            res.fence()
         for ri, seqs in by_runner.items():
             runner = self.prefillers[ri]
             chunk, tot = [], 0
@@ -303,6 +372,9 @@ class AgentServer:
             if item[0] == "prefill":
                 for info in item[2]:
                     self._prefill_done(t, info)
+            elif item[0] == "handoff":
+                for sess, rid, worker, n, staged in item[2]:
+                    self._emit(t, "HandoffComplete", sess, rid, worker, f"tokens={n} staged={int(staged)}")
             else:
                 _, _, first, n_busy, per_model = item
                 for rec in first:
@@ -379,7 +451,6 @@ class AgentServer:
 
         done_sessions = 0
         n_sessions = len(sessions)
-        dirty = False
         while done_sessions < n_sessions:
             t = now_us()
             while arrivals and arrivals[0].arrival_time * time_scale <= t:
@@ -413,16 +484,20 @@ class AgentServer:
                 req.rec.matched, req.rec.prefilled = m, pre
                 r = self.rows[row]
                 r.req, r.steps, r.held = req, 0, held
-                self._sess_len[row] = len(req.ctx) - 1
-                self._pages[row] = pages
-                self._first[row] = int(req.ctx[-1] % self.cfg.vocab)
-                self.batch.update_row(row, len(req.ctx) - 1, pages, self._first[row])
-                dirty = True
+                if self.handoff == "copy":  # moved into decode pages after its forward is queued
+                    r.ready = False
+                    self._handoffs.append((req, row, pages, held, req.worker))
+                else:
+                    self.batch.update_row(row, len(req.ctx) - 1, pages, int(req.ctx[-1] % self.cfg.vocab))
                 progressed = True
             if self._pending:
                 self._flush_prefills()
+            if self._handoffs:
+                self._hand_off()
+            if self.handoff == "copy":
+                self._reload_staged()
             self._poll()
-            busy = [r for r in self.rows if r.req is not None]
+            busy = [r for r in self.rows if r.req is not None and r.ready]
             if busy:
                 ev = self._events("decode")
                 self.runner.graph.replay()
@@ -433,7 +508,7 @@ class AgentServer:
                 first = [r.req.rec for r in busy if r.steps == 0]
                 self._inflight.append(("step", ev[1], first, len(busy), per_model))
                 for idx, r in enumerate(self.rows):
-                    if r.req is None:
+                    if r.req is None or not r.ready:
                         continue
                     r.steps += 1
                     rec = r.req.rec
@@ -446,6 +521,8 @@ class AgentServer:
                                    len(self.model_ids) + r.req.model_idx)
                         for pool, h in r.held:
                             pool.release(h)
+                        if r.dpages:  # handoff="copy": the context leaves the decode budget
+                            self.residency[r.req.model_idx].give(r.dpages)
                         sid = r.req.session
                         spec = spec_of[sid]
                         ctx[sid].extend(wl.synth_tokens(sid, wl.output_slot(step_idx[sid]), r.req.output_len))
@@ -462,6 +539,8 @@ class AgentServer:
                         else:
                             dispatch(sid, rec.done_us)
             elif not progressed:
+                if any(self._staged):
+                    continue  # staged contexts wait for a decode budget that only completions free
                 if arrivals:
                     wait = arrivals[0].arrival_time * time_scale - now_us()
                     if wait > 0:
@@ -518,8 +597,9 @@ def build_report(server: "AgentServer", records: list[RequestRecord], config_ech
     """report.json of a real-engine run in the reference's versioned schema
     (metrics.py:44-80; pool aggregates as cluster.py:232-252): every field is
     the reference's, measured on the GPU in real time (microseconds since the
-    run started) instead of virtual time. staging_handoff_count is 0: one GPU
-    hands off by pinning."""
+    run started) instead of virtual time. staging_handoff_count: handoffs
+    staged through host memory (handoff="copy"; 0 with the zero-copy pin
+    handoff)."""
     end = max([t for t, _ in server.token_completions] + [int(r.done_us or 0) for r in records] + [0])
     done = [r for r in records if r.done_us is not None and not r.failed]
     ttfts = [int(r.first_token_us - r.issue_us) for r in done if r.first_token_us is not None]
@@ -546,7 +626,7 @@ def build_report(server: "AgentServer", records: list[RequestRecord], config_ech
         "request_count": len(records),
         "completed_count": len(done),
         "failure_count": sum(1 for r in records if r.failed),
-        "staging_handoff_count": 0,
+        "staging_handoff_count": sum(r.staged_count for r in getattr(server, "residency", [])),
         "p95_e2e_us": _percentile(e2es, 95) if e2es else None,
         "mean_ttft_us": sum(ttfts) / len(ttfts) if ttfts else None,
         "p95_ttft_us": _percentile(ttfts, 95) if ttfts else None,

@@ -136,3 +136,81 @@ class HostKVTier:
     def stats(self) -> dict:
         return {"capacity_blocks": self.capacity, "resident_blocks": len(self.index.lru), "stored": self.stored,
                 "reloaded": self.reloaded, "key_collisions_rejected": self.index.collisions}
+
+
+class DecodeResidency:
+    """One decode worker's GPU-resident KV budget with staged handoff through
+    pinned host memory: the reference's decode-side accounting
+    (cluster.py:59-75: capacity_tokens = decode_capacity_blocks x block_size,
+    resident fraction) and staging rule (costs.py:66-83, cluster.py:376-394:
+    a handoff arriving while the resident fraction exceeds the staging
+    threshold is staged), with the data movement vLLM actually does
+    (App. B: KV staged in CPU memory, reloaded when the session is
+    scheduled).
+
+    Pages [first, first + capacity) of the KV cache belong to this worker.
+    take / give account the contexts admitted to the decode batch; stage()
+    gathers a context's pages (K8 copy on a side stream, then one D2H into a
+    pinned buffer) and reload() brings it back (one H2D, then a K8 scatter
+    into freshly taken pages). The bytes are moved, not recomputed: reload
+    is bit-exact."""
+
+    def __init__(self, kv: KVCache, first: int, capacity: int, threshold: float = 0.9):
+        from .transfer import PageAllocator
+        self.kv = kv
+        self.pages = kv.data.view(kv.n_pages, -1)
+        self.alloc = PageAllocator(first, capacity)
+        self.capacity, self.threshold = capacity, threshold
+        self.resident = 0
+        self.staged_count = 0
+        self.staged_bytes = 0
+        self.d2h = torch.cuda.Stream(device=kv.data.device)
+
+    def fraction(self) -> float:
+        return self.resident / self.capacity if self.capacity > 0 else 0.0
+
+    def must_stage(self, n: int) -> bool:
+        """cluster.py:379-381 (fraction > threshold), plus: the context does
+        not fit the free budget at all."""
+        return self.fraction() > self.threshold or self.resident + n > self.capacity
+
+    def can_take(self, n: int) -> bool:
+        return self.resident + n <= self.capacity
+
+    def take(self, n: int) -> list[int]:
+        pages = self.alloc.alloc(n)
+        self.resident += n
+        return pages
+
+    def give(self, pages: list[int]) -> None:
+        self.alloc.release(pages)
+        self.resident -= len(pages)
+
+    def stage(self, src_pages: list[int]) -> torch.Tensor:
+        """Context pages -> pinned host buffer (side stream, after the work
+        queued on the current stream that wrote them)."""
+        from .transfer import copy_pages
+        n = len(src_pages)
+        cur = torch.cuda.current_stream(self.kv.data.device)
+        host = torch.empty((n, self.pages.shape[1]), dtype=self.pages.dtype).pin_memory()
+        self.d2h.wait_stream(cur)
+        with torch.cuda.stream(self.d2h):
+            tmp = torch.empty((n, self.pages.shape[1]), dtype=self.pages.dtype, device=self.pages.device)
+            copy_pages(self.pages, tmp, src_pages, list(range(n)))
+            host.copy_(tmp, non_blocking=True)
+        self.staged_count += 1
+        self.staged_bytes += host.numel() * host.element_size()
+        return host
+
+    def reload(self, host: torch.Tensor, pages: list[int]) -> None:
+        """Pinned host buffer -> taken pages, ordered on the current stream
+        after the staging copy."""
+        from .transfer import copy_pages
+        self.fence()
+        tmp = host.to(self.pages.device, non_blocking=True)
+        copy_pages(tmp, self.pages, list(range(len(pages))), pages)
+
+    def fence(self) -> None:
+        """Later work on the current stream (which may overwrite the source
+        pages of a pending stage) waits for the staging copies."""
+        torch.cuda.current_stream(self.kv.data.device).wait_stream(self.d2h)
