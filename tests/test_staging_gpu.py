@@ -95,7 +95,7 @@ def test_decode_residency_stage_reload_bit_exact():
     assert res.resident == 14 and not res.must_stage(5)
 
 
-@pytest.mark.parametrize("capacity", [40, 4096])
+@pytest.mark.parametrize("capacity", [130, 4096])
 def test_agent_server_copy_handoff_with_staging(capacity):
     """handoff="copy" (the reference fleet's decode-side residency): contexts
     move into each decode worker's own budget, prefill pins drop at handoff;
@@ -123,7 +123,7 @@ def test_agent_server_copy_handoff_with_staging(capacity):
     rep = build_report(srv, recs, {"capacity": capacity})
     staged = sum(1 for ln in srv.trace if " HandoffComplete " in ln and ln.endswith("staged=1"))
     assert rep["staging_handoff_count"] == staged
-    if capacity == 40:
+    if capacity == 130:
         assert staged > 0
     else:
         assert staged == 0

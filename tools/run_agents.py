@@ -53,6 +53,10 @@ def main():
     ap.add_argument("--cap-grid", default=None, help="override DEFAULT_CAP_GRID, comma-separated")
     ap.add_argument("--initial-prompt-len", type=int, default=None)
     ap.add_argument("--merged-pool", action="store_true", help="PREFILLSHARE: one merged pool (not the fleet's)")
+    ap.add_argument("--turns", type=int, default=None)
+    ap.add_argument("--handoff", default="pin", choices=["pin", "copy"],
+                    help="copy: decode-side residency budget + staged handoff (the reference fleet)")
+    ap.add_argument("--decode-capacity", type=int, default=4500, help="decode budget per model, blocks")
     a = ap.parse_args()
     max_ctx = a.max_context or (5120 if a.pattern == "reflexion" else 4096)
     cfg = (LlamaConfig.llama8b(max_pos=max_ctx + 512) if a.shape == "8b"
@@ -110,7 +114,8 @@ def run_sweep(a, cfg, models, mods, base, max_ctx):
     def run(sessions, mode, cap):
         srv = AgentServer(cfg, models, ServingMode(mode), rows_per_module=a.rows, pool_pages_per_worker=a.pool_pages,
                           max_context=max_ctx, max_output=256, modules=mods, base=base,
-                          prefill_batch=not a.no_batch, merged_pool=a.merged_pool)
+                          prefill_batch=not a.no_batch, merged_pool=a.merged_pool, handoff=a.handoff,
+                          decode_capacity_blocks=a.decode_capacity)
         recs = srv.run(sessions, max_concurrent=cap or None, time_scale=a.time_scale)
         echo = {"mode": mode, "cap": cap, "shape": a.shape, "rows_per_model": a.rows,
                 "pool_blocks_per_worker": a.pool_pages, "sessions": len(sessions)}
@@ -120,14 +125,15 @@ def run_sweep(a, cfg, models, mods, base, max_ctx):
         line = {"mode": mode, "cap": cap, **{k: rep[k] for k in ("throughput_tok_per_s", "p95_e2e_us", "mean_ttft_us",
                                                                   "prefix_hit_ratio", "eviction_count",
                                                                   "failure_count")},
-                "req_per_s": rep["summary"].get("req_per_s")}
+                "req_per_s": rep["summary"].get("req_per_s"), "staging_handoff_count": rep["staging_handoff_count"],
+                "p95_ttft_us": rep["p95_ttft_us"], "completed": rep["completed_count"]}
         print(json.dumps(line), flush=True)
         del srv
         torch.cuda.empty_cache()
         return rep
 
     base_wl = wl.WorkloadConfig(pattern=a.pattern, arrival_rate_per_s=float(a.rate.split(",")[0]),
-                                duration_s=a.duration, initial_prompt_len=a.initial_prompt_len)
+                                duration_s=a.duration, initial_prompt_len=a.initial_prompt_len, turns=a.turns)
     grid = tuple(int(x) for x in a.cap_grid.split(",")) if a.cap_grid else sweep.DEFAULT_CAP_GRID
     values = [float(x) if a.sweep == "arrival_rate" else int(x) for x in a.values.split(",")]
     cells = sweep.run_sweep(run, base_wl, a.seed, a.sweep, values, a.modes.split(","),
