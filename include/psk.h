@@ -227,8 +227,12 @@ int psk_rope_append(const psk_decode_batch* b, const float* qkv, int32_t n_q_hea
  * end and cut into one equal run per SM (segment partials merged through a
  * per-group CTA directory); it falls back to fixed splits that fit the same
  * workspace for > 32 query rows per KV head or > 64 sessions.
+ * Above 32 query rows per KV head (fan-out) the tcgen05 kernel runs and, when
+ * its CTAs fit one wave, merges the splits itself (no second kernel).
  * q_rot bf16 [n_rows][nq][hd] -> out bf16 [n_rows][nq][hd]. workspace: fp32,
- * psk_decode_attn_workspace() bytes (for the same `splits`). */
+ * psk_decode_attn_workspace() bytes (for the same `splits`); its first
+ * 32 KiB are merge counters that must be zero before the first call (e.g. a
+ * zero-filled allocation); every call leaves them zero. */
 int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int32_t splits,
                               int64_t* bytes);
 int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_heads,

@@ -47,6 +47,7 @@ constexpr int NST = PSK_ATTN_NST;
 constexpr int TILE = PT * HD * 2;       // 4 KiB
 constexpr int STAGE = 2 * TILE;
 constexpr int GMAX = 64;
+constexpr int CNT_INTS = 8192;          // workspace head: fused-merge counters, {arrived, departed} per group
 constexpr int MAXR = 16;                // decode rows per session
 constexpr int OFF_Q = NST * STAGE;
 constexpr int OFF_BAR = OFF_Q + GMAX * 256;  // +16 KiB
@@ -69,6 +70,9 @@ struct Params {
   int* dir;  // stream-K mode (ns == 0): per group {first CTA, last CTA}, then the page total;
              // partial slot of (cta, group) = cta + group
   int sk_grid;  // stream-K: CTAs of the partial kernel
+  unsigned* cnt;  // fan-out kernel, fused merge: per group {arrived, departed}, zero between launches
+  int fused;      // fan-out kernel: the split CTAs merge their group themselves (no merge kernel)
+  int early;      // fan-out kernel: stream shared pages before the PDL wait (PSK_ATTN_EARLY=1)
 };
 
 // SW128 address of (token row, 16-byte chunk c16 in 0..15) in a K/V tile made
@@ -1099,13 +1103,14 @@ __global__ void __launch_bounds__(HD) decode_attn_merge(const __grid_constant__ 
 // 5th-gen tensor cores with the same CTA = (session, kv head, split) work
 // split and the same (m, l, o) partial format, so the merge kernel is shared.
 //   warp 0     TMA producer: 4 pages per 64-key chunk, 6 stages; lane p
-//              loads page p (in parallel): its K tile as two [16 x 64] boxes
-//              so the chunk's K sits as [dims 0-63 x 64 keys][dims 64-127 x
-//              64 keys] (one N=64 MMA per K-step covers the chunk), its V
-//              tile as one 3-D box [half0 | half1]
+//              loads page p (in parallel) as ONE 4-D box, the page's K and V
+//              for this (layer, head): [K|V][dims 0-63 | 64-127][16][64],
+//              8 KiB, 128B-swizzled, pages 8 KiB apart in the stage
 //   warp 1     MMA issuer + TMEM owner. Q and P live in TMEM (A operand
-//              from tensor memory): S_u = Q K^T (M128 N64, 8 MMAs) and
-//              O_u += P_u V_p (M128 N128 K16, one per page)
+//              from tensor memory): S_u = Q K^T as two M128 N32 MMAs per
+//              16-dim K-step whose B rows are the SW128 atoms of the 4 pages
+//              at an 8 KiB stride (tokens 0-7 of pages 0-3, then tokens
+//              8-15), and O_u += P_u V_p (M128 N128 K16, one per page)
 //   warps 2-9  two softmax groups u = 0, 1 taking alternate chunks, with
 //              separate TMEM accumulators O_0, O_1 and separate (m, l): the
 //              tensor core runs one group's MMAs while the other group does
@@ -1116,17 +1121,20 @@ __global__ void __launch_bounds__(HD) decode_attn_merge(const __grid_constant__ 
 // whose lane quarter holds live rows take part in the softmax.
 // TMEM columns: S_0 [0,64) S_1 [64,128) O_0 [128,256) O_1 [256,384)
 //               Q [384,448) (bf16 pairs) P_0 [448,480) P_1 [480,512).
+// S column 32 hh + 8 pp + t holds token 8 hh + t of page pp; P is stored in
+// page order (the PV MMA's K order), a register permutation.
 // (TMA ops cost ~60-80 ns each whatever their size below ~4 KiB, so ops
-// per page bound the stream: 4 per page ~25 GB/s per SM; one 8 KiB box
-// ~47 GB/s. Per-page N=16 S MMAs, which would allow one box per page, cost
-// more in MMA issue than they save: 54 us vs 39 us at 32k x 16 modules.)
+// per page bound the stream: the earlier layout, K as two [16 x 64] 2-D
+// boxes + V as one 3-D box per page so one N=64 MMA covered the chunk, took
+// 3 ops per page; per-page N=16 S MMAs cost more in MMA issue: 54 vs 39 us at
+// 32k x 16 modules.)
 namespace tcv {
 
 constexpr int CPG = 4;                  // pages per chunk
 constexpr int KC = CPG * PT;            // 64 keys
 constexpr int NSTG = 6;
-constexpr int KBYTES = CPG * TILE;      // 16 KiB: [half0 x 4 pages][half1 x 4 pages]
-constexpr int STG = 2 * KBYTES;         // + V 16 KiB: [page][half0 | half1]
+constexpr int PGB = 2 * TILE;           // 8 KiB per page: [K|V][half][16][64]
+constexpr int STG = CPG * PGB;          // 32 KiB per chunk
 constexpr int OFF_ML = NSTG * STG;
 constexpr int OFF_BAR = OFF_ML + 128 * 8;
 constexpr int OFF_PG = OFF_BAR + 256;
@@ -1136,9 +1144,64 @@ constexpr int THREADS = 320;
 constexpr uint32_t T_S = 0, T_O = 128, T_Q = 384, T_P = 448;
 constexpr float RESCALE_LOG2 = 8.f;
 
+// Fused merge of the fan-out kernel: the ns split CTAs of a (session, KV
+// head) group are co-resident (grid <= SMs, 1 CTA per SM), so after
+// publishing its partial each CTA waits for the group's other splits and
+// merges a 1/ns slice of the group's (query row, 4 dims) outputs by
+// log-sum-exp, instead of a second kernel that waits for the whole grid.
+// The last CTA to leave zeroes the group's counters for the next launch.
+__device__ __forceinline__ void fused_merge(const Params& p, int grp_id, int j, int h, int G, const int* s_rows) {
+  unsigned* cnt = p.cnt + 2 * grp_id;
+  const unsigned ns = (unsigned)p.ns;
+  __syncthreads();  // this CTA's partial is written
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(cnt, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+    } while (v < ns);
+    __threadfence();
+  }
+  __syncthreads();
+  const int T = G * (HD / 4);
+  const int t0 = (int)((int64_t)j * T / p.ns), t1 = (int)((int64_t)(j + 1) * T / p.ns);
+  for (int t = t0 + (int)threadIdx.x; t < t1; t += THREADS) {
+    const int g = t >> 5, d4 = (t & 31) * 4;
+    const int64_t base = (int64_t)grp_id * p.ns * GMAX + g;
+    float M = -INFINITY;
+#pragma unroll 8
+    for (int s = 0; s < p.ns; ++s) M = fmaxf(M, __ldcg(p.pm + base + (int64_t)s * GMAX));
+    const float Mr = M == -INFINITY ? 0.f : M;
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 6
+    for (int s = 0; s < p.ns; ++s) {
+      const int64_t sl = base + (int64_t)s * GMAX;
+      const float f = exp2f(__ldcg(p.pm + sl) - Mr);
+      const float4 o = __ldcg(reinterpret_cast<const float4*>(p.po + sl * HD + d4));
+      L += f * __ldcg(p.pl + sl);
+      acc.x += f * o.x;
+      acc.y += f * o.y;
+      acc.z += f * o.z;
+      acc.w += f * o.w;
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    const int qh = h * p.grp + g % p.grp;
+    __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(
+        p.out + ((int64_t)s_rows[g / p.grp] * p.nq + qh) * HD + d4);
+    dst[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+    dst[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(cnt + 1, 1u) == ns - 1) {  // every split has left the wait
+    cnt[0] = 0;
+    cnt[1] = 0;
+  }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
-    decode_attn_tc(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
-                   const __grid_constant__ Params p) {
+    decode_attn_tc(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ Params p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -1195,8 +1258,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     tma::mbar_init(g1_done, 32 * act);
     tma::fence_mbar_init();
-    tma::prefetch_map(&kmap);
-    tma::prefetch_map(&vmap);
+    tma::prefetch_map(&kvmap);
   }
   if (warp == 1) umma::tmem_alloc(&s_tmem, 512);
   __syncthreads();
@@ -1259,76 +1321,79 @@ __global__ void __launch_bounds__(THREADS, 1)
   trace_stamp(2);
 
   if (warp == 0) {
-    if (lane < CPG) {
-      const int pp = lane;
-      bool dep = false;
-      for (int c = 0; c < nch; ++c) {
-        const int st = c % NSTG;
-        tma::mbar_wait(&empty[st], ((c / NSTG) & 1) ^ 1);
-        if (pp == 0) tma::mbar_expect_tx(&full[st], STG);
-        __syncwarp(0xfu);
+    // whole warp, warp-uniform operands, one elected lane issues (no
+    // per-instruction waterfall loops)
+    bool dep = false;
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % NSTG;
+      tma::mbar_wait(&empty[st], ((c / NSTG) & 1) ^ 1);
+      // this step's private pages (and q) come from rope_append; the shared
+      // prompt pages are written by no kernel of the step, so with p.early
+      // they stream before the PDL wait
+      if (!dep && (!p.early || k0 + c * CPG + CPG > s_ps)) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        dep = true;
+      }
+      tma::mbar_expect_tx_e(&full[st], STG);
+#pragma unroll
+      for (int pp = 0; pp < CPG; ++pp) {
         const int j = c * CPG + pp;
         const int jj = j < np ? j : 0;  // past the end: any valid page, masked
-        if (!dep && (k0 + jj >= s_ps || !PSK_ATTN_EARLY)) {  // private page: wait for rope_append
-          asm volatile("griddepcontrol.wait;" ::: "memory");
-          dep = true;
-        }
         int info;
         const int page = jj < MAXP ? s_page[jj] : page_of(jj, info);
         const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
-        unsigned char* kr = smem + st * STG;
-        tma::load_2d(&kmap, &full[st], kr + pp * 2048, 0, row_k);
-        tma::load_2d(&kmap, &full[st], kr + CPG * 2048 + pp * 2048, 64, row_k);
-        tma::load_3d(&vmap, &full[st], kr + KBYTES + pp * TILE, 0, row_k + nkv * PT, 0);
+        tma::load_4d_e(&kvmap, &full[st], smem + st * STG + pp * PGB, 0, row_k, 0, 0);  // K and V, 8 KiB
       }
     }
     trace_stamp(3);
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t ID_S = umma::idesc_bf16(128, KC, false), ID_PV = umma::idesc_bf16(128, HD, true);
-      auto issue_s = [&](int c) {
-        const int u = c & 1;
-        const uint32_t kb = smem_u32(smem + (c % NSTG) * STG);
+    constexpr uint32_t ID_S = umma::idesc_bf16(128, KC / 2, false), ID_PV = umma::idesc_bf16(128, HD, true);
+    auto issue_s = [&](int c) {
+      const int u = c & 1;
+      const uint32_t kb = smem_u32(smem + (c % NSTG) * STG);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma::mma_ts(tmem + T_S + u * KC, tmem + T_Q + kk * 8,
-                       umma::desc_k_sw128(kb + (kk >> 2) * KBYTES / 2) + 2 * (kk & 3), ID_S, kk > 0);
-        umma::commit(&s_full[u]);
-      };
-      auto issue_pv = [&](int c) {
-        const int u = c & 1;
-        const uint32_t vb = smem_u32(smem + (c % NSTG) * STG) + KBYTES;
+      for (int kk = 0; kk < 8; ++kk)
 #pragma unroll
-        for (int pp = 0; pp < CPG; ++pp)
-          umma::mma_ts(tmem + T_O + u * HD, tmem + T_P + u * 32 + pp * 8,
-                       umma::desc_mn_sw128(vb + pp * TILE, 2048), ID_PV, (c >= 2 || pp > 0) ? 1u : 0u);
-        umma::commit(&pv_done[u]);
-        umma::commit(&empty[c % NSTG]);
-      };
-      for (int c = 0; c < nch && c < 2; ++c) {
-        tma::mbar_wait(&full[c], 0);
+        for (int hh = 0; hh < 2; ++hh)  // tokens 8 hh .. 8 hh + 7 of the 4 pages
+          umma::mma_ts_e(tmem + T_S + u * KC + hh * (KC / 2), tmem + T_Q + kk * 8,
+                         umma::desc_k_sw128_sbo(kb + (kk >> 2) * 2048 + hh * 1024, PGB) + 2 * (kk & 3), ID_S,
+                         kk > 0);
+      umma::commit_e(&s_full[u]);
+    };
+    auto issue_pv = [&](int c) {
+      const int u = c & 1;
+      const uint32_t vb = smem_u32(smem + (c % NSTG) * STG) + TILE;
+#pragma unroll
+      for (int pp = 0; pp < CPG; ++pp)
+        umma::mma_ts_e(tmem + T_O + u * HD, tmem + T_P + u * 32 + pp * 8, umma::desc_mn_sw128(vb + pp * PGB, 2048),
+                       ID_PV, (c >= 2 || pp > 0) ? 1u : 0u);
+      umma::commit_e(&pv_done[u]);
+      umma::commit_e(&empty[c % NSTG]);
+    };
+    for (int c = 0; c < nch && c < 2; ++c) {
+      tma::mbar_wait(&full[c], 0);
+      umma::fence_after();
+      issue_s(c);
+    }
+    for (int c = 0; c < nch; ++c) {
+      // S_u(c+2) as soon as softmax(c) has S_u(c) in registers, so it runs
+      // under that softmax; then PV_u(c) once P_u(c) is in TMEM
+      if (c + 2 < nch) {
+        tma::mbar_wait(&s_free[c & 1], (c >> 1) & 1);
+        tma::mbar_wait(&full[(c + 2) % NSTG], ((c + 2) / NSTG) & 1);
         umma::fence_after();
-        issue_s(c);
+        issue_s(c + 2);
       }
-      for (int c = 0; c < nch; ++c) {
-        // S_u(c+2) as soon as softmax(c) has S_u(c) in registers, so it runs
-        // under that softmax; then PV_u(c) once P_u(c) is in TMEM
-        if (c + 2 < nch) {
-          tma::mbar_wait(&s_free[c & 1], (c >> 1) & 1);
-          tma::mbar_wait(&full[(c + 2) % NSTG], ((c + 2) / NSTG) & 1);
-          umma::fence_after();
-          issue_s(c + 2);
-        }
-        tma::mbar_wait(&p_full[c & 1], (c >> 1) & 1);  // P_u(c) in TMEM, O_u settled
-        umma::fence_after();
-        issue_pv(c);
-      }
+      tma::mbar_wait(&p_full[c & 1], (c >> 1) & 1);  // P_u(c) in TMEM, O_u settled
+      umma::fence_after();
+      issue_pv(c);
     }
   } else if ((warp & 3) < act) {
     // Softmax warp: TMEM lane quarter q4, its 16 live lanes read with the
     // 16-lane shapes so all 32 threads work: thread t owns query rows
-    // gA = 16 q4 + t/4 and gB = gA + 8, keys 8i + 2(t%4) + {0,1} of the
-    // chunk (i = 0..7); the 4 threads of a row reduce with two shuffles.
+    // gA = 16 q4 + t/4 and gB = gA + 8, S columns 8i + 2(t%4) + {0,1}
+    // (i = 0..7) = tokens 8 (i / 4) + 2(t%4) + {0,1} of page i % 4; the 4
+    // threads of a row reduce with two shuffles.
     const int u = (warp - 2) >> 2;  // softmax group
     const int q4 = warp & 3;        // TMEM lane quarter
     const int t0 = lane & 3;
@@ -1370,12 +1435,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (!full) {  // warp-uniform: partial / private / past-the-end pages
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int inf = info[i >> 1];
+          const int inf = info[i & 3];
           const int own = (inf >> 8) - 1, lim = inf & 0xff;
           const bool okA = own < 0 || own == riA, okB = own < 0 || own == riB;
 #pragma unroll
           for (int b = 0; b < 2; ++b) {
-            const int e = 8 * (i & 1) + 2 * t0 + b;
+            const int e = 8 * (i >> 2) + 2 * t0 + b;
             if (!(okA && e < lim)) xa[2 * i + b] = -INFINITY;
             if (!(okB && e < lim)) xb[2 * i + b] = -INFINITY;
           }
@@ -1441,11 +1506,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       float sa[8], sb[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float a0 = fast_exp2(fmaf(xa[2 * i], sc, -bA)), a1 = fast_exp2(fmaf(xa[2 * i + 1], sc, -bA));
-        const float b0 = fast_exp2(fmaf(xb[2 * i], sc, -bB)), b1 = fast_exp2(fmaf(xb[2 * i + 1], sc, -bB));
+        // P pair column 4i + t0 = tokens 8 (i & 1) + 2 t0 + {0,1} of page i / 2 = S group 4 (i & 1) + i / 2
+        const int k = 4 * (i & 1) + (i >> 1);
+        const float a0 = fast_exp2(fmaf(xa[2 * k], sc, -bA)), a1 = fast_exp2(fmaf(xa[2 * k + 1], sc, -bA));
+        const float b0 = fast_exp2(fmaf(xb[2 * k], sc, -bB)), b1 = fast_exp2(fmaf(xb[2 * k + 1], sc, -bB));
         sa[i] = a0 + a1;
         sb[i] = b0 + b1;
-        pk[2 * i] = pack_bf16(a0, a1);      // row A, P column 4i + t0 = keys 8i + 2 t0 + {0,1}
+        pk[2 * i] = pack_bf16(a0, a1);      // row A
         pk[2 * i + 1] = pack_bf16(b0, b1);  // row B
       }
       umma::st16x128b_x8(tP, pk);
@@ -1541,6 +1608,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     umma::fence_after();
     umma::tmem_dealloc(tmem, 512);
   }
+  if (p.fused) fused_merge(p, sess * nkv + h, j_split, h, G, s_rows);
 }
 
 }  // namespace tcv
@@ -1651,7 +1719,10 @@ int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int
                               int64_t* bytes) {
   PSK_CHECK_ARG(b && bytes && splits >= 0, "psk_decode_attn_workspace: bad args");
   const int64_t groups = (int64_t)b->n_sess * n_kv_heads;
-  *bytes = ws_slots(b, n_kv_heads, splits) * GMAX * (HD + 2) * 4 + groups * 2 * 4 + 16;
+  // fan-out merge counters at a fixed offset (zero before the first launch,
+  // left zero by every launch, so one workspace serves any batch shape) |
+  // partials | CTA directory (+ page total)
+  *bytes = CNT_INTS * 4 + ws_slots(b, n_kv_heads, splits) * GMAX * (HD + 2) * 4 + groups * 2 * 4 + 16;
   return PSK_OK;
 }
 
@@ -1705,9 +1776,8 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
     if (hsplit > hmax) hsplit = (int)hmax;
     if (force > 0 && force <= hmax && b->n_sess * force <= 8 * (int64_t)sms) hsplit = force;
   }
-  CUtensorMap map, vmap;
-  int rc = psk::kv_tensor_map(kv, &map, use_tc ? psk::KV_BOX2D : (use_heads ? psk::KV_PAGE4D_ALL : psk::KV_PAGE4D));
-  if (!rc && use_tc) rc = psk::kv_tensor_map(kv, &vmap, psk::KV_TILE3D);
+  CUtensorMap map;
+  const int rc = psk::kv_tensor_map(kv, &map, use_heads ? psk::KV_PAGE4D_ALL : psk::KV_PAGE4D);
   if (rc) return rc;
   Params p;
   p.b = *b;
@@ -1720,12 +1790,19 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   p.ns = stream_k ? 0 : (use_heads ? hsplit : splits);
   // CTAs of the partial kernel
   const int64_t items = stream_k ? sms : (use_heads ? (int64_t)b->n_sess * hsplit : groups * splits);
-  float* ws = reinterpret_cast<float*>(workspace);
+  p.cnt = reinterpret_cast<unsigned*>(workspace);
+  float* ws = reinterpret_cast<float*>(workspace) + CNT_INTS;
   p.pm = ws;
   p.pl = ws + slots * GMAX;
   p.po = ws + 2 * slots * GMAX;
   p.dir = reinterpret_cast<int*>(ws + slots * GMAX * (HD + 2));
   p.sk_grid = sms;
+  // fan-out kernel: merge inside the partial kernel when every CTA is
+  // co-resident (one CTA per SM); PSK_ATTN_MERGE_KERNEL=1 keeps the kernel
+  static const bool merge_kernel = getenv("PSK_ATTN_MERGE_KERNEL") != nullptr;
+  p.fused = use_tc && !merge_kernel && items <= psk::device_sms() && 2 * groups <= CNT_INTS;
+  static const bool early = getenv("PSK_ATTN_EARLY") != nullptr;
+  p.early = early;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
   cudaStream_t s = psk::as_stream(stream);
   static bool init = false;
@@ -1754,7 +1831,7 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
     }
     cfg.blockDim = dim3(tcv::THREADS);
     cfg.dynamicSmemBytes = tcv::SMEM;
-    PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tcv::decode_attn_tc, map, vmap, p));
+    PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tcv::decode_attn_tc, map, p));
   } else if (stream_k) {
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = sk::SMEM;
@@ -1775,6 +1852,7 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
     psk::trace_report("decode_attn", (int)items, 5, names);
     psk::trace_disarm();
   }
+  if (p.fused) return PSK_OK;
   cudaLaunchConfig_t mcfg = {};
   mcfg.gridDim = dim3(b->n_rows, n_q_heads);
   mcfg.blockDim = dim3(HD);

@@ -447,8 +447,15 @@ __global__ void __launch_bounds__(THREADS_TC, 1)
 //               TMEM lane): one pass over S (64 fp32 from TMEM), exp2 with
 //               a lazily updated base max (O in TMEM is rescaled only when
 //               the row max grows by > 2^8; the final 1/l makes it exact),
-//               P (bf16) -> shared memory in the UMMA K-major layout
-// TMEM columns: S0 [0,64) S1 [64,128) O0 [128,256) O1 [256,384).
+//               P (bf16) -> TMEM, double-buffered per tile, so softmax(c+1)
+//               never waits for PV(c); the PV MMA takes P as its A operand
+//               from tensor memory (P_SMEM: P -> shared memory in the UMMA
+//               K-major layout, one buffer per tile, the round-1 kernel)
+// TMEM columns: S0 [0,64) S1 [64,128) O0 [128,256) O1 [256,384)
+//               P[tile][buffer] [384 + 32 (2 tile + buffer), +32) (bf16 pairs).
+// The producer and MMA warps run warp-converged (all 32 lanes, warp-uniform
+// operands, one elected lane issues): from an if (lane == 0) branch the
+// compiler wraps every TMA / MMA in an R2UR.BROADCAST waterfall loop.
 #ifndef PP_EMU
 // K3 softmax: exponentials per 8 computed on the FMA pipe (exp2_fma). Off:
 // alternating A/B at 4k (tools/ab_prefill.sh) measured 188 us/layer with 0,
@@ -473,15 +480,19 @@ constexpr int OFF_PG = OFF_BAR + 256;
 constexpr int SMEM = OFF_PG + MAXPG * 4 + 1024;
 constexpr int THREADS = 320;
 constexpr float RESCALE_LOG2 = 8.f;      // lazy-rescale threshold (log2 units)
+constexpr uint32_t T_P = 384;            // P buffers in TMEM (P_SMEM = false)
 
+template <bool P_SMEM>
 __global__ void __launch_bounds__(THREADS, 1)
     prefill_attn_pp(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ tc::TcParams p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  // pv_done[2 t + b]: PV_t of the chunks c with c % 2 == b (P buffer b);
+  // P_SMEM uses b = 0 only
   uint64_t *full = bars, *empty = bars + NSTG, *s_full = bars + 2 * NSTG, *p_full = s_full + 2,
-           *pv_done = p_full + 2, *s_free = pv_done + 2;
+           *pv_done = p_full + 2, *s_free = pv_done + 4;
   int* s_pg = reinterpret_cast<int*>(smem + OFF_PG);
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -517,7 +528,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       tma::mbar_init(&s_full[t], 1);
       tma::mbar_init(&s_free[t], 128);
       tma::mbar_init(&p_full[t], 128);
-      tma::mbar_init(&pv_done[t], 1);
+      tma::mbar_init(&pv_done[2 * t], 1);
+      tma::mbar_init(&pv_done[2 * t + 1], 1);
     }
     tma::fence_mbar_init();
     tma::prefetch_map(&kvmap);
@@ -549,68 +561,75 @@ __global__ void __launch_bounds__(THREADS, 1)
   psk::pdl_trigger();
 
   if (warp == 0) {
-    if (lane == 0) {
-      for (int c = 0; c < nch; ++c) {
-        const int st = c % NSTG;
-        tma::mbar_wait(&empty[st], ((c / NSTG) & 1) ^ 1);
-        tma::mbar_expect_tx(&full[st], STG);
-        unsigned char* kr = smem + st * STG;
-        unsigned char* vr = kr + KBYTES;
-        for (int pp = 0; pp < CPG; ++pp) {
-          const int j = c * CPG + pp;
-          const int jj = j < n_pages ? j : c * CPG;  // past the end: any valid page, masked
-          const int page = jj < MAXPG ? s_pg[jj] : pages[jj];
-          const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
-          const int row_v = row_k + nkv * PT;
-          tma::load_2d(&kvmap, &full[st], kr + pp * 2048, 0, row_k);
-          tma::load_2d(&kvmap, &full[st], kr + CPG * 2048 + pp * 2048, 64, row_k);
-          tma::load_2d(&kvmap, &full[st], vr + pp * TILE, 0, row_v);
-          tma::load_2d(&kvmap, &full[st], vr + pp * TILE + 2048, 64, row_v);
-        }
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % NSTG;
+      tma::mbar_wait(&empty[st], ((c / NSTG) & 1) ^ 1);
+      tma::mbar_expect_tx_e(&full[st], STG);
+      unsigned char* kr = smem + st * STG;
+      unsigned char* vr = kr + KBYTES;
+#pragma unroll
+      for (int pp = 0; pp < CPG; ++pp) {
+        const int j = c * CPG + pp;
+        const int jj = j < n_pages ? j : c * CPG;  // past the end: any valid page, masked
+        const int page = jj < MAXPG ? s_pg[jj] : pages[jj];
+        const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
+        const int row_v = row_k + nkv * PT;
+        tma::load_2d_e(&kvmap, &full[st], kr + pp * 2048, 0, row_k);
+        tma::load_2d_e(&kvmap, &full[st], kr + CPG * 2048 + pp * 2048, 64, row_k);
+        tma::load_2d_e(&kvmap, &full[st], vr + pp * TILE, 0, row_v);
+        tma::load_2d_e(&kvmap, &full[st], vr + pp * TILE + 2048, 64, row_v);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t ID_S = umma::idesc_bf16(128, KC, false), ID_PV = umma::idesc_bf16(128, HD, true);
-      auto issue_s = [&](int t, int c) {
-        const uint32_t kr = smem_u32(smem + (c % NSTG) * STG);
-        const uint32_t qt = sq + t * QBYTES;
+    constexpr uint32_t ID_S = umma::idesc_bf16(128, KC, false), ID_PV = umma::idesc_bf16(128, HD, true);
+    auto issue_s = [&](int t, int c) {
+      const uint32_t kr = smem_u32(smem + (c % NSTG) * STG);
+      const uint32_t qt = sq + t * QBYTES;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma::mma(tmem + t * KC, umma::desc_k_sw128(qt + (kk >> 2) * 16384) + 2 * (kk & 3),
+      for (int kk = 0; kk < 8; ++kk)
+        umma::mma_e(tmem + t * KC, umma::desc_k_sw128(qt + (kk >> 2) * 16384) + 2 * (kk & 3),
                     umma::desc_k_sw128(kr + (kk >> 2) * (CPG * 2048)) + 2 * (kk & 3), ID_S, kk > 0);
-        umma::commit(&s_full[t]);
-      };
-      auto issue_pv = [&](int t, int c) {
-        const uint32_t vr = smem_u32(smem + (c % NSTG) * STG) + KBYTES;
+      umma::commit_e(&s_full[t]);
+    };
+    auto issue_pv = [&](int t, int c) {
+      const uint32_t vr = smem_u32(smem + (c % NSTG) * STG) + KBYTES;
+      if (P_SMEM) {
         const uint32_t pt = sp + t * PBYTES;
 #pragma unroll
         for (int pp = 0; pp < CPG; ++pp)
-          umma::mma(tmem + 128 + t * HD, umma::desc_k_sw128(pt) + 2 * pp,
-                    umma::desc_mn_sw128(vr + pp * TILE, 2048), ID_PV, (c > 0 || pp > 0) ? 1u : 0u);
-        umma::commit(&pv_done[t]);
-      };
-      tma::mbar_wait(&full[0], 0);
-      umma::fence_after();
-      issue_s(0, 0);
-      issue_s(1, 0);
-      for (int c = 0; c < nch; ++c) {
-        const bool more = c + 1 < nch;
-        if (more) tma::mbar_wait(&full[(c + 1) % NSTG], ((c + 1) / NSTG) & 1);
-        for (int t = 0; t < 2; ++t) {
-          // S_t(c+1) as soon as softmax(c) holds S_t(c) in registers (it runs
-          // under that softmax), PV_t(c) once P_t(c) is written
-          if (more) {
-            tma::mbar_wait(&s_free[t], c & 1);
-            umma::fence_after();
-            issue_s(t, c + 1);
-          }
-          tma::mbar_wait(&p_full[t], c & 1);  // P_t(c) written, O_t settled
-          umma::fence_after();
-          issue_pv(t, c);
-        }
-        umma::commit(&empty[c % NSTG]);  // K/V stage free once both PVs completed
+          umma::mma_e(tmem + 128 + t * HD, umma::desc_k_sw128(pt) + 2 * pp,
+                      umma::desc_mn_sw128(vr + pp * TILE, 2048), ID_PV, (c > 0 || pp > 0) ? 1u : 0u);
+        umma::commit_e(&pv_done[2 * t]);
+      } else {
+        const uint32_t pt = tmem + T_P + (2 * t + (c & 1)) * (KC / 2);
+#pragma unroll
+        for (int pp = 0; pp < CPG; ++pp)
+          umma::mma_ts_e(tmem + 128 + t * HD, pt + pp * 8, umma::desc_mn_sw128(vr + pp * TILE, 2048), ID_PV,
+                         (c > 0 || pp > 0) ? 1u : 0u);
+        umma::commit_e(&pv_done[2 * t + (c & 1)]);
       }
+    };
+    tma::mbar_wait(&full[0], 0);
+    umma::fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    for (int c = 0; c < nch; ++c) {
+      const bool more = c + 1 < nch;
+      if (more) tma::mbar_wait(&full[(c + 1) % NSTG], ((c + 1) / NSTG) & 1);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        // S_t(c+1) as soon as softmax(c) holds S_t(c) in registers (it runs
+        // under that softmax), PV_t(c) once P_t(c) is written
+        if (more) {
+          tma::mbar_wait(&s_free[t], c & 1);
+          umma::fence_after();
+          issue_s(t, c + 1);
+        }
+        tma::mbar_wait(&p_full[t], c & 1);  // P_t(c) written, O_t settled
+        umma::fence_after();
+        issue_pv(t, c);
+      }
+      umma::commit_e(&empty[c % NSTG]);  // K/V stage free once both PVs completed
     }
   } else {
     const int t = (warp - 2) >> 2;   // tile
@@ -620,6 +639,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tS = tmem + ((uint32_t)lq << 16) + t * KC;
     const uint32_t tO = tmem + ((uint32_t)lq << 16) + 128 + t * HD;
     const uint32_t prow = sp + t * PBYTES + g * 128;
+    const uint32_t tP = tmem + ((uint32_t)lq << 16) + T_P;
     const int qpos = pos0 + t0 + r / p.grp;  // keys [0, qpos] visible
     float m_used = -INFINITY, l = 0.f;
     for (int c = 0; c < nch; ++c) {
@@ -647,10 +667,17 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int k = 0; k < w; ++k) tm[k] = fmaxf(tm[k], tm[k + w]);
       const float mx = tm[0] * p.scale_log2;
-      // PV_t(c-1) must be done before P_t is overwritten or O_t rescaled
-      if (c > 0) tma::mbar_wait(&pv_done[t], (c - 1) & 1);
+      // P_SMEM: PV_t(c-1) must be done before P_t is overwritten or O_t
+      // rescaled. TMEM P: PV_t(c-2) before P buffer c % 2 is overwritten,
+      // PV_t(c-1) only before a rescale of O_t.
+      if (P_SMEM) {
+        if (c > 0) tma::mbar_wait(&pv_done[2 * t], (c - 1) & 1);
+      } else if (c > 1) {
+        tma::mbar_wait(&pv_done[2 * t + (c & 1)], ((c >> 1) - 1) & 1);
+      }
       const bool grow = mx > m_used + RESCALE_LOG2 || (m_used == -INFINITY && mx > -INFINITY);
       if (__any_sync(0xffffffffu, grow && c > 0)) {
+        if (!P_SMEM) tma::mbar_wait(&pv_done[2 * t + ((c - 1) & 1)], ((c - 1) >> 1) & 1);
         umma::fence_after();
         const float alpha = grow ? exp2f(m_used - mx) : 1.f;
 #pragma unroll 1
@@ -668,6 +695,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (grow) m_used = mx;
       const float base = m_used == -INFINITY ? 0.f : m_used;
       float ls[KC / 8];
+      uint32_t pk[KC / 2];
 #pragma unroll
       for (int q = 0; q < KC / 8; ++q) {
         float pf[8];
@@ -679,16 +707,31 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         ls[q] = ((pf[0] + pf[1]) + (pf[2] + pf[3])) + ((pf[4] + pf[5]) + (pf[6] + pf[7]));
         const uint4 v = f32_to_bf16x8(pf);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(prow + (((q ^ (g & 7))) << 4)), "r"(v.x),
-                     "r"(v.y), "r"(v.z), "r"(v.w));
+        if (P_SMEM) {
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(prow + (((q ^ (g & 7))) << 4)), "r"(v.x),
+                       "r"(v.y), "r"(v.z), "r"(v.w));
+        } else {
+          pk[4 * q] = v.x;
+          pk[4 * q + 1] = v.y;
+          pk[4 * q + 2] = v.z;
+          pk[4 * q + 3] = v.w;
+        }
       }
       l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
-      umma::fence_proxy_async();
+      if (P_SMEM) {
+        umma::fence_proxy_async();
+      } else {
+        umma::st32(tP + (2 * t + (c & 1)) * (KC / 2), pk);
+        umma::wait_st();
+      }
       umma::fence_before();
       tma::mbar_arrive(&p_full[t]);
     }
     // epilogue: O_t / l -> bf16 rows of the output
-    tma::mbar_wait(&pv_done[t], (nch - 1) & 1);
+    if (P_SMEM)
+      tma::mbar_wait(&pv_done[2 * t], (nch - 1) & 1);
+    else
+      tma::mbar_wait(&pv_done[2 * t + ((nch - 1) & 1)], ((nch - 1) >> 1) & 1);
     umma::fence_after();
     const int tpos = t0 + r / p.grp;
     const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -715,6 +758,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     umma::fence_after();
     umma::tmem_dealloc(tmem, 512);
   }
+}
+
+typedef void (*KernelFn)(const CUtensorMap, const tc::TcParams);
+
+// The K3 variant in use (PSK_PREFILL_PSMEM=1: P through shared memory), its
+// shared-memory attribute set once.
+static KernelFn kernel() {
+  static KernelFn fn = nullptr;
+  if (!fn) {
+    const KernelFn f = getenv("PSK_PREFILL_PSMEM") ? prefill_attn_pp<true> : prefill_attn_pp<false>;
+    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess) return f;
+    fn = f;
+  }
+  return fn;
 }
 
 }  // namespace pp
@@ -777,13 +834,7 @@ int psk_prefill_attn(const void* q_rot, int32_t T, int32_t pos0, int32_t n_q_hea
     if (!tc1) {
       t.qb = 256 / grp;
       t.n_qblocks = (T + t.qb - 1) / t.qb;
-      static bool pp_attr = false;
-      if (!pp_attr) {
-        PSK_CUDA_TRY(cudaFuncSetAttribute(pp::prefill_attn_pp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          pp::SMEM));
-        pp_attr = true;
-      }
-      PSK_CUDA_TRY(psk::launch_pdl(pp::prefill_attn_pp, dim3(t.n_qblocks * kv.n_kv_heads), dim3(pp::THREADS),
+      PSK_CUDA_TRY(psk::launch_pdl(pp::kernel(), dim3(t.n_qblocks * kv.n_kv_heads), dim3(pp::THREADS),
                                    (size_t)pp::SMEM, psk::as_stream(stream), map, t));
       PSK_LAUNCH_CHECK();
       return PSK_OK;
@@ -835,12 +886,7 @@ int psk_prefill_attn_batch(const void* q_rot, int32_t n_items, const int32_t* it
   t.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
   t.qb = 256 / grp;
   t.items = items;
-  static bool pp_attr = false;
-  if (!pp_attr) {
-    PSK_CUDA_TRY(cudaFuncSetAttribute(pp::prefill_attn_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, pp::SMEM));
-    pp_attr = true;
-  }
-  PSK_CUDA_TRY(psk::launch_pdl(pp::prefill_attn_pp, dim3(n_items * kv.n_kv_heads), dim3(pp::THREADS),
+  PSK_CUDA_TRY(psk::launch_pdl(pp::kernel(), dim3(n_items * kv.n_kv_heads), dim3(pp::THREADS),
                                (size_t)pp::SMEM, psk::as_stream(stream), map, t));
   PSK_LAUNCH_CHECK();
   return PSK_OK;

@@ -68,6 +68,38 @@ __device__ __forceinline__ void load_4d(const CUtensorMap* map, uint64_t* bar, v
       : "memory");
 }
 
+// Warp-converged issue: the whole warp executes these with warp-uniform
+// operands and one elected lane issues. The operands then stay in uniform
+// registers; issuing from a lane-divergent branch (if (lane == 0)) makes the
+// compiler wrap every TMA / MMA in an R2UR.BROADCAST waterfall loop (~60
+// cycles per instruction).
+__device__ __forceinline__ void mbar_expect_tx_e(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(sa(bar)),
+      "r"(bytes)
+      : "memory");
+}
+
+__device__ __forceinline__ void load_2d_e(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];\n}\n" ::"r"(sa(dst)),
+      "l"(map), "r"(sa(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void load_4d_e(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                                          int c3) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2];\n}\n" ::"r"(sa(dst)),
+      "l"(map), "r"(sa(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }

@@ -12,7 +12,8 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0, dirty_ws=False, ramp=False):
+def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0, dirty_ws=False, ramp=False, reps=1,
+          ws=None):
     from paper_2602_12029_b200 import _lib
     from paper_2602_12029_b200.model import (DecodeBatch, DecodeRow, KVCache, LlamaConfig,
                                              SessionSpec)
@@ -50,11 +51,14 @@ def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0, dirty_ws
     lib = _lib.load()
     wsb = ctypes.c_int64()
     _lib.check(lib.psk_decode_attn_workspace(b.c_ref(), nkv, splits, ctypes.byref(wsb)))
-    ws = torch.zeros(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
+    if ws is None or ws.numel() * 4 < wsb.value:
+        ws = torch.zeros(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
     if dirty_ws:  # stale partials / directory from earlier launches must not leak in
-        ws.uniform_(-50.0, 50.0)
-    _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), nq, layer, kv.layout(), splits,
-                                   ws.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        ws[8192:].uniform_(-50.0, 50.0)  # the leading 32 KiB of merge counters stay zero (API contract)
+    for _ in range(reps):  # repeated launches reuse the workspace (fused-merge counters reset)
+        out.fill_(float("nan"))
+        _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), nq, layer, kv.layout(), splits,
+                                       ws.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     grp = nq // nkv
     for j, row in enumerate(b.rows):
@@ -69,6 +73,7 @@ def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0, dirty_ws
         ref = (torch.softmax(sc, -1).unsqueeze(1) @ Vq).squeeze(1)
         err = (out[j].float() - ref).abs().max().item()
         assert err <= 2e-2 * ref.abs().max().item() + 2e-3, f"row {j}: err {err}"
+    return ws
 
 
 @pytest.mark.parametrize("splits", [1, 3, 8, 37, 64])
@@ -87,6 +92,17 @@ def test_fanout_tcgen05_shapes(mods, splits):
     shared length ending mid-page, several split counts (incl. splits whose
     last 8-page chunk is partial)."""
     _case(32, 8, [1333], [mods], [(i * 37) % 200 for i in range(mods)], splits, seed=mods)
+
+
+def test_fanout_fused_merge_reuse():
+    """The fan-out kernel's in-kernel merge (one wave of split CTAs): three
+    launches on one workspace, then other split counts / groups on the same
+    workspace with stale partials; the group counters must come back to zero
+    after every launch."""
+    ws = _case(32, 8, [2000], [16], [i * 3 for i in range(16)], 18, seed=5, reps=3)
+    ws = _case(32, 8, [900], [16], [i for i in range(16)], 7, seed=6, reps=2, ws=ws, dirty_ws=True)
+    ws = _case(32, 8, [300, 77], [16, 9], [i % 20 for i in range(25)], 9, seed=7, reps=2, ws=ws)
+    assert ws[:8192].abs().sum().item() == 0.0
 
 
 def test_fanout_two_sessions_tcgen05():

@@ -17,15 +17,23 @@ from paper_2602_12029_b200 import _lib  # noqa: E402
 from paper_2602_12029_b200.model import KVCache, LlamaConfig, ModuleWeights, PrefillRunner  # noqa: E402
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+import os  # noqa: E402
+if os.environ.get("PSK_SEED") is not None:  # fixed prompt / queries (A/B runs)
+    torch.manual_seed(int(os.environ["PSK_SEED"]))
 cfg = LlamaConfig.llama8b(max_pos=T + 64)
 base = ModuleWeights(cfg, 3, with_head=False)
 kv = KVCache(cfg, T // 16 + 8)
 pre = PrefillRunner(cfg, base, kv, max_tokens=T)
 toks = torch.randint(0, cfg.vocab, (T,), device="cuda")
 pt = torch.arange(T // 16 + 1, dtype=torch.int32, device="cuda")
-dt = bench._time_launches(lambda: pre.run(toks, 0, pt), 3)
-fl = pre.flops(T)
-print(f"prefill T={T}: {dt * 1e3:.2f} ms  {fl / dt / 1e12:.1f} TFLOP/s")
+if "attnonly" in sys.argv[2:]:  # K3 alone: fill the KV once, no whole-prefill timing (power state)
+    pre.run(toks, 0, pt)
+    torch.cuda.synchronize()
+    dt = None
+else:
+    dt = bench._time_launches(lambda: pre.run(toks, 0, pt), 3)
+    fl = pre.flops(T)
+    print(f"prefill T={T}: {dt * 1e3:.2f} ms  {fl / dt / 1e12:.1f} TFLOP/s")
 if "quick" in sys.argv[2:]:
     sys.exit(0)
 if "batch" in sys.argv[2:]:  # G sequences of T tokens: G x run() vs one run_batch()
@@ -57,10 +65,34 @@ def attn():
     it[0] += 1
 
 
-da = bench._time_launches(attn, 16)
+import threading  # noqa: E402
+clocks, stop = [], threading.Event()
+
+
+def _poll():
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        hnd = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        while not stop.is_set():
+            clocks.append(pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM))
+            stop.wait(0.005)
+    except Exception:  # noqa: BLE001
+        pass
+
+
+th = threading.Thread(target=_poll, daemon=True)
+th.start()
+reps = 5 if "attnonly" in sys.argv[2:] else 1
+das = [bench._time_launches(attn, 64 if reps > 1 else 16) for _ in range(reps)]
+stop.set()
+th.join()
+da = min(das)
 afl = 4 * cfg.n_heads * cfg.head_dim * (T * (T + 1) / 2)  # QK^T + PV over the causal triangle
-print(f"prefill attention T={T}: {da * 1e6:.1f} us/layer  {afl / da / 1e12:.1f} TFLOP/s (causal flops)")
-if "attn" in sys.argv[2:]:
+clk = sorted(clocks)[len(clocks) // 2] if clocks else -1  # median SM clock while timing
+print(f"prefill attention T={T}: {da * 1e6:.1f} us/layer  {afl / da / 1e12:.1f} TFLOP/s (causal flops) "
+      f"sm_clock_median={clk} MHz runs={[round(x * 1e6, 1) for x in das]}")
+if "attn" in sys.argv[2:] or "attnonly" in sys.argv[2:]:
     sys.exit(0)
 
 # in-situ ablation: prefill with one launch kind replaced by a no-op
