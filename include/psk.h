@@ -204,6 +204,15 @@ int psk_gemv(const void* x, int32_t n_rows, int32_t K, const void* const* W,
 int psk_gemv_tc(const void* x, int32_t n_rows, int32_t K, const void* const* W_host,
                 const int32_t* mod_row_start, int32_t n_mod, int32_t max_rows_per_mod,
                 int32_t N, int32_t epilogue, void* out, void* workspace, void* stream);
+/* K5-TC for the decode step's fused QKV projection of every row of `b`
+ * (N = (n_q_heads + 2 n_kv_heads) * 128, unit = one head) with RoPE and the
+ * KV append fused into the epilogue: q_rot bf16 [n_rows][nq][128] and the
+ * rotated k / plain v of each row written into its private page at index
+ * priv_len[r], exactly as psk_gemv_tc(PSK_EPI_STORE_F32) followed by
+ * psk_rope_append (bit-identical). Same workspace as psk_gemv_tc. */
+int psk_gemv_tc_qkv_rope(const void* x, int32_t K, const void* const* W_host, const psk_decode_batch* b,
+                         int32_t max_rows_per_mod, int32_t n_q_heads, const float* rope, int32_t layer,
+                         psk_kv_layout kv, void* q_rot, void* workspace, void* stream);
 /* Bytes of the psk_gemv_tc workspace (stream-K partials + flags); allocate
  * once ZEROED and reuse for every call on the stream (the kernel leaves the
  * flags zeroed). */
@@ -235,6 +244,10 @@ int psk_rope_append(const psk_decode_batch* b, const float* qkv, int32_t n_q_hea
  * zero-filled allocation); every call leaves them zero. */
 int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int32_t splits,
                               int64_t* bytes);
+/* How many kernels psk_decode_attn launches for this batch (1: the fan-out
+ * kernel merging its own splits; 2: partial + merge; 0: no rows). */
+int psk_decode_attn_kernels(const psk_decode_batch* b, int32_t n_q_heads, int32_t n_kv_heads, int32_t splits,
+                            int32_t* n_kernels);
 int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_heads,
                     int32_t layer, psk_kv_layout kv, int32_t splits, void* workspace, void* out,
                     void* stream);

@@ -91,6 +91,23 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float* f) {
   }
 }
 
+// Rotate-half RoPE (Llama) of the pair (x1, x2) = dims (i, i + 64) of a
+// head: y1 = x1 c - x2 s, y2 = x2 c + x1 s. Explicit roundings, so every
+// decode kernel that appends K (psk_rope_append, the fused K5-TC QKV
+// epilogue) produces the same bits.
+__device__ __forceinline__ void rope_pair(float x1, float x2, float c, float s, float& y1, float& y2) {
+  y1 = __fmaf_rn(x1, c, -__fmul_rn(x2, s));
+  y2 = __fmaf_rn(x2, c, __fmul_rn(x1, s));
+}
+
+// bf16 K (kvsel 0) or V (1) row of (page, layer, kv head, token) in the
+// paged cache: page[layer][K|V][kv_head][token][head_dim].
+__device__ __forceinline__ __nv_bfloat16* kv_row(const psk_kv_layout& kv, int32_t page, int layer, int kvsel,
+                                                 int head, int tok) {
+  return reinterpret_cast<__nv_bfloat16*>(kv.base) + (int64_t)page * kv.page_elems +
+         ((((int64_t)layer * 2 + kvsel) * kv.n_kv_heads + head) * kv.page_tokens + tok) * kv.head_dim;
+}
+
 __device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
   uint4 v;
   __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);

@@ -99,11 +99,6 @@ __global__ void __launch_bounds__(NORM_THREADS) rmsnorm_rows_kernel(const float*
 
 // ---------------------------------------------------- RoPE + KV append ---
 
-__device__ __forceinline__ __nv_bfloat16* kv_ptr(const psk_kv_layout& kv, int32_t page, int layer,
-                                                 int kvsel, int head, int tok) {
-  return reinterpret_cast<__nv_bfloat16*>(kv.base) + (int64_t)page * kv.page_elems +
-         ((((int64_t)layer * 2 + kvsel) * kv.n_kv_heads + head) * kv.page_tokens + tok) * kv.head_dim;
-}
 
 // One CTA per row, 64 x 8 threads: thread (i, j) rotates dims (i, i + 64) of
 // heads j, j + 8, ... (q heads, then k), copies v; all of a thread's loads
@@ -129,15 +124,15 @@ __global__ void __launch_bounds__(64 * ROPE_HG) rope_append_kernel(psk_decode_ba
   // q and k heads: rotate-half
 #pragma unroll 4
   for (int h = j; h < nq + nkv; h += ROPE_HG) {
-    const float x1 = row[h * HD + i], x2 = row[h * HD + i + 64];
-    const __nv_bfloat16 y1 = f2bf(x1 * c - x2 * s), y2 = f2bf(x2 * c + x1 * s);
-    __nv_bfloat16* d = h < nq ? q_rot + ((int64_t)r * nq + h) * HD : kv_ptr(kv, page, layer, 0, h - nq, off);
-    d[i] = y1;
-    d[i + 64] = y2;
+    float y1, y2;
+    rope_pair(row[h * HD + i], row[h * HD + i + 64], c, s, y1, y2);
+    __nv_bfloat16* d = h < nq ? q_rot + ((int64_t)r * nq + h) * HD : kv_row(kv, page, layer, 0, h - nq, off);
+    d[i] = f2bf(y1);
+    d[i + 64] = f2bf(y2);
   }
   for (int h = j; h < nkv; h += ROPE_HG) {
     const float* vr = row + (nq + nkv + h) * HD;
-    __nv_bfloat16* vd = kv_ptr(kv, page, layer, 1, h, off);
+    __nv_bfloat16* vd = kv_row(kv, page, layer, 1, h, off);
     vd[i] = f2bf(vr[i]);
     vd[i + 64] = f2bf(vr[i + 64]);
   }

@@ -1726,6 +1726,27 @@ int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int
   return PSK_OK;
 }
 
+// Whether the fan-out (tcgen05) kernel runs and merges its splits itself:
+// > 32 query rows per KV head, its (session, head, split) CTAs fit one wave
+// (1 CTA per SM, all co-resident for the in-kernel merge).
+static bool fanout_fused(const psk_decode_batch* b, int32_t n_q_heads, int32_t n_kv_heads, int32_t splits) {
+  static const bool force_hmma = getenv("PSK_ATTN_HMMA") != nullptr;
+  static const bool merge_kernel = getenv("PSK_ATTN_MERGE_KERNEL") != nullptr;
+  const int grp = n_q_heads / n_kv_heads;
+  if (grp * b->max_rows_per_sess <= 32 || force_hmma || merge_kernel) return false;
+  const int64_t groups = (int64_t)b->n_sess * n_kv_heads;
+  if (splits == 0) splits = (int)(sm_count() / groups) > 1 ? (int)(sm_count() / groups) : 1;
+  return groups * splits <= psk::device_sms() && 2 * groups <= CNT_INTS;
+}
+
+int psk_decode_attn_kernels(const psk_decode_batch* b, int32_t n_q_heads, int32_t n_kv_heads, int32_t splits,
+                            int32_t* n_kernels) {
+  PSK_CHECK_ARG(b && n_kernels && n_kv_heads > 0 && n_q_heads % n_kv_heads == 0 && splits >= 0,
+                "psk_decode_attn_kernels: bad args");
+  *n_kernels = b->n_rows == 0 ? 0 : (fanout_fused(b, n_q_heads, n_kv_heads, splits) ? 1 : 2);
+  return PSK_OK;
+}
+
 int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_heads, int32_t layer,
                     psk_kv_layout kv, int32_t splits, void* workspace, void* out, void* stream) {
   PSK_CHECK_ARG(b && q_rot && out && workspace && kv.head_dim == HD && kv.page_tokens == PT &&
@@ -1799,8 +1820,7 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   p.sk_grid = sms;
   // fan-out kernel: merge inside the partial kernel when every CTA is
   // co-resident (one CTA per SM); PSK_ATTN_MERGE_KERNEL=1 keeps the kernel
-  static const bool merge_kernel = getenv("PSK_ATTN_MERGE_KERNEL") != nullptr;
-  p.fused = use_tc && !merge_kernel && items <= psk::device_sms() && 2 * groups <= CNT_INTS;
+  p.fused = use_tc && fanout_fused(b, n_q_heads, kv.n_kv_heads, splits);
   static const bool early = getenv("PSK_ATTN_EARLY") != nullptr;
   p.early = early;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);

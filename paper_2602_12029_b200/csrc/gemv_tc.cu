@@ -20,7 +20,10 @@
 //   warp 1   MMA issuer (one lane): 4 x tcgen05.mma per chunk into one of two
 //            TMEM accumulators (double-buffered across segments)
 //   warps 2-5  epilogue: tcgen05.ld 32x32b (thread = weight row, one column
-//            per activation row), fused store / residual add / SiLU*mul
+//            per activation row), fused store / residual add / SiLU*mul /
+//            the decode QKV epilogue (RoPE on q and k, q_rot out, k and v
+//            appended to each row's private KV page: a 128-row unit is one
+//            head, the rotate-half partner dims swap through shared memory)
 // Work unit = (module, 128-row weight block) x K; the CTAs split the
 // (unit, 64-column chunk) space stream-K style (below).
 //
@@ -62,6 +65,17 @@ struct Maps {
   CUtensorMap x;          // activations [n_rows][K], box {64, MN}
 };
 
+// EPI_QKV_ROPE (psk_gemv_tc_qkv_rope): the decode step's QKV projection with
+// RoPE + KV append fused (replaces psk_gemv_tc(STORE_F32) + psk_rope_append).
+constexpr int EPI_QKV_ROPE = 16;
+struct RopeArgs {
+  psk_decode_batch b;
+  psk_kv_layout kv;
+  const float* rope;       // [max_pos][64][2] (cos, sin)
+  __nv_bfloat16* q_rot;    // [n_rows][nq][128]
+  int nq, layer;
+};
+
 __device__ __forceinline__ void tmem_ld32_cols(uint32_t taddr, float* v) {
   uint32_t r[32];
   umma::ld32_async(taddr, r);
@@ -95,8 +109,10 @@ __device__ __forceinline__ int run_begin(int cta, int64_t total, int grid) {
 template <int MN, int EPI, int UW>
 __global__ void __launch_bounds__(THREADS, 1)
     gemv_tc_kernel(const __grid_constant__ Maps maps, const int32_t* __restrict__ mrs, int n_mod, int N, int K,
-                   void* __restrict__ out, float* __restrict__ part, int* __restrict__ flags) {
+                   void* __restrict__ out, float* __restrict__ part, int* __restrict__ flags,
+                   const __grid_constant__ RopeArgs ra) {
   using C = Cfg<MN, UW>;
+  static_assert(EPI != EPI_QKV_ROPE || UW == 1, "QKV epilogue: one head (128 rows) per unit");
   constexpr int UB = UW * BN;  // weight rows per unit
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -106,6 +122,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // EPI_QKV_ROPE: [MN][128] fp32 exchange tile + per-row (pos, page, token)
+  float* xch = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE + 256);
+  int* meta = reinterpret_cast<int*>(xch + MN * BN);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = N / UB;
@@ -242,6 +261,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool owner = sg.k0 == 0;
       const int acc = it & 1;
       bool waited_tfull = false;
+      if (EPI == EPI_QKV_ROPE && owner) {
+        // the previous unit's readers of xch / meta are done; stage this
+        // unit's row positions and append slots (sess_len + priv_len, page)
+        named_barrier_sync(3, 128);
+        const int t = threadIdx.x - 64;
+        if (t < M) {
+          const int row = xb + t, idx = ra.b.priv_len[row];
+          meta[3 * t] = ra.b.sess_len[ra.b.row_sess[row]] + idx;
+          meta[3 * t + 1] = ra.b.row_pages[(int64_t)row * ra.b.max_row_pages + idx / 16];
+          meta[3 * t + 2] = idx % 16;
+        }
+      }
 #pragma unroll 1
       for (int u = 0; u < UW; ++u) {
       const int n = blk * UB + u * BN + r;
@@ -314,7 +345,36 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int m = 0; m < MN; ++m) v[m] += a[m];
       }
-      if (EPI == PSK_EPI_SILU_MUL) {
+      if (EPI == EPI_QKV_ROPE) {
+        const int nkv = ra.kv.n_kv_heads, hd = blk;  // unit = head: q heads, then k, then v
+        if (hd < ra.nq + nkv) {
+#pragma unroll
+          for (int m = 0; m < MN; ++m) xch[m * BN + r] = v[m];
+        }
+        named_barrier_sync(3, 128);  // xch and meta visible
+        const int i = r & 63;
+#pragma unroll 4
+        for (int m = 0; m < MN; ++m) {
+          if (m >= M) break;
+          const int pos = meta[3 * m], page = meta[3 * m + 1], tok = meta[3 * m + 2];
+          if (hd >= ra.nq + nkv) {
+            kv_row(ra.kv, page, ra.layer, 1, hd - ra.nq - nkv, tok)[r] = f2bf(v[m]);
+            continue;
+          }
+          const float2 cs = reinterpret_cast<const float2*>(ra.rope)[(int64_t)pos * 64 + i];
+          const float o = xch[m * BN + (r ^ 64)];
+          float y1, y2;
+          if (r < 64)
+            rope_pair(v[m], o, cs.x, cs.y, y1, y2);
+          else
+            rope_pair(o, v[m], cs.x, cs.y, y1, y2);
+          const __nv_bfloat16 y = f2bf(r < 64 ? y1 : y2);
+          if (hd < ra.nq)
+            ra.q_rot[((int64_t)(xb + m) * ra.nq + hd) * BN + r] = y;
+          else
+            kv_row(ra.kv, page, ra.layer, 0, hd - ra.nq, tok)[r] = y;
+        }
+      } else if (EPI == PSK_EPI_SILU_MUL) {
         // rows interleaved [gate 8 | up 8]: the up row of gate row n is n + 8,
         // held by lane + 8 of this warp
         const bool gate = (r & 15) < 8;
@@ -396,7 +456,7 @@ constexpr int FLAG_BYTES = 4096;  // one int per CTA (<= 1024 SMs)
 
 template <int MN, int EPI, int UW>
 static int launch_uw(const void* x, int n_rows, int K, const void* const* W_host, const int32_t* mrs, int n_mod,
-                  int N, void* out, void* ws, cudaStream_t s) {
+                  int N, void* out, void* ws, cudaStream_t s, const RopeArgs& ra = RopeArgs{}) {
   Maps maps;
   for (int m = 0; m < n_mod; ++m) {
     int rc = make_map(&maps.w[m], W_host[m], N, K, BN, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
@@ -405,9 +465,12 @@ static int launch_uw(const void* x, int n_rows, int K, const void* const* W_host
   int rc = make_map(&maps.x, x, n_rows, K, MN, CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
   if (rc) return rc;
   auto k = gemv_tc_kernel<MN, EPI, UW>;
+  // + the QKV epilogue's exchange tile and row table
+  constexpr int smem_bytes = Cfg<MN, UW>::SMEM + (EPI == EPI_QKV_ROPE ? MN * BN * 4 + MN * 3 * 4 : 0);
+  static_assert(smem_bytes <= 232448, "shared memory");
   static bool attr = false;
   if (!attr) {
-    PSK_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<MN, UW>::SMEM));
+    PSK_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
     attr = true;
   }
   const int sms = sm_count();
@@ -423,8 +486,8 @@ static int launch_uw(const void* x, int n_rows, int K, const void* const* W_host
   if (whole_units && units <= sms) grid = (int)units;
   int* flags = reinterpret_cast<int*>(ws);
   float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + FLAG_BYTES);
-  PSK_CUDA_TRY(psk::launch_pdl(k, dim3(grid), dim3(THREADS), (size_t)Cfg<MN, UW>::SMEM, s, maps, mrs, n_mod, N, K,
-                               out, part, flags));
+  PSK_CUDA_TRY(psk::launch_pdl(k, dim3(grid), dim3(THREADS), (size_t)smem_bytes, s, maps, mrs, n_mod, N, K,
+                               out, part, flags, ra));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }
@@ -462,6 +525,36 @@ extern "C" int psk_gemv_tc_workspace(int64_t* bytes) {
   using namespace psk::gemv_tc;
   *bytes = FLAG_BYTES + (int64_t)psk::device_sms() * 2 * 64 * BN * 4;  // UW <= 2 blocks x MN <= 64 rows
   return PSK_OK;
+}
+
+extern "C" int psk_gemv_tc_qkv_rope(const void* x, int32_t K, const void* const* W_host, const psk_decode_batch* b,
+                                    int32_t max_rows_per_mod, int32_t n_q_heads, const float* rope, int32_t layer,
+                                    psk_kv_layout kv, void* q_rot, void* workspace, void* stream) {
+  using namespace psk::gemv_tc;
+  PSK_CHECK_ARG(x && W_host && b && rope && q_rot && workspace && K > 0 && K % 64 == 0 && b->n_mod > 0 &&
+                    b->n_mod <= MAXMOD && kv.head_dim == BN && kv.page_tokens == 16 && n_q_heads > 0,
+                "psk_gemv_tc_qkv_rope: bad args (K %% 64 == 0, 1..%d modules, head_dim 128, 16-token pages)",
+                MAXMOD);
+  if (b->n_rows == 0) return PSK_OK;
+  const int maxm = max_rows_per_mod > 0 ? max_rows_per_mod : b->n_rows;
+  const int N = (n_q_heads + 2 * kv.n_kv_heads) * BN;
+  RopeArgs ra;
+  ra.b = *b;
+  ra.kv = kv;
+  ra.rope = rope;
+  ra.q_rot = reinterpret_cast<__nv_bfloat16*>(q_rot);
+  ra.nq = n_q_heads;
+  ra.layer = layer;
+  cudaStream_t s = psk::as_stream(stream);
+  const int32_t* mrs = b->mod_row_start;
+  if (maxm <= 16)
+    return launch_uw<16, EPI_QKV_ROPE, 1>(x, b->n_rows, K, W_host, mrs, b->n_mod, N, q_rot, workspace, s, ra);
+  if (maxm <= 32)
+    return launch_uw<32, EPI_QKV_ROPE, 1>(x, b->n_rows, K, W_host, mrs, b->n_mod, N, q_rot, workspace, s, ra);
+  if (maxm <= 64)
+    return launch_uw<64, EPI_QKV_ROPE, 1>(x, b->n_rows, K, W_host, mrs, b->n_mod, N, q_rot, workspace, s, ra);
+  psk::set_error("psk_gemv_tc_qkv_rope: more than 64 rows per module (%d)", maxm);
+  return PSK_EINVAL;
 }
 
 extern "C" int psk_gemv_tc(const void* x, int32_t n_rows, int32_t K, const void* const* W_host,

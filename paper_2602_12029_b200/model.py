@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -433,7 +434,15 @@ class DecodeRunner:
                                                       C.byref(wsb)))
         self.ws = torch.zeros(wsb.value // 4 + 1, dtype=f32, device=dev)  # split counters start at 0
         self.graph: torch.cuda.CUDAGraph | None = None
-        self.launches_per_step = 1 + L * 9 + 3
+        # K5-TC: RoPE + KV append fused into the QKV GEMV's epilogue (one
+        # launch instead of two per layer; PSK_FUSED_QKV=0 keeps them apart)
+        self.fused_qkv = self.use_tc_gemv and os.environ.get("PSK_FUSED_QKV", "1") != "0"
+        # K6 launches 1 kernel when the fan-out kernel merges its splits
+        # itself, else 2 (partial + merge)
+        n_attn = C.c_int32()
+        _lib.check(self.lib.psk_decode_attn_kernels(batch.c_ref(), cfg.n_heads, cfg.n_kv_heads, self.splits,
+                                                    C.byref(n_attn)))
+        self.launches_per_step = 1 + L * (7 + n_attn.value - self.fused_qkv) + 3
 
     def _gemv(self, x, K: int, p_dev, p_host, N: int, epi: int, out, s: int) -> None:
         """K5 (mma.sync, <= 8 rows per module) or K5-TC (tcgen05, 9..64)."""
@@ -457,9 +466,13 @@ class DecodeRunner:
         for l in range(cfg.n_layers):
             chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_attn_norm[l]), _ptr(b.t_row_mod),
                                      C.c_float(cfg.norm_eps), _ptr(self.xn), s))
-            gemv(self.xn, d, self.p_wqkv[l], self.h_wqkv[l], cfg.qkv_dim, 1, self.qkv, s)
-            chk(lib.psk_rope_append(bc, _ptr(self.qkv), cfg.n_heads, _ptr(self.rope), l, kvl,
-                                    _ptr(self.q_rot), s))
+            if self.fused_qkv:
+                chk(lib.psk_gemv_tc_qkv_rope(_ptr(self.xn), d, self.h_wqkv[l], bc, b.max_rpm, cfg.n_heads,
+                                             _ptr(self.rope), l, kvl, _ptr(self.q_rot), _ptr(self.gemv_ws), s))
+            else:
+                gemv(self.xn, d, self.p_wqkv[l], self.h_wqkv[l], cfg.qkv_dim, 1, self.qkv, s)
+                chk(lib.psk_rope_append(bc, _ptr(self.qkv), cfg.n_heads, _ptr(self.rope), l, kvl,
+                                        _ptr(self.q_rot), s))
             chk(lib.psk_decode_attn(bc, _ptr(self.q_rot), cfg.n_heads, l, kvl, self.splits,
                                     _ptr(self.ws), _ptr(self.attn), s))
             gemv(self.attn, cfg.n_heads * cfg.head_dim, self.p_wo[l], self.h_wo[l], d, 2, self.h, s)

@@ -1,7 +1,7 @@
 """Drive each hot kernel a few times at the bench shapes, for ncu.
 
     ncu --set full -k regex:<kernel> -c 2 python tools/profile_kernels.py <which> [rows/module]
-which: gemv | gemv_tc | attn4k | attn4k_s8 | attn4k_s32 | attn32k | gemm | prefill_attn | all
+which: gemv | gemv_tc | qkv_rope | attn4k | attn4k_s8 | attn4k_s32 | attn32k | gemm | prefill_attn | kvcopy | all
 """
 import sys
 from pathlib import Path
@@ -71,6 +71,36 @@ if which == "gemv_tc":
     for _ in range(4):
         _lib.check(lib.psk_gemv_tc(x.data_ptr(), 4 * M, cfg.d_model, hp, mrs.data_ptr(), 4, M,
                                    2 * cfg.ffn, 3, act.data_ptr(), ws.data_ptr(), s))
+    torch.cuda.synchronize()
+if which == "qkv_rope":  # decode QKV GEMV with RoPE + KV append fused (K5-TC epilogue)
+    import ctypes
+    from paper_2602_12029_b200.model import DecodeBatch as DB, rope_table
+    M = int(sys.argv[2]) if len(sys.argv) > 2 else 32  # rows per module
+    mods = [ModuleWeights(cfg, 10 + i) for i in range(4)]
+    n_sess = M
+    kv = KVCache(cfg, n_sess * 4 + 4 * M * 2)
+    sess = [SessionSpec(shared_len=40, pages=[4 * i, 4 * i + 1, 4 * i + 2]) for i in range(n_sess)]
+    rows = [DecodeRow(module=m, session=i, first_token=0, pages=[4 * n_sess + 2 * (i * 4 + m)])
+            for i in range(n_sess) for m in range(4)]
+    b = DB(sess, rows, 4)
+    x = torch.randn(4 * M, cfg.d_model, device="cuda").to(torch.bfloat16)
+    q_rot = torch.empty(4 * M, cfg.n_heads, cfg.head_dim, dtype=torch.bfloat16, device="cuda")
+    rope = torch.from_numpy(rope_table(cfg)).cuda()
+    hp = (ctypes.c_void_p * 4)(*[m.wqkv[0].data_ptr() for m in mods])
+    wsb = ctypes.c_int64()
+    _lib.check(lib.psk_gemv_tc_workspace(ctypes.byref(wsb)))
+    ws = torch.zeros(wsb.value, dtype=torch.uint8, device="cuda")
+    for _ in range(4):
+        _lib.check(lib.psk_gemv_tc_qkv_rope(x.data_ptr(), cfg.d_model, hp, b.c_ref(), b.max_rpm, cfg.n_heads,
+                                            rope.data_ptr(), 0, kv.layout(), q_rot.data_ptr(), ws.data_ptr(), s))
+    torch.cuda.synchronize()
+if which == "kvcopy":  # K8: a 4k context's 257 pages (2 MiB each), same-device page copy
+    kv = KVCache(LlamaConfig.llama8b(), 2 * 257 + 2)  # all 32 layers: 2 MiB pages
+    src = torch.arange(257, dtype=torch.int32, device="cuda")
+    dst = torch.arange(257, 514, dtype=torch.int32, device="cuda")
+    for _ in range(4):
+        _lib.check(lib.psk_kv_copy_pages(kv.data.data_ptr(), kv.data.data_ptr(), src.data_ptr(), dst.data_ptr(), 257,
+                                         kv.data[0].numel() * 2, s))
     torch.cuda.synchronize()
 if which in ("gemv", "all"):
     M = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # rows per module

@@ -50,9 +50,12 @@ def time_step(n=40):
 
 
 kinds = {"rmsnorm": ["psk_rmsnorm_rows"], "rope_append": ["psk_rope_append"], "attention": ["psk_decode_attn"],
-         "gemv": ["psk_gemv", "psk_gemv_tc"], "embed+argmax": ["psk_embed_rows", "psk_argmax_advance"]}
+         "gemv": ["psk_gemv", "psk_gemv_tc"], "qkv+rope fused": ["psk_gemv_tc_qkv_rope"],
+         "embed+argmax": ["psk_embed_rows", "psk_argmax_advance"]}
 full = time_step()
-print(f"S={S}: full step {full:9.1f} us")
+print(f"S={S}: full step {full:9.1f} us (fused QKV epilogue: {r.fused_qkv})", flush=True)
+if "quick" in sys.argv[2:]:
+    sys.exit(0)
 for name, fns in kinds.items():
     saved = {f: getattr(lib, f) for f in fns}
     for f in fns:
