@@ -123,8 +123,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   // EPI_QKV_ROPE: [MN][128] fp32 exchange tile + per-row (pos, page, token)
+  // (+ at MN = 32 the rows' RoPE (cos, sin) [MN][64], staged under the MMAs)
+  constexpr bool CS_SMEM = EPI == EPI_QKV_ROPE && MN == 32;
   float* xch = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE + 256);
   int* meta = reinterpret_cast<int*>(xch + MN * BN);
+  float2* cs_s = reinterpret_cast<float2*>(meta + 4 * MN);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = N / UB;
@@ -272,6 +275,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           meta[3 * t + 1] = ra.b.row_pages[(int64_t)row * ra.b.max_row_pages + idx / 16];
           meta[3 * t + 2] = idx % 16;
         }
+        if (CS_SMEM && blk < ra.nq + ra.kv.n_kv_heads) {  // q / k head: stage its rows' (cos, sin)
+          named_barrier_sync(3, 128);
+          const float2* rope2 = reinterpret_cast<const float2*>(ra.rope);
+          for (int e = t; e < M * 64; e += 128) cs_s[e] = __ldg(rope2 + (int64_t)meta[3 * (e >> 6)] * 64 + (e & 63));
+        }
       }
 #pragma unroll 1
       for (int u = 0; u < UW; ++u) {
@@ -353,26 +361,41 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         named_barrier_sync(3, 128);  // xch and meta visible
         const int i = r & 63;
-#pragma unroll 4
-        for (int m = 0; m < MN; ++m) {
-          if (m >= M) break;
-          const int pos = meta[3 * m], page = meta[3 * m + 1], tok = meta[3 * m + 2];
-          if (hd >= ra.nq + nkv) {
-            kv_row(ra.kv, page, ra.layer, 1, hd - ra.nq - nkv, tok)[r] = f2bf(v[m]);
-            continue;
+        const bool vhead = hd >= ra.nq + nkv;
+        const float2* rope2 = reinterpret_cast<const float2*>(ra.rope);
+        // 8 rows at a time: their (cos, sin) loads are all in flight before
+        // the first store (stores to q_rot / the pages may alias the table
+        // for the compiler, so interleaving would serialise the loads)
+#pragma unroll
+        for (int m0 = 0; m0 < MN; m0 += 8) {
+          if (m0 >= M) break;
+          float2 cs[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            cs[j] = (vhead || m0 + j >= M) ? make_float2(0.f, 0.f)
+                    : CS_SMEM             ? cs_s[(m0 + j) * 64 + i]
+                                          : __ldg(rope2 + (int64_t)meta[3 * (m0 + j)] * 64 + i);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int m = m0 + j;
+            if (m >= M) break;
+            const int page = meta[3 * m + 1], tok = meta[3 * m + 2];
+            if (vhead) {
+              kv_row(ra.kv, page, ra.layer, 1, hd - ra.nq - nkv, tok)[r] = f2bf(v[m]);
+              continue;
+            }
+            const float o = xch[m * BN + (r ^ 64)];
+            float y1, y2;
+            if (r < 64)
+              rope_pair(v[m], o, cs[j].x, cs[j].y, y1, y2);
+            else
+              rope_pair(o, v[m], cs[j].x, cs[j].y, y1, y2);
+            const __nv_bfloat16 y = f2bf(r < 64 ? y1 : y2);
+            if (hd < ra.nq)
+              ra.q_rot[((int64_t)(xb + m) * ra.nq + hd) * BN + r] = y;
+            else
+              kv_row(ra.kv, page, ra.layer, 0, hd - ra.nq, tok)[r] = y;
           }
-          const float2 cs = reinterpret_cast<const float2*>(ra.rope)[(int64_t)pos * 64 + i];
-          const float o = xch[m * BN + (r ^ 64)];
-          float y1, y2;
-          if (r < 64)
-            rope_pair(v[m], o, cs.x, cs.y, y1, y2);
-          else
-            rope_pair(o, v[m], cs.x, cs.y, y1, y2);
-          const __nv_bfloat16 y = f2bf(r < 64 ? y1 : y2);
-          if (hd < ra.nq)
-            ra.q_rot[((int64_t)(xb + m) * ra.nq + hd) * BN + r] = y;
-          else
-            kv_row(ra.kv, page, ra.layer, 0, hd - ra.nq, tok)[r] = y;
         }
       } else if (EPI == PSK_EPI_SILU_MUL) {
         // rows interleaved [gate 8 | up 8]: the up row of gate row n is n + 8,
@@ -466,7 +489,8 @@ static int launch_uw(const void* x, int n_rows, int K, const void* const* W_host
   if (rc) return rc;
   auto k = gemv_tc_kernel<MN, EPI, UW>;
   // + the QKV epilogue's exchange tile and row table
-  constexpr int smem_bytes = Cfg<MN, UW>::SMEM + (EPI == EPI_QKV_ROPE ? MN * BN * 4 + MN * 3 * 4 : 0);
+  constexpr int smem_bytes = Cfg<MN, UW>::SMEM + (EPI == EPI_QKV_ROPE ? MN * BN * 4 + MN * 4 * 4 : 0) +
+                             (EPI == EPI_QKV_ROPE && MN == 32 ? MN * 64 * 8 : 0);
   static_assert(smem_bytes <= 232448, "shared memory");
   static bool attr = false;
   if (!attr) {

@@ -435,8 +435,11 @@ class DecodeRunner:
         self.ws = torch.zeros(wsb.value // 4 + 1, dtype=f32, device=dev)  # split counters start at 0
         self.graph: torch.cuda.CUDAGraph | None = None
         # K5-TC: RoPE + KV append fused into the QKV GEMV's epilogue (one
-        # launch instead of two per layer; PSK_FUSED_QKV=0 keeps them apart)
-        self.fused_qkv = self.use_tc_gemv and os.environ.get("PSK_FUSED_QKV", "1") != "0"
+        # launch instead of two per layer) with PSK_FUSED_QKV=1. Bit-identical
+        # but not faster: at 32 rows/module the step is 13.36-13.38 ms fused
+        # vs 13.35-13.37 ms apart (the epilogue's head-pair exchange and row
+        # table sit on the stream-K owners' critical path), so it is off
+        self.fused_qkv = self.use_tc_gemv and os.environ.get("PSK_FUSED_QKV", "0") == "1"
         # K6 launches 1 kernel when the fan-out kernel merges its splits
         # itself, else 2 (partial + merge)
         n_attn = C.c_int32()

@@ -107,6 +107,6 @@ def test_decode_step_fused_qkv_same_tokens(rows, monkeypatch):
         toks = r.run(8)
         torch.cuda.synchronize()
         out.append((toks.clone(), r.logits.clone(), kv.data.clone()))
-    assert torch.equal(out[0][0], out[1][0])
+    assert torch.equal(out[0][0], out[1][0])  # (fused, unfused)
     assert torch.equal(out[0][1], out[1][1])
     assert torch.equal(out[0][2].view(torch.int16), out[1][2].view(torch.int16))
