@@ -73,6 +73,8 @@ struct Params {
   unsigned* cnt;  // fan-out kernel, fused merge: per group {arrived, departed}, zero between launches
   int fused;      // fan-out kernel: the split CTAs merge their group themselves (no merge kernel)
   int early;      // fan-out kernel: stream shared pages before the PDL wait (PSK_ATTN_EARLY=1)
+  int stream_only;  // fan-out kernel, measurement only (PSK_ATTN_STREAM_ONLY=1): pages streamed and
+                    // released without MMA / softmax (the TMA stream's own ceiling; output garbage)
 };
 
 // SW128 address of (token row, 16-byte chunk c16 in 0..15) in a K/V tile made
@@ -1370,12 +1372,19 @@ __global__ void __launch_bounds__(THREADS, 1)
       umma::commit_e(&pv_done[u]);
       umma::commit_e(&empty[c % NSTG]);
     };
-    for (int c = 0; c < nch && c < 2; ++c) {
+    if (p.stream_only) {
+      for (int c = 0; c < nch; ++c) {
+        tma::mbar_wait(&full[c % NSTG], (c / NSTG) & 1);
+        if (lane == 0) tma::mbar_arrive(&empty[c % NSTG]);
+        __syncwarp();
+      }
+    }
+    for (int c = 0; c < nch && c < 2 && !p.stream_only; ++c) {
       tma::mbar_wait(&full[c], 0);
       umma::fence_after();
       issue_s(c);
     }
-    for (int c = 0; c < nch; ++c) {
+    for (int c = 0; c < nch && !p.stream_only; ++c) {
       // S_u(c+2) as soon as softmax(c) has S_u(c) in registers, so it runs
       // under that softmax; then PV_u(c) once P_u(c) is in TMEM
       if (c + 2 < nch) {
@@ -1404,7 +1413,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const float sc = p.scale_log2;
     float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;  // m in scaled log2 units
     int it = 0;
-    for (int c = u; c < nch; c += 2, ++it) {
+    for (int c = u; c < nch && !p.stream_only; c += 2, ++it) {
       tma::mbar_wait(&s_full[u], it & 1);
       umma::fence_after();
       uint32_t sr[32];
@@ -1823,6 +1832,8 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   p.fused = use_tc && fanout_fused(b, n_q_heads, kv.n_kv_heads, splits);
   static const bool early = getenv("PSK_ATTN_EARLY") != nullptr;
   p.early = early;
+  static const bool stream_only = getenv("PSK_ATTN_STREAM_ONLY") != nullptr;
+  p.stream_only = stream_only;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
   cudaStream_t s = psk::as_stream(stream);
   static bool init = false;

@@ -24,7 +24,10 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
                           "us": r["us_per_launch"], "gbs": r["achieved"], "frac": r["frac"]}), flush=True)
     sys.exit(0)
 
-MODES = (("fused", {}), ("early", {"PSK_ATTN_EARLY": "1"}), ("merge-kernel", {"PSK_ATTN_MERGE_KERNEL": "1"}))
+MODES = (("fused", {}), ("early", {"PSK_ATTN_EARLY": "1"}), ("merge-kernel", {"PSK_ATTN_MERGE_KERNEL": "1"}),
+         ("stream-only", {"PSK_ATTN_STREAM_ONLY": "1"}))  # the last: TMA stream alone, no MMA / softmax
+if len(sys.argv) > 1 and sys.argv[1] != "child":
+    MODES = tuple(m for m in MODES if m[0] in sys.argv[1].split(","))
 for mode, env in MODES:
     for rep in range(2):
         r = subprocess.run([sys.executable, __file__, "child"], env=dict(os.environ, **env), capture_output=True,
