@@ -390,6 +390,11 @@ class BlockPool:
         self._in_ids[:n] = b
         return n
 
+    @property
+    def max_handles(self) -> int:
+        """Block handles one pin / release call takes."""
+        return self._max_q
+
     def pin(self, blocks, now: int) -> None:
         """kvstore.py:237-240."""
         n = self._stage_handles(blocks)

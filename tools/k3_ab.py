@@ -14,18 +14,30 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 T = sys.argv[2] if len(sys.argv) > 2 else "4096"
-res = {"tmem-P": [], "smem-P": []}
+# extra args: name:KEY=VAL;KEY=VAL variants (default: TMEM-P vs shared-memory-P)
+variants = [("tmem-P", {}), ("smem-P", {"PSK_PREFILL_PSMEM": "1"})]
+if len(sys.argv) > 3:
+    variants = []
+    for a in sys.argv[3:]:
+        name, _, kv = a.partition(":")
+        variants.append((name, dict(x.split("=", 1) for x in kv.split(";") if x)))
+res = {name: [] for name, _ in variants}
 for rep in range(reps):
-    for name, env in (("tmem-P", {}), ("smem-P", {"PSK_PREFILL_PSMEM": "1"})):
-        r = subprocess.run([sys.executable, str(ROOT / "tools" / "bench_prefill.py"), T, "attn"],
+    for name, env in variants:
+        r = subprocess.run([sys.executable, str(ROOT / "tools" / "bench_prefill.py"), T, "attnonly"],
                            env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
         for line in r.stdout.splitlines():
             if line.startswith("prefill attention"):
                 us = float(line.split(":")[1].split("us")[0])
-                res[name].append(us)
+                clk = int(line.split("sm_clock_median=")[1].split()[0]) if "sm_clock_median=" in line else -1
+                res[name].append((us, clk))
                 print(f"{name} rep{rep}: {line}", flush=True)
         if r.returncode:
             print(r.stderr[-2000:])
 for name, v in res.items():
     if v:
-        print(f"{name}: median {statistics.median(v):.1f} us/layer, min {min(v):.1f}, max {max(v):.1f} (n={len(v)})")
+        us = [x[0] for x in v]
+        # cycles per layer (us x MHz) removes the power-cap clock drift between runs
+        cyc = [x[0] * x[1] for x in v if x[1] > 0]
+        print(f"{name}: median {statistics.median(us):.1f} us/layer, min {min(us):.1f} (n={len(us)}); "
+              f"median {statistics.median(cyc) / 1e3 if cyc else -1:.1f} kcycles/layer")
