@@ -251,6 +251,9 @@ class DecodeBatch:
     def __init__(self, sessions: list[SessionSpec], rows: list[DecodeRow], n_modules: int,
                  device: int = 0):
         dev = torch.device("cuda", device)
+        for i, sp in enumerate(sessions):  # the kernels read ceil(shared_len / 16) page ids of each session
+            if sp.shared_len < 0 or (sp.shared_len + PAGE_TOKENS - 1) // PAGE_TOKENS > len(sp.pages):
+                raise ValueError(f"session {i}: {len(sp.pages)} pages cannot hold shared_len {sp.shared_len}")
         order = sorted(range(len(rows)), key=lambda i: (rows[i].module, i))
         self.rows = [rows[i] for i in order]
         self.order = order  # batch row j is caller row order[j]

@@ -98,7 +98,7 @@ def test_decode_step_fused_qkv_same_tokens(rows, monkeypatch):
         kv = KVCache(cfg, 4 * S + 2 * S)
         g = torch.Generator(device="cuda").manual_seed(3)
         kv.data.copy_(torch.randn(kv.data.shape, device="cuda", generator=g).to(torch.bfloat16))
-        sess = [SessionSpec(shared_len=40 + s, pages=list(range(4 * s, 4 * s + 4))) for s in range(S)]
+        sess = [SessionSpec(shared_len=40 + s % 24, pages=list(range(4 * s, 4 * s + 4))) for s in range(S)]
         rws = [DecodeRow(module=m, session=s, first_token=5 + s + m, pages=[4 * S + 2 * s + m])
                for s in range(S) for m in range(2)]
         b = DecodeBatch(sess, rws, 2)
