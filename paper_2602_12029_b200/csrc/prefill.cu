@@ -443,14 +443,15 @@ __global__ void __launch_bounds__(THREADS_TC, 1)
 //               O_t += P_t V (M128 N128 K16 per page); issue order
 //               PV0(c) S0(c+1) PV1(c) S1(c+1) so one tile's softmax runs
 //               while the tensor core works on the other tile
-//   warps 2-5   softmax of tile 0, warps 6-9 tile 1 (thread = query row =
-//               TMEM lane): one pass over S (64 fp32 from TMEM), exp2 with
-//               a lazily updated base max (O in TMEM is rescaled only when
-//               the row max grows by > 2^8; the final 1/l makes it exact),
-//               P (bf16) -> TMEM, double-buffered per tile, so softmax(c+1)
-//               never waits for PV(c); the PV MMA takes P as its A operand
-//               from tensor memory (P_SMEM: P -> shared memory in the UMMA
-//               K-major layout, one buffer per tile, the round-1 kernel)
+//   softmax     SPLIT = 2 (default): warps 2-9 tile 0, 10-17 tile 1, two
+//               threads per query row (TMEM lane), 32 keys each, their
+//               partial row maxima swapped through shared memory per chunk;
+//               SPLIT = 1 (PSK_PREFILL_SPLIT=1): warps 2-5 / 6-9, a thread per
+//               row. One pass over S from TMEM, exp2 with a lazily updated
+//               base max (O in TMEM is rescaled only when the row max grows
+//               by > 2^8; the final 1/l makes it exact), P (bf16) -> TMEM,
+//               double-buffered per tile, so softmax(c+1) never waits for
+//               PV(c); the PV MMA takes P as its A operand from tensor memory
 // TMEM columns: S0 [0,64) S1 [64,128) O0 [128,256) O1 [256,384)
 //               P[tile][buffer] [384 + 32 (2 tile + buffer), +32) (bf16 pairs).
 // The producer and MMA warps run warp-converged (all 32 lanes, warp-uniform
@@ -471,29 +472,37 @@ constexpr int NSTG = 3;
 constexpr int KBYTES = CPG * TILE;       // 16 KiB: [dims 0-63 box x 4 pages][dims 64-127 box x 4 pages]
 constexpr int STG = 2 * KBYTES;          // + V 16 KiB: [page][box0 | box1]
 constexpr int QBYTES = 128 * HD * 2;     // 32 KiB per tile: [2 boxes][128 rows][128 B]
-constexpr int PBYTES = 128 * KC * 2;     // 16 KiB per tile: [128 rows][128 B]
 constexpr int OFF_Q = NSTG * STG;
-constexpr int OFF_P = OFF_Q + 2 * QBYTES;
-constexpr int OFF_BAR = OFF_P + 2 * PBYTES;
+constexpr int OFF_XCH = OFF_Q + 2 * QBYTES;  // SPLIT = 2: row max / sum exchange [tile][half][parity][128] fp32
+constexpr int OFF_BAR = OFF_XCH + 4096;
 constexpr int MAXPG = 2560;
 constexpr int OFF_PG = OFF_BAR + 256;
 constexpr int SMEM = OFF_PG + MAXPG * 4 + 1024;
-constexpr int THREADS = 320;
 constexpr float RESCALE_LOG2 = 8.f;      // lazy-rescale threshold (log2 units)
-constexpr uint32_t T_P = 384;            // P buffers in TMEM (P_SMEM = false)
+constexpr uint32_t T_P = 384;            // P buffers in TMEM
+constexpr int threads_of(int split) { return 64 + 2 * 128 * split; }
 
-template <bool P_SMEM>
-__global__ void __launch_bounds__(THREADS, 1)
+// SPLIT softmax threads per query row: 1 (one row per thread, the round-1
+// layout) or 2 (each thread takes 32 of a chunk's 64 keys; the pair -- same
+// TMEM lane quarter, warps 4 apart -- swaps its partial row maxima through
+// shared memory once per chunk, keeps its own partial row sum, and rescales
+// / writes its half of the O row). SPLIT = 2 doubles the softmax warps in
+// flight (18 warps per CTA) for the same work.
+template <int SPLIT>
+__global__ void __launch_bounds__(threads_of(SPLIT), 1)
     prefill_attn_pp(const __grid_constant__ CUtensorMap kvmap, const __grid_constant__ tc::TcParams p) {
+  constexpr int THREADS = threads_of(SPLIT);
+  constexpr int NC = KC / SPLIT;  // keys per softmax thread per chunk
+  constexpr int OC = HD / SPLIT;  // O columns per softmax thread
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  // pv_done[2 t + b]: PV_t of the chunks c with c % 2 == b (P buffer b);
-  // P_SMEM uses b = 0 only
+  // pv_done[2 t + b]: PV_t of the chunks c with c % 2 == b (P buffer b)
   uint64_t *full = bars, *empty = bars + NSTG, *s_full = bars + 2 * NSTG, *p_full = s_full + 2,
            *pv_done = p_full + 2, *s_free = pv_done + 4;
   int* s_pg = reinterpret_cast<int*>(smem + OFF_PG);
+  float* xch = reinterpret_cast<float*>(smem + OFF_XCH);
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkv = p.kv.n_kv_heads;
@@ -526,8 +535,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int t = 0; t < 2; ++t) {
       tma::mbar_init(&s_full[t], 1);
-      tma::mbar_init(&s_free[t], 128);
-      tma::mbar_init(&p_full[t], 128);
+      tma::mbar_init(&s_free[t], 128 * SPLIT);
+      tma::mbar_init(&p_full[t], 128 * SPLIT);
       tma::mbar_init(&pv_done[2 * t], 1);
       tma::mbar_init(&pv_done[2 * t + 1], 1);
     }
@@ -536,7 +545,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   if (warp == 1) umma::tmem_alloc(&s_tmem, 512);
   for (int j = threadIdx.x; j < n_pages && j < MAXPG; j += THREADS) s_pg[j] = pages[j];
-  const uint32_t sq = smem_u32(smem + OFF_Q), sp = smem_u32(smem + OFF_P);
+  const uint32_t sq = smem_u32(smem + OFF_Q);
   // PDL: the page table and items are host-written before the forward; q and
   // the layer's K/V come from the QKV GEMM just before this kernel
   psk::pdl_wait();
@@ -593,21 +602,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     };
     auto issue_pv = [&](int t, int c) {
       const uint32_t vr = smem_u32(smem + (c % NSTG) * STG) + KBYTES;
-      if (P_SMEM) {
-        const uint32_t pt = sp + t * PBYTES;
+      const uint32_t pt = tmem + T_P + (2 * t + (c & 1)) * (KC / 2);
 #pragma unroll
-        for (int pp = 0; pp < CPG; ++pp)
-          umma::mma_e(tmem + 128 + t * HD, umma::desc_k_sw128(pt) + 2 * pp,
-                      umma::desc_mn_sw128(vr + pp * TILE, 2048), ID_PV, (c > 0 || pp > 0) ? 1u : 0u);
-        umma::commit_e(&pv_done[2 * t]);
-      } else {
-        const uint32_t pt = tmem + T_P + (2 * t + (c & 1)) * (KC / 2);
-#pragma unroll
-        for (int pp = 0; pp < CPG; ++pp)
-          umma::mma_ts_e(tmem + 128 + t * HD, pt + pp * 8, umma::desc_mn_sw128(vr + pp * TILE, 2048), ID_PV,
-                         (c > 0 || pp > 0) ? 1u : 0u);
-        umma::commit_e(&pv_done[2 * t + (c & 1)]);
-      }
+      for (int pp = 0; pp < CPG; ++pp)
+        umma::mma_ts_e(tmem + 128 + t * HD, pt + pp * 8, umma::desc_mn_sw128(vr + pp * TILE, 2048), ID_PV,
+                       (c > 0 || pp > 0) ? 1u : 0u);
+      umma::commit_e(&pv_done[2 * t + (c & 1)]);
     };
     tma::mbar_wait(&full[0], 0);
     umma::fence_after();
@@ -625,63 +625,66 @@ __global__ void __launch_bounds__(THREADS, 1)
           umma::fence_after();
           issue_s(t, c + 1);
         }
-        tma::mbar_wait(&p_full[t], c & 1);  // P_t(c) written, O_t settled
+        tma::mbar_wait(&p_full[t], c & 1);  // P_t(c) written
         umma::fence_after();
         issue_pv(t, c);
       }
       umma::commit_e(&empty[c % NSTG]);  // K/V stage free once both PVs completed
     }
   } else {
-    const int t = (warp - 2) >> 2;   // tile
-    const int lq = (warp & 3) * 32;  // TMEM lane quarter of this warp
-    const int g = lq + lane;         // row in the tile
-    const int r = t * 128 + g;       // row in the CTA
-    const uint32_t tS = tmem + ((uint32_t)lq << 16) + t * KC;
-    const uint32_t tO = tmem + ((uint32_t)lq << 16) + 128 + t * HD;
-    const uint32_t prow = sp + t * PBYTES + g * 128;
-    const uint32_t tP = tmem + ((uint32_t)lq << 16) + T_P;
+    const int sw = warp - 2;
+    const int t = sw >> (SPLIT == 2 ? 3 : 2);            // tile
+    const int hf = SPLIT == 2 ? (sw >> 2) & 1 : 0;       // half of the chunk's keys / of the O row
+    const int lq = (warp & 3) * 32;                      // TMEM lane quarter of this warp
+    const int g = lq + lane;                             // row in the tile
+    const int r = t * 128 + g;                           // row in the CTA
+    const int bar_id = 1 + t * 4 + (warp & 3);           // SPLIT = 2: the pair's named barrier
+    const uint32_t tS = tmem + ((uint32_t)lq << 16) + t * KC + hf * NC;
+    const uint32_t tO = tmem + ((uint32_t)lq << 16) + 128 + t * HD + hf * OC;
+    const uint32_t tP = tmem + ((uint32_t)lq << 16) + T_P + hf * (NC / 2);
     const int qpos = pos0 + t0 + r / p.grp;  // keys [0, qpos] visible
     float m_used = -INFINITY, l = 0.f;
     for (int c = 0; c < nch; ++c) {
-      const int key0 = c * KC;
+      const int key0 = c * KC + hf * NC;
       tma::mbar_wait(&s_full[t], c & 1);
       umma::fence_after();
-      uint32_t sr[KC];
-      umma::ld32_async(tS, sr);
-      umma::ld32_async(tS + 32, sr + 32);
+      uint32_t sr[NC];
+#pragma unroll
+      for (int k = 0; k < NC / 32; ++k) umma::ld32_async(tS + 32 * k, sr + 32 * k);
       umma::wait_ld();
       umma::fence_before();
       tma::mbar_arrive(&s_free[t]);  // S_t may be overwritten by S_t(c+1)
       // causal mask only on the chunks that cross the warp's diagonal
-      if (!__all_sync(0xffffffffu, key0 + KC - 1 <= qpos)) {
+      if (!__all_sync(0xffffffffu, key0 + NC - 1 <= qpos)) {
 #pragma unroll
-        for (int e = 0; e < KC; ++e)
+        for (int e = 0; e < NC; ++e)
           if (key0 + e > qpos) sr[e] = __float_as_uint(-INFINITY);
       }
       // tree max of the raw scores (no serial chain), then into log2 units
-      float tm[KC / 2];
+      float tm[NC / 2];
 #pragma unroll
-      for (int k = 0; k < KC / 2; ++k) tm[k] = fmaxf(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1]));
+      for (int k = 0; k < NC / 2; ++k) tm[k] = fmaxf(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1]));
 #pragma unroll
-      for (int w = KC / 4; w >= 1; w >>= 1)
+      for (int w = NC / 4; w >= 1; w >>= 1)
 #pragma unroll
         for (int k = 0; k < w; ++k) tm[k] = fmaxf(tm[k], tm[k + w]);
-      const float mx = tm[0] * p.scale_log2;
-      // P_SMEM: PV_t(c-1) must be done before P_t is overwritten or O_t
-      // rescaled. TMEM P: PV_t(c-2) before P buffer c % 2 is overwritten,
-      // PV_t(c-1) only before a rescale of O_t.
-      if (P_SMEM) {
-        if (c > 0) tma::mbar_wait(&pv_done[2 * t], (c - 1) & 1);
-      } else if (c > 1) {
-        tma::mbar_wait(&pv_done[2 * t + (c & 1)], ((c >> 1) - 1) & 1);
+      float rmax = tm[0];
+      if (SPLIT == 2) {  // the row's other half (double-buffered by chunk parity)
+        xch[((t * 2 + hf) * 2 + (c & 1)) * 128 + g] = rmax;
+        named_barrier_sync(bar_id, 64);
+        rmax = fmaxf(rmax, xch[((t * 2 + (hf ^ 1)) * 2 + (c & 1)) * 128 + g]);
       }
+      const float mx = rmax * p.scale_log2;
+      // PV_t(c-2) before P buffer c % 2 is overwritten; PV_t(c-1) only
+      // before a rescale of O_t
+      if (c > 1) tma::mbar_wait(&pv_done[2 * t + (c & 1)], ((c >> 1) - 1) & 1);
       const bool grow = mx > m_used + RESCALE_LOG2 || (m_used == -INFINITY && mx > -INFINITY);
       if (__any_sync(0xffffffffu, grow && c > 0)) {
-        if (!P_SMEM) tma::mbar_wait(&pv_done[2 * t + ((c - 1) & 1)], ((c - 1) >> 1) & 1);
+        tma::mbar_wait(&pv_done[2 * t + ((c - 1) & 1)], ((c - 1) >> 1) & 1);
         umma::fence_after();
         const float alpha = grow ? exp2f(m_used - mx) : 1.f;
 #pragma unroll 1
-        for (int q = 0; q < HD / 32; ++q) {
+        for (int q = 0; q < OC / 32; ++q) {
           uint32_t o[32];
           umma::ld32_async(tO + q * 32, o);
           umma::wait_ld();
@@ -694,10 +697,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (grow) m_used = mx;
       const float base = m_used == -INFINITY ? 0.f : m_used;
-      float ls[KC / 8];
-      uint32_t pk[KC / 2];
+      float ls[NC / 8];
+      uint32_t pk[NC / 2];
 #pragma unroll
-      for (int q = 0; q < KC / 8; ++q) {
+      for (int q = 0; q < NC / 8; ++q) {
         float pf[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {  // p = 2^(s * scale - m); masked: 2^-inf = 0
@@ -707,37 +710,38 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         ls[q] = ((pf[0] + pf[1]) + (pf[2] + pf[3])) + ((pf[4] + pf[5]) + (pf[6] + pf[7]));
         const uint4 v = f32_to_bf16x8(pf);
-        if (P_SMEM) {
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(prow + (((q ^ (g & 7))) << 4)), "r"(v.x),
-                       "r"(v.y), "r"(v.z), "r"(v.w));
-        } else {
-          pk[4 * q] = v.x;
-          pk[4 * q + 1] = v.y;
-          pk[4 * q + 2] = v.z;
-          pk[4 * q + 3] = v.w;
-        }
+        pk[4 * q] = v.x;
+        pk[4 * q + 1] = v.y;
+        pk[4 * q + 2] = v.z;
+        pk[4 * q + 3] = v.w;
       }
-      l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
-      if (P_SMEM) {
-        umma::fence_proxy_async();
-      } else {
+#pragma unroll
+      for (int w = NC / 16; w >= 1; w >>= 1)
+#pragma unroll
+        for (int k = 0; k < w; ++k) ls[k] += ls[k + w];
+      l += ls[0];
+      if (SPLIT == 2)
+        umma::st16(tP + (2 * t + (c & 1)) * (KC / 2), pk);
+      else
         umma::st32(tP + (2 * t + (c & 1)) * (KC / 2), pk);
-        umma::wait_st();
-      }
+      umma::wait_st();
       umma::fence_before();
       tma::mbar_arrive(&p_full[t]);
     }
-    // epilogue: O_t / l -> bf16 rows of the output
-    if (P_SMEM)
-      tma::mbar_wait(&pv_done[2 * t], (nch - 1) & 1);
-    else
-      tma::mbar_wait(&pv_done[2 * t + ((nch - 1) & 1)], ((nch - 1) >> 1) & 1);
+    if (SPLIT == 2) {  // the row sum: this half's + the other's
+      named_barrier_sync(bar_id, 64);  // the last chunk's max reads are done
+      xch[(t * 2 + hf) * 2 * 128 + g] = l;
+      named_barrier_sync(bar_id, 64);
+      l += xch[(t * 2 + (hf ^ 1)) * 2 * 128 + g];
+    }
+    // epilogue: this thread's OC columns of O_t / l -> bf16 row of the output
+    tma::mbar_wait(&pv_done[2 * t + ((nch - 1) & 1)], ((nch - 1) >> 1) & 1);
     umma::fence_after();
     const int tpos = t0 + r / p.grp;
     const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* dst = odst + ((int64_t)tpos * p.nq + h * p.grp + r % p.grp) * HD;
+    __nv_bfloat16* dst = odst + ((int64_t)tpos * p.nq + h * p.grp + r % p.grp) * HD + hf * OC;
 #pragma unroll 1
-    for (int q = 0; q < HD / 32; ++q) {
+    for (int q = 0; q < OC / 32; ++q) {
       uint32_t o[32];
       umma::ld32_async(tO + q * 32, o);
       umma::wait_ld();
@@ -761,17 +765,22 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 typedef void (*KernelFn)(const CUtensorMap, const tc::TcParams);
+struct Variant {
+  KernelFn fn;
+  int threads;
+};
 
-// The K3 variant in use (PSK_PREFILL_PSMEM=1: P through shared memory), its
-// shared-memory attribute set once.
-static KernelFn kernel() {
-  static KernelFn fn = nullptr;
-  if (!fn) {
-    const KernelFn f = getenv("PSK_PREFILL_PSMEM") ? prefill_attn_pp<true> : prefill_attn_pp<false>;
-    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess) return f;
-    fn = f;
+// The K3 variant in use (PSK_PREFILL_SPLIT=1: one softmax thread per row),
+// its shared-memory attribute set once.
+static Variant kernel() {
+  static Variant v{nullptr, 0};
+  if (!v.fn) {
+    const bool one = getenv("PSK_PREFILL_SPLIT") && getenv("PSK_PREFILL_SPLIT")[0] == '1';
+    const Variant c = one ? Variant{prefill_attn_pp<1>, threads_of(1)} : Variant{prefill_attn_pp<2>, threads_of(2)};
+    if (cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess) return c;
+    v = c;
   }
-  return fn;
+  return v;
 }
 
 }  // namespace pp
@@ -834,8 +843,9 @@ int psk_prefill_attn(const void* q_rot, int32_t T, int32_t pos0, int32_t n_q_hea
     if (!tc1) {
       t.qb = 256 / grp;
       t.n_qblocks = (T + t.qb - 1) / t.qb;
-      PSK_CUDA_TRY(psk::launch_pdl(pp::kernel(), dim3(t.n_qblocks * kv.n_kv_heads), dim3(pp::THREADS),
-                                   (size_t)pp::SMEM, psk::as_stream(stream), map, t));
+      const pp::Variant v = pp::kernel();
+      PSK_CUDA_TRY(psk::launch_pdl(v.fn, dim3(t.n_qblocks * kv.n_kv_heads), dim3(v.threads), (size_t)pp::SMEM,
+                                   psk::as_stream(stream), map, t));
       PSK_LAUNCH_CHECK();
       return PSK_OK;
     }
@@ -886,8 +896,9 @@ int psk_prefill_attn_batch(const void* q_rot, int32_t n_items, const int32_t* it
   t.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
   t.qb = 256 / grp;
   t.items = items;
-  PSK_CUDA_TRY(psk::launch_pdl(pp::kernel(), dim3(n_items * kv.n_kv_heads), dim3(pp::THREADS),
-                               (size_t)pp::SMEM, psk::as_stream(stream), map, t));
+  const pp::Variant v = pp::kernel();
+  PSK_CUDA_TRY(psk::launch_pdl(v.fn, dim3(n_items * kv.n_kv_heads), dim3(v.threads), (size_t)pp::SMEM,
+                               psk::as_stream(stream), map, t));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }
