@@ -184,3 +184,16 @@ def test_k6_bench_shape_32_sessions_x4():
     rng = np.random.default_rng(5)
     _k6_case([4095] * 32, [4] * 32, rng.integers(0, 256, 128).tolist(), seed=22)
 
+
+
+def test_k3_one_thread_per_row_variant():
+    """The K3 variant with one softmax thread per query row
+    (PSK_PREFILL_SPLIT=1, read once per process: the K3 cases above rerun in
+    a child) matches the fp32 reference as the default two-thread kernel does."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PSK_PREFILL_SPLIT="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", __file__, "-k", "k3 and not variant",
+                        "-p", "no:cacheprovider"], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

@@ -177,3 +177,14 @@ def test_8b_shape_twenty_rows_per_module():
     runner, res = _run_case(cfg, prompts, [(m, s) for s in range(20) for m in range(2)], max_new=3)
     assert runner.use_tc_gemv
     assert sum(f for _, _, f in res) <= 4
+
+
+def test_decode_batch_rejects_short_page_tables():
+    """A session whose page list cannot hold its shared length would make the
+    kernels read page ids past the table: DecodeBatch refuses it."""
+    from paper_2602_12029_b200.model import DecodeBatch, DecodeRow, SessionSpec
+    with pytest.raises(ValueError):
+        DecodeBatch([SessionSpec(shared_len=65, pages=[0, 1, 2, 3])],
+                    [DecodeRow(module=0, session=0, first_token=1, pages=[4])], 1)
+    DecodeBatch([SessionSpec(shared_len=64, pages=[0, 1, 2, 3])],
+                [DecodeRow(module=0, session=0, first_token=1, pages=[4])], 1)
