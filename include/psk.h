@@ -213,6 +213,17 @@ int psk_gemv_tc(const void* x, int32_t n_rows, int32_t K, const void* const* W_h
 int psk_gemv_tc_qkv_rope(const void* x, int32_t K, const void* const* W_host, const psk_decode_batch* b,
                          int32_t max_rows_per_mod, int32_t n_q_heads, const float* rope, int32_t layer,
                          psk_kv_layout kv, void* q_rot, void* workspace, void* stream);
+/* K5-TC residual projection with the next RMSNorm fused (o-proj -> MLP norm,
+ * down-proj -> next layer's attention norm): h[r,:] += y, then
+ * xn[r,:] = bf16(h[r,:] * rsqrt(mean(h[r,:]^2) + eps) * gamma[module]),
+ * as psk_gemv_tc(PSK_EPI_RESID_ADD) followed by psk_rmsnorm_rows (sums of
+ * squares in another order). When one CTA per 128-row unit fits the SMs
+ * the units of a module meet at an in-kernel grid barrier; otherwise the
+ * call runs those two kernels. Same workspace as psk_gemv_tc. */
+int psk_gemv_tc_resid_norm(const void* x, int32_t n_rows, int32_t K, const void* const* W_host,
+                           const int32_t* mod_row_start, int32_t n_mod, int32_t max_rows_per_mod, int32_t N,
+                           float* h, const void* const* gamma, const int32_t* row_mod, float eps, void* xn,
+                           void* workspace, void* stream);
 /* Bytes of the psk_gemv_tc workspace (stream-K partials + flags); allocate
  * once ZEROED and reuse for every call on the stream (the kernel leaves the
  * flags zeroed). */

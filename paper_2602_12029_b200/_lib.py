@@ -100,6 +100,7 @@ _SIGS: dict[str, list] = {
     "psk_gemv": [_P, _I32, _I32, _P, _P, _I32, _I32, _I32, _I32, _P, _P],
     "psk_gemv_tc": [_P, _I32, _I32, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P],
     "psk_gemv_tc_workspace": [C.POINTER(_I64)],
+    "psk_gemv_tc_resid_norm": [_P, _I32, _I32, _P, _P, _I32, _I32, _I32, _P, _P, _P, _F, _P, _P, _P],
     "psk_gemv_tc_qkv_rope": [_P, _I32, _P, C.POINTER(DecodeBatchC), _I32, _I32, _P, _I32, KVLayout, _P, _P, _P],
     "psk_rope_append": [C.POINTER(DecodeBatchC), _P, _I32, _P, _I32, KVLayout, _P, _P],
     "psk_decode_attn_workspace": [C.POINTER(DecodeBatchC), _I32, _I32, C.POINTER(_I64)],

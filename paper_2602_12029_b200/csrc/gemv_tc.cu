@@ -67,13 +67,24 @@ struct Maps {
 
 // EPI_QKV_ROPE (psk_gemv_tc_qkv_rope): the decode step's QKV projection with
 // RoPE + KV append fused (replaces psk_gemv_tc(STORE_F32) + psk_rope_append).
+// EPI_RESID_NORM (psk_gemv_tc_resid_norm): residual add + the next RMSNorm
+// (replaces psk_gemv_tc(RESID_ADD) + psk_rmsnorm_rows); one CTA per whole
+// unit, the module's units meet at a grid barrier to sum their rows' squares.
 constexpr int EPI_QKV_ROPE = 16;
+constexpr int EPI_RESID_NORM = 17;
+constexpr int NORM_MAXNB = 64;  // 128-row units per module (N <= 8192)
 struct RopeArgs {
   psk_decode_batch b;
   psk_kv_layout kv;
   const float* rope;       // [max_pos][64][2] (cos, sin)
   __nv_bfloat16* q_rot;    // [n_rows][nq][128]
   int nq, layer;
+  // EPI_RESID_NORM
+  const __nv_bfloat16* const* gamma;  // per module of the batch
+  __nv_bfloat16* xn;                  // [n_rows][N] bf16(h * rsqrt(mean(h^2) + eps) * gamma)
+  float eps;
+  float* ssq;                         // [MAXMOD][64 rows][NORM_MAXNB] per-unit partial sums of squares
+  unsigned* cnt;                      // [MAXMOD][2] arrived / departed (zero between launches)
 };
 
 __device__ __forceinline__ void tmem_ld32_cols(uint32_t taddr, float* v) {
@@ -112,7 +123,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                    void* __restrict__ out, float* __restrict__ part, int* __restrict__ flags,
                    const __grid_constant__ RopeArgs ra) {
   using C = Cfg<MN, UW>;
-  static_assert(EPI != EPI_QKV_ROPE || UW == 1, "QKV epilogue: one head (128 rows) per unit");
+  static_assert((EPI != EPI_QKV_ROPE && EPI != EPI_RESID_NORM) || UW == 1, "one 128-row block per unit");
   constexpr int UB = UW * BN;  // weight rows per unit
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -286,7 +297,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int n = blk * UB + u * BN + r;
       float v[MN];
       // residual prefetch: its latency overlaps this segment's MMAs
-      if (EPI == PSK_EPI_RESID_ADD && owner) {
+      if ((EPI == PSK_EPI_RESID_ADD || EPI == EPI_RESID_NORM) && owner) {
 #pragma unroll
         for (int m = 0; m < MN; ++m)
           v[m] = m < M ? reinterpret_cast<const float*>(out)[(int64_t)(xb + m) * N + n] : 0.f;
@@ -417,7 +428,54 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (m >= M) break;
           const int64_t o = (int64_t)(xb + m) * N + n;
           if (EPI == PSK_EPI_STORE_BF16) reinterpret_cast<__nv_bfloat16*>(out)[o] = f2bf(v[m]);
-          if (EPI == PSK_EPI_STORE_F32 || EPI == PSK_EPI_RESID_ADD) reinterpret_cast<float*>(out)[o] = v[m];
+          if (EPI == PSK_EPI_STORE_F32 || EPI == PSK_EPI_RESID_ADD || EPI == EPI_RESID_NORM)
+            reinterpret_cast<float*>(out)[o] = v[m];
+        }
+        if (EPI == EPI_RESID_NORM) {
+          // this unit's 128 features of each row: sum of squares -> ssq; then,
+          // once every unit of the module has published (grid barrier: all
+          // CTAs co-resident, one per unit), each row's rstd from the nb
+          // partials in a fixed order and the normalised features -> xn
+          float* red = xch;  // [4 lane quarters][MN]
+#pragma unroll
+          for (int m = 0; m < MN; ++m) {
+            float sq = m < M ? v[m] * v[m] : 0.f;
+            sq = warp_sum(sq);
+            if (lane == 0) red[q * MN + m] = sq;
+          }
+          named_barrier_sync(3, 128);
+          const int t = threadIdx.x - 64;
+          float* part = ra.ssq + (int64_t)mod * 64 * NORM_MAXNB;
+          if (t < M) part[t * NORM_MAXNB + blk] = (red[t] + red[MN + t]) + (red[2 * MN + t] + red[3 * MN + t]);
+          named_barrier_sync(3, 128);
+          unsigned* cnt = ra.cnt + 2 * mod;
+          if (threadIdx.x == 64) {
+            __threadfence();
+            atomicAdd(cnt, 1u);
+            unsigned arrived;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(arrived) : "l"(cnt) : "memory");
+            } while (arrived < (unsigned)nb);
+            __threadfence();
+          }
+          named_barrier_sync(3, 128);
+          if (t < M) {
+            float tot = 0.f;
+            for (int b = 0; b < nb; ++b) tot += __ldcg(part + t * NORM_MAXNB + b);
+            red[t] = rsqrtf(tot / (float)N + ra.eps);
+          }
+          named_barrier_sync(3, 128);
+          const float gm = bf2f(ra.gamma[mod][n]);
+#pragma unroll
+          for (int m = 0; m < MN; ++m) {
+            if (m >= M) break;
+            ra.xn[(int64_t)(xb + m) * N + n] = f2bf(v[m] * red[m] * gm);
+          }
+          named_barrier_sync(3, 128);  // red reads done before a next unit (none: one unit per CTA)
+          if (threadIdx.x == 64 && atomicAdd(cnt + 1, 1u) == (unsigned)nb - 1) {  // every unit has left the wait
+            cnt[0] = 0;
+            cnt[1] = 0;
+          }
         }
       }
       }  // u
@@ -490,7 +548,8 @@ static int launch_uw(const void* x, int n_rows, int K, const void* const* W_host
   auto k = gemv_tc_kernel<MN, EPI, UW>;
   // + the QKV epilogue's exchange tile and row table
   constexpr int smem_bytes = Cfg<MN, UW>::SMEM + (EPI == EPI_QKV_ROPE ? MN * BN * 4 + MN * 4 * 4 : 0) +
-                             (EPI == EPI_QKV_ROPE && MN == 32 ? MN * 64 * 8 : 0);
+                             (EPI == EPI_QKV_ROPE && MN == 32 ? MN * 64 * 8 : 0) +
+                             (EPI == EPI_RESID_NORM ? 4 * MN * 4 : 0);
   static_assert(smem_bytes <= 232448, "shared memory");
   static bool attr = false;
   if (!attr) {
@@ -544,11 +603,44 @@ static int dispatch(int epi, const void* x, int n_rows, int K, const void* const
 }  // namespace gemv_tc
 }  // namespace psk
 
+static int64_t part_bytes() { return (int64_t)psk::device_sms() * 2 * 64 * psk::gemv_tc::BN * 4; }  // UW <= 2 x MN <= 64
+
 extern "C" int psk_gemv_tc_workspace(int64_t* bytes) {
   PSK_CHECK_ARG(bytes != nullptr, "psk_gemv_tc_workspace: null out");
   using namespace psk::gemv_tc;
-  *bytes = FLAG_BYTES + (int64_t)psk::device_sms() * 2 * 64 * BN * 4;  // UW <= 2 blocks x MN <= 64 rows
+  // flags | stream-K partials | RMSNorm-epilogue counters + partial sums of squares
+  *bytes = FLAG_BYTES + part_bytes() + 256 + (int64_t)MAXMOD * 64 * NORM_MAXNB * 4;
   return PSK_OK;
+}
+
+extern "C" int psk_gemv_tc_resid_norm(const void* x, int32_t n_rows, int32_t K, const void* const* W_host,
+                                      const int32_t* mod_row_start, int32_t n_mod, int32_t max_rows_per_mod,
+                                      int32_t N, float* h, const void* const* gamma, const int32_t* row_mod,
+                                      float eps, void* xn, void* workspace, void* stream) {
+  using namespace psk::gemv_tc;
+  PSK_CHECK_ARG(x && W_host && mod_row_start && h && gamma && xn && workspace && n_rows >= 0 && K > 0 &&
+                    K % 64 == 0 && n_mod > 0 && n_mod <= MAXMOD && N > 0 && N % BN == 0,
+                "psk_gemv_tc_resid_norm: bad args");
+  if (n_rows == 0) return PSK_OK;
+  const int maxm = max_rows_per_mod > 0 ? max_rows_per_mod : n_rows;
+  cudaStream_t s = psk::as_stream(stream);
+  static const bool whole_units = !(getenv("PSK_GEMV_GRID") && getenv("PSK_GEMV_GRID")[0] == '0');
+  const bool fused = whole_units && (int64_t)n_mod * (N / BN) <= sm_count() && N / BN <= NORM_MAXNB && maxm <= 64;
+  if (!fused) {  // the stream-K split (or > 64 rows): residual GEMV, then the norm kernel
+    const int rc = psk_gemv_tc(x, n_rows, K, W_host, mod_row_start, n_mod, max_rows_per_mod, N, PSK_EPI_RESID_ADD,
+                               h, workspace, stream);
+    return rc ? rc : psk_rmsnorm_rows(h, n_rows, N, gamma, row_mod, eps, xn, stream);
+  }
+  RopeArgs ra{};
+  ra.gamma = reinterpret_cast<const __nv_bfloat16* const*>(gamma);
+  ra.xn = reinterpret_cast<__nv_bfloat16*>(xn);
+  ra.eps = eps;
+  char* w = reinterpret_cast<char*>(workspace) + FLAG_BYTES + part_bytes();
+  ra.cnt = reinterpret_cast<unsigned*>(w);
+  ra.ssq = reinterpret_cast<float*>(w + 256);
+  if (maxm <= 16) return launch_uw<16, EPI_RESID_NORM, 1>(x, n_rows, K, W_host, mod_row_start, n_mod, N, h, workspace, s, ra);
+  if (maxm <= 32) return launch_uw<32, EPI_RESID_NORM, 1>(x, n_rows, K, W_host, mod_row_start, n_mod, N, h, workspace, s, ra);
+  return launch_uw<64, EPI_RESID_NORM, 1>(x, n_rows, K, W_host, mod_row_start, n_mod, N, h, workspace, s, ra);
 }
 
 extern "C" int psk_gemv_tc_qkv_rope(const void* x, int32_t K, const void* const* W_host, const psk_decode_batch* b,

@@ -443,12 +443,22 @@ class DecodeRunner:
         # vs 13.35-13.37 ms apart (the epilogue's head-pair exchange and row
         # table sit on the stream-K owners' critical path), so it is off
         self.fused_qkv = self.use_tc_gemv and os.environ.get("PSK_FUSED_QKV", "0") == "1"
+        # K5-TC: the o-proj / down-proj residual GEMVs also write the next
+        # RMSNorm's output (psk_gemv_tc_resid_norm) with PSK_FUSED_NORM=1.
+        # Correct but slower: the in-kernel grid barrier over a module's
+        # units holds every CTA until the slowest, so the next GEMV can no
+        # longer stream its weights under this one's tail (13.68-13.69 vs
+        # 13.32-13.36 ms per step at 32 rows/module); off by default
+        self.fused_norm = self.use_tc_gemv and os.environ.get("PSK_FUSED_NORM", "0") == "1"
         # K6 launches 1 kernel when the fan-out kernel merges its splits
         # itself, else 2 (partial + merge)
         n_attn = C.c_int32()
         _lib.check(self.lib.psk_decode_attn_kernels(batch.c_ref(), cfg.n_heads, cfg.n_kv_heads, self.splits,
                                                     C.byref(n_attn)))
-        self.launches_per_step = 1 + L * (7 + n_attn.value - self.fused_qkv) + 3
+        norm_fused = self.fused_norm and batch.n_mod * (cfg.d_model // 128) <= sms and batch.max_rpm <= 64
+        # embed, L x [norm, qkv, rope, attention, o, norm, gate/up, down], final norm, head, argmax; the
+        # fused norms drop 2 launches per layer (layer 0's norm stays, the final norm rides the last down GEMV)
+        self.launches_per_step = 1 + L * (7 + n_attn.value - self.fused_qkv - 2 * norm_fused) + 3
 
     def _gemv(self, x, K: int, p_dev, p_host, N: int, epi: int, out, s: int) -> None:
         """K5 (mma.sync, <= 8 rows per module) or K5-TC (tcgen05, 9..64)."""
@@ -460,6 +470,13 @@ class DecodeRunner:
             _lib.check(self.lib.psk_gemv(_ptr(x), b.n_rows, K, _ptr(p_dev), _ptr(b.t_mrs), b.n_mod, b.max_rpm, N,
                                          epi, _ptr(out), s))
 
+    def _gemv_norm(self, x, K: int, p_host, gamma, s: int) -> None:
+        """K5-TC residual GEMV (h += W x) + the next RMSNorm (xn) in one call."""
+        b, cfg = self.b, self.cfg
+        _lib.check(self.lib.psk_gemv_tc_resid_norm(_ptr(x), b.n_rows, K, p_host, _ptr(b.t_mrs), b.n_mod, b.max_rpm,
+                                                   cfg.d_model, _ptr(self.h), _ptr(gamma), _ptr(b.t_row_mod),
+                                                   C.c_float(cfg.norm_eps), _ptr(self.xn), _ptr(self.gemv_ws), s))
+
     # -- one step, eager ----------------------------------------------------
     def _step(self, s: int) -> None:
         lib, cfg, b = self.lib, self.cfg, self.b
@@ -470,8 +487,9 @@ class DecodeRunner:
         gemv = self._gemv
         chk(lib.psk_embed_rows(bc, _ptr(self.p_embed), d, _ptr(self.h), s))
         for l in range(cfg.n_layers):
-            chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_attn_norm[l]), _ptr(b.t_row_mod),
-                                     C.c_float(cfg.norm_eps), _ptr(self.xn), s))
+            if l == 0 or not self.fused_norm:  # (fused: the previous down GEMV wrote this norm)
+                chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_attn_norm[l]), _ptr(b.t_row_mod),
+                                         C.c_float(cfg.norm_eps), _ptr(self.xn), s))
             if self.fused_qkv:
                 chk(lib.psk_gemv_tc_qkv_rope(_ptr(self.xn), d, self.h_wqkv[l], bc, b.max_rpm, cfg.n_heads,
                                              _ptr(self.rope), l, kvl, _ptr(self.q_rot), _ptr(self.gemv_ws), s))
@@ -481,13 +499,21 @@ class DecodeRunner:
                                         _ptr(self.q_rot), s))
             chk(lib.psk_decode_attn(bc, _ptr(self.q_rot), cfg.n_heads, l, kvl, self.splits,
                                     _ptr(self.ws), _ptr(self.attn), s))
-            gemv(self.attn, cfg.n_heads * cfg.head_dim, self.p_wo[l], self.h_wo[l], d, 2, self.h, s)
-            chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_mlp_norm[l]), _ptr(b.t_row_mod),
-                                     C.c_float(cfg.norm_eps), _ptr(self.xn), s))
+            if self.fused_norm:  # residual GEMV + the MLP norm in one launch
+                self._gemv_norm(self.attn, cfg.n_heads * cfg.head_dim, self.h_wo[l], self.p_mlp_norm[l], s)
+            else:
+                gemv(self.attn, cfg.n_heads * cfg.head_dim, self.p_wo[l], self.h_wo[l], d, 2, self.h, s)
+                chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_mlp_norm[l]), _ptr(b.t_row_mod),
+                                         C.c_float(cfg.norm_eps), _ptr(self.xn), s))
             gemv(self.xn, d, self.p_wgu[l], self.h_wgu[l], 2 * cfg.ffn, 3, self.act, s)
-            gemv(self.act, cfg.ffn, self.p_wdown[l], self.h_wdown[l], d, 2, self.h, s)
-        chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_final_norm), _ptr(b.t_row_mod),
-                                 C.c_float(cfg.norm_eps), _ptr(self.xn), s))
+            nxt = self.p_attn_norm[l + 1] if l + 1 < cfg.n_layers else self.p_final_norm
+            if self.fused_norm:  # residual GEMV + the next layer's attention norm (or the final norm)
+                self._gemv_norm(self.act, cfg.ffn, self.h_wdown[l], nxt, s)
+            else:
+                gemv(self.act, cfg.ffn, self.p_wdown[l], self.h_wdown[l], d, 2, self.h, s)
+        if not self.fused_norm:
+            chk(lib.psk_rmsnorm_rows(_ptr(self.h), R, d, _ptr(self.p_final_norm), _ptr(b.t_row_mod),
+                                     C.c_float(cfg.norm_eps), _ptr(self.xn), s))
         gemv(self.xn, d, self.p_head, self.h_head, cfg.vocab, 1, self.logits, s)
         chk(lib.psk_argmax_advance(bc, _ptr(self.logits), cfg.vocab, _ptr(self.out_tokens),
                                    self.max_new, s))

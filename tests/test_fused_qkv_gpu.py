@@ -110,3 +110,32 @@ def test_decode_step_fused_qkv_same_tokens(rows, monkeypatch):
     assert torch.equal(out[0][0], out[1][0])  # (fused, unfused)
     assert torch.equal(out[0][1], out[1][1])
     assert torch.equal(out[0][2].view(torch.int16), out[1][2].view(torch.int16))
+
+
+@pytest.mark.parametrize("rows", [12, 40])
+def test_decode_step_fused_norm_close(rows, monkeypatch):
+    """PSK_FUSED_NORM=1 (residual GEMV + next RMSNorm in one launch, grid
+    barrier over a module's units) vs the separate norm kernels: the sums of
+    squares add in another order, so logits agree to bf16 rounding, and the
+    greedy tokens agree except at near-ties."""
+    from paper_2602_12029_b200.model import (DecodeBatch, DecodeRow, DecodeRunner, KVCache, LlamaConfig,
+                                             ModuleWeights, SessionSpec)
+    cfg = LlamaConfig.tiny()
+    mods = [ModuleWeights(cfg, 11 + i) for i in range(2)]
+    out = []
+    S = rows
+    for fused in ("1", "0"):
+        monkeypatch.setenv("PSK_FUSED_NORM", fused)
+        kv = KVCache(cfg, 4 * S + 2 * S)
+        g = torch.Generator(device="cuda").manual_seed(3)
+        kv.data.copy_(torch.randn(kv.data.shape, device="cuda", generator=g).to(torch.bfloat16))
+        sess = [SessionSpec(shared_len=40 + s % 24, pages=list(range(4 * s, 4 * s + 4))) for s in range(S)]
+        rws = [DecodeRow(module=m, session=s, first_token=5 + s + m, pages=[4 * S + 2 * s + m])
+               for s in range(S) for m in range(2)]
+        r = DecodeRunner(cfg, mods, kv, DecodeBatch(sess, rws, 2), 8)
+        assert r.fused_norm == (fused == "1")
+        r.run(1)
+        torch.cuda.synchronize()
+        out.append(r.logits.clone())
+    a, b = out
+    assert (a - b).abs().max().item() <= 2e-2 * b.abs().max().item()
