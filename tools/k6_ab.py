@@ -13,6 +13,8 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 SHAPES = [(32767, 16, 1, 1), (32767, 8, 1, 1), (4095, 16, 1, 1), (4095, 16, 8, 16), (16383, 16, 2, 1)]
+if os.environ.get("K6_SHAPES"):  # "shared:modules:sessions:priv,..."
+    SHAPES = [tuple(int(v) for v in x.split(":")) for x in os.environ["K6_SHAPES"].split(",")]
 
 if len(sys.argv) > 1 and sys.argv[1] == "child":
     sys.path.insert(0, str(ROOT))
