@@ -177,9 +177,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      for (int m = 0; m < n_mod && m < MAXMOD; ++m) tma::prefetch_map(&maps.w[m]);
-      tma::prefetch_map(&maps.x);
+    // warp-converged (all lanes, warp-uniform operands, one elected lane
+    // issues): from if (lane == 0) every TMA / MMA became an R2UR waterfall loop
+    {
+      if (lane == 0) {
+        for (int m = 0; m < n_mod && m < MAXMOD; ++m) tma::prefetch_map(&maps.w[m]);
+        tma::prefetch_map(&maps.x);
+      }
+      __syncwarp();
       // x rows come from the previous kernel: the first ring fill issues the
       // weight boxes at once and the x boxes after the PDL wait
       int pend_k[C::STAGES], pend_n[C::STAGES], pend_row[C::STAGES];
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       int j = 0;  // stage counter
       auto load_x = [&](int s, int k0c, int n, int row) {
         for (int b = 0; b < n; ++b)
-          tma::load_2d(&maps.x, &full[s], smem + s * C::STAGE + C::CH * UW * A_BYTES + b * C::B_BYTES,
+          tma::load_2d_e(&maps.x, &full[s], smem + s * C::STAGE + C::CH * UW * A_BYTES + b * C::B_BYTES,
                        (k0c + b) * BK, row);
       };
       for (int c = c0; c < c1;) {
@@ -206,11 +211,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             waited = true;
           }
           tma::mbar_wait(&empty[s], ((j / C::STAGES) & 1) ^ 1);
-          tma::mbar_expect_tx(&full[s], n * (UW * A_BYTES + C::B_BYTES));
+          tma::mbar_expect_tx_e(&full[s], n * (UW * A_BYTES + C::B_BYTES));
           unsigned char* st = smem + s * C::STAGE;
           for (int b = 0; b < n; ++b)
             for (int u = 0; u < UW; ++u)
-              tma::load_2d(&maps.w[mod], &full[s], st + (b * UW + u) * A_BYTES, (kc + b) * BK, blk * UB + u * BN);
+              tma::load_2d_e(&maps.w[mod], &full[s], st + (b * UW + u) * A_BYTES, (kc + b) * BK, blk * UB + u * BN);
           if (waited) {
             load_x(s, kc, n, xb);
           } else {
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       constexpr uint32_t idesc = umma::idesc_bf16(BN, MN, false);
       int j = 0, it = 0;
       for (int c = c0; c < c1;) {
@@ -251,12 +256,12 @@ __global__ void __launch_bounds__(THREADS, 1)
               const uint64_t da = umma::desc_k_sw128(a + (b * UW + u) * A_BYTES);
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k)
-                umma::mma(tacc + u * MN, da + 2 * k, db + 2 * k, idesc, (kc + b != sg.k0 || k != 0) ? 1u : 0u);
+                umma::mma_e(tacc + u * MN, da + 2 * k, db + 2 * k, idesc, (kc + b != sg.k0 || k != 0) ? 1u : 0u);
             }
           }
-          umma::commit(&empty[s]);
+          umma::commit_e(&empty[s]);
         }
-        umma::commit(&tfull[acc]);
+        umma::commit_e(&tfull[acc]);
         ++it;
       }
     }
