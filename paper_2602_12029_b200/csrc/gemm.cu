@@ -583,6 +583,40 @@ __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
       : "memory");
 }
 
+// Warp-converged forms (the whole warp executes them with warp-uniform
+// operands, one elected lane issues; from an if (lane == 0) branch each TMA /
+// MMA became an R2UR.BROADCAST waterfall loop).
+__device__ __forceinline__ void mbar_expect_tx_e(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(
+          smem_addr(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair_e(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];\n}\n" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(smem_addr(bar) & 0xFEFFFFFFu), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_bf16_e(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma2_commit_both_e(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+          smem_addr(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                      const __grid_constant__ CUtensorMap tmap_bp, int M, int N, int K, Epi e, Sched sc) {
@@ -631,7 +665,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   pdl_trigger();
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
       pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
@@ -645,14 +679,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (piece >= 0) {
-            if (rank == 0) mbar_expect_tx(&full[stage], 2 * (A_BYTES + hp * BK * 2));
-            tma_load_2d_pair(&tmap_a, &full[stage], sA + stage * A_BYTES, kb * BK, row0);
-            tma_load_2d_pair(&tmap_bp, &full[stage], sB + stage * B_BYTES, kb * BK,
+            if (rank == 0) mbar_expect_tx_e(&full[stage], 2 * (A_BYTES + hp * BK * 2));
+            tma_load_2d_pair_e(&tmap_a, &full[stage], sA + stage * A_BYTES, kb * BK, row0);
+            tma_load_2d_pair_e(&tmap_bp, &full[stage], sB + stage * B_BYTES, kb * BK,
                              nb * BN + piece * 2 * hp + (int)rank * hp);
           } else {
-            if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
-            tma_load_2d_pair(&tmap_a, &full[stage], sA + stage * A_BYTES, kb * BK, row0);
-            tma_load_2d_pair(&tmap_b, &full[stage], sB + stage * B_BYTES, kb * BK, nb * BN + (int)rank * (BN / 2));
+            if (rank == 0) mbar_expect_tx_e(&full[stage], 2 * STAGE_BYTES);
+            tma_load_2d_pair_e(&tmap_a, &full[stage], sA + stage * A_BYTES, kb * BK, row0);
+            tma_load_2d_pair_e(&tmap_b, &full[stage], sB + stage * B_BYTES, kb * BK, nb * BN + (int)rank * (BN / 2));
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -660,7 +694,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {
       constexpr uint32_t idesc_full = idesc_bf16(BM2, BN);
       const uint32_t idesc_piece = idesc_bf16(BM2, BN / sc.S);
       int stage = 0;
@@ -681,11 +715,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const uint64_t db = smem_desc_sw128(sB + stage * B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma2_bf16(tacc, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
-          umma2_commit_both(&empty[stage]);
+            umma2_bf16_e(tacc, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          umma2_commit_both_e(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma2_commit_both(&tfull[acc]);
+        umma2_commit_both_e(&tfull[acc]);
       }
     }
     __syncwarp();
