@@ -1104,11 +1104,11 @@ __global__ void __launch_bounds__(HD) decode_attn_merge(const __grid_constant__ 
 // the legacy tensor pipe, not HBM. This variant runs both products on the
 // 5th-gen tensor cores with the same CTA = (session, kv head, split) work
 // split and the same (m, l, o) partial format, so the merge kernel is shared.
-//   warp 0     TMA producer: 4 pages per 64-key chunk, 6 stages; lane p
-//              loads page p (in parallel) as ONE 4-D box, the page's K and V
-//              for this (layer, head): [K|V][dims 0-63 | 64-127][16][64],
-//              8 KiB, 128B-swizzled, pages 8 KiB apart in the stage
-//   warp 1     MMA issuer + TMEM owner. Q and P live in TMEM (A operand
+//   warp 0     TMA producer (warp-converged, one elected lane issues): 4
+//              pages per 64-key chunk, 6 stages; each page as ONE 4-D box,
+//              its K and V for this (layer, head): [K|V][dims 0-63 |
+//              64-127][16][64], 8 KiB, 128B-swizzled, pages 8 KiB apart
+//   warp 1     MMA issuer (warp-converged) + TMEM owner. Q and P live in TMEM (A operand
 //              from tensor memory): S_u = Q K^T as two M128 N32 MMAs per
 //              16-dim K-step whose B rows are the SW128 atoms of the 4 pages
 //              at an 8 KiB stride (tokens 0-7 of pages 0-3, then tokens
@@ -1118,7 +1118,9 @@ __global__ void __launch_bounds__(HD) decode_attn_merge(const __grid_constant__ 
 //              tensor core runs one group's MMAs while the other group does
 //              its softmax; O is rescaled in TMEM only when a row max grows
 //              by > 2^8 (lazy, exact after the final 1/l). At the end group 0
-//              folds O_1 into O_0 and writes the split partial.
+//              folds O_1 into O_0 and writes the split partial; when the
+//              grid is one wave the split CTAs then merge their group
+//              themselves (fused_merge), otherwise decode_attn_merge runs.
 // Query rows = TMEM lanes (rows >= G are never read), so only the warps
 // whose lane quarter holds live rows take part in the softmax.
 // TMEM columns: S_0 [0,64) S_1 [64,128) O_0 [128,256) O_1 [256,384)
