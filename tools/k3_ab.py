@@ -1,7 +1,8 @@
-"""K3 A/B: the TMEM-P kernel (default) vs the shared-memory-P kernel
-(PSK_PREFILL_PSMEM=1), alternating child processes (the variant is read
-once per process), medians of per-child timings of the 4k causal attention
-(32 layers cycled, CUDA-graph replay).
+"""K3 A/B: variants of the prefill attention kernel given as
+name:KEY=VAL;KEY=VAL (env of the child; e.g. PSK_PREFILL_SPLIT=1, or
+PSK_LIB=<variant .so>), alternating child processes (variants are read once
+per process), min / median of per-child timings of the 4k causal attention
+(32 layers cycled, CUDA-graph replay, SM clock sampled while timing).
 
     python tools/k3_ab.py [reps] [T]
 """
