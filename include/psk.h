@@ -251,8 +251,10 @@ int psk_rope_append(const psk_decode_batch* b, const float* qkv, int32_t n_q_hea
  * its CTAs fit one wave, merges the splits itself (no second kernel).
  * q_rot bf16 [n_rows][nq][hd] -> out bf16 [n_rows][nq][hd]. workspace: fp32,
  * psk_decode_attn_workspace() bytes (for the same `splits`); its first
- * 32 KiB are merge counters that must be zero before the first call (e.g. a
- * zero-filled allocation); every call leaves them zero. */
+ * 32 KiB are merge counters (generation << 16 | arrivals per (session, KV
+ * head)) that must be zero before the first call (e.g. a zero-filled
+ * allocation); every call leaves the arrival counts zero (generations
+ * advance). */
 int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int32_t splits,
                               int64_t* bytes);
 /* How many kernels psk_decode_attn launches for this batch (1: the fan-out
@@ -262,6 +264,14 @@ int psk_decode_attn_kernels(const psk_decode_batch* b, int32_t n_q_heads, int32_
 int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_heads,
                     int32_t layer, psk_kv_layout kv, int32_t splits, void* workspace, void* out,
                     void* stream);
+/* Diagnostics (no reference counterpart): with PSK_TRACE_RING=1 in the
+ * environment every fan-out (tcgen05) launch stamps its CTAs' phases
+ * (%globaltimer ns: entry, barriers, first TMA, last TMA, partial written,
+ * group merged, exit) into the next slot of a 512-launch device ring of
+ * ctas_stride x 8 stamps; this copies up to n_u64 values of the ring to host
+ * (synchronizing the device; host may be NULL to query only) and reports
+ * the launches recorded so far. */
+int psk_decode_attn_trace_ring(uint64_t* host, int64_t n_u64, int32_t* launches, int32_t* ctas_stride);
 
 /* Greedy step end: tokens[r] = argmax(logits[r]) (first max, as tf.argMax /
  * torch.argmax), out_tokens[r*max_new + priv_len[r]] = it (if in range),

@@ -106,6 +106,7 @@ _SIGS: dict[str, list] = {
     "psk_decode_attn_workspace": [C.POINTER(DecodeBatchC), _I32, _I32, C.POINTER(_I64)],
     "psk_decode_attn_kernels": [C.POINTER(DecodeBatchC), _I32, _I32, _I32, C.POINTER(_I32)],
     "psk_decode_attn": [C.POINTER(DecodeBatchC), _P, _I32, _I32, KVLayout, _I32, _P, _P, _P],
+    "psk_decode_attn_trace_ring": [_P, _I64, C.POINTER(_I32), C.POINTER(_I32)],
     "psk_argmax_advance": [C.POINTER(DecodeBatchC), _P, _I32, _P, _I32, _P],
     "psk_argmax_rows": [_P, _I32, _I32, _P, _P],
     # prefill (K1-K3)
@@ -138,6 +139,8 @@ def load() -> C.CDLL:
                                    "(the CUDA extension is required; there is no CPU fallback)")
     lib = C.CDLL(str(path), mode=os.RTLD_LOCAL | os.RTLD_NOW)
     for name, args in _SIGS.items():
+        if "PSK_LIB" in os.environ and not hasattr(lib, name):
+            continue  # an older tuning variant (A/B builds) may lack newer entry points
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = _RESTYPE.get(name, C.c_int)

@@ -47,7 +47,7 @@ constexpr int NST = PSK_ATTN_NST;
 constexpr int TILE = PT * HD * 2;       // 4 KiB
 constexpr int STAGE = 2 * TILE;
 constexpr int GMAX = 64;
-constexpr int CNT_INTS = 8192;          // workspace head: fused-merge counters, {arrived, departed} per group
+constexpr int CNT_INTS = 8192;          // workspace head: fused-merge words (2 ints per group)
 constexpr int MAXR = 16;                // decode rows per session
 constexpr int OFF_Q = NST * STAGE;
 constexpr int OFF_BAR = OFF_Q + GMAX * 256;  // +16 KiB
@@ -70,12 +70,23 @@ struct Params {
   int* dir;  // stream-K mode (ns == 0): per group {first CTA, last CTA}, then the page total;
              // partial slot of (cta, group) = cta + group
   int sk_grid;  // stream-K: CTAs of the partial kernel
-  unsigned* cnt;  // fan-out kernel, fused merge: per group {arrived, departed}, zero between launches
+  unsigned* cnt;  // fan-out kernel, fused merge: per group generation << 16 | arrivals (+ a spare word)
   int fused;      // fan-out kernel: the split CTAs merge their group themselves (no merge kernel)
-  int early;      // fan-out kernel: stream shared pages before the PDL wait (PSK_ATTN_EARLY=1)
+  int early;      // fan-out kernel: stream shared pages before the PDL wait (default; PSK_ATTN_LATE=1: off)
   int stream_only;  // fan-out kernel, measurement only (PSK_ATTN_STREAM_ONLY=1): pages streamed and
                     // released without MMA / softmax (the TMA stream's own ceiling; output garbage)
+  unsigned long long* ring;  // fan-out kernel, diagnostics (PSK_TRACE_RING=1): this launch's slot of
+                             // per-CTA %globaltimer stamps, 8 per CTA (nullptr: off)
 };
+
+// Launch-ring stamp (thread 0 of the CTA = the producer warp's lane 0)
+__device__ __forceinline__ void ring_stamp(const Params& p, int k) {
+  if (p.ring != nullptr && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    p.ring[(size_t)blockIdx.x * 8 + k] = v;
+  }
+}
 
 // SW128 address of (token row, 16-byte chunk c16 in 0..15) in a K/V tile made
 // of two [16 x 128 B] TMA boxes (dims 0-63, 64-127).
@@ -1046,8 +1057,10 @@ __global__ void __launch_bounds__(HD) decode_attn_merge(const __grid_constant__ 
   // the row tables are static within a step: read them before the wait
   const int g = p.b.row_in_sess[r] * p.grp + qh % p.grp;
   const int grp_id = p.b.row_sess[r] * nkv + h;
+  // let the next kernel (the o-proj GEMV streaming its weights) be scheduled
+  // now: its own griddepcontrol.wait still waits for this grid to complete
+  asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");  // the o-proj GEMV may start streaming weights
   // partial slots of this (session, KV head): splits mode ns consecutive
   // slots; stream-K mode slots cta + group for the CTAs in dir[group]
   int64_t first;
@@ -1148,29 +1161,16 @@ constexpr int THREADS = 320;
 constexpr uint32_t T_S = 0, T_O = 128, T_Q = 384, T_P = 448;
 constexpr float RESCALE_LOG2 = 8.f;
 
-// Fused merge of the fan-out kernel: the ns split CTAs of a (session, KV
-// head) group are co-resident (grid <= SMs, 1 CTA per SM), so after
-// publishing its partial each CTA waits for the group's other splits and
-// merges a 1/ns slice of the group's (query row, 4 dims) outputs by
-// log-sum-exp, instead of a second kernel that waits for the whole grid.
-// The last CTA to leave zeroes the group's counters for the next launch.
-__device__ __forceinline__ void fused_merge(const Params& p, int grp_id, int j, int h, int G, const int* s_rows) {
-  unsigned* cnt = p.cnt + 2 * grp_id;
-  const unsigned ns = (unsigned)p.ns;
-  __syncthreads();  // this CTA's partial is written
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(cnt, 1u);
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-    } while (v < ns);
-    __threadfence();
-  }
-  __syncthreads();
+// Slice j of a (session, KV head) group's split merge: the group's (query
+// row, 4 dims) outputs [j T / ns, (j + 1) T / ns), each folded over the ns
+// split partials by log-sum-exp. (Measured and kept over K lanes per output
+// with all partials' loads in flight + shuffle combine: no faster at 32k x 16
+// modules, slower at 8 sessions x 4k; tools/k6_ab.py.)
+template <int NT>
+__device__ __forceinline__ void merge_slice(const Params& p, int grp_id, int j, int h, int G, const int* rows) {
   const int T = G * (HD / 4);
   const int t0 = (int)((int64_t)j * T / p.ns), t1 = (int)((int64_t)(j + 1) * T / p.ns);
-  for (int t = t0 + (int)threadIdx.x; t < t1; t += THREADS) {
+  for (int t = t0 + (int)threadIdx.x; t < t1; t += NT) {
     const int g = t >> 5, d4 = (t & 31) * 4;
     const int64_t base = (int64_t)grp_id * p.ns * GMAX + g;
     float M = -INFINITY;
@@ -1193,15 +1193,46 @@ __device__ __forceinline__ void fused_merge(const Params& p, int grp_id, int j, 
     const float inv = L > 0.f ? 1.f / L : 0.f;
     const int qh = h * p.grp + g % p.grp;
     __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(
-        p.out + ((int64_t)s_rows[g / p.grp] * p.nq + qh) * HD + d4);
+        p.out + ((int64_t)rows[g / p.grp] * p.nq + qh) * HD + d4);
     dst[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
     dst[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
   }
-  __syncthreads();
-  if (threadIdx.x == 0 && atomicAdd(cnt + 1, 1u) == ns - 1) {  // every split has left the wait
-    cnt[0] = 0;
-    cnt[1] = 0;
+}
+
+// Fused merge of the fan-out kernel: the ns split CTAs of a (session, KV
+// head) group are co-resident (grid <= SMs, 1 CTA per SM), so after
+// publishing its partial each CTA waits for the group's other splits and
+// merges a 1/ns slice of the group's (query row, 4 dims) outputs by
+// log-sum-exp, instead of a second kernel that waits for the whole grid.
+// One word per group: generation << 16 | arrivals. The last arrival adds
+// (1 << 16) - ns (next generation, arrivals back to 0); the others wait for
+// the generation to move past the one their arrival saw. A CTA releases its
+// dependents (PDL) only after its arrival, so a back-to-back launch of this
+// kernel never reaches the word before every arrival of this launch (and its
+// generation step) is in: the words need no reset pass and no departure count.
+__device__ __forceinline__ void fused_merge(const Params& p, int grp_id, int j, int h, int G, const int* s_rows) {
+  unsigned* cnt = p.cnt + 2 * grp_id;
+  const unsigned ns = (unsigned)p.ns;
+  __syncthreads();  // this CTA's partial is written
+  __shared__ unsigned s_target;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned old = atomicAdd(cnt, 1u);
+    if ((old & 0xffffu) == ns - 1) atomicAdd(cnt, 0x10000u - ns);
+    s_target = ((old >> 16) + 1u) & 0xffffu;
   }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (threadIdx.x == 0) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+    } while ((short)((v >> 16) - s_target) < 0);
+    __threadfence();
+  }
+  ring_stamp(p, 5);
+  __syncthreads();
+  merge_slice<THREADS>(p, grp_id, j, h, G, s_rows);
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -1232,6 +1263,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int act = (G + 15) / 16;  // softmax warps with live rows, per group
 
   trace_stamp(0);
+  ring_stamp(p, 0);
   if (threadIdx.x < nr) {
     const int r = p.b.sess_rows[(int64_t)sess * p.b.max_rows_per_sess + threadIdx.x];
     s_rows[threadIdx.x] = r;
@@ -1267,6 +1299,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 1) umma::tmem_alloc(&s_tmem, 512);
   __syncthreads();
   trace_stamp(1);
+  ring_stamp(p, 1);
   const int total = s_total;
   const int k0 = (int)((int64_t)j_split * total / p.ns);
   const int k1 = (int)((int64_t)(j_split + 1) * total / p.ns);
@@ -1348,8 +1381,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int row_k = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv + h) * PT);
         tma::load_4d_e(&kvmap, &full[st], smem + st * STG + pp * PGB, 0, row_k, 0, 0);  // K and V, 8 KiB
       }
+      if (c == 0) ring_stamp(p, 2);
     }
     trace_stamp(3);
+    ring_stamp(p, 3);
   } else if (warp == 1) {
     constexpr uint32_t ID_S = umma::idesc_bf16(128, KC / 2, false), ID_PV = umma::idesc_bf16(128, HD, true);
     auto issue_s = [&](int c) {
@@ -1611,15 +1646,19 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   }
-  asm volatile("griddepcontrol.launch_dependents;");
+  // (with the in-kernel merge the CTA releases its dependents in fused_merge,
+  // once its group's counters are re-armed)
+  if (!p.fused) asm volatile("griddepcontrol.launch_dependents;");
   umma::fence_before();
   __syncthreads();
   trace_stamp(4);
+  ring_stamp(p, 4);
   if (warp == 1) {
     umma::fence_after();
     umma::tmem_dealloc(tmem, 512);
   }
   if (p.fused) fused_merge(p, sess * nkv + h, j_split, h, G, s_rows);
+  ring_stamp(p, 6);
 }
 
 }  // namespace tcv
@@ -1709,6 +1748,33 @@ extern "C" {
 
 static int sm_count() { return psk::sm_budget(); }
 
+// Launch ring (diagnostics, PSK_TRACE_RING=1): each fan-out launch (captured
+// launches included: the slot is fixed at launch / capture time) stamps its
+// CTAs' phases into the next of RING_SLOTS slots of RING_CTAS x 8 stamps.
+static constexpr int RING_SLOTS = 512, RING_CTAS = 256;
+static unsigned long long* g_ring = nullptr;
+static int g_ring_n = 0;
+static unsigned long long* ring_slot(int ctas) {
+  static const bool on = getenv("PSK_TRACE_RING") != nullptr;
+  if (!on || ctas > RING_CTAS) return nullptr;
+  if (!g_ring) {
+    if (cudaMalloc(&g_ring, sizeof(unsigned long long) * RING_SLOTS * RING_CTAS * 8) != cudaSuccess) return nullptr;
+    cudaMemset(g_ring, 0, sizeof(unsigned long long) * RING_SLOTS * RING_CTAS * 8);
+  }
+  return g_ring + (size_t)(g_ring_n++ % RING_SLOTS) * RING_CTAS * 8;
+}
+
+int psk_decode_attn_trace_ring(uint64_t* host, int64_t n_u64, int32_t* launches, int32_t* ctas_stride) {
+  PSK_CHECK_ARG(launches && ctas_stride, "psk_decode_attn_trace_ring: bad args");
+  *launches = g_ring_n;
+  *ctas_stride = RING_CTAS;
+  if (!g_ring || !host) return PSK_OK;
+  const int64_t cap = (int64_t)RING_SLOTS * RING_CTAS * 8;
+  PSK_CUDA_TRY(cudaDeviceSynchronize());
+  PSK_CUDA_TRY(cudaMemcpy(host, g_ring, sizeof(uint64_t) * (n_u64 < cap ? n_u64 : cap), cudaMemcpyDeviceToHost));
+  return PSK_OK;
+}
+
 // Partial slots the workspace holds: enough for the caller's fixed splits,
 // the stream-K schedule (grid + groups) and the all-heads kernel (one
 // wave of (session, split) CTAs: groups x sms / n_sess).
@@ -1730,8 +1796,9 @@ int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int
                               int64_t* bytes) {
   PSK_CHECK_ARG(b && bytes && splits >= 0, "psk_decode_attn_workspace: bad args");
   const int64_t groups = (int64_t)b->n_sess * n_kv_heads;
-  // fan-out merge counters at a fixed offset (zero before the first launch,
-  // left zero by every launch, so one workspace serves any batch shape) |
+  // fan-out merge counters at a fixed offset (zero before the first launch;
+  // every launch leaves the arrival counts zero, so one workspace serves any
+  // batch shape) |
   // partials | CTA directory (+ page total)
   *bytes = CNT_INTS * 4 + ws_slots(b, n_kv_heads, splits) * GMAX * (HD + 2) * 4 + groups * 2 * 4 + 16;
   return PSK_OK;
@@ -1832,10 +1899,18 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   // fan-out kernel: merge inside the partial kernel when every CTA is
   // co-resident (one CTA per SM); PSK_ATTN_MERGE_KERNEL=1 keeps the kernel
   p.fused = use_tc && fanout_fused(b, n_q_heads, kv.n_kv_heads, splits);
-  static const bool early = getenv("PSK_ATTN_EARLY") != nullptr;
-  p.early = early;
+
+  // The fan-out kernel streams the shared prompt pages before its PDL wait:
+  // no kernel of a decode step writes them, and the step's first kernel
+  // (embed_rows) waits for all earlier work (prefill, handoff copies) before
+  // it lets its dependents launch, so they are complete whenever this kernel
+  // runs. 32k x 16 modules 32.9 -> 32.4 us, 8 x 4k x 16 35.3 -> 35.0 us
+  // (same box, tools/k6_ab.py). PSK_ATTN_LATE=1 waits first.
+  static const bool late = getenv("PSK_ATTN_LATE") != nullptr;
+  p.early = !late;
   static const bool stream_only = getenv("PSK_ATTN_STREAM_ONLY") != nullptr;
   p.stream_only = stream_only;
+  p.ring = use_tc ? ring_slot((int)items) : nullptr;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
   cudaStream_t s = psk::as_stream(stream);
   static bool init = false;

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0, dirty_ws=False, ramp=False, reps=1,
-          ws=None):
+          ws=None, b2b=False):
     from paper_2602_12029_b200 import _lib
     from paper_2602_12029_b200.model import (DecodeBatch, DecodeRow, KVCache, LlamaConfig,
                                              SessionSpec)
@@ -55,8 +55,9 @@ def _case(nq, nkv, sess_lens, rows_per_sess, priv_lens, splits, seed=0, dirty_ws
         ws = torch.zeros(wsb.value // 4 + 1, dtype=torch.float32, device="cuda")
     if dirty_ws:  # stale partials / directory from earlier launches must not leak in
         ws[8192:].uniform_(-50.0, 50.0)  # the leading 32 KiB of merge counters stay zero (API contract)
-    for _ in range(reps):  # repeated launches reuse the workspace (fused-merge counters reset)
-        out.fill_(float("nan"))
+    for i in range(reps):  # repeated launches reuse the workspace (fused-merge counters reset)
+        if not b2b or i == 0:  # b2b: launches back to back (PDL-chained, no other kernel between)
+            out.fill_(float("nan"))
         _lib.check(lib.psk_decode_attn(b.c_ref(), q.data_ptr(), nq, layer, kv.layout(), splits,
                                        ws.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
@@ -98,11 +99,25 @@ def test_fanout_fused_merge_reuse():
     """The fan-out kernel's in-kernel merge (one wave of split CTAs): three
     launches on one workspace, then other split counts / groups on the same
     workspace with stale partials; the group counters must come back to zero
-    after every launch."""
+    after every launch (arrival counts; the generations advance)."""
     ws = _case(32, 8, [2000], [16], [i * 3 for i in range(16)], 18, seed=5, reps=3)
     ws = _case(32, 8, [900], [16], [i for i in range(16)], 7, seed=6, reps=2, ws=ws, dirty_ws=True)
     ws = _case(32, 8, [300, 77], [16, 9], [i % 20 for i in range(25)], 9, seed=7, reps=2, ws=ws)
-    assert ws[:8192].abs().sum().item() == 0.0
+    cnt = ws[:8192].view(torch.int32)
+    assert (cnt[0::2] & 0xFFFF).sum().item() == 0  # arrivals back to zero
+    assert (cnt[0::2] >> 16).sum().item() > 0      # the groups' generations advanced
+
+
+@pytest.mark.parametrize("lens,splits", [([300], 18), ([40, 70], 9), ([4095], 18)])
+def test_fanout_back_to_back(lens, splits):
+    """Hundreds of fan-out launches back to back (each PDL-released by the
+    previous one, which frees its CTAs' SMs while the rest of its grid is still
+    merging): short splits reach the group counters early; they must find them
+    re-armed (no lost arrival = no hang, no early pass = exact results)."""
+    ws = _case(32, 8, lens, [16] * len(lens), [i * 5 % 37 for i in range(16 * len(lens))], splits, seed=21,
+               reps=400, b2b=True)
+    cnt = ws[:8192].view(torch.int32)
+    assert (cnt[0::2] & 0xFFFF).sum().item() == 0
 
 
 def test_fanout_two_sessions_tcgen05():

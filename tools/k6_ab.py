@@ -1,9 +1,11 @@
 """K6 A/B at the fan-out shapes: the config-4 shape (32k shared tokens x 16
-modules) and smaller fan-outs, in-kernel merge vs the merge kernel
-(PSK_ATTN_MERGE_KERNEL=1) vs shared pages streamed before the PDL wait
-(PSK_ATTN_EARLY=1); env read once per process: one child per mode.
+modules) and smaller fan-outs: the default (in-kernel merge, shared pages
+streamed before the PDL wait) vs the PDL wait first (PSK_ATTN_LATE=1) vs the
+merge kernel (PSK_ATTN_MERGE_KERNEL=1) vs the TMA stream alone, and against
+another build of the library (PSK_LIB); env read once per process: one child
+per mode.
 
-    python tools/k6_ab.py
+    python tools/k6_ab.py [mode,mode,...]
 """
 import json
 import os
@@ -26,8 +28,13 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
                           "us": r["us_per_launch"], "gbs": r["achieved"], "frac": r["frac"]}), flush=True)
     sys.exit(0)
 
-MODES = (("fused", {}), ("early", {"PSK_ATTN_EARLY": "1"}), ("merge-kernel", {"PSK_ATTN_MERGE_KERNEL": "1"}),
-         ("stream-only", {"PSK_ATTN_STREAM_ONLY": "1"}))  # the last: TMA stream alone, no MMA / softmax
+MODES = (("fused", {}),  # default: in-kernel merge, shared pages streamed before the PDL wait
+         ("late", {"PSK_ATTN_LATE": "1"}),  # PDL wait before the first page
+         ("merge-kernel", {"PSK_ATTN_MERGE_KERNEL": "1"}),
+         ("stream-only", {"PSK_ATTN_STREAM_ONLY": "1"}),  # TMA stream alone, no MMA / softmax
+         # A/B against another build of the library (variants/, tools/README.md)
+         ("head", {"PSK_LIB": str(ROOT / "variants" / "libpsk_head.so")}),
+         ("head-early", {"PSK_LIB": str(ROOT / "variants" / "libpsk_head.so"), "PSK_ATTN_EARLY": "1"}))
 if len(sys.argv) > 1 and sys.argv[1] != "child":
     MODES = tuple(m for m in MODES if m[0] in sys.argv[1].split(","))
 for mode, env in MODES:
