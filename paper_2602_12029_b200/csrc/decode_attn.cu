@@ -79,6 +79,34 @@ struct Params {
                              // per-CTA %globaltimer stamps, 8 per CTA (nullptr: off)
 };
 
+// In-kernel split merge barrier (the split CTAs of a group are co-resident:
+// grid <= SMs, 1 CTA per SM). One word per group: generation << 16 |
+// arrivals. The last arrival adds (1 << 16) - ns (next generation, arrivals
+// back to 0); the others wait for the generation to move past the one their
+// arrival saw. A CTA releases its PDL dependents only after its arrival, so a
+// back-to-back launch of the kernel never reaches the word before every
+// arrival of this launch (and its generation step) is in: no reset pass and
+// no departure count. Call with the CTA's partial written (all threads).
+__device__ __forceinline__ void split_barrier(unsigned* word, unsigned ns) {
+  __shared__ unsigned s_target;
+  __syncthreads();  // this CTA's partial is written
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned old = atomicAdd(word, 1u);
+    if ((old & 0xffffu) == ns - 1) atomicAdd(word, 0x10000u - ns);
+    s_target = ((old >> 16) + 1u) & 0xffffu;
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (threadIdx.x == 0) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(word) : "memory");
+    } while ((short)((v >> 16) - s_target) < 0);
+    __threadfence();
+  }
+}
+
 // Launch-ring stamp (thread 0 of the CTA = the producer warp's lane 0)
 __device__ __forceinline__ void ring_stamp(const Params& p, int k) {
   if (p.ring != nullptr && threadIdx.x == 0) {
@@ -1039,8 +1067,43 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
   trace_stamp(3);
-  asm volatile("griddepcontrol.launch_dependents;");
+  if (!p.fused) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    return;
+  }
+  // In-kernel merge (the session's splits are co-resident): wait for them,
+  // then fold slice j_split of the session's (head, row, 4 dims) outputs.
+  split_barrier(p.cnt + 2 * sess * nkv, (unsigned)p.ns);
+  __syncthreads();
   trace_stamp(4);
+  const int GT = G * (HD / 4), T = nkv * GT;
+  const int t0 = (int)((int64_t)j_split * T / p.ns), t1 = (int)((int64_t)(j_split + 1) * T / p.ns);
+  for (int t = t0 + (int)threadIdx.x; t < t1; t += THREADS) {
+    const int h = t / GT, rem = t - h * GT;
+    const int g = rem >> 5, d4 = (rem & 31) * 4;
+    const int64_t base = (int64_t)(sess * nkv + h) * p.ns * GMAX + g;
+    float M = -INFINITY;
+    for (int s = 0; s < p.ns; ++s) M = fmaxf(M, __ldcg(p.pm + base + (int64_t)s * GMAX));
+    const float Mr = M == -INFINITY ? 0.f : M;
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int s = 0; s < p.ns; ++s) {
+      const int64_t sl = base + (int64_t)s * GMAX;
+      const float f = exp2f(__ldcg(p.pm + sl) - Mr);
+      const float4 o = __ldcg(reinterpret_cast<const float4*>(p.po + sl * HD + d4));
+      L += f * __ldcg(p.pl + sl);
+      acc.x += f * o.x;
+      acc.y += f * o.y;
+      acc.z += f * o.z;
+      acc.w += f * o.w;
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(
+        p.out + ((int64_t)s_rows[g / p.grp] * p.nq + h * p.grp + g % p.grp) * HD + d4);
+    dst[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+    dst[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+  }
 }
 
 }  // namespace hk
@@ -1199,37 +1262,12 @@ __device__ __forceinline__ void merge_slice(const Params& p, int grp_id, int j, 
   }
 }
 
-// Fused merge of the fan-out kernel: the ns split CTAs of a (session, KV
-// head) group are co-resident (grid <= SMs, 1 CTA per SM), so after
-// publishing its partial each CTA waits for the group's other splits and
-// merges a 1/ns slice of the group's (query row, 4 dims) outputs by
-// log-sum-exp, instead of a second kernel that waits for the whole grid.
-// One word per group: generation << 16 | arrivals. The last arrival adds
-// (1 << 16) - ns (next generation, arrivals back to 0); the others wait for
-// the generation to move past the one their arrival saw. A CTA releases its
-// dependents (PDL) only after its arrival, so a back-to-back launch of this
-// kernel never reaches the word before every arrival of this launch (and its
-// generation step) is in: the words need no reset pass and no departure count.
+// Fused merge of the fan-out kernel: after publishing its partial each
+// split CTA waits for the group's other splits (split_barrier) and merges a
+// 1/ns slice of the group's (query row, 4 dims) outputs by log-sum-exp,
+// instead of a second kernel that waits for the whole grid.
 __device__ __forceinline__ void fused_merge(const Params& p, int grp_id, int j, int h, int G, const int* s_rows) {
-  unsigned* cnt = p.cnt + 2 * grp_id;
-  const unsigned ns = (unsigned)p.ns;
-  __syncthreads();  // this CTA's partial is written
-  __shared__ unsigned s_target;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned old = atomicAdd(cnt, 1u);
-    if ((old & 0xffffu) == ns - 1) atomicAdd(cnt, 0x10000u - ns);
-    s_target = ((old >> 16) + 1u) & 0xffffu;
-  }
-  __syncthreads();
-  asm volatile("griddepcontrol.launch_dependents;");
-  if (threadIdx.x == 0) {
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-    } while ((short)((v >> 16) - s_target) < 0);
-    __threadfence();
-  }
+  split_barrier(p.cnt + 2 * grp_id, (unsigned)p.ns);
   ring_stamp(p, 5);
   __syncthreads();
   merge_slice<THREADS>(p, grp_id, j, h, G, s_rows);
@@ -1804,6 +1842,41 @@ int psk_decode_attn_workspace(const psk_decode_batch* b, int32_t n_kv_heads, int
   return PSK_OK;
 }
 
+// The all-heads kernel's plan: whether it runs (<= 16 query rows per KV head
+// everywhere and at least one (session, head) group per SM), its splits per
+// session (one wave of (session, split) CTAs) and whether those CTAs merge
+// their session themselves (the wave fits the device: all co-resident).
+// Measured at 4k shared tokens x 4 modules (tools/hsplit_ab.py): 32 sessions
+// 4 splits 114.5 us vs 5 / 6 / 7 / 8 / 9 splits 142.8 / 124.8 / 118.3 /
+// 117.1 / 122.6 us (more than one wave, or more, shorter CTAs that lose to
+// their per-CTA prologue); 64 sessions 2 splits 216.9 us, 4 splits 213.1.
+// With fewer groups the per-head kernel's finer splits win (8 sessions:
+// 42.7 vs 45.8 us; 32 sessions: 152 vs 144 us; 1 session: 12.4 vs 21 us at
+// 4k). PSK_ATTN_HSPLIT=n overrides the splits (bounded by the workspace's 8
+// waves); PSK_ATTN_MERGE_KERNEL=1 keeps the merge kernel.
+static bool heads_plan(const psk_decode_batch* b, int32_t n_q_heads, int32_t n_kv_heads, int32_t splits,
+                       int* hsplit, bool* fused) {
+  static const bool force_hmma = getenv("PSK_ATTN_HMMA") != nullptr;
+  static const bool no_heads = getenv("PSK_ATTN_PER_HEAD") != nullptr;
+  static const bool merge_kernel = getenv("PSK_ATTN_MERGE_KERNEL") != nullptr;
+  static const int force = getenv("PSK_ATTN_HSPLIT") ? atoi(getenv("PSK_ATTN_HSPLIT")) : 0;
+  const int grp = n_q_heads / n_kv_heads;
+  const int sms = sm_count();
+  const bool use_tc = grp * b->max_rows_per_sess > 32 && !force_hmma;
+  if (use_tc || no_heads || splits <= 0 || grp * b->max_rows_per_sess > 16 || n_kv_heads > hk::MAXKV ||
+      (int64_t)b->n_sess * n_kv_heads < sms)
+    return false;
+  const int64_t max_pages = (int64_t)b->max_sess_pages + (int64_t)b->max_rows_per_sess * b->max_row_pages;
+  const int64_t hmax = max_pages / 4 > 1 ? max_pages / 4 : 1;
+  int h = sms / b->n_sess > 1 ? sms / b->n_sess : 1;
+  if (h > hmax) h = (int)hmax;
+  if (force > 0 && force <= hmax && b->n_sess * force <= 8 * (int64_t)sms) h = force;
+  *hsplit = h;
+  *fused = !merge_kernel && (int64_t)b->n_sess * h <= psk::device_sms() &&
+           2 * (int64_t)b->n_sess * n_kv_heads <= CNT_INTS;
+  return true;
+}
+
 // Whether the fan-out (tcgen05) kernel runs and merges its splits itself:
 // > 32 query rows per KV head, its (session, head, split) CTAs fit one wave
 // (1 CTA per SM, all co-resident for the in-kernel merge).
@@ -1821,7 +1894,10 @@ int psk_decode_attn_kernels(const psk_decode_batch* b, int32_t n_q_heads, int32_
                             int32_t* n_kernels) {
   PSK_CHECK_ARG(b && n_kernels && n_kv_heads > 0 && n_q_heads % n_kv_heads == 0 && splits >= 0,
                 "psk_decode_attn_kernels: bad args");
-  *n_kernels = b->n_rows == 0 ? 0 : (fanout_fused(b, n_q_heads, n_kv_heads, splits) ? 1 : 2);
+  int hsplit = 1;
+  bool hfused = false;
+  const bool heads = heads_plan(b, n_q_heads, n_kv_heads, splits, &hsplit, &hfused);
+  *n_kernels = b->n_rows == 0 ? 0 : ((heads ? hfused : fanout_fused(b, n_q_heads, n_kv_heads, splits)) ? 1 : 2);
   return PSK_OK;
 }
 
@@ -1843,13 +1919,9 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   const int sms = sm_count();
   const int64_t groups = (int64_t)b->n_sess * kv.n_kv_heads;
   const int64_t slots = ws_slots(b, kv.n_kv_heads, splits);
-  // <= 16 query rows per KV head everywhere and at least one (session, head)
-  // group per SM: the all-heads kernel (CTA = (session, split), 64 KiB page
-  // boxes, no fold). With fewer groups the per-head kernel's finer splits win
-  // (8 sessions: 42.7 vs 45.8 us; 32 sessions: 152 vs 144 us; 1 session:
-  // 12.4 vs 21 us at 4k).
-  const bool use_heads = !use_tc && !no_heads && splits > 0 && grp * b->max_rows_per_sess <= 16 &&
-                         kv.n_kv_heads <= hk::MAXKV && (int64_t)b->n_sess * kv.n_kv_heads >= sm_count();
+  int hsplit = 1;
+  bool hfused = false;
+  const bool use_heads = heads_plan(b, n_q_heads, kv.n_kv_heads, splits, &hsplit, &hfused);
   // stream-K mode (splits == 0) for the mma.sync path when the session
   // tables and one run's page list fit in shared memory; otherwise (and for
   // the tcgen05 path) fixed splits that fit the same workspace
@@ -1859,21 +1931,6 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
     const int64_t run_bound = (groups * per_group + sms - 1) / sms + 1;
     stream_k = !use_tc && b->n_sess <= sk::MAXS && run_bound <= sk::MAXP;
     if (!stream_k) splits = (int)(sms / groups) > 1 ? (int)(sms / groups) : 1;  // one wave, fits the slots
-  }
-  int hsplit = 1;
-  if (use_heads) {
-    const int64_t max_pages = (int64_t)b->max_sess_pages + (int64_t)b->max_rows_per_sess * b->max_row_pages;
-    // splits per session: one wave of (session, split) CTAs. Measured at 4k
-    // shared tokens x 4 modules (tools/hsplit_ab.py): 32 sessions 4 splits
-    // 114.5 us vs 5 / 6 / 7 / 8 / 9 splits 142.8 / 124.8 / 118.3 / 117.1 /
-    // 122.6 us (more, shorter CTAs lose to their per-CTA prologue and odd
-    // splits to DRAM locality); 64 sessions 2 splits 216.9 us, 4 splits 213.1.
-    // PSK_ATTN_HSPLIT=n overrides (bounded by the workspace's 8 waves).
-    static const int force = getenv("PSK_ATTN_HSPLIT") ? atoi(getenv("PSK_ATTN_HSPLIT")) : 0;
-    const int64_t hmax = max_pages / 4 > 1 ? max_pages / 4 : 1;
-    hsplit = sms / b->n_sess > 1 ? sms / b->n_sess : 1;
-    if (hsplit > hmax) hsplit = (int)hmax;
-    if (force > 0 && force <= hmax && b->n_sess * force <= 8 * (int64_t)sms) hsplit = force;
   }
   CUtensorMap map;
   const int rc = psk::kv_tensor_map(kv, &map, use_heads ? psk::KV_PAGE4D_ALL : psk::KV_PAGE4D);
@@ -1898,7 +1955,7 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
   p.sk_grid = sms;
   // fan-out kernel: merge inside the partial kernel when every CTA is
   // co-resident (one CTA per SM); PSK_ATTN_MERGE_KERNEL=1 keeps the kernel
-  p.fused = use_tc && fanout_fused(b, n_q_heads, kv.n_kv_heads, splits);
+  p.fused = use_tc ? fanout_fused(b, n_q_heads, kv.n_kv_heads, splits) : (use_heads && hfused);
 
   // The fan-out kernel streams the shared prompt pages before its PDL wait:
   // no kernel of a decode step writes them, and the step's first kernel

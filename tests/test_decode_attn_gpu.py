@@ -120,6 +120,16 @@ def test_fanout_back_to_back(lens, splits):
     assert (cnt[0::2] & 0xFFFF).sum().item() == 0
 
 
+@pytest.mark.parametrize("lens", [[300] * 20, [37 * i % 900 + 1 for i in range(24)]])
+def test_all_heads_back_to_back(lens):
+    """The all-heads kernel's in-kernel session merge under hundreds of
+    PDL-chained back-to-back launches (see test_fanout_back_to_back)."""
+    n = len(lens)
+    ws = _case(32, 8, lens, [4] * n, [(3 * i) % 40 for i in range(4 * n)], 1, seed=23, reps=300, b2b=True)
+    cnt = ws[:8192].view(torch.int32)
+    assert (cnt[0::2] & 0xFFFF).sum().item() == 0
+
+
 def test_fanout_two_sessions_tcgen05():
     _case(32, 8, [700, 129], [6, 16], [i % 40 for i in range(22)], 9, seed=11)
 
