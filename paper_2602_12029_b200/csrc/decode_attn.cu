@@ -889,6 +889,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     return p.b.row_pages[(int64_t)s_rows[i] * p.b.max_row_pages + (k - s_pstart[i])];
   };
   for (int j = threadIdx.x; j < np && j < MAXP_SMEM; j += THREADS) s_page[j] = page_of(k0 + j);
+  // The producer streams the first two ring stages of shared prompt pages
+  // before the PDL wait (no kernel of a decode step writes them; see
+  // psk_decode_attn); stage 2 holds Q until the stream starts.
+  int pre = 0;
+  if (p.early && threadIdx.x == MAXKV * 32) {
+    for (; pre < NST - 1 && pre < np && k0 + pre < s_ps; ++pre) {
+      const int page = page_of(k0 + pre);
+      const int row0 = (int)((((int64_t)page * p.kv.n_layers + p.layer) * 2 * nkv) * PT);
+      tma::mbar_expect_tx(&full[pre], STG);
+      tma::load_4d(&kvmap, &full[pre], smem + pre * STAGE_MAX, 0, row0, 0, 0);
+    }
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // q / the appended K,V come from rope_append
   // Q of every head: rows g of head h at [h][16][256 B] (swizzled)
   {
@@ -930,7 +942,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == MAXKV) {
     // ---------------- TMA producer: one box per page, all heads ----------------
     if (lane == 0) {
-      for (int j = 0; j < np; ++j) {
+      for (int j = pre; j < np; ++j) {
         const int st = j % NST;
         tma::mbar_wait(&empty[st], ((j / NST) & 1) ^ 1);
         const int page = j < MAXP_SMEM ? s_page[j] : page_of(k0 + j);
