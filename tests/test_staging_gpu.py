@@ -117,7 +117,9 @@ def test_agent_server_copy_handoff_with_staging(capacity):
     srv = AgentServer(cfg, models, ServingMode.PREFILLSHARE, rows_per_module=4, pool_pages_per_worker=512,
                       max_context=2048, max_output=128, modules=mods, base=base, handoff="copy",
                       decode_capacity_blocks=capacity)
-    recs = srv.run(sessions, time_scale=0.3, record_trace=True)
+    # the small budget needs contexts resident together: arrivals compressed
+    # harder there (how many overlap otherwise depends on the decode speed)
+    recs = srv.run(sessions, time_scale=0.3 if capacity > 130 else 0.05, record_trace=True)
     assert len(recs) == n_req and all(r.done_us is not None and not r.failed for r in recs)
     check_trace(srv.trace, sessions, n_req, len(models))
     rep = build_report(srv, recs, {"capacity": capacity})
