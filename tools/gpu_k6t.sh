@@ -1,4 +1,4 @@
 #!/bin/bash
-for i in 1 2 3; do timeout 600 python -m pytest tests/test_staging_gpu.py -x -q 2>&1 | tail -1; done
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1
-echo "gpu tests rc=$?"; tail -3 gpurun_out/gpu_tests.log
+PSK_ATTN_HK_INTERLEAVE=1 timeout 600 python -m pytest tests/test_decode_attn_gpu.py -x -q -k "all_heads" 2>&1 | tail -1
+export K6_SHAPES="4095:4:32:256,4095:4:32:1,4095:4:64:100"
+timeout 900 python tools/k6_ab.py fused,interleave 2>&1
