@@ -249,6 +249,12 @@ int psk_rope_append(const psk_decode_batch* b, const float* qkv, int32_t n_q_hea
  * workspace for > 32 query rows per KV head or > 64 sessions.
  * Above 32 query rows per KV head (fan-out) the tcgen05 kernel runs and, when
  * its CTAs fit one wave, merges the splits itself (no second kernel).
+ * Launched with programmatic dependent launch: it may read the sessions'
+ * shared prefix pages before waiting on the previous kernel of the stream
+ * (only q and the private pages come from it), so those pages must be
+ * complete when that kernel releases its dependents -- as in a decode step,
+ * whose first kernel (psk_embed_rows) waits for all earlier work first.
+ * PSK_ATTN_LATE=1 makes every read wait.
  * q_rot bf16 [n_rows][nq][hd] -> out bf16 [n_rows][nq][hd]. workspace: fp32,
  * psk_decode_attn_workspace() bytes (for the same `splits`); its first
  * 32 KiB are merge counters (generation << 16 | arrivals per (session, KV
