@@ -820,7 +820,6 @@ namespace hk {
 
 constexpr int NST = 3;
 constexpr int MAXKV = 8;                       // consumer warps = KV heads
-constexpr int MAXP = 2048;
 __host__ __device__ constexpr int stage_bytes(int nkv) { return 2 * nkv * TILE; }  // K|V x heads x 4 KiB
 constexpr int STAGE_MAX = stage_bytes(MAXKV);   // 64 KiB
 constexpr int OFF_Q = 2 * STAGE_MAX;            // Q is staged in ring stage 2 before the stream starts
