@@ -1,4 +1,6 @@
 #!/bin/bash
-PSK_ATTN_HK_INTERLEAVE=1 timeout 600 python -m pytest tests/test_decode_attn_gpu.py -x -q -k "all_heads" 2>&1 | tail -1
-export K6_SHAPES="4095:4:32:256,4095:4:32:1,4095:4:64:100"
-timeout 900 python tools/k6_ab.py fused,interleave 2>&1
+# K5-TC at 32 rows/module: 2 k-chunks per stage x 5 stages (variants/libpsk_ch2.so) vs 3 x 3 (default).
+for i in 1 2 3; do
+  echo "ch3: $(timeout 600 python tools/step_ablation.py 32 quick 2>&1 | tail -1)"
+  echo "ch2: $(PSK_LIB=variants/libpsk_ch2.so timeout 600 python tools/step_ablation.py 32 quick 2>&1 | tail -1)"
+done
