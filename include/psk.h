@@ -278,6 +278,12 @@ int psk_decode_attn(const psk_decode_batch* b, const void* q_rot, int32_t n_q_he
  * (synchronizing the device; host may be NULL to query only) and reports
  * the launches recorded so far. */
 int psk_decode_attn_trace_ring(uint64_t* host, int64_t n_u64, int32_t* launches, int32_t* ctas_stride);
+/* Diagnostics: the same launch ring for the K5-TC GEMV (PSK_TRACE_RING=1;
+ * 1024 launches of ctas_stride x 8 stamps: entry, setup done, first TMA,
+ * PDL wait passed, last TMA, last MMA commit, epilogue done, exit); meta
+ * (may be NULL) receives {N, grid} per slot (2 x 1024 ints). */
+int psk_gemv_tc_trace_ring(uint64_t* host, int64_t n_u64, int32_t* meta, int32_t* launches,
+                           int32_t* ctas_stride);
 
 /* Greedy step end: tokens[r] = argmax(logits[r]) (first max, as tf.argMax /
  * torch.argmax), out_tokens[r*max_new + priv_len[r]] = it (if in range),

@@ -107,6 +107,7 @@ _SIGS: dict[str, list] = {
     "psk_decode_attn_kernels": [C.POINTER(DecodeBatchC), _I32, _I32, _I32, C.POINTER(_I32)],
     "psk_decode_attn": [C.POINTER(DecodeBatchC), _P, _I32, _I32, KVLayout, _I32, _P, _P, _P],
     "psk_decode_attn_trace_ring": [_P, _I64, C.POINTER(_I32), C.POINTER(_I32)],
+    "psk_gemv_tc_trace_ring": [_P, _I64, _P, C.POINTER(_I32), C.POINTER(_I32)],
     "psk_argmax_advance": [C.POINTER(DecodeBatchC), _P, _I32, _P, _I32, _P],
     "psk_argmax_rows": [_P, _I32, _I32, _P, _P],
     # prefill (K1-K3)

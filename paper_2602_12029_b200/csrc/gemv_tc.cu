@@ -85,7 +85,18 @@ struct RopeArgs {
   float eps;
   float* ssq;                         // [MAXMOD][64 rows][NORM_MAXNB] per-unit partial sums of squares
   unsigned* cnt;                      // [MAXMOD][2] arrived / departed (zero between launches)
+  unsigned long long* ring;           // diagnostics (PSK_TRACE_RING=1): this launch's [CTA][8] stamps
+  int ring_n;                         //   and its N (which projection)
 };
+
+// Launch-ring stamp (%globaltimer) of phase k by the calling thread
+__device__ __forceinline__ void gring(const RopeArgs& ra, int k) {
+  if (ra.ring != nullptr) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    ra.ring[(size_t)blockIdx.x * 8 + k] = v;
+  }
+}
 
 __device__ __forceinline__ void tmem_ld32_cols(uint32_t taddr, float* v) {
   uint32_t r[32];
@@ -159,6 +170,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   };
 
   if (threadIdx.x == 0) {
+    gring(ra, 0);
     for (int s = 0; s < C::STAGES; ++s) {
       tma::mbar_init(&full[s], 1);
       tma::mbar_init(&empty[s], 1);
@@ -175,6 +187,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   umma::fence_after();
   pdl_trigger();  // the next kernel may start streaming its weights as our CTAs drain
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) gring(ra, 1);
 
   if (warp == 0) {
     // warp-converged (all lanes, warp-uniform operands, one elected lane
@@ -207,6 +220,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int s = j % C::STAGES;
           if (!waited && j == C::STAGES) {
             pdl_wait();
+            if (lane == 0) gring(ra, 3);
             for (int i = 0; i < npend; ++i) load_x(i, pend_k[i], pend_n[i], pend_row[i]);
             waited = true;
           }
@@ -216,6 +230,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int b = 0; b < n; ++b)
             for (int u = 0; u < UW; ++u)
               tma::load_2d_e(&maps.w[mod], &full[s], st + (b * UW + u) * A_BYTES, (kc + b) * BK, blk * UB + u * BN);
+          if (j == 0 && lane == 0) gring(ra, 2);
           if (waited) {
             load_x(s, kc, n, xb);
           } else {
@@ -228,8 +243,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (!waited) {
         pdl_wait();
+        if (lane == 0) gring(ra, 3);
         for (int i = 0; i < npend; ++i) load_x(i, pend_k[i], pend_n[i], pend_row[i]);
       }
+      if (lane == 0) gring(ra, 4);
     }
   } else if (warp == 1) {
     {
@@ -264,6 +281,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         umma::commit_e(&tfull[acc]);
         ++it;
       }
+      if (lane == 0) gring(ra, 5);
     }
   } else {
     // epilogue: warp w reads TMEM lane quarter w % 4 = weight rows 32q..32q+31
@@ -486,6 +504,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }  // u
       ++it;
     }
+    if (threadIdx.x == 64) gring(ra, 6);
   }
   umma::fence_before();
   __syncthreads();
@@ -493,9 +512,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     umma::fence_after();
     umma::tmem_dealloc(tmem, C::TMEM_COLS);
   }
+  if (threadIdx.x == 0) gring(ra, 7);
 }
 
 // ------------------------------------------------------------ host side --
+
+static int sm_count();
+static unsigned long long* ring_slot(int N, int grid);
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -538,6 +561,27 @@ static int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
 
 static int sm_count() { return psk::sm_budget(); }
 
+// Launch ring (diagnostics, PSK_TRACE_RING=1): every launch (captured ones
+// included: the slot is fixed at launch / capture time) stamps its CTAs'
+// phases into the next of RING_SLOTS slots of RING_CTAS x 8 stamps; the
+// slot's N and grid are kept on the host.
+static constexpr int RING_SLOTS = 1024, RING_CTAS = 160;
+static unsigned long long* g_ring = nullptr;
+static int g_ring_n = 0;
+static int g_ring_meta[RING_SLOTS][2];
+static unsigned long long* ring_slot(int N, int grid) {
+  static const bool on = getenv("PSK_TRACE_RING") != nullptr;
+  if (!on || grid > RING_CTAS) return nullptr;
+  if (!g_ring) {
+    if (cudaMalloc(&g_ring, sizeof(unsigned long long) * RING_SLOTS * RING_CTAS * 8) != cudaSuccess) return nullptr;
+    cudaMemset(g_ring, 0, sizeof(unsigned long long) * RING_SLOTS * RING_CTAS * 8);
+  }
+  const int slot = g_ring_n++ % RING_SLOTS;
+  g_ring_meta[slot][0] = N;
+  g_ring_meta[slot][1] = grid;
+  return g_ring + (size_t)slot * RING_CTAS * 8;
+}
+
 constexpr int FLAG_BYTES = 4096;  // one int per CTA (<= 1024 SMs)
 
 template <int MN, int EPI, int UW>
@@ -574,8 +618,11 @@ static int launch_uw(const void* x, int n_rows, int K, const void* const* W_host
   if (whole_units && units <= sms) grid = (int)units;
   int* flags = reinterpret_cast<int*>(ws);
   float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + FLAG_BYTES);
+  RopeArgs rr = ra;
+  rr.ring = ring_slot(N, grid);
+  rr.ring_n = N;
   PSK_CUDA_TRY(psk::launch_pdl(k, dim3(grid), dim3(THREADS), (size_t)smem_bytes, s, maps, mrs, n_mod, N, K,
-                               out, part, flags, ra));
+                               out, part, flags, rr));
   PSK_LAUNCH_CHECK();
   return PSK_OK;
 }
@@ -609,6 +656,24 @@ static int dispatch(int epi, const void* x, int n_rows, int K, const void* const
 }  // namespace psk
 
 static int64_t part_bytes() { return (int64_t)psk::device_sms() * 2 * 64 * psk::gemv_tc::BN * 4; }  // UW <= 2 x MN <= 64
+
+extern "C" int psk_gemv_tc_trace_ring(uint64_t* host, int64_t n_u64, int32_t* meta, int32_t* launches,
+                                      int32_t* ctas_stride) {
+  using namespace psk::gemv_tc;
+  PSK_CHECK_ARG(launches && ctas_stride, "psk_gemv_tc_trace_ring: bad args");
+  *launches = g_ring_n;
+  *ctas_stride = RING_CTAS;
+  if (!g_ring || !host) return PSK_OK;
+  const int64_t cap = (int64_t)RING_SLOTS * RING_CTAS * 8;
+  PSK_CUDA_TRY(cudaDeviceSynchronize());
+  PSK_CUDA_TRY(cudaMemcpy(host, g_ring, sizeof(uint64_t) * (n_u64 < cap ? n_u64 : cap), cudaMemcpyDeviceToHost));
+  if (meta)
+    for (int i = 0; i < RING_SLOTS; ++i) {
+      meta[2 * i] = g_ring_meta[i][0];
+      meta[2 * i + 1] = g_ring_meta[i][1];
+    }
+  return PSK_OK;
+}
 
 extern "C" int psk_gemv_tc_workspace(int64_t* bytes) {
   PSK_CHECK_ARG(bytes != nullptr, "psk_gemv_tc_workspace: null out");

@@ -78,10 +78,10 @@ __global__ void bulk_kernel(const char* __restrict__ src, int64_t bytes, int sta
 
 
 __global__ void tma_kernel(const __grid_constant__ CUtensorMap map, int64_t row_blocks, int kchunks, int stages,
-                           int nbox, float* sink) {
+                           int nbox, float* sink, const __grid_constant__ CUtensorMap xmap, int xbox) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
-  const int stage_bytes = nbox * 16384;
+  const int stage_bytes = nbox * (16384 + xbox * 4096);  // xbox: + one 32 x 64 activation box per k-chunk (L2)
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)stages * stage_bytes);
   uint64_t* empty = full + stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x / 32 - 1;
@@ -106,12 +106,19 @@ __global__ void tma_kernel(const __grid_constant__ CUtensorMap map, int64_t row_
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[s])), "r"(stage_bytes));
         const int64_t rb = u / per_unit;
         const int kc0 = (int)(u % per_unit) * nbox;
-        for (int b = 0; b < nbox; ++b)
+        for (int b = 0; b < nbox; ++b) {
           asm volatile(
               "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
                   sa(sm + (size_t)s * stage_bytes + b * 16384)),
               "l"(&map), "r"(sa(&full[s])), "r"((kc0 + b) * 64), "r"((int)(rb * 128))
               : "memory");
+          if (xbox)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+                    sa(sm + (size_t)s * stage_bytes + nbox * 16384 + b * 4096)),
+                "l"(&xmap), "r"(sa(&full[s])), "r"((kc0 + b) * 64), "r"(0)
+                : "memory");
+        }
       }
     }
     __syncwarp();
@@ -205,13 +212,22 @@ int main() {
       enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_128B, promo ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      struct T { int stages, nbox; } tc[] = {{12, 1}, {6, 2}, {3, 4}, {4, 3}};
+      // x: a 32-row activation tensor (L2-resident), one 32 x 64 box per k-chunk when xbox
+      CUtensorMap xmap;
+      cuuint64_t xdims[2] = {(cuuint64_t)K, 32};
+      cuuint32_t xb[2] = {64, 32};
+      enc(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, xdims, strides, xb, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      struct T { int stages, nbox, xbox; } tc[] = {{12, 1, 0}, {6, 2, 0}, {3, 4, 0}, {4, 3, 0}, {3, 3, 0},
+                                                   {3, 3, 1}, {2, 4, 1}, {5, 2, 1}, {10, 1, 1}};
       for (auto t : tc) {
-        const int smem = t.stages * t.nbox * 16384 + 1024 + 256;
+        const int smem = t.stages * t.nbox * (16384 + t.xbox * 4096) + 1024 + 256;
         cudaFuncSetAttribute(tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         char name[128];
-        snprintf(name, sizeof name, "tma 128x64 SW128 boxes: %d stages x %d boxes promo=%d", t.stages, t.nbox, promo);
-        timeit([&] { tma_kernel<<<sms, 288, smem>>>(map, rows / 128, (int)(K / 64), t.stages, t.nbox, sink); }, name);
+        snprintf(name, sizeof name, "tma 128x64 SW128 boxes: %d stages x %d boxes%s promo=%d", t.stages, t.nbox,
+                 t.xbox ? " (+x box each)" : "", promo);
+        timeit([&] { tma_kernel<<<sms, 288, smem>>>(map, rows / 128, (int)(K / 64), t.stages, t.nbox, sink, xmap,
+                                                     t.xbox); }, name);
       }
     }
   }

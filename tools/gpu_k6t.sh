@@ -1,6 +1,3 @@
 #!/bin/bash
-# K5-TC at 32 rows/module: 2 k-chunks per stage x 5 stages (variants/libpsk_ch2.so) vs 3 x 3 (default).
-for i in 1 2 3; do
-  echo "ch3: $(timeout 600 python tools/step_ablation.py 32 quick 2>&1 | tail -1)"
-  echo "ch2: $(PSK_LIB=variants/libpsk_ch2.so timeout 600 python tools/step_ablation.py 32 quick 2>&1 | tail -1)"
-done
+timeout 900 python -m pytest tests/test_gemv_gpu.py tests/test_fused_qkv_gpu.py -x -q 2>&1 | tail -1
+timeout 900 python tools/step_trace.py 32 2>&1 | tail -22
