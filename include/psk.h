@@ -351,6 +351,40 @@ int psk_embed_tokens(const int64_t* tokens, int32_t T, const void* table, int32_
 int psk_kv_copy_pages(const void* src_base, void* dst_base, const int32_t* src_pages,
                       const int32_t* dst_pages, int32_t n_pages, int64_t page_bytes, void* stream);
 
+/* ------------------------------------------------------------------------ *
+ * TinyLM — the reference's own model (frontend/src/model.ts:112-331) on the
+ * GPU, fp32, over a paged prompt cache. Replaces TinyLM.forward(tokens,
+ * past) (model.ts:246-331): `past_len` tokens already in the sequences'
+ * pages (PromptCache, model.ts:41-88, as block tables: slice(n) is a shorter
+ * table, so a decode module reads the base module's pages in place), n_new
+ * tokens per sequence appended at positions past_len.. (their K/V written
+ * into the pages the block table names; the caller gives a sequence a
+ * private copy of a partially filled page before appending to it).
+ * prev_first[b] = token before tokens[b][0] (the cache's last covered token;
+ * -1 when the cache is empty), the prev-token channel of model.ts:262-270.
+ * logits [batch][n_new][vocab] fp32. Pages: [page][layer][K|V][head][16][hd]
+ * fp32. Errors as model.ts:249-258 (PSK_EINVAL: over-length, width not
+ * divisible by heads). scratch: psk_tiny_scratch_floats floats.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t layers, width, heads, context, vocab;
+  const float* tok_emb;  /* [vocab][width] */
+  const float* prev_emb; /* [vocab][width] */
+  const float* pos_emb;  /* [context][width] */
+  const float* lnf_g;
+  const float* lnf_b;
+  const float* head; /* [width][vocab] */
+  /* device array of layers x 12 pointers (model.ts:147-169 order): ln1g ln1b
+   * wq wk wv wo ([width][width], x @ W) ln2g ln2b wUp [width][4 width] bUp
+   * wDown [4 width][width] bDown */
+  const float* const* blocks;
+} psk_tiny_model;
+int psk_tiny_scratch_floats(const psk_tiny_model* m, int32_t batch, int32_t n_new, int64_t* out);
+int psk_tiny_forward(const psk_tiny_model* m, int32_t batch, int32_t n_new, int32_t past_len,
+                     const int32_t* tokens, const int32_t* prev_first, const int32_t* block_table,
+                     int32_t max_pages, float* kv_pages, int64_t n_pages, float* scratch, float* logits,
+                     void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -63,6 +63,14 @@ class DecodeBatchC(C.Structure):
     ]
 
 
+class TinyModelC(C.Structure):
+    """psk_tiny_model (include/psk.h)."""
+    _fields_ = [("layers", C.c_int32), ("width", C.c_int32), ("heads", C.c_int32), ("context", C.c_int32),
+                ("vocab", C.c_int32), ("tok_emb", C.c_void_p), ("prev_emb", C.c_void_p),
+                ("pos_emb", C.c_void_p), ("lnf_g", C.c_void_p), ("lnf_b", C.c_void_p), ("head", C.c_void_p),
+                ("blocks", C.c_void_p)]
+
+
 _P = C.c_void_p
 _I32 = C.c_int32
 _I64 = C.c_int64
@@ -120,6 +128,8 @@ _SIGS: dict[str, list] = {
     "psk_gemm_qkv_rope_kv_rows": [_P, _P, _I32, _I32, _I32, _P, _P, _P, KVLayout, _I32, _P, _P],
     "psk_embed_tokens": [_P, _I32, _P, _I32, _P, _P],
     "psk_kv_copy_pages": [_P, _P, _P, _P, _I32, _I64, _P],
+    "psk_tiny_scratch_floats": [_P, _I32, _I32, _P],
+    "psk_tiny_forward": [_P, _I32, _I32, _I32, _P, _P, _P, _I32, _P, _I64, _P, _P, _P],
 }
 _RESTYPE = {
     "psk_last_error": C.c_char_p,

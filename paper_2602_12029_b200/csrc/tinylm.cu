@@ -1,0 +1,218 @@
+// TinyLM forward on the GPU over a paged prompt cache (psk_tiny_forward).
+//
+// The reference's own model (frontend/src/model.ts:112-331): token +
+// previous-token + learned position embeddings, L x [LayerNorm -> Q/K/V ->
+// causal softmax attention over [cached prefix | new tokens] -> Wo ->
+// residual -> LayerNorm -> GELU-tanh MLP (biases) -> residual], final
+// LayerNorm -> head. fp32 like the reference (tfjs is fp32).
+//
+// B200 form: one CTA per sequence runs every layer of the forward
+// (a 64-256 wide model is launch- and latency-bound: one launch per
+// forward, activations in L1/L2-resident scratch). The prompt cache is
+// paged instead of model.ts's concatenated [B, H, S, hd] tensors: 16-token
+// pages [page][layer][K|V][head][16][hd], a block table per sequence, so a
+// decode module's forward reads the frozen base's pages of the shared
+// prefix in place (PromptCache.slice, model.ts:58-70, becomes a shorter
+// block table) and appends its own tokens to its own pages.
+#include "common.cuh"
+#include "psk.h"
+
+namespace psk {
+namespace tiny {
+
+constexpr int PT = 16;
+constexpr int THREADS = 256;
+constexpr int WARPS = THREADS / 32;
+constexpr int NPTR = 12;  // per-layer parameter pointers (psk.h)
+
+struct Args {
+  psk_tiny_model m;
+  int T, S0, max_pages;
+  const int32_t* tokens;
+  const int32_t* prev_first;
+  const int32_t* table;
+  float* kv;
+  float* scratch;
+  float* logits;
+};
+
+// LayerNorm of T rows of width d, eps 1e-5, biased variance (model.ts:120-123): warp per row.
+__device__ void layer_norm(const float* in, float* out, const float* g, const float* b, int T, int d) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = warp; t < T; t += WARPS) {
+    const float* x = in + (int64_t)t * d;
+    float s = 0.f;
+    for (int c = lane; c < d; c += 32) s += x[c];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mean = s / d;
+    float v = 0.f;
+    for (int c = lane; c < d; c += 32) {
+      const float e = x[c] - mean;
+      v += e * e;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const float inv = 1.f / sqrtf(v / d + 1e-5f);
+    for (int c = lane; c < d; c += 32) out[(int64_t)t * d + c] = (x[c] - mean) * inv * g[c] + b[c];
+  }
+}
+
+__device__ __forceinline__ float gelu_tanh(float x) {  // model.ts:114-118
+  return 0.5f * x * (1.f + tanhf((x + 0.044715f * x * x * x) * 0.7978845608028654f));
+}
+
+// Y[t, n] (op)= sum_k X[t, k] W[k, n] (+ bias[n]) for t < T, n < N: thread
+// per output, consecutive threads on consecutive n (W rows coalesced, the X
+// row broadcast).
+template <class Out>
+__device__ void matmul(const float* X, int T, int K, const float* W, int N, const float* bias, Out out) {
+  for (int i = threadIdx.x; i < T * N; i += THREADS) {
+    const int t = i / N, n = i - t * N;
+    const float* x = X + (int64_t)t * K;
+    float acc = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) acc = fmaf(x[k], W[(int64_t)k * N + n], acc);
+    if (bias) acc += bias[n];
+    out(t, n, acc);
+  }
+}
+
+__global__ void __launch_bounds__(THREADS) tiny_forward_kernel(const Args a) {
+  extern __shared__ float s_p[];  // per warp: the attention row's probabilities
+  const psk_tiny_model& m = a.m;
+  const int b = blockIdx.x, T = a.T, S0 = a.S0, d = m.width, H = m.heads, hd = d / H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t page_f = (int64_t)m.layers * 2 * PT * d;  // floats per page
+  float* x = a.scratch + (int64_t)b * 8 * T * d;
+  float* xn = x + (int64_t)T * d;
+  float* q = xn + (int64_t)T * d;
+  float* ctx = q + (int64_t)T * d;
+  float* hid = ctx + (int64_t)T * d;  // [T][4d]
+  const int32_t* tok = a.tokens + (int64_t)b * T;
+  const int32_t* tab = a.table + (int64_t)b * a.max_pages;
+  // embeddings (model.ts:262-276): previous token of position 0 = the last
+  // token the cache covers (-1: none -> no prev-token term)
+  for (int i = threadIdx.x; i < T * d; i += THREADS) {
+    const int t = i / d, c = i - t * d;
+    const int prev = t > 0 ? tok[t - 1] : a.prev_first[b];
+    float v = m.tok_emb[(int64_t)tok[t] * d + c] + (prev >= 0 ? m.prev_emb[(int64_t)prev * d + c] : 0.f);
+    x[i] = v + m.pos_emb[(int64_t)(S0 + t) * d + c];
+  }
+  __syncthreads();
+  const float scale = 1.f / sqrtf((float)hd);
+  for (int l = 0; l < m.layers; ++l) {
+    const float* const* w = m.blocks + (int64_t)l * NPTR;
+    layer_norm(x, xn, w[0], w[1], T, d);
+    __syncthreads();
+    matmul(xn, T, d, w[2], d, nullptr, [&](int t, int n, float v) { q[(int64_t)t * d + n] = v; });
+    // K / V of the new tokens -> their pages (positions S0 .. S0 + T - 1)
+    for (int kv = 0; kv < 2; ++kv)
+      matmul(xn, T, d, w[3 + kv], d, nullptr, [&](int t, int n, float v) {
+        const int pos = S0 + t, hh = n / hd;
+        float* pg = a.kv + (int64_t)tab[pos / PT] * page_f;
+        pg[(((int64_t)(l * 2 + kv) * H + hh) * PT + pos % PT) * hd + (n - hh * hd)] = v;
+      });
+    __syncthreads();
+    // attention: a warp per (new token, head) over keys 0 .. S0 + t (the
+    // reference's -1e9 mask on later keys is an exact zero after exp)
+    float* pr = s_p + (int64_t)warp * m.context;
+    for (int w8 = warp; w8 < T * H; w8 += WARPS) {
+      const int t = w8 / H, hh = w8 - t * H, S = S0 + t + 1;
+      const float* qv = q + (int64_t)t * d + hh * hd;
+      float mx = -INFINITY;
+      for (int j = lane; j < S; j += 32) {
+        const float* kr = a.kv + (int64_t)tab[j / PT] * page_f + (((int64_t)(l * 2) * H + hh) * PT + j % PT) * hd;
+        float s = 0.f;
+        for (int e = 0; e < hd; ++e) s = fmaf(qv[e], kr[e], s);
+        s *= scale;
+        pr[j] = s;
+        mx = fmaxf(mx, s);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      float sum = 0.f;
+      for (int j = lane; j < S; j += 32) {
+        const float e = expf(pr[j] - mx);
+        pr[j] = e;
+        sum += e;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      __syncwarp();
+      const float inv = 1.f / sum;
+      for (int e = lane; e < hd; e += 32) {
+        float acc = 0.f;
+        for (int j = 0; j < S; ++j)
+          acc = fmaf(pr[j], a.kv[(int64_t)tab[j / PT] * page_f + (((int64_t)(l * 2 + 1) * H + hh) * PT + j % PT) * hd + e],
+                     acc);
+        ctx[(int64_t)t * d + hh * hd + e] = acc * inv;
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    matmul(ctx, T, d, w[5], d, nullptr, [&](int t, int n, float v) { x[(int64_t)t * d + n] += v; });
+    __syncthreads();
+    layer_norm(x, xn, w[6], w[7], T, d);
+    __syncthreads();
+    matmul(xn, T, d, w[8], 4 * d, w[9], [&](int t, int n, float v) { hid[(int64_t)t * 4 * d + n] = gelu_tanh(v); });
+    __syncthreads();
+    matmul(hid, T, 4 * d, w[10], d, w[11], [&](int t, int n, float v) { x[(int64_t)t * d + n] += v; });
+    __syncthreads();
+  }
+  layer_norm(x, xn, m.lnf_g, m.lnf_b, T, d);
+  __syncthreads();
+  float* lg = a.logits + (int64_t)b * T * m.vocab;
+  matmul(xn, T, d, m.head, m.vocab, nullptr, [&](int t, int n, float v) { lg[(int64_t)t * m.vocab + n] = v; });
+}
+
+}  // namespace tiny
+}  // namespace psk
+
+extern "C" {
+
+int psk_tiny_scratch_floats(const psk_tiny_model* m, int32_t batch, int32_t n_new, int64_t* out) {
+  PSK_CHECK_ARG(m && out && batch >= 0 && n_new >= 0, "psk_tiny_scratch_floats: bad args");
+  *out = (int64_t)batch * 8 * n_new * m->width;
+  return PSK_OK;
+}
+
+int psk_tiny_forward(const psk_tiny_model* m, int32_t batch, int32_t n_new, int32_t past_len,
+                     const int32_t* tokens, const int32_t* prev_first, const int32_t* block_table,
+                     int32_t max_pages, float* kv_pages, int64_t n_pages, float* scratch, float* logits,
+                     void* stream) {
+  using namespace psk::tiny;
+  PSK_CHECK_ARG(m && tokens && prev_first && block_table && kv_pages && scratch && logits && m->blocks,
+                "psk_tiny_forward: null argument");
+  PSK_CHECK_ARG(m->layers > 0 && m->width > 0 && m->heads > 0 && m->width % m->heads == 0 && m->vocab > 0,
+                "width %d not divisible by heads %d", m->width, m->heads);
+  PSK_CHECK_ARG(batch > 0 && n_new > 0 && past_len >= 0, "psk_tiny_forward: empty batch");
+  PSK_CHECK_ARG(past_len + n_new <= m->context, "sequence length %d exceeds context %d", past_len + n_new,
+                m->context);
+  PSK_CHECK_ARG((int64_t)max_pages * PT >= past_len + n_new && n_pages > 0,
+                "block table of %d pages cannot hold %d tokens", max_pages, past_len + n_new);
+  const size_t smem = sizeof(float) * WARPS * m->context;
+  PSK_CHECK_ARG(smem <= 200 * 1024, "context %d too long for the attention row buffer", m->context);
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    PSK_CUDA_TRY(cudaFuncSetAttribute(tiny_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    smem_set = smem;
+  }
+  Args a;
+  a.m = *m;
+  a.T = n_new;
+  a.S0 = past_len;
+  a.max_pages = max_pages;
+  a.tokens = tokens;
+  a.prev_first = prev_first;
+  a.table = block_table;
+  a.kv = kv_pages;
+  a.scratch = scratch;
+  a.logits = logits;
+  tiny_forward_kernel<<<batch, THREADS, smem, psk::as_stream(stream)>>>(a);
+  PSK_LAUNCH_CHECK();
+  return PSK_OK;
+}
+
+}  // extern "C"
