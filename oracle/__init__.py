@@ -20,9 +20,10 @@ product path fails loudly without its CUDA extension.
   oracle/tinylm.py  literal restatement of the reference TinyLM
                     (frontend/src/model.ts:112-331, rng.ts splitmix64 /
                     Box-Muller init; RNG pinned by rng.test.ts:5-13), with the
-                    reference's KV-cache property tests mirrored. Tensor parity
-                    is unpinned at the tfjs boundary (no node in the image; the
-                    reference publishes no tensor golden values).
+                    reference's KV-cache property tests mirrored; the checker of
+                    the GPU TinyLM (paper_2602_12029_b200/tinylm.py). Tensor
+                    parity is unpinned at the tfjs boundary (no node in the
+                    image; the reference publishes no tensor golden values).
 
 The router and workload generator have no separate oracle module: the
 product's own router.py / workload.py are compared directly with traces the
