@@ -542,6 +542,46 @@ def pd_split_point(world: int, rank: int, local: int, ctrl, duration: float = 10
     return out
 
 
+def tinylm_point(n_prompts: int = 32, n: int = 255, ratio: float = 0.5, reps: int = 5) -> dict:
+    """The reference's own TinyLM at its DEFAULT_MODEL (model.ts:26-31: 4
+    layers, width 128, 4 heads, 256 context; vocab 64): one evaluateSharing
+    call (evaluate.ts:21-50: base cache of n prompts, slice at m = ceil(r n),
+    decode module's forward of the tails, greedy predictions) through the
+    public API (host prompts in, host predictions out), GPU (psk_tiny_forward,
+    fp32) vs the CPU oracle restatement on the same call (torch fp32, all host
+    threads). Wall time per call, median of `reps`."""
+    import torch
+
+    import oracle.tinylm as O
+    from paper_2602_12029_b200 import tinylm as G
+    shape = (4, 128, 4, 256, 64)
+    pool = G.TinyKVPool(G.TinyConfig(*shape), n_prompts * 2 * (n // 16 + 2) + 16)
+    gb, gd = G.TinyLM.init(G.TinyConfig(*shape), 1, pool=pool), G.TinyLM.init(G.TinyConfig(*shape), 2, pool=pool)
+    ob, od = O.TinyLM.init(O.TinyConfig(*shape), 1), O.TinyLM.init(O.TinyConfig(*shape), 2)
+    r = O.Rng(7)
+    prompts = [[r.int(64) for _ in range(n)] for _ in range(n_prompts)]
+
+    def gpu_call():
+        pool.next = 0  # the call's pages are reused (same shapes every rep)
+        pool.filled[:] = 0
+        return G.sharing_predictions(gd, gb, ratio, prompts)
+
+    gpu_call()
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        got = gpu_call()
+        ts.append(time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    want = O.evaluate_sharing_predictions(od, ob, ratio, prompts)
+    t_cpu = time.perf_counter() - t0
+    g_ms = statistics.median(ts) * 1e3
+    return {"workload": f"evaluateSharing at r={ratio}: {n_prompts} prompts x {n} tokens, DEFAULT_MODEL",
+            "gpu_ms_per_call": round(g_ms, 2), "cpu_oracle_ms_per_call": round(t_cpu * 1e3, 1),
+            "cpu_threads": torch.get_num_threads(), "predictions_match_oracle": got == want}
+
+
 def prefill_roofline(eng, peaks) -> dict:
     import torch
     T = PROMPT
@@ -703,6 +743,7 @@ def main() -> None:
         torch.cuda.empty_cache()
         out["decode_attn_fanout_32k_x16"] = decode_attn_fanout(peaks)
         out["pool"] = pool_ops()
+        out["tinylm"] = tinylm_point()
         if world == 1:
             ref = CpuReference(S)
             ref.sample()  # warm-up
