@@ -62,24 +62,60 @@ __device__ __forceinline__ float gelu_tanh(float x) {  // model.ts:114-118
   return 0.5f * x * (1.f + tanhf((x + 0.044715f * x * x * x) * 0.7978845608028654f));
 }
 
-// Y[t, n] (op)= sum_k X[t, k] W[k, n] (+ bias[n]) for t < T, n < N: thread
-// per output, consecutive threads on consecutive n (W rows coalesced, the X
-// row broadcast).
+// Y[t, n] (op)= sum_k X[t, k] W[k, n] (+ bias[n]) for t < T, n < N: 64 x 64
+// output tiles through shared memory (16-deep k slabs of X and W), each
+// thread a 4 x 4 register block; k accumulates in order. Call with every
+// thread of the CTA.
+constexpr int BM = 64, BN = 64, BK = 16;
+struct Tiles {
+  float A[BK][BM + 4], B[BK][BN];
+};
 template <class Out>
-__device__ void matmul(const float* X, int T, int K, const float* W, int N, const float* bias, Out out) {
-  for (int i = threadIdx.x; i < T * N; i += THREADS) {
-    const int t = i / N, n = i - t * N;
-    const float* x = X + (int64_t)t * K;
-    float acc = 0.f;
-#pragma unroll 4
-    for (int k = 0; k < K; ++k) acc = fmaf(x[k], W[(int64_t)k * N + n], acc);
-    if (bias) acc += bias[n];
-    out(t, n, acc);
-  }
+__device__ void matmul(Tiles& tl, const float* X, int T, int K, const float* W, int N, const float* bias, Out out) {
+  auto& As = tl.A;
+  auto& Bs = tl.B;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  for (int m0 = 0; m0 < T; m0 += BM)
+    for (int n0 = 0; n0 < N; n0 += BN) {
+      float acc[4][4] = {};
+      for (int k0 = 0; k0 < K; k0 += BK) {
+        for (int i = threadIdx.x; i < BM * BK; i += THREADS) {
+          const int r = i / BK, c = i - r * BK, t = m0 + r, k = k0 + c;
+          As[c][r] = (t < T && k < K) ? X[(int64_t)t * K + k] : 0.f;
+        }
+        for (int i = threadIdx.x; i < BK * BN; i += THREADS) {
+          const int r = i / BN, c = i - r * BN, k = k0 + r, n = n0 + c;
+          Bs[r][c] = (k < K && n < N) ? W[(int64_t)k * N + n] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+          float a4[4], b4[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            a4[i] = As[kk][ty * 4 + i];
+            b4[i] = Bs[kk][tx * 4 + i];
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a4[i], b4[j], acc[i][j]);
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+          if (t < T && n < N) out(t, n, acc[i][j] + (bias ? bias[n] : 0.f));
+        }
+    }
 }
 
-__global__ void __launch_bounds__(THREADS) tiny_forward_kernel(const Args a) {
-  extern __shared__ float s_p[];  // per warp: the attention row's probabilities
+__global__ void __launch_bounds__(THREADS, 1) tiny_forward_kernel(const Args a) {
+  extern __shared__ float s_p[];  // one head's K / V rows, then per warp: probabilities + q
+  __shared__ Tiles tiles;
   const psk_tiny_model& m = a.m;
   const int b = blockIdx.x, T = a.T, S0 = a.S0, d = m.width, H = m.heads, hd = d / H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -105,65 +141,80 @@ __global__ void __launch_bounds__(THREADS) tiny_forward_kernel(const Args a) {
     const float* const* w = m.blocks + (int64_t)l * NPTR;
     layer_norm(x, xn, w[0], w[1], T, d);
     __syncthreads();
-    matmul(xn, T, d, w[2], d, nullptr, [&](int t, int n, float v) { q[(int64_t)t * d + n] = v; });
+    matmul(tiles, xn, T, d, w[2], d, nullptr, [&](int t, int n, float v) { q[(int64_t)t * d + n] = v; });
     // K / V of the new tokens -> their pages (positions S0 .. S0 + T - 1)
     for (int kv = 0; kv < 2; ++kv)
-      matmul(xn, T, d, w[3 + kv], d, nullptr, [&](int t, int n, float v) {
+      matmul(tiles, xn, T, d, w[3 + kv], d, nullptr, [&](int t, int n, float v) {
         const int pos = S0 + t, hh = n / hd;
         float* pg = a.kv + (int64_t)tab[pos / PT] * page_f;
         pg[(((int64_t)(l * 2 + kv) * H + hh) * PT + pos % PT) * hd + (n - hh * hd)] = v;
       });
     __syncthreads();
-    // attention: a warp per (new token, head) over keys 0 .. S0 + t (the
-    // reference's -1e9 mask on later keys is an exact zero after exp)
-    float* pr = s_p + (int64_t)warp * m.context;
-    for (int w8 = warp; w8 < T * H; w8 += WARPS) {
-      const int t = w8 / H, hh = w8 - t * H, S = S0 + t + 1;
-      const float* qv = q + (int64_t)t * d + hh * hd;
-      float mx = -INFINITY;
-      for (int j = lane; j < S; j += 32) {
-        const float* kr = a.kv + (int64_t)tab[j / PT] * page_f + (((int64_t)(l * 2) * H + hh) * PT + j % PT) * hd;
-        float s = 0.f;
-        for (int e = 0; e < hd; ++e) s = fmaf(qv[e], kr[e], s);
-        s *= scale;
-        pr[j] = s;
-        mx = fmaxf(mx, s);
+    // attention, head by head: the head's K / V rows for keys 0 .. S0+T-1
+    // staged in shared memory ([key][hd + 1]: conflict-free for a lane per
+    // key and for a lane per dim), then a warp per new token t over keys
+    // 0 .. S0 + t (the reference's -1e9 mask on later keys is an exact zero
+    // after exp)
+    const int S_all = S0 + T, hs = hd + 1;
+    float* Ks = s_p;
+    float* Vs = Ks + (int64_t)S_all * hs;
+    float* pr = Vs + (int64_t)S_all * hs + (int64_t)warp * (m.context + hd);
+    float* qs = pr + m.context;
+    for (int hh = 0; hh < H; ++hh) {
+      for (int i = threadIdx.x; i < S_all * hd; i += THREADS) {
+        const int j = i / hd, e = i - j * hd;
+        const float* pg = a.kv + (int64_t)tab[j / PT] * page_f + (((int64_t)(l * 2) * H + hh) * PT + j % PT) * hd + e;
+        Ks[j * hs + e] = pg[0];
+        Vs[j * hs + e] = pg[(int64_t)H * PT * hd];  // V sits H tiles after K
       }
+      __syncthreads();
+      for (int t = warp; t < T; t += WARPS) {
+        const int S = S0 + t + 1;
+        for (int e = lane; e < hd; e += 32) qs[e] = q[(int64_t)t * d + hh * hd + e];
+        __syncwarp();
+        float mx = -INFINITY;
+        for (int j = lane; j < S; j += 32) {
+          const float* kr = Ks + j * hs;
+          float sc = 0.f;
+          for (int e = 0; e < hd; ++e) sc = fmaf(qs[e], kr[e], sc);
+          sc *= scale;
+          pr[j] = sc;
+          mx = fmaxf(mx, sc);
+        }
 #pragma unroll
-      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      float sum = 0.f;
-      for (int j = lane; j < S; j += 32) {
-        const float e = expf(pr[j] - mx);
-        pr[j] = e;
-        sum += e;
-      }
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float sum = 0.f;
+        for (int j = lane; j < S; j += 32) {
+          const float ex = expf(pr[j] - mx);
+          pr[j] = ex;
+          sum += ex;
+        }
 #pragma unroll
-      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      __syncwarp();
-      const float inv = 1.f / sum;
-      for (int e = lane; e < hd; e += 32) {
-        float acc = 0.f;
-        for (int j = 0; j < S; ++j)
-          acc = fmaf(pr[j], a.kv[(int64_t)tab[j / PT] * page_f + (((int64_t)(l * 2 + 1) * H + hh) * PT + j % PT) * hd + e],
-                     acc);
-        ctx[(int64_t)t * d + hh * hd + e] = acc * inv;
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        __syncwarp();
+        const float inv = 1.f / sum;
+        for (int e = lane; e < hd; e += 32) {
+          float acc = 0.f;
+          for (int j = 0; j < S; ++j) acc = fmaf(pr[j], Vs[j * hs + e], acc);
+          ctx[(int64_t)t * d + hh * hd + e] = acc * inv;
+        }
+        __syncwarp();
       }
-      __syncwarp();
+      __syncthreads();
     }
-    __syncthreads();
-    matmul(ctx, T, d, w[5], d, nullptr, [&](int t, int n, float v) { x[(int64_t)t * d + n] += v; });
+    matmul(tiles, ctx, T, d, w[5], d, nullptr, [&](int t, int n, float v) { x[(int64_t)t * d + n] += v; });
     __syncthreads();
     layer_norm(x, xn, w[6], w[7], T, d);
     __syncthreads();
-    matmul(xn, T, d, w[8], 4 * d, w[9], [&](int t, int n, float v) { hid[(int64_t)t * 4 * d + n] = gelu_tanh(v); });
+    matmul(tiles, xn, T, d, w[8], 4 * d, w[9], [&](int t, int n, float v) { hid[(int64_t)t * 4 * d + n] = gelu_tanh(v); });
     __syncthreads();
-    matmul(hid, T, 4 * d, w[10], d, w[11], [&](int t, int n, float v) { x[(int64_t)t * d + n] += v; });
+    matmul(tiles, hid, T, 4 * d, w[10], d, w[11], [&](int t, int n, float v) { x[(int64_t)t * d + n] += v; });
     __syncthreads();
   }
   layer_norm(x, xn, m.lnf_g, m.lnf_b, T, d);
   __syncthreads();
   float* lg = a.logits + (int64_t)b * T * m.vocab;
-  matmul(xn, T, d, m.head, m.vocab, nullptr, [&](int t, int n, float v) { lg[(int64_t)t * m.vocab + n] = v; });
+  matmul(tiles, xn, T, d, m.head, m.vocab, nullptr, [&](int t, int n, float v) { lg[(int64_t)t * m.vocab + n] = v; });
 }
 
 }  // namespace tiny
@@ -191,8 +242,9 @@ int psk_tiny_forward(const psk_tiny_model* m, int32_t batch, int32_t n_new, int3
                 m->context);
   PSK_CHECK_ARG((int64_t)max_pages * PT >= past_len + n_new && n_pages > 0,
                 "block table of %d pages cannot hold %d tokens", max_pages, past_len + n_new);
-  const size_t smem = sizeof(float) * WARPS * m->context;
-  PSK_CHECK_ARG(smem <= 200 * 1024, "context %d too long for the attention row buffer", m->context);
+  const int hd = m->width / m->heads;
+  const size_t smem = sizeof(float) * (2 * (size_t)(past_len + n_new) * (hd + 1) + WARPS * (size_t)(m->context + hd));
+  PSK_CHECK_ARG(smem <= 200 * 1024, "context %d x head dim %d too large for the staged attention", m->context, hd);
   static size_t smem_set = 0;
   if (smem > 48 * 1024 && smem > smem_set) {
     PSK_CUDA_TRY(cudaFuncSetAttribute(tiny_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
