@@ -63,9 +63,9 @@ __device__ __forceinline__ float gelu_tanh(float x) {  // model.ts:114-118
 }
 
 // Y[t, n] (op)= sum_k X[t, k] W[k, n] (+ bias[n]) for t < T, n < N: 64 x 64
-// output tiles through shared memory (16-deep k slabs of X and W), each
-// thread a 4 x 4 register block; k accumulates in order. Call with every
-// thread of the CTA.
+// output tiles through shared memory (16-deep k slabs of X and W, the next
+// slab's loads in flight under this one's FMAs), each thread a 4 x 4
+// register block; k accumulates in order. Call with every thread of the CTA.
 constexpr int BM = 64, BN = 64, BK = 16;
 struct Tiles {
   float A[BK][BM + 4], B[BK][BN];
@@ -78,16 +78,35 @@ __device__ void matmul(Tiles& tl, const float* X, int T, int K, const float* W, 
   for (int m0 = 0; m0 < T; m0 += BM)
     for (int n0 = 0; n0 < N; n0 += BN) {
       float acc[4][4] = {};
-      for (int k0 = 0; k0 < K; k0 += BK) {
-        for (int i = threadIdx.x; i < BM * BK; i += THREADS) {
-          const int r = i / BK, c = i - r * BK, t = m0 + r, k = k0 + c;
-          As[c][r] = (t < T && k < K) ? X[(int64_t)t * K + k] : 0.f;
+      // the next k slab is loaded into registers while this one computes
+      constexpr int LA = BM * BK / THREADS, LB = BK * BN / THREADS;
+      float ra[LA], rb[LB];
+      auto load = [&](int k0) {
+#pragma unroll
+        for (int u = 0; u < LA; ++u) {
+          const int i = threadIdx.x + u * THREADS, r = i / BK, c = i - r * BK, t = m0 + r, k = k0 + c;
+          ra[u] = (t < T && k < K) ? X[(int64_t)t * K + k] : 0.f;
         }
-        for (int i = threadIdx.x; i < BK * BN; i += THREADS) {
-          const int r = i / BN, c = i - r * BN, k = k0 + r, n = n0 + c;
-          Bs[r][c] = (k < K && n < N) ? W[(int64_t)k * N + n] : 0.f;
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          const int i = threadIdx.x + u * THREADS, r = i / BN, c = i - r * BN, k = k0 + r, n = n0 + c;
+          rb[u] = (k < K && n < N) ? W[(int64_t)k * N + n] : 0.f;
+        }
+      };
+      load(0);
+      for (int k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+        for (int u = 0; u < LA; ++u) {
+          const int i = threadIdx.x + u * THREADS, r = i / BK;
+          As[i - r * BK][r] = ra[u];
+        }
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          const int i = threadIdx.x + u * THREADS, r = i / BN;
+          Bs[r][i - r * BN] = rb[u];
         }
         __syncthreads();
+        if (k0 + BK < K) load(k0 + BK);
 #pragma unroll
         for (int kk = 0; kk < BK; ++kk) {
           float a4[4], b4[4];
