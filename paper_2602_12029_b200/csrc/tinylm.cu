@@ -6,9 +6,11 @@
 // residual -> LayerNorm -> GELU-tanh MLP (biases) -> residual], final
 // LayerNorm -> head. fp32 like the reference (tfjs is fp32).
 //
-// B200 form: one CTA per sequence runs every layer of the forward
-// (a 64-256 wide model is launch- and latency-bound: one launch per
-// forward, activations in L1/L2-resident scratch). The prompt cache is
+// B200 form: one launch per forward; a sequence is one 8-CTA thread-block
+// cluster that runs every layer, each phase (embeddings, LayerNorm rows,
+// GEMM output tiles, attention (head, token-phase) units) split over the
+// cluster's CTAs with a cluster barrier between phases (a 64-256 wide
+// model is latency-bound; activations stay in L2-resident scratch). The prompt cache is
 // paged instead of model.ts's concatenated [B, H, S, hd] tensors: 16-token
 // pages [page][layer][K|V][head][16][hd], a block table per sequence, so a
 // decode module's forward reads the frozen base's pages of the shared
@@ -24,6 +26,14 @@ constexpr int PT = 16;
 constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
 constexpr int NPTR = 12;  // per-layer parameter pointers (psk.h)
+constexpr int CL = 8;     // CTAs per sequence (one thread-block cluster)
+
+// Phase boundary of a sequence's forward: every CTA of the cluster has
+// finished the phase and its global writes are visible (release / acquire
+// at cluster scope).
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 struct Args {
   psk_tiny_model m;
@@ -37,9 +47,9 @@ struct Args {
 };
 
 // LayerNorm of T rows of width d, eps 1e-5, biased variance (model.ts:120-123): warp per row.
-__device__ void layer_norm(const float* in, float* out, const float* g, const float* b, int T, int d) {
+__device__ void layer_norm(const float* in, float* out, const float* g, const float* b, int T, int d, int rank) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int t = warp; t < T; t += WARPS) {
+  for (int t = rank * WARPS + warp; t < T; t += CL * WARPS) {
     const float* x = in + (int64_t)t * d;
     float s = 0.f;
     for (int c = lane; c < d; c += 32) s += x[c];
@@ -71,12 +81,15 @@ struct Tiles {
   float A[BK][BM + 4], B[BK][BN];
 };
 template <class Out>
-__device__ void matmul(Tiles& tl, const float* X, int T, int K, const float* W, int N, const float* bias, Out out) {
+__device__ void matmul(Tiles& tl, int rank, const float* X, int T, int K, const float* W, int N, const float* bias,
+                       Out out) {
   auto& As = tl.A;
   auto& Bs = tl.B;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  for (int m0 = 0; m0 < T; m0 += BM)
-    for (int n0 = 0; n0 < N; n0 += BN) {
+  const int tn = (N + BN - 1) / BN, tiles = ((T + BM - 1) / BM) * tn;
+  for (int ti = rank; ti < tiles; ti += CL) {  // output tiles split over the cluster
+    const int m0 = (ti / tn) * BM, n0 = (ti % tn) * BN;
+    {
       float acc[4][4] = {};
       // the next k slab is loaded into registers while this one computes
       constexpr int LA = BM * BK / THREADS, LB = BK * BN / THREADS;
@@ -130,13 +143,14 @@ __device__ void matmul(Tiles& tl, const float* X, int T, int K, const float* W, 
           if (t < T && n < N) out(t, n, acc[i][j] + (bias ? bias[n] : 0.f));
         }
     }
+  }
 }
 
 __global__ void __launch_bounds__(THREADS, 1) tiny_forward_kernel(const Args a) {
   extern __shared__ float s_p[];  // one head's K / V rows, then per warp: probabilities + q
   __shared__ Tiles tiles;
   const psk_tiny_model& m = a.m;
-  const int b = blockIdx.x, T = a.T, S0 = a.S0, d = m.width, H = m.heads, hd = d / H;
+  const int b = blockIdx.x / CL, rank = blockIdx.x % CL, T = a.T, S0 = a.S0, d = m.width, H = m.heads, hd = d / H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t page_f = (int64_t)m.layers * 2 * PT * d;  // floats per page
   float* x = a.scratch + (int64_t)b * 8 * T * d;
@@ -148,27 +162,27 @@ __global__ void __launch_bounds__(THREADS, 1) tiny_forward_kernel(const Args a) 
   const int32_t* tab = a.table + (int64_t)b * a.max_pages;
   // embeddings (model.ts:262-276): previous token of position 0 = the last
   // token the cache covers (-1: none -> no prev-token term)
-  for (int i = threadIdx.x; i < T * d; i += THREADS) {
+  for (int i = rank * THREADS + threadIdx.x; i < T * d; i += CL * THREADS) {
     const int t = i / d, c = i - t * d;
     const int prev = t > 0 ? tok[t - 1] : a.prev_first[b];
     float v = m.tok_emb[(int64_t)tok[t] * d + c] + (prev >= 0 ? m.prev_emb[(int64_t)prev * d + c] : 0.f);
     x[i] = v + m.pos_emb[(int64_t)(S0 + t) * d + c];
   }
-  __syncthreads();
+  cluster_sync();
   const float scale = 1.f / sqrtf((float)hd);
   for (int l = 0; l < m.layers; ++l) {
     const float* const* w = m.blocks + (int64_t)l * NPTR;
-    layer_norm(x, xn, w[0], w[1], T, d);
-    __syncthreads();
-    matmul(tiles, xn, T, d, w[2], d, nullptr, [&](int t, int n, float v) { q[(int64_t)t * d + n] = v; });
+    layer_norm(x, xn, w[0], w[1], T, d, rank);
+    cluster_sync();
+    matmul(tiles, rank, xn, T, d, w[2], d, nullptr, [&](int t, int n, float v) { q[(int64_t)t * d + n] = v; });
     // K / V of the new tokens -> their pages (positions S0 .. S0 + T - 1)
     for (int kv = 0; kv < 2; ++kv)
-      matmul(tiles, xn, T, d, w[3 + kv], d, nullptr, [&](int t, int n, float v) {
+      matmul(tiles, rank, xn, T, d, w[3 + kv], d, nullptr, [&](int t, int n, float v) {
         const int pos = S0 + t, hh = n / hd;
         float* pg = a.kv + (int64_t)tab[pos / PT] * page_f;
         pg[(((int64_t)(l * 2 + kv) * H + hh) * PT + pos % PT) * hd + (n - hh * hd)] = v;
       });
-    __syncthreads();
+    cluster_sync();
     // attention, head by head: the head's K / V rows for keys 0 .. S0+T-1
     // staged in shared memory ([key][hd + 1]: conflict-free for a lane per
     // key and for a lane per dim), then a warp per new token t over keys
@@ -179,7 +193,11 @@ __global__ void __launch_bounds__(THREADS, 1) tiny_forward_kernel(const Args a) 
     float* Vs = Ks + (int64_t)S_all * hs;
     float* pr = Vs + (int64_t)S_all * hs + (int64_t)warp * (m.context + hd);
     float* qs = pr + m.context;
-    for (int hh = 0; hh < H; ++hh) {
+    // units (head, token phase) over the cluster: a head's tokens are split
+    // ts::hsplit among hsplit CTAs when the cluster has more CTAs than heads
+    const int hsplit = CL % H == 0 ? CL / H : 1;
+    for (int u = rank; u < H * hsplit; u += CL) {
+      const int hh = u / hsplit, ts = u % hsplit;
       for (int i = threadIdx.x; i < S_all * hd; i += THREADS) {
         const int j = i / hd, e = i - j * hd;
         const float* pg = a.kv + (int64_t)tab[j / PT] * page_f + (((int64_t)(l * 2) * H + hh) * PT + j % PT) * hd + e;
@@ -187,7 +205,7 @@ __global__ void __launch_bounds__(THREADS, 1) tiny_forward_kernel(const Args a) 
         Vs[j * hs + e] = pg[(int64_t)H * PT * hd];  // V sits H tiles after K
       }
       __syncthreads();
-      for (int t = warp; t < T; t += WARPS) {
+      for (int t = ts + warp * hsplit; t < T; t += WARPS * hsplit) {
         const int S = S0 + t + 1;
         for (int e = lane; e < hd; e += 32) qs[e] = q[(int64_t)t * d + hh * hd + e];
         __syncwarp();
@@ -221,19 +239,20 @@ __global__ void __launch_bounds__(THREADS, 1) tiny_forward_kernel(const Args a) 
       }
       __syncthreads();
     }
-    matmul(tiles, ctx, T, d, w[5], d, nullptr, [&](int t, int n, float v) { x[(int64_t)t * d + n] += v; });
-    __syncthreads();
-    layer_norm(x, xn, w[6], w[7], T, d);
-    __syncthreads();
-    matmul(tiles, xn, T, d, w[8], 4 * d, w[9], [&](int t, int n, float v) { hid[(int64_t)t * 4 * d + n] = gelu_tanh(v); });
-    __syncthreads();
-    matmul(tiles, hid, T, 4 * d, w[10], d, w[11], [&](int t, int n, float v) { x[(int64_t)t * d + n] += v; });
-    __syncthreads();
+    cluster_sync();
+    matmul(tiles, rank, ctx, T, d, w[5], d, nullptr, [&](int t, int n, float v) { x[(int64_t)t * d + n] += v; });
+    cluster_sync();
+    layer_norm(x, xn, w[6], w[7], T, d, rank);
+    cluster_sync();
+    matmul(tiles, rank, xn, T, d, w[8], 4 * d, w[9], [&](int t, int n, float v) { hid[(int64_t)t * 4 * d + n] = gelu_tanh(v); });
+    cluster_sync();
+    matmul(tiles, rank, hid, T, 4 * d, w[10], d, w[11], [&](int t, int n, float v) { x[(int64_t)t * d + n] += v; });
+    cluster_sync();
   }
-  layer_norm(x, xn, m.lnf_g, m.lnf_b, T, d);
-  __syncthreads();
+  layer_norm(x, xn, m.lnf_g, m.lnf_b, T, d, rank);
+  cluster_sync();
   float* lg = a.logits + (int64_t)b * T * m.vocab;
-  matmul(tiles, xn, T, d, m.head, m.vocab, nullptr, [&](int t, int n, float v) { lg[(int64_t)t * m.vocab + n] = v; });
+  matmul(tiles, rank, xn, T, d, m.head, m.vocab, nullptr, [&](int t, int n, float v) { lg[(int64_t)t * m.vocab + n] = v; });
 }
 
 }  // namespace tiny
@@ -281,8 +300,19 @@ int psk_tiny_forward(const psk_tiny_model* m, int32_t batch, int32_t n_new, int3
   a.kv = kv_pages;
   a.scratch = scratch;
   a.logits = logits;
-  tiny_forward_kernel<<<batch, THREADS, smem, psk::as_stream(stream)>>>(a);
-  PSK_LAUNCH_CHECK();
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)batch * CL);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = psk::as_stream(stream);
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  PSK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tiny_forward_kernel, a));
   return PSK_OK;
 }
 
