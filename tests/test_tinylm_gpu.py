@@ -134,3 +134,42 @@ def test_errors_as_the_reference():
         cache.slice(4)
     with pytest.raises(ValueError):
         G.sharing_predictions(g, g, 0.5, [])
+
+
+def test_base_cache_slice_property():
+    """model.test.ts:125-142 on the GPU: the cache of x equals the cache of
+    x + suffix sliced to len(x)."""
+    g, _ = _pair(SMALL, 6)
+    r = O.Rng(4)
+    x, suf = [r.int(19) for _ in range(20)], [r.int(19) for _ in range(5)]
+    short, long = G.build_base_cache(g, [x]), G.build_base_cache(g, [x + suf]).slice(20)
+    assert long.tokens[0] == x
+    for l in range(SMALL[0]):
+        (ks, vs), (kl, vl) = short.kv(l), long.kv(l)
+        assert (ks - kl).abs().max().item() < 1e-5 and (vs - vl).abs().max().item() < 1e-5
+
+
+def test_incremental_equals_full_and_injected_prefix():
+    """model.test.ts:167-191 and A9 (acceptance.test.ts:75-92, reduced) on the GPU."""
+    g, _ = _pair(SMALL, 8)
+    r = O.Rng(7)
+    for _ in range(6):
+        prompt = [r.int(19) for _ in range(4 + r.int(20))]
+        assert G.generate(g, prompt, 6, incremental=True) == G.generate(g, prompt, 6, incremental=False)
+    prompt = [r.int(19) for _ in range(22)]
+    cache = G.build_base_cache(g, [prompt])
+    assert G.generate(g, prompt, 5, past=cache.slice(6)) == G.generate(g, prompt, 5)
+    assert G.generate(g, prompt, 5, past=cache.slice(17)) == G.generate(g, prompt, 5)
+    assert G.generate(g, [1, 2, 3], 0) == []
+
+
+def test_evaluate_sharing_contract():
+    """evaluate.test.ts:9-47 on the GPU: r = 0 is the decode model alone;
+    r = 1 with dec = base equals the base alone."""
+    pool = G.TinyKVPool(G.TinyConfig(*SMALL), 512)
+    base, dec = _pair(SMALL, 0, pool)[0], _pair(SMALL, 1, pool)[0]
+    r = O.Rng(42)
+    prompts = [[r.int(19) for _ in range(9)] for _ in range(8)]
+    own = [G.generate(dec, p, 1)[0] for p in prompts]
+    assert G.sharing_predictions(dec, base, 0, prompts) == own
+    assert G.sharing_predictions(base, base, 1, prompts) == G.sharing_predictions(base, base, 0, prompts)
