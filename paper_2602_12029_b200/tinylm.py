@@ -214,9 +214,10 @@ class TinyLM:
         tab = np.array([t + [t[0]] * (maxp - len(t)) for t in tables], dtype=np.int32)
         prev = np.array([past.tokens[b][-1] if past is not None and s0 > 0 else -1 for b in range(B)],
                         dtype=np.int32)
-        toks = torch.tensor(np.asarray(tokens, dtype=np.int32), device=self.dev)
-        if int(toks.min()) < 0 or int(toks.max()) >= self.cfg.vocab:
+        host = np.asarray(tokens, dtype=np.int64)
+        if host.min() < 0 or host.max() >= self.cfg.vocab:  # checked on the host: no device sync
             raise ValueError("token id outside the vocabulary")
+        toks = torch.from_numpy(host.astype(np.int32)).to(self.dev)
         d_tab = torch.from_numpy(tab).to(self.dev)
         d_prev = torch.from_numpy(prev).to(self.dev)
         nf = C.c_int64()
