@@ -1223,7 +1223,10 @@ namespace tcv {
 
 constexpr int CPG = 4;                  // pages per chunk
 constexpr int KC = CPG * PT;            // 64 keys
-constexpr int NSTG = 6;
+#ifndef PSK_FANOUT_NSTG
+#define PSK_FANOUT_NSTG 6  // ring stages (32 KiB each)
+#endif
+constexpr int NSTG = PSK_FANOUT_NSTG;
 constexpr int PGB = 2 * TILE;           // 8 KiB per page: [K|V][half][16][64]
 constexpr int STG = CPG * PGB;          // 32 KiB per chunk
 constexpr int OFF_ML = NSTG * STG;
