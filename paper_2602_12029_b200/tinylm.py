@@ -71,7 +71,9 @@ class TinyConfig:
 
 class TinyKVPool:
     """Pages [page][layer][K|V][head][16][hd] fp32 on one GPU, handed out in
-    order; `filled[p]` = tokens written into page p so far (append-only)."""
+    order and never reused (size it for the caches a run builds; models
+    that share one pool read each other's caches in place); `filled[p]` =
+    tokens written into page p so far (append-only)."""
 
     def __init__(self, cfg: TinyConfig, n_pages: int, device: int = 0):
         hd = cfg.width // cfg.heads
@@ -180,6 +182,23 @@ class TinyLM:
         """model.ts:181-198 (parameters from init_params), on the GPU."""
         return TinyLM(cfg, init_params(cfg, seed), **kw)
 
+    def _import(self, past: PromptCache) -> PromptCache:
+        """A cache built by a model with another page pool (model.ts caches
+        are plain tensors any model can consume): its pages copied into this
+        model's pool (same layer / head geometry required)."""
+        if past.pool.data.shape[1:] != self.pool.data.shape[1:]:
+            raise ValueError("cache geometry (layers, heads, head dim) differs from this model's")
+        tables = []
+        for t in past.tables:
+            new = [self.pool.alloc() for _ in t]
+            if new:
+                src = torch.tensor(t, dtype=torch.long, device=past.pool.data.device)
+                dst = torch.tensor(new, dtype=torch.long, device=self.dev)
+                self.pool.data[dst] = past.pool.data[src].to(self.dev)
+                self.pool.filled[new] = past.pool.filled[t]
+            tables.append(new)
+        return PromptCache(self.pool, tables, past.tokens)
+
     def _writable_table(self, table: list[int], s0: int, n_new: int) -> list[int]:
         """Pages for positions s0 .. s0 + n_new - 1 appended to a row's table;
         a partially filled last page that someone else has filled past s0 is
@@ -208,7 +227,7 @@ class TinyLM:
         if s0 + T > self.cfg.context:
             raise ValueError(f"sequence length {s0 + T} exceeds context {self.cfg.context}")
         if past is not None and past.pool is not self.pool:
-            raise ValueError("cache lives in another model's page pool")
+            past = self._import(past)
         tables = [self._writable_table(past.tables[b] if past is not None else [], s0, T) for b in range(B)]
         maxp = max(len(t) for t in tables)
         tab = np.array([t + [t[0]] * (maxp - len(t)) for t in tables], dtype=np.int32)

@@ -173,3 +173,14 @@ def test_evaluate_sharing_contract():
     own = [G.generate(dec, p, 1)[0] for p in prompts]
     assert G.sharing_predictions(dec, base, 0, prompts) == own
     assert G.sharing_predictions(base, base, 1, prompts) == G.sharing_predictions(base, base, 0, prompts)
+
+
+def test_cache_from_another_pool():
+    """Models built without a shared pool still consume each other's caches
+    (model.ts caches are plain tensors): the pages are imported."""
+    gb, ob = _pair(SMALL, 1)
+    gd, od = _pair(SMALL, 2)
+    assert gb.pool is not gd.pool
+    prompts = _prompts(5, 4, 27, 19)
+    for ratio in (0.3, 0.77):
+        assert G.sharing_predictions(gd, gb, ratio, prompts) == O.evaluate_sharing_predictions(od, ob, ratio, prompts)
