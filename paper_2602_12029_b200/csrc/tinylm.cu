@@ -38,6 +38,7 @@ __device__ __forceinline__ void cluster_sync() {
 struct Args {
   psk_tiny_model m;
   int T, S0, max_pages;
+  int staged;  // attention K / V rows staged in shared memory (else read from the pages)
   const int32_t* tokens;
   const int32_t* prev_first;
   const int32_t* table;
@@ -188,17 +189,21 @@ __global__ void __launch_bounds__(THREADS, 1) tiny_forward_kernel(const Args a) 
     // key and for a lane per dim), then a warp per new token t over keys
     // 0 .. S0 + t (the reference's -1e9 mask on later keys is an exact zero
     // after exp)
+    // (a head too large for shared memory is read from its pages instead)
     const int S_all = S0 + T, hs = hd + 1;
     float* Ks = s_p;
-    float* Vs = Ks + (int64_t)S_all * hs;
-    float* pr = Vs + (int64_t)S_all * hs + (int64_t)warp * (m.context + hd);
+    float* Vs = Ks + (a.staged ? (int64_t)S_all * hs : 0);
+    float* pr = Vs + (a.staged ? (int64_t)S_all * hs : 0) + (int64_t)warp * (m.context + hd);
     float* qs = pr + m.context;
     // units (head, token phase) over the cluster: a head's tokens are split
     // ts::hsplit among hsplit CTAs when the cluster has more CTAs than heads
     const int hsplit = CL % H == 0 ? CL / H : 1;
     for (int u = rank; u < H * hsplit; u += CL) {
       const int hh = u / hsplit, ts = u % hsplit;
-      for (int i = threadIdx.x; i < S_all * hd; i += THREADS) {
+      auto kv_row = [&](int j, int kv) -> const float* {
+        return a.kv + (int64_t)tab[j / PT] * page_f + (((int64_t)(l * 2 + kv) * H + hh) * PT + j % PT) * hd;
+      };
+      for (int i = threadIdx.x; a.staged && i < S_all * hd; i += THREADS) {
         const int j = i / hd, e = i - j * hd;
         const float* pg = a.kv + (int64_t)tab[j / PT] * page_f + (((int64_t)(l * 2) * H + hh) * PT + j % PT) * hd + e;
         Ks[j * hs + e] = pg[0];
@@ -211,7 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1) tiny_forward_kernel(const Args a) 
         __syncwarp();
         float mx = -INFINITY;
         for (int j = lane; j < S; j += 32) {
-          const float* kr = Ks + j * hs;
+          const float* kr = a.staged ? Ks + j * hs : kv_row(j, 0);
           float sc = 0.f;
           for (int e = 0; e < hd; ++e) sc = fmaf(qs[e], kr[e], sc);
           sc *= scale;
@@ -232,7 +237,10 @@ __global__ void __launch_bounds__(THREADS, 1) tiny_forward_kernel(const Args a) 
         const float inv = 1.f / sum;
         for (int e = lane; e < hd; e += 32) {
           float acc = 0.f;
-          for (int j = 0; j < S; ++j) acc = fmaf(pr[j], Vs[j * hs + e], acc);
+          if (a.staged)
+            for (int j = 0; j < S; ++j) acc = fmaf(pr[j], Vs[j * hs + e], acc);
+          else
+            for (int j = 0; j < S; ++j) acc = fmaf(pr[j], kv_row(j, 1)[e], acc);
           ctx[(int64_t)t * d + hh * hd + e] = acc * inv;
         }
         __syncwarp();
@@ -281,8 +289,12 @@ int psk_tiny_forward(const psk_tiny_model* m, int32_t batch, int32_t n_new, int3
   PSK_CHECK_ARG((int64_t)max_pages * PT >= past_len + n_new && n_pages > 0,
                 "block table of %d pages cannot hold %d tokens", max_pages, past_len + n_new);
   const int hd = m->width / m->heads;
-  const size_t smem = sizeof(float) * (2 * (size_t)(past_len + n_new) * (hd + 1) + WARPS * (size_t)(m->context + hd));
-  PSK_CHECK_ARG(smem <= 200 * 1024, "context %d x head dim %d too large for the staged attention", m->context, hd);
+  const size_t rows = sizeof(float) * WARPS * (size_t)(m->context + hd);
+  const size_t kv_stage = sizeof(float) * 2 * (size_t)(past_len + n_new) * (hd + 1);
+  const bool staged = rows + kv_stage <= 200 * 1024;
+  const size_t smem = staged ? rows + kv_stage : rows;
+  PSK_CHECK_ARG(smem <= 200 * 1024, "context %d x head dim %d too large for the attention row buffers", m->context,
+                hd);
   static size_t smem_set = 0;
   if (smem > 48 * 1024 && smem > smem_set) {
     PSK_CUDA_TRY(cudaFuncSetAttribute(tiny_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -292,6 +304,7 @@ int psk_tiny_forward(const psk_tiny_model* m, int32_t batch, int32_t n_new, int3
   Args a;
   a.m = *m;
   a.T = n_new;
+  a.staged = staged;
   a.S0 = past_len;
   a.max_pages = max_pages;
   a.tokens = tokens;

@@ -184,3 +184,17 @@ def test_cache_from_another_pool():
     prompts = _prompts(5, 4, 27, 19)
     for ratio in (0.3, 0.77):
         assert G.sharing_predictions(gd, gb, ratio, prompts) == O.evaluate_sharing_predictions(od, ob, ratio, prompts)
+
+
+@pytest.mark.parametrize("shape,n", [((2, 128, 1, 256, 30), 256), ((1, 64, 2, 40, 11), 40)])
+def test_wide_heads_and_full_context(shape, n):
+    """One 128-dim head at a 256-token context (K / V read from the pages:
+    too large to stage in shared memory) and a forward filling the context
+    exactly, then one more token over the cache at the limit - 1."""
+    g, o = _pair(shape, 9)
+    toks = _prompts(2, 2, n, shape[4])
+    gl, gc = g.forward(toks)
+    ol, oc = o.forward(toks)
+    _close(gl, ol)
+    gl2, _ = g.forward([[1], [2]], gc.slice(n - 1))
+    _close(gl2, o.forward([[1], [2]], oc.slice(n - 1))[0])
